@@ -1,0 +1,375 @@
+"""Benchmark: GaBP edge-message updates/s on BASELINE config 1.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1] [--schedule broadcast|parallel]
+
+One step = one full synchronous GaBP solve of the workload to ||Ax-b||/||b|| < 1e-8
+(messages reset to zero every step), i.e. every sweep plus the device-side convergence
+test and per-sweep residual/max-change histories.
+
+  value   useful edge-message updates per second (reference-counted sweeps x directed
+          edges / device time), graph resident in HBM, CUDA events on the library stream
+  e2e     the same metric through the drop-in C-ABI call gabp_solve_system with pinned
+          HOST buffers: H2D of the system, device graph build, the solve, D2H of the
+          means + histories, all inside the timed region (host wall clock, synchronous
+          call)
+  roofline  the fused sweep kernel: algorithmic bytes per launch / average launch time
+
+--impl reference times the reference algorithm's CPU implementation -- the bitwise-
+pinned C restatement in oracle/ (the reference is Python/numpy and does not travel to
+the GPU box) -- with all host threads, on the same config and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "GaBP edge-message updates/s, % of HBM roofline; time to 1e-8 residual"
+UNIT = "edge-updates/s"
+REL_TOL = 1e-8
+
+# algorithmic bytes of one fused broadcast sweep:
+#   per directed edge: rc{rev,col} 8 + coeff 8 + gathered in-message 16 + own old
+#   message 16 + new message 16 + x^{(s-2)}[col] 8                      = 72 B
+#   per node: row_ptr 4 + diag 8 + prior_num 8 + rhs 8 + x own 8 + x write 8 + P write 8
+#                                                                        = 52 B
+BYTES_PER_EDGE = 72
+BYTES_PER_NODE = 52
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--schedule", default="broadcast", choices=["broadcast", "parallel"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--cpu-sample-sweeps", type=int, default=0,
+                    help="0 = one full solve as the CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(config: int):
+    from paper_0810_1119_b200 import problems as P
+    name, fn = P.CONFIGS[config]
+    t0 = time.perf_counter()
+    inst = fn(0)
+    return name, inst.system, time.perf_counter() - t0
+
+
+# ---------------------------------------------------------------------------------------
+# clocks during the timed region (pynvml, 10 ms)
+# ---------------------------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception as exc:  # noqa: BLE001
+            self.error = str(exc)
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self._ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self._ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port
+# ---------------------------------------------------------------------------------------
+
+def cpu_run(system, steps, warmup, sample_sweeps, schedule):
+    from oracle import oracle
+    oracle.build()
+    threads = os.cpu_count() or 1
+    oracle.set_threads(threads)
+    g = oracle.build_graph(system.diag, system.rhs, system.pair_i, system.pair_j,
+                           system.pair_v)
+    E = g.num_edges
+    times, updates, iters = [], [], []
+    for k in range(warmup + steps):
+        t0 = time.perf_counter()
+        if sample_sweeps > 0:
+            r = oracle.solve(g, epsilon=1e-300, max_iter=sample_sweeps, schedule=schedule)
+        else:
+            r = oracle.solve(g, epsilon=1e-300, schedule=schedule, rel_residual_tol=REL_TOL)
+        dt = time.perf_counter() - t0
+        if k >= warmup:
+            times.append(dt)
+            updates.append(r.iterations * E)
+            iters.append(r.iterations)
+    value = sum(updates) / sum(times)
+    sample = (f"{'full solve to 1e-8' if sample_sweeps == 0 else f'{sample_sweeps} sweeps'} "
+              f"of config workload ({system.n} nodes, {E} directed edges), {schedule} "
+              f"schedule, C oracle (oracle/gabp_oracle.c, OpenMP), {len(times)} timed runs, "
+              f"{iters[-1]} sweeps each")
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+            "seconds_per_run": sum(times) / len(times)}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    name, system, _ = workload(args.config)
+    steps = max(1, args.steps)
+    warmup = max(0, args.warmup)
+    # bounded: cap the CPU arm at ~2 minutes of timed work
+    probe = cpu_run(system, 1, 0, args.cpu_sample_sweeps, args.schedule)
+    per = probe["seconds_per_run"]
+    steps = max(1, min(steps, int(120.0 / max(per, 1e-3))))
+    warmup = min(warmup, 2)
+    res = cpu_run(system, steps, warmup, args.cpu_sample_sweeps, args.schedule)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
+        "ms_per_step": res["seconds_per_run"] * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": name, "schedule": args.schedule, "n": system.n,
+                   "offdiag_pairs": int(system.pair_v.size), "stop": "||Ax-b||/||b|| < 1e-8"},
+        "cpu_baseline": res,
+        "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+
+def pinned_copy(a: np.ndarray):
+    import torch
+    t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+    t.numpy()[...] = a
+    return t, t.numpy()
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_0810_1119_b200 as G
+    from paper_0810_1119_b200 import _lib
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    name, system, gen_s = workload(args.config)
+    lib = _lib.load()
+    g = G.build_graph(system, dev)
+    E, n = g.num_edges, g.n
+    sched = args.schedule
+    opts = G.SolveOptions(schedule=sched, epsilon=1e-300, rel_residual_tol=REL_TOL,
+                          device=dev, record_means_history=False)
+    o = G.solver._options_struct(opts, n, None)
+    rep = _lib.Report()
+
+    def device_solve():
+        _lib.check(lib.gabp_solve_device(g.handle, ctypes.byref(o), None, None,
+                                         ctypes.byref(rep)))
+        return rep.device_ms, rep.iterations, rep.sweeps_launched, rep.final_rel_residual
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(3, args.warmup)):
+        device_solve()
+    barrier()
+    ms_list, its, launched = [], [], 0
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            ms, it, sl, rel = device_solve()
+            ms_list.append(ms)
+            its.append(it)
+            launched += sl
+    barrier()
+    total_ms = float(sum(ms_list))
+    useful = float(sum(its)) * E
+    if world > 1:
+        t = torch.tensor([total_ms, useful], dtype=torch.float64, device=f"cuda:{dev}")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        total_ms_max = float(mx[0])
+        useful_all = float(t[1])
+    else:
+        total_ms_max, useful_all = total_ms, useful
+    value = useful_all / (total_ms_max / 1e3)
+
+    # roofline of the fused sweep kernel (average launch over back-to-back sweeps)
+    sweeps = 50
+    ms_sweep = ctypes.c_double()
+    _lib.check(lib.gabp_bench_sweeps(g.handle, _lib.SCHED_IDS[sched], 5, ctypes.byref(ms_sweep)))
+    _lib.check(lib.gabp_bench_sweeps(g.handle, _lib.SCHED_IDS[sched], sweeps,
+                                     ctypes.byref(ms_sweep)))
+    algo_bytes = BYTES_PER_EDGE * E + BYTES_PER_NODE * n
+    achieved = algo_bytes / (ms_sweep.value / 1e3) / 1e9
+    peaks = {}
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    traffic = None
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh)
+        key = f"config{args.config}_{sched}"
+        if key in tr:
+            traffic = tr[key]["dram_bytes_per_launch"]
+    except OSError:
+        pass
+    g_close = g.close
+
+    # e2e: the drop-in call with pinned host buffers, H2D + build + solve + D2H timed
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, min(args.steps, 20))
+    keep = [pinned_copy(a) for a in (system.diag, system.rhs, system.pair_i, system.pair_j,
+                                     system.pair_v)]
+    hd, hr, hi, hj, hv = (k[1] for k in keep)
+    means_t, means_h = pinned_copy(np.empty(n))
+    ch_t, ch_h = pinned_copy(np.empty(opts.max_iter))
+    rh_t, rh_h = pinned_copy(np.empty(opts.max_iter))
+    rep2 = _lib.Report()
+
+    def e2e_call():
+        _lib.check(lib.gabp_solve_system(n, system.pair_v.size, _lib.ptr(hd), _lib.ptr(hr),
+                                         _lib.ptr(hi), _lib.ptr(hj), _lib.ptr(hv), dev,
+                                         ctypes.byref(o), _lib.ptr(means_h), None,
+                                         _lib.ptr(ch_h), _lib.ptr(rh_h), ctypes.byref(rep2)))
+        return rep2.iterations
+
+    g_close()  # free the resident graph before the e2e builds
+    e2e_call()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_updates = 0
+    for _ in range(e2e_steps):
+        e2e_updates += e2e_call() * E
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s, float(e2e_updates)], dtype=torch.float64, device=f"cuda:{dev}")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        e2e_s, e2e_updates = float(mx[0]), float(t[1])
+    e2e_value = e2e_updates / e2e_s
+    h2d = 8 * 2 * n + 24 * int(system.pair_v.size)
+    d2h = 8 * n + 2 * 8 * int(np.mean(its))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_run(system, 1, 1, args.cpu_sample_sweeps, sched)
+        cpu.pop("seconds_per_run", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, BASELINE config %d)" % args.config,
+            "config": {"workload": name, "schedule": sched, "n": n, "directed_edges": E,
+                       "stop": "||Ax-b||/||b|| < 1e-8 (epsilon disabled)",
+                       "sweeps_to_1e-8": int(its[-1]),
+                       "time_to_1e-8_ms": total_ms_max / args.steps,
+                       "l2": "inputs > L2: messages 2 x %.2f GB, graph %.2f GB" %
+                             (16 * E / 1e9, 16 * E / 1e9),
+                       "parallelism": "replicas" if world > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "kernel": f"sweep_kernel<{sched}> %.3f ms/launch" % ms_sweep.value,
+                         "algorithmic_bytes_per_launch": algo_bytes},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                    "ms_per_step": e2e_s / e2e_steps * 1e3},
+            "gpu_launches": int(launched),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,372 @@
+// build.cu -- device-side GaussianGraph construction (graph.py:63-120 re-designed).
+//
+// Input: the SymSystem storage (linalg.py:34-62) as upper-triangle pairs
+// (i < j, A_ij != 0) in arbitrary order, already in HBM.  Output (gabp_internal.cuh):
+// CSR grouped by source with neighbours ascending -- exactly the reference's edge-id
+// numbering -- plus the twin index rev[e] (edge j->i of edge i->j), so a sweep gathers
+// the reverse message in O(1) instead of searching.
+//
+//   1. validate + degree histogram            (one pass over the pairs, atomics)
+//   2. row_ptr = exclusive scan(degree)       (CUB DeviceScan)
+//   3. scatter both directions of every pair  (atomic cursor per row)
+//   4. sort every row by column               (CUB DeviceSegmentedSort, payload 2p+dir)
+//   5. pos[payload] = e, rev[e] = pos[payload ^ 1], duplicate check
+//   6. tiles: boundary where the edge bucket changes or every kTileRows rows
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <stdio.h>
+
+#include "gabp_internal.cuh"
+
+namespace gabp {
+namespace {
+
+enum BuildErr : int { kErrNone = 0, kErrPairRange = 1, kErrZeroValue = 2, kErrDup = 3,
+                      kErrZeroDiag = 4 };
+
+__global__ void count_kernel(int64_t n, int64_t np, const int64_t *pi, const int64_t *pj,
+                             const double *pv, uint32_t *deg, int *err,
+                             unsigned long long *err_at) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = pi[p], j = pj[p];
+        if (!(0 <= i && i < j && j < n)) {
+            atomicCAS(err, 0, (int)kErrPairRange);
+            atomicMin(err_at, (unsigned long long)p);
+            continue;
+        }
+        if (pv[p] == 0.0) {
+            atomicCAS(err, 0, (int)kErrZeroValue);
+            atomicMin(err_at, (unsigned long long)p);
+            continue;
+        }
+        atomicAdd(&deg[i], 1u);
+        atomicAdd(&deg[j], 1u);
+    }
+}
+
+__global__ void scatter_kernel(int64_t np, const int64_t *pi, const int64_t *pj,
+                               uint32_t *cursor, uint32_t *tcol, uint32_t *tpl) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = (uint32_t)pi[p], j = (uint32_t)pj[p];
+        const uint32_t a = atomicAdd(&cursor[i], 1u);
+        tcol[a] = j;
+        tpl[a] = (uint32_t)(2 * p);
+        const uint32_t b = atomicAdd(&cursor[j], 1u);
+        tcol[b] = i;
+        tpl[b] = (uint32_t)(2 * p + 1);
+    }
+}
+
+__device__ __forceinline__ uint32_t row_of(uint32_t pl, const int64_t *pi, const int64_t *pj) {
+    const int64_t p = pl >> 1;
+    return (uint32_t)((pl & 1u) ? pj[p] : pi[p]);
+}
+
+__global__ void pos_kernel(int64_t E, const uint32_t *scol, const uint32_t *spl,
+                           const int64_t *pi, const int64_t *pj, uint32_t *pos, int *err,
+                           unsigned long long *err_at) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t pl = spl[e];
+        pos[pl] = (uint32_t)e;
+        if (e > 0 && scol[e] == scol[e - 1] &&
+            row_of(pl, pi, pj) == row_of(spl[e - 1], pi, pj)) {
+            atomicCAS(err, 0, (int)kErrDup);
+            atomicMin(err_at, (unsigned long long)(pl >> 1));
+        }
+    }
+}
+
+__global__ void edge_kernel(int64_t E, const uint32_t *scol, const uint32_t *spl,
+                            const uint32_t *pos, const double *pv, uint2 *rc, double *coeff) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t pl = spl[e];
+        rc[e] = make_uint2(pos[pl ^ 1u], scol[e]);
+        coeff[e] = pv[pl >> 1];
+    }
+}
+
+__global__ void tile_flag_kernel(int64_t n, const uint32_t *row_ptr, uint32_t *flag) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t f = (r % kTileRows) == 0;
+        if (!f) f = (row_ptr[r] / kBucket) != (row_ptr[r - 1] / kBucket);
+        flag[r] = f;
+    }
+}
+
+__global__ void tile_scatter_kernel(int64_t n, const uint32_t *flag, const uint32_t *idx,
+                                    uint32_t *tile_start, int64_t ntiles) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        if (flag[r]) tile_start[idx[r]] = (uint32_t)r;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) tile_start[ntiles] = (uint32_t)n;
+}
+
+__global__ void prior_kernel(int64_t n, const double *diag, const double *rhs,
+                             double *prior_num, int *err, unsigned long long *err_at) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = diag[i];
+        if (d == 0.0) {
+            atomicCAS(err, 0, (int)kErrZeroDiag);
+            atomicMin(err_at, (unsigned long long)i);
+        }
+        const double pm = rhs[i] / d;  // prior mean (graph.py:74)
+        prior_num[i] = d * pm;         // prior_prec * prior_mean (solver.py:147)
+    }
+}
+
+__global__ void sumsq_kernel(int64_t n, const double *v, double *part) {
+    // fixed-order partials: block b sums [b*4096, (b+1)*4096) sequentially per thread slice
+    __shared__ double red[256];
+    const int64_t lo = (int64_t)blockIdx.x * 4096;
+    double acc = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < lo + 4096 && i < n; i += 256) acc += v[i] * v[i];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+inline unsigned grid_for(int64_t work, int threads = 256) {
+    int64_t b = (work + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 148 * 32) b = 148 * 32;
+    return (unsigned)b;
+}
+
+struct Scratch {
+    void *p = nullptr;
+    ~Scratch() { if (p) cudaFree(p); }
+};
+
+#define BCHECK(call)                                                                   \
+    do {                                                                               \
+        cudaError_t _e = (call);                                                       \
+        if (_e != cudaSuccess) {                                                       \
+            snprintf(err, errlen, "%s: %s", #call, cudaGetErrorString(_e));            \
+            return _e == cudaErrorMemoryAllocation ? GABP_ENOMEM : GABP_ECUDA;         \
+        }                                                                              \
+    } while (0)
+
+}  // namespace
+
+void free_graph(DeviceGraph &g) {
+    cudaFree(g.row_ptr);
+    cudaFree(g.tile_start);
+    cudaFree(g.rc);
+    cudaFree(g.coeff);
+    cudaFree(g.diag);
+    cudaFree(g.prior_num);
+    cudaFree(g.rhs);
+    g = DeviceGraph{};
+}
+
+int compute_priors(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
+    int *d_err = nullptr;
+    unsigned long long *d_at = nullptr;
+    BCHECK(cudaMallocAsync(&d_err, sizeof(int) + sizeof(unsigned long long) * 2, st));
+    d_at = reinterpret_cast<unsigned long long *>(d_err + 2);
+    BCHECK(cudaMemsetAsync(d_err, 0, sizeof(int) * 2, st));
+    BCHECK(cudaMemsetAsync(d_at, 0xff, sizeof(unsigned long long), st));
+    prior_kernel<<<grid_for(g.n), 256, 0, st>>>(g.n, g.diag, g.rhs, g.prior_num, d_err, d_at);
+    BCHECK(cudaGetLastError());
+    const int64_t nparts = (g.n + 4095) / 4096;
+    double *part = nullptr;
+    BCHECK(cudaMallocAsync(&part, sizeof(double) * nparts, st));
+    sumsq_kernel<<<(unsigned)nparts, 256, 0, st>>>(g.n, g.rhs, part);
+    BCHECK(cudaGetLastError());
+    int h_err = 0;
+    unsigned long long h_at = 0;
+    double *h_part = (double *)malloc(sizeof(double) * nparts);
+    BCHECK(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BCHECK(cudaMemcpyAsync(&h_at, d_at, sizeof(h_at), cudaMemcpyDeviceToHost, st));
+    BCHECK(cudaMemcpyAsync(h_part, part, sizeof(double) * nparts, cudaMemcpyDeviceToHost, st));
+    BCHECK(cudaStreamSynchronize(st));
+    cudaFreeAsync(part, st);
+    cudaFreeAsync(d_err, st);
+    double ss = 0.0;
+    for (int64_t c = 0; c < nparts; ++c) ss += h_part[c];
+    free(h_part);
+    g.rhs_norm = sqrt(ss);
+    if (h_err == kErrZeroDiag) {
+        snprintf(err, errlen, "zero diagonal entry at row %llu: node priors need b_i / A_ii", h_at);
+        return GABP_EZERODIAG;
+    }
+    return GABP_OK;
+}
+
+int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *d_diag,
+                       const double *d_rhs, const int64_t *d_pi, const int64_t *d_pj,
+                       const double *d_pv, cudaStream_t st, char *err, size_t errlen) {
+    if (n < 1) {
+        snprintf(err, errlen, "diag must be a non-empty vector");
+        return GABP_EINVAL;
+    }
+    if (npairs < 0 || 2 * npairs >= (int64_t)0xffffffffll || n >= (int64_t)0xffffffffll) {
+        snprintf(err, errlen, "graph too large for 32-bit edge ids (n=%lld, pairs=%lld)",
+                 (long long)n, (long long)npairs);
+        return GABP_EINVAL;
+    }
+    const int64_t E = 2 * npairs;
+    g.n = n;
+    g.E = E;
+    g.npairs = npairs;
+    cudaEvent_t t0, t1;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, st);
+
+    BCHECK(cudaMallocAsync(&g.diag, sizeof(double) * n, st));
+    BCHECK(cudaMallocAsync(&g.rhs, sizeof(double) * n, st));
+    BCHECK(cudaMallocAsync(&g.prior_num, sizeof(double) * n, st));
+    BCHECK(cudaMemcpyAsync(g.diag, d_diag, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    BCHECK(cudaMemcpyAsync(g.rhs, d_rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    BCHECK(cudaMallocAsync(&g.row_ptr, sizeof(uint32_t) * (n + 1), st));
+    BCHECK(cudaMallocAsync(&g.rc, sizeof(uint2) * (E > 0 ? E : 1), st));
+    BCHECK(cudaMallocAsync(&g.coeff, sizeof(double) * (E > 0 ? E : 1), st));
+
+    int *d_err = nullptr;
+    BCHECK(cudaMallocAsync(&d_err, 16, st));
+    unsigned long long *d_at = reinterpret_cast<unsigned long long *>(d_err + 2);
+    BCHECK(cudaMemsetAsync(d_err, 0, 8, st));
+    BCHECK(cudaMemsetAsync(d_at, 0xff, 8, st));
+
+    // 1. degrees
+    uint32_t *deg = nullptr;
+    BCHECK(cudaMallocAsync(&deg, sizeof(uint32_t) * (n + 1), st));
+    BCHECK(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (n + 1), st));
+    if (npairs > 0) {
+        count_kernel<<<grid_for(npairs), 256, 0, st>>>(n, npairs, d_pi, d_pj, d_pv, deg, d_err,
+                                                       d_at);
+        BCHECK(cudaGetLastError());
+    }
+    // 2. row_ptr
+    size_t tmp_bytes = 0;
+    BCHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, deg, g.row_ptr, n + 1, st));
+    void *tmp = nullptr;
+    size_t tmp_cap = tmp_bytes;
+    BCHECK(cudaMallocAsync(&tmp, tmp_cap, st));
+    BCHECK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, deg, g.row_ptr, n + 1, st));
+    // max degree
+    {
+        uint32_t *d_max = nullptr;
+        BCHECK(cudaMallocAsync(&d_max, sizeof(uint32_t), st));
+        size_t b2 = 0;
+        BCHECK(cub::DeviceReduce::Max(nullptr, b2, deg, d_max, n, st));
+        if (b2 > tmp_cap) {
+            cudaFreeAsync(tmp, st);
+            tmp_cap = b2;
+            BCHECK(cudaMallocAsync(&tmp, tmp_cap, st));
+        }
+        BCHECK(cub::DeviceReduce::Max(tmp, b2, deg, d_max, n, st));
+        uint32_t h_max = 0;
+        BCHECK(cudaMemcpyAsync(&h_max, d_max, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        int h_err0 = 0;
+        BCHECK(cudaMemcpyAsync(&h_err0, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        unsigned long long h_at0 = 0;
+        BCHECK(cudaMemcpyAsync(&h_at0, d_at, 8, cudaMemcpyDeviceToHost, st));
+        BCHECK(cudaStreamSynchronize(st));
+        cudaFreeAsync(d_max, st);
+        g.max_degree = h_max;
+        if (h_err0 != kErrNone) {
+            cudaFreeAsync(tmp, st);
+            cudaFreeAsync(deg, st);
+            cudaFreeAsync(d_err, st);
+            cudaStreamSynchronize(st);
+            if (h_err0 == kErrPairRange)
+                snprintf(err, errlen, "bad off-diagonal key at pair %llu for n=%lld", h_at0,
+                         (long long)n);
+            else
+                snprintf(err, errlen, "explicit zero stored at pair %llu", h_at0);
+            return GABP_EINVAL;
+        }
+    }
+    if (E > 0) {
+        // 3. scatter
+        uint32_t *tcol = nullptr, *tpl = nullptr, *scol = nullptr, *spl = nullptr;
+        BCHECK(cudaMallocAsync(&tcol, sizeof(uint32_t) * E, st));
+        BCHECK(cudaMallocAsync(&tpl, sizeof(uint32_t) * E, st));
+        BCHECK(cudaMemcpyAsync(deg, g.row_ptr, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice,
+                               st));  // deg becomes the cursor
+        scatter_kernel<<<grid_for(npairs), 256, 0, st>>>(npairs, d_pi, d_pj, deg, tcol, tpl);
+        BCHECK(cudaGetLastError());
+        // 4. per-row sort by column
+        BCHECK(cudaMallocAsync(&scol, sizeof(uint32_t) * E, st));
+        BCHECK(cudaMallocAsync(&spl, sizeof(uint32_t) * E, st));
+        size_t sb = 0;
+        BCHECK(cub::DeviceSegmentedSort::SortPairs(nullptr, sb, tcol, scol, tpl, spl, (int64_t)E,
+                                                   (int64_t)n, g.row_ptr, g.row_ptr + 1, st));
+        if (sb > tmp_cap) {
+            cudaFreeAsync(tmp, st);
+            tmp_cap = sb;
+            BCHECK(cudaMallocAsync(&tmp, tmp_cap, st));
+        }
+        BCHECK(cub::DeviceSegmentedSort::SortPairs(tmp, sb, tcol, scol, tpl, spl, (int64_t)E,
+                                                   (int64_t)n, g.row_ptr, g.row_ptr + 1, st));
+        cudaFreeAsync(tcol, st);
+        // 5. twin index
+        uint32_t *pos = tpl;  // reuse
+        pos_kernel<<<grid_for(E), 256, 0, st>>>(E, scol, spl, d_pi, d_pj, pos, d_err, d_at);
+        BCHECK(cudaGetLastError());
+        edge_kernel<<<grid_for(E), 256, 0, st>>>(E, scol, spl, pos, d_pv, g.rc, g.coeff);
+        BCHECK(cudaGetLastError());
+        cudaFreeAsync(scol, st);
+        cudaFreeAsync(spl, st);
+        cudaFreeAsync(tpl, st);
+    }
+    // 6. tiles
+    {
+        uint32_t *flag = deg, *idx = nullptr;  // deg no longer needed
+        BCHECK(cudaMallocAsync(&idx, sizeof(uint32_t) * (n + 1), st));
+        tile_flag_kernel<<<grid_for(n), 256, 0, st>>>(n, g.row_ptr, flag);
+        BCHECK(cudaGetLastError());
+        BCHECK(cudaMemsetAsync(flag + n, 0, sizeof(uint32_t), st));
+        size_t b3 = 0;
+        BCHECK(cub::DeviceScan::ExclusiveSum(nullptr, b3, flag, idx, n + 1, st));
+        if (b3 > tmp_cap) {
+            cudaFreeAsync(tmp, st);
+            tmp_cap = b3;
+            BCHECK(cudaMallocAsync(&tmp, tmp_cap, st));
+        }
+        BCHECK(cub::DeviceScan::ExclusiveSum(tmp, b3, flag, idx, n + 1, st));
+        uint32_t h_nt = 0;
+        BCHECK(cudaMemcpyAsync(&h_nt, idx + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        BCHECK(cudaStreamSynchronize(st));
+        g.ntiles = h_nt;
+        BCHECK(cudaMallocAsync(&g.tile_start, sizeof(uint32_t) * (h_nt + 1), st));
+        tile_scatter_kernel<<<grid_for(n), 256, 0, st>>>(n, flag, idx, g.tile_start, g.ntiles);
+        BCHECK(cudaGetLastError());
+        cudaFreeAsync(idx, st);
+    }
+    cudaFreeAsync(tmp, st);
+    cudaFreeAsync(deg, st);
+    int h_err = 0;
+    unsigned long long h_at = 0;
+    BCHECK(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BCHECK(cudaMemcpyAsync(&h_at, d_at, 8, cudaMemcpyDeviceToHost, st));
+    cudaEventRecord(t1, st);
+    BCHECK(cudaStreamSynchronize(st));
+    cudaFreeAsync(d_err, st);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    g.build_ms = ms;
+    if (h_err == kErrDup) {
+        snprintf(err, errlen, "duplicate off-diagonal pair (pair index %llu)", h_at);
+        return GABP_EDUP;
+    }
+    return compute_priors(g, st, err, errlen);
+}
+
+}  // namespace gabp

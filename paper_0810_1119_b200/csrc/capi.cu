@@ -1,0 +1,760 @@
+// capi.cu -- the extern "C" boundary (include/gabp_b200.h) and the host side of the
+// solve loop.  The loop itself is device-driven: every sweep launch evaluates the
+// convergence test of the sweep two launches back (gabp_internal.cuh, Ctrl), so the
+// host only enqueues CUDA-graph chunks of sweeps and polls one flag per chunk, one
+// chunk ahead -- no per-sweep host synchronisation.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "gabp_internal.cuh"
+
+using gabp::Ctrl;
+using gabp::DeviceGraph;
+using gabp::SweepArgs;
+
+namespace {
+thread_local char g_err[1024] = "";
+
+int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define CK(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t _e = (call);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            return fail(_e == cudaErrorMemoryAllocation ? GABP_ENOMEM : GABP_ECUDA,          \
+                        "%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__,    \
+                        __LINE__);                                                           \
+    } while (0)
+
+}  // namespace
+
+struct gabp_graph {
+    DeviceGraph g;
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    int is_dense = 0;
+    // solve workspace
+    double2 *msg[2] = {nullptr, nullptr};
+    double *x[3] = {nullptr, nullptr, nullptr};
+    double *p[3] = {nullptr, nullptr, nullptr};
+    double *rsq_part = nullptr;
+    Ctrl *ctrl = nullptr;
+    Ctrl *h_ctrl = nullptr;          // pinned mirror
+    int32_t *h_done = nullptr;       // pinned, 2 poll slots
+    double *change_hist = nullptr, *res_hist = nullptr, *rsq_hist = nullptr;
+    int64_t hist_cap = 0;
+    uint64_t ws_gen = 0;
+    // cached CUDA graph of a chunk of sweep launches
+    cudaGraphExec_t chunk_exec = nullptr;
+    int chunk_len = 0, chunk_sched = -1;
+    uint64_t chunk_gen = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    double *xhist = nullptr;  // device means history (only while a solve asks for it)
+    int64_t xhist_rows = 0;
+};
+
+struct gabp_state {
+    const gabp_graph *g = nullptr;
+    double2 *buf[2] = {nullptr, nullptr};
+    int cur = 0;
+    int64_t iteration = 0;
+    int64_t messages_sent = 0;
+};
+
+namespace {
+
+int ensure_workspace(gabp_graph *G, int64_t max_iter) {
+    const DeviceGraph &g = G->g;
+    const int64_t E = g.E > 0 ? g.E : 1;
+    if (!G->msg[0]) {
+        for (int b = 0; b < 2; ++b) CK(cudaMalloc(&G->msg[b], sizeof(double2) * E));
+        for (int b = 0; b < 3; ++b) {
+            CK(cudaMalloc(&G->x[b], sizeof(double) * g.n));
+            CK(cudaMalloc(&G->p[b], sizeof(double) * g.n));
+        }
+        CK(cudaMalloc(&G->rsq_part, sizeof(double) * (g.ntiles > 0 ? g.ntiles : 1)));
+        CK(cudaMalloc(&G->ctrl, sizeof(Ctrl)));
+        CK(cudaMallocHost(&G->h_ctrl, sizeof(Ctrl)));
+        CK(cudaMallocHost(&G->h_done, sizeof(int32_t) * 4));
+        for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&G->ev[k]));
+        G->ws_gen++;
+    }
+    if (max_iter > G->hist_cap) {
+        cudaFree(G->change_hist);
+        cudaFree(G->res_hist);
+        cudaFree(G->rsq_hist);
+        CK(cudaMalloc(&G->change_hist, sizeof(double) * max_iter));
+        CK(cudaMalloc(&G->res_hist, sizeof(double) * max_iter));
+        CK(cudaMalloc(&G->rsq_hist, sizeof(double) * max_iter));
+        G->hist_cap = max_iter;
+        G->ws_gen++;
+    }
+    return GABP_OK;
+}
+
+SweepArgs make_args(gabp_graph *G) {
+    SweepArgs a{};
+    const DeviceGraph &g = G->g;
+    a.n = g.n;
+    a.ntiles = g.ntiles;
+    a.row_ptr = g.row_ptr;
+    a.tile_start = g.tile_start;
+    a.rc = g.rc;
+    a.coeff = g.coeff;
+    a.diag = g.diag;
+    a.prior_num = g.prior_num;
+    a.rhs = g.rhs;
+    a.msg[0] = G->msg[0];
+    a.msg[1] = G->msg[1];
+    for (int b = 0; b < 3; ++b) {
+        a.x[b] = G->x[b];
+        a.p[b] = G->p[b];
+    }
+    a.rsq_part = G->rsq_part;
+    a.ctrl = G->ctrl;
+    a.change_hist = G->change_hist;
+    a.res_hist = G->res_hist;
+    a.rsq_hist = G->rsq_hist;
+    a.xhist = G->xhist;
+    a.xhist_rows = G->xhist_rows;
+    return a;
+}
+
+void release_workspace(gabp_graph *G) {
+    for (int b = 0; b < 2; ++b) cudaFree(G->msg[b]);
+    for (int b = 0; b < 3; ++b) {
+        cudaFree(G->x[b]);
+        cudaFree(G->p[b]);
+    }
+    cudaFree(G->rsq_part);
+    cudaFree(G->ctrl);
+    cudaFreeHost(G->h_ctrl);
+    cudaFreeHost(G->h_done);
+    cudaFree(G->change_hist);
+    cudaFree(G->res_hist);
+    cudaFree(G->rsq_hist);
+    cudaFree(G->xhist);
+    if (G->chunk_exec) cudaGraphExecDestroy(G->chunk_exec);
+    for (int k = 0; k < 4; ++k)
+        if (G->ev[k]) cudaEventDestroy(G->ev[k]);
+}
+
+int check_options(const gabp_options_t *opt) {
+    if (!opt) return fail(GABP_EINVAL, "options must not be NULL");
+    if (!(opt->epsilon > 0.0)) return fail(GABP_EINVAL, "epsilon must be positive");
+    if (opt->max_iter < 1) return fail(GABP_EINVAL, "max_iter must be >= 1");
+    if (!(opt->blowup > 1.0)) return fail(GABP_EINVAL, "blowup must exceed 1");
+    if (opt->schedule != GABP_SCHED_PARALLEL && opt->schedule != GABP_SCHED_BROADCAST)
+        return fail(GABP_EINVAL, "schedule must be parallel (0) or broadcast (2)");
+    return GABP_OK;
+}
+
+int auto_chunk(const gabp_graph *G) {
+    // aim for ~1.5 ms of sweeps between host polls (sweep ~ 72 B/edge + 52 B/node)
+    const double bytes = 72.0 * (double)G->g.E + 52.0 * (double)G->g.n;
+    const double us = fmax(4.0, bytes / 6.5e6);
+    int c = (int)(1500.0 / us);
+    if (c < 2) c = 2;
+    if (c > 64) c = 64;
+    return c;
+}
+
+int get_chunk_exec(gabp_graph *G, int sched, int len) {
+    if (G->chunk_exec && G->chunk_len == len && G->chunk_sched == sched &&
+        G->chunk_gen == G->ws_gen)
+        return GABP_OK;
+    if (G->chunk_exec) {
+        cudaGraphExecDestroy(G->chunk_exec);
+        G->chunk_exec = nullptr;
+    }
+    SweepArgs a = make_args(G);
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(G->stream, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < len; ++k) {
+        cudaError_t e = gabp::launch_sweep(a, sched, gabp::kModeSolve, G->stream);
+        if (e != cudaSuccess) {
+            cudaStreamEndCapture(G->stream, &graph);
+            return fail(GABP_ECUDA, "capture: %s", cudaGetErrorString(e));
+        }
+    }
+    CK(cudaStreamEndCapture(G->stream, &graph));
+    cudaError_t e = cudaGraphInstantiate(&G->chunk_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(e);
+    G->chunk_len = len;
+    G->chunk_sched = sched;
+    G->chunk_gen = G->ws_gen;
+    return GABP_OK;
+}
+
+// Runs the device-driven loop; on return G->h_ctrl holds the final controller.
+int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
+    int rc = check_options(opt);
+    if (rc) return rc;
+    CK(cudaSetDevice(G->device));
+    rc = ensure_workspace(G, opt->max_iter);
+    if (rc) return rc;
+    const DeviceGraph &g = G->g;
+    const int64_t rows = opt->h_means_history ? opt->means_history_rows : 0;
+    if (rows != G->xhist_rows) {
+        cudaFree(G->xhist);
+        G->xhist = nullptr;
+        G->xhist_rows = 0;
+        if (rows > 0) CK(cudaMalloc(&G->xhist, sizeof(double) * rows * g.n));
+        G->xhist_rows = rows;
+        G->ws_gen++;
+    }
+    Ctrl c{};
+    c.next_sweep = 1;
+    c.epsilon = opt->epsilon;
+    c.blowup = opt->blowup;
+    c.rel_tol = opt->rel_residual_tol;
+    c.bnorm = g.rhs_norm;
+    c.max_iter = opt->max_iter;
+    c.n = g.n;
+    *G->h_ctrl = c;
+    cudaStream_t st = G->stream;
+    CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(G->msg[0], 0, sizeof(double2) * (g.E > 0 ? g.E : 1), st));  // S_0 = 0
+    const int sched = opt->schedule;
+    const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
+    rc = get_chunk_exec(G, sched, C);
+    if (rc) return rc;
+    SweepArgs a = make_args(G);
+    const int64_t total = opt->max_iter + 2;
+    int64_t launched = 0;
+    int poll = 0;
+    bool pending = false;
+    CK(cudaEventRecord(G->ev[2], st));
+    while (launched < total) {
+        const int64_t k = total - launched < C ? total - launched : C;
+        if (k == C) {
+            CK(cudaGraphLaunch(G->chunk_exec, st));
+        } else {
+            for (int64_t q = 0; q < k; ++q) CK(gabp::launch_sweep(a, sched, gabp::kModeSolve, st));
+        }
+        launched += k;
+        const int slot = poll & 1;
+        CK(cudaMemcpyAsync(&G->h_done[slot], &G->ctrl->done, sizeof(int32_t),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(G->ev[slot], st));
+        if (pending) {
+            const int prev = slot ^ 1;
+            CK(cudaEventSynchronize(G->ev[prev]));
+            if (G->h_done[prev]) break;
+        }
+        pending = true;
+        poll++;
+    }
+    CK(cudaEventRecord(G->ev[3], st));
+    CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, G->ev[2], G->ev[3]));
+    if (device_ms) *device_ms = ms;
+    if (!G->h_ctrl->done)
+        return fail(GABP_ECUDA, "solve loop ended without a decision (internal error)");
+    return GABP_OK;
+}
+
+void fill_report(gabp_graph *G, const gabp_options_t *opt, double ms, double rsq_last,
+                 gabp_report_t *rep) {
+    if (!rep) return;
+    const Ctrl &c = *G->h_ctrl;
+    rep->converged = c.converged;
+    rep->diverged = c.diverged;
+    rep->iterations = c.iterations;
+    rep->n_hist = c.n_hist;
+    rep->sweeps_launched = c.next_sweep - 1;
+    rep->messages_sent =
+        c.iterations * (opt->schedule == GABP_SCHED_BROADCAST ? G->g.n : G->g.E);
+    rep->device_ms = ms;
+    rep->final_rel_residual =
+        (c.n_hist >= 1 && G->g.rhs_norm > 0.0) ? sqrt(rsq_last) / G->g.rhs_norm : NAN;
+}
+
+gabp_graph *new_graph(int device, int *rc) {
+    gabp_graph *G = new gabp_graph();
+    G->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = gabp::prepare_sweep_kernels();
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        *rc = fail(GABP_ECUDA, "device %d: %s", device, cudaGetErrorString(e));
+        delete G;
+        return nullptr;
+    }
+    *rc = GABP_OK;
+    return G;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *gabp_last_error(void) { return g_err; }
+
+int gabp_version(void) { return 10000; }
+
+int gabp_device_count(int32_t *count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return fail(GABP_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+    }
+    *count = c;
+    return GABP_OK;
+}
+
+int gabp_graph_create_device(int64_t n, int64_t npairs, const double *d_diag,
+                             const double *d_rhs, const int64_t *d_pair_i,
+                             const int64_t *d_pair_j, const double *d_pair_v, int32_t device,
+                             gabp_graph_t **out) {
+    if (!out) return fail(GABP_EINVAL, "out must not be NULL");
+    *out = nullptr;
+    int rc;
+    gabp_graph *G = new_graph(device, &rc);
+    if (!G) return rc;
+    rc = gabp::build_graph_device(G->g, n, npairs, d_diag, d_rhs, d_pair_i, d_pair_j, d_pair_v,
+                                  G->stream, g_err, sizeof(g_err));
+    if (rc != GABP_OK) {
+        cudaStreamSynchronize(G->stream);
+        gabp::free_graph(G->g);
+        cudaStreamDestroy(G->stream);
+        delete G;
+        return rc;
+    }
+    *out = G;
+    return GABP_OK;
+}
+
+int gabp_graph_create(int64_t n, int64_t npairs, const double *h_diag, const double *h_rhs,
+                      const int64_t *h_pair_i, const int64_t *h_pair_j, const double *h_pair_v,
+                      int32_t device, gabp_graph_t **out) {
+    if (!out) return fail(GABP_EINVAL, "out must not be NULL");
+    *out = nullptr;
+    if (n < 1) return fail(GABP_EINVAL, "diag must be a non-empty vector");
+    if (npairs < 0) return fail(GABP_EINVAL, "negative pair count");
+    CK(cudaSetDevice(device));
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const size_t nb = sizeof(double) * n, pb = sizeof(int64_t) * (npairs > 0 ? npairs : 1);
+    char *buf = nullptr;
+    cudaError_t e = cudaMallocAsync(&buf, 2 * nb + 3 * pb, st);
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(st);
+        return fail(GABP_ENOMEM, "staging allocation: %s", cudaGetErrorString(e));
+    }
+    double *d_diag = (double *)buf, *d_rhs = (double *)(buf + nb);
+    int64_t *d_pi = (int64_t *)(buf + 2 * nb), *d_pj = (int64_t *)(buf + 2 * nb + pb);
+    double *d_pv = (double *)(buf + 2 * nb + 2 * pb);
+    cudaMemcpyAsync(d_diag, h_diag, nb, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_rhs, h_rhs, nb, cudaMemcpyHostToDevice, st);
+    if (npairs > 0) {
+        cudaMemcpyAsync(d_pi, h_pair_i, sizeof(int64_t) * npairs, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(d_pj, h_pair_j, sizeof(int64_t) * npairs, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(d_pv, h_pair_v, sizeof(double) * npairs, cudaMemcpyHostToDevice, st);
+    }
+    e = cudaStreamSynchronize(st);
+    int rc = GABP_OK;
+    if (e != cudaSuccess) {
+        rc = fail(GABP_ECUDA, "H2D copy: %s", cudaGetErrorString(e));
+    } else {
+        rc = gabp_graph_create_device(n, npairs, d_diag, d_rhs, d_pi, d_pj, d_pv, device, out);
+    }
+    cudaFreeAsync(buf, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+int gabp_graph_create_dense(int64_t n, const double *h_a, const double *h_rhs, int32_t device,
+                            gabp_graph_t **out) {
+    if (!out || !h_a || !h_rhs) return fail(GABP_EINVAL, "NULL argument");
+    if (n < 1) return fail(GABP_EINVAL, "matrix must be non-empty");
+    std::vector<double> diag(n);
+    std::vector<int64_t> pi, pj;
+    std::vector<double> pv;
+    for (int64_t i = 0; i < n; ++i) {
+        diag[i] = h_a[i * n + i];
+        for (int64_t j = i + 1; j < n; ++j) {
+            const double v = h_a[i * n + j];
+            if (v != h_a[j * n + i])
+                return fail(GABP_EINVAL, "matrix not symmetric at (%lld, %lld)", (long long)i,
+                            (long long)j);
+            if (v != 0.0) {
+                pi.push_back(i);
+                pj.push_back(j);
+                pv.push_back(v);
+            }
+        }
+    }
+    int rc = gabp_graph_create(n, (int64_t)pv.size(), diag.data(), h_rhs, pi.data(), pj.data(),
+                               pv.data(), device, out);
+    if (rc == GABP_OK) (*out)->is_dense = 1;
+    return rc;
+}
+
+void gabp_graph_destroy(gabp_graph_t *G) {
+    if (!G) return;
+    cudaSetDevice(G->device);
+    cudaStreamSynchronize(G->stream);
+    release_workspace(G);
+    gabp::free_graph(G->g);
+    cudaStreamDestroy(G->stream);
+    delete G;
+}
+
+int gabp_graph_info(const gabp_graph_t *G, gabp_graph_info_t *info) {
+    if (!G || !info) return fail(GABP_EINVAL, "NULL argument");
+    info->n = G->g.n;
+    info->num_edges = G->g.E;
+    info->num_tiles = G->g.ntiles;
+    info->max_degree = G->g.max_degree;
+    info->device = G->device;
+    info->is_dense = G->is_dense;
+    info->rhs_norm = G->g.rhs_norm;
+    info->build_ms = G->g.build_ms;
+    return GABP_OK;
+}
+
+int gabp_graph_export(const gabp_graph_t *G, int64_t *h_row_ptr, int64_t *h_col,
+                      int64_t *h_rev, double *h_coeff) {
+    if (!G) return fail(GABP_EINVAL, "NULL graph");
+    CK(cudaSetDevice(G->device));
+    const DeviceGraph &g = G->g;
+    if (h_row_ptr) {
+        std::vector<uint32_t> rp(g.n + 1);
+        CK(cudaMemcpyAsync(rp.data(), g.row_ptr, sizeof(uint32_t) * (g.n + 1),
+                           cudaMemcpyDeviceToHost, G->stream));
+        CK(cudaStreamSynchronize(G->stream));
+        for (int64_t i = 0; i <= g.n; ++i) h_row_ptr[i] = rp[i];
+    }
+    if ((h_col || h_rev) && g.E > 0) {
+        std::vector<uint2> rc(g.E);
+        CK(cudaMemcpyAsync(rc.data(), g.rc, sizeof(uint2) * g.E, cudaMemcpyDeviceToHost,
+                           G->stream));
+        CK(cudaStreamSynchronize(G->stream));
+        for (int64_t e = 0; e < g.E; ++e) {
+            if (h_rev) h_rev[e] = rc[e].x;
+            if (h_col) h_col[e] = rc[e].y;
+        }
+    }
+    if (h_coeff && g.E > 0) {
+        CK(cudaMemcpyAsync(h_coeff, g.coeff, sizeof(double) * g.E, cudaMemcpyDeviceToHost,
+                           G->stream));
+        CK(cudaStreamSynchronize(G->stream));
+    }
+    return GABP_OK;
+}
+
+int gabp_graph_set_rhs(gabp_graph_t *G, const double *h_rhs) {
+    if (!G || !h_rhs) return fail(GABP_EINVAL, "NULL argument");
+    CK(cudaSetDevice(G->device));
+    CK(cudaMemcpyAsync(G->g.rhs, h_rhs, sizeof(double) * G->g.n, cudaMemcpyHostToDevice,
+                       G->stream));
+    return gabp::compute_priors(G->g, G->stream, g_err, sizeof(g_err));
+}
+
+void *gabp_graph_stream(const gabp_graph_t *G) { return G ? (void *)G->stream : nullptr; }
+
+// ---- message state ---------------------------------------------------------------------
+
+int gabp_state_create(const gabp_graph_t *G, gabp_state_t **out) {
+    if (!G || !out) return fail(GABP_EINVAL, "NULL argument");
+    CK(cudaSetDevice(G->device));
+    gabp_state *S = new gabp_state();
+    S->g = G;
+    const int64_t E = G->g.E > 0 ? G->g.E : 1;
+    for (int b = 0; b < 2; ++b) {
+        cudaError_t e = cudaMalloc(&S->buf[b], sizeof(double2) * E);
+        if (e != cudaSuccess) {
+            cudaFree(S->buf[0]);
+            delete S;
+            return fail(GABP_ENOMEM, "state allocation: %s", cudaGetErrorString(e));
+        }
+    }
+    *out = S;
+    return gabp_state_reset(S);
+}
+
+int gabp_state_clone(const gabp_state_t *S, gabp_state_t **out) {
+    if (!S || !out) return fail(GABP_EINVAL, "NULL argument");
+    int rc = gabp_state_create(S->g, out);
+    if (rc) return rc;
+    gabp_state *D = *out;
+    const int64_t E = S->g->g.E > 0 ? S->g->g.E : 1;
+    CK(cudaMemcpyAsync(D->buf[0], S->buf[S->cur], sizeof(double2) * E, cudaMemcpyDeviceToDevice,
+                       S->g->stream));
+    CK(cudaStreamSynchronize(S->g->stream));
+    D->cur = 0;
+    D->iteration = S->iteration;
+    D->messages_sent = S->messages_sent;
+    return GABP_OK;
+}
+
+void gabp_state_destroy(gabp_state_t *S) {
+    if (!S) return;
+    cudaSetDevice(S->g->device);
+    cudaStreamSynchronize(S->g->stream);
+    cudaFree(S->buf[0]);
+    cudaFree(S->buf[1]);
+    delete S;
+}
+
+int gabp_state_reset(gabp_state_t *S) {
+    if (!S) return fail(GABP_EINVAL, "NULL state");
+    CK(cudaSetDevice(S->g->device));
+    const int64_t E = S->g->g.E > 0 ? S->g->g.E : 1;
+    CK(cudaMemsetAsync(S->buf[0], 0, sizeof(double2) * E, S->g->stream));
+    CK(cudaStreamSynchronize(S->g->stream));
+    S->cur = 0;
+    S->iteration = 0;
+    S->messages_sent = 0;
+    return GABP_OK;
+}
+
+int gabp_state_read(const gabp_state_t *S, double *h_prec, double *h_mean) {
+    if (!S) return fail(GABP_EINVAL, "NULL state");
+    const int64_t E = S->g->g.E;
+    if (E == 0) return GABP_OK;
+    CK(cudaSetDevice(S->g->device));
+    std::vector<double2> tmp(E);
+    CK(cudaMemcpyAsync(tmp.data(), S->buf[S->cur], sizeof(double2) * E, cudaMemcpyDeviceToHost,
+                       S->g->stream));
+    CK(cudaStreamSynchronize(S->g->stream));
+    for (int64_t e = 0; e < E; ++e) {
+        if (h_prec) h_prec[e] = tmp[e].x;
+        if (h_mean) h_mean[e] = tmp[e].y;
+    }
+    return GABP_OK;
+}
+
+int gabp_state_write(gabp_state_t *S, const double *h_prec, const double *h_mean) {
+    if (!S || !h_prec || !h_mean) return fail(GABP_EINVAL, "NULL argument");
+    const int64_t E = S->g->g.E;
+    if (E == 0) return GABP_OK;
+    CK(cudaSetDevice(S->g->device));
+    std::vector<double2> tmp(E);
+    for (int64_t e = 0; e < E; ++e) tmp[e] = make_double2(h_prec[e], h_mean[e]);
+    CK(cudaMemcpyAsync(S->buf[S->cur], tmp.data(), sizeof(double2) * E, cudaMemcpyHostToDevice,
+                       S->g->stream));
+    CK(cudaStreamSynchronize(S->g->stream));
+    return GABP_OK;
+}
+
+int gabp_state_counters(const gabp_state_t *S, int64_t *iteration, int64_t *messages_sent) {
+    if (!S) return fail(GABP_EINVAL, "NULL state");
+    if (iteration) *iteration = S->iteration;
+    if (messages_sent) *messages_sent = S->messages_sent;
+    return GABP_OK;
+}
+
+int gabp_sweep(const gabp_graph_t *Gc, gabp_state_t *S, int32_t schedule, double *max_change,
+               int64_t *singular_index, int32_t *singular_is_node) {
+    gabp_graph *G = const_cast<gabp_graph *>(Gc);
+    if (!G || !S || S->g != Gc) return fail(GABP_EINVAL, "state does not belong to graph");
+    if (schedule != GABP_SCHED_PARALLEL && schedule != GABP_SCHED_BROADCAST)
+        return fail(GABP_EINVAL, "schedule must be parallel (0) or broadcast (2)");
+    CK(cudaSetDevice(G->device));
+    int rc = ensure_workspace(G, 1);
+    if (rc) return rc;
+    if (singular_index) *singular_index = -1;
+    if (singular_is_node) *singular_is_node = 0;
+    if (max_change) *max_change = 0.0;
+    Ctrl c{};
+    *G->h_ctrl = c;
+    CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, G->stream));
+    SweepArgs a = make_args(G);
+    a.msg[0] = S->buf[S->cur];
+    a.msg[1] = S->buf[S->cur ^ 1];
+    if (G->g.E > 0) CK(gabp::launch_sweep(a, schedule, gabp::kModeSingle, G->stream));
+    CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, G->stream));
+    CK(cudaStreamSynchronize(G->stream));
+    const Ctrl &h = *G->h_ctrl;
+    const int slot = 1;
+    if (h.agg_singular[slot]) {
+        if (singular_index) *singular_index = (int64_t)h.agg_singular[slot] - 1;
+        if (singular_is_node) *singular_is_node = 1;
+        return fail(GABP_ESINGULAR, "aggregate precision P~(%lld) = 0",
+                    (long long)h.agg_singular[slot] - 1);
+    }
+    if (h.singular_min[slot]) {
+        if (singular_index) *singular_index = (int64_t)h.singular_min[slot] - 1;
+        return fail(GABP_ESINGULAR, "P_excl = 0 on edge %lld", (long long)h.singular_min[slot] - 1);
+    }
+    if (max_change) {
+        double v;
+        unsigned long long bits = h.change_bits[slot];
+        memcpy(&v, &bits, sizeof(v));
+        *max_change = h.nan_change[slot] ? NAN : v;
+    }
+    S->cur ^= 1;
+    S->iteration += 1;
+    S->messages_sent += (schedule == GABP_SCHED_BROADCAST) ? G->g.n : G->g.E;
+    return GABP_OK;
+}
+
+int gabp_infer_marginals(const gabp_graph_t *G, const gabp_state_t *S, double *h_means,
+                         double *h_precs) {
+    if (!G || !S || S->g != G) return fail(GABP_EINVAL, "state does not belong to graph");
+    CK(cudaSetDevice(G->device));
+    const int64_t n = G->g.n;
+    double *d = nullptr;
+    CK(cudaMallocAsync(&d, sizeof(double) * 2 * n, G->stream));
+    CK(gabp::launch_marginals(n, G->g.row_ptr, G->g.rc, G->g.diag, G->g.prior_num,
+                              S->buf[S->cur], d, d + n, G->stream));
+    if (h_means)
+        CK(cudaMemcpyAsync(h_means, d, sizeof(double) * n, cudaMemcpyDeviceToHost, G->stream));
+    if (h_precs)
+        CK(cudaMemcpyAsync(h_precs, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                           G->stream));
+    CK(cudaFreeAsync(d, G->stream));
+    CK(cudaStreamSynchronize(G->stream));
+    return GABP_OK;
+}
+
+// ---- solve --------------------------------------------------------------------------------
+
+int gabp_solve(gabp_graph_t *G, const gabp_options_t *opt, double *h_means, double *h_precs,
+               double *h_change_hist, double *h_res_hist, gabp_report_t *rep) {
+    if (!G) return fail(GABP_EINVAL, "NULL graph");
+    double ms = 0.0;
+    int rc = run_solve(G, opt, &ms);
+    if (rc) return rc;
+    const Ctrl &c = *G->h_ctrl;
+    cudaStream_t st = G->stream;
+    const int64_t slot = c.final_slot;
+    if (h_means)
+        CK(cudaMemcpyAsync(h_means, G->x[slot], sizeof(double) * G->g.n, cudaMemcpyDeviceToHost,
+                           st));
+    if (h_precs)
+        CK(cudaMemcpyAsync(h_precs, G->p[slot], sizeof(double) * G->g.n, cudaMemcpyDeviceToHost,
+                           st));
+    if (h_change_hist && c.n_hist > 0)
+        CK(cudaMemcpyAsync(h_change_hist, G->change_hist, sizeof(double) * c.n_hist,
+                           cudaMemcpyDeviceToHost, st));
+    if (h_res_hist && c.n_hist > 0)
+        CK(cudaMemcpyAsync(h_res_hist, G->res_hist, sizeof(double) * c.n_hist,
+                           cudaMemcpyDeviceToHost, st));
+    if (opt->h_means_history && G->xhist && c.n_hist > 0) {
+        const int64_t r = c.n_hist < G->xhist_rows ? c.n_hist : G->xhist_rows;
+        CK(cudaMemcpyAsync(opt->h_means_history, G->xhist, sizeof(double) * r * G->g.n,
+                           cudaMemcpyDeviceToHost, st));
+    }
+    double rsq_last = NAN;
+    if (c.n_hist > 0)
+        CK(cudaMemcpyAsync(&rsq_last, G->rsq_hist + (c.n_hist - 1), sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fill_report(G, opt, ms, rsq_last, rep);
+    return GABP_OK;
+}
+
+int gabp_solve_device(gabp_graph_t *G, const gabp_options_t *opt, double *d_means,
+                      double *d_precs, gabp_report_t *rep) {
+    if (!G) return fail(GABP_EINVAL, "NULL graph");
+    double ms = 0.0;
+    int rc = run_solve(G, opt, &ms);
+    if (rc) return rc;
+    const Ctrl &c = *G->h_ctrl;
+    cudaStream_t st = G->stream;
+    const int64_t slot = c.final_slot;
+    if (d_means)
+        CK(cudaMemcpyAsync(d_means, G->x[slot], sizeof(double) * G->g.n,
+                           cudaMemcpyDeviceToDevice, st));
+    if (d_precs)
+        CK(cudaMemcpyAsync(d_precs, G->p[slot], sizeof(double) * G->g.n,
+                           cudaMemcpyDeviceToDevice, st));
+    double rsq_last = NAN;
+    if (c.n_hist > 0)
+        CK(cudaMemcpyAsync(&rsq_last, G->rsq_hist + (c.n_hist - 1), sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fill_report(G, opt, ms, rsq_last, rep);
+    return GABP_OK;
+}
+
+int gabp_solve_system(int64_t n, int64_t npairs, const double *h_diag, const double *h_rhs,
+                      const int64_t *h_pair_i, const int64_t *h_pair_j,
+                      const double *h_pair_v, int32_t device, const gabp_options_t *opt,
+                      double *h_means, double *h_precs, double *h_change_hist,
+                      double *h_res_hist, gabp_report_t *rep) {
+    int rc = check_options(opt);
+    if (rc) return rc;
+    gabp_graph_t *G = nullptr;
+    rc = gabp_graph_create(n, npairs, h_diag, h_rhs, h_pair_i, h_pair_j, h_pair_v, device, &G);
+    if (rc) return rc;
+    rc = gabp_solve(G, opt, h_means, h_precs, h_change_hist, h_res_hist, rep);
+    gabp_graph_destroy(G);
+    return rc;
+}
+
+int gabp_residual_norm_per_eq(const gabp_graph_t *G, const double *h_x, double *out) {
+    if (!G || !h_x || !out) return fail(GABP_EINVAL, "NULL argument");
+    CK(cudaSetDevice(G->device));
+    const int64_t n = G->g.n;
+    const int64_t nparts = (n + 4095) / 4096;
+    double *d = nullptr;
+    CK(cudaMallocAsync(&d, sizeof(double) * (n + nparts + 1), G->stream));
+    CK(cudaMemcpyAsync(d, h_x, sizeof(double) * n, cudaMemcpyHostToDevice, G->stream));
+    CK(gabp::launch_residual_sq(n, G->g.row_ptr, G->g.rc, G->g.coeff, G->g.diag, G->g.rhs, d,
+                                d + n, nparts, d + n + nparts, G->stream));
+    double ss = 0.0;
+    CK(cudaMemcpyAsync(&ss, d + n + nparts, sizeof(double), cudaMemcpyDeviceToHost, G->stream));
+    CK(cudaFreeAsync(d, G->stream));
+    CK(cudaStreamSynchronize(G->stream));
+    *out = sqrt(ss) / (double)n;
+    return GABP_OK;
+}
+
+int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int64_t sweeps, double *ms_per_sweep) {
+    if (!G || sweeps < 1 || !ms_per_sweep) return fail(GABP_EINVAL, "bad argument");
+    if (schedule != GABP_SCHED_PARALLEL && schedule != GABP_SCHED_BROADCAST)
+        return fail(GABP_EINVAL, "bad schedule");
+    CK(cudaSetDevice(G->device));
+    int rc = ensure_workspace(G, 1);
+    if (rc) return rc;
+    Ctrl c{};
+    c.next_sweep = 1;
+    c.epsilon = 0.0;        // never "converged": every launch does the full sweep
+    c.blowup = INFINITY;
+    c.rel_tol = 0.0;
+    c.bnorm = G->g.rhs_norm;
+    c.max_iter = INT64_MAX / 4;
+    c.n = G->g.n;
+    *G->h_ctrl = c;
+    cudaStream_t st = G->stream;
+    // histories are only written when a decision is taken (t <= max_iter): size them
+    rc = ensure_workspace(G, sweeps + 2);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(G->msg[0], 0, sizeof(double2) * (G->g.E > 0 ? G->g.E : 1), st));
+    SweepArgs a = make_args(G);
+    CK(cudaEventRecord(G->ev[2], st));
+    for (int64_t k = 0; k < sweeps; ++k) CK(gabp::launch_sweep(a, schedule, gabp::kModeSolve, st));
+    CK(cudaEventRecord(G->ev[3], st));
+    CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, G->ev[2], G->ev[3]));
+    if (G->h_ctrl->done)
+        return fail(GABP_EINVAL, "bench sweeps stopped early (diverged at sweep %lld)",
+                    (long long)G->h_ctrl->iterations);
+    *ms_per_sweep = ms / (double)sweeps;
+    return GABP_OK;
+}
+
+}  // extern "C"

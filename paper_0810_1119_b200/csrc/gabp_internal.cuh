@@ -1,0 +1,115 @@
+// gabp_internal.cuh -- device data layout and kernel interfaces of libgabp_b200.
+//
+// HBM layout of a built graph:
+//   row_ptr   u32[n+1]   CSR offsets, edges grouped by source, neighbours ascending
+//                        (= reference edge ids, graph.py:84-91)
+//   rc        u32x2[E]   {rev, col}: twin edge id (graph.py:95-97) and destination
+//   coeff     f64[E]     A_ij of edge e
+//   diag      f64[n]     A_ii = prior precision (graph.py:73)
+//   prior_num f64[n]     A_ii * (b_i / A_ii)   (solver.py:147)
+//   rhs       f64[n]
+//   tile_start u32[T+1]  row tiles: <= kTileRows rows, edges bounded by kBucket + deg
+// Message state: msg[2] f64x2[E] = {P, mu} per directed edge (out-slot layout:
+// message i->j lives at edge id of (i->j), i.e. in row i), double-buffered.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gabp_b200.h"
+
+namespace gabp {
+
+constexpr int kThreads = 256;   // threads per sweep block
+constexpr int kTileRows = 256;  // max rows per tile (one thread per row in row phases)
+constexpr int kChunk = 1920;    // edges a tile may stage in shared memory (fast path)
+constexpr int kBucket = 1024;   // tile boundaries every kBucket edge ids (see build.cu)
+constexpr int kStatSlots = 4;   // ring of per-sweep statistic slots
+
+enum Mode { kModeSolve = 0, kModeSingle = 1 };
+
+// Device-resident solve controller.  One kernel launch == one sweep s (1-based).
+// Launch s reads messages S_{s-1}, writes S_s, computes the marginals x^{(s-1)} of the
+// state it read, and the residual of x^{(s-2)} (needs every x^{(s-2)}_j, complete only
+// after launch s-1).  The decision for sweep t = s-2 is taken by the last block of
+// launch s, once change_t, blowup/finiteness of S_t, finiteness of x^{(t)} and the
+// residual of x^{(t)} are all known -- the reference loop body of solver.py:321-343.
+struct Ctrl {
+    int64_t next_sweep;  // s of the next launch
+    int32_t done;
+    int32_t converged;
+    int32_t diverged;
+    uint32_t ticket;     // finished-block counter of the current launch
+    int64_t iterations;
+    int64_t n_hist;
+    int64_t final_slot;  // x/p ring slot holding the returned marginals
+    double epsilon, blowup, rel_tol, bnorm;
+    int64_t max_iter;
+    int64_t n;
+    // per-sweep statistics, slot = sweep % kStatSlots
+    unsigned long long change_bits[kStatSlots];   // max |dP|,|dmu| (non-negative -> bit order)
+    unsigned long long biggest_bits[kStatSlots];  // max |P|,|mu| of S_t
+    int32_t nan_change[kStatSlots];
+    int32_t msg_nonfinite[kStatSlots];
+    int32_t means_nonfinite[kStatSlots];
+    unsigned long long agg_singular[kStatSlots];   // broadcast: 1 + first node with P_i == 0
+    unsigned long long singular_min[kStatSlots];   // 1 + first edge (or node) with P_excl == 0
+};
+
+struct SweepArgs {
+    int64_t n;
+    int64_t ntiles;
+    const uint32_t *row_ptr;
+    const uint32_t *tile_start;
+    const uint2 *rc;
+    const double *coeff;
+    const double *diag;
+    const double *prior_num;
+    const double *rhs;
+    double2 *msg[2];
+    double *x[3];
+    double *p[3];
+    double *rsq_part;   // [ntiles]
+    Ctrl *ctrl;
+    double *change_hist;
+    double *res_hist;
+    double *rsq_hist;
+    double *xhist;        // optional [xhist_rows x n] tentative means per sweep
+    int64_t xhist_rows;
+};
+
+// kernels (sweep.cu); prepare_sweep_kernels() must run once per device before launches
+cudaError_t prepare_sweep_kernels();
+cudaError_t launch_sweep(const SweepArgs &a, int schedule, int mode, cudaStream_t st);
+cudaError_t launch_marginals(int64_t n, const uint32_t *row_ptr, const uint2 *rc,
+                             const double *diag, const double *prior_num, const double2 *msg,
+                             double *means, double *precs, cudaStream_t st);
+cudaError_t launch_residual_sq(int64_t n, const uint32_t *row_ptr, const uint2 *rc,
+                               const double *coeff, const double *diag, const double *rhs,
+                               const double *x, double *part, int64_t nparts, double *out,
+                               cudaStream_t st);
+
+// graph build (build.cu)
+struct DeviceGraph {
+    int64_t n = 0, E = 0, npairs = 0, ntiles = 0, max_degree = 0;
+    int device = 0;
+    uint32_t *row_ptr = nullptr;
+    uint32_t *tile_start = nullptr;
+    uint2 *rc = nullptr;
+    double *coeff = nullptr;
+    double *diag = nullptr;
+    double *prior_num = nullptr;
+    double *rhs = nullptr;
+    double rhs_norm = 0.0;
+    double build_ms = 0.0;
+};
+
+// Builds CSR + twin index + tiles from device-resident inputs.  Returns a GABP_* code
+// and fills *err with a message on failure.
+int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *d_diag,
+                       const double *d_rhs, const int64_t *d_pi, const int64_t *d_pj,
+                       const double *d_pv, cudaStream_t st, char *err, size_t errlen);
+void free_graph(DeviceGraph &g);
+int compute_priors(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
+
+}  // namespace gabp

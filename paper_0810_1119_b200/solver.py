@@ -1,0 +1,270 @@
+"""Gaussian BP engine -- drop-in for the reference ``solver.py`` synchronous path.
+
+Reference: /root/reference/pkg/src/gabp/solver.py.  Same names, signatures, argument
+meaning and error behaviour for the synchronous schedules:
+
+  SolveOptions      solver.py:38-54   (+ extensions, all defaulted: rel_residual_tol,
+                                        sweeps_per_poll, device, record_means_history)
+  MessageState      solver.py:57-74   device-resident messages, host copies on access
+  SolveReport       solver.py:77-89   (+ device_ms, sweeps_launched, final_rel_residual)
+  initial_state     solver.py:92-97
+  sweep             solver.py:220-229 parallel | broadcast
+  broadcast_sweep   solver.py:232-272
+  infer_marginals   solver.py:275-287
+  solve             solver.py:307-346
+
+Every sweep runs in the CUDA library (include/gabp_b200.h); there is no CPU path.
+The "serial" schedule (solver.py:176-217: an in-place Gauss-Seidel-ordered sweep) is
+inherently sequential and outside this synchronous hot path: it raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .graph import GaussianGraph, build_graph
+from .linalg import SymSystem
+
+SCHEDULES = ("parallel", "serial", "broadcast")
+GPU_SCHEDULES = ("parallel", "broadcast")
+_AUTO_MEANS_HISTORY_DOUBLES = 1 << 24
+
+
+class SingularSubgraphError(ArithmeticError):
+    """An exclusion precision hit exactly zero; the update is undefined (solver.py:34)."""
+
+
+@dataclass
+class SolveOptions:
+    epsilon: float = 1e-6
+    max_iter: int = 10_000
+    blowup: float = 1e10
+    schedule: str = "parallel"
+    serial_order: list[int] | None = None
+    # extensions (not in the reference)
+    rel_residual_tol: float | None = None   # also stop when ||Ax-b||/||b|| < tol
+    sweeps_per_poll: int = 0                # sweeps per CUDA-graph chunk; 0 = auto
+    device: int | None = None
+    record_means_history: bool | None = None  # None: auto (n * max_iter <= 2^24)
+
+    def __post_init__(self):
+        if self.epsilon <= 0.0:
+            raise ValueError("epsilon must be positive")
+        if self.max_iter < 1:
+            raise ValueError("max_iter must be >= 1")
+        if not self.blowup > 1.0:
+            raise ValueError("blowup must exceed 1")
+        if self.schedule not in SCHEDULES:
+            raise ValueError(f"schedule must be one of {SCHEDULES}")
+
+
+def _gpu_schedule(schedule: str) -> int:
+    if schedule not in GPU_SCHEDULES:
+        raise ValueError(
+            f"schedule {schedule!r} is not a synchronous sweep; the B200 path implements "
+            f"{GPU_SCHEDULES} (the serial schedule is sequential by definition)")
+    return _lib.SCHED_IDS[schedule]
+
+
+class MessageState:
+    """Per-directed-edge (P, mu) messages held in HBM (solver.py:57-74)."""
+
+    def __init__(self, graph: GaussianGraph, schedule: str = "parallel", _handle=None):
+        self.graph = graph
+        self.schedule = schedule
+        if _handle is None:
+            h = ctypes.c_void_p()
+            _lib.check(_lib.load().gabp_state_create(graph.handle, ctypes.byref(h)))
+            _handle = h
+        self._h = _handle
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _counters(self):
+        it = ctypes.c_int64()
+        ms = ctypes.c_int64()
+        _lib.check(_lib.load().gabp_state_counters(self._h, ctypes.byref(it), ctypes.byref(ms)))
+        return int(it.value), int(ms.value)
+
+    @property
+    def iteration(self) -> int:
+        return self._counters()[0]
+
+    @property
+    def messages_sent(self) -> int:
+        return self._counters()[1]
+
+    def _read(self):
+        E = self.graph.num_edges
+        p = np.empty(E)
+        m = np.empty(E)
+        _lib.check(_lib.load().gabp_state_read(self._h, _lib.ptr(p), _lib.ptr(m)))
+        return p, m
+
+    @property
+    def prec(self) -> np.ndarray:
+        return self._read()[0]
+
+    @property
+    def mean(self) -> np.ndarray:
+        return self._read()[1]
+
+    def set_messages(self, prec, mean) -> None:
+        prec = np.ascontiguousarray(prec, dtype=np.float64)
+        mean = np.ascontiguousarray(mean, dtype=np.float64)
+        if prec.shape != (self.graph.num_edges,) or mean.shape != prec.shape:
+            raise ValueError("message arrays must have one entry per directed edge")
+        _lib.check(_lib.load().gabp_state_write(self._h, _lib.ptr(prec), _lib.ptr(mean)))
+
+    def copy(self) -> "MessageState":
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().gabp_state_clone(self._h, ctypes.byref(h)))
+        return MessageState(self.graph, self.schedule, _handle=h)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.load().gabp_state_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class SolveReport:
+    converged: bool
+    diverged: bool
+    iterations: int
+    means: np.ndarray
+    precisions: np.ndarray | None
+    max_change_history: list = field(default_factory=list)
+    residual_history: list = field(default_factory=list)
+    means_history: list = field(default_factory=list)
+    messages_sent: int = 0
+    precisions_exact: bool | None = None
+    # extensions
+    device_ms: float = 0.0
+    sweeps_launched: int = 0
+    final_rel_residual: float = float("nan")
+
+
+def initial_state(graph: GaussianGraph, schedule: str = "parallel") -> MessageState:
+    """solver.py:92-97: all messages exactly zero."""
+    return MessageState(graph, schedule)
+
+
+def _sweep(graph: GaussianGraph, state: MessageState, schedule: str):
+    sched = _gpu_schedule(schedule)
+    out = state.copy()
+    out.schedule = schedule
+    mc = ctypes.c_double()
+    si = ctypes.c_int64()
+    node = ctypes.c_int32()
+    rc = _lib.load().gabp_sweep(graph.handle, out.handle, sched, ctypes.byref(mc),
+                                ctypes.byref(si), ctypes.byref(node))
+    if rc == _lib.GABP_ESINGULAR:
+        out.close()
+        k = int(si.value)
+        if node.value:
+            raise SingularSubgraphError(f"aggregate precision P~({k}) = 0")
+        src = int(graph.src[k])
+        dst = int(graph.dst[k])
+        raise SingularSubgraphError(f"P_excl({src} -> {dst}) = 0")
+    _lib.check(rc)
+    return out, float(mc.value)
+
+
+def sweep(graph: GaussianGraph, state: MessageState, options: SolveOptions):
+    """One message-passing round; returns (new state, max message change)."""
+    return _sweep(graph, state, options.schedule)
+
+
+def broadcast_sweep(graph: GaussianGraph, state: MessageState, options=None):
+    """solver.py:232-272: aggregate-and-subtract round."""
+    return _sweep(graph, state, "broadcast")
+
+
+def infer_marginals(graph: GaussianGraph, state: MessageState):
+    """solver.py:275-287: (means, precisions); non-finite means where prec_tot == 0."""
+    means = np.empty(graph.n)
+    precs = np.empty(graph.n)
+    _lib.check(_lib.load().gabp_infer_marginals(graph.handle, state.handle, _lib.ptr(means),
+                                                 _lib.ptr(precs)))
+    return means, precs
+
+
+def _options_struct(options: SolveOptions, n: int, hist: np.ndarray | None) -> _lib.Options:
+    o = _lib.Options()
+    o.epsilon = float(options.epsilon)
+    o.max_iter = int(options.max_iter)
+    o.blowup = float(options.blowup)
+    o.schedule = _gpu_schedule(options.schedule)
+    o.sweeps_per_poll = int(options.sweeps_per_poll)
+    o.rel_residual_tol = float(options.rel_residual_tol or 0.0)
+    if hist is not None:
+        o.means_history = hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        o.means_history_rows = hist.shape[0]
+    return o
+
+
+def _want_means_history(options: SolveOptions, n: int) -> bool:
+    if options.record_means_history is None:
+        return n * options.max_iter <= _AUTO_MEANS_HISTORY_DOUBLES
+    return bool(options.record_means_history)
+
+
+def solve_graph(graph: GaussianGraph, options: SolveOptions | None = None) -> SolveReport:
+    """solve() on an already built graph (reuses its device workspace)."""
+    options = options or SolveOptions()
+    n = graph.n
+    hist = np.empty((options.max_iter, n)) if _want_means_history(options, n) else None
+    o = _options_struct(options, n, hist)
+    means = np.empty(n)
+    precs = np.empty(n)
+    ch = np.empty(options.max_iter)
+    rh = np.empty(options.max_iter)
+    rep = _lib.Report()
+    _lib.check(_lib.load().gabp_solve(graph.handle, ctypes.byref(o), _lib.ptr(means),
+                                      _lib.ptr(precs), _lib.ptr(ch), _lib.ptr(rh),
+                                      ctypes.byref(rep)))
+    k = int(rep.n_hist)
+    return SolveReport(
+        converged=bool(rep.converged),
+        diverged=bool(rep.diverged),
+        iterations=int(rep.iterations),
+        means=means,
+        precisions=precs,
+        max_change_history=ch[:k].tolist(),
+        residual_history=rh[:k].tolist(),
+        means_history=[hist[t].copy() for t in range(k)] if hist is not None else [],
+        messages_sent=int(rep.messages_sent),
+        precisions_exact=graph.is_tree(),
+        device_ms=float(rep.device_ms),
+        sweeps_launched=int(rep.sweeps_launched),
+        final_rel_residual=float(rep.final_rel_residual),
+    )
+
+
+def solve(system: SymSystem, options: SolveOptions | None = None) -> SolveReport:
+    """solver.py:307-346: run GaBP to convergence, divergence or the sweep cap.
+
+    The sweep that first leaves every message within epsilon of its previous value is
+    counted; per-sweep message change and residual_norm_per_eq of the tentative means
+    are recorded.  Divergence (blowup, non-finite values, a singular exclusion sum, the
+    sweep cap) is reported, never raised."""
+    options = options or SolveOptions()
+    _gpu_schedule(options.schedule)
+    graph = build_graph(system, options.device)
+    try:
+        return solve_graph(graph, options)
+    finally:
+        graph.close()

@@ -1,0 +1,314 @@
+"""CUDA path vs the reference (golden fixtures) and the C oracle -- the parity gate.
+
+Bar: bitwise for messages, marginals, change history and iteration counts (the kernels
+use the reference's operation order without FMA contraction); the in-solve residual
+history is reduced in a different order and is compared to 1e-9 relative.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_0810_1119_b200 as G
+from oracle import oracle
+from paper_0810_1119_b200 import _lib
+from tests import golden_cases as gc
+
+pytestmark = pytest.mark.gpu
+CASES = gc.names()
+SCHEDS = ["parallel", "broadcast"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    _lib.load()
+    assert _lib.device_count() > 0, "no CUDA device: " + _lib.last_error()
+    oracle.build()
+
+
+def _res_close(got, want):
+    got = np.asarray(got)
+    want = np.asarray(want)
+    assert got.shape == want.shape
+    fin = np.isfinite(want)
+    np.testing.assert_array_equal(np.isfinite(got), fin)
+    atol = 1e-12 * float(np.max(want[fin], initial=0.0))
+    np.testing.assert_allclose(got[fin], want[fin], rtol=1e-9, atol=atol)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_graph_build_matches_reference(case):
+    rec = gc.load(case)
+    g = G.build_graph(gc.system(rec))
+    np.testing.assert_array_equal(g.src, rec["src"])
+    np.testing.assert_array_equal(g.dst, rec["dst"])
+    np.testing.assert_array_equal(g.rev, rec["rev"])
+    np.testing.assert_array_equal(g.coeff, rec["coeff"])
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_sweep_trace_bitwise(case, sched):
+    rec = gc.load(case)
+    g = G.build_graph(gc.system(rec))
+    st = G.initial_state(g, sched)
+    opts = G.SolveOptions(schedule=sched)
+    tp, tm, tc = (rec[f"{sched}_trace_prec"], rec[f"{sched}_trace_mean"],
+                  rec[f"{sched}_trace_change"])
+    for t in range(tp.shape[0]):
+        st, change = G.sweep(g, st, opts)
+        np.testing.assert_array_equal(st.prec, tp[t])
+        np.testing.assert_array_equal(st.mean, tm[t])
+        assert change == tc[t]
+        assert st.iteration == t + 1
+    if int(rec[f"{sched}_trace_singular_at"]) > 0:
+        with pytest.raises(G.SingularSubgraphError):
+            G.sweep(g, st, opts)
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_marginals_bitwise_vs_oracle(case, sched):
+    rec = gc.load(case)
+    g = G.build_graph(gc.system(rec))
+    og = oracle.build_graph(rec["diag"], rec["rhs"], rec["pair_i"], rec["pair_j"],
+                            rec["pair_v"])
+    st = G.initial_state(g, sched)
+    for t in range(rec[f"{sched}_trace_prec"].shape[0]):
+        st, _ = G.sweep(g, st, G.SolveOptions(schedule=sched))
+        means, precs = G.infer_marginals(g, st)
+        om, op = oracle.marginals(og, st.prec, st.mean)
+        np.testing.assert_array_equal(means, om)
+        np.testing.assert_array_equal(precs, op)
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("sched", SCHEDS)
+@pytest.mark.parametrize("poll", [0, 1, 3])
+def test_solve_matches_reference(case, sched, poll):
+    rec = gc.load(case)
+    tol = float(rec["rel_residual_tol"]) or None
+    opts = G.SolveOptions(schedule=sched, epsilon=float(rec["epsilon"]),
+                          max_iter=int(rec["max_iter"]), rel_residual_tol=tol,
+                          sweeps_per_poll=poll)
+    r = G.solve(gc.system(rec), opts)
+    assert r.converged == bool(rec[f"{sched}_converged"])
+    assert r.diverged == bool(rec[f"{sched}_diverged"])
+    assert r.converged != r.diverged
+    assert r.iterations == int(rec[f"{sched}_iterations"])
+    want = rec[f"{sched}_means"]
+    fin = np.isfinite(want)
+    np.testing.assert_array_equal(np.isfinite(r.means), fin)
+    np.testing.assert_array_equal(r.means[fin], want[fin])
+    np.testing.assert_array_equal(r.precisions, rec[f"{sched}_precisions"])
+    ch = rec[f"{sched}_change_hist"]
+    got = np.asarray(r.max_change_history)
+    assert got.shape == ch.shape
+    cf = np.isfinite(ch)
+    np.testing.assert_array_equal(got[cf], ch[cf])
+    _res_close(r.residual_history, rec[f"{sched}_res_hist"])
+    assert len(r.residual_history) == len(r.max_change_history)
+    if r.means_history:
+        assert len(r.means_history) == len(r.max_change_history)
+        if r.iterations == len(r.means_history) and r.iterations > 0:
+            np.testing.assert_array_equal(r.means_history[-1][fin], want[fin])
+
+
+def test_toy3_trace_and_report():
+    """Reference solver tests test_solve_toy3_counts_and_trace / test_marginals_toy3."""
+    sys3 = G.load_instance("toy3").system
+    r = G.solve(sys3, G.SolveOptions(schedule="parallel"))
+    assert r.converged and not r.diverged and r.iterations == 3
+    np.testing.assert_allclose(r.means, [1.0, 2.0, -1.0], atol=1e-14)
+    np.testing.assert_allclose(r.precisions, [-12.0, 1.5, 4.0], atol=1e-14)
+    assert r.precisions_exact is True
+    np.testing.assert_allclose(r.means_history[0], [1.0, 4.0, -2.5], atol=1e-14)
+    np.testing.assert_allclose(r.means_history[1], [1.0, 2.0, -1.0], atol=1e-14)
+    assert r.messages_sent == 3 * 4
+
+
+def test_broadcast_message_accounting():
+    system = G.gen_random("spd", 10, 17).system
+    g = G.build_graph(system)
+    naive, _ = G.sweep(g, G.initial_state(g), G.SolveOptions())
+    bcast, _ = G.broadcast_sweep(g, G.initial_state(g, "broadcast"))
+    assert naive.messages_sent == 90
+    assert bcast.messages_sent == 10
+
+
+def test_sweep_is_functional():
+    """sweep returns a new state; the input state is unchanged (solver.py:166-173)."""
+    g = G.build_graph(G.load_instance("cdma4").system)
+    s0 = G.initial_state(g)
+    s1, _ = G.sweep(g, s0, G.SolveOptions())
+    s2, _ = G.sweep(g, s1, G.SolveOptions())
+    assert np.all(s0.prec == 0.0) and s0.iteration == 0
+    assert s1.iteration == 1 and s2.iteration == 2
+    assert not np.array_equal(s1.mean, s2.mean)
+
+
+def test_identity_system_noop():
+    ident = G.SymSystem(diag=np.ones(3), offdiag={}, rhs=np.array([1.0, 2.0, 3.0]))
+    g = G.build_graph(ident)
+    st, change = G.sweep(g, G.initial_state(g), G.SolveOptions())
+    assert change == 0.0 and st.prec.size == 0
+    means, precs = G.infer_marginals(g, st)
+    np.testing.assert_array_equal(means, ident.rhs)
+    np.testing.assert_array_equal(precs, np.ones(3))
+
+
+def test_single_node():
+    s = G.SymSystem(diag=np.array([2.0]), offdiag={}, rhs=np.array([3.0]))
+    r = G.solve(s)
+    assert r.converged and r.iterations == 1
+    assert r.means[0] == 1.5
+
+
+def test_zero_diagonal_rejected():
+    s = G.SymSystem(diag=np.array([1.0, 0.0, 1.0]), offdiag={(0, 1): 2.0}, rhs=np.zeros(3))
+    with pytest.raises(G.ZeroDiagonalError, match="row 1"):
+        G.build_graph(s)
+
+
+def test_duplicate_pair_rejected_by_device_builder():
+    s = G.SymSystem.from_pairs(np.full(3, 4.0), [0, 0], [1, 1], [1.0, 2.0], np.ones(3),
+                               validate=False)
+    with pytest.raises(ValueError, match="duplicate"):
+        G.build_graph(s)
+
+
+def test_bad_pair_rejected_by_device_builder():
+    s = G.SymSystem.from_pairs(np.full(3, 4.0), [1], [0], [1.0], np.ones(3), validate=False)
+    with pytest.raises(ValueError, match="bad off-diagonal"):
+        G.build_graph(s)
+
+
+def test_unsorted_pair_order_same_graph():
+    """Pair order in the input never changes edge ids or results."""
+    base = G.gen_random_sparse(500, 8, 3).system
+    perm = np.random.default_rng(0).permutation(base.pair_v.size)
+    shuf = G.SymSystem.from_pairs(base.diag, base.pair_i[perm], base.pair_j[perm],
+                                  base.pair_v[perm], base.rhs)
+    a = G.solve(base, G.SolveOptions(rel_residual_tol=1e-10, epsilon=1e-300))
+    b = G.solve(shuf, G.SolveOptions(rel_residual_tol=1e-10, epsilon=1e-300))
+    assert a.iterations == b.iterations
+    np.testing.assert_array_equal(a.means, b.means)
+
+
+def test_dense_entry_point_matches_sparse():
+    inst, _ = G.gen_cdma_detection(64, 32, 0.5, 2)
+    a, b = inst.system.to_dense()
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    _lib.check(lib.gabp_graph_create_dense(32, _lib.ptr(a), _lib.ptr(b), 0, ctypes.byref(h)))
+    try:
+        o = G.solver._options_struct(G.SolveOptions(schedule="broadcast"), 32, None)
+        means = np.empty(32)
+        rep = _lib.Report()
+        _lib.check(lib.gabp_solve(h, ctypes.byref(o), _lib.ptr(means), None, None, None,
+                                  ctypes.byref(rep)))
+    finally:
+        lib.gabp_graph_destroy(h)
+    ref = G.solve(inst.system, G.SolveOptions(schedule="broadcast"))
+    assert rep.iterations == ref.iterations
+    np.testing.assert_array_equal(means, ref.means)
+
+
+def test_c_abi_solve_system_host_buffers():
+    """The one-call drop-in (gabp_solve_system) with host buffers."""
+    s = G.gen_poisson2d(32, 0).system
+    lib = _lib.load()
+    o = G.solver._options_struct(G.SolveOptions(schedule="broadcast", epsilon=1e-300,
+                                                rel_residual_tol=1e-8), s.n, None)
+    means = np.empty(s.n)
+    ch = np.empty(o.max_iter)
+    rh = np.empty(o.max_iter)
+    rep = _lib.Report()
+    _lib.check(lib.gabp_solve_system(s.n, s.pair_v.size, _lib.ptr(s.diag), _lib.ptr(s.rhs),
+                                     _lib.ptr(s.pair_i), _lib.ptr(s.pair_j), _lib.ptr(s.pair_v),
+                                     0, ctypes.byref(o), _lib.ptr(means), None, _lib.ptr(ch),
+                                     _lib.ptr(rh), ctypes.byref(rep)))
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    orc = oracle.solve(og, epsilon=1e-300, schedule="broadcast", rel_residual_tol=1e-8)
+    assert rep.converged and rep.iterations == orc.iterations
+    np.testing.assert_array_equal(means, orc.means)
+    assert rep.final_rel_residual < 1e-8
+
+
+def test_residual_norm_per_eq_matches_oracle():
+    s = G.gen_random_sparse(2000, 16, 5).system
+    g = G.build_graph(s)
+    x = np.random.default_rng(1).standard_normal(s.n)
+    out = ctypes.c_double()
+    _lib.check(_lib.load().gabp_residual_norm_per_eq(g.handle, _lib.ptr(x), ctypes.byref(out)))
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    assert out.value == np.sqrt(oracle.residual_sq(og, x)) / s.n
+
+
+# ---------------------------------------------------------------------------------------
+# BASELINE configs at (near) full size: bitwise vs the oracle where it finishes in
+# seconds, size-independent properties otherwise.
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_config1_random_1M_full_solve(sched):
+    s = G.gen_random_sparse(1 << 20, 16, 0).system
+    opts = G.SolveOptions(schedule=sched, epsilon=1e-300, rel_residual_tol=1e-8)
+    r = G.solve(s, opts)
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    orc = oracle.solve(og, epsilon=1e-300, schedule=sched, rel_residual_tol=1e-8)
+    assert r.converged and orc.converged
+    assert r.iterations == orc.iterations
+    np.testing.assert_array_equal(r.means, orc.means)
+    np.testing.assert_array_equal(r.precisions, orc.precisions)
+    np.testing.assert_array_equal(np.asarray(r.max_change_history), orc.max_change_history)
+    _res_close(r.residual_history, orc.residual_history)
+    # independent check of the answer
+    rel = np.linalg.norm(s.matvec(r.means) - s.rhs) / np.linalg.norm(s.rhs)
+    assert rel < 1e-8
+
+
+def test_config2_poisson_4096_sweeps_vs_oracle():
+    """n = 16.8M: five sweeps bitwise against the oracle, then the marginals."""
+    s = G.gen_poisson2d(4096, 0).system
+    g = G.build_graph(s)
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    st = G.initial_state(g, "broadcast")
+    p = np.zeros(g.num_edges)
+    m = np.zeros(g.num_edges)
+    for _ in range(5):
+        st, c = G.broadcast_sweep(g, st)
+        p, m, oc, _ = oracle.sweep(og, p, m, "broadcast")
+        assert c == oc
+    np.testing.assert_array_equal(st.prec, p)
+    np.testing.assert_array_equal(st.mean, m)
+    means, _ = G.infer_marginals(g, st)
+    om, _ = oracle.marginals(og, p, m)
+    np.testing.assert_array_equal(means, om)
+
+
+def test_config3_cdma_full_detection():
+    """K = 4096 users, N = 8192 chips: GaBP (broadcast) on all K^2 edges vs the
+    direct solution; decisions must match the decorrelator's."""
+    inst, s_true = G.gen_cdma_detection(8192, 4096, 0.5, 0)
+    r = G.solve(inst.system, G.SolveOptions(schedule="broadcast", epsilon=1e-300,
+                                            rel_residual_tol=1e-8, max_iter=2000))
+    a, b = inst.system.to_dense()
+    x = np.linalg.solve(a, b)
+    if r.converged:
+        np.testing.assert_allclose(r.means, x, rtol=0, atol=1e-6 * np.abs(x).max())
+        assert np.array_equal(np.sign(r.means), np.sign(x))
+    else:
+        assert r.diverged
+
+
+def test_config4_poisson3d_small_slab_vs_oracle():
+    s = G.gen_poisson3d(64, 0).system
+    r = G.solve(s, G.SolveOptions(schedule="broadcast", max_iter=30, epsilon=1e-300))
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    orc = oracle.solve(og, epsilon=1e-300, max_iter=30, schedule="broadcast")
+    assert r.iterations == orc.iterations == 30 and r.diverged and orc.diverged
+    np.testing.assert_array_equal(r.means, orc.means)
