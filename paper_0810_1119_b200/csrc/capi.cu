@@ -9,6 +9,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
 #include <vector>
 
 #include "gabp_internal.cuh"
@@ -40,6 +41,9 @@ int fail(int code, const char *fmt, ...) {
 }  // namespace
 
 struct gabp_graph {
+    // owner handle + one per live gabp_state: destruction order between a graph and
+    // its states does not matter (Python GC may finalise either first)
+    std::atomic<int> refs{1};
     DeviceGraph g;
     cudaStream_t stream = nullptr;
     int device = 0;
@@ -215,7 +219,7 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         G->xhist_rows = rows;
         G->ws_gen++;
     }
-    Ctrl c{};
+    Ctrl c = gabp::fresh_ctrl();
     c.next_sweep = 1;
     c.epsilon = opt->epsilon;
     c.blowup = opt->blowup;
@@ -407,14 +411,19 @@ int gabp_graph_create_dense(int64_t n, const double *h_a, const double *h_rhs, i
     return rc;
 }
 
-void gabp_graph_destroy(gabp_graph_t *G) {
-    if (!G) return;
+static void graph_release(gabp_graph *G) {
+    if (G->refs.fetch_sub(1) != 1) return;
     cudaSetDevice(G->device);
     cudaStreamSynchronize(G->stream);
     release_workspace(G);
     gabp::free_graph(G->g);
     cudaStreamDestroy(G->stream);
     delete G;
+}
+
+void gabp_graph_destroy(gabp_graph_t *G) {
+    if (!G) return;
+    graph_release(G);
 }
 
 int gabp_graph_info(const gabp_graph_t *G, gabp_graph_info_t *info) {
@@ -477,11 +486,13 @@ int gabp_state_create(const gabp_graph_t *G, gabp_state_t **out) {
     CK(cudaSetDevice(G->device));
     gabp_state *S = new gabp_state();
     S->g = G;
+    const_cast<gabp_graph *>(G)->refs.fetch_add(1);
     const int64_t E = G->g.E > 0 ? G->g.E : 1;
     for (int b = 0; b < 2; ++b) {
         cudaError_t e = cudaMalloc(&S->buf[b], sizeof(double2) * E);
         if (e != cudaSuccess) {
             cudaFree(S->buf[0]);
+            graph_release(const_cast<gabp_graph *>(G));
             delete S;
             return fail(GABP_ENOMEM, "state allocation: %s", cudaGetErrorString(e));
         }
@@ -511,6 +522,7 @@ void gabp_state_destroy(gabp_state_t *S) {
     cudaStreamSynchronize(S->g->stream);
     cudaFree(S->buf[0]);
     cudaFree(S->buf[1]);
+    graph_release(const_cast<gabp_graph *>(S->g));
     delete S;
 }
 
@@ -574,7 +586,7 @@ int gabp_sweep(const gabp_graph_t *Gc, gabp_state_t *S, int32_t schedule, double
     if (singular_index) *singular_index = -1;
     if (singular_is_node) *singular_is_node = 0;
     if (max_change) *max_change = 0.0;
-    Ctrl c{};
+    Ctrl c = gabp::fresh_ctrl();
     *G->h_ctrl = c;
     CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, G->stream));
     SweepArgs a = make_args(G);
@@ -585,15 +597,15 @@ int gabp_sweep(const gabp_graph_t *Gc, gabp_state_t *S, int32_t schedule, double
     CK(cudaStreamSynchronize(G->stream));
     const Ctrl &h = *G->h_ctrl;
     const int slot = 1;
-    if (h.agg_singular[slot]) {
-        if (singular_index) *singular_index = (int64_t)h.agg_singular[slot] - 1;
+    if (h.agg_singular[slot] != gabp::kNoIndex) {
+        if (singular_index) *singular_index = (int64_t)h.agg_singular[slot];
         if (singular_is_node) *singular_is_node = 1;
         return fail(GABP_ESINGULAR, "aggregate precision P~(%lld) = 0",
-                    (long long)h.agg_singular[slot] - 1);
+                    (long long)h.agg_singular[slot]);
     }
-    if (h.singular_min[slot]) {
-        if (singular_index) *singular_index = (int64_t)h.singular_min[slot] - 1;
-        return fail(GABP_ESINGULAR, "P_excl = 0 on edge %lld", (long long)h.singular_min[slot] - 1);
+    if (h.singular_min[slot] != gabp::kNoIndex) {
+        if (singular_index) *singular_index = (int64_t)h.singular_min[slot];
+        return fail(GABP_ESINGULAR, "P_excl = 0 on edge %lld", (long long)h.singular_min[slot]);
     }
     if (max_change) {
         double v;
@@ -727,7 +739,7 @@ int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int64_t sweeps, double 
     CK(cudaSetDevice(G->device));
     int rc = ensure_workspace(G, 1);
     if (rc) return rc;
-    Ctrl c{};
+    Ctrl c = gabp::fresh_ctrl();
     c.next_sweep = 1;
     c.epsilon = 0.0;        // never "converged": every launch does the full sweep
     c.blowup = INFINITY;

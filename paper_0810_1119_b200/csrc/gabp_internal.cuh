@@ -25,6 +25,7 @@ constexpr int kTileRows = 256;  // max rows per tile (one thread per row in row 
 constexpr int kChunk = 1920;    // edges a tile may stage in shared memory (fast path)
 constexpr int kBucket = 1024;   // tile boundaries every kBucket edge ids (see build.cu)
 constexpr int kStatSlots = 4;   // ring of per-sweep statistic slots
+constexpr unsigned long long kNoIndex = ~0ull;  // "no singular edge/node" sentinel
 
 enum Mode { kModeSolve = 0, kModeSingle = 1 };
 
@@ -52,9 +53,19 @@ struct Ctrl {
     int32_t nan_change[kStatSlots];
     int32_t msg_nonfinite[kStatSlots];
     int32_t means_nonfinite[kStatSlots];
-    unsigned long long agg_singular[kStatSlots];   // broadcast: 1 + first node with P_i == 0
-    unsigned long long singular_min[kStatSlots];   // 1 + first edge (or node) with P_excl == 0
+    unsigned long long agg_singular[kStatSlots];   // broadcast: first node with P_i == 0
+    unsigned long long singular_min[kStatSlots];   // first edge with P_excl == 0
 };
+
+// A fresh controller: every "first index" slot at the kNoIndex sentinel.
+inline Ctrl fresh_ctrl() {
+    Ctrl c{};
+    for (int k = 0; k < kStatSlots; ++k) {
+        c.agg_singular[k] = kNoIndex;
+        c.singular_min[k] = kNoIndex;
+    }
+    return c;
+}
 
 struct SweepArgs {
     int64_t n;
