@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libgabp_b200.so")
+LIB_PATH = os.environ.get("GABP_LIB") or os.path.join(_PKG, "lib", "libgabp_b200.so")
 
 GABP_OK = 0
 GABP_EINVAL = -1

@@ -108,6 +108,15 @@ __global__ void tile_scatter_kernel(int64_t n, const uint32_t *flag, const uint3
     if (blockIdx.x == 0 && threadIdx.x == 0) tile_start[ntiles] = (uint32_t)n;
 }
 
+__global__ void tile_info_kernel(int64_t ntiles, const uint32_t *tile_start,
+                                 const uint32_t *row_ptr, uint4 *info) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r0 = tile_start[t], r1 = tile_start[t + 1];
+        info[t] = make_uint4(r0, r1, row_ptr[r0], row_ptr[r1]);
+    }
+}
+
 __global__ void prior_kernel(int64_t n, const double *diag, const double *rhs,
                              double *prior_num, int *err, unsigned long long *err_at) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -163,6 +172,7 @@ struct Scratch {
 void free_graph(DeviceGraph &g) {
     cudaFree(g.row_ptr);
     cudaFree(g.tile_start);
+    cudaFree(g.tile_info);
     cudaFree(g.rc);
     cudaFree(g.coeff);
     cudaFree(g.diag);
@@ -226,14 +236,20 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
     cudaEventCreate(&t1);
     cudaEventRecord(t0, st);
 
-    BCHECK(cudaMallocAsync(&g.diag, sizeof(double) * n, st));
-    BCHECK(cudaMallocAsync(&g.rhs, sizeof(double) * n, st));
-    BCHECK(cudaMallocAsync(&g.prior_num, sizeof(double) * n, st));
+    BCHECK(cudaMallocAsync(&g.diag, sizeof(double) * (n + kNodePad), st));
+    BCHECK(cudaMallocAsync(&g.rhs, sizeof(double) * (n + kNodePad), st));
+    BCHECK(cudaMallocAsync(&g.prior_num, sizeof(double) * (n + kNodePad), st));
+    BCHECK(cudaMemsetAsync(g.diag + n, 0, sizeof(double) * kNodePad, st));
+    BCHECK(cudaMemsetAsync(g.rhs + n, 0, sizeof(double) * kNodePad, st));
+    BCHECK(cudaMemsetAsync(g.prior_num + n, 0, sizeof(double) * kNodePad, st));
     BCHECK(cudaMemcpyAsync(g.diag, d_diag, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     BCHECK(cudaMemcpyAsync(g.rhs, d_rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-    BCHECK(cudaMallocAsync(&g.row_ptr, sizeof(uint32_t) * (n + 1), st));
-    BCHECK(cudaMallocAsync(&g.rc, sizeof(uint2) * (E > 0 ? E : 1), st));
-    BCHECK(cudaMallocAsync(&g.coeff, sizeof(double) * (E > 0 ? E : 1), st));
+    BCHECK(cudaMallocAsync(&g.row_ptr, sizeof(uint32_t) * (n + 1 + kNodePad), st));
+    BCHECK(cudaMemsetAsync(g.row_ptr + n + 1, 0, sizeof(uint32_t) * kNodePad, st));
+    BCHECK(cudaMallocAsync(&g.rc, sizeof(uint2) * (E + 2), st));
+    BCHECK(cudaMallocAsync(&g.coeff, sizeof(double) * (E + 2), st));
+    BCHECK(cudaMemsetAsync(g.rc + E, 0, sizeof(uint2) * 2, st));
+    BCHECK(cudaMemsetAsync(g.coeff + E, 0, sizeof(double) * 2, st));
 
     int *d_err = nullptr;
     BCHECK(cudaMallocAsync(&d_err, 16, st));
@@ -345,6 +361,10 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
         g.ntiles = h_nt;
         BCHECK(cudaMallocAsync(&g.tile_start, sizeof(uint32_t) * (h_nt + 1), st));
         tile_scatter_kernel<<<grid_for(n), 256, 0, st>>>(n, flag, idx, g.tile_start, g.ntiles);
+        BCHECK(cudaGetLastError());
+        BCHECK(cudaMallocAsync(&g.tile_info, sizeof(uint4) * (h_nt + 1), st));
+        tile_info_kernel<<<grid_for(g.ntiles), 256, 0, st>>>(g.ntiles, g.tile_start, g.row_ptr,
+                                                            g.tile_info);
         BCHECK(cudaGetLastError());
         cudaFreeAsync(idx, st);
     }

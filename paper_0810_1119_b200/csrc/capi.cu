@@ -84,8 +84,9 @@ int ensure_workspace(gabp_graph *G, int64_t max_iter) {
     if (!G->msg[0]) {
         for (int b = 0; b < 2; ++b) CK(cudaMalloc(&G->msg[b], sizeof(double2) * E));
         for (int b = 0; b < 3; ++b) {
-            CK(cudaMalloc(&G->x[b], sizeof(double) * g.n));
-            CK(cudaMalloc(&G->p[b], sizeof(double) * g.n));
+            CK(cudaMalloc(&G->x[b], sizeof(double) * (g.n + gabp::kNodePad)));
+            CK(cudaMalloc(&G->p[b], sizeof(double) * (g.n + gabp::kNodePad)));
+            CK(cudaMemset(G->x[b], 0, sizeof(double) * (g.n + gabp::kNodePad)));
         }
         CK(cudaMalloc(&G->rsq_part, sizeof(double) * (g.ntiles > 0 ? g.ntiles : 1)));
         CK(cudaMalloc(&G->ctrl, sizeof(Ctrl)));
@@ -114,6 +115,7 @@ SweepArgs make_args(gabp_graph *G) {
     a.ntiles = g.ntiles;
     a.row_ptr = g.row_ptr;
     a.tile_start = g.tile_start;
+    a.tile_info = g.tile_info;
     a.rc = g.rc;
     a.coeff = g.coeff;
     a.diag = g.diag;
@@ -611,7 +613,7 @@ int gabp_sweep(const gabp_graph_t *Gc, gabp_state_t *S, int32_t schedule, double
         double v;
         unsigned long long bits = h.change_bits[slot];
         memcpy(&v, &bits, sizeof(v));
-        *max_change = h.nan_change[slot] ? NAN : v;
+        *max_change = v;
     }
     S->cur ^= 1;
     S->iteration += 1;
@@ -767,6 +769,11 @@ int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int64_t sweeps, double 
                     (long long)G->h_ctrl->iterations);
     *ms_per_sweep = ms / (double)sweeps;
     return GABP_OK;
+}
+
+// Debug hook (GABP_TIMELINE builds): clock64 timeline of CTA 0.
+int gabp_debug_timeline(long long *out, int32_t n) {
+    return gabp::read_timeline(out, n) == 0 ? GABP_OK : fail(GABP_EINVAL, "not a timeline build");
 }
 
 }  // extern "C"

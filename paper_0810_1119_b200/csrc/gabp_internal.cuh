@@ -20,10 +20,26 @@
 
 namespace gabp {
 
-constexpr int kThreads = 256;   // threads per sweep block
-constexpr int kTileRows = 256;  // max rows per tile (one thread per row in row phases)
-constexpr int kChunk = 1920;    // edges a tile may stage in shared memory (fast path)
-constexpr int kBucket = 1024;   // tile boundaries every kBucket edge ids (see build.cu)
+#ifndef GABP_EPT
+#define GABP_EPT 2
+#endif
+#ifndef GABP_CTAS_PER_SM
+#define GABP_CTAS_PER_SM 4
+#endif
+#ifndef GABP_THREADS
+#define GABP_THREADS 128
+#endif
+constexpr int kThreads = GABP_THREADS;  // threads per sweep CTA
+constexpr int kTileRows = kThreads;     // max rows per tile (one thread per row)
+constexpr int kEPT = GABP_EPT;  // staged edges per thread per tile
+constexpr int kChunk = kThreads * kEPT;  // edges a tile may stage (fast path)
+constexpr int kBucket = kChunk * 3 / 4;  // tile boundaries every kBucket edge ids (build.cu)
+constexpr int kCtasPerSm = GABP_CTAS_PER_SM;
+#ifndef GABP_STAGES
+#define GABP_STAGES 3
+#endif
+constexpr int kStages = GABP_STAGES;    // contiguous-stream stage ring depth
+constexpr int kNodePad = 4;     // node arrays are padded so 16-byte staging may overrun
 constexpr int kStatSlots = 4;   // ring of per-sweep statistic slots
 constexpr unsigned long long kNoIndex = ~0ull;  // "no singular edge/node" sentinel
 
@@ -49,9 +65,7 @@ struct Ctrl {
     int64_t n;
     // per-sweep statistics, slot = sweep % kStatSlots
     unsigned long long change_bits[kStatSlots];   // max |dP|,|dmu| (non-negative -> bit order)
-    unsigned long long biggest_bits[kStatSlots];  // max |P|,|mu| of S_t
-    int32_t nan_change[kStatSlots];
-    int32_t msg_nonfinite[kStatSlots];
+    int32_t msg_nonfinite[kStatSlots];            // some |message| > blowup or not finite
     int32_t means_nonfinite[kStatSlots];
     unsigned long long agg_singular[kStatSlots];   // broadcast: first node with P_i == 0
     unsigned long long singular_min[kStatSlots];   // first edge with P_excl == 0
@@ -72,6 +86,7 @@ struct SweepArgs {
     int64_t ntiles;
     const uint32_t *row_ptr;
     const uint32_t *tile_start;
+    const uint4 *tile_info;
     const uint2 *rc;
     const double *coeff;
     const double *diag;
@@ -80,7 +95,7 @@ struct SweepArgs {
     double2 *msg[2];
     double *x[3];
     double *p[3];
-    double *rsq_part;   // [ntiles]
+    double *rsq_part;   // [>= persistent grid] per-CTA residual partials
     Ctrl *ctrl;
     double *change_hist;
     double *res_hist;
@@ -91,6 +106,7 @@ struct SweepArgs {
 
 // kernels (sweep.cu); prepare_sweep_kernels() must run once per device before launches
 cudaError_t prepare_sweep_kernels();
+int read_timeline(long long *out, int n);  // GABP_TIMELINE builds only
 cudaError_t launch_sweep(const SweepArgs &a, int schedule, int mode, cudaStream_t st);
 cudaError_t launch_marginals(int64_t n, const uint32_t *row_ptr, const uint2 *rc,
                              const double *diag, const double *prior_num, const double2 *msg,
@@ -106,7 +122,8 @@ struct DeviceGraph {
     int device = 0;
     uint32_t *row_ptr = nullptr;
     uint32_t *tile_start = nullptr;
-    uint2 *rc = nullptr;
+    uint4 *tile_info = nullptr;   // {r0, r1, e0, e1} per tile
+    uint2 *rc = nullptr;          // E + 2 entries (padding for 16-byte staging)
     double *coeff = nullptr;
     double *diag = nullptr;
     double *prior_num = nullptr;
