@@ -40,12 +40,15 @@ METRIC = "GaBP edge-message updates/s, % of HBM roofline; time to 1e-8 residual"
 UNIT = "edge-updates/s"
 REL_TOL = 1e-8
 
-# algorithmic bytes of one fused broadcast sweep:
-#   per directed edge: rc{rev,col} 8 + coeff 8 + gathered in-message 16 + own old
-#   message 16 + new message 16 + x^{(s-2)}[col] 8                      = 72 B
-#   per node: row_ptr 4 + diag 8 + prior_num 8 + rhs 8 + x own 8 + x write 8 + P write 8
-#                                                                        = 52 B
-BYTES_PER_EDGE = 72
+# algorithmic (compulsory) bytes of one synchronous sweep, every array element moved once
+# (DESIGN.md "Roofline"):
+#   per directed edge: graph record {rev, col, A_ij} 16 + previous message 16 read
+#                      + new message 16 write                            = 48 B
+#   per node: row offset 4 + {A_ii, prior numerator} 16 + b_i 8 + x_i^{(s-2)} 8 read
+#             + x_i^{(s-1)} 8 + P_i 8 write                              = 52 B
+# Re-reads (the twin-message or node-aggregate gather, x_j for the residual) are not
+# algorithmic; they show up in the measured "traffic" (ncu dram bytes) instead.
+BYTES_PER_EDGE = 48
 BYTES_PER_NODE = 52
 
 
@@ -267,8 +270,9 @@ def run_ours(args):
     # roofline of the fused sweep kernel (average launch over back-to-back sweeps)
     sweeps = 50
     ms_sweep = ctypes.c_double()
-    _lib.check(lib.gabp_bench_sweeps(g.handle, _lib.SCHED_IDS[sched], 5, ctypes.byref(ms_sweep)))
-    _lib.check(lib.gabp_bench_sweeps(g.handle, _lib.SCHED_IDS[sched], sweeps,
+    _lib.check(lib.gabp_bench_sweeps(g.handle, _lib.SCHED_IDS[sched], 0, 5,
+                                     ctypes.byref(ms_sweep)))
+    _lib.check(lib.gabp_bench_sweeps(g.handle, _lib.SCHED_IDS[sched], 0, sweeps,
                                      ctypes.byref(ms_sweep)))
     algo_bytes = BYTES_PER_EDGE * E + BYTES_PER_NODE * n
     achieved = algo_bytes / (ms_sweep.value / 1e3) / 1e9
@@ -281,15 +285,18 @@ def run_ours(args):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     traffic = None
+    traffic_src = None
     try:
         with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
             tr = json.load(fh)
         key = f"config{args.config}_{sched}"
         if key in tr:
             traffic = tr[key]["dram_bytes_per_launch"]
+            traffic_src = tr[key].get("source")
     except OSError:
         pass
     g_close = g.close
+    g_info_span = float(g.info.twin_span)
 
     # e2e: the drop-in call with pinned host buffers, H2D + build + solve + D2H timed
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, min(args.steps, 20))
@@ -348,7 +355,9 @@ def run_ours(args):
                        "parallelism": "replicas" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "peak_source": peak_src,
+                         "gather_mode": "auto (twin_span %.0f edges)" % g_info_span,
                          "kernel": f"sweep_kernel<{sched}> %.3f ms/launch" % ms_sweep.value,
                          "algorithmic_bytes_per_launch": algo_bytes},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,

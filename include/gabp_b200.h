@@ -39,6 +39,10 @@ extern "C" {
 #define GABP_SCHED_PARALLEL 0  /* solver.py:146 _sweep_parallel (exclusion sums) */
 #define GABP_SCHED_BROADCAST 2 /* solver.py:232 broadcast_sweep (aggregate + subtract) */
 
+#define GABP_GATHER_AUTO 0      /* pick by the twin-message locality of the graph */
+#define GABP_GATHER_MESSAGE 1   /* gather the twin message m_ji itself */
+#define GABP_GATHER_RECOMPUTE 2 /* broadcast only: gather node j's aggregate, recompute m_ji */
+
 typedef struct gabp_graph gabp_graph_t;  /* device-resident GaussianGraph */
 typedef struct gabp_state gabp_state_t;  /* device-resident MessageState  */
 
@@ -51,6 +55,7 @@ typedef struct {
     int32_t is_dense;     /* 1 for graphs made by gabp_graph_create_dense */
     double rhs_norm;      /* ||b||_2 */
     double build_ms;      /* device time of the last build (CUDA events) */
+    double twin_span;     /* mean |rev(e) - e| over edges (twin-gather locality) */
 } gabp_graph_info_t;
 
 /* SolveOptions (solver.py:38-54) + extensions after the first four fields. */
@@ -64,6 +69,8 @@ typedef struct {
     double *h_means_history;  /* optional host [rows x n]: tentative means per sweep
                                  (SolveReport.means_history, solver.py:327-332); NULL = off */
     int64_t means_history_rows;
+    int32_t gather_mode;      /* GABP_GATHER_* (results are bitwise identical in every mode) */
+    int32_t reserved;
 } gabp_options_t;
 
 /* SolveReport (solver.py:77-89) scalar part; histories go to caller arrays. */
@@ -173,7 +180,8 @@ int gabp_residual_norm_per_eq(const gabp_graph_t *g, const double *h_x, double *
 /* Sweep-kernel timing hook for bench.py: runs `sweeps` synchronous sweeps of the
  * solve kernel from the current state and returns the average device time per
  * sweep kernel launch (CUDA events on the graph stream). */
-int gabp_bench_sweeps(gabp_graph_t *g, int32_t schedule, int64_t sweeps, double *ms_per_sweep);
+int gabp_bench_sweeps(gabp_graph_t *g, int32_t schedule, int32_t gather_mode, int64_t sweeps,
+                      double *ms_per_sweep);
 
 #ifdef __cplusplus
 }

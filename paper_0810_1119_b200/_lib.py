@@ -24,6 +24,7 @@ GABP_ESINGULAR = -5
 GABP_EDUP = -6
 
 SCHED_IDS = {"parallel": 0, "broadcast": 2}
+GATHER_IDS = {"auto": 0, "message": 1, "recompute": 2}
 
 # every symbol include/gabp_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED = (
@@ -43,7 +44,8 @@ class GraphInfo(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("num_edges", ctypes.c_int64),
                 ("num_tiles", ctypes.c_int64), ("max_degree", ctypes.c_int64),
                 ("device", ctypes.c_int32), ("is_dense", ctypes.c_int32),
-                ("rhs_norm", ctypes.c_double), ("build_ms", ctypes.c_double)]
+                ("rhs_norm", ctypes.c_double), ("build_ms", ctypes.c_double),
+                ("twin_span", ctypes.c_double)]
 
 
 class Options(ctypes.Structure):
@@ -51,7 +53,8 @@ class Options(ctypes.Structure):
                 ("blowup", ctypes.c_double), ("schedule", ctypes.c_int32),
                 ("sweeps_per_poll", ctypes.c_int32), ("rel_residual_tol", ctypes.c_double),
                 ("means_history", ctypes.POINTER(ctypes.c_double)),
-                ("means_history_rows", ctypes.c_int64)]
+                ("means_history_rows", ctypes.c_int64),
+                ("gather_mode", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class Report(ctypes.Structure):
@@ -120,7 +123,7 @@ def load():
                                              ctypes.POINTER(Options), _vp, _vp, _vp, _vp,
                                              ctypes.POINTER(Report)]),
         "gabp_residual_norm_per_eq": (ctypes.c_int, [_vp, _vp, _dp]),
-        "gabp_bench_sweeps": (ctypes.c_int, [_vp, _i32, _i64, _dp]),
+        "gabp_bench_sweeps": (ctypes.c_int, [_vp, _i32, _i32, _i64, _dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

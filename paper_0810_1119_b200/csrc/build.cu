@@ -81,13 +81,27 @@ __global__ void pos_kernel(int64_t E, const uint32_t *scol, const uint32_t *spl,
 }
 
 __global__ void edge_kernel(int64_t E, const uint32_t *scol, const uint32_t *spl,
-                            const uint32_t *pos, const double *pv, uint2 *rc, double *coeff) {
+                            const uint32_t *pos, const double *pv, EdgeRec *er) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
          e += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t pl = spl[e];
-        rc[e] = make_uint2(pos[pl ^ 1u], scol[e]);
-        coeff[e] = pv[pl >> 1];
+        EdgeRec r;
+        r.rev = pos[pl ^ 1u];
+        r.col = scol[e];
+        r.coeff = pv[pl >> 1];
+        er[e] = r;
     }
+}
+
+__global__ void twin_span_kernel(int64_t E, const EdgeRec *er, double *sum) {
+    double acc = 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = er[e].rev;
+        acc += (double)(r > e ? r - e : e - r);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(sum, acc);  // heuristic only: order irrelevant
 }
 
 __global__ void tile_flag_kernel(int64_t n, const uint32_t *row_ptr, uint32_t *flag) {
@@ -118,7 +132,8 @@ __global__ void tile_info_kernel(int64_t ntiles, const uint32_t *tile_start,
 }
 
 __global__ void prior_kernel(int64_t n, const double *diag, const double *rhs,
-                             double *prior_num, int *err, unsigned long long *err_at) {
+                             double *prior_num, NodeRec *nd, int *err,
+                             unsigned long long *err_at) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double d = diag[i];
@@ -128,6 +143,10 @@ __global__ void prior_kernel(int64_t n, const double *diag, const double *rhs,
         }
         const double pm = rhs[i] / d;  // prior mean (graph.py:74)
         prior_num[i] = d * pm;         // prior_prec * prior_mean (solver.py:147)
+        NodeRec r;
+        r.diag = d;
+        r.pnum = d * pm;
+        nd[i] = r;
     }
 }
 
@@ -173,8 +192,8 @@ void free_graph(DeviceGraph &g) {
     cudaFree(g.row_ptr);
     cudaFree(g.tile_start);
     cudaFree(g.tile_info);
-    cudaFree(g.rc);
-    cudaFree(g.coeff);
+    cudaFree(g.er);
+    cudaFree(g.nd);
     cudaFree(g.diag);
     cudaFree(g.prior_num);
     cudaFree(g.rhs);
@@ -188,7 +207,8 @@ int compute_priors(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
     d_at = reinterpret_cast<unsigned long long *>(d_err + 2);
     BCHECK(cudaMemsetAsync(d_err, 0, sizeof(int) * 2, st));
     BCHECK(cudaMemsetAsync(d_at, 0xff, sizeof(unsigned long long), st));
-    prior_kernel<<<grid_for(g.n), 256, 0, st>>>(g.n, g.diag, g.rhs, g.prior_num, d_err, d_at);
+    prior_kernel<<<grid_for(g.n), 256, 0, st>>>(g.n, g.diag, g.rhs, g.prior_num, g.nd, d_err,
+                                                d_at);
     BCHECK(cudaGetLastError());
     const int64_t nparts = (g.n + 4095) / 4096;
     double *part = nullptr;
@@ -246,10 +266,9 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
     BCHECK(cudaMemcpyAsync(g.rhs, d_rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     BCHECK(cudaMallocAsync(&g.row_ptr, sizeof(uint32_t) * (n + 1 + kNodePad), st));
     BCHECK(cudaMemsetAsync(g.row_ptr + n + 1, 0, sizeof(uint32_t) * kNodePad, st));
-    BCHECK(cudaMallocAsync(&g.rc, sizeof(uint2) * (E + 2), st));
-    BCHECK(cudaMallocAsync(&g.coeff, sizeof(double) * (E + 2), st));
-    BCHECK(cudaMemsetAsync(g.rc + E, 0, sizeof(uint2) * 2, st));
-    BCHECK(cudaMemsetAsync(g.coeff + E, 0, sizeof(double) * 2, st));
+    BCHECK(cudaMallocAsync(&g.er, sizeof(EdgeRec) * (E > 0 ? E : 1), st));
+    BCHECK(cudaMallocAsync(&g.nd, sizeof(NodeRec) * (n + kNodePad), st));
+    BCHECK(cudaMemsetAsync(g.nd + n, 0, sizeof(NodeRec) * kNodePad, st));
 
     int *d_err = nullptr;
     BCHECK(cudaMallocAsync(&d_err, 16, st));
@@ -334,11 +353,21 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
         uint32_t *pos = tpl;  // reuse
         pos_kernel<<<grid_for(E), 256, 0, st>>>(E, scol, spl, d_pi, d_pj, pos, d_err, d_at);
         BCHECK(cudaGetLastError());
-        edge_kernel<<<grid_for(E), 256, 0, st>>>(E, scol, spl, pos, d_pv, g.rc, g.coeff);
+        edge_kernel<<<grid_for(E), 256, 0, st>>>(E, scol, spl, pos, d_pv, g.er);
         BCHECK(cudaGetLastError());
         cudaFreeAsync(scol, st);
         cudaFreeAsync(spl, st);
         cudaFreeAsync(tpl, st);
+        double *d_span = nullptr;
+        BCHECK(cudaMallocAsync(&d_span, sizeof(double), st));
+        BCHECK(cudaMemsetAsync(d_span, 0, sizeof(double), st));
+        twin_span_kernel<<<grid_for(E), 256, 0, st>>>(E, g.er, d_span);
+        BCHECK(cudaGetLastError());
+        double h_span = 0.0;
+        BCHECK(cudaMemcpyAsync(&h_span, d_span, sizeof(double), cudaMemcpyDeviceToHost, st));
+        BCHECK(cudaStreamSynchronize(st));
+        cudaFreeAsync(d_span, st);
+        g.twin_span = h_span / (double)E;
     }
     // 6. tiles
     {

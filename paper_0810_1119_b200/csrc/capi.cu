@@ -49,7 +49,8 @@ struct gabp_graph {
     int device = 0;
     int is_dense = 0;
     // solve workspace
-    double2 *msg[2] = {nullptr, nullptr};
+    double2 *msg[3] = {nullptr, nullptr, nullptr};
+    double2 *agg[2] = {nullptr, nullptr};
     double *x[3] = {nullptr, nullptr, nullptr};
     double *p[3] = {nullptr, nullptr, nullptr};
     double *rsq_part = nullptr;
@@ -61,7 +62,7 @@ struct gabp_graph {
     uint64_t ws_gen = 0;
     // cached CUDA graph of a chunk of sweep launches
     cudaGraphExec_t chunk_exec = nullptr;
-    int chunk_len = 0, chunk_sched = -1;
+    int chunk_len = 0, chunk_sched = -1, chunk_gather = -1;
     uint64_t chunk_gen = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     double *xhist = nullptr;  // device means history (only while a solve asks for it)
@@ -82,7 +83,8 @@ int ensure_workspace(gabp_graph *G, int64_t max_iter) {
     const DeviceGraph &g = G->g;
     const int64_t E = g.E > 0 ? g.E : 1;
     if (!G->msg[0]) {
-        for (int b = 0; b < 2; ++b) CK(cudaMalloc(&G->msg[b], sizeof(double2) * E));
+        for (int b = 0; b < 3; ++b) CK(cudaMalloc(&G->msg[b], sizeof(double2) * E));
+        for (int b = 0; b < 2; ++b) CK(cudaMalloc(&G->agg[b], sizeof(double2) * (g.n + 1)));
         for (int b = 0; b < 3; ++b) {
             CK(cudaMalloc(&G->x[b], sizeof(double) * (g.n + gabp::kNodePad)));
             CK(cudaMalloc(&G->p[b], sizeof(double) * (g.n + gabp::kNodePad)));
@@ -116,13 +118,13 @@ SweepArgs make_args(gabp_graph *G) {
     a.row_ptr = g.row_ptr;
     a.tile_start = g.tile_start;
     a.tile_info = g.tile_info;
-    a.rc = g.rc;
-    a.coeff = g.coeff;
+    a.er = g.er;
+    a.nd = g.nd;
     a.diag = g.diag;
     a.prior_num = g.prior_num;
     a.rhs = g.rhs;
-    a.msg[0] = G->msg[0];
-    a.msg[1] = G->msg[1];
+    for (int b = 0; b < 3; ++b) a.msg[b] = G->msg[b];
+    for (int b = 0; b < 2; ++b) a.agg[b] = G->agg[b];
     for (int b = 0; b < 3; ++b) {
         a.x[b] = G->x[b];
         a.p[b] = G->p[b];
@@ -138,7 +140,8 @@ SweepArgs make_args(gabp_graph *G) {
 }
 
 void release_workspace(gabp_graph *G) {
-    for (int b = 0; b < 2; ++b) cudaFree(G->msg[b]);
+    for (int b = 0; b < 3; ++b) cudaFree(G->msg[b]);
+    for (int b = 0; b < 2; ++b) cudaFree(G->agg[b]);
     for (int b = 0; b < 3; ++b) {
         cudaFree(G->x[b]);
         cudaFree(G->p[b]);
@@ -166,6 +169,16 @@ int check_options(const gabp_options_t *opt) {
     return GABP_OK;
 }
 
+// Gather mode of the broadcast solve: recompute the twin message from the node aggregate
+// (L2-resident, contiguous DRAM traffic only) when the twin messages are far away in
+// memory; gather the twin message itself when it is near (structured grids).
+int pick_gather(const gabp_graph *G, const gabp_options_t *opt) {
+    if (opt->schedule != GABP_SCHED_BROADCAST) return gabp::kGatherMessage;
+    if (opt->gather_mode == GABP_GATHER_MESSAGE) return gabp::kGatherMessage;
+    if (opt->gather_mode == GABP_GATHER_RECOMPUTE) return gabp::kGatherRecompute;
+    return G->g.twin_span * 16.0 > 4.0e6 ? gabp::kGatherRecompute : gabp::kGatherMessage;
+}
+
 int auto_chunk(const gabp_graph *G) {
     // aim for ~1.5 ms of sweeps between host polls (sweep ~ 72 B/edge + 52 B/node)
     const double bytes = 72.0 * (double)G->g.E + 52.0 * (double)G->g.n;
@@ -176,9 +189,9 @@ int auto_chunk(const gabp_graph *G) {
     return c;
 }
 
-int get_chunk_exec(gabp_graph *G, int sched, int len) {
+int get_chunk_exec(gabp_graph *G, int sched, int gather, int len) {
     if (G->chunk_exec && G->chunk_len == len && G->chunk_sched == sched &&
-        G->chunk_gen == G->ws_gen)
+        G->chunk_gather == gather && G->chunk_gen == G->ws_gen)
         return GABP_OK;
     if (G->chunk_exec) {
         cudaGraphExecDestroy(G->chunk_exec);
@@ -188,7 +201,7 @@ int get_chunk_exec(gabp_graph *G, int sched, int len) {
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(G->stream, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < len; ++k) {
-        cudaError_t e = gabp::launch_sweep(a, sched, gabp::kModeSolve, G->stream);
+        cudaError_t e = gabp::launch_sweep(a, sched, gabp::kModeSolve, gather, G->stream);
         if (e != cudaSuccess) {
             cudaStreamEndCapture(G->stream, &graph);
             return fail(GABP_ECUDA, "capture: %s", cudaGetErrorString(e));
@@ -200,6 +213,7 @@ int get_chunk_exec(gabp_graph *G, int sched, int len) {
     CK(e);
     G->chunk_len = len;
     G->chunk_sched = sched;
+    G->chunk_gather = gather;
     G->chunk_gen = G->ws_gen;
     return GABP_OK;
 }
@@ -234,8 +248,9 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
     CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(G->msg[0], 0, sizeof(double2) * (g.E > 0 ? g.E : 1), st));  // S_0 = 0
     const int sched = opt->schedule;
+    const int gather = pick_gather(G, opt);
     const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
-    rc = get_chunk_exec(G, sched, C);
+    rc = get_chunk_exec(G, sched, gather, C);
     if (rc) return rc;
     SweepArgs a = make_args(G);
     const int64_t total = opt->max_iter + 2;
@@ -248,7 +263,8 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         if (k == C) {
             CK(cudaGraphLaunch(G->chunk_exec, st));
         } else {
-            for (int64_t q = 0; q < k; ++q) CK(gabp::launch_sweep(a, sched, gabp::kModeSolve, st));
+            for (int64_t q = 0; q < k; ++q)
+                CK(gabp::launch_sweep(a, sched, gabp::kModeSolve, gather, st));
         }
         launched += k;
         const int slot = poll & 1;
@@ -438,6 +454,7 @@ int gabp_graph_info(const gabp_graph_t *G, gabp_graph_info_t *info) {
     info->is_dense = G->is_dense;
     info->rhs_norm = G->g.rhs_norm;
     info->build_ms = G->g.build_ms;
+    info->twin_span = G->g.twin_span;
     return GABP_OK;
 }
 
@@ -453,20 +470,16 @@ int gabp_graph_export(const gabp_graph_t *G, int64_t *h_row_ptr, int64_t *h_col,
         CK(cudaStreamSynchronize(G->stream));
         for (int64_t i = 0; i <= g.n; ++i) h_row_ptr[i] = rp[i];
     }
-    if ((h_col || h_rev) && g.E > 0) {
-        std::vector<uint2> rc(g.E);
-        CK(cudaMemcpyAsync(rc.data(), g.rc, sizeof(uint2) * g.E, cudaMemcpyDeviceToHost,
+    if ((h_col || h_rev || h_coeff) && g.E > 0) {
+        std::vector<gabp::EdgeRec> er(g.E);
+        CK(cudaMemcpyAsync(er.data(), g.er, sizeof(gabp::EdgeRec) * g.E, cudaMemcpyDeviceToHost,
                            G->stream));
         CK(cudaStreamSynchronize(G->stream));
         for (int64_t e = 0; e < g.E; ++e) {
-            if (h_rev) h_rev[e] = rc[e].x;
-            if (h_col) h_col[e] = rc[e].y;
+            if (h_rev) h_rev[e] = er[e].rev;
+            if (h_col) h_col[e] = er[e].col;
+            if (h_coeff) h_coeff[e] = er[e].coeff;
         }
-    }
-    if (h_coeff && g.E > 0) {
-        CK(cudaMemcpyAsync(h_coeff, g.coeff, sizeof(double) * g.E, cudaMemcpyDeviceToHost,
-                           G->stream));
-        CK(cudaStreamSynchronize(G->stream));
     }
     return GABP_OK;
 }
@@ -594,7 +607,8 @@ int gabp_sweep(const gabp_graph_t *Gc, gabp_state_t *S, int32_t schedule, double
     SweepArgs a = make_args(G);
     a.msg[0] = S->buf[S->cur];
     a.msg[1] = S->buf[S->cur ^ 1];
-    if (G->g.E > 0) CK(gabp::launch_sweep(a, schedule, gabp::kModeSingle, G->stream));
+    if (G->g.E > 0)
+        CK(gabp::launch_sweep(a, schedule, gabp::kModeSingle, gabp::kGatherMessage, G->stream));
     CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, G->stream));
     CK(cudaStreamSynchronize(G->stream));
     const Ctrl &h = *G->h_ctrl;
@@ -628,7 +642,7 @@ int gabp_infer_marginals(const gabp_graph_t *G, const gabp_state_t *S, double *h
     const int64_t n = G->g.n;
     double *d = nullptr;
     CK(cudaMallocAsync(&d, sizeof(double) * 2 * n, G->stream));
-    CK(gabp::launch_marginals(n, G->g.row_ptr, G->g.rc, G->g.diag, G->g.prior_num,
+    CK(gabp::launch_marginals(n, G->g.row_ptr, G->g.er, G->g.diag, G->g.prior_num,
                               S->buf[S->cur], d, d + n, G->stream));
     if (h_means)
         CK(cudaMemcpyAsync(h_means, d, sizeof(double) * n, cudaMemcpyDeviceToHost, G->stream));
@@ -724,8 +738,8 @@ int gabp_residual_norm_per_eq(const gabp_graph_t *G, const double *h_x, double *
     double *d = nullptr;
     CK(cudaMallocAsync(&d, sizeof(double) * (n + nparts + 1), G->stream));
     CK(cudaMemcpyAsync(d, h_x, sizeof(double) * n, cudaMemcpyHostToDevice, G->stream));
-    CK(gabp::launch_residual_sq(n, G->g.row_ptr, G->g.rc, G->g.coeff, G->g.diag, G->g.rhs, d,
-                                d + n, nparts, d + n + nparts, G->stream));
+    CK(gabp::launch_residual_sq(n, G->g.row_ptr, G->g.er, G->g.diag, G->g.rhs, d, d + n, nparts,
+                                d + n + nparts, G->stream));
     double ss = 0.0;
     CK(cudaMemcpyAsync(&ss, d + n + nparts, sizeof(double), cudaMemcpyDeviceToHost, G->stream));
     CK(cudaFreeAsync(d, G->stream));
@@ -734,7 +748,8 @@ int gabp_residual_norm_per_eq(const gabp_graph_t *G, const double *h_x, double *
     return GABP_OK;
 }
 
-int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int64_t sweeps, double *ms_per_sweep) {
+int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int32_t gather_mode, int64_t sweeps,
+                      double *ms_per_sweep) {
     if (!G || sweeps < 1 || !ms_per_sweep) return fail(GABP_EINVAL, "bad argument");
     if (schedule != GABP_SCHED_PARALLEL && schedule != GABP_SCHED_BROADCAST)
         return fail(GABP_EINVAL, "bad schedule");
@@ -757,8 +772,13 @@ int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int64_t sweeps, double 
     CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(G->msg[0], 0, sizeof(double2) * (G->g.E > 0 ? G->g.E : 1), st));
     SweepArgs a = make_args(G);
+    gabp_options_t o{};
+    o.schedule = schedule;
+    o.gather_mode = gather_mode;
+    const int gather = pick_gather(G, &o);
     CK(cudaEventRecord(G->ev[2], st));
-    for (int64_t k = 0; k < sweeps; ++k) CK(gabp::launch_sweep(a, schedule, gabp::kModeSolve, st));
+    for (int64_t k = 0; k < sweeps; ++k)
+        CK(gabp::launch_sweep(a, schedule, gabp::kModeSolve, gather, st));
     CK(cudaEventRecord(G->ev[3], st));
     CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -3,14 +3,17 @@
 // HBM layout of a built graph:
 //   row_ptr   u32[n+1]   CSR offsets, edges grouped by source, neighbours ascending
 //                        (= reference edge ids, graph.py:84-91)
-//   rc        u32x2[E]   {rev, col}: twin edge id (graph.py:95-97) and destination
-//   coeff     f64[E]     A_ij of edge e
-//   diag      f64[n]     A_ii = prior precision (graph.py:73)
-//   prior_num f64[n]     A_ii * (b_i / A_ii)   (solver.py:147)
+//   er        EdgeRec[E] {rev, col, coeff}: twin edge id (graph.py:95-97), destination,
+//                        A_ij -- one 16-byte record, one bulk copy per tile
+//   nd        NodeRec[n] {A_ii, prior_num}: prior precision (graph.py:73) and
+//                        A_ii * (b_i / A_ii) (solver.py:147)
+//   diag, prior_num f64[n] the same node values as plain arrays (auxiliary kernels)
 //   rhs       f64[n]
 //   tile_start u32[T+1]  row tiles: <= kTileRows rows, edges bounded by kBucket + deg
-// Message state: msg[2] f64x2[E] = {P, mu} per directed edge (out-slot layout:
-// message i->j lives at edge id of (i->j), i.e. in row i), double-buffered.
+// Message state: msg[3] f64x2[E] = {P, mu} per directed edge (out-slot layout:
+// message i->j lives at edge id of (i->j), i.e. in row i), a ring of three sweeps.
+// agg[2] f64x2[n] = {P_i, P_i * mu~_i}: node aggregates of the previous state, used by
+// the aggregate-recompute gather mode (sweep.cu).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -44,6 +47,17 @@ constexpr int kStatSlots = 4;   // ring of per-sweep statistic slots
 constexpr unsigned long long kNoIndex = ~0ull;  // "no singular edge/node" sentinel
 
 enum Mode { kModeSolve = 0, kModeSingle = 1 };
+
+struct __align__(16) EdgeRec {
+    uint32_t rev;   // id of the twin edge j -> i
+    uint32_t col;   // destination node j
+    double coeff;   // A_ij
+};
+
+struct __align__(16) NodeRec {
+    double diag;    // A_ii
+    double pnum;    // A_ii * (b_i / A_ii)
+};
 
 // Device-resident solve controller.  One kernel launch == one sweep s (1-based).
 // Launch s reads messages S_{s-1}, writes S_s, computes the marginals x^{(s-1)} of the
@@ -87,12 +101,13 @@ struct SweepArgs {
     const uint32_t *row_ptr;
     const uint32_t *tile_start;
     const uint4 *tile_info;
-    const uint2 *rc;
-    const double *coeff;
+    const EdgeRec *er;
+    const NodeRec *nd;
     const double *diag;
     const double *prior_num;
     const double *rhs;
-    double2 *msg[2];
+    double2 *msg[3];
+    double2 *agg[2];
     double *x[3];
     double *p[3];
     double *rsq_part;   // [>= persistent grid] per-CTA residual partials
@@ -107,14 +122,16 @@ struct SweepArgs {
 // kernels (sweep.cu); prepare_sweep_kernels() must run once per device before launches
 cudaError_t prepare_sweep_kernels();
 int read_timeline(long long *out, int n);  // GABP_TIMELINE builds only
-cudaError_t launch_sweep(const SweepArgs &a, int schedule, int mode, cudaStream_t st);
-cudaError_t launch_marginals(int64_t n, const uint32_t *row_ptr, const uint2 *rc,
+// gather: kGatherMessage (twin message msg_old[rev]) or kGatherRecompute (node aggregate of
+// the previous state + recomputation, broadcast schedule in solve mode only)
+enum Gather { kGatherMessage = 0, kGatherRecompute = 1 };
+cudaError_t launch_sweep(const SweepArgs &a, int schedule, int mode, int gather, cudaStream_t st);
+cudaError_t launch_marginals(int64_t n, const uint32_t *row_ptr, const EdgeRec *er,
                              const double *diag, const double *prior_num, const double2 *msg,
                              double *means, double *precs, cudaStream_t st);
-cudaError_t launch_residual_sq(int64_t n, const uint32_t *row_ptr, const uint2 *rc,
-                               const double *coeff, const double *diag, const double *rhs,
-                               const double *x, double *part, int64_t nparts, double *out,
-                               cudaStream_t st);
+cudaError_t launch_residual_sq(int64_t n, const uint32_t *row_ptr, const EdgeRec *er,
+                               const double *diag, const double *rhs, const double *x,
+                               double *part, int64_t nparts, double *out, cudaStream_t st);
 
 // graph build (build.cu)
 struct DeviceGraph {
@@ -123,13 +140,14 @@ struct DeviceGraph {
     uint32_t *row_ptr = nullptr;
     uint32_t *tile_start = nullptr;
     uint4 *tile_info = nullptr;   // {r0, r1, e0, e1} per tile
-    uint2 *rc = nullptr;          // E + 2 entries (padding for 16-byte staging)
-    double *coeff = nullptr;
+    EdgeRec *er = nullptr;
+    NodeRec *nd = nullptr;
     double *diag = nullptr;
     double *prior_num = nullptr;
     double *rhs = nullptr;
     double rhs_norm = 0.0;
     double build_ms = 0.0;
+    double twin_span = 0.0;  // mean |rev(e) - e| in edges: locality of the twin gather
 };
 
 // Builds CSR + twin index + tiles from device-resident inputs.  Returns a GABP_* code

@@ -50,6 +50,7 @@ class SolveOptions:
     sweeps_per_poll: int = 0                # sweeps per CUDA-graph chunk; 0 = auto
     device: int | None = None
     record_means_history: bool | None = None  # None: auto (n * max_iter <= 2^24)
+    gather_mode: str = "auto"               # auto | message | recompute (bitwise-identical)
 
     def __post_init__(self):
         if self.epsilon <= 0.0:
@@ -60,6 +61,8 @@ class SolveOptions:
             raise ValueError("blowup must exceed 1")
         if self.schedule not in SCHEDULES:
             raise ValueError(f"schedule must be one of {SCHEDULES}")
+        if self.gather_mode not in _lib.GATHER_IDS:
+            raise ValueError(f"gather_mode must be one of {tuple(_lib.GATHER_IDS)}")
 
 
 def _gpu_schedule(schedule: str) -> int:
@@ -210,6 +213,7 @@ def _options_struct(options: SolveOptions, n: int, hist: np.ndarray | None) -> _
     o.schedule = _gpu_schedule(options.schedule)
     o.sweeps_per_poll = int(options.sweeps_per_poll)
     o.rel_residual_tol = float(options.rel_residual_tol or 0.0)
+    o.gather_mode = _lib.GATHER_IDS[options.gather_mode]
     if hist is not None:
         o.means_history = hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         o.means_history_rows = hist.shape[0]

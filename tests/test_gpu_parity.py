@@ -312,3 +312,36 @@ def test_config4_poisson3d_small_slab_vs_oracle():
     orc = oracle.solve(og, epsilon=1e-300, max_iter=30, schedule="broadcast")
     assert r.iterations == orc.iterations == 30 and r.diverged and orc.diverged
     np.testing.assert_array_equal(r.means, orc.means)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_gather_modes_bitwise_identical(case):
+    """Broadcast solve with the twin-message gather and with the aggregate recompute
+    (sweep.cu): same iterations, means, precisions and change history as the reference."""
+    rec = gc.load(case)
+    tol = float(rec["rel_residual_tol"]) or None
+    out = {}
+    for mode in ("message", "recompute"):
+        opts = G.SolveOptions(schedule="broadcast", epsilon=float(rec["epsilon"]),
+                              max_iter=int(rec["max_iter"]), rel_residual_tol=tol,
+                              gather_mode=mode)
+        out[mode] = G.solve(gc.system(rec), opts)
+    a, b = out["message"], out["recompute"]
+    assert a.iterations == b.iterations == int(rec["broadcast_iterations"])
+    assert a.converged == b.converged
+    np.testing.assert_array_equal(a.means, b.means)
+    np.testing.assert_array_equal(a.precisions, b.precisions)
+    np.testing.assert_array_equal(np.asarray(a.max_change_history),
+                                  np.asarray(b.max_change_history))
+
+
+@pytest.mark.parametrize("mode", ["message", "recompute"])
+def test_config1_gather_modes(mode):
+    s = G.gen_random_sparse(1 << 18, 16, 3).system
+    opts = G.SolveOptions(schedule="broadcast", epsilon=1e-300, rel_residual_tol=1e-10,
+                          gather_mode=mode)
+    r = G.solve(s, opts)
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    orc = oracle.solve(og, epsilon=1e-300, schedule="broadcast", rel_residual_tol=1e-10)
+    assert r.iterations == orc.iterations
+    np.testing.assert_array_equal(r.means, orc.means)

@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=1)
 ap.add_argument("--schedule", default="broadcast")
 ap.add_argument("--sweeps", type=int, default=4)
+ap.add_argument("--gather", default="auto", choices=["auto", "message", "recompute"])
 ap.add_argument("--solve", action="store_true", help="also run one full solve")
 args = ap.parse_args()
 
@@ -22,11 +23,13 @@ name, fn = problems.CONFIGS[args.config]
 system = fn(0).system
 g = G.build_graph(system, 0)
 ms = ctypes.c_double()
-_lib.check(_lib.load().gabp_bench_sweeps(g.handle, _lib.SCHED_IDS[args.schedule], args.sweeps,
+_lib.check(_lib.load().gabp_bench_sweeps(g.handle, _lib.SCHED_IDS[args.schedule],
+                                          _lib.GATHER_IDS[args.gather], args.sweeps,
                                           ctypes.byref(ms)))
-print(f"{name}: {args.sweeps} sweeps, {ms.value:.3f} ms/sweep (unprofiled number only if "
-      "not under ncu)")
+print(f"{name} [{args.schedule}/{args.gather}, twin_span {g.info.twin_span:.0f}]: "
+      f"{args.sweeps} sweeps, {ms.value:.3f} ms/sweep (unprofiled number only if not under ncu)")
 if args.solve:
     r = G.solve_graph(g, G.SolveOptions(schedule=args.schedule, epsilon=1e-300,
-                                        rel_residual_tol=1e-8, record_means_history=False))
+                                        rel_residual_tol=1e-8, record_means_history=False,
+                                        gather_mode=args.gather))
     print("solve", r.iterations, r.converged, r.device_ms)
