@@ -105,6 +105,13 @@ int gabp_graph_create_device(int64_t n, int64_t npairs, const double *d_diag,
                              const int64_t *d_pair_j, const double *d_pair_v, int32_t device,
                              gabp_graph_t **out);
 
+/* Same as gabp_graph_create, but only rows [row_lo, row_hi) are swept: the graph of one
+ * rank's row block plus its halo rows (paper_0810_1119_b200/dist.py). */
+int gabp_graph_create_ex(int64_t n, int64_t npairs, const double *h_diag, const double *h_rhs,
+                         const int64_t *h_pair_i, const int64_t *h_pair_j,
+                         const double *h_pair_v, int64_t row_lo, int64_t row_hi,
+                         int32_t device, gabp_graph_t **out);
+
 /* Dense variant (linear detection, BASELINE config 3): A given as a row-major n x n
  * symmetric matrix; exact zeros off the diagonal are non-edges (linalg.py:81-82). */
 int gabp_graph_create_dense(int64_t n, const double *h_a, const double *h_rhs, int32_t device,
@@ -176,6 +183,30 @@ int gabp_solve_system(int64_t n, int64_t npairs, const double *h_diag, const dou
 
 /* residual_norm_per_eq(system, x) (linalg.py:285-288): sqrt(sum (Ax-b)^2) / n. */
 int gabp_residual_norm_per_eq(const gabp_graph_t *g, const double *h_x, double *out);
+
+/* ---- multi-rank (row blocks) -------------------------------- */
+
+/* 128-byte ncclUniqueId for gabp_dist_attach (rank 0 creates, the caller broadcasts). */
+int gabp_nccl_unique_id(void *out128);
+
+/* Make a graph built with gabp_graph_create_ex one rank of a multi-rank broadcast solve.
+ * Per peer q: send_counts[q] owned local node ids (concatenated in send_idx) whose
+ * aggregates and marginals the peer needs, recv_counts[q] halo local ids filled from it.
+ * nccl_id == NULL: in-process partitions on one device (gabp_dist_solve_local).
+ * gabp_solve on an attached graph then runs the NCCL loop and returns the owned rows. */
+int gabp_dist_attach(gabp_graph_t *g, const void *nccl_id, int32_t rank, int32_t world,
+                     int64_t n_global, double bnorm_global, int32_t npeers,
+                     const int32_t *peers, const int64_t *send_counts, const int64_t *send_idx,
+                     const int64_t *recv_counts, const int64_t *recv_idx);
+
+/* Runs the multi-rank loop over nparts in-process partitions (rank p = parts[p]). */
+int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_options_t *opt,
+                          double *device_ms);
+
+/* Outputs of the last solve of a partition: owned rows of means/precs, histories. */
+int gabp_dist_results(gabp_graph_t *g, const gabp_options_t *opt, double *h_means,
+                      double *h_precs, double *h_change_hist, double *h_res_hist,
+                      gabp_report_t *rep);
 
 /* Sweep-kernel timing hook for bench.py: runs `sweeps` synchronous sweeps of the
  * solve kernel from the current state and returns the average device time per

@@ -36,7 +36,8 @@ EXPORTED = (
     "gabp_state_read", "gabp_state_write", "gabp_state_counters",
     "gabp_sweep", "gabp_infer_marginals",
     "gabp_solve", "gabp_solve_device", "gabp_solve_system", "gabp_residual_norm_per_eq",
-    "gabp_bench_sweeps",
+    "gabp_bench_sweeps", "gabp_graph_create_ex", "gabp_nccl_unique_id", "gabp_dist_attach",
+    "gabp_dist_solve_local", "gabp_dist_results",
 )
 
 
@@ -124,6 +125,14 @@ def load():
                                              ctypes.POINTER(Report)]),
         "gabp_residual_norm_per_eq": (ctypes.c_int, [_vp, _vp, _dp]),
         "gabp_bench_sweeps": (ctypes.c_int, [_vp, _i32, _i32, _i64, _dp]),
+        "gabp_graph_create_ex": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
+                                                _i32, ctypes.POINTER(_vp)]),
+        "gabp_nccl_unique_id": (ctypes.c_int, [_vp]),
+        "gabp_dist_attach": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i64, ctypes.c_double, _i32,
+                                            _vp, _vp, _vp, _vp, _vp]),
+        "gabp_dist_solve_local": (ctypes.c_int, [_i32, _vp, ctypes.POINTER(Options), _dp]),
+        "gabp_dist_results": (ctypes.c_int, [_vp, ctypes.POINTER(Options), _vp, _vp, _vp, _vp,
+                                             ctypes.POINTER(Report)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

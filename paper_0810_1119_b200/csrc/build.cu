@@ -104,22 +104,25 @@ __global__ void twin_span_kernel(int64_t E, const EdgeRec *er, double *sum) {
     if ((threadIdx.x & 31) == 0) atomicAdd(sum, acc);  // heuristic only: order irrelevant
 }
 
-__global__ void tile_flag_kernel(int64_t n, const uint32_t *row_ptr, uint32_t *flag) {
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
-         r += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t f = (r % kTileRows) == 0;
+// Tiles cover the swept rows [row_lo, row_lo + m): flag[k] for row row_lo + k.
+__global__ void tile_flag_kernel(int64_t row_lo, int64_t m, const uint32_t *row_ptr,
+                                 uint32_t *flag) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = row_lo + k;
+        uint32_t f = (k % kTileRows) == 0;
         if (!f) f = (row_ptr[r] / kBucket) != (row_ptr[r - 1] / kBucket);
-        flag[r] = f;
+        flag[k] = f;
     }
 }
 
-__global__ void tile_scatter_kernel(int64_t n, const uint32_t *flag, const uint32_t *idx,
-                                    uint32_t *tile_start, int64_t ntiles) {
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
-         r += (int64_t)gridDim.x * blockDim.x) {
-        if (flag[r]) tile_start[idx[r]] = (uint32_t)r;
+__global__ void tile_scatter_kernel(int64_t row_lo, int64_t m, const uint32_t *flag,
+                                    const uint32_t *idx, uint32_t *tile_start, int64_t ntiles) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (flag[k]) tile_start[idx[k]] = (uint32_t)(row_lo + k);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) tile_start[ntiles] = (uint32_t)n;
+    if (blockIdx.x == 0 && threadIdx.x == 0) tile_start[ntiles] = (uint32_t)(row_lo + m);
 }
 
 __global__ void tile_info_kernel(int64_t ntiles, const uint32_t *tile_start,
@@ -237,7 +240,15 @@ int compute_priors(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
 
 int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *d_diag,
                        const double *d_rhs, const int64_t *d_pi, const int64_t *d_pj,
-                       const double *d_pv, cudaStream_t st, char *err, size_t errlen) {
+                       const double *d_pv, int64_t row_lo, int64_t row_hi, cudaStream_t st,
+                       char *err, size_t errlen) {
+    if (row_lo < 0 || row_hi > n || row_lo >= row_hi) {
+        row_lo = 0;
+        row_hi = n;
+    }
+    g.row_lo = row_lo;
+    g.row_hi = row_hi;
+    const int64_t m_rows = row_hi - row_lo;
     if (n < 1) {
         snprintf(err, errlen, "diag must be a non-empty vector");
         return GABP_EINVAL;
@@ -373,23 +384,25 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
     {
         uint32_t *flag = deg, *idx = nullptr;  // deg no longer needed
         BCHECK(cudaMallocAsync(&idx, sizeof(uint32_t) * (n + 1), st));
-        tile_flag_kernel<<<grid_for(n), 256, 0, st>>>(n, g.row_ptr, flag);
+        tile_flag_kernel<<<grid_for(m_rows), 256, 0, st>>>(row_lo, m_rows, g.row_ptr, flag);
         BCHECK(cudaGetLastError());
-        BCHECK(cudaMemsetAsync(flag + n, 0, sizeof(uint32_t), st));
+        BCHECK(cudaMemsetAsync(flag + m_rows, 0, sizeof(uint32_t), st));
         size_t b3 = 0;
-        BCHECK(cub::DeviceScan::ExclusiveSum(nullptr, b3, flag, idx, n + 1, st));
+        BCHECK(cub::DeviceScan::ExclusiveSum(nullptr, b3, flag, idx, m_rows + 1, st));
         if (b3 > tmp_cap) {
             cudaFreeAsync(tmp, st);
             tmp_cap = b3;
             BCHECK(cudaMallocAsync(&tmp, tmp_cap, st));
         }
-        BCHECK(cub::DeviceScan::ExclusiveSum(tmp, b3, flag, idx, n + 1, st));
+        BCHECK(cub::DeviceScan::ExclusiveSum(tmp, b3, flag, idx, m_rows + 1, st));
         uint32_t h_nt = 0;
-        BCHECK(cudaMemcpyAsync(&h_nt, idx + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        BCHECK(cudaMemcpyAsync(&h_nt, idx + m_rows, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               st));
         BCHECK(cudaStreamSynchronize(st));
         g.ntiles = h_nt;
         BCHECK(cudaMallocAsync(&g.tile_start, sizeof(uint32_t) * (h_nt + 1), st));
-        tile_scatter_kernel<<<grid_for(n), 256, 0, st>>>(n, flag, idx, g.tile_start, g.ntiles);
+        tile_scatter_kernel<<<grid_for(m_rows), 256, 0, st>>>(row_lo, m_rows, flag, idx,
+                                                              g.tile_start, g.ntiles);
         BCHECK(cudaGetLastError());
         BCHECK(cudaMallocAsync(&g.tile_info, sizeof(uint4) * (h_nt + 1), st));
         tile_info_kernel<<<grid_for(g.ntiles), 256, 0, st>>>(g.ntiles, g.tile_start, g.row_ptr,

@@ -9,6 +9,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is loaded at run time (gabp_dist_attach)
+
 #include <atomic>
 #include <vector>
 
@@ -40,6 +43,36 @@ int fail(int code, const char *fmt, ...) {
 
 }  // namespace
 
+// ---- NCCL, loaded on first use so the library has no link-time NCCL dependency --------
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
+                              ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    const char *(*errorString)(ncclResult_t) = nullptr;
+};
+
+// Multi-rank state of a graph that holds one rank's row block.
+struct DistState {
+    int rank = 0, world = 1;
+    int64_t n_global = 0;
+    double bnorm = 0.0;
+    bool local = false;            // in-process partitions (no NCCL): gabp_dist_solve_local
+    ncclComm_t comm = nullptr;
+    std::vector<int> peers;
+    std::vector<int64_t> scount, rcount, soff, roff;  // nodes per peer, offsets
+    uint32_t *d_sidx = nullptr, *d_ridx = nullptr;
+    double *d_sbuf = nullptr, *d_rbuf = nullptr;       // 3 doubles per node, per-peer blocks
+    double *d_stats = nullptr;                          // [0..4] max, [5] sum
+};
+
 struct gabp_graph {
     // owner handle + one per live gabp_state: destruction order between a graph and
     // its states does not matter (Python GC may finalise either first)
@@ -67,6 +100,7 @@ struct gabp_graph {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     double *xhist = nullptr;  // device means history (only while a solve asks for it)
     int64_t xhist_rows = 0;
+    DistState *dist = nullptr;
 };
 
 struct gabp_state {
@@ -78,6 +112,37 @@ struct gabp_state {
 };
 
 namespace {
+
+NcclApi g_nccl;
+
+int load_nccl() {
+    if (g_nccl.h) return GABP_OK;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return fail(GABP_ECUDA, "cannot load libnccl.so.2: %s", dlerror());
+#define NCCL_SYM(field, name)                                                           \
+    g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name));             \
+    if (!g_nccl.field) return fail(GABP_ECUDA, "libnccl lacks %s", name);
+    NCCL_SYM(getUniqueId, "ncclGetUniqueId");
+    NCCL_SYM(commInitRank, "ncclCommInitRank");
+    NCCL_SYM(commDestroy, "ncclCommDestroy");
+    NCCL_SYM(allReduce, "ncclAllReduce");
+    NCCL_SYM(send, "ncclSend");
+    NCCL_SYM(recv, "ncclRecv");
+    NCCL_SYM(groupStart, "ncclGroupStart");
+    NCCL_SYM(groupEnd, "ncclGroupEnd");
+    NCCL_SYM(errorString, "ncclGetErrorString");
+#undef NCCL_SYM
+    g_nccl.h = h;
+    return GABP_OK;
+}
+
+#define NK(call)                                                                          \
+    do {                                                                                  \
+        ncclResult_t _r = (call);                                                         \
+        if (_r != ncclSuccess)                                                            \
+            return fail(GABP_ECUDA, "%s failed: %s", #call, g_nccl.errorString(_r));      \
+    } while (0)
 
 int ensure_workspace(gabp_graph *G, int64_t max_iter) {
     const DeviceGraph &g = G->g;
@@ -155,6 +220,16 @@ void release_workspace(gabp_graph *G) {
     cudaFree(G->rsq_hist);
     cudaFree(G->xhist);
     if (G->chunk_exec) cudaGraphExecDestroy(G->chunk_exec);
+    if (G->dist) {
+        cudaFree(G->dist->d_sidx);
+        cudaFree(G->dist->d_ridx);
+        cudaFree(G->dist->d_sbuf);
+        cudaFree(G->dist->d_rbuf);
+        cudaFree(G->dist->d_stats);
+        if (G->dist->comm && g_nccl.commDestroy) g_nccl.commDestroy(G->dist->comm);
+        delete G->dist;
+        G->dist = nullptr;
+    }
     for (int k = 0; k < 4; ++k)
         if (G->ev[k]) cudaEventDestroy(G->ev[k]);
 }
@@ -218,8 +293,8 @@ int get_chunk_exec(gabp_graph *G, int sched, int gather, int len) {
     return GABP_OK;
 }
 
-// Runs the device-driven loop; on return G->h_ctrl holds the final controller.
-int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
+// Common setup of a solve: options, workspace, controller, S_0 = 0.
+int solve_setup(gabp_graph *G, const gabp_options_t *opt) {
     int rc = check_options(opt);
     if (rc) return rc;
     CK(cudaSetDevice(G->device));
@@ -240,23 +315,125 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
     c.epsilon = opt->epsilon;
     c.blowup = opt->blowup;
     c.rel_tol = opt->rel_residual_tol;
-    c.bnorm = g.rhs_norm;
+    c.bnorm = G->dist ? G->dist->bnorm : g.rhs_norm;
     c.max_iter = opt->max_iter;
-    c.n = g.n;
+    c.n = G->dist ? G->dist->n_global : g.n;
     *G->h_ctrl = c;
     cudaStream_t st = G->stream;
     CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(G->msg[0], 0, sizeof(double2) * (g.E > 0 ? g.E : 1), st));  // S_0 = 0
+    return GABP_OK;
+}
+
+// Poll bookkeeping shared by the loops: the done flag of chunk k is read after chunk k+1
+// has been enqueued, so the device never idles on the host.
+struct Poller {
+    gabp_graph *G;
+    int poll = 0;
+    bool pending = false;
+    // returns 1 when the previous chunk's flag says done
+    int after_chunk(cudaStream_t st, int *rc) {
+        const int slot = poll & 1;
+        cudaError_t e = cudaMemcpyAsync(&G->h_done[slot], &G->ctrl->done, sizeof(int32_t),
+                                        cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaEventRecord(G->ev[slot], st);
+        int done = 0;
+        if (e == cudaSuccess && pending) {
+            e = cudaEventSynchronize(G->ev[slot ^ 1]);
+            done = G->h_done[slot ^ 1];
+        }
+        pending = true;
+        poll++;
+        if (e != cudaSuccess) *rc = fail(GABP_ECUDA, "poll: %s", cudaGetErrorString(e));
+        return done;
+    }
+};
+
+int finish_loop(gabp_graph *G, double *device_ms) {
+    cudaStream_t st = G->stream;
+    CK(cudaEventRecord(G->ev[3], st));
+    CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, G->ev[2], G->ev[3]));
+    if (device_ms) *device_ms = ms;
+    if (!G->h_ctrl->done)
+        return fail(GABP_ECUDA, "solve loop ended without a decision (internal error)");
+    return GABP_OK;
+}
+
+// One multi-rank launch on this rank, NCCL transport: sweep, all-reduce of the launch's
+// statistics, decision, halo exchange of the node aggregates and marginals.
+int dist_launch_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
+    DistState *D = G->dist;
+    CK(gabp::launch_sweep(a, GABP_SCHED_BROADCAST, gabp::kModeSolve, gabp::kGatherRecompute, st));
+    if (D->world > 1) {
+        NK(g_nccl.allReduce(D->d_stats, D->d_stats, 5, ncclFloat64, ncclMax, D->comm, st));
+        NK(g_nccl.allReduce(D->d_stats + 5, D->d_stats + 5, 1, ncclFloat64, ncclSum, D->comm,
+                            st));
+    }
+    CK(gabp::launch_finish(a, st));
+    if (D->peers.empty()) return GABP_OK;
+    for (size_t q = 0; q < D->peers.size(); ++q)
+        CK(gabp::launch_halo_pack(a, D->d_sidx + D->soff[q], D->scount[q],
+                                  D->d_sbuf + 3 * D->soff[q], st));
+    NK(g_nccl.groupStart());
+    for (size_t q = 0; q < D->peers.size(); ++q) {
+        if (D->scount[q])
+            NK(g_nccl.send(D->d_sbuf + 3 * D->soff[q], 3 * D->scount[q], ncclFloat64,
+                           D->peers[q], D->comm, st));
+        if (D->rcount[q])
+            NK(g_nccl.recv(D->d_rbuf + 3 * D->roff[q], 3 * D->rcount[q], ncclFloat64,
+                           D->peers[q], D->comm, st));
+    }
+    NK(g_nccl.groupEnd());
+    for (size_t q = 0; q < D->peers.size(); ++q)
+        CK(gabp::launch_halo_unpack(a, D->d_ridx + D->roff[q], D->rcount[q],
+                                    D->d_rbuf + 3 * D->roff[q], st));
+    return GABP_OK;
+}
+
+SweepArgs make_dist_args(gabp_graph *G) {
+    SweepArgs a = make_args(G);
+    a.dist = 1;
+    a.dstats = G->dist->d_stats;
+    return a;
+}
+
+// Runs the device-driven loop; on return G->h_ctrl holds the final controller.
+int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
+    int rc = solve_setup(G, opt);
+    if (rc) return rc;
+    cudaStream_t st = G->stream;
+    const int64_t total = opt->max_iter + 2;
+    int64_t launched = 0;
+    Poller P{G};
+    if (G->dist) {
+        if (G->dist->local)
+            return fail(GABP_EINVAL, "in-process partition: use gabp_dist_solve_local");
+        if (opt->schedule != GABP_SCHED_BROADCAST)
+            return fail(GABP_EINVAL, "the multi-rank solve runs the broadcast schedule");
+        SweepArgs a = make_dist_args(G);
+        const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
+        CK(cudaEventRecord(G->ev[2], st));
+        while (launched < total) {
+            const int64_t k = total - launched < C ? total - launched : C;
+            for (int64_t q = 0; q < k; ++q) {
+                rc = dist_launch_nccl(G, a, st);
+                if (rc) return rc;
+            }
+            launched += k;
+            if (P.after_chunk(st, &rc)) break;
+            if (rc) return rc;
+        }
+        return finish_loop(G, device_ms);
+    }
     const int sched = opt->schedule;
     const int gather = pick_gather(G, opt);
     const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
     rc = get_chunk_exec(G, sched, gather, C);
     if (rc) return rc;
     SweepArgs a = make_args(G);
-    const int64_t total = opt->max_iter + 2;
-    int64_t launched = 0;
-    int poll = 0;
-    bool pending = false;
     CK(cudaEventRecord(G->ev[2], st));
     while (launched < total) {
         const int64_t k = total - launched < C ? total - launched : C;
@@ -267,27 +444,10 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
                 CK(gabp::launch_sweep(a, sched, gabp::kModeSolve, gather, st));
         }
         launched += k;
-        const int slot = poll & 1;
-        CK(cudaMemcpyAsync(&G->h_done[slot], &G->ctrl->done, sizeof(int32_t),
-                           cudaMemcpyDeviceToHost, st));
-        CK(cudaEventRecord(G->ev[slot], st));
-        if (pending) {
-            const int prev = slot ^ 1;
-            CK(cudaEventSynchronize(G->ev[prev]));
-            if (G->h_done[prev]) break;
-        }
-        pending = true;
-        poll++;
+        if (P.after_chunk(st, &rc)) break;
+        if (rc) return rc;
     }
-    CK(cudaEventRecord(G->ev[3], st));
-    CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, G->ev[2], G->ev[3]));
-    if (device_ms) *device_ms = ms;
-    if (!G->h_ctrl->done)
-        return fail(GABP_ECUDA, "solve loop ended without a decision (internal error)");
-    return GABP_OK;
+    return finish_loop(G, device_ms);
 }
 
 void fill_report(gabp_graph *G, const gabp_options_t *opt, double ms, double rsq_last,
@@ -340,17 +500,17 @@ int gabp_device_count(int32_t *count) {
     return GABP_OK;
 }
 
-int gabp_graph_create_device(int64_t n, int64_t npairs, const double *d_diag,
-                             const double *d_rhs, const int64_t *d_pair_i,
-                             const int64_t *d_pair_j, const double *d_pair_v, int32_t device,
-                             gabp_graph_t **out) {
+static int create_device_range(int64_t n, int64_t npairs, const double *d_diag,
+                               const double *d_rhs, const int64_t *d_pair_i,
+                               const int64_t *d_pair_j, const double *d_pair_v, int64_t row_lo,
+                               int64_t row_hi, int32_t device, gabp_graph_t **out) {
     if (!out) return fail(GABP_EINVAL, "out must not be NULL");
     *out = nullptr;
     int rc;
     gabp_graph *G = new_graph(device, &rc);
     if (!G) return rc;
     rc = gabp::build_graph_device(G->g, n, npairs, d_diag, d_rhs, d_pair_i, d_pair_j, d_pair_v,
-                                  G->stream, g_err, sizeof(g_err));
+                                  row_lo, row_hi, G->stream, g_err, sizeof(g_err));
     if (rc != GABP_OK) {
         cudaStreamSynchronize(G->stream);
         gabp::free_graph(G->g);
@@ -362,9 +522,25 @@ int gabp_graph_create_device(int64_t n, int64_t npairs, const double *d_diag,
     return GABP_OK;
 }
 
+int gabp_graph_create_device(int64_t n, int64_t npairs, const double *d_diag,
+                             const double *d_rhs, const int64_t *d_pair_i,
+                             const int64_t *d_pair_j, const double *d_pair_v, int32_t device,
+                             gabp_graph_t **out) {
+    return create_device_range(n, npairs, d_diag, d_rhs, d_pair_i, d_pair_j, d_pair_v, 0, n,
+                               device, out);
+}
+
 int gabp_graph_create(int64_t n, int64_t npairs, const double *h_diag, const double *h_rhs,
                       const int64_t *h_pair_i, const int64_t *h_pair_j, const double *h_pair_v,
                       int32_t device, gabp_graph_t **out) {
+    return gabp_graph_create_ex(n, npairs, h_diag, h_rhs, h_pair_i, h_pair_j, h_pair_v, 0, n,
+                                device, out);
+}
+
+int gabp_graph_create_ex(int64_t n, int64_t npairs, const double *h_diag, const double *h_rhs,
+                         const int64_t *h_pair_i, const int64_t *h_pair_j,
+                         const double *h_pair_v, int64_t row_lo, int64_t row_hi,
+                         int32_t device, gabp_graph_t **out) {
     if (!out) return fail(GABP_EINVAL, "out must not be NULL");
     *out = nullptr;
     if (n < 1) return fail(GABP_EINVAL, "diag must be a non-empty vector");
@@ -394,7 +570,8 @@ int gabp_graph_create(int64_t n, int64_t npairs, const double *h_diag, const dou
     if (e != cudaSuccess) {
         rc = fail(GABP_ECUDA, "H2D copy: %s", cudaGetErrorString(e));
     } else {
-        rc = gabp_graph_create_device(n, npairs, d_diag, d_rhs, d_pi, d_pj, d_pv, device, out);
+        rc = create_device_range(n, npairs, d_diag, d_rhs, d_pi, d_pj, d_pv, row_lo, row_hi,
+                                 device, out);
     }
     cudaFreeAsync(buf, st);
     cudaStreamSynchronize(st);
@@ -656,20 +833,20 @@ int gabp_infer_marginals(const gabp_graph_t *G, const gabp_state_t *S, double *h
 
 // ---- solve --------------------------------------------------------------------------------
 
-int gabp_solve(gabp_graph_t *G, const gabp_options_t *opt, double *h_means, double *h_precs,
-               double *h_change_hist, double *h_res_hist, gabp_report_t *rep) {
-    if (!G) return fail(GABP_EINVAL, "NULL graph");
-    double ms = 0.0;
-    int rc = run_solve(G, opt, &ms);
-    if (rc) return rc;
+// Copies a finished solve's outputs to the host; a rank's graph returns its owned rows.
+static int copy_results(gabp_graph *G, const gabp_options_t *opt, double ms, double *h_means,
+                        double *h_precs, double *h_change_hist, double *h_res_hist,
+                        gabp_report_t *rep) {
     const Ctrl &c = *G->h_ctrl;
     cudaStream_t st = G->stream;
     const int64_t slot = c.final_slot;
+    const int64_t r0 = G->dist ? G->g.row_lo : 0;
+    const int64_t nr = G->dist ? G->g.row_hi - G->g.row_lo : G->g.n;
     if (h_means)
-        CK(cudaMemcpyAsync(h_means, G->x[slot], sizeof(double) * G->g.n, cudaMemcpyDeviceToHost,
+        CK(cudaMemcpyAsync(h_means, G->x[slot] + r0, sizeof(double) * nr, cudaMemcpyDeviceToHost,
                            st));
     if (h_precs)
-        CK(cudaMemcpyAsync(h_precs, G->p[slot], sizeof(double) * G->g.n, cudaMemcpyDeviceToHost,
+        CK(cudaMemcpyAsync(h_precs, G->p[slot] + r0, sizeof(double) * nr, cudaMemcpyDeviceToHost,
                            st));
     if (h_change_hist && c.n_hist > 0)
         CK(cudaMemcpyAsync(h_change_hist, G->change_hist, sizeof(double) * c.n_hist,
@@ -677,7 +854,7 @@ int gabp_solve(gabp_graph_t *G, const gabp_options_t *opt, double *h_means, doub
     if (h_res_hist && c.n_hist > 0)
         CK(cudaMemcpyAsync(h_res_hist, G->res_hist, sizeof(double) * c.n_hist,
                            cudaMemcpyDeviceToHost, st));
-    if (opt->h_means_history && G->xhist && c.n_hist > 0) {
+    if (!G->dist && opt->h_means_history && G->xhist && c.n_hist > 0) {
         const int64_t r = c.n_hist < G->xhist_rows ? c.n_hist : G->xhist_rows;
         CK(cudaMemcpyAsync(opt->h_means_history, G->xhist, sizeof(double) * r * G->g.n,
                            cudaMemcpyDeviceToHost, st));
@@ -688,7 +865,166 @@ int gabp_solve(gabp_graph_t *G, const gabp_options_t *opt, double *h_means, doub
                            cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     fill_report(G, opt, ms, rsq_last, rep);
+    if (rep && G->dist) {
+        rep->messages_sent = c.iterations * G->dist->n_global;
+        rep->final_rel_residual = (c.n_hist >= 1 && G->dist->bnorm > 0.0)
+                                      ? sqrt(rsq_last) / G->dist->bnorm : NAN;
+    }
     return GABP_OK;
+}
+
+int gabp_solve(gabp_graph_t *G, const gabp_options_t *opt, double *h_means, double *h_precs,
+               double *h_change_hist, double *h_res_hist, gabp_report_t *rep) {
+    if (!G) return fail(GABP_EINVAL, "NULL graph");
+    double ms = 0.0;
+    int rc = run_solve(G, opt, &ms);
+    if (rc) return rc;
+    return copy_results(G, opt, ms, h_means, h_precs, h_change_hist, h_res_hist, rep);
+}
+
+// ---- multi-rank -----------------------------------------------------------------------
+
+int gabp_nccl_unique_id(void *out128) {
+    if (!out128) return fail(GABP_EINVAL, "NULL argument");
+    int rc = load_nccl();
+    if (rc) return rc;
+    ncclUniqueId id;
+    NK(g_nccl.getUniqueId(&id));
+    memcpy(out128, &id, sizeof(id));
+    return GABP_OK;
+}
+
+int gabp_dist_attach(gabp_graph_t *G, const void *nccl_id, int32_t rank, int32_t world,
+                     int64_t n_global, double bnorm_global, int32_t npeers,
+                     const int32_t *peers, const int64_t *send_counts, const int64_t *send_idx,
+                     const int64_t *recv_counts, const int64_t *recv_idx) {
+    if (!G || world < 1 || rank < 0 || rank >= world || npeers < 0)
+        return fail(GABP_EINVAL, "bad multi-rank arguments");
+    if (G->dist) return fail(GABP_EINVAL, "graph already attached");
+    CK(cudaSetDevice(G->device));
+    DistState *D = new DistState();
+    D->rank = rank;
+    D->world = world;
+    D->n_global = n_global;
+    D->bnorm = bnorm_global;
+    D->local = (nccl_id == nullptr);
+    // per-peer blocks start at even node offsets: 3*off doubles stays 16-byte aligned for
+    // the {P, P mu~} pairs of the halo buffers
+    int64_t ns = 0, nr = 0;
+    for (int q = 0; q < npeers; ++q) {
+        D->peers.push_back(peers[q]);
+        D->soff.push_back(ns);
+        D->roff.push_back(nr);
+        D->scount.push_back(send_counts[q]);
+        D->rcount.push_back(recv_counts[q]);
+        ns += (send_counts[q] + 1) & ~1ll;
+        nr += (recv_counts[q] + 1) & ~1ll;
+    }
+    G->dist = D;  // released with the graph from here on
+    std::vector<uint32_t> si(ns > 0 ? ns : 1, 0u), ri(nr > 0 ? nr : 1, 0u);
+    int64_t ks = 0, kr = 0;
+    for (int q = 0; q < npeers; ++q) {
+        for (int64_t k = 0; k < send_counts[q]; ++k) si[D->soff[q] + k] = (uint32_t)send_idx[ks++];
+        for (int64_t k = 0; k < recv_counts[q]; ++k) ri[D->roff[q] + k] = (uint32_t)recv_idx[kr++];
+    }
+    CK(cudaMalloc(&D->d_sidx, sizeof(uint32_t) * si.size()));
+    CK(cudaMalloc(&D->d_ridx, sizeof(uint32_t) * ri.size()));
+    CK(cudaMalloc(&D->d_sbuf, sizeof(double) * 3 * si.size()));
+    CK(cudaMalloc(&D->d_rbuf, sizeof(double) * 3 * ri.size()));
+    CK(cudaMalloc(&D->d_stats, sizeof(double) * 8));
+    CK(cudaMemcpy(D->d_sidx, si.data(), sizeof(uint32_t) * si.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(D->d_ridx, ri.data(), sizeof(uint32_t) * ri.size(), cudaMemcpyHostToDevice));
+    if (!D->local && world > 1) {
+        int rc = load_nccl();
+        if (rc) return rc;
+        ncclUniqueId id;
+        memcpy(&id, nccl_id, sizeof(id));
+        NK(g_nccl.commInitRank(&D->comm, world, id, rank));
+    }
+    return GABP_OK;
+}
+
+// One GPU, several row blocks in this process: the multi-rank loop with the cross-rank
+// reduction done on the host and the halo moved with device-to-device copies.  Same
+// kernels as the NCCL path; used to test the partitioned solve on a single device.
+int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_options_t *opt,
+                          double *device_ms) {
+    if (nparts < 1 || !parts) return fail(GABP_EINVAL, "no partitions");
+    for (int p = 0; p < nparts; ++p)
+        if (!parts[p] || !parts[p]->dist || !parts[p]->dist->local || parts[p]->dist->rank != p)
+            return fail(GABP_EINVAL, "partition %d is not attached in local mode as rank %d", p,
+                        p);
+    if (opt && opt->schedule != GABP_SCHED_BROADCAST)
+        return fail(GABP_EINVAL, "the multi-rank solve runs the broadcast schedule");
+    std::vector<SweepArgs> args(nparts);
+    for (int p = 0; p < nparts; ++p) {
+        int rc = solve_setup(parts[p], opt);
+        if (rc) return rc;
+        args[p] = make_dist_args(parts[p]);
+    }
+    gabp_graph *G0 = parts[0];
+    CK(cudaEventRecord(G0->ev[2], G0->stream));
+    const int64_t total = opt->max_iter + 2;
+    for (int64_t s = 0; s < total; ++s) {
+        for (int p = 0; p < nparts; ++p)
+            CK(gabp::launch_sweep(args[p], GABP_SCHED_BROADCAST, gabp::kModeSolve,
+                                  gabp::kGatherRecompute, parts[p]->stream));
+        double red[6] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0};
+        for (int p = 0; p < nparts; ++p) {
+            double st6[6];
+            CK(cudaMemcpyAsync(st6, parts[p]->dist->d_stats, sizeof(st6),
+                               cudaMemcpyDeviceToHost, parts[p]->stream));
+            CK(cudaStreamSynchronize(parts[p]->stream));
+            for (int k = 0; k < 5; ++k) red[k] = fmax(red[k], st6[k]);
+            red[5] += st6[5];
+        }
+        for (int p = 0; p < nparts; ++p) {
+            CK(cudaMemcpyAsync(parts[p]->dist->d_stats, red, sizeof(red), cudaMemcpyHostToDevice,
+                               parts[p]->stream));
+            CK(gabp::launch_finish(args[p], parts[p]->stream));
+            DistState *D = parts[p]->dist;
+            for (size_t q = 0; q < D->peers.size(); ++q)
+                CK(gabp::launch_halo_pack(args[p], D->d_sidx + D->soff[q], D->scount[q],
+                                          D->d_sbuf + 3 * D->soff[q], parts[p]->stream));
+            CK(cudaStreamSynchronize(parts[p]->stream));
+        }
+        for (int p = 0; p < nparts; ++p) {  // move each peer's block for p into p's recv
+            DistState *D = parts[p]->dist;
+            for (size_t q = 0; q < D->peers.size(); ++q) {
+                const int src = D->peers[q];
+                DistState *S = parts[src]->dist;
+                size_t qs = 0;
+                while (qs < S->peers.size() && S->peers[qs] != p) ++qs;
+                if (qs == S->peers.size() || S->scount[qs] != D->rcount[q])
+                    return fail(GABP_EINVAL, "halo lists of ranks %d and %d disagree", p, src);
+                CK(cudaMemcpyAsync(D->d_rbuf + 3 * D->roff[q], S->d_sbuf + 3 * S->soff[qs],
+                                   sizeof(double) * 3 * D->rcount[q], cudaMemcpyDeviceToDevice,
+                                   parts[p]->stream));
+            }
+            for (size_t q = 0; q < D->peers.size(); ++q)
+                CK(gabp::launch_halo_unpack(args[p], D->d_ridx + D->roff[q], D->rcount[q],
+                                            D->d_rbuf + 3 * D->roff[q], parts[p]->stream));
+        }
+        for (int p = 0; p < nparts; ++p) CK(cudaStreamSynchronize(parts[p]->stream));
+        int32_t done = 0;
+        CK(cudaMemcpy(&done, &G0->ctrl->done, sizeof(done), cudaMemcpyDeviceToHost));
+        if (done) break;
+    }
+    double ms = 0.0;
+    for (int p = 0; p < nparts; ++p) {
+        int rc = finish_loop(parts[p], p == 0 ? &ms : nullptr);
+        if (rc && p == 0) return rc;
+    }
+    if (device_ms) *device_ms = ms;
+    return GABP_OK;
+}
+
+// Outputs of the last solve of a partition (owned rows only).
+int gabp_dist_results(gabp_graph_t *G, const gabp_options_t *opt, double *h_means,
+                      double *h_precs, double *h_change_hist, double *h_res_hist,
+                      gabp_report_t *rep) {
+    if (!G || !G->dist) return fail(GABP_EINVAL, "not a partition");
+    return copy_results(G, opt, 0.0, h_means, h_precs, h_change_hist, h_res_hist, rep);
 }
 
 int gabp_solve_device(gabp_graph_t *G, const gabp_options_t *opt, double *d_means,

@@ -1,0 +1,99 @@
+// dist.cu -- device side of the multi-rank solve.
+//
+// Per launch s each rank runs sweep_kernel in dist mode (its last CTA publishes the
+// rank's statistics in dstats instead of deciding), the host reduces dstats across ranks
+// (NCCL all-reduce, or an in-process reduction for the one-GPU partition test), then
+// finish_kernel applies the global statistics and takes the decision for sweep s-2 --
+// identical on every rank -- and the halo kernels move the node aggregates {P_j, P_j mu~_j}
+// and marginals x_j the next launch gathers for remote neighbours.
+#include "gabp_internal.cuh"
+
+namespace gabp {
+namespace {
+
+__global__ void finish_kernel(const SweepArgs a) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    volatile Ctrl *c = a.ctrl;
+    if (c->done) return;
+    const int64_t s = c->next_sweep;
+    const int slot = (int)(s % kStatSlots);
+    const double *d = a.dstats;
+    c->change_bits[slot] = (unsigned long long)__double_as_longlong(d[0]);
+    c->msg_nonfinite[slot] = d[1] > 0.0 ? 1 : 0;
+    c->means_nonfinite[(s - 1) % kStatSlots] = d[2] > 0.0 ? 1 : 0;
+    c->singular_min[slot] = d[3] > -1e299 ? (unsigned long long)(-d[3]) : kNoIndex;
+    c->agg_singular[slot] = d[4] > -1e299 ? (unsigned long long)(-d[4]) : kNoIndex;
+    decide_sweep(c, a, s - 2, d[5]);
+    const int nslot = (int)((s + 1) % kStatSlots);
+    c->change_bits[nslot] = 0ull;
+    c->msg_nonfinite[nslot] = 0;
+    c->means_nonfinite[nslot] = 0;
+    c->agg_singular[nslot] = kNoIndex;
+    c->singular_min[nslot] = kNoIndex;
+    c->next_sweep = s + 1;
+    __threadfence();
+}
+
+// Halo buffers: cnt x {P, P mu~} (2 doubles) followed by cnt x x_j.
+// After finish_kernel of launch s (next_sweep == s+1) the launch-s outputs are
+// agg[(s-1)&1] (aggregates of S_{s-1}) and x[(s-1)%3] (x^{(s-1)}): exactly what launch s+1
+// gathers for remote neighbours.
+__global__ void halo_pack_kernel(const SweepArgs a, const uint32_t *idx, int64_t cnt,
+                                 double *buf) {
+    const int64_t s = ((volatile Ctrl *)a.ctrl)->next_sweep - 1;
+    const double2 *agg = a.agg[(s - 1) & 1];
+    const double *x = a.x[(s - 1) % 3];
+    double2 *bagg = reinterpret_cast<double2 *>(buf);
+    double *bx = buf + 2 * cnt;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = idx[k];
+        bagg[k] = agg[i];
+        bx[k] = x[i];
+    }
+}
+
+__global__ void halo_unpack_kernel(const SweepArgs a, const uint32_t *idx, int64_t cnt,
+                                   const double *buf) {
+    const int64_t s = ((volatile Ctrl *)a.ctrl)->next_sweep - 1;
+    double2 *agg = a.agg[(s - 1) & 1];
+    double *x = a.x[(s - 1) % 3];
+    const double2 *bagg = reinterpret_cast<const double2 *>(buf);
+    const double *bx = buf + 2 * cnt;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = idx[k];
+        agg[i] = bagg[k];
+        x[i] = bx[k];
+    }
+}
+
+inline unsigned blocks_for(int64_t cnt) {
+    int64_t b = (cnt + 255) / 256;
+    if (b < 1) b = 1;
+    if (b > 148 * 8) b = 148 * 8;
+    return (unsigned)b;
+}
+
+}  // namespace
+
+cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st) {
+    finish_kernel<<<1, 32, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_pack(const SweepArgs &a, const uint32_t *idx, int64_t cnt, double *buf,
+                             cudaStream_t st) {
+    if (cnt <= 0) return cudaSuccess;
+    halo_pack_kernel<<<blocks_for(cnt), 256, 0, st>>>(a, idx, cnt, buf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_unpack(const SweepArgs &a, const uint32_t *idx, int64_t cnt,
+                               const double *buf, cudaStream_t st) {
+    if (cnt <= 0) return cudaSuccess;
+    halo_unpack_kernel<<<blocks_for(cnt), 256, 0, st>>>(a, idx, cnt, buf);
+    return cudaGetLastError();
+}
+
+}  // namespace gabp

@@ -117,6 +117,11 @@ struct SweepArgs {
     double *rsq_hist;
     double *xhist;        // optional [xhist_rows x n] tentative means per sweep
     int64_t xhist_rows;
+    // multi-rank mode: the last CTA publishes this rank's statistics of the launch into
+    // dstats ([0..4] reduced with max across ranks, [5] with sum) instead of deciding;
+    // finish_kernel decides once the reduction is done (dist.cu)
+    int dist;
+    double *dstats;
 };
 
 // kernels (sweep.cu); prepare_sweep_kernels() must run once per device before launches
@@ -133,6 +138,54 @@ cudaError_t launch_residual_sq(int64_t n, const uint32_t *row_ptr, const EdgeRec
                                const double *diag, const double *rhs, const double *x,
                                double *part, int64_t nparts, double *out, cudaStream_t st);
 
+// Decision for sweep t (solver.py:321-345), executed by one thread of the last CTA (or of
+// finish_kernel in multi-rank mode).
+__device__ __forceinline__ void decide_sweep(volatile Ctrl *c, SweepArgs const &a, int64_t t, double rsq_t) {
+    if (t < 1 || c->done || t > c->max_iter) return;
+    const int slot = (int)(t % kStatSlots);
+    if (c->singular_min[slot] != kNoIndex || c->agg_singular[slot] != kNoIndex) {
+        // SingularSubgraphError: state not advanced, no history row (solver.py:322-326)
+        c->diverged = 1;
+        c->iterations = t - 1;
+        c->n_hist = t - 1;
+        c->final_slot = (t - 1) % 3;
+        c->done = 1;
+        return;
+    }
+    // max change over the finite differences (a NaN difference, possible only when a
+    // message is non-finite -- the run is then diverged -- is not propagated)
+    const double change =
+        __longlong_as_double((long long)(unsigned long long)c->change_bits[slot]);
+    const bool means_finite = !c->means_nonfinite[slot];
+    const double res = means_finite ? sqrt(rsq_t) / (double)c->n : INFINITY;
+    a.change_hist[t - 1] = change;
+    a.res_hist[t - 1] = res;
+    a.rsq_hist[t - 1] = means_finite ? rsq_t : INFINITY;
+    c->n_hist = t;
+    c->iterations = t;
+    c->final_slot = t % 3;
+    if (c->msg_nonfinite[slot] || !means_finite) {  // not finite or biggest > blowup
+        c->diverged = 1;
+        c->done = 1;
+    } else if (change < c->epsilon) {
+        c->converged = 1;
+        c->done = 1;
+    } else if (c->rel_tol > 0.0 && sqrt(rsq_t) < c->rel_tol * c->bnorm) {
+        c->converged = 1;
+        c->done = 1;
+    } else if (t >= c->max_iter) {
+        c->diverged = 1;  // sweep cap (solver.py:344-345)
+        c->done = 1;
+    }
+}
+
+// multi-rank helpers (dist.cu)
+cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st);
+cudaError_t launch_halo_pack(const SweepArgs &a, const uint32_t *idx, int64_t cnt, double *buf,
+                             cudaStream_t st);
+cudaError_t launch_halo_unpack(const SweepArgs &a, const uint32_t *idx, int64_t cnt,
+                               const double *buf, cudaStream_t st);
+
 // graph build (build.cu)
 struct DeviceGraph {
     int64_t n = 0, E = 0, npairs = 0, ntiles = 0, max_degree = 0;
@@ -148,13 +201,16 @@ struct DeviceGraph {
     double rhs_norm = 0.0;
     double build_ms = 0.0;
     double twin_span = 0.0;  // mean |rev(e) - e| in edges: locality of the twin gather
+    int64_t row_lo = 0, row_hi = 0;  // swept rows
 };
 
 // Builds CSR + twin index + tiles from device-resident inputs.  Returns a GABP_* code
 // and fills *err with a message on failure.
+// Only rows [row_lo, row_hi) are swept (a rank's owned block; the rest are halo rows).
 int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *d_diag,
                        const double *d_rhs, const int64_t *d_pi, const int64_t *d_pj,
-                       const double *d_pv, cudaStream_t st, char *err, size_t errlen);
+                       const double *d_pv, int64_t row_lo, int64_t row_hi, cudaStream_t st,
+                       char *err, size_t errlen);
 void free_graph(DeviceGraph &g);
 int compute_priors(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
 

@@ -345,3 +345,35 @@ def test_config1_gather_modes(mode):
     orc = oracle.solve(og, epsilon=1e-300, schedule="broadcast", rel_residual_tol=1e-10)
     assert r.iterations == orc.iterations
     np.testing.assert_array_equal(r.means, orc.means)
+
+
+# ---------------------------------------------------------------------------------------
+# multi-rank path: row blocks as in-process partitions on one GPU (same kernels, halo
+# lists and decision logic as the NCCL path)
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kind,nparts", [("poisson", 1), ("poisson", 2), ("poisson", 4),
+                                         ("random", 3), ("cdma", 2), ("toy", 2)])
+def test_partitioned_solve_bitwise_equal_single(kind, nparts):
+    from paper_0810_1119_b200 import dist as D
+    if kind == "poisson":
+        s = G.gen_poisson2d(64, 5).system
+    elif kind == "random":
+        s = G.gen_random_sparse(20000, 8, 2).system
+    elif kind == "cdma":
+        s = G.gen_cdma_detection(64, 32, 0.5, 2)[0].system
+    else:
+        s = G.load_instance("cdma4").system
+    opts = G.SolveOptions(schedule="broadcast", epsilon=1e-300, rel_residual_tol=1e-9,
+                          max_iter=3000)
+    if kind == "toy":
+        opts = G.SolveOptions(schedule="broadcast")
+    one = G.solve(s, opts)
+    part = D.solve_partitioned_local(s, nparts, opts)
+    assert part.iterations == one.iterations
+    assert part.converged == one.converged
+    np.testing.assert_array_equal(part.means, one.means)
+    np.testing.assert_array_equal(part.precisions, one.precisions)
+    np.testing.assert_array_equal(np.asarray(part.max_change_history),
+                                  np.asarray(one.max_change_history))
+    _res_close(part.residual_history, one.residual_history)
