@@ -188,49 +188,92 @@ def solve_partitioned_local(system: SymSystem, nparts: int, options=None, device
             lib.gabp_graph_destroy(h)
 
 
+class DistributedGraph:
+    """One rank's row block of a system, built once on this rank's GPU and attached to the
+    multi-rank loop (NCCL halo exchange inside the CUDA library); solve() may be called
+    repeatedly.  Every rank constructs it with the same system."""
+
+    def __init__(self, system: SymSystem, group=None, device: int | None = None):
+        import torch.distributed as dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = _lib.default_device() if device is None else int(device)
+        self.n = system.n
+        bounds = partition_rows(system.n, self.world)
+        self.part = local_part(system, bounds, self.rank)
+        bnorm = float(np.sqrt(np.sum(system.rhs * system.rhs)))
+        lib = _lib.load()
+        nid = None
+        if self.world > 1:
+            raw = (ctypes.c_char * 128)()
+            if self.rank == 0:
+                _lib.check(lib.gabp_nccl_unique_id(raw))
+            obj = [bytes(raw) if self.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            nid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        self._h = _part_graph(self.part, self.device)
+        _attach(self._h, self.part, nid, bnorm)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def solve_local_report(self, options):
+        """Solve; returns (this rank's owned means, precs, Report, change, residual)."""
+        from .solver import _options_struct
+        lib = _lib.load()
+        o = _options_struct(options, self.n, None)
+        if self.world == 1:  # one rank: the local driver (no NCCL needed)
+            arr = (ctypes.c_void_p * 1)(self._h.value)
+            ms = ctypes.c_double()
+            _lib.check(lib.gabp_dist_solve_local(1, arr, ctypes.byref(o), ctypes.byref(ms)))
+        p = self.part
+        m = np.empty(p.hi - p.lo)
+        pr = np.empty(p.hi - p.lo)
+        ch = np.empty(options.max_iter)
+        rh = np.empty(options.max_iter)
+        rep = _lib.Report()
+        if self.world > 1:
+            _lib.check(lib.gabp_solve(self._h, ctypes.byref(o), _lib.ptr(m), _lib.ptr(pr),
+                                      _lib.ptr(ch), _lib.ptr(rh), ctypes.byref(rep)))
+        else:
+            _lib.check(lib.gabp_dist_results(self._h, ctypes.byref(o), _lib.ptr(m),
+                                             _lib.ptr(pr), _lib.ptr(ch), _lib.ptr(rh),
+                                             ctypes.byref(rep)))
+            rep.device_ms = ms.value
+        return m, pr, rep, ch, rh
+
+    def solve(self, options=None):
+        """Full report on every rank (means gathered from all ranks)."""
+        import torch.distributed as dist
+        from .solver import SolveOptions
+        options = options or SolveOptions(schedule="broadcast")
+        m, pr, rep, ch, rh = self.solve_local_report(options)
+        gathered = [None] * self.world
+        dist.all_gather_object(gathered, (self.part.lo, self.part.hi, m, pr), group=self.group)
+        parts = [type("P", (), {"lo": g[0], "hi": g[1]}) for g in gathered]
+        return _report(parts, [(g[2], g[3]) for g in gathered], rep, ch, rh, rep.device_ms)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().gabp_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def solve_distributed(system: SymSystem, options=None, group=None):
     """Multi-GPU broadcast solve over torch.distributed ranks (one GPU per rank, NCCL
     halo exchange inside the CUDA library).  Every rank passes the same system and gets
     the full report (means gathered from all ranks)."""
-    import torch.distributed as dist
-    from .solver import SolveOptions, _options_struct
-    options = options or SolveOptions(schedule="broadcast")
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    device = options.device if options.device is not None else _lib.default_device()
-    bounds = partition_rows(system.n, world)
-    part = local_part(system, bounds, rank)
-    bnorm = float(np.sqrt(np.sum(system.rhs * system.rhs)))
-    lib = _lib.load()
-    nid = (ctypes.c_char * 128)()
-    if world > 1:
-        if rank == 0:
-            _lib.check(lib.gabp_nccl_unique_id(nid))
-        obj = [bytes(nid) if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        nid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
-    h = _part_graph(part, device)
+    dg = DistributedGraph(system, group,
+                          None if options is None else getattr(options, "device", None))
     try:
-        _attach(h, part, nid if world > 1 else None, bnorm)
-        if world == 1:  # single rank: the local driver with one partition
-            arr = (ctypes.c_void_p * 1)(h.value)
-            o = _options_struct(options, system.n, None)
-            ms = ctypes.c_double()
-            _lib.check(lib.gabp_dist_solve_local(1, arr, ctypes.byref(o), ctypes.byref(ms)))
-        o = _options_struct(options, system.n, None)
-        m = np.empty(part.hi - part.lo)
-        pr = np.empty(part.hi - part.lo)
-        ch = np.empty(options.max_iter)
-        rh = np.empty(options.max_iter)
-        rep = _lib.Report()
-        if world > 1:
-            _lib.check(lib.gabp_solve(h, ctypes.byref(o), _lib.ptr(m), _lib.ptr(pr),
-                                      _lib.ptr(ch), _lib.ptr(rh), ctypes.byref(rep)))
-        else:
-            _lib.check(lib.gabp_dist_results(h, ctypes.byref(o), _lib.ptr(m), _lib.ptr(pr),
-                                             _lib.ptr(ch), _lib.ptr(rh), ctypes.byref(rep)))
-        gathered = [None] * world
-        dist.all_gather_object(gathered, (part.lo, part.hi, m, pr), group=group)
-        parts = [type("P", (), {"lo": g[0], "hi": g[1]}) for g in gathered]
-        return _report(parts, [(g[2], g[3]) for g in gathered], rep, ch, rh, rep.device_ms)
+        return dg.solve(options)
     finally:
-        lib.gabp_graph_destroy(h)
+        dg.close()
