@@ -101,6 +101,11 @@ struct gabp_graph {
     double *xhist = nullptr;  // device means history (only while a solve asks for it)
     int64_t xhist_rows = 0;
     DistState *dist = nullptr;
+    // dense variant (gabp_graph_create_dense): A and the padded message matrix ring
+    int64_t K = 0;
+    double *dA = nullptr;
+    double2 *dmsg[3] = {nullptr, nullptr, nullptr};
+    double2 *dnode = nullptr;
 };
 
 struct gabp_state {
@@ -220,6 +225,9 @@ void release_workspace(gabp_graph *G) {
     cudaFree(G->rsq_hist);
     cudaFree(G->xhist);
     if (G->chunk_exec) cudaGraphExecDestroy(G->chunk_exec);
+    cudaFree(G->dA);
+    for (int b = 0; b < 3; ++b) cudaFree(G->dmsg[b]);
+    cudaFree(G->dnode);
     if (G->dist) {
         cudaFree(G->dist->d_sidx);
         cudaFree(G->dist->d_ridx);
@@ -429,6 +437,30 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         return finish_loop(G, device_ms);
     }
     const int sched = opt->schedule;
+    if (G->is_dense && sched == GABP_SCHED_BROADCAST && opt->gather_mode == GABP_GATHER_AUTO) {
+        // dense variant: column walk + edge tiles (dense.cu), same controller protocol
+        const int64_t K = G->K;
+        for (int b = 0; b < 3; ++b)
+            if (!G->dmsg[b]) CK(cudaMalloc(&G->dmsg[b], sizeof(double2) * K * K));
+        if (!G->dnode) CK(cudaMalloc(&G->dnode, sizeof(double2) * K));
+        CK(cudaMemsetAsync(G->dmsg[0], 0, sizeof(double2) * K * K, st));
+        gabp::DenseArgs d{};
+        d.K = K;
+        d.A = G->dA;
+        for (int b = 0; b < 3; ++b) d.msg[b] = G->dmsg[b];
+        d.node = G->dnode;
+        SweepArgs a = make_args(G);
+        const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : 8;
+        CK(cudaEventRecord(G->ev[2], st));
+        while (launched < total) {
+            const int64_t k = total - launched < C ? total - launched : C;
+            for (int64_t q = 0; q < k; ++q) CK(gabp::launch_dense_sweep(a, d, st));
+            launched += k;
+            if (P.after_chunk(st, &rc)) break;
+            if (rc) return rc;
+        }
+        return finish_loop(G, device_ms);
+    }
     const int gather = pick_gather(G, opt);
     const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
     rc = get_chunk_exec(G, sched, gather, C);
@@ -602,8 +634,13 @@ int gabp_graph_create_dense(int64_t n, const double *h_a, const double *h_rhs, i
     }
     int rc = gabp_graph_create(n, (int64_t)pv.size(), diag.data(), h_rhs, pi.data(), pj.data(),
                                pv.data(), device, out);
-    if (rc == GABP_OK) (*out)->is_dense = 1;
-    return rc;
+    if (rc != GABP_OK) return rc;
+    gabp_graph *G = *out;
+    G->is_dense = 1;
+    G->K = n;
+    CK(cudaMalloc(&G->dA, sizeof(double) * n * n));
+    CK(cudaMemcpy(G->dA, h_a, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+    return GABP_OK;
 }
 
 static void graph_release(gabp_graph *G) {

@@ -32,10 +32,13 @@ namespace gabp {
 #ifndef GABP_THREADS
 #define GABP_THREADS 128
 #endif
+#ifndef GABP_WARP
+#define GABP_WARP 0   // 1: warp-independent tiles (sweep_warp_kernel)
+#endif
 constexpr int kThreads = GABP_THREADS;  // threads per sweep CTA
-constexpr int kTileRows = kThreads;     // max rows per tile (one thread per row)
+constexpr int kTileRows = GABP_WARP ? 32 : kThreads;  // max rows per tile (thread per row)
 constexpr int kEPT = GABP_EPT;  // staged edges per thread per tile
-constexpr int kChunk = kThreads * kEPT;  // edges a tile may stage (fast path)
+constexpr int kChunk = kTileRows * kEPT;  // edges a tile may stage (fast path)
 constexpr int kBucket = kChunk * 3 / 4;  // tile boundaries every kBucket edge ids (build.cu)
 constexpr int kCtasPerSm = GABP_CTAS_PER_SM;
 #ifndef GABP_STAGES
@@ -178,6 +181,15 @@ __device__ __forceinline__ void decide_sweep(volatile Ctrl *c, SweepArgs const &
         c->done = 1;
     }
 }
+
+// dense variant (dense.cu): A row-major K x K, messages a padded K x K matrix ring
+struct DenseArgs {
+    int64_t K;
+    const double *A;
+    double2 *msg[3];
+    double2 *node;   // {P_i, P_i mu~_i} of the state read by the launch
+};
+cudaError_t launch_dense_sweep(const SweepArgs &a, const DenseArgs &d, cudaStream_t st);
 
 // multi-rank helpers (dist.cu)
 cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st);

@@ -42,10 +42,19 @@ def gaussian_product(a: ScalarGaussian, b: ScalarGaussian) -> ScalarGaussian:
     return ScalarGaussian(mean=(a.prec * a.mean + b.prec * b.mean) / prec, prec=prec)
 
 
-class GaussianGraph:
-    """Handle to a graph built on the GPU (graph.py:53-120)."""
+DENSE_MIN_FILL = 0.5       # off-diagonal fill above which the dense kernels are used
+DENSE_MIN_N = 256          # ... for systems from this size
+DENSE_MAX_N = 1 << 14      # ... up to this size (3 x n^2 x 16 B of messages)
 
-    def __init__(self, system: SymSystem, device: int | None = None):
+
+class GaussianGraph:
+    """Handle to a graph built on the GPU (graph.py:53-120).
+
+    Systems whose off-diagonal fill exceeds DENSE_MIN_FILL (linear detection, BASELINE
+    config 3) also get the dense representation: the broadcast solve then runs the dense
+    column-walk / edge-tile kernels (csrc/dense.cu), bitwise identical to the sparse path."""
+
+    def __init__(self, system: SymSystem, device: int | None = None, dense: bool | None = None):
         lib = _lib.load()
         zero = np.flatnonzero(system.diag == 0.0)
         if zero.size:
@@ -54,11 +63,20 @@ class GaussianGraph:
         self.system = system
         self.n = system.n
         self.device = _lib.default_device() if device is None else int(device)
+        if dense is None:
+            fill = 2.0 * system.pair_v.size / max(system.n * (system.n - 1), 1)
+            dense = DENSE_MIN_N <= system.n <= DENSE_MAX_N and fill > DENSE_MIN_FILL
         h = ctypes.c_void_p()
-        rc = lib.gabp_graph_create(system.n, system.pair_v.size, _lib.ptr(system.diag),
-                                   _lib.ptr(system.rhs), _lib.ptr(system.pair_i),
-                                   _lib.ptr(system.pair_j), _lib.ptr(system.pair_v),
-                                   self.device, ctypes.byref(h))
+        if dense:
+            a, _ = system.to_dense()
+            a = np.ascontiguousarray(a)
+            rc = lib.gabp_graph_create_dense(system.n, _lib.ptr(a), _lib.ptr(system.rhs),
+                                             self.device, ctypes.byref(h))
+        else:
+            rc = lib.gabp_graph_create(system.n, system.pair_v.size, _lib.ptr(system.diag),
+                                       _lib.ptr(system.rhs), _lib.ptr(system.pair_i),
+                                       _lib.ptr(system.pair_j), _lib.ptr(system.pair_v),
+                                       self.device, ctypes.byref(h))
         if rc == _lib.GABP_EZERODIAG:
             raise ZeroDiagonalError(_lib.last_error())
         if rc in (_lib.GABP_EINVAL, _lib.GABP_EDUP):
@@ -152,6 +170,7 @@ class GaussianGraph:
         return bool(seen.all())
 
 
-def build_graph(system: SymSystem, device: int | None = None) -> GaussianGraph:
+def build_graph(system: SymSystem, device: int | None = None,
+                dense: bool | None = None) -> GaussianGraph:
     """graph.py:161-163: build the graphical model on the GPU."""
-    return GaussianGraph(system, device)
+    return GaussianGraph(system, device, dense)

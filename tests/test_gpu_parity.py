@@ -290,19 +290,41 @@ def test_config2_poisson_4096_sweeps_vs_oracle():
     np.testing.assert_array_equal(means, om)
 
 
-def test_config3_cdma_full_detection():
-    """K = 4096 users, N = 8192 chips: GaBP (broadcast) on all K^2 edges vs the
-    direct solution; decisions must match the decorrelator's."""
-    inst, s_true = G.gen_cdma_detection(8192, 4096, 0.5, 0)
-    r = G.solve(inst.system, G.SolveOptions(schedule="broadcast", epsilon=1e-300,
-                                            rel_residual_tol=1e-8, max_iter=2000))
-    a, b = inst.system.to_dense()
-    x = np.linalg.solve(a, b)
-    if r.converged:
-        np.testing.assert_allclose(r.means, x, rtol=0, atol=1e-6 * np.abs(x).max())
-        assert np.array_equal(np.sign(r.means), np.sign(x))
-    else:
-        assert r.diverged
+def test_config3_cdma_full_dense_vs_oracle():
+    """K = 4096 users, N = 8192 chips, all K^2 edges, dense kernels: GaBP diverges on this
+    instance (K/N = 0.5, sigma^2 = 0.5 is not walk-summable); the run must reproduce the
+    oracle's trajectory bitwise -- same sweep of divergence, same last means."""
+    inst, _ = G.gen_cdma_detection(8192, 4096, 0.5, 0)
+    s = inst.system
+    opts = G.SolveOptions(schedule="broadcast", epsilon=1e-300, rel_residual_tol=1e-8,
+                          max_iter=2000)
+    g = G.build_graph(s)
+    assert g.info.is_dense
+    r = G.solve_graph(g, opts)
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    orc = oracle.solve(og, epsilon=1e-300, schedule="broadcast", rel_residual_tol=1e-8,
+                       max_iter=2000)
+    assert r.diverged == orc.diverged and r.converged == orc.converged
+    assert r.iterations == orc.iterations
+    np.testing.assert_array_equal(np.asarray(r.max_change_history), orc.max_change_history)
+    fin = np.isfinite(orc.means)
+    np.testing.assert_array_equal(r.means[fin], orc.means[fin])
+
+
+@pytest.mark.parametrize("K,N,seed", [(32, 64, 2), (200, 400, 5), (300, 1200, 9)])
+def test_dense_kernels_bitwise_equal_sparse(K, N, seed):
+    inst, _ = G.gen_cdma_detection(N, K, 0.5, seed)
+    s = inst.system
+    opts = G.SolveOptions(schedule="broadcast", epsilon=1e-300, rel_residual_tol=1e-10,
+                          max_iter=400)
+    d = G.solve_graph(G.build_graph(s, dense=True), opts)
+    sp = G.solve_graph(G.build_graph(s, dense=False), opts)
+    assert d.iterations == sp.iterations and d.converged == sp.converged
+    np.testing.assert_array_equal(d.means, sp.means)
+    np.testing.assert_array_equal(d.precisions, sp.precisions)
+    np.testing.assert_array_equal(np.asarray(d.max_change_history),
+                                  np.asarray(sp.max_change_history))
+    _res_close(d.residual_history, sp.residual_history)
 
 
 def test_config4_poisson3d_small_slab_vs_oracle():
@@ -353,7 +375,8 @@ def test_config1_gather_modes(mode):
 # ---------------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("kind,nparts", [("poisson", 1), ("poisson", 2), ("poisson", 4),
-                                         ("random", 3), ("cdma", 2), ("toy", 2)])
+                                         ("random", 3), ("cdma", 2), ("toy", 2),
+                                         ("cdma_big", 2)])
 def test_partitioned_solve_bitwise_equal_single(kind, nparts):
     from paper_0810_1119_b200 import dist as D
     if kind == "poisson":
@@ -362,6 +385,8 @@ def test_partitioned_solve_bitwise_equal_single(kind, nparts):
         s = G.gen_random_sparse(20000, 8, 2).system
     elif kind == "cdma":
         s = G.gen_cdma_detection(64, 32, 0.5, 2)[0].system
+    elif kind == "cdma_big":  # rows of degree ~400: unstaged (slow) tiles with cut edges
+        s = G.gen_cdma_detection(1024, 400, 0.5, 2)[0].system
     else:
         s = G.load_instance("cdma4").system
     opts = G.SolveOptions(schedule="broadcast", epsilon=1e-300, rel_residual_tol=1e-9,
