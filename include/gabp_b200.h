@@ -39,9 +39,12 @@ extern "C" {
 #define GABP_SCHED_PARALLEL 0  /* solver.py:146 _sweep_parallel (exclusion sums) */
 #define GABP_SCHED_BROADCAST 2 /* solver.py:232 broadcast_sweep (aggregate + subtract) */
 
-#define GABP_GATHER_AUTO 0      /* pick by the twin-message locality of the graph */
-#define GABP_GATHER_MESSAGE 1   /* gather the twin message m_ji itself */
-#define GABP_GATHER_RECOMPUTE 2 /* broadcast only: gather node j's aggregate, recompute m_ji */
+#define GABP_GATHER_AUTO 0      /* slice layout when built, else by twin-message locality */
+#define GABP_GATHER_MESSAGE 1   /* row tiles, gather the twin message m_ji itself */
+#define GABP_GATHER_RECOMPUTE 2 /* row tiles, broadcast only: gather node j's aggregate and
+                                   recompute m_ji */
+#define GABP_GATHER_SLICE 3     /* slice layout (lane per row), broadcast solve only:
+                                   recompute m_ji as GABP_GATHER_RECOMPUTE */
 
 typedef struct gabp_graph gabp_graph_t;  /* device-resident GaussianGraph */
 typedef struct gabp_state gabp_state_t;  /* device-resident MessageState  */
@@ -56,6 +59,8 @@ typedef struct {
     double rhs_norm;      /* ||b||_2 */
     double build_ms;      /* device time of the last build (CUDA events) */
     double twin_span;     /* mean |rev(e) - e| over edges (twin-gather locality) */
+    int64_t num_slices;   /* 32-row slices of the slice layout (0: not built) */
+    int64_t num_slots;    /* edge slots of the slice layout, padding included */
 } gabp_graph_info_t;
 
 /* SolveOptions (solver.py:38-54) + extensions after the first four fields. */

@@ -24,7 +24,7 @@ GABP_ESINGULAR = -5
 GABP_EDUP = -6
 
 SCHED_IDS = {"parallel": 0, "broadcast": 2}
-GATHER_IDS = {"auto": 0, "message": 1, "recompute": 2}
+GATHER_IDS = {"auto": 0, "message": 1, "recompute": 2, "slice": 3}
 
 # every symbol include/gabp_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED = (
@@ -46,7 +46,8 @@ class GraphInfo(ctypes.Structure):
                 ("num_tiles", ctypes.c_int64), ("max_degree", ctypes.c_int64),
                 ("device", ctypes.c_int32), ("is_dense", ctypes.c_int32),
                 ("rhs_norm", ctypes.c_double), ("build_ms", ctypes.c_double),
-                ("twin_span", ctypes.c_double)]
+                ("twin_span", ctypes.c_double), ("num_slices", ctypes.c_int64),
+                ("num_slots", ctypes.c_int64)]
 
 
 class Options(ctypes.Structure):

@@ -200,6 +200,10 @@ void free_graph(DeviceGraph &g) {
     cudaFree(g.diag);
     cudaFree(g.prior_num);
     cudaFree(g.rhs);
+    cudaFree(g.slice_info);
+    cudaFree(g.lane_info);
+    cudaFree(g.scol);
+    cudaFree(g.scoef);
     g = DeviceGraph{};
 }
 
@@ -427,6 +431,11 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
     if (h_err == kErrDup) {
         snprintf(err, errlen, "duplicate off-diagonal pair (pair index %llu)", h_at);
         return GABP_EDUP;
+    }
+    if (g.max_degree <= kSliceMaxDegree) {
+        const int rc = build_slices(g, st, err, errlen);
+        if (rc == GABP_ENOMEM || rc == GABP_ECUDA) return rc;
+        err[0] = 0;  // too many slots for 32-bit ids: the row tiles remain
     }
     return compute_priors(g, st, err, errlen);
 }

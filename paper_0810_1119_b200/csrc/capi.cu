@@ -149,9 +149,15 @@ int load_nccl() {
             return fail(GABP_ECUDA, "%s failed: %s", #call, g_nccl.errorString(_r));      \
     } while (0)
 
+// message slots of the solve ring: CSR edges, or slice slots (padding included)
+int64_t msg_slots(const DeviceGraph &g) {
+    int64_t m = g.E > g.nslots ? g.E : g.nslots;
+    return m > 0 ? m : 1;
+}
+
 int ensure_workspace(gabp_graph *G, int64_t max_iter) {
     const DeviceGraph &g = G->g;
-    const int64_t E = g.E > 0 ? g.E : 1;
+    const int64_t E = msg_slots(g);
     if (!G->msg[0]) {
         for (int b = 0; b < 3; ++b) CK(cudaMalloc(&G->msg[b], sizeof(double2) * E));
         for (int b = 0; b < 2; ++b) CK(cudaMalloc(&G->agg[b], sizeof(double2) * (g.n + 1)));
@@ -160,7 +166,8 @@ int ensure_workspace(gabp_graph *G, int64_t max_iter) {
             CK(cudaMalloc(&G->p[b], sizeof(double) * (g.n + gabp::kNodePad)));
             CK(cudaMemset(G->x[b], 0, sizeof(double) * (g.n + gabp::kNodePad)));
         }
-        CK(cudaMalloc(&G->rsq_part, sizeof(double) * (g.ntiles > 0 ? g.ntiles : 1)));
+        // one partial per CTA of a persistent launch (either layout)
+        CK(cudaMalloc(&G->rsq_part, sizeof(double) * (g.ntiles > 8192 ? g.ntiles : 8192)));
         CK(cudaMalloc(&G->ctrl, sizeof(Ctrl)));
         CK(cudaMallocHost(&G->h_ctrl, sizeof(Ctrl)));
         CK(cudaMallocHost(&G->h_done, sizeof(int32_t) * 4));
@@ -206,6 +213,11 @@ SweepArgs make_args(gabp_graph *G) {
     a.rsq_hist = G->rsq_hist;
     a.xhist = G->xhist;
     a.xhist_rows = G->xhist_rows;
+    a.nslices = g.nslices;
+    a.slice_info = g.slice_info;
+    a.lane_info = g.lane_info;
+    a.scol = g.scol;
+    a.scoef = g.scoef;
     return a;
 }
 
@@ -249,7 +261,23 @@ int check_options(const gabp_options_t *opt) {
     if (!(opt->blowup > 1.0)) return fail(GABP_EINVAL, "blowup must exceed 1");
     if (opt->schedule != GABP_SCHED_PARALLEL && opt->schedule != GABP_SCHED_BROADCAST)
         return fail(GABP_EINVAL, "schedule must be parallel (0) or broadcast (2)");
+    if (opt->gather_mode < GABP_GATHER_AUTO || opt->gather_mode > GABP_GATHER_SLICE)
+        return fail(GABP_EINVAL, "unknown gather mode %d", opt->gather_mode);
+    if (opt->gather_mode == GABP_GATHER_SLICE && opt->schedule != GABP_SCHED_BROADCAST)
+        return fail(GABP_EINVAL, "the slice layout runs the broadcast schedule");
     return GABP_OK;
+}
+
+int check_slice(const gabp_graph *G, const gabp_options_t *opt) {
+    if (opt->gather_mode == GABP_GATHER_SLICE && G->g.nslices == 0)
+        return fail(GABP_EINVAL, "graph has no slice layout (max degree %lld)",
+                    (long long)G->g.max_degree);
+    return GABP_OK;
+}
+
+// kernel family of a multi-rank launch: slice layout when built, else recomputing tiles
+int dist_gather(const gabp_graph *G) {
+    return G->g.nslices > 0 ? gabp::kGatherSlice : gabp::kGatherRecompute;
 }
 
 // Gather mode of the broadcast solve: recompute the twin message from the node aggregate
@@ -259,6 +287,7 @@ int pick_gather(const gabp_graph *G, const gabp_options_t *opt) {
     if (opt->schedule != GABP_SCHED_BROADCAST) return gabp::kGatherMessage;
     if (opt->gather_mode == GABP_GATHER_MESSAGE) return gabp::kGatherMessage;
     if (opt->gather_mode == GABP_GATHER_RECOMPUTE) return gabp::kGatherRecompute;
+    if (G->g.nslices > 0) return gabp::kGatherSlice;  // AUTO or SLICE
     return G->g.twin_span * 16.0 > 4.0e6 ? gabp::kGatherRecompute : gabp::kGatherMessage;
 }
 
@@ -329,7 +358,7 @@ int solve_setup(gabp_graph *G, const gabp_options_t *opt) {
     *G->h_ctrl = c;
     cudaStream_t st = G->stream;
     CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(G->msg[0], 0, sizeof(double2) * (g.E > 0 ? g.E : 1), st));  // S_0 = 0
+    CK(cudaMemsetAsync(G->msg[0], 0, sizeof(double2) * msg_slots(g), st));  // S_0 = 0
     return GABP_OK;
 }
 
@@ -374,7 +403,7 @@ int finish_loop(gabp_graph *G, double *device_ms) {
 // statistics, decision, halo exchange of the node aggregates and marginals.
 int dist_launch_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
     DistState *D = G->dist;
-    CK(gabp::launch_sweep(a, GABP_SCHED_BROADCAST, gabp::kModeSolve, gabp::kGatherRecompute, st));
+    CK(gabp::launch_sweep(a, GABP_SCHED_BROADCAST, gabp::kModeSolve, dist_gather(G), st));
     if (D->world > 1) {
         NK(g_nccl.allReduce(D->d_stats, D->d_stats, 5, ncclFloat64, ncclMax, D->comm, st));
         NK(g_nccl.allReduce(D->d_stats + 5, D->d_stats + 5, 1, ncclFloat64, ncclSum, D->comm,
@@ -461,6 +490,8 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         }
         return finish_loop(G, device_ms);
     }
+    rc = check_slice(G, opt);
+    if (rc) return rc;
     const int gather = pick_gather(G, opt);
     const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
     rc = get_chunk_exec(G, sched, gather, C);
@@ -503,6 +534,7 @@ gabp_graph *new_graph(int device, int *rc) {
     G->device = device;
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = gabp::prepare_sweep_kernels();
+    if (e == cudaSuccess) e = gabp::prepare_slice_kernels();
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         *rc = fail(GABP_ECUDA, "device %d: %s", device, cudaGetErrorString(e));
@@ -669,6 +701,8 @@ int gabp_graph_info(const gabp_graph_t *G, gabp_graph_info_t *info) {
     info->rhs_norm = G->g.rhs_norm;
     info->build_ms = G->g.build_ms;
     info->twin_span = G->g.twin_span;
+    info->num_slices = G->g.nslices;
+    info->num_slots = G->g.nslots;
     return GABP_OK;
 }
 
@@ -1005,7 +1039,7 @@ int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_optio
     for (int64_t s = 0; s < total; ++s) {
         for (int p = 0; p < nparts; ++p)
             CK(gabp::launch_sweep(args[p], GABP_SCHED_BROADCAST, gabp::kModeSolve,
-                                  gabp::kGatherRecompute, parts[p]->stream));
+                                  dist_gather(parts[p]), parts[p]->stream));
         double red[6] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0};
         for (int p = 0; p < nparts; ++p) {
             double st6[6];
@@ -1143,11 +1177,17 @@ int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int32_t gather_mode, in
     rc = ensure_workspace(G, sweeps + 2);
     if (rc) return rc;
     CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(G->msg[0], 0, sizeof(double2) * (G->g.E > 0 ? G->g.E : 1), st));
+    CK(cudaMemsetAsync(G->msg[0], 0, sizeof(double2) * msg_slots(G->g), st));
     SweepArgs a = make_args(G);
     gabp_options_t o{};
     o.schedule = schedule;
     o.gather_mode = gather_mode;
+    o.epsilon = 1.0;
+    o.max_iter = 1;
+    o.blowup = 2.0;
+    rc = check_options(&o);
+    if (rc == GABP_OK) rc = check_slice(G, &o);
+    if (rc) return rc;
     const int gather = pick_gather(G, &o);
     CK(cudaEventRecord(G->ev[2], st));
     for (int64_t k = 0; k < sweeps; ++k)

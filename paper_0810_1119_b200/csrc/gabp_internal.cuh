@@ -32,11 +32,8 @@ namespace gabp {
 #ifndef GABP_THREADS
 #define GABP_THREADS 128
 #endif
-#ifndef GABP_WARP
-#define GABP_WARP 0   // 1: warp-independent tiles (sweep_warp_kernel)
-#endif
 constexpr int kThreads = GABP_THREADS;  // threads per sweep CTA
-constexpr int kTileRows = GABP_WARP ? 32 : kThreads;  // max rows per tile (thread per row)
+constexpr int kTileRows = kThreads;  // max rows per tile (thread per row)
 constexpr int kEPT = GABP_EPT;  // staged edges per thread per tile
 constexpr int kChunk = kTileRows * kEPT;  // edges a tile may stage (fast path)
 constexpr int kBucket = kChunk * 3 / 4;  // tile boundaries every kBucket edge ids (build.cu)
@@ -125,6 +122,12 @@ struct SweepArgs {
     // finish_kernel decides once the reduction is done (dist.cu)
     int dist;
     double *dstats;
+    // slice layout (slice.cu): lane-per-row broadcast solve
+    int64_t nslices;
+    const uint2 *slice_info;   // {slot base, width} per slice of 32 rows
+    const uint4 *lane_info;    // {row, first edge id, degree, 0} per lane
+    const uint32_t *scol;      // destination of each slot
+    const double *scoef;       // A_ij of each slot
 };
 
 // kernels (sweep.cu); prepare_sweep_kernels() must run once per device before launches
@@ -132,7 +135,7 @@ cudaError_t prepare_sweep_kernels();
 int read_timeline(long long *out, int n);  // GABP_TIMELINE builds only
 // gather: kGatherMessage (twin message msg_old[rev]) or kGatherRecompute (node aggregate of
 // the previous state + recomputation, broadcast schedule in solve mode only)
-enum Gather { kGatherMessage = 0, kGatherRecompute = 1 };
+enum Gather { kGatherMessage = 0, kGatherRecompute = 1, kGatherSlice = 2 };
 cudaError_t launch_sweep(const SweepArgs &a, int schedule, int mode, int gather, cudaStream_t st);
 cudaError_t launch_marginals(int64_t n, const uint32_t *row_ptr, const EdgeRec *er,
                              const double *diag, const double *prior_num, const double2 *msg,
@@ -214,6 +217,12 @@ struct DeviceGraph {
     double build_ms = 0.0;
     double twin_span = 0.0;  // mean |rev(e) - e| in edges: locality of the twin gather
     int64_t row_lo = 0, row_hi = 0;  // swept rows
+    // slice layout (build_slices, slice.cu); nslices == 0 when not built
+    int64_t nslices = 0, nslots = 0;
+    uint2 *slice_info = nullptr;
+    uint4 *lane_info = nullptr;
+    uint32_t *scol = nullptr;
+    double *scoef = nullptr;
 };
 
 // Builds CSR + twin index + tiles from device-resident inputs.  Returns a GABP_* code
@@ -224,6 +233,11 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
                        const double *d_pv, int64_t row_lo, int64_t row_hi, cudaStream_t st,
                        char *err, size_t errlen);
 void free_graph(DeviceGraph &g);
+// slice layout of the swept rows (slice.cu); GABP_OK or an error (the tile layout stays)
+int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
+cudaError_t prepare_slice_kernels();
+cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st);
+constexpr int64_t kSliceMaxDegree = 4096;  // rows longer than this: tile layout only
 int compute_priors(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
 
 }  // namespace gabp

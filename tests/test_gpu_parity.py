@@ -343,21 +343,22 @@ def test_gather_modes_bitwise_identical(case):
     rec = gc.load(case)
     tol = float(rec["rel_residual_tol"]) or None
     out = {}
-    for mode in ("message", "recompute"):
+    for mode in ("message", "recompute", "slice"):
         opts = G.SolveOptions(schedule="broadcast", epsilon=float(rec["epsilon"]),
                               max_iter=int(rec["max_iter"]), rel_residual_tol=tol,
                               gather_mode=mode)
         out[mode] = G.solve(gc.system(rec), opts)
-    a, b = out["message"], out["recompute"]
-    assert a.iterations == b.iterations == int(rec["broadcast_iterations"])
-    assert a.converged == b.converged
-    np.testing.assert_array_equal(a.means, b.means)
-    np.testing.assert_array_equal(a.precisions, b.precisions)
-    np.testing.assert_array_equal(np.asarray(a.max_change_history),
-                                  np.asarray(b.max_change_history))
+    a = out["message"]
+    for b in (out["recompute"], out["slice"]):
+        assert a.iterations == b.iterations == int(rec["broadcast_iterations"])
+        assert a.converged == b.converged
+        np.testing.assert_array_equal(a.means, b.means)
+        np.testing.assert_array_equal(a.precisions, b.precisions)
+        np.testing.assert_array_equal(np.asarray(a.max_change_history),
+                                      np.asarray(b.max_change_history))
 
 
-@pytest.mark.parametrize("mode", ["message", "recompute"])
+@pytest.mark.parametrize("mode", ["message", "recompute", "slice"])
 def test_config1_gather_modes(mode):
     s = G.gen_random_sparse(1 << 18, 16, 3).system
     opts = G.SolveOptions(schedule="broadcast", epsilon=1e-300, rel_residual_tol=1e-10,
@@ -402,3 +403,75 @@ def test_partitioned_solve_bitwise_equal_single(kind, nparts):
     np.testing.assert_array_equal(np.asarray(part.max_change_history),
                                   np.asarray(one.max_change_history))
     _res_close(part.residual_history, one.residual_history)
+
+
+# ---------------------------------------------------------------------------------------
+# slice layout (csrc/slice.cu): degree-sorted 32-row slices, lane per row
+# ---------------------------------------------------------------------------------------
+
+def _ragged_system(seed=5):
+    """Isolated nodes, a degree-100 hub, a chain and random pairs; n not a multiple of 32."""
+    rng = np.random.default_rng(seed)
+    n = 1000
+    pairs = {}
+    for j in range(1, 101):                       # hub 0
+        pairs[(0, j)] = rng.uniform(-1, 1)
+    for i in range(200, 400):                     # chain
+        pairs[(i, i + 1)] = rng.uniform(-1, 1)
+    for _ in range(1500):                         # random sparse part
+        i, j = sorted(rng.choice(np.arange(400, 980), 2, replace=False))
+        pairs[(int(i), int(j))] = rng.uniform(-1, 1)
+    # rows 980..999 stay isolated
+    pi = np.array([p[0] for p in pairs], dtype=np.int64)
+    pj = np.array([p[1] for p in pairs], dtype=np.int64)
+    pv = np.array(list(pairs.values()))
+    absrow = np.zeros(n)
+    np.add.at(absrow, pi, np.abs(pv))
+    np.add.at(absrow, pj, np.abs(pv))
+    diag = 1.2 * absrow + (absrow == 0)
+    rhs = rng.standard_normal(n)
+    return G.SymSystem.from_pairs(diag, pi, pj, pv, rhs)
+
+
+def test_slice_layout_built():
+    s = G.gen_poisson2d(33, 0).system
+    g = G.build_graph(s)
+    assert g.info.num_slices == (s.n + 31) // 32
+    assert g.info.num_slots >= g.num_edges
+
+
+def test_slice_ragged_vs_tiles_and_oracle():
+    s = _ragged_system()
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    orc = oracle.solve(og, epsilon=1e-12, max_iter=200, schedule="broadcast")
+    for mode in ("slice", "message", "recompute"):
+        r = G.solve(s, G.SolveOptions(schedule="broadcast", epsilon=1e-12, max_iter=200,
+                                      gather_mode=mode))
+        assert r.iterations == orc.iterations, mode
+        assert r.converged == orc.converged
+        np.testing.assert_array_equal(r.means, orc.means)
+        np.testing.assert_array_equal(r.precisions, orc.precisions)
+        np.testing.assert_array_equal(np.asarray(r.max_change_history),
+                                      np.asarray(orc.max_change_history))
+
+
+def test_slice_needs_broadcast_and_layout():
+    s = G.gen_poisson2d(8, 0).system
+    with pytest.raises(ValueError):
+        G.SolveOptions(schedule="parallel", gather_mode="slice")
+    # a hub longer than the slice limit: tiles only, auto still solves
+    n = 5001
+    pi = np.zeros(n - 1, dtype=np.int64)
+    pj = np.arange(1, n, dtype=np.int64)
+    pv = np.full(n - 1, 0.01)
+    hub = G.SymSystem.from_pairs(np.full(n, 100.0), pi, pj, pv, np.ones(n))
+    g = G.build_graph(hub)
+    assert g.info.num_slices == 0
+    with pytest.raises(_lib.GabpError):
+        G.solve_graph(g, G.SolveOptions(schedule="broadcast", gather_mode="slice"))
+    r = G.solve_graph(g, G.SolveOptions(schedule="broadcast", epsilon=1e-12))
+    og = oracle.build_graph(hub.diag, hub.rhs, hub.pair_i, hub.pair_j, hub.pair_v)
+    orc = oracle.solve(og, epsilon=1e-12, schedule="broadcast")
+    assert r.iterations == orc.iterations
+    np.testing.assert_array_equal(r.means, orc.means)
+    del s

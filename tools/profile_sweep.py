@@ -15,7 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=1)
 ap.add_argument("--schedule", default="broadcast")
 ap.add_argument("--sweeps", type=int, default=4)
-ap.add_argument("--gather", default="auto", choices=["auto", "message", "recompute"])
+ap.add_argument("--gather", default="auto", choices=["auto", "message", "recompute", "slice"])
 ap.add_argument("--solve", action="store_true", help="also run one full solve")
 args = ap.parse_args()
 
