@@ -201,7 +201,11 @@ void free_graph(DeviceGraph &g) {
     cudaFree(g.prior_num);
     cudaFree(g.rhs);
     cudaFree(g.slice_info);
-    cudaFree(g.lane_info);
+    cudaFree(g.pos);
+    cudaFree(g.srow);
+    cudaFree(g.sdeg);
+    cudaFree(g.snd);
+    cudaFree(g.srhs);
     cudaFree(g.scol);
     cudaFree(g.scoef);
     g = DeviceGraph{};
@@ -217,6 +221,7 @@ int compute_priors(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
     prior_kernel<<<grid_for(g.n), 256, 0, st>>>(g.n, g.diag, g.rhs, g.prior_num, g.nd, d_err,
                                                 d_at);
     BCHECK(cudaGetLastError());
+    BCHECK(refresh_slice_nodes(g, st));
     const int64_t nparts = (g.n + 4095) / 4096;
     double *part = nullptr;
     BCHECK(cudaMallocAsync(&part, sizeof(double) * nparts, st));

@@ -83,7 +83,7 @@ struct gabp_graph {
     int is_dense = 0;
     // solve workspace
     double2 *msg[3] = {nullptr, nullptr, nullptr};
-    double2 *agg[2] = {nullptr, nullptr};
+    double2 *agg[3] = {nullptr, nullptr, nullptr};
     double *x[3] = {nullptr, nullptr, nullptr};
     double *p[3] = {nullptr, nullptr, nullptr};
     double *rsq_part = nullptr;
@@ -99,6 +99,8 @@ struct gabp_graph {
     uint64_t chunk_gen = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     double *xhist = nullptr;  // device means history (only while a solve asks for it)
+    bool slice_order = false;  // the last solve's x / p ring is in slice position order
+    double *xs = nullptr, *ps = nullptr;  // row-order copies of the returned marginals
     int64_t xhist_rows = 0;
     DistState *dist = nullptr;
     // dense variant (gabp_graph_create_dense): A and the padded message matrix ring
@@ -158,14 +160,18 @@ int64_t msg_slots(const DeviceGraph &g) {
 int ensure_workspace(gabp_graph *G, int64_t max_iter) {
     const DeviceGraph &g = G->g;
     const int64_t E = msg_slots(g);
+    // node arrays: row order (tiles) or position order (slices, padding lanes + halo)
+    const int64_t nn = (g.n > g.npos ? g.n : g.npos) + gabp::kNodePad;
     if (!G->msg[0]) {
         for (int b = 0; b < 3; ++b) CK(cudaMalloc(&G->msg[b], sizeof(double2) * E));
-        for (int b = 0; b < 2; ++b) CK(cudaMalloc(&G->agg[b], sizeof(double2) * (g.n + 1)));
+        for (int b = 0; b < 3; ++b) CK(cudaMalloc(&G->agg[b], sizeof(double2) * nn));
         for (int b = 0; b < 3; ++b) {
-            CK(cudaMalloc(&G->x[b], sizeof(double) * (g.n + gabp::kNodePad)));
-            CK(cudaMalloc(&G->p[b], sizeof(double) * (g.n + gabp::kNodePad)));
-            CK(cudaMemset(G->x[b], 0, sizeof(double) * (g.n + gabp::kNodePad)));
+            CK(cudaMalloc(&G->x[b], sizeof(double) * nn));
+            CK(cudaMalloc(&G->p[b], sizeof(double) * nn));
+            CK(cudaMemset(G->x[b], 0, sizeof(double) * nn));
         }
+        CK(cudaMalloc(&G->xs, sizeof(double) * (g.n + 1)));
+        CK(cudaMalloc(&G->ps, sizeof(double) * (g.n + 1)));
         // one partial per CTA of a persistent launch (either layout)
         CK(cudaMalloc(&G->rsq_part, sizeof(double) * (g.ntiles > 8192 ? g.ntiles : 8192)));
         CK(cudaMalloc(&G->ctrl, sizeof(Ctrl)));
@@ -201,7 +207,7 @@ SweepArgs make_args(gabp_graph *G) {
     a.prior_num = g.prior_num;
     a.rhs = g.rhs;
     for (int b = 0; b < 3; ++b) a.msg[b] = G->msg[b];
-    for (int b = 0; b < 2; ++b) a.agg[b] = G->agg[b];
+    for (int b = 0; b < 3; ++b) a.agg[b] = G->agg[b];
     for (int b = 0; b < 3; ++b) {
         a.x[b] = G->x[b];
         a.p[b] = G->p[b];
@@ -213,9 +219,13 @@ SweepArgs make_args(gabp_graph *G) {
     a.rsq_hist = G->rsq_hist;
     a.xhist = G->xhist;
     a.xhist_rows = G->xhist_rows;
+    a.msg_lag = 0;
     a.nslices = g.nslices;
     a.slice_info = g.slice_info;
-    a.lane_info = g.lane_info;
+    a.sdeg = g.sdeg;
+    a.srow = g.srow;
+    a.snd = g.snd;
+    a.srhs = g.srhs;
     a.scol = g.scol;
     a.scoef = g.scoef;
     return a;
@@ -223,7 +233,9 @@ SweepArgs make_args(gabp_graph *G) {
 
 void release_workspace(gabp_graph *G) {
     for (int b = 0; b < 3; ++b) cudaFree(G->msg[b]);
-    for (int b = 0; b < 2; ++b) cudaFree(G->agg[b]);
+    for (int b = 0; b < 3; ++b) cudaFree(G->agg[b]);
+    cudaFree(G->xs);
+    cudaFree(G->ps);
     for (int b = 0; b < 3; ++b) {
         cudaFree(G->x[b]);
         cudaFree(G->p[b]);
@@ -391,9 +403,11 @@ int finish_loop(gabp_graph *G, double *device_ms) {
     CK(cudaEventRecord(G->ev[3], st));
     CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, G->ev[2], G->ev[3]));
-    if (device_ms) *device_ms = ms;
+    if (device_ms) {  // (partitions other than rank 0 never record the start event)
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, G->ev[2], G->ev[3]));
+        *device_ms = ms;
+    }
     if (!G->h_ctrl->done)
         return fail(GABP_ECUDA, "solve loop ended without a decision (internal error)");
     return GABP_OK;
@@ -434,6 +448,7 @@ SweepArgs make_dist_args(gabp_graph *G) {
     SweepArgs a = make_args(G);
     a.dist = 1;
     a.dstats = G->dist->d_stats;
+    a.msg_lag = dist_gather(G) == gabp::kGatherSlice ? 1 : 0;
     return a;
 }
 
@@ -451,6 +466,7 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         if (opt->schedule != GABP_SCHED_BROADCAST)
             return fail(GABP_EINVAL, "the multi-rank solve runs the broadcast schedule");
         SweepArgs a = make_dist_args(G);
+        G->slice_order = dist_gather(G) == gabp::kGatherSlice;
         const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
         CK(cudaEventRecord(G->ev[2], st));
         while (launched < total) {
@@ -468,6 +484,7 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
     const int sched = opt->schedule;
     if (G->is_dense && sched == GABP_SCHED_BROADCAST && opt->gather_mode == GABP_GATHER_AUTO) {
         // dense variant: column walk + edge tiles (dense.cu), same controller protocol
+        G->slice_order = false;
         const int64_t K = G->K;
         for (int b = 0; b < 3; ++b)
             if (!G->dmsg[b]) CK(cudaMalloc(&G->dmsg[b], sizeof(double2) * K * K));
@@ -493,6 +510,7 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
     rc = check_slice(G, opt);
     if (rc) return rc;
     const int gather = pick_gather(G, opt);
+    G->slice_order = gather == gabp::kGatherSlice;
     const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
     rc = get_chunk_exec(G, sched, gather, C);
     if (rc) return rc;
@@ -904,6 +922,17 @@ int gabp_infer_marginals(const gabp_graph_t *G, const gabp_state_t *S, double *h
 
 // ---- solve --------------------------------------------------------------------------------
 
+// Marginals of the last solve in row order: the slice path keeps them in position order.
+static int rows_order(gabp_graph *G, int64_t r0, int64_t nr, const double **xm,
+                      const double **pm) {
+    if (!G->slice_order) return GABP_OK;
+    CK(gabp::slice_to_rows(G->g, r0, nr, *xm, G->xs, G->stream));
+    CK(gabp::slice_to_rows(G->g, r0, nr, *pm, G->ps, G->stream));
+    *xm = G->xs;
+    *pm = G->ps;
+    return GABP_OK;
+}
+
 // Copies a finished solve's outputs to the host; a rank's graph returns its owned rows.
 static int copy_results(gabp_graph *G, const gabp_options_t *opt, double ms, double *h_means,
                         double *h_precs, double *h_change_hist, double *h_res_hist,
@@ -913,12 +942,13 @@ static int copy_results(gabp_graph *G, const gabp_options_t *opt, double ms, dou
     const int64_t slot = c.final_slot;
     const int64_t r0 = G->dist ? G->g.row_lo : 0;
     const int64_t nr = G->dist ? G->g.row_hi - G->g.row_lo : G->g.n;
+    const double *xm = G->x[slot], *pm = G->p[slot];
+    int rc = rows_order(G, r0, nr, &xm, &pm);
+    if (rc) return rc;
     if (h_means)
-        CK(cudaMemcpyAsync(h_means, G->x[slot] + r0, sizeof(double) * nr, cudaMemcpyDeviceToHost,
-                           st));
+        CK(cudaMemcpyAsync(h_means, xm + r0, sizeof(double) * nr, cudaMemcpyDeviceToHost, st));
     if (h_precs)
-        CK(cudaMemcpyAsync(h_precs, G->p[slot] + r0, sizeof(double) * nr, cudaMemcpyDeviceToHost,
-                           st));
+        CK(cudaMemcpyAsync(h_precs, pm + r0, sizeof(double) * nr, cudaMemcpyDeviceToHost, st));
     if (h_change_hist && c.n_hist > 0)
         CK(cudaMemcpyAsync(h_change_hist, G->change_hist, sizeof(double) * c.n_hist,
                            cudaMemcpyDeviceToHost, st));
@@ -1005,6 +1035,11 @@ int gabp_dist_attach(gabp_graph_t *G, const void *nccl_id, int32_t rank, int32_t
     CK(cudaMalloc(&D->d_stats, sizeof(double) * 8));
     CK(cudaMemcpy(D->d_sidx, si.data(), sizeof(uint32_t) * si.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(D->d_ridx, ri.data(), sizeof(uint32_t) * ri.size(), cudaMemcpyHostToDevice));
+    if (dist_gather(G) == gabp::kGatherSlice) {  // halo lists in position numbering
+        CK(gabp::slice_map_index(G->g, D->d_sidx, ns, G->stream));
+        CK(gabp::slice_map_index(G->g, D->d_ridx, nr, G->stream));
+        CK(cudaStreamSynchronize(G->stream));
+    }
     if (!D->local && world > 1) {
         int rc = load_nccl();
         if (rc) return rc;
@@ -1032,6 +1067,7 @@ int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_optio
         int rc = solve_setup(parts[p], opt);
         if (rc) return rc;
         args[p] = make_dist_args(parts[p]);
+        parts[p]->slice_order = dist_gather(parts[p]) == gabp::kGatherSlice;
     }
     gabp_graph *G0 = parts[0];
     CK(cudaEventRecord(G0->ev[2], G0->stream));
@@ -1107,12 +1143,13 @@ int gabp_solve_device(gabp_graph_t *G, const gabp_options_t *opt, double *d_mean
     const Ctrl &c = *G->h_ctrl;
     cudaStream_t st = G->stream;
     const int64_t slot = c.final_slot;
+    const double *xm = G->x[slot], *pm = G->p[slot];
+    rc = rows_order(G, 0, G->g.n, &xm, &pm);
+    if (rc) return rc;
     if (d_means)
-        CK(cudaMemcpyAsync(d_means, G->x[slot], sizeof(double) * G->g.n,
-                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(d_means, xm, sizeof(double) * G->g.n, cudaMemcpyDeviceToDevice, st));
     if (d_precs)
-        CK(cudaMemcpyAsync(d_precs, G->p[slot], sizeof(double) * G->g.n,
-                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(d_precs, pm, sizeof(double) * G->g.n, cudaMemcpyDeviceToDevice, st));
     double rsq_last = NAN;
     if (c.n_hist > 0)
         CK(cudaMemcpyAsync(&rsq_last, G->rsq_hist + (c.n_hist - 1), sizeof(double),

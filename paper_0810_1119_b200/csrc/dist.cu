@@ -17,11 +17,12 @@ __global__ void finish_kernel(const SweepArgs a) {
     if (c->done) return;
     const int64_t s = c->next_sweep;
     const int slot = (int)(s % kStatSlots);
+    const int mslot = (int)((s - a.msg_lag) % kStatSlots);  // sweep of the message stats
     const double *d = a.dstats;
-    c->change_bits[slot] = (unsigned long long)__double_as_longlong(d[0]);
-    c->msg_nonfinite[slot] = d[1] > 0.0 ? 1 : 0;
+    c->change_bits[mslot] = (unsigned long long)__double_as_longlong(d[0]);
+    c->msg_nonfinite[mslot] = d[1] > 0.0 ? 1 : 0;
     c->means_nonfinite[(s - 1) % kStatSlots] = d[2] > 0.0 ? 1 : 0;
-    c->singular_min[slot] = d[3] > -1e299 ? (unsigned long long)(-d[3]) : kNoIndex;
+    c->singular_min[mslot] = d[3] > -1e299 ? (unsigned long long)(-d[3]) : kNoIndex;
     c->agg_singular[slot] = d[4] > -1e299 ? (unsigned long long)(-d[4]) : kNoIndex;
     decide_sweep(c, a, s - 2, d[5]);
     const int nslot = (int)((s + 1) % kStatSlots);
@@ -36,12 +37,12 @@ __global__ void finish_kernel(const SweepArgs a) {
 
 // Halo buffers: cnt x {P, P mu~} (2 doubles) followed by cnt x x_j.
 // After finish_kernel of launch s (next_sweep == s+1) the launch-s outputs are
-// agg[(s-1)&1] (aggregates of S_{s-1}) and x[(s-1)%3] (x^{(s-1)}): exactly what launch s+1
-// gathers for remote neighbours.
+// agg[(s-1)%3] (aggregates of S_{s-1}) and x[(s-1)%3] (x^{(s-1)}): exactly what launch s+1
+// gathers for remote neighbours (indices are local ids, or positions on the slice path).
 __global__ void halo_pack_kernel(const SweepArgs a, const uint32_t *idx, int64_t cnt,
                                  double *buf) {
     const int64_t s = ((volatile Ctrl *)a.ctrl)->next_sweep - 1;
-    const double2 *agg = a.agg[(s - 1) & 1];
+    const double2 *agg = a.agg[(s - 1) % 3];
     const double *x = a.x[(s - 1) % 3];
     double2 *bagg = reinterpret_cast<double2 *>(buf);
     double *bx = buf + 2 * cnt;
@@ -56,7 +57,7 @@ __global__ void halo_pack_kernel(const SweepArgs a, const uint32_t *idx, int64_t
 __global__ void halo_unpack_kernel(const SweepArgs a, const uint32_t *idx, int64_t cnt,
                                    const double *buf) {
     const int64_t s = ((volatile Ctrl *)a.ctrl)->next_sweep - 1;
-    double2 *agg = a.agg[(s - 1) & 1];
+    double2 *agg = a.agg[(s - 1) % 3];
     double *x = a.x[(s - 1) % 3];
     const double2 *bagg = reinterpret_cast<const double2 *>(buf);
     const double *bx = buf + 2 * cnt;

@@ -12,8 +12,8 @@
 //   tile_start u32[T+1]  row tiles: <= kTileRows rows, edges bounded by kBucket + deg
 // Message state: msg[3] f64x2[E] = {P, mu} per directed edge (out-slot layout:
 // message i->j lives at edge id of (i->j), i.e. in row i), a ring of three sweeps.
-// agg[2] f64x2[n] = {P_i, P_i * mu~_i}: node aggregates of the previous state, used by
-// the aggregate-recompute gather mode (sweep.cu).
+// agg[3] f64x2[n] = {P_i, P_i * mu~_i}: node aggregates of the last states, used by the
+// aggregate-recompute gathers (sweep.cu, slice.cu).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -107,7 +107,7 @@ struct SweepArgs {
     const double *prior_num;
     const double *rhs;
     double2 *msg[3];
-    double2 *agg[2];
+    double2 *agg[3];
     double *x[3];
     double *p[3];
     double *rsq_part;   // [>= persistent grid] per-CTA residual partials
@@ -122,12 +122,16 @@ struct SweepArgs {
     // finish_kernel decides once the reduction is done (dist.cu)
     int dist;
     double *dstats;
-    // slice layout (slice.cu): lane-per-row broadcast solve
+    int msg_lag;        // message statistics of a launch refer to sweep s - msg_lag
+    // slice layout (slice.cu): lane-per-row broadcast solve, nodes in position order
     int64_t nslices;
     const uint2 *slice_info;   // {slot base, width} per slice of 32 rows
-    const uint4 *lane_info;    // {row, first edge id, degree, 0} per lane
-    const uint32_t *scol;      // destination of each slot
-    const double *scoef;       // A_ij of each slot
+    const uint32_t *sdeg;      // degree per position
+    const uint32_t *srow;      // local row per position (~0: padding / halo)
+    const double2 *snd;        // {A_ii, A_ii mu_ii} per position
+    const double *srhs;        // b_i per position
+    const uint32_t *scol;      // position of the destination, per slot
+    const double *scoef;       // A_ij per slot
 };
 
 // kernels (sweep.cu); prepare_sweep_kernels() must run once per device before launches
@@ -218,9 +222,12 @@ struct DeviceGraph {
     double twin_span = 0.0;  // mean |rev(e) - e| in edges: locality of the twin gather
     int64_t row_lo = 0, row_hi = 0;  // swept rows
     // slice layout (build_slices, slice.cu); nslices == 0 when not built
-    int64_t nslices = 0, nslots = 0;
+    int64_t nslices = 0, nslots = 0, npos = 0;
     uint2 *slice_info = nullptr;
-    uint4 *lane_info = nullptr;
+    uint32_t *pos = nullptr;    // local row -> position
+    uint32_t *srow = nullptr, *sdeg = nullptr;
+    double2 *snd = nullptr;
+    double *srhs = nullptr;
     uint32_t *scol = nullptr;
     double *scoef = nullptr;
 };
@@ -237,6 +244,10 @@ void free_graph(DeviceGraph &g);
 int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
 cudaError_t prepare_slice_kernels();
 cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st);
+cudaError_t refresh_slice_nodes(const DeviceGraph &g, cudaStream_t st);
+cudaError_t slice_to_rows(const DeviceGraph &g, int64_t lo, int64_t cnt, const double *in,
+                          double *out, cudaStream_t st);
+cudaError_t slice_map_index(const DeviceGraph &g, uint32_t *idx, int64_t cnt, cudaStream_t st);
 constexpr int64_t kSliceMaxDegree = 4096;  // rows longer than this: tile layout only
 int compute_priors(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
 
