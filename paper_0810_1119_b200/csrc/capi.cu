@@ -69,7 +69,7 @@ struct DistState {
     std::vector<int> peers;
     std::vector<int64_t> scount, rcount, soff, roff;  // nodes per peer, offsets
     uint32_t *d_sidx = nullptr, *d_ridx = nullptr;
-    double *d_sbuf = nullptr, *d_rbuf = nullptr;       // 3 doubles per node, per-peer blocks
+    double *d_sbuf = nullptr, *d_rbuf = nullptr;       // 4 doubles per node, per-peer blocks
     double *d_stats = nullptr;                          // [0..4] max, [5] sum
 };
 
@@ -84,6 +84,7 @@ struct gabp_graph {
     // solve workspace
     double2 *msg[3] = {nullptr, nullptr, nullptr};
     double2 *agg[3] = {nullptr, nullptr, nullptr};
+    gabp::NodeState *rec[3] = {nullptr, nullptr, nullptr};  // slice path node states
     double *x[3] = {nullptr, nullptr, nullptr};
     double *p[3] = {nullptr, nullptr, nullptr};
     double *rsq_part = nullptr;
@@ -153,7 +154,8 @@ int load_nccl() {
 
 // message slots of the solve ring: CSR edges, or slice slots (padding included)
 int64_t msg_slots(const DeviceGraph &g) {
-    int64_t m = g.E > g.nslots ? g.E : g.nslots;
+    const int64_t ns = g.nslices > 0 ? g.nslots + gabp::kSlotPad : 0;
+    const int64_t m = g.E > ns ? g.E : ns;
     return m > 0 ? m : 1;
 }
 
@@ -170,6 +172,9 @@ int ensure_workspace(gabp_graph *G, int64_t max_iter) {
             CK(cudaMalloc(&G->p[b], sizeof(double) * nn));
             CK(cudaMemset(G->x[b], 0, sizeof(double) * nn));
         }
+        if (g.nslices > 0)
+            for (int b = 0; b < 3; ++b)
+                CK(cudaMalloc(&G->rec[b], sizeof(gabp::NodeState) * (g.npos + gabp::kNodePad)));
         CK(cudaMalloc(&G->xs, sizeof(double) * (g.n + 1)));
         CK(cudaMalloc(&G->ps, sizeof(double) * (g.n + 1)));
         // one partial per CTA of a persistent launch (either layout)
@@ -220,6 +225,9 @@ SweepArgs make_args(gabp_graph *G) {
     a.xhist = G->xhist;
     a.xhist_rows = G->xhist_rows;
     a.msg_lag = 0;
+    for (int b = 0; b < 3; ++b) a.rec[b] = G->rec[b];
+    a.slice_variant = g.slice_variant;
+    a.slice_path = 0;
     a.nslices = g.nslices;
     a.slice_info = g.slice_info;
     a.sdeg = g.sdeg;
@@ -234,6 +242,7 @@ SweepArgs make_args(gabp_graph *G) {
 void release_workspace(gabp_graph *G) {
     for (int b = 0; b < 3; ++b) cudaFree(G->msg[b]);
     for (int b = 0; b < 3; ++b) cudaFree(G->agg[b]);
+    for (int b = 0; b < 3; ++b) cudaFree(G->rec[b]);
     cudaFree(G->xs);
     cudaFree(G->ps);
     for (int b = 0; b < 3; ++b) {
@@ -427,20 +436,20 @@ int dist_launch_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
     if (D->peers.empty()) return GABP_OK;
     for (size_t q = 0; q < D->peers.size(); ++q)
         CK(gabp::launch_halo_pack(a, D->d_sidx + D->soff[q], D->scount[q],
-                                  D->d_sbuf + 3 * D->soff[q], st));
+                                  D->d_sbuf + 4 * D->soff[q], st));
     NK(g_nccl.groupStart());
     for (size_t q = 0; q < D->peers.size(); ++q) {
         if (D->scount[q])
-            NK(g_nccl.send(D->d_sbuf + 3 * D->soff[q], 3 * D->scount[q], ncclFloat64,
+            NK(g_nccl.send(D->d_sbuf + 4 * D->soff[q], 4 * D->scount[q], ncclFloat64,
                            D->peers[q], D->comm, st));
         if (D->rcount[q])
-            NK(g_nccl.recv(D->d_rbuf + 3 * D->roff[q], 3 * D->rcount[q], ncclFloat64,
+            NK(g_nccl.recv(D->d_rbuf + 4 * D->roff[q], 4 * D->rcount[q], ncclFloat64,
                            D->peers[q], D->comm, st));
     }
     NK(g_nccl.groupEnd());
     for (size_t q = 0; q < D->peers.size(); ++q)
         CK(gabp::launch_halo_unpack(a, D->d_ridx + D->roff[q], D->rcount[q],
-                                    D->d_rbuf + 3 * D->roff[q], st));
+                                    D->d_rbuf + 4 * D->roff[q], st));
     return GABP_OK;
 }
 
@@ -449,6 +458,7 @@ SweepArgs make_dist_args(gabp_graph *G) {
     a.dist = 1;
     a.dstats = G->dist->d_stats;
     a.msg_lag = dist_gather(G) == gabp::kGatherSlice ? 1 : 0;
+    a.slice_path = a.msg_lag;
     return a;
 }
 
@@ -922,12 +932,14 @@ int gabp_infer_marginals(const gabp_graph_t *G, const gabp_state_t *S, double *h
 
 // ---- solve --------------------------------------------------------------------------------
 
-// Marginals of the last solve in row order: the slice path keeps them in position order.
-static int rows_order(gabp_graph *G, int64_t r0, int64_t nr, const double **xm,
+// Marginals of the last solve in row order: the slice path keeps them in position order,
+// in the node state records {P_i, P_i mu~_i, x_i, -}.
+static int rows_order(gabp_graph *G, int64_t slot, int64_t r0, int64_t nr, const double **xm,
                       const double **pm) {
     if (!G->slice_order) return GABP_OK;
-    CK(gabp::slice_to_rows(G->g, r0, nr, *xm, G->xs, G->stream));
-    CK(gabp::slice_to_rows(G->g, r0, nr, *pm, G->ps, G->stream));
+    const double *rec = reinterpret_cast<const double *>(G->rec[slot]);
+    CK(gabp::slice_to_rows(G->g, r0, nr, rec + 2, 4, G->xs, G->stream));
+    CK(gabp::slice_to_rows(G->g, r0, nr, rec, 4, G->ps, G->stream));
     *xm = G->xs;
     *pm = G->ps;
     return GABP_OK;
@@ -943,7 +955,7 @@ static int copy_results(gabp_graph *G, const gabp_options_t *opt, double ms, dou
     const int64_t r0 = G->dist ? G->g.row_lo : 0;
     const int64_t nr = G->dist ? G->g.row_hi - G->g.row_lo : G->g.n;
     const double *xm = G->x[slot], *pm = G->p[slot];
-    int rc = rows_order(G, r0, nr, &xm, &pm);
+    int rc = rows_order(G, slot, r0, nr, &xm, &pm);
     if (rc) return rc;
     if (h_means)
         CK(cudaMemcpyAsync(h_means, xm + r0, sizeof(double) * nr, cudaMemcpyDeviceToHost, st));
@@ -1030,8 +1042,8 @@ int gabp_dist_attach(gabp_graph_t *G, const void *nccl_id, int32_t rank, int32_t
     }
     CK(cudaMalloc(&D->d_sidx, sizeof(uint32_t) * si.size()));
     CK(cudaMalloc(&D->d_ridx, sizeof(uint32_t) * ri.size()));
-    CK(cudaMalloc(&D->d_sbuf, sizeof(double) * 3 * si.size()));
-    CK(cudaMalloc(&D->d_rbuf, sizeof(double) * 3 * ri.size()));
+    CK(cudaMalloc(&D->d_sbuf, sizeof(double) * 4 * si.size()));
+    CK(cudaMalloc(&D->d_rbuf, sizeof(double) * 4 * ri.size()));
     CK(cudaMalloc(&D->d_stats, sizeof(double) * 8));
     CK(cudaMemcpy(D->d_sidx, si.data(), sizeof(uint32_t) * si.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(D->d_ridx, ri.data(), sizeof(uint32_t) * ri.size(), cudaMemcpyHostToDevice));
@@ -1092,7 +1104,7 @@ int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_optio
             DistState *D = parts[p]->dist;
             for (size_t q = 0; q < D->peers.size(); ++q)
                 CK(gabp::launch_halo_pack(args[p], D->d_sidx + D->soff[q], D->scount[q],
-                                          D->d_sbuf + 3 * D->soff[q], parts[p]->stream));
+                                          D->d_sbuf + 4 * D->soff[q], parts[p]->stream));
             CK(cudaStreamSynchronize(parts[p]->stream));
         }
         for (int p = 0; p < nparts; ++p) {  // move each peer's block for p into p's recv
@@ -1104,13 +1116,13 @@ int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_optio
                 while (qs < S->peers.size() && S->peers[qs] != p) ++qs;
                 if (qs == S->peers.size() || S->scount[qs] != D->rcount[q])
                     return fail(GABP_EINVAL, "halo lists of ranks %d and %d disagree", p, src);
-                CK(cudaMemcpyAsync(D->d_rbuf + 3 * D->roff[q], S->d_sbuf + 3 * S->soff[qs],
-                                   sizeof(double) * 3 * D->rcount[q], cudaMemcpyDeviceToDevice,
+                CK(cudaMemcpyAsync(D->d_rbuf + 4 * D->roff[q], S->d_sbuf + 4 * S->soff[qs],
+                                   sizeof(double) * 4 * D->rcount[q], cudaMemcpyDeviceToDevice,
                                    parts[p]->stream));
             }
             for (size_t q = 0; q < D->peers.size(); ++q)
                 CK(gabp::launch_halo_unpack(args[p], D->d_ridx + D->roff[q], D->rcount[q],
-                                            D->d_rbuf + 3 * D->roff[q], parts[p]->stream));
+                                            D->d_rbuf + 4 * D->roff[q], parts[p]->stream));
         }
         for (int p = 0; p < nparts; ++p) CK(cudaStreamSynchronize(parts[p]->stream));
         int32_t done = 0;
@@ -1144,7 +1156,7 @@ int gabp_solve_device(gabp_graph_t *G, const gabp_options_t *opt, double *d_mean
     cudaStream_t st = G->stream;
     const int64_t slot = c.final_slot;
     const double *xm = G->x[slot], *pm = G->p[slot];
-    rc = rows_order(G, 0, G->g.n, &xm, &pm);
+    rc = rows_order(G, slot, 0, G->g.n, &xm, &pm);
     if (rc) return rc;
     if (d_means)
         CK(cudaMemcpyAsync(d_means, xm, sizeof(double) * G->g.n, cudaMemcpyDeviceToDevice, st));

@@ -35,37 +35,45 @@ __global__ void finish_kernel(const SweepArgs a) {
     __threadfence();
 }
 
-// Halo buffers: cnt x {P, P mu~} (2 doubles) followed by cnt x x_j.
-// After finish_kernel of launch s (next_sweep == s+1) the launch-s outputs are
-// agg[(s-1)%3] (aggregates of S_{s-1}) and x[(s-1)%3] (x^{(s-1)}): exactly what launch s+1
+// Halo buffers: cnt records of 4 doubles per node -- {P, P mu~, x, 0}: the node state of
+// the slice path verbatim, or the tile path's aggregate and marginal.
+// After finish_kernel of launch s (next_sweep == s+1) the launch-s outputs are the state
+// of S_{s-1} (rec[(s-1)%3], or agg[(s-1)%3] and x[(s-1)%3]): exactly what launch s+1
 // gathers for remote neighbours (indices are local ids, or positions on the slice path).
 __global__ void halo_pack_kernel(const SweepArgs a, const uint32_t *idx, int64_t cnt,
                                  double *buf) {
     const int64_t s = ((volatile Ctrl *)a.ctrl)->next_sweep - 1;
-    const double2 *agg = a.agg[(s - 1) % 3];
-    const double *x = a.x[(s - 1) % 3];
-    double2 *bagg = reinterpret_cast<double2 *>(buf);
-    double *bx = buf + 2 * cnt;
+    double4 *b4 = reinterpret_cast<double4 *>(buf);
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
          k += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t i = idx[k];
-        bagg[k] = agg[i];
-        bx[k] = x[i];
+        if (a.slice_path) {
+            const NodeState r = a.rec[(s - 1) % 3][i];
+            b4[k] = make_double4(r.P, r.N, r.x, 0.0);
+        } else {
+            const double2 g = a.agg[(s - 1) % 3][i];
+            b4[k] = make_double4(g.x, g.y, a.x[(s - 1) % 3][i], 0.0);
+        }
     }
 }
 
 __global__ void halo_unpack_kernel(const SweepArgs a, const uint32_t *idx, int64_t cnt,
                                    const double *buf) {
     const int64_t s = ((volatile Ctrl *)a.ctrl)->next_sweep - 1;
-    double2 *agg = a.agg[(s - 1) % 3];
-    double *x = a.x[(s - 1) % 3];
-    const double2 *bagg = reinterpret_cast<const double2 *>(buf);
-    const double *bx = buf + 2 * cnt;
+    const double4 *b4 = reinterpret_cast<const double4 *>(buf);
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
          k += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t i = idx[k];
-        agg[i] = bagg[k];
-        x[i] = bx[k];
+        const double4 v = b4[k];
+        if (a.slice_path) {
+            NodeState &r = a.rec[(s - 1) % 3][i];
+            r.P = v.x;
+            r.N = v.y;
+            r.x = v.z;
+        } else {
+            a.agg[(s - 1) % 3][i] = make_double2(v.x, v.y);
+            a.x[(s - 1) % 3][i] = v.z;
+        }
     }
 }
 

@@ -54,6 +54,15 @@ struct __align__(16) EdgeRec {
     double coeff;   // A_ij
 };
 
+// Per-sweep state of a node on the slice path: aggregate {P_i, P_i mu~_i} of S_t and the
+// marginal x_i^{(t)} -- one 32-byte sector, gathered with one 256-bit load.
+struct __align__(32) NodeState {
+    double P;   // P_i = A_ii + sum_k P_ki
+    double N;   // P_i * mu~_i
+    double x;   // x_i = N_i / P_i (the marginal mean)
+    double pad;
+};
+
 struct __align__(16) NodeRec {
     double diag;    // A_ii
     double pnum;    // A_ii * (b_i / A_ii)
@@ -70,6 +79,8 @@ struct Ctrl {
     int32_t done;
     int32_t converged;
     int32_t diverged;
+    int32_t redo;        // slice path: 1 = a fast launch met a slow-path division, 2 = the
+                         // exact relaunch of that sweep is pending (slice.cu)
     uint32_t ticket;     // finished-block counter of the current launch
     int64_t iterations;
     int64_t n_hist;
@@ -123,6 +134,9 @@ struct SweepArgs {
     int dist;
     double *dstats;
     int msg_lag;        // message statistics of a launch refer to sweep s - msg_lag
+    NodeState *rec[3];  // slice path: node state of S_t in rec[t % 3] (position order)
+    int slice_variant;  // slice kernel: 0 register batches, 1 cp.async ring
+    int slice_path;     // this launch family is the slice path (halo records)
     // slice layout (slice.cu): lane-per-row broadcast solve, nodes in position order
     int64_t nslices;
     const uint2 *slice_info;   // {slot base, width} per slice of 32 rows
@@ -223,6 +237,7 @@ struct DeviceGraph {
     int64_t row_lo = 0, row_hi = 0;  // swept rows
     // slice layout (build_slices, slice.cu); nslices == 0 when not built
     int64_t nslices = 0, nslots = 0, npos = 0;
+    int slice_variant = 0;      // 0: register batches (long rows), 1: cp.async ring
     uint2 *slice_info = nullptr;
     uint32_t *pos = nullptr;    // local row -> position
     uint32_t *srow = nullptr, *sdeg = nullptr;
@@ -246,9 +261,10 @@ cudaError_t prepare_slice_kernels();
 cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st);
 cudaError_t refresh_slice_nodes(const DeviceGraph &g, cudaStream_t st);
 cudaError_t slice_to_rows(const DeviceGraph &g, int64_t lo, int64_t cnt, const double *in,
-                          double *out, cudaStream_t st);
+                          int stride, double *out, cudaStream_t st);
 cudaError_t slice_map_index(const DeviceGraph &g, uint32_t *idx, int64_t cnt, cudaStream_t st);
 constexpr int64_t kSliceMaxDegree = 4096;  // rows longer than this: tile layout only
+constexpr int64_t kSlotPad = 256;          // slot arrays are padded by 8 batches of 32
 int compute_priors(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
 
 }  // namespace gabp

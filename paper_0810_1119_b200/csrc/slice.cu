@@ -10,235 +10,562 @@
 // every per-edge stream is a fully coalesced warp access, and only the neighbour gathers
 // are random (node arrays, L2-resident for the headline graph).
 //
-// State on this path: per edge slot the INCOMING pair I_ij^{(t)} = (P_ji, P_ji mu_ji) of
-// S_t (message j -> i, the terms row i sums), a ring of three; per node the aggregate
-// {P_i, P_i mu~_i} of S_t, a ring of three.  Launch s (one sweep, solver.py:232-272):
-//   m_ij^{(s-2)} = msg(agg_i(S_{s-3}), I_ij^{(s-3)})      own outgoing messages, rebuilt
-//   m_ij^{(s-1)} = msg(agg_i(S_{s-2}), I_ij^{(s-2)})      with launch s-1's / s-2's operands
-//   I_ij^{(s-1)} = msg(agg_j(S_{s-2}), m_ij^{(s-2)})      = m_ji^{(s-1)}, exactly as row j
-//                                                         built it (same operands, same bits)
+// State on this path: per edge slot the INCOMING message I_ij^{(t)} = m_ji^{(t)} = (P, mu)
+// of S_t (the term row i sums), a ring of three; per node the aggregate {P_i, P_i mu~_i}
+// of S_t, a ring of three.  Launch s (one sweep, solver.py:232-272):
+//   m_ij^{(s-2)} = msg(agg_i(S_{s-3}), I_ij^{(s-3)})    own outgoing message, rebuilt with
+//                                                     the operands launch s-2 used
+//   I_ij^{(s-1)} = msg(agg_j(S_{s-2}), m_ij^{(s-2)})    = m_ji^{(s-1)} exactly as row j's
+//                                                     sweep s-1 built it (same bits)
 //   P_i = A_ii + sum_j P_ji, N_i = A_ii mu_ii + sum_j P_ji mu_ji   ascending j (np.add.at)
 //   x_i^{(s-1)} = N_i / P_i, agg_i(S_{s-1}) = {P_i, P_i x_i}, residual row of x^{(s-2)}
 // with msg(agg, m) = (-A_ij^2 / (agg.P - m.P), (agg.N - m.P m.mu) / A_ij) (solver.py:249-257).
-// One streaming pass per edge: 44 B read + 16 B written, no staging, no CTA barrier.  The
-// statistics of sweep s-1's messages (max change, blowup, P_excl == 0) are taken here, one
-// launch after the sweep itself and still one launch before its decision (Ctrl slots).
+// Every directed message is exactly one row's incoming message, so sweep s-1's statistics
+// (max |change| against I^{(s-2)}, blowup, P_excl == 0 with the reference's edge id) are
+// taken on I^{(s-1)} here -- one launch after the sweep, one launch before its decision
+// (Ctrl statistic slots, LAG = 1).  Per edge: 4 divisions, 44 B read + 16 B written in one
+// streaming pass; no staging, no CTA barrier.
 // Launch 1 sees I^{(0)} = 0 (solve_setup zeroes the ring); launch 2 uses m^{(0)} = 0.
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_radix_sort.cuh>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "sweep_common.cuh"
-
-#ifndef GABP_SLICE_THREADS
-#define GABP_SLICE_THREADS 256
-#endif
-#ifndef GABP_SLICE_CTAS
-#define GABP_SLICE_CTAS 2
-#endif
-#ifndef GABP_SLICE_U
-#define GABP_SLICE_U 2
-#endif
 
 namespace gabp {
 namespace {
 
-constexpr int kSliceThreads = GABP_SLICE_THREADS;
-constexpr int kSliceWarps = kSliceThreads / 32;
-constexpr int kU = GABP_SLICE_U;  // edges of one lane in flight per batch
-
+// ---- shared pieces -----------------------------------------------------------------------
 struct SliceSmem {
-    TailSmem<kSliceWarps> tail;
+    TailSmem<8> tail;  // up to 256 threads per CTA
     int64_t sweep;
     int skip;
 };
 
+// IEEE a / b.  The fast kernels use the replicated div.rn fast path only and flag the
+// launch when an operand leaves its range (the exact twin then redoes the sweep): no call
+// in the hot loop, so no ABI-preserved registers.
+template <bool EXACT>
+__device__ __forceinline__ double qdiv(double a, double b, unsigned &slow) {
+    if (EXACT) return a / b;
+    bool ok;
+    const double q = ddiv_fast(a, b, ok);
+    slow |= ok ? 0u : 1u;
+    return q;
+}
+
 // msg(agg, m): the outgoing message of an edge from its row aggregate and the incoming
-// pair, as (P, mu); ok is false when a division left the fast path.
+// pair, as (P, mu) (solver.py:249-257)
+template <bool EXACT>
 __device__ __forceinline__ void edge_msg(double c, double pe, double num, double &P, double &mu,
-                                         bool &ok) {
-    bool o1, o2;
-    P = ddiv_fast(-c * c, pe, o1);
-    mu = ddiv_fast(num, c, o2);
-    ok = o1 && o2;
-}
-__device__ __forceinline__ void edge_msg_slow(double c, double pe, double num, double &P,
-                                              double &mu) {
-    P = div_slow(-c * c, pe);
-    mu = div_slow(num, c);
+                                         unsigned &slow) {
+    P = qdiv<EXACT>(-c * c, pe, slow);
+    mu = qdiv<EXACT>(num, c, slow);
 }
 
-// PH: 1 = launch 1 (no incoming yet), 2 = launch 2 (m^{(0)} = 0, no residual), 3 = s >= 3
-template <int PH>
-__device__ __forceinline__ void slice_sweep(const SweepArgs &a, int64_t s, Stats &st, int lane) {
-    const double2 *__restrict__ I2 = a.msg[(s + 1) % 3];   // I^{(s-2)}
-    const double2 *__restrict__ I3 = a.msg[s % 3];         // I^{(s-3)}
-    double2 *__restrict__ I1 = a.msg[(s - 1) % 3];         // I^{(s-1)}, written
-    const double2 *__restrict__ agg2 = a.agg[(s + 1) % 3];  // agg(S_{s-2})
-    const double2 *__restrict__ agg3 = a.agg[s % 3];        // agg(S_{s-3})
-    double2 *__restrict__ agg1 = a.agg[(s - 1) % 3];        // agg(S_{s-1}), written
-    const double *__restrict__ x2 = a.x[(s + 1) % 3];       // x^{(s-2)}
-    double *__restrict__ x1 = a.x[(s - 1) % 3];
-    double *__restrict__ p1 = a.p[(s - 1) % 3];
-    double *xh = (a.xhist && s >= 2 && s - 1 <= a.xhist_rows) ? a.xhist + (s - 2) * a.n : nullptr;
-    const uint32_t *__restrict__ scol = a.scol;
-    const double *__restrict__ scoef = a.scoef;
+// CSR edge id of the message j -> i held in slot q of position p (exact launch only)
+__device__ __forceinline__ uint32_t twin_edge(const SweepArgs &a, int64_t p, uint32_t q) {
+    return a.er[a.row_ptr[a.srow[p]] + q].rev;
+}
 
-    const int64_t nwarps = (int64_t)gridDim.x * kSliceWarps;
-    for (int64_t sl = (int64_t)blockIdx.x * kSliceWarps + (threadIdx.x >> 5); sl < a.nslices;
+__device__ __forceinline__ void ld_node(const NodeState *g, double &P, double &N, double &x) {
+    double pad;
+    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(P), "=d"(N), "=d"(x), "=d"(pad) : "l"(g));
+}
+__device__ __forceinline__ void st_node(NodeState *g, double P, double N, double x) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(g), "d"(P), "d"(N), "d"(x),
+                 "d"(0.0) : "memory");
+}
+
+// Statistics of sweep s-1 on its message j -> i = (ip, im) against S_{s-2}'s (i2);
+// a zero P_excl or aggregate is reported by the exact launch (the fast one flags it).
+template <bool EXACT>
+__device__ __forceinline__ void msg_stats(Stats &st, const SweepArgs &a, double ip, double im,
+                                          double2 i2, double pe, int64_t p, uint32_t q) {
+    const double d1 = fabs(ip - i2.x), d2 = fabs(im - i2.y);
+    st.chg = d1 > st.chg ? d1 : st.chg;
+    st.chg = d2 > st.chg ? d2 : st.chg;
+    if (!(fabs(ip) <= st.lim) || !(fabs(im) <= st.lim)) st.out_of_range = 1u;
+    if (pe == 0.0) {
+        if (EXACT)
+            st.sing = min(st.sing, twin_edge(a, p, q));
+        else
+            st.redo = 1u;
+    }
+}
+
+// Row done: marginal of S_{s-1} and the node state record (solver.py:247-255, 286).
+template <int PH, bool EXACT>
+__device__ __forceinline__ void node_done(Stats &st, const SweepArgs &a, NodeState *rec1,
+                                          double *xh, int64_t p, double sp, double sn, double y,
+                                          double rhs_i) {
+    const double xi = qdiv<EXACT>(sn, sp, st.redo);
+    if (!(fabs(xi) <= DBL_MAX)) st.means_bad = 1u;
+    if (xh) xh[__ldg(a.srow + p)] = xi;
+    if (sp == 0.0) {
+        if (EXACT)
+            st.agg_sing = min(st.agg_sing, __ldg(a.srow + p));
+        else
+            st.redo = 1u;
+    }
+    st_node(rec1 + p, sp, sp * xi, xi);  // (sum_p * mu_tilde)
+    if (PH == 3) {
+        const double r = y - rhs_i;
+        st.rsq += r * r;
+    }
+}
+
+// Ring pointers of launch s, R = s % 3 as a constant (kernel-parameter loads).
+template <int R>
+struct Ring {
+    const double2 *I2, *I3;  // I^{(s-2)}, I^{(s-3)}
+    double2 *I1;             // I^{(s-1)}, written
+    const NodeState *g2, *g3;  // node state of S_{s-2} (gathered), S_{s-3} (own)
+    NodeState *g1;           // node state of S_{s-1}, written
+    __device__ __forceinline__ Ring(const SweepArgs &a)
+        : I2(a.msg[(R + 1) % 3]), I3(a.msg[R]), I1(a.msg[(R + 2) % 3]),
+          g2(a.rec[(R + 1) % 3]), g3(a.rec[R]), g1(a.rec[(R + 2) % 3]) {}
+};
+
+__device__ __forceinline__ double *xhist_row(const SweepArgs &a, int64_t s) {
+    return (a.xhist && s >= 2 && s - 1 <= a.xhist_rows) ? a.xhist + (s - 2) * a.n : nullptr;
+}
+
+// Launch 1: the incoming messages of S_0 are +0, so each row's sums are its prior plus +0.
+template <int NW, bool EXACT>
+__device__ __forceinline__ void slice_first(const SweepArgs &a, int64_t s, Stats &st, int lane) {
+    NodeState *rec1 = a.rec[0];  // S_0 (s = 1)
+    double *xh = xhist_row(a, s);
+    const int64_t nwarps = (int64_t)gridDim.x * NW;
+    for (int64_t sl = (int64_t)blockIdx.x * NW + (threadIdx.x >> 5); sl < a.nslices;
          sl += nwarps) {
-        const uint2 si = __ldg(a.slice_info + sl);  // {slot base, width}
+        const int64_t p = sl * 32 + lane;
+        const double2 nd = __ldg(a.snd + p);
+        const uint32_t d = __ldg(a.sdeg + p);
+        double sp = nd.x, sn = nd.y;
+        if (d > 0) {  // P + 0 (+ 0 ...) == P + 0
+            sp = sp + 0.0;
+            sn = sn + 0.0;
+        }
+        if (nd.x != 0.0) node_done<1, EXACT>(st, a, rec1, xh, p, sp, sn, 0.0, 0.0);
+    }
+}
+
+// ---- variant 0: register batches (long rows) -----------------------------------------------
+// A warp walks its slices; per batch of kUL edge columns every lane issues its contiguous
+// loads (scoef, scol, I^{(s-2)}, I^{(s-3)}) as one group, then the 256-bit neighbour
+// gathers, then computes.  Slot arrays are padded by kUL columns, so loads past a slice's
+// width stay in bounds and need no predicate.
+#ifndef GABP_SLICE_UL
+#define GABP_SLICE_UL 3
+#endif
+constexpr int kUL = GABP_SLICE_UL;
+constexpr int kLThreads = 256;
+constexpr int kLWarps = kLThreads / 32;
+
+__device__ __forceinline__ double ldcs_f64(const double *p) {
+    double v;
+    asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldcs_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.global.cs.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ldcs_f64x2(const double2 *p) {
+    double2 v;
+    asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
+template <int PH, int R, bool EXACT>
+__device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, Stats &st,
+                                                int lane) {
+    const Ring<R> r(a);
+    double *xh = xhist_row(a, s);
+    const int64_t nwarps = (int64_t)gridDim.x * kLWarps;
+    for (int64_t sl = (int64_t)blockIdx.x * kLWarps + (threadIdx.x >> 5); sl < a.nslices;
+         sl += nwarps) {
+        const uint2 si = __ldg(a.slice_info + sl);
         const int64_t p = sl * 32 + lane;
         const uint32_t d = __ldg(a.sdeg + p);
-        const uint32_t row = __ldg(a.srow + p);   // ~0: padding lane (d == 0)
-        const double2 nd = __ldg(a.snd + p);      // {A_ii, A_ii mu_ii}
-        double2 a2 = make_double2(0.0, 0.0), a3 = make_double2(0.0, 0.0);
+        const double2 nd = __ldg(a.snd + p);
+        double2 a3 = make_double2(0.0, 0.0);
         double y = 0.0, rhs_i = 0.0;
-        if (PH >= 2) a2 = __ldcg(agg2 + p);
         if (PH == 3) {
-            a3 = __ldcg(agg3 + p);
-            y = nd.x * __ldcg(x2 + p);
+            a3 = __ldcg(reinterpret_cast<const double2 *>(r.g3 + p));
+            y = nd.x * __ldcg(&r.g2[p].x);
             rhs_i = __ldg(a.srhs + p);
         }
         double sp = nd.x, sn = nd.y;
         const uint32_t base = si.x + lane, w = si.y;
-        if (PH == 1) {
-            if (d > 0) {  // incoming messages of S_0 are +0: P + 0 (+ 0 ...) == P + 0
-                sp = sp + 0.0;
-                sn = sn + 0.0;
-            }
-        } else {
-            for (uint32_t q0 = 0; q0 < w; q0 += kU) {
-                double c[kU], xg[kU];
-                uint32_t col[kU];
-                double2 i2[kU], i3[kU], ag[kU];
+        uint32_t coln[kUL];  // scol of the next batch, loaded one batch ahead
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {  // contiguous streams, all issued together
-                    const uint32_t q = q0 + u, slot = base + 32u * q;
-                    const bool v = q < d;
-                    c[u] = v ? __ldcs(scoef + slot) : 1.0;
-                    col[u] = v ? __ldcs(scol + slot) : 0u;
-                    i2[u] = make_double2(0.0, 0.0);
+        for (int u = 0; u < kUL; ++u) coln[u] = ldcs_u32(a.scol + base + 32u * u);
+        for (uint32_t q0 = 0; q0 < w; q0 += kUL) {
+            double c[kUL];
+            uint32_t col[kUL];
+            double2 i2[kUL], i3[kUL];
+#pragma unroll
+            for (int u = 0; u < kUL; ++u) col[u] = coln[u];
+            double gP[kUL], gN[kUL], gx[kUL];
+#pragma unroll
+            for (int u = 0; u < kUL; ++u) ld_node(r.g2 + col[u], gP[u], gN[u], gx[u]);
+#pragma unroll
+            for (int u = 0; u < kUL; ++u) {
+                const uint32_t slot = base + 32u * (q0 + u);
+                c[u] = ldcs_f64(a.scoef + slot);
+                coln[u] = ldcs_u32(a.scol + slot + 32u * kUL);  // in bounds: slot padding
+                if (PH == 3) {
+                    i2[u] = ldcs_f64x2(r.I2 + slot);
+                    i3[u] = ldcs_f64x2(r.I3 + slot);
+                } else {
+                    i2[u] = make_double2(0.0, 0.0);  // I^{(0)} = 0 at launch 2
                     i3[u] = make_double2(0.0, 0.0);
-                    if (PH == 3) {
-                        i2[u] = v ? __ldcs(I2 + slot) : make_double2(0.0, 0.0);
-                        i3[u] = v ? __ldcs(I3 + slot) : make_double2(0.0, 0.0);
-                    }
                 }
+            }
+            double m2p[kUL], m2m[kUL], ip[kUL], im[kUL], pe[kUL];
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {  // neighbour gathers
-                    const bool v = q0 + u < d;
-                    ag[u] = v ? __ldcg(agg2 + col[u]) : make_double2(1.0, 1.0);
-                    xg[u] = 0.0;
-                    if (PH == 3) xg[u] = v ? __ldcg(x2 + col[u]) : 0.0;
+            for (int u = 0; u < kUL; ++u) {
+                const bool v = q0 + u < d;
+                if (!v) c[u] = 1.0;
+                m2p[u] = 0.0;  // m^{(0)} = 0 at launch 2
+                m2m[u] = 0.0;
+                if (PH == 3) {  // own outgoing message of sweep s-2
+                    const double pe2 = v ? a3.x - i3[u].x : 1.0;
+                    const double nu2 = v ? a3.y - i3[u].x * i3[u].y : 1.0;
+                    edge_msg<EXACT>(c[u], pe2, nu2, m2p[u], m2m[u], st.redo);
                 }
-                // own outgoing messages of sweeps s-2 (m2) and s-1 (m1)
-                double m2p[kU], m2m[kU], m1p[kU], m1m[kU], pe1[kU], nu1[kU], pe2[kU], nu2[kU];
-                bool ok = true;
+            }
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const bool v = q0 + u < d;
-                    pe1[u] = v ? a2.x - i2[u].x : 1.0;
-                    nu1[u] = v ? a2.y - i2[u].y : 1.0;
-                    bool o;
-                    edge_msg(c[u], pe1[u], nu1[u], m1p[u], m1m[u], o);
-                    ok = ok && o;
-                    m2p[u] = 0.0;
-                    m2m[u] = 0.0;
-                    if (PH == 3) {
-                        pe2[u] = v ? a3.x - i3[u].x : 1.0;
-                        nu2[u] = v ? a3.y - i3[u].y : 1.0;
-                        edge_msg(c[u], pe2[u], nu2[u], m2p[u], m2m[u], o);
-                        ok = ok && o;
-                    }
-                }
-                if (!ok) {  // rare: some operand outside the fast-path range
+            for (int u = 0; u < kUL; ++u) {  // incoming of S_{s-1}
+                const bool v = q0 + u < d;
+                pe[u] = v ? gP[u] - m2p[u] : 1.0;
+                const double num = v ? gN[u] - m2p[u] * m2m[u] : 1.0;
+                edge_msg<EXACT>(c[u], pe[u], num, ip[u], im[u], st.redo);
+            }
 #pragma unroll
-                    for (int u = 0; u < kU; ++u) {
-                        edge_msg_slow(c[u], pe1[u], nu1[u], m1p[u], m1m[u]);
-                        if (PH == 3) edge_msg_slow(c[u], pe2[u], nu2[u], m2p[u], m2m[u]);
-                    }
-                }
-                // incoming of S_{s-1}: m_ji^{(s-1)} rebuilt from agg_j(S_{s-2}) and m_ij^{(s-2)}
-                double ip[kU], im[kU], pe[kU], num[kU];
-                ok = true;
-#pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const bool v = q0 + u < d;
-                    pe[u] = v ? ag[u].x - m2p[u] : 1.0;
-                    num[u] = v ? ag[u].y - m2p[u] * m2m[u] : 1.0;
-                    bool o;
-                    edge_msg(c[u], pe[u], num[u], ip[u], im[u], o);
-                    ok = ok && o;
-                }
-                if (!ok) {
-#pragma unroll
-                    for (int u = 0; u < kU; ++u) edge_msg_slow(c[u], pe[u], num[u], ip[u], im[u]);
-                }
-#pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const uint32_t q = q0 + u;
-                    if (q < d) {
-                        const double pm = ip[u] * im[u];  // (prec * mean), solver.py:243
-                        sp = sp + ip[u];
-                        sn = sn + pm;
-                        if (PH == 3) y = y + c[u] * xg[u];
-                        __stcs(I1 + base + 32u * q, make_double2(ip[u], pm));
-                        // statistics of sweep s-1 (its message m1 against m2 = S_{s-2})
-                        const double d1 = fabs(m1p[u] - m2p[u]), d2 = fabs(m1m[u] - m2m[u]);
-                        st.chg = d1 > st.chg ? d1 : st.chg;
-                        st.chg = d2 > st.chg ? d2 : st.chg;
-                        if (!(fabs(m1p[u]) <= st.lim) || !(fabs(m1m[u]) <= st.lim))
-                            st.out_of_range = 1u;
-                        if (pe1[u] == 0.0) st.sing = min(st.sing, __ldg(a.row_ptr + row) + q);
-                    }
+            for (int u = 0; u < kUL; ++u) {
+                const uint32_t q = q0 + u;
+                if (q < d) {
+                    sp = sp + ip[u];
+                    sn = sn + ip[u] * im[u];  // (prec * mean), solver.py:243
+                    if (PH == 3) y = y + c[u] * gx[u];
+                    __stcs(r.I1 + base + 32u * q, make_double2(ip[u], im[u]));
+                    msg_stats<EXACT>(st, a, ip[u], im[u], i2[u], pe[u], p, q);
                 }
             }
         }
-        // ---- node: marginal of S_{s-1}, aggregate, residual row of x^{(s-2)} -------------
-        if (row != 0xffffffffu) {
-            bool ok;
-            double xi = ddiv_fast(sn, sp, ok);  // infer_marginals (solver.py:286)
-            if (!ok) xi = div_slow(sn, sp);
-            x1[p] = xi;
-            p1[p] = sp;
-            if (!(fabs(xi) <= DBL_MAX)) st.means_bad = 1u;
-            if (xh) xh[row] = xi;
-            const double nn = sp * xi;  // (sum_p * mu_tilde), solver.py:247-255
-            if (sp == 0.0) st.agg_sing = min(st.agg_sing, row);
-            agg1[p] = make_double2(sp, nn);
-            if (PH == 3) {
-                const double r = y - rhs_i;
-                st.rsq += r * r;
-            }
+        if (nd.x != 0.0) node_done<PH, EXACT>(st, a, r.g1, xh, p, sp, sn, y, rhs_i);
+    }
+}
+
+// ---- variant 1: cp.async ring (short rows) -----------------------------------------------
+// Each warp walks the flat item sequence (slice, batch of kUP edge columns) of its slices.
+// Everything an item reads is brought in by cp.async, each lane copying its own elements
+// (lane-interleaved, conflict-free; a lane only reads what it copied, so completion is the
+// per-thread cp.async.wait_group): at iteration k a lane issues, as one commit group,
+//   item k+D: scoef, I^{(s-2)}, I^{(s-3)}, the neighbour state {P, N} and x (addresses from
+//             scol, already resident), and on a slice's first item the row header
+//             (A_ii, prior numerator, degree, own state of S_{s-3} / x^{(s-2)}, b_i)
+//   item k+2D: scol into its own (D+1)-entry ring
+// then waits for the group of iteration k-D and computes item k from shared memory only.
+// DRAM and L2 latency are covered by D items of every resident warp.
+#ifndef GABP_SLICE_UP
+#define GABP_SLICE_UP 2
+#endif
+#ifndef GABP_SLICE_DEPTH
+#define GABP_SLICE_DEPTH 2
+#endif
+constexpr int kUP = GABP_SLICE_UP;
+constexpr int kDepth = GABP_SLICE_DEPTH;
+constexpr int kStages = kDepth + 1;
+constexpr int kPThreads = 128;
+constexpr int kPWarps = kPThreads / 32;
+
+struct __align__(16) WarpStage {
+    double2 i2[kUP][32];
+    double2 i3[kUP][32];
+    double2 ag[kUP][32];
+    double2 nd[32];
+    double2 a3[32];
+    double c[kUP][32];
+    double xg[kUP][32];
+    double xo[32];
+    double rhs[32];
+    uint32_t deg[32];
+};
+struct __align__(16) WarpRing {
+    WarpStage st[kStages];
+    uint32_t col[kStages][kUP][32];
+};
+constexpr size_t kPipeSmem = sizeof(WarpRing) * kPWarps;
+
+__device__ __forceinline__ uint32_t su32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cpa4(void *d, const void *g, bool p) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q cp.async.ca.shared.global [%0], [%1], 4;\n}\n"
+                 ::"r"(su32(d)), "l"(g), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void cpa8(void *d, const void *g, bool p) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q cp.async.ca.shared.global [%0], [%1], 8;\n}\n"
+                 ::"r"(su32(d)), "l"(g), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void cpa16(void *d, const void *g, bool p) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q cp.async.cg.shared.global [%0], [%1], 16;\n}\n"
+                 ::"r"(su32(d)), "l"(g), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void cpa16ca(void *d, const void *g, bool p) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q cp.async.ca.shared.global [%0], [%1], 16;\n}\n"
+                 ::"r"(su32(d)), "l"(g), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// position in a warp's item sequence; {base, width} of the warp's next two slices are
+// loaded ahead so crossing into a slice never waits on its descriptor
+struct Cursor {
+    int64_t sl;           // slice (>= nslices: past the end)
+    uint32_t b, nb;       // batch within the slice, batches of the slice (>= 1)
+    uint32_t base, w;     // slot base and width of the slice
+    uint2 next, next2;    // {base, width} of slices sl + nwarps, sl + 2 nwarps
+};
+
+__device__ __forceinline__ uint2 slice_at(const SweepArgs &a, int64_t sl) {
+    return sl < a.nslices ? __ldg(a.slice_info + sl) : make_uint2(0u, 0u);
+}
+__device__ __forceinline__ void cursor_enter(Cursor &c, uint2 si) {
+    c.b = 0;
+    c.base = si.x;
+    c.w = si.y;
+    c.nb = si.y > 0 ? (si.y + kUP - 1) / kUP : 1u;
+}
+__device__ __forceinline__ void cursor_init(Cursor &c, const SweepArgs &a, int64_t sl,
+                                            int64_t nwarps) {
+    c.sl = sl;
+    cursor_enter(c, slice_at(a, sl));
+    c.next = slice_at(a, sl + nwarps);
+    c.next2 = slice_at(a, sl + 2 * nwarps);
+}
+__device__ __forceinline__ void cursor_next(Cursor &c, const SweepArgs &a, int64_t nwarps) {
+    if (c.b + 1 < c.nb) {
+        ++c.b;
+    } else {
+        c.sl += nwarps;
+        cursor_enter(c, c.next);
+        c.next = c.next2;
+        c.next2 = slice_at(a, c.sl + 2 * nwarps);
+    }
+}
+
+template <int PH, int R>
+__device__ __forceinline__ void issue_item(WarpStage &S, const uint32_t (&col)[kUP][32],
+                                           const Cursor &c, const SweepArgs &a,
+                                           const Ring<R> &r, int lane) {
+    if (c.sl >= a.nslices) return;
+    if (c.b == 0) {
+        const int64_t p = c.sl * 32 + lane;
+        cpa16(&S.nd[lane], a.snd + p, true);
+        cpa4(&S.deg[lane], a.sdeg + p, true);
+        if (PH == 3) {
+            cpa16(&S.a3[lane], r.g3 + p, true);
+            cpa8(&S.xo[lane], &r.g2[p].x, true);
+            cpa8(&S.rhs[lane], a.srhs + p, true);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kUP; ++u) {
+        const uint32_t q = c.b * kUP + u;
+        const bool v = q < c.w;
+        const uint32_t slot = c.base + lane + 32u * q;
+        const uint32_t j = col[u][lane];
+        cpa8(&S.c[u][lane], a.scoef + slot, v);
+        cpa16(&S.ag[u][lane], r.g2 + j, v);
+        if (PH == 3) {
+            cpa16(&S.i2[u][lane], r.I2 + slot, v);
+            cpa16(&S.i3[u][lane], r.I3 + slot, v);
+            cpa8(&S.xg[u][lane], &r.g2[j].x, v);
         }
     }
 }
 
-__global__ void __launch_bounds__(kSliceThreads, GABP_SLICE_CTAS) slice_kernel(const SweepArgs a) {
-    __shared__ SliceSmem S;
-    const int tid = threadIdx.x;
-    if (tid == 0) {
+__device__ __forceinline__ void issue_col(uint32_t (&col)[kUP][32], const Cursor &c,
+                                          const SweepArgs &a, int lane) {
+    if (c.sl >= a.nslices) return;
+#pragma unroll
+    for (int u = 0; u < kUP; ++u) {
+        const uint32_t q = c.b * kUP + u;
+        cpa4(&col[u][lane], a.scol + c.base + lane + 32u * q, q < c.w);
+    }
+}
+
+template <int PH, int R, bool EXACT>
+__device__ __forceinline__ void slice_sweep_pipe(const SweepArgs &a, int64_t s, Stats &st,
+                                                 int lane, WarpRing &ring) {
+    const Ring<R> r(a);
+    double *xh = xhist_row(a, s);
+    const int64_t nwarps = (int64_t)gridDim.x * kPWarps;
+    const int64_t first = (int64_t)blockIdx.x * kPWarps + (threadIdx.x >> 5);
+    Cursor C, P, Q;  // items k (compute), k + D (stage), k + 2D (scol)
+    cursor_init(C, a, first, nwarps);
+    P = C;
+    Q = C;
+    // prologue: scol of items 0 .. D-1; then items 0 .. D-1 with scol of D .. 2D-1
+#pragma unroll
+    for (int k = 0; k < kDepth; ++k) {
+        issue_col(ring.col[k], Q, a, lane);
+        cursor_next(Q, a, nwarps);
+    }
+    cpa_commit();
+    cpa_wait<0>();
+#pragma unroll
+    for (int k = 0; k < kDepth; ++k) {
+        issue_item<PH, R>(ring.st[k], ring.col[k], P, a, r, lane);
+        cursor_next(P, a, nwarps);
+        issue_col(ring.col[(k + kDepth) % kStages], Q, a, lane);
+        cursor_next(Q, a, nwarps);
+        cpa_commit();
+    }
+
+    uint32_t d = 0;
+    double2 a3 = make_double2(0.0, 0.0);
+    double sp = 0.0, sn = 0.0, y = 0.0, rhs_i = 0.0, diag = 0.0;
+    for (uint32_t k = 0; C.sl < a.nslices; ++k) {
+        cpa_wait<kDepth - 1>();  // item k and scol of item k+D landed
+        const uint32_t sk = k % kStages, sd = (k + kDepth) % kStages;
+        issue_item<PH, R>(ring.st[sd], ring.col[sd], P, a, r, lane);
+        cursor_next(P, a, nwarps);
+        issue_col(ring.col[(k + 2 * kDepth) % kStages], Q, a, lane);
+        cursor_next(Q, a, nwarps);
+        cpa_commit();
+
+        const WarpStage &S = ring.st[sk];
+        if (C.b == 0) {  // row header
+            d = S.deg[lane];
+            const double2 nd = S.nd[lane];
+            diag = nd.x;
+            sp = nd.x;
+            sn = nd.y;
+            if (PH == 3) {
+                a3 = S.a3[lane];
+                y = nd.x * S.xo[lane];
+                rhs_i = S.rhs[lane];
+            }
+        }
+        double c[kUP], m2p[kUP], m2m[kUP], ip[kUP], im[kUP], pe[kUP];
+#pragma unroll
+        for (int u = 0; u < kUP; ++u) {
+            const bool v = C.b * kUP + u < d;
+            c[u] = v ? S.c[u][lane] : 1.0;
+            m2p[u] = 0.0;  // m^{(0)} = 0 at launch 2
+            m2m[u] = 0.0;
+            if (PH == 3) {  // own outgoing message of sweep s-2
+                const double2 i3 = S.i3[u][lane];
+                const double pe2 = v ? a3.x - i3.x : 1.0;
+                const double nu2 = v ? a3.y - i3.x * i3.y : 1.0;
+                edge_msg<EXACT>(c[u], pe2, nu2, m2p[u], m2m[u], st.redo);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUP; ++u) {  // incoming of S_{s-1}
+            const bool v = C.b * kUP + u < d;
+            const double2 ag = S.ag[u][lane];
+            pe[u] = v ? ag.x - m2p[u] : 1.0;
+            const double num = v ? ag.y - m2p[u] * m2m[u] : 1.0;
+            edge_msg<EXACT>(c[u], pe[u], num, ip[u], im[u], st.redo);
+        }
+        const int64_t p = C.sl * 32 + lane;
+#pragma unroll
+        for (int u = 0; u < kUP; ++u) {
+            const uint32_t q = C.b * kUP + u;
+            if (q < d) {
+                sp = sp + ip[u];
+                sn = sn + ip[u] * im[u];  // (prec * mean), solver.py:243
+                if (PH == 3) y = y + c[u] * S.xg[u][lane];
+                __stcs(r.I1 + C.base + lane + 32u * q, make_double2(ip[u], im[u]));
+                const double2 i2 = PH == 3 ? S.i2[u][lane] : make_double2(0.0, 0.0);
+                msg_stats<EXACT>(st, a, ip[u], im[u], i2, pe[u], p, q);
+            }
+        }
+        if (C.b + 1 == C.nb && diag != 0.0)  // row done (A_ii == 0: padding lane)
+            node_done<PH, EXACT>(st, a, r.g1, xh, p, sp, sn, y, rhs_i);
+        cursor_next(C, a, nwarps);
+    }
+    cpa_wait<0>();  // nothing may land in the ring after the warp leaves
+}
+
+// ---- kernels ---------------------------------------------------------------------------------
+__device__ __forceinline__ bool slice_prologue(SliceSmem &S, const SweepArgs &a, bool exact) {
+    if (threadIdx.x == 0) {
         volatile Ctrl *vc = a.ctrl;
         const int64_t s = vc->next_sweep;
-        S.skip = vc->done || s > vc->max_iter + 2;
+        S.skip = vc->done || s > vc->max_iter + 2 || (exact && vc->redo != 2);
         S.sweep = s;
     }
     __syncthreads();
-    if (S.skip) return;
-    const int64_t s = S.sweep;
-    Stats st;
-    st.lim = fmin(a.ctrl->blowup, DBL_MAX);
-    if (s >= 3)
-        slice_sweep<3>(a, s, st, tid & 31);
-    else if (s == 2)
-        slice_sweep<2>(a, s, st, tid & 31);
-    else
-        slice_sweep<1>(a, s, st, tid & 31);
-    sweep_epilogue<kSliceThreads, kModeSolve, 1>(S.tail, a, s, s >= 3, st, tid);
+    return !S.skip;
 }
 
-int g_slice_grid = 0;
+// EXACT = false: the sweep with fast-path divisions only (every launch).  EXACT = true:
+// the same sweep with IEEE divisions, launched right after it; it runs only when the fast
+// launch flagged an out-of-range division or a singular value (Ctrl.redo == 2).
+template <bool EXACT>
+__global__ void __launch_bounds__(kLThreads, 2) slice_kernel_ldg(const SweepArgs a) {
+    __shared__ SliceSmem S;
+    if (!slice_prologue(S, a, EXACT)) return;
+    const int64_t s = S.sweep;
+    const int tid = threadIdx.x, lane = tid & 31;
+    Stats st;
+    st.lim = fmin(a.ctrl->blowup, DBL_MAX);
+    if (s >= 3) {
+        const int r = (int)(s % 3);
+        if (r == 0)
+            slice_sweep_ldg<3, 0, EXACT>(a, s, st, lane);
+        else if (r == 1)
+            slice_sweep_ldg<3, 1, EXACT>(a, s, st, lane);
+        else
+            slice_sweep_ldg<3, 2, EXACT>(a, s, st, lane);
+    } else if (s == 2) {
+        slice_sweep_ldg<2, 2, EXACT>(a, s, st, lane);
+    } else {
+        slice_first<kLWarps, EXACT>(a, s, st, lane);
+    }
+    sweep_epilogue<kLThreads, kModeSolve, 1>(*reinterpret_cast<TailSmem<kLWarps> *>(&S.tail), a,
+                                              s, s >= 3, st, tid);
+}
+
+__global__ void __launch_bounds__(kPThreads, 3) slice_kernel_pipe(const SweepArgs a) {
+    __shared__ SliceSmem S;
+    extern __shared__ __align__(16) unsigned char pipe_raw[];
+    WarpRing &ring = reinterpret_cast<WarpRing *>(pipe_raw)[threadIdx.x >> 5];
+    if (!slice_prologue(S, a, false)) return;
+    const int64_t s = S.sweep;
+    const int tid = threadIdx.x, lane = tid & 31;
+    Stats st;
+    st.lim = fmin(a.ctrl->blowup, DBL_MAX);
+    if (s >= 3) {
+        const int r = (int)(s % 3);
+        if (r == 0)
+            slice_sweep_pipe<3, 0, false>(a, s, st, lane, ring);
+        else if (r == 1)
+            slice_sweep_pipe<3, 1, false>(a, s, st, lane, ring);
+        else
+            slice_sweep_pipe<3, 2, false>(a, s, st, lane, ring);
+    } else if (s == 2) {
+        slice_sweep_pipe<2, 2, false>(a, s, st, lane, ring);
+    } else {
+        slice_first<kPWarps, false>(a, s, st, lane);
+    }
+    sweep_epilogue<kPThreads, kModeSolve, 1>(*reinterpret_cast<TailSmem<kPWarps> *>(&S.tail), a,
+                                              s, s >= 3, st, tid);
+}
+
+int g_grid_ldg = 0, g_grid_pipe = 0;
 
 // ---- build -------------------------------------------------------------------------------
 constexpr int kSortWin = 1024;  // rows per degree-sort window (a multiple of 32)
@@ -326,15 +653,15 @@ __global__ void slice_nodes_kernel(int64_t npos, const uint32_t *srow, const Nod
         snd[p] = make_double2(nd[r].diag, nd[r].pnum);
         srhs[p] = rhs[r];
     } else {
-        snd[p] = make_double2(1.0, 0.0);
+        snd[p] = make_double2(0.0, 0.0);  // A_ii == 0 marks a padding lane
         srhs[p] = 0.0;
     }
 }
 
 __global__ void gather_pos_kernel(int64_t lo, int64_t cnt, const uint32_t *pos, const double *in,
-                                  double *out) {
+                                  int stride, double *out) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < cnt) out[lo + k] = in[pos[lo + k]];
+    if (k < cnt) out[lo + k] = in[(int64_t)pos[lo + k] * stride];
 }
 
 __global__ void map_pos_kernel(int64_t cnt, const uint32_t *pos, uint32_t *idx) {
@@ -408,8 +735,15 @@ int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
         SCHECK(cudaMallocAsync(&g.sdeg, sizeof(uint32_t) * npos, st));
         SCHECK(cudaMallocAsync(&g.snd, sizeof(double2) * npos, st));
         SCHECK(cudaMallocAsync(&g.srhs, sizeof(double) * npos, st));
-        SCHECK(cudaMallocAsync(&g.scol, sizeof(uint32_t) * (nslots > 0 ? nslots : 1), st));
-        SCHECK(cudaMallocAsync(&g.scoef, sizeof(double) * (nslots > 0 ? nslots : 1), st));
+        // + kSlotPad: the register-batch kernel loads whole batches past a slice's width
+        SCHECK(cudaMallocAsync(&g.scol, sizeof(uint32_t) * (nslots + kSlotPad), st));
+        SCHECK(cudaMallocAsync(&g.scoef, sizeof(double) * (nslots + kSlotPad), st));
+        SCHECK(cudaMemsetAsync(g.scol + nslots, 0, sizeof(uint32_t) * kSlotPad, st));
+        SCHECK(cudaMemsetAsync(g.scoef + nslots, 0, sizeof(double) * kSlotPad, st));
+        // kernel variant: register batches for long rows, the cp.async ring for short ones
+        const double mean_w = (double)nslots / (double)(nslices * 32);
+        g.slice_variant = mean_w > 8.0 ? 0 : 1;
+        if (const char *ev = getenv("GABP_SLICE_VARIANT")) g.slice_variant = atoi(ev) ? 1 : 0;
         slice_info_kernel<<<grid_of(nslices), 256, 0, st>>>(nslices, wslots, base,
                                                             g.slice_info);
         const int64_t big = m > g.n - m ? m : g.n - m;
@@ -441,11 +775,11 @@ cudaError_t refresh_slice_nodes(const DeviceGraph &g, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-// out[i] = in[pos[i]] for local rows [lo, lo + cnt): position order -> row order
+// out[i] = in[stride * pos[i]] for local rows [lo, lo + cnt): position order -> row order
 cudaError_t slice_to_rows(const DeviceGraph &g, int64_t lo, int64_t cnt, const double *in,
-                          double *out, cudaStream_t st) {
+                          int stride, double *out, cudaStream_t st) {
     if (cnt <= 0) return cudaSuccess;
-    gather_pos_kernel<<<grid_of(cnt), 256, 0, st>>>(lo, cnt, g.pos, in, out);
+    gather_pos_kernel<<<grid_of(cnt), 256, 0, st>>>(lo, cnt, g.pos, in, stride, out);
     return cudaGetLastError();
 }
 
@@ -462,18 +796,39 @@ cudaError_t prepare_slice_kernels() {
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
         return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slice_kernel, kSliceThreads, 0)) !=
+    if ((e = cudaFuncSetAttribute(slice_kernel_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kPipeSmem)) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(slice_kernel_pipe,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100)) !=
         cudaSuccess)
         return e;
-    g_slice_grid = sms * (occ > 0 ? occ : 1);
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slice_kernel_pipe, kPThreads,
+                                                           kPipeSmem)) != cudaSuccess)
+        return e;
+    g_grid_pipe = sms * (occ > 0 ? occ : 1);
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slice_kernel_ldg<false>,
+                                                           kLThreads, 0)) != cudaSuccess)
+        return e;
+    g_grid_ldg = sms * (occ > 0 ? occ : 1);
     return cudaSuccess;
 }
 
 cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st) {
-    int64_t grid = g_slice_grid > 0 ? g_slice_grid : 148 * GABP_SLICE_CTAS;
-    const int64_t need = (a.nslices + kSliceWarps - 1) / kSliceWarps;
+    const int64_t nw = a.slice_variant ? kPWarps : kLWarps;
+    int64_t grid = a.slice_variant ? g_grid_pipe : g_grid_ldg;
+    if (grid <= 0) grid = 148 * 2;
+    const int64_t need = (a.nslices + nw - 1) / nw;
     if (grid > need) grid = need > 0 ? need : 1;
-    slice_kernel<<<(unsigned)grid, kSliceThreads, 0, st>>>(a);
+    if (a.slice_variant)
+        slice_kernel_pipe<<<(unsigned)grid, kPThreads, kPipeSmem, st>>>(a);
+    else
+        slice_kernel_ldg<false><<<(unsigned)grid, kLThreads, 0, st>>>(a);
+    // exact twin: exits at once unless the fast launch flagged itself (Ctrl.redo)
+    int64_t gx = g_grid_ldg > 0 ? g_grid_ldg : 148 * 2;
+    const int64_t nx = (a.nslices + kLWarps - 1) / kLWarps;
+    if (gx > nx) gx = nx > 0 ? nx : 1;
+    slice_kernel_ldg<true><<<(unsigned)gx, kLThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -475,3 +475,21 @@ def test_slice_needs_broadcast_and_layout():
     assert r.iterations == orc.iterations
     np.testing.assert_array_equal(r.means, orc.means)
     del s
+
+
+def test_slice_exact_relaunch_zero_rhs():
+    """b = 0 on part of the rows makes 0 / A_ij divisions, which leave the fast division
+    path: the fast slice launch flags itself and its exact twin redoes the sweep."""
+    s = G.gen_poisson2d(40, 1).system
+    rhs = s.rhs.copy()
+    rhs[: s.n // 2] = 0.0
+    s2 = G.SymSystem.from_pairs(s.diag, s.pair_i, s.pair_j, s.pair_v, rhs)
+    og = oracle.build_graph(s2.diag, s2.rhs, s2.pair_i, s2.pair_j, s2.pair_v)
+    orc = oracle.solve(og, epsilon=1e-10, max_iter=400, schedule="broadcast")
+    r = G.solve(s2, G.SolveOptions(schedule="broadcast", epsilon=1e-10, max_iter=400,
+                                   gather_mode="slice"))
+    assert r.iterations == orc.iterations and r.converged == orc.converged
+    np.testing.assert_array_equal(r.means, orc.means)
+    np.testing.assert_array_equal(r.precisions, orc.precisions)
+    np.testing.assert_array_equal(np.asarray(r.max_change_history),
+                                  np.asarray(orc.max_change_history))
