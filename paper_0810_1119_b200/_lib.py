@@ -47,7 +47,8 @@ class GraphInfo(ctypes.Structure):
                 ("device", ctypes.c_int32), ("is_dense", ctypes.c_int32),
                 ("rhs_norm", ctypes.c_double), ("build_ms", ctypes.c_double),
                 ("twin_span", ctypes.c_double), ("num_slices", ctypes.c_int64),
-                ("num_slots", ctypes.c_int64)]
+                ("num_slots", ctypes.c_int64), ("slice_variant", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class Options(ctypes.Structure):

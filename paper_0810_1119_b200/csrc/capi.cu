@@ -731,6 +731,8 @@ int gabp_graph_info(const gabp_graph_t *G, gabp_graph_info_t *info) {
     info->twin_span = G->g.twin_span;
     info->num_slices = G->g.nslices;
     info->num_slots = G->g.nslots;
+    info->slice_variant = G->g.slice_variant;
+    info->reserved = 0;
     return GABP_OK;
 }
 

@@ -219,6 +219,13 @@ class DistributedGraph:
     def handle(self):
         return self._h
 
+    @property
+    def slice_path(self) -> bool:
+        """The rank's block runs the slice-layout kernels (else the row tiles)."""
+        info = _lib.GraphInfo()
+        _lib.check(_lib.load().gabp_graph_info(self._h, ctypes.byref(info)))
+        return int(info.num_slices) > 0
+
     def solve_local_report(self, options):
         """Solve; returns (this rank's owned means, precs, Report, change, residual)."""
         from .solver import _options_struct
