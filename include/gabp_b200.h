@@ -61,7 +61,7 @@ typedef struct {
     double twin_span;     /* mean |rev(e) - e| over edges (twin-gather locality) */
     int64_t num_slices;   /* 32-row slices of the slice layout (0: not built) */
     int64_t num_slots;    /* edge slots of the slice layout, padding included */
-    int32_t slice_variant;/* slice kernel: 0 register batches (long rows), 1 cp.async ring */
+    int32_t slice_variant;/* slice kernel: 0 register batches, 1 cp.async ring, 2 TMA ring (default) */
     int32_t reserved;
 } gabp_graph_info_t;
 

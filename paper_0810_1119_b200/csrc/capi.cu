@@ -227,6 +227,7 @@ SweepArgs make_args(gabp_graph *G) {
     a.msg_lag = 0;
     for (int b = 0; b < 3; ++b) a.rec[b] = G->rec[b];
     a.slice_variant = g.slice_variant;
+    a.slice_unit = g.slice_unit;
     a.slice_path = 0;
     a.nslices = g.nslices;
     a.slice_info = g.slice_info;

@@ -94,6 +94,8 @@ struct Ctrl {
     int32_t means_nonfinite[kStatSlots];
     unsigned long long agg_singular[kStatSlots];   // broadcast: first node with P_i == 0
     unsigned long long singular_min[kStatSlots];   // first edge with P_excl == 0
+    uint32_t work[kStatSlots];  // slice TMA kernel: next work unit of launch s (slot s % 4);
+                                // the last CTA of launch s zeroes slot (s + 2) % 4
 };
 
 // A fresh controller: every "first index" slot at the kNoIndex sentinel.
@@ -135,7 +137,8 @@ struct SweepArgs {
     double *dstats;
     int msg_lag;        // message statistics of a launch refer to sweep s - msg_lag
     NodeState *rec[3];  // slice path: node state of S_t in rec[t % 3] (position order)
-    int slice_variant;  // slice kernel: 0 register batches, 1 cp.async ring
+    int slice_variant;  // slice kernel: 0 register batches, 1 cp.async ring, 2 TMA ring
+    int slice_unit;     // TMA ring: slices per dynamically claimed work unit
     int slice_path;     // this launch family is the slice path (halo records)
     // slice layout (slice.cu): lane-per-row broadcast solve, nodes in position order
     int64_t nslices;
@@ -237,7 +240,8 @@ struct DeviceGraph {
     int64_t row_lo = 0, row_hi = 0;  // swept rows
     // slice layout (build_slices, slice.cu); nslices == 0 when not built
     int64_t nslices = 0, nslots = 0, npos = 0;
-    int slice_variant = 0;      // 0: register batches (long rows), 1: cp.async ring
+    int slice_variant = 0;      // 0: register batches, 1: cp.async ring, 2: TMA ring
+    int slice_unit = 1;         // TMA ring: slices per work unit (>= ~8 chunks per claim)
     uint2 *slice_info = nullptr;
     uint32_t *pos = nullptr;    // local row -> position
     uint32_t *srow = nullptr, *sdeg = nullptr;

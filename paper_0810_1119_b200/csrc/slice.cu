@@ -499,8 +499,330 @@ __device__ __forceinline__ void slice_sweep_pipe(const SweepArgs &a, int64_t s, 
     cpa_wait<0>();  // nothing may land in the ring after the warp leaves
 }
 
+// ---- variant 2: per-warp TMA ring (any row width) ----------------------------------------
+// Each warp owns a ring of kTS stages in shared memory and walks a sequence of chunks
+// (slice, kTC edge columns).  For chunk k+kTS-1, lane 0 issues 1-D bulk copies (TMA,
+// cp.async.bulk, completion counted on the stage's mbarrier) of the chunk's contiguous
+// slot streams -- scoef, scol, I^{(s-2)}, I^{(s-3)} -- and, on a slice's first chunk, of its
+// 32-row header (node priors, degrees, b, own node states of S_{s-3} and S_{s-2}).  So the
+// DRAM stream is in flight independently of the compute; only the neighbour gathers
+// (L2-resident node states) are register loads, issued one chunk ahead from the landed
+// scol.  Slices are claimed dynamically in units of kslice_unit consecutive slices
+// (Ctrl.work), so every SM streams until the end of the sweep and the machine sweeps the
+// slices roughly in position order (grid neighbours stay L2 hits).
+#ifndef GABP_TMA_C
+#define GABP_TMA_C 2
+#endif
+#ifndef GABP_TMA_NS
+#define GABP_TMA_NS 4
+#endif
+#ifndef GABP_TMA_WARPS
+#define GABP_TMA_WARPS 16
+#endif
+#ifndef GABP_TMA_MINB
+#define GABP_TMA_MINB 1
+#endif
+constexpr int kTC = GABP_TMA_C;      // edge columns per chunk
+constexpr int kTS = GABP_TMA_NS;     // stages per warp
+constexpr int kTW = GABP_TMA_WARPS;  // warps per CTA
+constexpr int kTThreads = 32 * kTW;
+
+struct __align__(128) TStage {
+    double2 i2[kTC][32];  // I^{(s-2)} (statistics)
+    double2 i3[kTC][32];  // I^{(s-3)} (own message rebuild)
+    double c[kTC][32];
+    uint32_t col[kTC][32];
+};
+struct TMeta {
+    int64_t sl;       // slice (< 0: no chunk)
+    uint32_t b, nb;   // chunk within the slice, chunks of the slice (>= 1)
+    uint32_t base, w; // slot base and width of the slice
+};
+struct __align__(128) TWarp {
+    TStage st[kTS];
+    uint64_t bar[kTS];
+    TMeta meta[kTS];
+};
+constexpr size_t kTmaSmem = sizeof(TWarp) * kTW;
+static_assert(kTS >= 3, "the chunk k+1 stage must differ from the refilled k-1 stage");
+
+__device__ __forceinline__ void t_mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void t_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void t_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void t_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "TW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra TW_%=;\n}\n" ::"r"(su32(bar)),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
+// streamed once per sweep: evict-first, so the gathered node states keep the L2
+__device__ __forceinline__ void t_bulk_ef(void *dst, const void *src, unsigned bytes,
+                                          uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;\n" ::"r"(su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void t_bulk(void *dst, const void *src, unsigned bytes,
+                                       uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar))
+        : "memory");
+}
+
+// Issue-side cursor of a warp: work units claimed ahead (cur: being issued, nxt: its
+// slice descriptors in flight, pend: lane 0's claim in flight), so neither the claim's
+// atomic nor the descriptor load is waited for when the cursor crosses into a unit.
+struct TCursor {
+    int64_t ucur, unxt;   // units (>= nunits: none)
+    uint2 icur, inxt;     // lane k: {base, width} of slice (unit * U + k), k < U
+    uint32_t pend;        // lane 0: unit of the next claim
+    uint32_t k;           // slice within ucur
+    uint32_t b, nb;       // chunk within the slice
+    int64_t sl;           // slice being issued (< 0: done)
+    uint32_t base, w;
+};
+
+__device__ __forceinline__ uint2 unit_info(const SweepArgs &a, int64_t u, int lane) {
+    const int64_t sl = u * a.slice_unit + lane;
+    return (lane < a.slice_unit && sl < a.nslices) ? __ldg(a.slice_info + sl)
+                                                   : make_uint2(0u, 0u);
+}
+
+template <int PH, int R>
+__device__ __forceinline__ void t_issue(TWarp &W, int stage, TCursor &c, const SweepArgs &a,
+                                        const Ring<R> &r, int64_t nunits, uint32_t *ctr,
+                                        uint64_t pol, int lane) {
+    TMeta m;
+    m.sl = c.sl;
+    if (c.sl >= 0) {
+        m.b = c.b;
+        m.nb = c.nb;
+        m.base = c.base;
+        m.w = c.w;
+        if (lane == 0) {
+            const uint32_t q0 = c.b * kTC;
+            const uint32_t nc = c.w > q0 ? min((uint32_t)kTC, c.w - q0) : 0u;
+            const uint32_t slot = c.base + 32u * q0;
+            const unsigned bytes = nc * 32u * (PH == 3 ? 44u : 12u);
+            TStage &S = W.st[stage];
+            uint64_t *bar = &W.bar[stage];
+            t_expect_tx(bar, bytes);  // (0 bytes: isolated rows only, the arrive completes it)
+            if (nc) {
+                t_bulk_ef(&S.c[0][0], a.scoef + slot, nc * 256u, bar, pol);
+                t_bulk_ef(&S.col[0][0], a.scol + slot, nc * 128u, bar, pol);
+                if (PH == 3) {
+                    t_bulk_ef(&S.i2[0][0], r.I2 + slot, nc * 512u, bar, pol);
+                    t_bulk_ef(&S.i3[0][0], r.I3 + slot, nc * 512u, bar, pol);
+                }
+            }
+            W.meta[stage] = m;
+        }
+        if (++c.b >= c.nb) {
+            ++c.k;
+            for (;;) {  // next slice of the unit, else the next unit
+                if (c.ucur >= nunits) {
+                    c.sl = -1;
+                    break;
+                }
+                const int64_t sl = c.ucur * a.slice_unit + c.k;
+                if (c.k < (uint32_t)a.slice_unit && sl < a.nslices) {
+                    const uint32_t bw = __shfl_sync(~0u, c.icur.x, c.k);
+                    const uint32_t ww = __shfl_sync(~0u, c.icur.y, c.k);
+                    c.sl = sl;
+                    c.base = bw;
+                    c.w = ww;
+                    c.b = 0;
+                    c.nb = ww > 0 ? (ww + kTC - 1) / kTC : 1u;
+                    break;
+                }
+                c.ucur = c.unxt;
+                c.icur = c.inxt;
+                c.unxt = (int64_t)__shfl_sync(~0u, c.pend, 0);
+                c.inxt = unit_info(a, c.unxt, lane);
+                c.k = 0;
+                if (lane == 0) c.pend = atomicAdd(ctr, 1u);
+            }
+        }
+    } else if (lane == 0) {
+        W.meta[stage] = m;
+    }
+}
+
+// Own-row header of a slice (lane = row): prior, degree, and the own node states of
+// S_{s-3} (message rebuild) and S_{s-2} (x_i of the residual row), register loads issued
+// one chunk ahead of use like the gathers.
+struct THdr {
+    double2 nd;   // {A_ii, prior numerator}
+    double2 a3;   // {P_i, N_i} of S_{s-3}
+    double xo;    // x_i^{(s-2)}
+    double rhs;
+    uint32_t d;
+};
+template <int PH, int R>
+__device__ __forceinline__ void t_header(const SweepArgs &a, const Ring<R> &r, int64_t sl,
+                                         int lane, THdr &h) {
+    const int64_t p = sl * 32 + lane;
+    h.nd = __ldg(a.snd + p);
+    h.d = __ldg(a.sdeg + p);
+    if (PH == 3) {
+        h.a3 = __ldcg(reinterpret_cast<const double2 *>(r.g3 + p));
+        h.xo = __ldcg(&r.g2[p].x);
+        h.rhs = __ldg(a.srhs + p);
+    }
+}
+
+// neighbour gathers of a landed chunk (node states of S_{s-2}), one chunk ahead of use
+__device__ __forceinline__ void t_gather(const TStage &S, const TMeta &m, const NodeState *g2,
+                                         int lane, double (&gP)[kTC], double (&gN)[kTC],
+                                         double (&gx)[kTC]) {
+#pragma unroll
+    for (int u = 0; u < kTC; ++u) {
+        if (m.b * kTC + u < m.w) {
+            ld_node(g2 + S.col[u][lane], gP[u], gN[u], gx[u]);
+        } else {
+            gP[u] = 1.0;
+            gN[u] = 1.0;
+            gx[u] = 0.0;
+        }
+    }
+}
+
+template <int PH, int R>
+__device__ __forceinline__ void slice_sweep_tma(const SweepArgs &a, int64_t s, Stats &st,
+                                                int lane, TWarp &W, uint32_t *ctr) {
+    const Ring<R> r(a);
+    double *xh = xhist_row(a, s);
+    const int64_t nunits = (a.nslices + a.slice_unit - 1) / a.slice_unit;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    if (lane < kTS) t_mbar_init(&W.bar[lane], 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncwarp();
+
+    // claim the first three units: cur, nxt (descriptors), pend (lane 0)
+    TCursor c;
+    uint32_t u0 = 0, u1 = 0;
+    if (lane == 0) {
+        u0 = atomicAdd(ctr, 1u);
+        u1 = atomicAdd(ctr, 1u);
+        c.pend = atomicAdd(ctr, 1u);
+    }
+    c.ucur = (int64_t)__shfl_sync(~0u, u0, 0);
+    c.unxt = (int64_t)__shfl_sync(~0u, u1, 0);
+    c.icur = unit_info(a, c.ucur, lane);
+    c.inxt = unit_info(a, c.unxt, lane);
+    c.k = 0;
+    if (c.ucur < nunits) {
+        c.sl = c.ucur * a.slice_unit;
+        c.base = __shfl_sync(~0u, c.icur.x, 0);
+        c.w = __shfl_sync(~0u, c.icur.y, 0);
+        c.b = 0;
+        c.nb = c.w > 0 ? (c.w + kTC - 1) / kTC : 1u;
+    } else {
+        c.sl = -1;
+    }
+#pragma unroll
+    for (int j = 0; j < kTS - 1; ++j) t_issue<PH, R>(W, j, c, a, r, nunits, ctr, pol, lane);
+    __syncwarp();
+    TMeta m = W.meta[0];
+    if (m.sl < 0) return;
+    double gP[kTC], gN[kTC], gx[kTC];
+    THdr hn;
+    t_header<PH, R>(a, r, m.sl, lane, hn);
+    t_wait(&W.bar[0], 0u);
+    t_gather(W.st[0], m, r.g2, lane, gP, gN, gx);
+
+    uint32_t d = 0;
+    double2 a3 = make_double2(0.0, 0.0);
+    double sp = 0.0, sn = 0.0, y = 0.0, rhs_i = 0.0, diag = 0.0;
+    for (uint32_t k = 0;; ++k) {
+        if (m.b == 0) {  // row header (loaded one chunk ago)
+            d = hn.d;
+            diag = hn.nd.x;
+            sp = hn.nd.x;
+            sn = hn.nd.y;
+            if (PH == 3) {
+                a3 = hn.a3;
+                y = hn.nd.x * hn.xo;
+                rhs_i = hn.rhs;
+            }
+        }
+        __syncwarp();  // every lane is done with chunk k-1's stage
+        t_issue<PH, R>(W, (int)((k + kTS - 1) % kTS), c, a, r, nunits, ctr, pol, lane);
+        __syncwarp();
+        // header and gathers of chunk k+1
+        double nP[kTC] = {}, nN[kTC] = {}, nx[kTC] = {};
+        const int sn1 = (int)((k + 1) % kTS);
+        const TMeta mn = W.meta[sn1];
+        if (mn.sl >= 0) {
+            if (mn.b == 0) t_header<PH, R>(a, r, mn.sl, lane, hn);
+            t_wait(&W.bar[sn1], ((k + 1) / kTS) & 1u);
+            t_gather(W.st[sn1], mn, r.g2, lane, nP, nN, nx);
+        }
+        const TStage &S = W.st[k % kTS];
+        double cc[kTC], m2p[kTC], m2m[kTC], ip[kTC], im[kTC], pe[kTC];
+#pragma unroll
+        for (int u = 0; u < kTC; ++u) {
+            const bool v = m.b * kTC + u < d;
+            cc[u] = v ? S.c[u][lane] : 1.0;
+            m2p[u] = 0.0;  // m^{(0)} = 0 at launch 2
+            m2m[u] = 0.0;
+            if (PH == 3) {  // own outgoing message of sweep s-2
+                const double2 i3 = S.i3[u][lane];
+                const double pe2 = v ? a3.x - i3.x : 1.0;
+                const double nu2 = v ? a3.y - i3.x * i3.y : 1.0;
+                edge_msg<false>(cc[u], pe2, nu2, m2p[u], m2m[u], st.redo);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kTC; ++u) {  // incoming of S_{s-1}
+            const bool v = m.b * kTC + u < d;
+            pe[u] = v ? gP[u] - m2p[u] : 1.0;
+            const double num = v ? gN[u] - m2p[u] * m2m[u] : 1.0;
+            edge_msg<false>(cc[u], pe[u], num, ip[u], im[u], st.redo);
+        }
+        const int64_t p = m.sl * 32 + lane;
+#pragma unroll
+        for (int u = 0; u < kTC; ++u) {
+            const uint32_t q = m.b * kTC + u;
+            if (q < d) {
+                sp = sp + ip[u];
+                sn = sn + ip[u] * im[u];  // (prec * mean), solver.py:243
+                if (PH == 3) y = y + cc[u] * gx[u];
+                __stcs(r.I1 + m.base + lane + 32u * q, make_double2(ip[u], im[u]));
+                const double2 i2 = PH == 3 ? S.i2[u][lane] : make_double2(0.0, 0.0);
+                msg_stats<false>(st, a, ip[u], im[u], i2, pe[u], p, q);
+            }
+        }
+        if (m.b + 1 == m.nb && diag != 0.0)  // row done (A_ii == 0: padding lane)
+            node_done<PH, false>(st, a, r.g1, xh, p, sp, sn, y, rhs_i);
+        if (mn.sl < 0) break;
+        m = mn;
+#pragma unroll
+        for (int u = 0; u < kTC; ++u) {
+            gP[u] = nP[u];
+            gN[u] = nN[u];
+            gx[u] = nx[u];
+        }
+    }
+}
+
 // ---- kernels ---------------------------------------------------------------------------------
-__device__ __forceinline__ bool slice_prologue(SliceSmem &S, const SweepArgs &a, bool exact) {
+template <class SM>
+__device__ __forceinline__ bool slice_prologue(SM &S, const SweepArgs &a, bool exact) {
     if (threadIdx.x == 0) {
         volatile Ctrl *vc = a.ctrl;
         const int64_t s = vc->next_sweep;
@@ -565,7 +887,41 @@ __global__ void __launch_bounds__(kPThreads, 3) slice_kernel_pipe(const SweepArg
                                               s, s >= 3, st, tid);
 }
 
-int g_grid_ldg = 0, g_grid_pipe = 0;
+template <int NW>
+struct TmaSmem {
+    TailSmem<NW> tail;
+    int64_t sweep;
+    int skip;
+};
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, GABP_TMA_MINB) slice_kernel_tma(const SweepArgs a) {
+    __shared__ TmaSmem<NW> S;
+    extern __shared__ __align__(128) unsigned char tma_raw[];
+    TWarp &W = reinterpret_cast<TWarp *>(tma_raw)[threadIdx.x >> 5];
+    if (!slice_prologue(S, a, false)) return;
+    const int64_t s = S.sweep;
+    const int tid = threadIdx.x, lane = tid & 31;
+    uint32_t *ctr = &a.ctrl->work[s % kStatSlots];
+    Stats st;
+    st.lim = fmin(a.ctrl->blowup, DBL_MAX);
+    if (s >= 3) {
+        const int r = (int)(s % 3);
+        if (r == 0)
+            slice_sweep_tma<3, 0>(a, s, st, lane, W, ctr);
+        else if (r == 1)
+            slice_sweep_tma<3, 1>(a, s, st, lane, W, ctr);
+        else
+            slice_sweep_tma<3, 2>(a, s, st, lane, W, ctr);
+    } else if (s == 2) {
+        slice_sweep_tma<2, 2>(a, s, st, lane, W, ctr);
+    } else {
+        slice_first<NW, false>(a, s, st, lane);
+    }
+    sweep_epilogue<NW * 32, kModeSolve, 1>(S.tail, a, s, s >= 3, st, tid);
+}
+
+int g_grid_ldg = 0, g_grid_pipe = 0, g_grid_tma = 0;
 
 // ---- build -------------------------------------------------------------------------------
 constexpr int kSortWin = 1024;  // rows per degree-sort window (a multiple of 32)
@@ -742,8 +1098,12 @@ int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
         SCHECK(cudaMemsetAsync(g.scoef + nslots, 0, sizeof(double) * kSlotPad, st));
         // kernel variant: register batches for long rows, the cp.async ring for short ones
         const double mean_w = (double)nslots / (double)(nslices * 32);
-        g.slice_variant = mean_w > 8.0 ? 0 : 1;
-        if (const char *ev = getenv("GABP_SLICE_VARIANT")) g.slice_variant = atoi(ev) ? 1 : 0;
+        g.slice_variant = 2;
+        if (const char *ev = getenv("GABP_SLICE_VARIANT")) g.slice_variant = atoi(ev);
+        if (g.slice_variant < 0 || g.slice_variant > 2) g.slice_variant = 2;
+        // TMA ring: claim units of >= 8 chunks (one atomic per unit)
+        const double chunks = fmax(1.0, ceil(mean_w / kTC));
+        g.slice_unit = (int)fmin(32.0, fmax(1.0, round(8.0 / chunks)));
         slice_info_kernel<<<grid_of(nslices), 256, 0, st>>>(nslices, wslots, base,
                                                             g.slice_info);
         const int64_t big = m > g.n - m ? m : g.n - m;
@@ -811,10 +1171,18 @@ cudaError_t prepare_slice_kernels() {
                                                            kLThreads, 0)) != cudaSuccess)
         return e;
     g_grid_ldg = sms * (occ > 0 ? occ : 1);
+    if ((e = cudaFuncSetAttribute(slice_kernel_tma<kTW>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kTmaSmem)) != cudaSuccess)
+        return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slice_kernel_tma<kTW>,
+                                                           kTThreads, kTmaSmem)) != cudaSuccess)
+        return e;
+    g_grid_tma = sms * (occ > 0 ? occ : 1);
     return cudaSuccess;
 }
 
-cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st) {
+static void launch_slice_fast(const SweepArgs &a, cudaStream_t st) {
     const int64_t nw = a.slice_variant ? kPWarps : kLWarps;
     int64_t grid = a.slice_variant ? g_grid_pipe : g_grid_ldg;
     if (grid <= 0) grid = 148 * 2;
@@ -824,6 +1192,17 @@ cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st) {
         slice_kernel_pipe<<<(unsigned)grid, kPThreads, kPipeSmem, st>>>(a);
     else
         slice_kernel_ldg<false><<<(unsigned)grid, kLThreads, 0, st>>>(a);
+}
+
+cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st) {
+    if (a.slice_variant == 2) {
+        int64_t grid = g_grid_tma > 0 ? g_grid_tma : 148;
+        const int64_t need = (a.nslices + kTW - 1) / kTW;
+        if (grid > need) grid = need > 0 ? need : 1;
+        slice_kernel_tma<kTW><<<(unsigned)grid, kTThreads, kTmaSmem, st>>>(a);
+    } else {
+        launch_slice_fast(a, st);
+    }
     // exact twin: exits at once unless the fast launch flagged itself (Ctrl.redo)
     int64_t gx = g_grid_ldg > 0 ? g_grid_ldg : 148 * 2;
     const int64_t nx = (a.nslices + kLWarps - 1) / kLWarps;
@@ -831,5 +1210,6 @@ cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st) {
     slice_kernel_ldg<true><<<(unsigned)gx, kLThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
+
 
 }  // namespace gabp

@@ -493,3 +493,30 @@ def test_slice_exact_relaunch_zero_rhs():
     np.testing.assert_array_equal(r.precisions, orc.precisions)
     np.testing.assert_array_equal(np.asarray(r.max_change_history),
                                   np.asarray(orc.max_change_history))
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("which", ["ragged", "random64k", "poisson2d_200"])
+def test_slice_kernel_variants_bitwise(variant, which, monkeypatch):
+    """Every slice kernel (0 register batches, 1 cp.async ring, 2 TMA ring with dynamic
+    work units) gives the oracle's bits; GABP_SLICE_VARIANT is read when the layout is
+    built."""
+    monkeypatch.setenv("GABP_SLICE_VARIANT", str(variant))
+    if which == "ragged":
+        s = _ragged_system()
+    elif which == "random64k":
+        s = G.gen_random_sparse(1 << 16, 16, 3).system
+    else:
+        s = G.gen_poisson2d(200, 4).system
+    g = G.build_graph(s)
+    assert int(g.info.slice_variant) == variant
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    orc = oracle.solve(og, epsilon=1e-300, max_iter=60, schedule="broadcast",
+                       rel_residual_tol=1e-8)
+    r = G.solve_graph(g, G.SolveOptions(schedule="broadcast", epsilon=1e-300, max_iter=60,
+                                        rel_residual_tol=1e-8, gather_mode="slice"))
+    assert r.iterations == orc.iterations and r.converged == orc.converged
+    np.testing.assert_array_equal(r.means, orc.means)
+    np.testing.assert_array_equal(r.precisions, orc.precisions)
+    np.testing.assert_array_equal(np.asarray(r.max_change_history),
+                                  np.asarray(orc.max_change_history))
