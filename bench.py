@@ -401,7 +401,10 @@ def run_ours(args):
     t0 = time.perf_counter()
     e2e_updates = 0
     for _ in range(e2e_steps):
+        tc = time.perf_counter()
         e2e_updates += e2e_call() * E
+        if os.environ.get("BENCH_DEBUG"):
+            print(f"e2e call {1e3 * (time.perf_counter() - tc):.1f} ms", file=sys.stderr)
     barrier()
     e2e_s = time.perf_counter() - t0
     if world > 1:

@@ -177,7 +177,7 @@ inline unsigned grid_for(int64_t work, int threads = 256) {
 
 struct Scratch {
     void *p = nullptr;
-    ~Scratch() { if (p) cudaFree(p); }
+    ~Scratch() { if (p) cudaFreeAsync(p, 0); }
 };
 
 #define BCHECK(call)                                                                   \
@@ -191,23 +191,24 @@ struct Scratch {
 
 }  // namespace
 
-void free_graph(DeviceGraph &g) {
-    cudaFree(g.row_ptr);
-    cudaFree(g.tile_start);
-    cudaFree(g.tile_info);
-    cudaFree(g.er);
-    cudaFree(g.nd);
-    cudaFree(g.diag);
-    cudaFree(g.prior_num);
-    cudaFree(g.rhs);
-    cudaFree(g.slice_info);
-    cudaFree(g.pos);
-    cudaFree(g.srow);
-    cudaFree(g.sdeg);
-    cudaFree(g.snd);
-    cudaFree(g.srhs);
-    cudaFree(g.scol);
-    cudaFree(g.scoef);
+void free_graph(DeviceGraph &g, cudaStream_t st) {
+    // stream-ordered: the blocks go back to the device pool (retained, see new_graph)
+    if (g.row_ptr) cudaFreeAsync(g.row_ptr, st);
+    if (g.tile_start) cudaFreeAsync(g.tile_start, st);
+    if (g.tile_info) cudaFreeAsync(g.tile_info, st);
+    if (g.er) cudaFreeAsync(g.er, st);
+    if (g.nd) cudaFreeAsync(g.nd, st);
+    if (g.diag) cudaFreeAsync(g.diag, st);
+    if (g.prior_num) cudaFreeAsync(g.prior_num, st);
+    if (g.rhs) cudaFreeAsync(g.rhs, st);
+    if (g.slice_info) cudaFreeAsync(g.slice_info, st);
+    if (g.pos) cudaFreeAsync(g.pos, st);
+    if (g.srow) cudaFreeAsync(g.srow, st);
+    if (g.sdeg) cudaFreeAsync(g.sdeg, st);
+    if (g.snd) cudaFreeAsync(g.snd, st);
+    if (g.srhs) cudaFreeAsync(g.srhs, st);
+    if (g.scol) cudaFreeAsync(g.scol, st);
+    if (g.scoef) cudaFreeAsync(g.scoef, st);
     g = DeviceGraph{};
 }
 

@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <dlfcn.h>
+#include <chrono>
 #include <nccl.h>  // types only: libnccl is loaded at run time (gabp_dist_attach)
 
 #include <atomic>
@@ -152,6 +153,22 @@ int load_nccl() {
             return fail(GABP_ECUDA, "%s failed: %s", #call, g_nccl.errorString(_r));      \
     } while (0)
 
+// GABP_HOST_TIMING=1: host-clock phase times of the drop-in calls on stderr
+double host_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+bool host_timing() {
+    static const int on = getenv("GABP_HOST_TIMING") ? atoi(getenv("GABP_HOST_TIMING")) : 0;
+    return on != 0;
+}
+
+// stream-ordered free of a pool block (no-op for NULL)
+inline void afree(void *p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
 // message slots of the solve ring: CSR edges, or slice slots (padding included)
 int64_t msg_slots(const DeviceGraph &g) {
     const int64_t ns = g.nslices > 0 ? g.nslots + gabp::kSlotPad : 0;
@@ -160,38 +177,43 @@ int64_t msg_slots(const DeviceGraph &g) {
 }
 
 int ensure_workspace(gabp_graph *G, int64_t max_iter) {
+    // stream-ordered allocations from the retained device pool: a repeated solve or a new
+    // graph of similar size reuses cached blocks instead of mapping fresh memory
     const DeviceGraph &g = G->g;
+    cudaStream_t st = G->stream;
     const int64_t E = msg_slots(g);
     // node arrays: row order (tiles) or position order (slices, padding lanes + halo)
     const int64_t nn = (g.n > g.npos ? g.n : g.npos) + gabp::kNodePad;
     if (!G->msg[0]) {
-        for (int b = 0; b < 3; ++b) CK(cudaMalloc(&G->msg[b], sizeof(double2) * E));
-        for (int b = 0; b < 3; ++b) CK(cudaMalloc(&G->agg[b], sizeof(double2) * nn));
+        for (int b = 0; b < 3; ++b) CK(cudaMallocAsync(&G->msg[b], sizeof(double2) * E, st));
+        for (int b = 0; b < 3; ++b) CK(cudaMallocAsync(&G->agg[b], sizeof(double2) * nn, st));
         for (int b = 0; b < 3; ++b) {
-            CK(cudaMalloc(&G->x[b], sizeof(double) * nn));
-            CK(cudaMalloc(&G->p[b], sizeof(double) * nn));
-            CK(cudaMemset(G->x[b], 0, sizeof(double) * nn));
+            CK(cudaMallocAsync(&G->x[b], sizeof(double) * nn, st));
+            CK(cudaMallocAsync(&G->p[b], sizeof(double) * nn, st));
+            CK(cudaMemsetAsync(G->x[b], 0, sizeof(double) * nn, st));
         }
         if (g.nslices > 0)
             for (int b = 0; b < 3; ++b)
-                CK(cudaMalloc(&G->rec[b], sizeof(gabp::NodeState) * (g.npos + gabp::kNodePad)));
-        CK(cudaMalloc(&G->xs, sizeof(double) * (g.n + 1)));
-        CK(cudaMalloc(&G->ps, sizeof(double) * (g.n + 1)));
+                CK(cudaMallocAsync(&G->rec[b], sizeof(gabp::NodeState) * (g.npos + gabp::kNodePad), st));
+        CK(cudaMallocAsync(&G->xs, sizeof(double) * (g.n + 1), st));
+        CK(cudaMallocAsync(&G->ps, sizeof(double) * (g.n + 1), st));
         // one partial per CTA of a persistent launch (either layout)
-        CK(cudaMalloc(&G->rsq_part, sizeof(double) * (g.ntiles > 8192 ? g.ntiles : 8192)));
-        CK(cudaMalloc(&G->ctrl, sizeof(Ctrl)));
+        CK(cudaMallocAsync(&G->rsq_part, sizeof(double) * (g.ntiles > 8192 ? g.ntiles : 8192), st));
+        CK(cudaMallocAsync(&G->ctrl, sizeof(Ctrl), st));
         CK(cudaMallocHost(&G->h_ctrl, sizeof(Ctrl)));
         CK(cudaMallocHost(&G->h_done, sizeof(int32_t) * 4));
         for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&G->ev[k]));
+        CK(cudaStreamSynchronize(st));  // usable from any stream from here on
         G->ws_gen++;
     }
     if (max_iter > G->hist_cap) {
-        cudaFree(G->change_hist);
-        cudaFree(G->res_hist);
-        cudaFree(G->rsq_hist);
-        CK(cudaMalloc(&G->change_hist, sizeof(double) * max_iter));
-        CK(cudaMalloc(&G->res_hist, sizeof(double) * max_iter));
-        CK(cudaMalloc(&G->rsq_hist, sizeof(double) * max_iter));
+        afree(G->change_hist, st);
+        afree(G->res_hist, st);
+        afree(G->rsq_hist, st);
+        CK(cudaMallocAsync(&G->change_hist, sizeof(double) * max_iter, st));
+        CK(cudaMallocAsync(&G->res_hist, sizeof(double) * max_iter, st));
+        CK(cudaMallocAsync(&G->rsq_hist, sizeof(double) * max_iter, st));
+        CK(cudaStreamSynchronize(st));
         G->hist_cap = max_iter;
         G->ws_gen++;
     }
@@ -241,23 +263,24 @@ SweepArgs make_args(gabp_graph *G) {
 }
 
 void release_workspace(gabp_graph *G) {
-    for (int b = 0; b < 3; ++b) cudaFree(G->msg[b]);
-    for (int b = 0; b < 3; ++b) cudaFree(G->agg[b]);
-    for (int b = 0; b < 3; ++b) cudaFree(G->rec[b]);
-    cudaFree(G->xs);
-    cudaFree(G->ps);
+    cudaStream_t st = G->stream;
+    for (int b = 0; b < 3; ++b) afree(G->msg[b], st);
+    for (int b = 0; b < 3; ++b) afree(G->agg[b], st);
+    for (int b = 0; b < 3; ++b) afree(G->rec[b], st);
+    afree(G->xs, st);
+    afree(G->ps, st);
     for (int b = 0; b < 3; ++b) {
-        cudaFree(G->x[b]);
-        cudaFree(G->p[b]);
+        afree(G->x[b], st);
+        afree(G->p[b], st);
     }
-    cudaFree(G->rsq_part);
-    cudaFree(G->ctrl);
+    afree(G->rsq_part, st);
+    afree(G->ctrl, st);
     cudaFreeHost(G->h_ctrl);
     cudaFreeHost(G->h_done);
-    cudaFree(G->change_hist);
-    cudaFree(G->res_hist);
-    cudaFree(G->rsq_hist);
-    cudaFree(G->xhist);
+    afree(G->change_hist, st);
+    afree(G->res_hist, st);
+    afree(G->rsq_hist, st);
+    afree(G->xhist, st);
     if (G->chunk_exec) cudaGraphExecDestroy(G->chunk_exec);
     cudaFree(G->dA);
     for (int b = 0; b < 3; ++b) cudaFree(G->dmsg[b]);
@@ -362,10 +385,10 @@ int solve_setup(gabp_graph *G, const gabp_options_t *opt) {
     const DeviceGraph &g = G->g;
     const int64_t rows = opt->h_means_history ? opt->means_history_rows : 0;
     if (rows != G->xhist_rows) {
-        cudaFree(G->xhist);
+        afree(G->xhist, G->stream);
         G->xhist = nullptr;
         G->xhist_rows = 0;
-        if (rows > 0) CK(cudaMalloc(&G->xhist, sizeof(double) * rows * g.n));
+        if (rows > 0) CK(cudaMallocAsync(&G->xhist, sizeof(double) * rows * g.n, G->stream));
         G->xhist_rows = rows;
         G->ws_gen++;
     }
@@ -564,6 +587,15 @@ gabp_graph *new_graph(int device, int *rc) {
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = gabp::prepare_sweep_kernels();
     if (e == cudaSuccess) e = gabp::prepare_slice_kernels();
+    if (e == cudaSuccess) {
+        // keep freed blocks in the device pool (graphs, workspaces and build scratch are
+        // stream-ordered allocations): no re-mapping on the next build or solve
+        cudaMemPool_t pool;
+        e = cudaDeviceGetDefaultMemPool(&pool, device);
+        uint64_t keep = UINT64_MAX;
+        if (e == cudaSuccess)
+            e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         *rc = fail(GABP_ECUDA, "device %d: %s", device, cudaGetErrorString(e));
@@ -606,7 +638,8 @@ static int create_device_range(int64_t n, int64_t npairs, const double *d_diag,
                                   row_lo, row_hi, G->stream, g_err, sizeof(g_err));
     if (rc != GABP_OK) {
         cudaStreamSynchronize(G->stream);
-        gabp::free_graph(G->g);
+        gabp::free_graph(G->g, G->stream);
+        cudaStreamSynchronize(G->stream);
         cudaStreamDestroy(G->stream);
         delete G;
         return rc;
@@ -638,6 +671,7 @@ int gabp_graph_create_ex(int64_t n, int64_t npairs, const double *h_diag, const 
     *out = nullptr;
     if (n < 1) return fail(GABP_EINVAL, "diag must be a non-empty vector");
     if (npairs < 0) return fail(GABP_EINVAL, "negative pair count");
+    const double t_start = host_ms();
     CK(cudaSetDevice(device));
     cudaStream_t st;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -659,6 +693,7 @@ int gabp_graph_create_ex(int64_t n, int64_t npairs, const double *h_diag, const 
         cudaMemcpyAsync(d_pv, h_pair_v, sizeof(double) * npairs, cudaMemcpyHostToDevice, st);
     }
     e = cudaStreamSynchronize(st);
+    const double t1 = host_ms();
     int rc = GABP_OK;
     if (e != cudaSuccess) {
         rc = fail(GABP_ECUDA, "H2D copy: %s", cudaGetErrorString(e));
@@ -666,6 +701,10 @@ int gabp_graph_create_ex(int64_t n, int64_t npairs, const double *h_diag, const 
         rc = create_device_range(n, npairs, d_diag, d_rhs, d_pi, d_pj, d_pv, row_lo, row_hi,
                                  device, out);
     }
+    if (host_timing())
+        fprintf(stderr, "[gabp] graph_create: staging + H2D %.2f ms, device build %.2f ms "
+                        "(core %.2f on device)\n",
+                t1 - t_start, host_ms() - t1, rc == GABP_OK ? (*out)->g.build_ms : 0.0);
     cudaFreeAsync(buf, st);
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
@@ -709,7 +748,8 @@ static void graph_release(gabp_graph *G) {
     cudaSetDevice(G->device);
     cudaStreamSynchronize(G->stream);
     release_workspace(G);
-    gabp::free_graph(G->g);
+    gabp::free_graph(G->g, G->stream);
+    cudaStreamSynchronize(G->stream);
     cudaStreamDestroy(G->stream);
     delete G;
 }
@@ -1182,10 +1222,20 @@ int gabp_solve_system(int64_t n, int64_t npairs, const double *h_diag, const dou
     int rc = check_options(opt);
     if (rc) return rc;
     gabp_graph_t *G = nullptr;
+    const double t0 = host_ms();
     rc = gabp_graph_create(n, npairs, h_diag, h_rhs, h_pair_i, h_pair_j, h_pair_v, device, &G);
     if (rc) return rc;
-    rc = gabp_solve(G, opt, h_means, h_precs, h_change_hist, h_res_hist, rep);
+    const double t1 = host_ms();
+    double ms = 0.0;
+    rc = run_solve(G, opt, &ms);
+    const double t2 = host_ms();
+    if (!rc) rc = copy_results(G, opt, ms, h_means, h_precs, h_change_hist, h_res_hist, rep);
+    const double t3 = host_ms();
     gabp_graph_destroy(G);
+    if (host_timing())
+        fprintf(stderr, "[gabp] solve_system: create %.2f ms, solve %.2f ms (device %.2f), "
+                        "results %.2f ms, destroy %.2f ms\n",
+                t1 - t0, t2 - t1, ms, t3 - t2, host_ms() - t3);
     return rc;
 }
 

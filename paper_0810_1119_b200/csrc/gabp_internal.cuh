@@ -258,7 +258,7 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
                        const double *d_rhs, const int64_t *d_pi, const int64_t *d_pj,
                        const double *d_pv, int64_t row_lo, int64_t row_hi, cudaStream_t st,
                        char *err, size_t errlen);
-void free_graph(DeviceGraph &g);
+void free_graph(DeviceGraph &g, cudaStream_t st);
 // slice layout of the swept rows (slice.cu); GABP_OK or an error (the tile layout stays)
 int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
 cudaError_t prepare_slice_kernels();
