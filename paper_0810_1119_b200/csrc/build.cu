@@ -26,18 +26,13 @@ enum BuildErr : int { kErrNone = 0, kErrPairRange = 1, kErrZeroValue = 2, kErrDu
                       kErrZeroDiag = 4 };
 
 __global__ void count_kernel(int64_t n, int64_t np, const int64_t *pi, const int64_t *pj,
-                             const double *pv, uint32_t *deg, int *err,
+                             uint32_t *deg, int *err,
                              unsigned long long *err_at) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np;
          p += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = pi[p], j = pj[p];
         if (!(0 <= i && i < j && j < n)) {
             atomicCAS(err, 0, (int)kErrPairRange);
-            atomicMin(err_at, (unsigned long long)p);
-            continue;
-        }
-        if (pv[p] == 0.0) {
-            atomicCAS(err, 0, (int)kErrZeroValue);
             atomicMin(err_at, (unsigned long long)p);
             continue;
         }
@@ -80,8 +75,11 @@ __global__ void pos_kernel(int64_t E, const uint32_t *scol, const uint32_t *spl,
     }
 }
 
+// (the explicit-zero check of the pair values lives here: the values may still be in
+// flight from the host while the structural passes run)
 __global__ void edge_kernel(int64_t E, const uint32_t *scol, const uint32_t *spl,
-                            const uint32_t *pos, const double *pv, EdgeRec *er) {
+                            const uint32_t *pos, const double *pv, EdgeRec *er, int *err,
+                            unsigned long long *err_at) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
          e += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t pl = spl[e];
@@ -90,6 +88,10 @@ __global__ void edge_kernel(int64_t E, const uint32_t *scol, const uint32_t *spl
         r.col = scol[e];
         r.coeff = pv[pl >> 1];
         er[e] = r;
+        if (r.coeff == 0.0 && !(pl & 1u)) {
+            atomicCAS(err, 0, (int)kErrZeroValue);
+            atomicMin(err_at, (unsigned long long)(pl >> 1));
+        }
     }
 }
 
@@ -251,7 +253,8 @@ int compute_priors(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
 int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *d_diag,
                        const double *d_rhs, const int64_t *d_pi, const int64_t *d_pj,
                        const double *d_pv, int64_t row_lo, int64_t row_hi, cudaStream_t st,
-                       char *err, size_t errlen) {
+                       char *err, size_t errlen, cudaEvent_t idx_ready, cudaEvent_t val_ready) {
+    if (idx_ready) BCHECK(cudaStreamWaitEvent(st, idx_ready, 0));
     if (row_lo < 0 || row_hi > n || row_lo >= row_hi) {
         row_lo = 0;
         row_hi = n;
@@ -283,8 +286,6 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
     BCHECK(cudaMemsetAsync(g.diag + n, 0, sizeof(double) * kNodePad, st));
     BCHECK(cudaMemsetAsync(g.rhs + n, 0, sizeof(double) * kNodePad, st));
     BCHECK(cudaMemsetAsync(g.prior_num + n, 0, sizeof(double) * kNodePad, st));
-    BCHECK(cudaMemcpyAsync(g.diag, d_diag, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-    BCHECK(cudaMemcpyAsync(g.rhs, d_rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     BCHECK(cudaMallocAsync(&g.row_ptr, sizeof(uint32_t) * (n + 1 + kNodePad), st));
     BCHECK(cudaMemsetAsync(g.row_ptr + n + 1, 0, sizeof(uint32_t) * kNodePad, st));
     BCHECK(cudaMallocAsync(&g.er, sizeof(EdgeRec) * (E > 0 ? E : 1), st));
@@ -302,8 +303,7 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
     BCHECK(cudaMallocAsync(&deg, sizeof(uint32_t) * (n + 1), st));
     BCHECK(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (n + 1), st));
     if (npairs > 0) {
-        count_kernel<<<grid_for(npairs), 256, 0, st>>>(n, npairs, d_pi, d_pj, d_pv, deg, d_err,
-                                                       d_at);
+        count_kernel<<<grid_for(npairs), 256, 0, st>>>(n, npairs, d_pi, d_pj, deg, d_err, d_at);
         BCHECK(cudaGetLastError());
     }
     // 2. row_ptr
@@ -374,7 +374,8 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
         uint32_t *pos = tpl;  // reuse
         pos_kernel<<<grid_for(E), 256, 0, st>>>(E, scol, spl, d_pi, d_pj, pos, d_err, d_at);
         BCHECK(cudaGetLastError());
-        edge_kernel<<<grid_for(E), 256, 0, st>>>(E, scol, spl, pos, d_pv, g.er);
+        if (val_ready) BCHECK(cudaStreamWaitEvent(st, val_ready, 0));
+        edge_kernel<<<grid_for(E), 256, 0, st>>>(E, scol, spl, pos, d_pv, g.er, d_err, d_at);
         BCHECK(cudaGetLastError());
         cudaFreeAsync(scol, st);
         cudaFreeAsync(spl, st);
@@ -420,6 +421,9 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
         BCHECK(cudaGetLastError());
         cudaFreeAsync(idx, st);
     }
+    if (val_ready) BCHECK(cudaStreamWaitEvent(st, val_ready, 0));  // (again if E > 0: harmless)
+    BCHECK(cudaMemcpyAsync(g.diag, d_diag, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    BCHECK(cudaMemcpyAsync(g.rhs, d_rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     cudaFreeAsync(tmp, st);
     cudaFreeAsync(deg, st);
     int h_err = 0;
@@ -437,6 +441,10 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
     if (h_err == kErrDup) {
         snprintf(err, errlen, "duplicate off-diagonal pair (pair index %llu)", h_at);
         return GABP_EDUP;
+    }
+    if (h_err == kErrZeroValue) {
+        snprintf(err, errlen, "explicit zero stored at pair %llu", h_at);
+        return GABP_EINVAL;
     }
     if (g.max_degree <= kSliceMaxDegree) {
         const int rc = build_slices(g, st, err, errlen);

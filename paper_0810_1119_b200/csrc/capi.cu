@@ -14,6 +14,7 @@
 #include <nccl.h>  // types only: libnccl is loaded at run time (gabp_dist_attach)
 
 #include <atomic>
+#include <mutex>
 #include <vector>
 
 #include "gabp_internal.cuh"
@@ -74,6 +75,12 @@ struct DistState {
     double *d_stats = nullptr;                          // [0..4] max, [5] sum
 };
 
+// pinned host mirror of a graph's controller and poll flags (capi.cu pinned_get)
+struct PinnedBlock {
+    Ctrl ctrl;
+    int32_t done[4];
+};
+
 struct gabp_graph {
     // owner handle + one per live gabp_state: destruction order between a graph and
     // its states does not matter (Python GC may finalise either first)
@@ -92,6 +99,9 @@ struct gabp_graph {
     Ctrl *ctrl = nullptr;
     Ctrl *h_ctrl = nullptr;          // pinned mirror
     int32_t *h_done = nullptr;       // pinned, 2 poll slots
+    char *ws_base = nullptr;         // the solve workspace block (msg ... ctrl)
+    size_t ws_bytes = 0;
+    PinnedBlock *pin = nullptr;
     double *change_hist = nullptr, *res_hist = nullptr, *rsq_hist = nullptr;
     int64_t hist_cap = 0;
     uint64_t ws_gen = 0;
@@ -176,46 +186,141 @@ int64_t msg_slots(const DeviceGraph &g) {
     return m > 0 ? m : 1;
 }
 
-int ensure_workspace(gabp_graph *G, int64_t max_iter) {
-    // stream-ordered allocations from the retained device pool: a repeated solve or a new
-    // graph of similar size reuses cached blocks instead of mapping fresh memory
+// Pinned host mirrors (controller + poll flags) come from a process-wide slab: a
+// cudaMallocHost per graph costs about a millisecond of page locking.
+std::mutex g_pin_mu;
+std::vector<PinnedBlock *> g_pin_free;
+
+PinnedBlock *pinned_get() {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (g_pin_free.empty()) {
+        constexpr int kPer = 64;
+        PinnedBlock *slab = nullptr;
+        if (cudaMallocHost(&slab, sizeof(PinnedBlock) * kPer) != cudaSuccess) return nullptr;
+        for (int k = 0; k < kPer; ++k) g_pin_free.push_back(slab + k);  // never returned
+    }
+    PinnedBlock *b = g_pin_free.back();
+    g_pin_free.pop_back();
+    return b;
+}
+void pinned_put(PinnedBlock *b) {
+    if (!b) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(b);
+}
+
+// Spare large blocks (a released solve workspace, a graph-create staging buffer) are
+// kept per device and handed to the next request of a similar size.  Taking them from the
+// pool instead costs a re-mapping of the whole range whenever smaller allocations have
+// been carved out of the freed block in between (about 1 ms per GB).
+struct SpareBlock {
+    int device = -1;
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+std::mutex g_spare_mu;
+SpareBlock g_spare[2][16];  // [kind][slot]: 0 workspace, 1 staging
+
+void *spare_take(int kind, int device, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_spare_mu);
+    for (auto &b : g_spare[kind])
+        if (b.p && b.device == device && b.bytes >= bytes && b.bytes <= 2 * bytes + (64u << 20)) {
+            void *p = b.p;
+            b.p = nullptr;
+            return p;
+        }
+    return nullptr;
+}
+// p must be idle (its stream synchronized); returns false when no slot is free
+bool spare_keep(int kind, int device, void *p, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_spare_mu);
+    for (auto &b : g_spare[kind])
+        if (!b.p) {
+            b.device = device;
+            b.p = p;
+            b.bytes = bytes;
+            return true;
+        }
+    return false;
+}
+
+// One stream-ordered block from the retained device pool holds the whole solve workspace
+// (a repeated solve, or a new graph of similar size, reuses the cached block).
+struct Carve {
+    char *base;
+    size_t off = 0;
+    template <class T>
+    T *take(int64_t count) {
+        off = (off + 255) & ~(size_t)255;
+        T *p = reinterpret_cast<T *>(base ? base + off : nullptr);
+        off += sizeof(T) * (size_t)(count > 0 ? count : 1);
+        return p;
+    }
+};
+
+void carve_workspace(gabp_graph *G, Carve &c) {
     const DeviceGraph &g = G->g;
-    cudaStream_t st = G->stream;
     const int64_t E = msg_slots(g);
     // node arrays: row order (tiles) or position order (slices, padding lanes + halo)
     const int64_t nn = (g.n > g.npos ? g.n : g.npos) + gabp::kNodePad;
-    if (!G->msg[0]) {
-        for (int b = 0; b < 3; ++b) CK(cudaMallocAsync(&G->msg[b], sizeof(double2) * E, st));
-        for (int b = 0; b < 3; ++b) CK(cudaMallocAsync(&G->agg[b], sizeof(double2) * nn, st));
-        for (int b = 0; b < 3; ++b) {
-            CK(cudaMallocAsync(&G->x[b], sizeof(double) * nn, st));
-            CK(cudaMallocAsync(&G->p[b], sizeof(double) * nn, st));
-            CK(cudaMemsetAsync(G->x[b], 0, sizeof(double) * nn, st));
-        }
-        if (g.nslices > 0)
-            for (int b = 0; b < 3; ++b)
-                CK(cudaMallocAsync(&G->rec[b], sizeof(gabp::NodeState) * (g.npos + gabp::kNodePad), st));
-        CK(cudaMallocAsync(&G->xs, sizeof(double) * (g.n + 1), st));
-        CK(cudaMallocAsync(&G->ps, sizeof(double) * (g.n + 1), st));
-        // one partial per CTA of a persistent launch (either layout)
-        CK(cudaMallocAsync(&G->rsq_part, sizeof(double) * (g.ntiles > 8192 ? g.ntiles : 8192), st));
-        CK(cudaMallocAsync(&G->ctrl, sizeof(Ctrl), st));
-        CK(cudaMallocHost(&G->h_ctrl, sizeof(Ctrl)));
-        CK(cudaMallocHost(&G->h_done, sizeof(int32_t) * 4));
-        for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&G->ev[k]));
+    for (int b = 0; b < 3; ++b) G->msg[b] = c.take<double2>(E);
+    for (int b = 0; b < 3; ++b) G->agg[b] = c.take<double2>(nn);
+    for (int b = 0; b < 3; ++b) {
+        G->x[b] = c.take<double>(nn);
+        G->p[b] = c.take<double>(nn);
+    }
+    for (int b = 0; b < 3; ++b)
+        G->rec[b] = g.nslices > 0 ? c.take<gabp::NodeState>(g.npos + gabp::kNodePad) : nullptr;
+    G->xs = c.take<double>(g.n + 1);
+    G->ps = c.take<double>(g.n + 1);
+    // one partial per CTA of a persistent launch (either layout)
+    G->rsq_part = c.take<double>(g.ntiles > 8192 ? g.ntiles : 8192);
+    G->ctrl = c.take<Ctrl>(1);
+}
+
+int ensure_workspace(gabp_graph *G, int64_t max_iter) {
+    cudaStream_t st = G->stream;
+    const DeviceGraph &g = G->g;
+    const double tw0 = host_ms();
+    double tw1 = tw0, tw2 = tw0;
+    if (!G->ws_base) {
+        Carve size{nullptr};
+        carve_workspace(G, size);
+        G->ws_base = static_cast<char *>(spare_take(0, G->device, size.off));
+        if (!G->ws_base) CK(cudaMallocAsync(&G->ws_base, size.off, st));
+        G->ws_bytes = size.off;
+        tw1 = host_ms();
+        Carve c{G->ws_base};
+        carve_workspace(G, c);
+        const int64_t nn = (g.n > g.npos ? g.n : g.npos) + gabp::kNodePad;
+        for (int b = 0; b < 3; ++b) CK(cudaMemsetAsync(G->x[b], 0, sizeof(double) * nn, st));
+        G->pin = pinned_get();
+        if (!G->pin) return fail(GABP_ENOMEM, "pinned host allocation failed");
+        G->h_ctrl = &G->pin->ctrl;
+        G->h_done = G->pin->done;
+        for (int k = 0; k < 4; ++k) CK(cudaEventCreateWithFlags(&G->ev[k], cudaEventDefault));
+        tw2 = host_ms();
         CK(cudaStreamSynchronize(st));  // usable from any stream from here on
         G->ws_gen++;
     }
     if (max_iter > G->hist_cap) {
         afree(G->change_hist, st);
-        afree(G->res_hist, st);
-        afree(G->rsq_hist, st);
-        CK(cudaMallocAsync(&G->change_hist, sizeof(double) * max_iter, st));
-        CK(cudaMallocAsync(&G->res_hist, sizeof(double) * max_iter, st));
-        CK(cudaMallocAsync(&G->rsq_hist, sizeof(double) * max_iter, st));
+        CK(cudaMallocAsync(&G->change_hist, sizeof(double) * 3 * max_iter, st));
+        G->res_hist = G->change_hist + max_iter;
+        G->rsq_hist = G->change_hist + 2 * max_iter;
         CK(cudaStreamSynchronize(st));
         G->hist_cap = max_iter;
         G->ws_gen++;
+    }
+    if (host_timing()) {
+        cudaMemPool_t pool;
+        cudaDeviceGetMemPool(&pool, G->device);
+        uint64_t res = 0, used = 0;
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        fprintf(stderr, "[gabp] workspace: alloc %.2f ms, carve+memset+pin+events %.2f ms, "
+                        "syncs + history %.2f ms; pool reserved %.2f GB used %.2f GB\n",
+                tw1 - tw0, tw2 - tw1, host_ms() - tw2, res / 1e9, used / 1e9);
     }
     return GABP_OK;
 }
@@ -249,7 +354,6 @@ SweepArgs make_args(gabp_graph *G) {
     a.msg_lag = 0;
     for (int b = 0; b < 3; ++b) a.rec[b] = G->rec[b];
     a.slice_variant = g.slice_variant;
-    a.slice_unit = g.slice_unit;
     a.slice_path = 0;
     a.nslices = g.nslices;
     a.slice_info = g.slice_info;
@@ -264,23 +368,11 @@ SweepArgs make_args(gabp_graph *G) {
 
 void release_workspace(gabp_graph *G) {
     cudaStream_t st = G->stream;
-    for (int b = 0; b < 3; ++b) afree(G->msg[b], st);
-    for (int b = 0; b < 3; ++b) afree(G->agg[b], st);
-    for (int b = 0; b < 3; ++b) afree(G->rec[b], st);
-    afree(G->xs, st);
-    afree(G->ps, st);
-    for (int b = 0; b < 3; ++b) {
-        afree(G->x[b], st);
-        afree(G->p[b], st);
-    }
-    afree(G->rsq_part, st);
-    afree(G->ctrl, st);
-    cudaFreeHost(G->h_ctrl);
-    cudaFreeHost(G->h_done);
-    afree(G->change_hist, st);
-    afree(G->res_hist, st);
-    afree(G->rsq_hist, st);
+    // (graph_release synchronized the stream: the block is idle)
+    if (G->ws_base && !spare_keep(0, G->device, G->ws_base, G->ws_bytes)) afree(G->ws_base, st);
+    afree(G->change_hist, st);  // (res_hist, rsq_hist live in the same block)
     afree(G->xhist, st);
+    pinned_put(G->pin);
     if (G->chunk_exec) cudaGraphExecDestroy(G->chunk_exec);
     cudaFree(G->dA);
     for (int b = 0; b < 3; ++b) cudaFree(G->dmsg[b]);
@@ -488,6 +580,7 @@ SweepArgs make_dist_args(gabp_graph *G) {
 
 // Runs the device-driven loop; on return G->h_ctrl holds the final controller.
 int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
+    const double t_setup = host_ms();
     int rc = solve_setup(G, opt);
     if (rc) return rc;
     cudaStream_t st = G->stream;
@@ -546,8 +639,12 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
     const int gather = pick_gather(G, opt);
     G->slice_order = gather == gabp::kGatherSlice;
     const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
+    const double tc0 = host_ms();
     rc = get_chunk_exec(G, sched, gather, C);
     if (rc) return rc;
+    if (host_timing())
+        fprintf(stderr, "[gabp] run_solve: setup %.2f ms, chunk graph (%d sweeps) %.2f ms\n",
+                tc0 - t_setup, C, host_ms() - tc0);
     SweepArgs a = make_args(G);
     CK(cudaEventRecord(G->ev[2], st));
     while (launched < total) {
@@ -628,14 +725,17 @@ int gabp_device_count(int32_t *count) {
 static int create_device_range(int64_t n, int64_t npairs, const double *d_diag,
                                const double *d_rhs, const int64_t *d_pair_i,
                                const int64_t *d_pair_j, const double *d_pair_v, int64_t row_lo,
-                               int64_t row_hi, int32_t device, gabp_graph_t **out) {
+                               int64_t row_hi, int32_t device, gabp_graph_t **out,
+                               cudaEvent_t idx_ready = nullptr,
+                               cudaEvent_t val_ready = nullptr) {
     if (!out) return fail(GABP_EINVAL, "out must not be NULL");
     *out = nullptr;
     int rc;
     gabp_graph *G = new_graph(device, &rc);
     if (!G) return rc;
     rc = gabp::build_graph_device(G->g, n, npairs, d_diag, d_rhs, d_pair_i, d_pair_j, d_pair_v,
-                                  row_lo, row_hi, G->stream, g_err, sizeof(g_err));
+                                  row_lo, row_hi, G->stream, g_err, sizeof(g_err), idx_ready,
+                                  val_ready);
     if (rc != GABP_OK) {
         cudaStreamSynchronize(G->stream);
         gabp::free_graph(G->g, G->stream);
@@ -673,41 +773,61 @@ int gabp_graph_create_ex(int64_t n, int64_t npairs, const double *h_diag, const 
     if (npairs < 0) return fail(GABP_EINVAL, "negative pair count");
     const double t_start = host_ms();
     CK(cudaSetDevice(device));
-    cudaStream_t st;
+    // Two copy streams: the pair indices first (the structural passes of the build -- degree
+    // count, scan, scatter, row sort -- need only them), the values and node vectors
+    // behind them on a second stream; the build waits on their events.
+    cudaStream_t st, sv;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&sv, cudaStreamNonBlocking));
+    cudaEvent_t ev_buf, ev_idx, ev_val;
+    CK(cudaEventCreateWithFlags(&ev_buf, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_idx, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_val, cudaEventDisableTiming));
     const size_t nb = sizeof(double) * n, pb = sizeof(int64_t) * (npairs > 0 ? npairs : 1);
-    char *buf = nullptr;
-    cudaError_t e = cudaMallocAsync(&buf, 2 * nb + 3 * pb, st);
+    const size_t sbytes = 2 * nb + 3 * pb;
+    char *buf = static_cast<char *>(spare_take(1, device, sbytes));
+    cudaError_t e = buf ? cudaSuccess : cudaMallocAsync(&buf, sbytes, st);
     if (e != cudaSuccess) {
         cudaStreamDestroy(st);
+        cudaStreamDestroy(sv);
         return fail(GABP_ENOMEM, "staging allocation: %s", cudaGetErrorString(e));
     }
+    cudaEventRecord(ev_buf, st);
+    cudaStreamWaitEvent(sv, ev_buf, 0);
     double *d_diag = (double *)buf, *d_rhs = (double *)(buf + nb);
     int64_t *d_pi = (int64_t *)(buf + 2 * nb), *d_pj = (int64_t *)(buf + 2 * nb + pb);
     double *d_pv = (double *)(buf + 2 * nb + 2 * pb);
-    cudaMemcpyAsync(d_diag, h_diag, nb, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d_rhs, h_rhs, nb, cudaMemcpyHostToDevice, st);
     if (npairs > 0) {
         cudaMemcpyAsync(d_pi, h_pair_i, sizeof(int64_t) * npairs, cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(d_pj, h_pair_j, sizeof(int64_t) * npairs, cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(d_pv, h_pair_v, sizeof(double) * npairs, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(d_pv, h_pair_v, sizeof(double) * npairs, cudaMemcpyHostToDevice, sv);
     }
-    e = cudaStreamSynchronize(st);
-    const double t1 = host_ms();
+    cudaMemcpyAsync(d_diag, h_diag, nb, cudaMemcpyHostToDevice, sv);
+    cudaMemcpyAsync(d_rhs, h_rhs, nb, cudaMemcpyHostToDevice, sv);
+    cudaEventRecord(ev_idx, st);
+    e = cudaEventRecord(ev_val, sv);
     int rc = GABP_OK;
     if (e != cudaSuccess) {
         rc = fail(GABP_ECUDA, "H2D copy: %s", cudaGetErrorString(e));
     } else {
         rc = create_device_range(n, npairs, d_diag, d_rhs, d_pi, d_pj, d_pv, row_lo, row_hi,
-                                 device, out);
+                                 device, out, ev_idx, ev_val);
     }
+    const cudaError_t e1 = cudaStreamSynchronize(st), e2 = cudaStreamSynchronize(sv);
+    if (rc == GABP_OK && (e1 != cudaSuccess || e2 != cudaSuccess))
+        rc = fail(GABP_ECUDA, "H2D copy: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
     if (host_timing())
-        fprintf(stderr, "[gabp] graph_create: staging + H2D %.2f ms, device build %.2f ms "
-                        "(core %.2f on device)\n",
-                t1 - t_start, host_ms() - t1, rc == GABP_OK ? (*out)->g.build_ms : 0.0);
-    cudaFreeAsync(buf, st);
-    cudaStreamSynchronize(st);
+        fprintf(stderr, "[gabp] graph_create: H2D + device build %.2f ms (core %.2f on device)\n",
+                host_ms() - t_start, rc == GABP_OK ? (*out)->g.build_ms : 0.0);
+    if (!spare_keep(1, device, buf, sbytes)) {  // both streams and the build are idle
+        cudaFreeAsync(buf, st);
+        cudaStreamSynchronize(st);
+    }
+    cudaEventDestroy(ev_buf);
+    cudaEventDestroy(ev_idx);
+    cudaEventDestroy(ev_val);
     cudaStreamDestroy(st);
+    cudaStreamDestroy(sv);
     return rc;
 }
 

@@ -137,12 +137,11 @@ struct SweepArgs {
     double *dstats;
     int msg_lag;        // message statistics of a launch refer to sweep s - msg_lag
     NodeState *rec[3];  // slice path: node state of S_t in rec[t % 3] (position order)
-    int slice_variant;  // slice kernel: 0 register batches, 1 cp.async ring, 2 TMA ring
-    int slice_unit;     // TMA ring: slices per dynamically claimed work unit
+    int slice_variant;  // slice kernel: 0 register batches, 1 cp.async ring, 2 group TMA ring
     int slice_path;     // this launch family is the slice path (halo records)
     // slice layout (slice.cu): lane-per-row broadcast solve, nodes in position order
     int64_t nslices;
-    const uint2 *slice_info;   // {slot base, width} per slice of 32 rows
+    const uint2 *slice_info;   // {slot base, width} per slice of 32 rows (group width)
     const uint32_t *sdeg;      // degree per position
     const uint32_t *srow;      // local row per position (~0: padding / halo)
     const double2 *snd;        // {A_ii, A_ii mu_ii} per position
@@ -240,8 +239,7 @@ struct DeviceGraph {
     int64_t row_lo = 0, row_hi = 0;  // swept rows
     // slice layout (build_slices, slice.cu); nslices == 0 when not built
     int64_t nslices = 0, nslots = 0, npos = 0;
-    int slice_variant = 0;      // 0: register batches, 1: cp.async ring, 2: TMA ring
-    int slice_unit = 1;         // TMA ring: slices per work unit (>= ~8 chunks per claim)
+    int slice_variant = 2;      // 0: register batches, 1: cp.async ring, 2: group TMA ring
     uint2 *slice_info = nullptr;
     uint32_t *pos = nullptr;    // local row -> position
     uint32_t *srow = nullptr, *sdeg = nullptr;
@@ -257,7 +255,8 @@ struct DeviceGraph {
 int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *d_diag,
                        const double *d_rhs, const int64_t *d_pi, const int64_t *d_pj,
                        const double *d_pv, int64_t row_lo, int64_t row_hi, cudaStream_t st,
-                       char *err, size_t errlen);
+                       char *err, size_t errlen, cudaEvent_t idx_ready = nullptr,
+                       cudaEvent_t val_ready = nullptr);
 void free_graph(DeviceGraph &g, cudaStream_t st);
 // slice layout of the swept rows (slice.cu); GABP_OK or an error (the tile layout stays)
 int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
@@ -268,7 +267,7 @@ cudaError_t slice_to_rows(const DeviceGraph &g, int64_t lo, int64_t cnt, const d
                           int stride, double *out, cudaStream_t st);
 cudaError_t slice_map_index(const DeviceGraph &g, uint32_t *idx, int64_t cnt, cudaStream_t st);
 constexpr int64_t kSliceMaxDegree = 4096;  // rows longer than this: tile layout only
-constexpr int64_t kSlotPad = 256;          // slot arrays are padded by 8 batches of 32
+constexpr int64_t kSlotPad = 4096;         // slot arrays are padded by 8 group columns
 int compute_priors(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
 
 }  // namespace gabp

@@ -2,13 +2,16 @@
 //
 // Layout (build_slices below).  The swept rows are stably
 // sorted by degree (descending) inside windows of kSortWin rows and cut into slices of 32
-// rows; row r of the sort sits at "position" p = 32 * slice + lane.  Slice s has width
-// w_s = its largest degree, and the q-th edge (ascending neighbour, = reference edge order)
-// of the row in lane l lives at slot base_s + 32 q + l.  Nodes are numbered by position
-// on this path (x, p and the aggregates live in position order; scol holds the neighbour's
-// position; a rank's halo rows take positions after the owned ones), so every own-row and
-// every per-edge stream is a fully coalesced warp access, and only the neighbour gathers
-// are random (node arrays, L2-resident for the headline graph).
+// rows; row r of the sort sits at "position" p = 32 * slice + lane.  kGroup consecutive
+// slices form a group of width w_g = its largest degree (the first row's, as the rows are
+// sorted), and the q-th edge (ascending neighbour, = reference edge order) of the row in
+// lane l of slice s lives at slot base_s + kStride q + l, base_s = gbase_g + 32 (s % kGroup):
+// column q of a group is kStride = 32 kGroup contiguous slots.  Nodes are numbered by
+// position on this path (x, p and the aggregates live in position order; scol holds the
+// neighbour's position; a rank's halo rows take positions after the owned ones), so every
+// own-row and every per-edge stream is a fully coalesced warp access (and a group chunk one
+// bulk copy per stream), and only the neighbour gathers are random (node arrays,
+// L2-resident for the headline graph).
 //
 // State on this path: per edge slot the INCOMING message I_ij^{(t)} = m_ji^{(t)} = (P, mu)
 // of S_t (the term row i sums), a ring of three; per node the aggregate {P_i, P_i mu~_i}
@@ -27,7 +30,7 @@
 // streaming pass; no staging, no CTA barrier.
 // Launch 1 sees I^{(0)} = 0 (solve_setup zeroes the ring); launch 2 uses m^{(0)} = 0.
 #include <cub/device/device_scan.cuh>
-#include <cub/device/device_segmented_radix_sort.cuh>
+#include <cub/device/device_radix_sort.cuh>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -35,6 +38,12 @@
 
 namespace gabp {
 namespace {
+
+#ifndef GABP_SLICE_GROUP
+#define GABP_SLICE_GROUP 15
+#endif
+constexpr int kGroup = GABP_SLICE_GROUP;  // slices per group (consumer warps per CTA)
+constexpr int kStride = 32 * kGroup;      // slots per group column
 
 // ---- shared pieces -----------------------------------------------------------------------
 struct SliceSmem {
@@ -47,21 +56,18 @@ struct SliceSmem {
 // launch when an operand leaves its range (the exact twin then redoes the sweep): no call
 // in the hot loop, so no ABI-preserved registers.
 template <bool EXACT>
-__device__ __forceinline__ double qdiv(double a, double b, unsigned &slow) {
+__device__ __forceinline__ double qdiv(double a, double b, Stats &st) {
     if (EXACT) return a / b;
-    bool ok;
-    const double q = ddiv_fast(a, b, ok);
-    slow |= ok ? 0u : 1u;
-    return q;
+    return ddiv_fast_acc(a, b, st.dr);
 }
 
 // msg(agg, m): the outgoing message of an edge from its row aggregate and the incoming
 // pair, as (P, mu) (solver.py:249-257)
 template <bool EXACT>
 __device__ __forceinline__ void edge_msg(double c, double pe, double num, double &P, double &mu,
-                                         unsigned &slow) {
-    P = qdiv<EXACT>(-c * c, pe, slow);
-    mu = qdiv<EXACT>(num, c, slow);
+                                         Stats &st) {
+    P = qdiv<EXACT>(-c * c, pe, st);
+    mu = qdiv<EXACT>(num, c, st);
 }
 
 // CSR edge id of the message j -> i held in slot q of position p (exact launch only)
@@ -85,8 +91,7 @@ template <bool EXACT>
 __device__ __forceinline__ void msg_stats(Stats &st, const SweepArgs &a, double ip, double im,
                                           double2 i2, double pe, int64_t p, uint32_t q) {
     const double d1 = fabs(ip - i2.x), d2 = fabs(im - i2.y);
-    st.chg = d1 > st.chg ? d1 : st.chg;
-    st.chg = d2 > st.chg ? d2 : st.chg;
+    st.chg = fmax(st.chg, fmax(d1, d2));  // NaN differences ignored, as '>' ignores them
     if (!(fabs(ip) <= st.lim) || !(fabs(im) <= st.lim)) st.out_of_range = 1u;
     if (pe == 0.0) {
         if (EXACT)
@@ -101,7 +106,7 @@ template <int PH, bool EXACT>
 __device__ __forceinline__ void node_done(Stats &st, const SweepArgs &a, NodeState *rec1,
                                           double *xh, int64_t p, double sp, double sn, double y,
                                           double rhs_i) {
-    const double xi = qdiv<EXACT>(sn, sp, st.redo);
+    const double xi = qdiv<EXACT>(sn, sp, st);
     if (!(fabs(xi) <= DBL_MAX)) st.means_bad = 1u;
     if (xh) xh[__ldg(a.srow + p)] = xi;
     if (sp == 0.0) {
@@ -204,7 +209,7 @@ __device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, S
         const uint32_t base = si.x + lane, w = si.y;
         uint32_t coln[kUL];  // scol of the next batch, loaded one batch ahead
 #pragma unroll
-        for (int u = 0; u < kUL; ++u) coln[u] = ldcs_u32(a.scol + base + 32u * u);
+        for (int u = 0; u < kUL; ++u) coln[u] = ldcs_u32(a.scol + base + (uint32_t)kStride * u);
         for (uint32_t q0 = 0; q0 < w; q0 += kUL) {
             double c[kUL];
             uint32_t col[kUL];
@@ -216,9 +221,9 @@ __device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, S
             for (int u = 0; u < kUL; ++u) ld_node(r.g2 + col[u], gP[u], gN[u], gx[u]);
 #pragma unroll
             for (int u = 0; u < kUL; ++u) {
-                const uint32_t slot = base + 32u * (q0 + u);
+                const uint32_t slot = base + (uint32_t)kStride * (q0 + u);
                 c[u] = ldcs_f64(a.scoef + slot);
-                coln[u] = ldcs_u32(a.scol + slot + 32u * kUL);  // in bounds: slot padding
+                coln[u] = ldcs_u32(a.scol + slot + (uint32_t)kStride * kUL);  // in bounds: padding
                 if (PH == 3) {
                     i2[u] = ldcs_f64x2(r.I2 + slot);
                     i3[u] = ldcs_f64x2(r.I3 + slot);
@@ -237,7 +242,7 @@ __device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, S
                 if (PH == 3) {  // own outgoing message of sweep s-2
                     const double pe2 = v ? a3.x - i3[u].x : 1.0;
                     const double nu2 = v ? a3.y - i3[u].x * i3[u].y : 1.0;
-                    edge_msg<EXACT>(c[u], pe2, nu2, m2p[u], m2m[u], st.redo);
+                    edge_msg<EXACT>(c[u], pe2, nu2, m2p[u], m2m[u], st);
                 }
             }
 #pragma unroll
@@ -245,7 +250,7 @@ __device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, S
                 const bool v = q0 + u < d;
                 pe[u] = v ? gP[u] - m2p[u] : 1.0;
                 const double num = v ? gN[u] - m2p[u] * m2m[u] : 1.0;
-                edge_msg<EXACT>(c[u], pe[u], num, ip[u], im[u], st.redo);
+                edge_msg<EXACT>(c[u], pe[u], num, ip[u], im[u], st);
             }
 #pragma unroll
             for (int u = 0; u < kUL; ++u) {
@@ -254,7 +259,7 @@ __device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, S
                     sp = sp + ip[u];
                     sn = sn + ip[u] * im[u];  // (prec * mean), solver.py:243
                     if (PH == 3) y = y + c[u] * gx[u];
-                    __stcs(r.I1 + base + 32u * q, make_double2(ip[u], im[u]));
+                    __stcs(r.I1 + base + (uint32_t)kStride * q, make_double2(ip[u], im[u]));
                     msg_stats<EXACT>(st, a, ip[u], im[u], i2[u], pe[u], p, q);
                 }
             }
@@ -382,7 +387,7 @@ __device__ __forceinline__ void issue_item(WarpStage &S, const uint32_t (&col)[k
     for (int u = 0; u < kUP; ++u) {
         const uint32_t q = c.b * kUP + u;
         const bool v = q < c.w;
-        const uint32_t slot = c.base + lane + 32u * q;
+        const uint32_t slot = c.base + lane + (uint32_t)kStride * q;
         const uint32_t j = col[u][lane];
         cpa8(&S.c[u][lane], a.scoef + slot, v);
         cpa16(&S.ag[u][lane], r.g2 + j, v);
@@ -400,7 +405,7 @@ __device__ __forceinline__ void issue_col(uint32_t (&col)[kUP][32], const Cursor
 #pragma unroll
     for (int u = 0; u < kUP; ++u) {
         const uint32_t q = c.b * kUP + u;
-        cpa4(&col[u][lane], a.scol + c.base + lane + 32u * q, q < c.w);
+        cpa4(&col[u][lane], a.scol + c.base + lane + (uint32_t)kStride * q, q < c.w);
     }
 }
 
@@ -468,7 +473,7 @@ __device__ __forceinline__ void slice_sweep_pipe(const SweepArgs &a, int64_t s, 
                 const double2 i3 = S.i3[u][lane];
                 const double pe2 = v ? a3.x - i3.x : 1.0;
                 const double nu2 = v ? a3.y - i3.x * i3.y : 1.0;
-                edge_msg<EXACT>(c[u], pe2, nu2, m2p[u], m2m[u], st.redo);
+                edge_msg<EXACT>(c[u], pe2, nu2, m2p[u], m2m[u], st);
             }
         }
 #pragma unroll
@@ -477,7 +482,7 @@ __device__ __forceinline__ void slice_sweep_pipe(const SweepArgs &a, int64_t s, 
             const double2 ag = S.ag[u][lane];
             pe[u] = v ? ag.x - m2p[u] : 1.0;
             const double num = v ? ag.y - m2p[u] * m2m[u] : 1.0;
-            edge_msg<EXACT>(c[u], pe[u], num, ip[u], im[u], st.redo);
+            edge_msg<EXACT>(c[u], pe[u], num, ip[u], im[u], st);
         }
         const int64_t p = C.sl * 32 + lane;
 #pragma unroll
@@ -487,7 +492,7 @@ __device__ __forceinline__ void slice_sweep_pipe(const SweepArgs &a, int64_t s, 
                 sp = sp + ip[u];
                 sn = sn + ip[u] * im[u];  // (prec * mean), solver.py:243
                 if (PH == 3) y = y + c[u] * S.xg[u][lane];
-                __stcs(r.I1 + C.base + lane + 32u * q, make_double2(ip[u], im[u]));
+                __stcs(r.I1 + C.base + lane + (uint32_t)kStride * q, make_double2(ip[u], im[u]));
                 const double2 i2 = PH == 3 ? S.i2[u][lane] : make_double2(0.0, 0.0);
                 msg_stats<EXACT>(st, a, ip[u], im[u], i2, pe[u], p, q);
             }
@@ -499,52 +504,49 @@ __device__ __forceinline__ void slice_sweep_pipe(const SweepArgs &a, int64_t s, 
     cpa_wait<0>();  // nothing may land in the ring after the warp leaves
 }
 
-// ---- variant 2: per-warp TMA ring (any row width) ----------------------------------------
-// Each warp owns a ring of kTS stages in shared memory and walks a sequence of chunks
-// (slice, kTC edge columns).  For chunk k+kTS-1, lane 0 issues 1-D bulk copies (TMA,
-// cp.async.bulk, completion counted on the stage's mbarrier) of the chunk's contiguous
-// slot streams -- scoef, scol, I^{(s-2)}, I^{(s-3)} -- and, on a slice's first chunk, of its
-// 32-row header (node priors, degrees, b, own node states of S_{s-3} and S_{s-2}).  So the
-// DRAM stream is in flight independently of the compute; only the neighbour gathers
-// (L2-resident node states) are register loads, issued one chunk ahead from the landed
-// scol.  Slices are claimed dynamically in units of kslice_unit consecutive slices
-// (Ctrl.work), so every SM streams until the end of the sweep and the machine sweeps the
-// slices roughly in position order (grid neighbours stay L2 hits).
-#ifndef GABP_TMA_C
-#define GABP_TMA_C 2
+// ---- variant 2: CTA-lockstep TMA ring over slice groups (default) ----------------------
+// A CTA owns one slice group (kGroup slices, column q of the group = kStride contiguous
+// slots, see the layout note at the top) at a time: consumer warp w runs slice w of the
+// group, lane per row, and all consumers walk the group's columns together in chunks of
+// kGC columns.  One producer warp claims groups dynamically (Ctrl.work, claims and
+// descriptor loads kept two groups ahead), and for every chunk issues one 1-D bulk copy
+// (TMA, cp.async.bulk) per slot stream -- scoef, scol, I^{(s-2)}, I^{(s-3)}, kGC x kStride
+// slots each -- into a kGS-stage shared-memory ring: full[stage] completes on the copies'
+// byte count, empty[stage] on the kGroup consumers' releases.  So the DRAM stream stays in
+// flight independently of the compute, and a chunk costs a consumer one barrier wait and
+// one release.  Only the neighbour gathers (L2-resident node states) and the 32-row header
+// are register loads, issued one chunk ahead of use.
+#ifndef GABP_GRP_C
+#define GABP_GRP_C 2
 #endif
-#ifndef GABP_TMA_NS
-#define GABP_TMA_NS 4
+#ifndef GABP_GRP_NS
+#define GABP_GRP_NS 4
 #endif
-#ifndef GABP_TMA_WARPS
-#define GABP_TMA_WARPS 16
-#endif
-#ifndef GABP_TMA_MINB
-#define GABP_TMA_MINB 1
-#endif
-constexpr int kTC = GABP_TMA_C;      // edge columns per chunk
-constexpr int kTS = GABP_TMA_NS;     // stages per warp
-constexpr int kTW = GABP_TMA_WARPS;  // warps per CTA
-constexpr int kTThreads = 32 * kTW;
+constexpr int kGC = GABP_GRP_C;   // edge columns per chunk
+constexpr int kGS = GABP_GRP_NS;  // ring stages
+constexpr int kGThreads = 32 * (kGroup + 1);
+static_assert(kGS >= 2, "the ring needs two stages");
 
-struct __align__(128) TStage {
-    double2 i2[kTC][32];  // I^{(s-2)} (statistics)
-    double2 i3[kTC][32];  // I^{(s-3)} (own message rebuild)
-    double c[kTC][32];
-    uint32_t col[kTC][32];
+struct __align__(128) GStage {
+    double2 i2[kGC][kStride];  // I^{(s-2)} (statistics)
+    double2 i3[kGC][kStride];  // I^{(s-3)} (own message rebuild)
+    double c[kGC][kStride];
+    uint32_t col[kGC][kStride];
 };
-struct TMeta {
-    int64_t sl;       // slice (< 0: no chunk)
-    uint32_t b, nb;   // chunk within the slice, chunks of the slice (>= 1)
-    uint32_t base, w; // slot base and width of the slice
+struct __align__(16) GMeta {
+    int32_t g;            // group (< 0: end of the launch's work)
+    uint32_t b, nb;       // chunk within the group, chunks of the group (>= 1)
+    uint32_t w;           // group width (columns)
+    uint32_t gbase;       // first slot of the group
+    uint32_t pad[3];
 };
-struct __align__(128) TWarp {
-    TStage st[kTS];
-    uint64_t bar[kTS];
-    TMeta meta[kTS];
+struct __align__(128) GRing {
+    GStage st[kGS];
+    uint64_t full[kGS];
+    uint64_t empty[kGS];
+    GMeta meta[kGS];
 };
-constexpr size_t kTmaSmem = sizeof(TWarp) * kTW;
-static_assert(kTS >= 3, "the chunk k+1 stage must differ from the refilled k-1 stage");
+constexpr size_t kGrpSmem = sizeof(GRing);
 
 __device__ __forceinline__ void t_mbar_init(uint64_t *bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
@@ -574,90 +576,72 @@ __device__ __forceinline__ void t_bulk_ef(void *dst, const void *src, unsigned b
         "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
         : "memory");
 }
-__device__ __forceinline__ void t_bulk(void *dst, const void *src, unsigned bytes,
-                                       uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-        ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar))
-        : "memory");
+
+__device__ __forceinline__ uint2 group_info(const SweepArgs &a, int64_t g, int64_t ngroups) {
+    return g < ngroups ? __ldg(a.slice_info + g * kGroup) : make_uint2(0u, 0u);
+}
+__device__ __forceinline__ uint32_t chunks_of(uint32_t w) {
+    return w > 0 ? (w + kGC - 1) / kGC : 1u;
 }
 
-// Issue-side cursor of a warp: work units claimed ahead (cur: being issued, nxt: its
-// slice descriptors in flight, pend: lane 0's claim in flight), so neither the claim's
-// atomic nor the descriptor load is waited for when the cursor crosses into a unit.
-struct TCursor {
-    int64_t ucur, unxt;   // units (>= nunits: none)
-    uint2 icur, inxt;     // lane k: {base, width} of slice (unit * U + k), k < U
-    uint32_t pend;        // lane 0: unit of the next claim
-    uint32_t k;           // slice within ucur
-    uint32_t b, nb;       // chunk within the slice
-    int64_t sl;           // slice being issued (< 0: done)
-    uint32_t base, w;
-};
-
-__device__ __forceinline__ uint2 unit_info(const SweepArgs &a, int64_t u, int lane) {
-    const int64_t sl = u * a.slice_unit + lane;
-    return (lane < a.slice_unit && sl < a.nslices) ? __ldg(a.slice_info + sl)
-                                                   : make_uint2(0u, 0u);
-}
-
+// Producer warp: claims groups and fills the ring until the claims run out.
 template <int PH, int R>
-__device__ __forceinline__ void t_issue(TWarp &W, int stage, TCursor &c, const SweepArgs &a,
-                                        const Ring<R> &r, int64_t nunits, uint32_t *ctr,
-                                        uint64_t pol, int lane) {
-    TMeta m;
-    m.sl = c.sl;
-    if (c.sl >= 0) {
-        m.b = c.b;
-        m.nb = c.nb;
-        m.base = c.base;
-        m.w = c.w;
+__device__ __forceinline__ void grp_produce(const SweepArgs &a, GRing &G, uint32_t *ctr,
+                                            int lane) {
+    const Ring<R> r(a);
+    const int64_t ngroups = a.nslices / kGroup;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    uint32_t u0 = 0, u1 = 0, pend = 0;
+    if (lane == 0) {
+        u0 = atomicAdd(ctr, 1u);
+        u1 = atomicAdd(ctr, 1u);
+        pend = atomicAdd(ctr, 1u);
+    }
+    int64_t gcur = __shfl_sync(~0u, u0, 0), gnxt = __shfl_sync(~0u, u1, 0);
+    uint2 icur = group_info(a, gcur, ngroups), inxt = group_info(a, gnxt, ngroups);
+    uint32_t b = 0, nb = chunks_of(icur.y);
+    for (uint32_t k = 0;; ++k) {
+        const int stg = (int)(k % kGS);
+        if (k >= (uint32_t)kGS) t_wait(&G.empty[stg], ((k / kGS) - 1u) & 1u);
+        if (gcur >= ngroups) {  // no more work: wake the consumers with an end marker
+            if (lane == 0) {
+                G.meta[stg].g = -1;
+                t_arrive(&G.full[stg]);
+            }
+            return;
+        }
         if (lane == 0) {
-            const uint32_t q0 = c.b * kTC;
-            const uint32_t nc = c.w > q0 ? min((uint32_t)kTC, c.w - q0) : 0u;
-            const uint32_t slot = c.base + 32u * q0;
-            const unsigned bytes = nc * 32u * (PH == 3 ? 44u : 12u);
-            TStage &S = W.st[stage];
-            uint64_t *bar = &W.bar[stage];
-            t_expect_tx(bar, bytes);  // (0 bytes: isolated rows only, the arrive completes it)
+            const uint32_t w = icur.y, q0 = b * kGC;
+            const uint32_t nc = w > q0 ? min((uint32_t)kGC, w - q0) : 0u;
+            const uint32_t slot = icur.x + (uint32_t)kStride * q0;
+            GMeta &m = G.meta[stg];
+            m.g = (int32_t)gcur;
+            m.b = b;
+            m.nb = nb;
+            m.w = w;
+            m.gbase = icur.x;
+            GStage &S = G.st[stg];
+            // (0 bytes: a group of isolated rows; the arrive alone completes the phase)
+            t_expect_tx(&G.full[stg], nc * (uint32_t)kStride * (PH == 3 ? 44u : 12u));
             if (nc) {
-                t_bulk_ef(&S.c[0][0], a.scoef + slot, nc * 256u, bar, pol);
-                t_bulk_ef(&S.col[0][0], a.scol + slot, nc * 128u, bar, pol);
+                t_bulk_ef(&S.c[0][0], a.scoef + slot, nc * kStride * 8u, &G.full[stg], pol);
+                t_bulk_ef(&S.col[0][0], a.scol + slot, nc * kStride * 4u, &G.full[stg], pol);
                 if (PH == 3) {
-                    t_bulk_ef(&S.i2[0][0], r.I2 + slot, nc * 512u, bar, pol);
-                    t_bulk_ef(&S.i3[0][0], r.I3 + slot, nc * 512u, bar, pol);
+                    t_bulk_ef(&S.i2[0][0], r.I2 + slot, nc * kStride * 16u, &G.full[stg], pol);
+                    t_bulk_ef(&S.i3[0][0], r.I3 + slot, nc * kStride * 16u, &G.full[stg], pol);
                 }
             }
-            W.meta[stage] = m;
         }
-        if (++c.b >= c.nb) {
-            ++c.k;
-            for (;;) {  // next slice of the unit, else the next unit
-                if (c.ucur >= nunits) {
-                    c.sl = -1;
-                    break;
-                }
-                const int64_t sl = c.ucur * a.slice_unit + c.k;
-                if (c.k < (uint32_t)a.slice_unit && sl < a.nslices) {
-                    const uint32_t bw = __shfl_sync(~0u, c.icur.x, c.k);
-                    const uint32_t ww = __shfl_sync(~0u, c.icur.y, c.k);
-                    c.sl = sl;
-                    c.base = bw;
-                    c.w = ww;
-                    c.b = 0;
-                    c.nb = ww > 0 ? (ww + kTC - 1) / kTC : 1u;
-                    break;
-                }
-                c.ucur = c.unxt;
-                c.icur = c.inxt;
-                c.unxt = (int64_t)__shfl_sync(~0u, c.pend, 0);
-                c.inxt = unit_info(a, c.unxt, lane);
-                c.k = 0;
-                if (lane == 0) c.pend = atomicAdd(ctr, 1u);
-            }
+        if (++b >= nb) {  // next group: claimed two groups ago, descriptor loaded one ago
+            gcur = gnxt;
+            icur = inxt;
+            gnxt = __shfl_sync(~0u, pend, 0);
+            inxt = group_info(a, gnxt, ngroups);
+            if (lane == 0) pend = atomicAdd(ctr, 1u);
+            b = 0;
+            nb = chunks_of(icur.y);
         }
-    } else if (lane == 0) {
-        W.meta[stage] = m;
     }
 }
 
@@ -672,9 +656,8 @@ struct THdr {
     uint32_t d;
 };
 template <int PH, int R>
-__device__ __forceinline__ void t_header(const SweepArgs &a, const Ring<R> &r, int64_t sl,
-                                         int lane, THdr &h) {
-    const int64_t p = sl * 32 + lane;
+__device__ __forceinline__ void t_header(const SweepArgs &a, const Ring<R> &r, int64_t p,
+                                         THdr &h) {
     h.nd = __ldg(a.snd + p);
     h.d = __ldg(a.sdeg + p);
     if (PH == 3) {
@@ -685,13 +668,13 @@ __device__ __forceinline__ void t_header(const SweepArgs &a, const Ring<R> &r, i
 }
 
 // neighbour gathers of a landed chunk (node states of S_{s-2}), one chunk ahead of use
-__device__ __forceinline__ void t_gather(const TStage &S, const TMeta &m, const NodeState *g2,
-                                         int lane, double (&gP)[kTC], double (&gN)[kTC],
-                                         double (&gx)[kTC]) {
+__device__ __forceinline__ void t_gather(const GStage &S, const GMeta &m, const NodeState *g2,
+                                         int t, double (&gP)[kGC], double (&gN)[kGC],
+                                         double (&gx)[kGC]) {
 #pragma unroll
-    for (int u = 0; u < kTC; ++u) {
-        if (m.b * kTC + u < m.w) {
-            ld_node(g2 + S.col[u][lane], gP[u], gN[u], gx[u]);
+    for (int u = 0; u < kGC; ++u) {
+        if (m.b * kGC + u < m.w) {
+            ld_node(g2 + S.col[u][t], gP[u], gN[u], gx[u]);
         } else {
             gP[u] = 1.0;
             gN[u] = 1.0;
@@ -700,50 +683,20 @@ __device__ __forceinline__ void t_gather(const TStage &S, const TMeta &m, const 
     }
 }
 
+// Consumer warp `warp`: slice warp of every group, lane per row.
 template <int PH, int R>
-__device__ __forceinline__ void slice_sweep_tma(const SweepArgs &a, int64_t s, Stats &st,
-                                                int lane, TWarp &W, uint32_t *ctr) {
+__device__ __forceinline__ void grp_consume(const SweepArgs &a, int64_t s, Stats &st, int lane,
+                                            int warp, GRing &G) {
     const Ring<R> r(a);
     double *xh = xhist_row(a, s);
-    const int64_t nunits = (a.nslices + a.slice_unit - 1) / a.slice_unit;
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    if (lane < kTS) t_mbar_init(&W.bar[lane], 1u);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    __syncwarp();
-
-    // claim the first three units: cur, nxt (descriptors), pend (lane 0)
-    TCursor c;
-    uint32_t u0 = 0, u1 = 0;
-    if (lane == 0) {
-        u0 = atomicAdd(ctr, 1u);
-        u1 = atomicAdd(ctr, 1u);
-        c.pend = atomicAdd(ctr, 1u);
-    }
-    c.ucur = (int64_t)__shfl_sync(~0u, u0, 0);
-    c.unxt = (int64_t)__shfl_sync(~0u, u1, 0);
-    c.icur = unit_info(a, c.ucur, lane);
-    c.inxt = unit_info(a, c.unxt, lane);
-    c.k = 0;
-    if (c.ucur < nunits) {
-        c.sl = c.ucur * a.slice_unit;
-        c.base = __shfl_sync(~0u, c.icur.x, 0);
-        c.w = __shfl_sync(~0u, c.icur.y, 0);
-        c.b = 0;
-        c.nb = c.w > 0 ? (c.w + kTC - 1) / kTC : 1u;
-    } else {
-        c.sl = -1;
-    }
-#pragma unroll
-    for (int j = 0; j < kTS - 1; ++j) t_issue<PH, R>(W, j, c, a, r, nunits, ctr, pol, lane);
-    __syncwarp();
-    TMeta m = W.meta[0];
-    if (m.sl < 0) return;
-    double gP[kTC], gN[kTC], gx[kTC];
+    const int t = warp * 32 + lane;  // index within a group column
+    t_wait(&G.full[0], 0u);
+    GMeta m = G.meta[0];
+    if (m.g < 0) return;
+    double gP[kGC], gN[kGC], gx[kGC];
     THdr hn;
-    t_header<PH, R>(a, r, m.sl, lane, hn);
-    t_wait(&W.bar[0], 0u);
-    t_gather(W.st[0], m, r.g2, lane, gP, gN, gx);
+    t_header<PH, R>(a, r, ((int64_t)m.g * kGroup + warp) * 32 + lane, hn);
+    t_gather(G.st[0], m, r.g2, t, gP, gN, gx);
 
     uint32_t d = 0;
     double2 a3 = make_double2(0.0, 0.0);
@@ -760,64 +713,75 @@ __device__ __forceinline__ void slice_sweep_tma(const SweepArgs &a, int64_t s, S
                 rhs_i = hn.rhs;
             }
         }
-        __syncwarp();  // every lane is done with chunk k-1's stage
-        t_issue<PH, R>(W, (int)((k + kTS - 1) % kTS), c, a, r, nunits, ctr, pol, lane);
-        __syncwarp();
         // header and gathers of chunk k+1
-        double nP[kTC] = {}, nN[kTC] = {}, nx[kTC] = {};
-        const int sn1 = (int)((k + 1) % kTS);
-        const TMeta mn = W.meta[sn1];
-        if (mn.sl >= 0) {
-            if (mn.b == 0) t_header<PH, R>(a, r, mn.sl, lane, hn);
-            t_wait(&W.bar[sn1], ((k + 1) / kTS) & 1u);
-            t_gather(W.st[sn1], mn, r.g2, lane, nP, nN, nx);
+        double nP[kGC] = {}, nN[kGC] = {}, nx[kGC] = {};
+        const int s1 = (int)((k + 1) % kGS);
+        t_wait(&G.full[s1], ((k + 1) / kGS) & 1u);
+        const GMeta mn = G.meta[s1];
+        if (mn.g >= 0) {
+            if (mn.b == 0) t_header<PH, R>(a, r, ((int64_t)mn.g * kGroup + warp) * 32 + lane, hn);
+            t_gather(G.st[s1], mn, r.g2, t, nP, nN, nx);
         }
-        const TStage &S = W.st[k % kTS];
-        double cc[kTC], m2p[kTC], m2m[kTC], ip[kTC], im[kTC], pe[kTC];
+        const int s0 = (int)(k % kGS);
+        const GStage &S = G.st[s0];
+        double cc[kGC], m2p[kGC], m2m[kGC], ip[kGC], im[kGC], pe[kGC];
+        double2 i2v[kGC];
 #pragma unroll
-        for (int u = 0; u < kTC; ++u) {
-            const bool v = m.b * kTC + u < d;
-            cc[u] = v ? S.c[u][lane] : 1.0;
+        for (int u = 0; u < kGC; ++u) {
+            const bool v = m.b * kGC + u < d;
+            cc[u] = v ? S.c[u][t] : 1.0;
             m2p[u] = 0.0;  // m^{(0)} = 0 at launch 2
             m2m[u] = 0.0;
+            i2v[u] = make_double2(0.0, 0.0);
             if (PH == 3) {  // own outgoing message of sweep s-2
-                const double2 i3 = S.i3[u][lane];
+                const double2 i3 = S.i3[u][t];
+                i2v[u] = S.i2[u][t];
                 const double pe2 = v ? a3.x - i3.x : 1.0;
                 const double nu2 = v ? a3.y - i3.x * i3.y : 1.0;
-                edge_msg<false>(cc[u], pe2, nu2, m2p[u], m2m[u], st.redo);
+                edge_msg<false>(cc[u], pe2, nu2, m2p[u], m2m[u], st);
             }
         }
+        __syncwarp();
+        if (lane == 0) t_arrive(&G.empty[s0]);  // the stage's data is in registers now
 #pragma unroll
-        for (int u = 0; u < kTC; ++u) {  // incoming of S_{s-1}
-            const bool v = m.b * kTC + u < d;
+        for (int u = 0; u < kGC; ++u) {  // incoming of S_{s-1}
+            const bool v = m.b * kGC + u < d;
             pe[u] = v ? gP[u] - m2p[u] : 1.0;
             const double num = v ? gN[u] - m2p[u] * m2m[u] : 1.0;
-            edge_msg<false>(cc[u], pe[u], num, ip[u], im[u], st.redo);
+            edge_msg<false>(cc[u], pe[u], num, ip[u], im[u], st);
         }
-        const int64_t p = m.sl * 32 + lane;
+        const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
 #pragma unroll
-        for (int u = 0; u < kTC; ++u) {
-            const uint32_t q = m.b * kTC + u;
+        for (int u = 0; u < kGC; ++u) {
+            const uint32_t q = m.b * kGC + u;
             if (q < d) {
                 sp = sp + ip[u];
                 sn = sn + ip[u] * im[u];  // (prec * mean), solver.py:243
                 if (PH == 3) y = y + cc[u] * gx[u];
-                __stcs(r.I1 + m.base + lane + 32u * q, make_double2(ip[u], im[u]));
-                const double2 i2 = PH == 3 ? S.i2[u][lane] : make_double2(0.0, 0.0);
-                msg_stats<false>(st, a, ip[u], im[u], i2, pe[u], p, q);
+                __stcs(r.I1 + m.gbase + (uint32_t)kStride * q + t, make_double2(ip[u], im[u]));
+                msg_stats<false>(st, a, ip[u], im[u], i2v[u], pe[u], p, q);
             }
         }
         if (m.b + 1 == m.nb && diag != 0.0)  // row done (A_ii == 0: padding lane)
             node_done<PH, false>(st, a, r.g1, xh, p, sp, sn, y, rhs_i);
-        if (mn.sl < 0) break;
+        if (mn.g < 0) break;
         m = mn;
 #pragma unroll
-        for (int u = 0; u < kTC; ++u) {
+        for (int u = 0; u < kGC; ++u) {
             gP[u] = nP[u];
             gN[u] = nN[u];
             gx[u] = nx[u];
         }
     }
+}
+
+template <int PH, int R>
+__device__ __forceinline__ void slice_sweep_grp(const SweepArgs &a, int64_t s, Stats &st,
+                                                int lane, int warp, GRing &G, uint32_t *ctr) {
+    if (warp == kGroup)
+        grp_produce<PH, R>(a, G, ctr, lane);
+    else
+        grp_consume<PH, R>(a, s, st, lane, warp, G);
 }
 
 // ---- kernels ---------------------------------------------------------------------------------
@@ -887,78 +851,89 @@ __global__ void __launch_bounds__(kPThreads, 3) slice_kernel_pipe(const SweepArg
                                               s, s >= 3, st, tid);
 }
 
-template <int NW>
-struct TmaSmem {
-    TailSmem<NW> tail;
+struct GrpSmem {
+    TailSmem<kGroup + 1> tail;
     int64_t sweep;
     int skip;
 };
 
-template <int NW>
-__global__ void __launch_bounds__(NW * 32, GABP_TMA_MINB) slice_kernel_tma(const SweepArgs a) {
-    __shared__ TmaSmem<NW> S;
-    extern __shared__ __align__(128) unsigned char tma_raw[];
-    TWarp &W = reinterpret_cast<TWarp *>(tma_raw)[threadIdx.x >> 5];
+__global__ void __launch_bounds__(kGThreads, 1) slice_kernel_grp(const SweepArgs a) {
+    __shared__ GrpSmem S;
+    extern __shared__ __align__(128) unsigned char grp_raw[];
+    GRing &G = *reinterpret_cast<GRing *>(grp_raw);
     if (!slice_prologue(S, a, false)) return;
     const int64_t s = S.sweep;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < kGS) {
+        t_mbar_init(&G.full[tid], 1u);
+        t_mbar_init(&G.empty[tid], (unsigned)kGroup);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
     uint32_t *ctr = &a.ctrl->work[s % kStatSlots];
     Stats st;
     st.lim = fmin(a.ctrl->blowup, DBL_MAX);
     if (s >= 3) {
         const int r = (int)(s % 3);
         if (r == 0)
-            slice_sweep_tma<3, 0>(a, s, st, lane, W, ctr);
+            slice_sweep_grp<3, 0>(a, s, st, lane, warp, G, ctr);
         else if (r == 1)
-            slice_sweep_tma<3, 1>(a, s, st, lane, W, ctr);
+            slice_sweep_grp<3, 1>(a, s, st, lane, warp, G, ctr);
         else
-            slice_sweep_tma<3, 2>(a, s, st, lane, W, ctr);
+            slice_sweep_grp<3, 2>(a, s, st, lane, warp, G, ctr);
     } else if (s == 2) {
-        slice_sweep_tma<2, 2>(a, s, st, lane, W, ctr);
+        slice_sweep_grp<2, 2>(a, s, st, lane, warp, G, ctr);
     } else {
-        slice_first<NW, false>(a, s, st, lane);
+        slice_first<kGroup + 1, false>(a, s, st, lane);
     }
-    sweep_epilogue<NW * 32, kModeSolve, 1>(S.tail, a, s, s >= 3, st, tid);
+    sweep_epilogue<kGThreads, kModeSolve, 1>(S.tail, a, s, s >= 3, st, tid);
 }
 
-int g_grid_ldg = 0, g_grid_pipe = 0, g_grid_tma = 0;
+int g_grid_ldg = 0, g_grid_pipe = 0, g_grid_grp = 0;
 
 // ---- build -------------------------------------------------------------------------------
-constexpr int kSortWin = 1024;  // rows per degree-sort window (a multiple of 32)
+constexpr int kSortWin = kStride * 2048;  // rows per degree-sort window (whole groups)
+static_assert(kSlotPad >= kStride * (kUL + 1), "slot padding must cover a register batch");
 
-__global__ void slice_deg_kernel(int64_t row_lo, int64_t m, const uint32_t *row_ptr,
-                                 uint32_t *deg, uint32_t *rows) {
+// Sort key of a swept row: window id above 13 bits of (8191 - degree), so one ascending
+// stable radix sort orders every window by degree, descending (degrees <= 4096).
+constexpr int kDegBits = 13;
+static_assert(kSliceMaxDegree < (1 << kDegBits), "degree must fit the key");
+__global__ void slice_key_kernel(int64_t row_lo, int64_t m, const uint32_t *row_ptr,
+                                 uint32_t *key, uint32_t *rows) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= m) return;
     const int64_t i = row_lo + r;
-    deg[r] = row_ptr[i + 1] - row_ptr[i];
+    const uint32_t d = row_ptr[i + 1] - row_ptr[i];
+    key[r] = ((uint32_t)(r / kSortWin) << kDegBits) | ((1u << kDegBits) - 1u - d);
     rows[r] = (uint32_t)i;
 }
 
-__global__ void seg_offsets_kernel(int64_t nseg, int64_t m, int64_t *off) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k > nseg) return;
-    off[k] = k * kSortWin < m ? k * kSortWin : m;
+__global__ void key_to_deg_kernel(int64_t m, uint32_t *k) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < m) k[r] = (1u << kDegBits) - 1u - (k[r] & ((1u << kDegBits) - 1u));
 }
 
-// slots of each slice (degrees are sorted descending inside windows of whole slices)
-__global__ void slice_width_kernel(int64_t nslices, int64_t m, const uint32_t *sdeg,
-                                   unsigned long long *wslots) {
-    const int64_t sl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (sl >= nslices) return;
+// slots of each group: kStride x its largest degree (degrees are sorted descending inside
+// windows of whole groups, so that is the degree of its first row)
+__global__ void group_width_kernel(int64_t ngroups, int64_t m, const uint32_t *sdeg,
+                                   unsigned long long *gslots) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ngroups) return;
     uint32_t w = 0;
-    for (int l = 0; l < 32; ++l) {
-        const int64_t p = sl * 32 + l;
-        if (p < m && sdeg[p] > w) w = sdeg[p];
-    }
-    wslots[sl] = 32ull * w;
+    for (int64_t p = g * kStride; p < (g + 1) * kStride && p < m; ++p)
+        if (sdeg[p] > w) w = sdeg[p];
+    gslots[g] = (unsigned long long)kStride * w;
 }
 
-__global__ void slice_info_kernel(int64_t nslices, const unsigned long long *wslots,
-                                  const unsigned long long *base, uint2 *info) {
+// {slot base, width} of every slice: base_s = gbase_g + 32 (s % kGroup)
+__global__ void slice_info_kernel(int64_t nslices, const unsigned long long *gslots,
+                                  const unsigned long long *gbase, uint2 *info) {
     const int64_t sl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (sl >= nslices) return;
-    info[sl] = make_uint2((uint32_t)base[sl], (uint32_t)(wslots[sl] / 32));
+    const int64_t g = sl / kGroup;
+    info[sl] = make_uint2((uint32_t)(gbase[g] + 32 * (sl % kGroup)),
+                          (uint32_t)(gslots[g] / kStride));
 }
 
 // position of every local node: owned rows by the sort, halo rows after the slices
@@ -988,7 +963,7 @@ __global__ void slice_fill_kernel(int64_t nslices, const uint32_t *srow, const u
     const uint32_t l = (uint32_t)(p & 31), d = sdeg[p];
     const uint32_t eb = d ? row_ptr[srow[p]] : 0u;
     for (uint32_t q = 0; q < si.y; ++q) {
-        const uint32_t slot = si.x + 32u * q + l;
+        const uint32_t slot = si.x + (uint32_t)kStride * q + l;
         if (q < d) {
             const EdgeRec r = er[eb + q];
             scol[slot] = pos[r.col];
@@ -1041,44 +1016,45 @@ inline unsigned grid_of(int64_t n) { return (unsigned)((n + 255) / 256 > 0 ? (n 
 int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
     const int64_t m = g.row_hi - g.row_lo;
     if (m <= 0) return GABP_OK;
-    const int64_t nslices = (m + 31) / 32;
+    const int64_t ngroups = (m + kStride - 1) / kStride;
+    const int64_t nslices = ngroups * kGroup;  // padding slices complete the last group
     const int64_t m_pad = nslices * 32;
     const int64_t npos = m_pad + (g.n - m);
     const int64_t nseg = (m + kSortWin - 1) / kSortWin;
     uint32_t *deg = nullptr, *rows = nullptr, *sorted_deg = nullptr, *sorted_rows = nullptr;
-    int64_t *off = nullptr;
-    unsigned long long *wslots = nullptr, *base = nullptr;
+    unsigned long long *gslots = nullptr, *gbase = nullptr;
     SCHECK(cudaMallocAsync(&deg, sizeof(uint32_t) * m, st));
     SCHECK(cudaMallocAsync(&rows, sizeof(uint32_t) * m, st));
     SCHECK(cudaMallocAsync(&sorted_deg, sizeof(uint32_t) * m, st));
     SCHECK(cudaMallocAsync(&sorted_rows, sizeof(uint32_t) * m, st));
-    SCHECK(cudaMallocAsync(&off, sizeof(int64_t) * (nseg + 1), st));
-    SCHECK(cudaMallocAsync(&wslots, sizeof(unsigned long long) * (nslices + 1), st));
-    SCHECK(cudaMallocAsync(&base, sizeof(unsigned long long) * (nslices + 1), st));
-    slice_deg_kernel<<<grid_of(m), 256, 0, st>>>(g.row_lo, m, g.row_ptr, deg, rows);
-    seg_offsets_kernel<<<grid_of(nseg + 1), 256, 0, st>>>(nseg, m, off);
+    SCHECK(cudaMallocAsync(&gslots, sizeof(unsigned long long) * (ngroups + 1), st));
+    SCHECK(cudaMallocAsync(&gbase, sizeof(unsigned long long) * (ngroups + 1), st));
+    slice_key_kernel<<<grid_of(m), 256, 0, st>>>(g.row_lo, m, g.row_ptr, deg, rows);
     SCHECK(cudaGetLastError());
     // stable: rows of equal degree keep their order (structured grids stay contiguous)
+    int end_bit = kDegBits;
+    while (end_bit < 32 && ((nseg - 1) >> (end_bit - kDegBits)) > 0) ++end_bit;
     size_t tb = 0;
-    SCHECK(cub::DeviceSegmentedRadixSort::SortPairsDescending(
-        nullptr, tb, deg, sorted_deg, rows, sorted_rows, m, nseg, off, off + 1, 0, 32, st));
+    SCHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, deg, sorted_deg, rows, sorted_rows, m,
+                                           0, end_bit, st));
     void *tmp = nullptr;
     SCHECK(cudaMallocAsync(&tmp, tb, st));
-    SCHECK(cub::DeviceSegmentedRadixSort::SortPairsDescending(
-        tmp, tb, deg, sorted_deg, rows, sorted_rows, m, nseg, off, off + 1, 0, 32, st));
+    SCHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, deg, sorted_deg, rows, sorted_rows, m, 0,
+                                           end_bit, st));
     cudaFreeAsync(tmp, st);
-    slice_width_kernel<<<grid_of(nslices), 256, 0, st>>>(nslices, m, sorted_deg, wslots);
-    SCHECK(cudaMemsetAsync(wslots + nslices, 0, sizeof(unsigned long long), st));
+    key_to_deg_kernel<<<grid_of(m), 256, 0, st>>>(m, sorted_deg);
+    group_width_kernel<<<grid_of(ngroups), 256, 0, st>>>(ngroups, m, sorted_deg, gslots);
+    SCHECK(cudaMemsetAsync(gslots + ngroups, 0, sizeof(unsigned long long), st));
     size_t sb = 0;
-    SCHECK(cub::DeviceScan::ExclusiveSum(nullptr, sb, wslots, base, nslices + 1, st));
+    SCHECK(cub::DeviceScan::ExclusiveSum(nullptr, sb, gslots, gbase, ngroups + 1, st));
     SCHECK(cudaMallocAsync(&tmp, sb, st));
-    SCHECK(cub::DeviceScan::ExclusiveSum(tmp, sb, wslots, base, nslices + 1, st));
+    SCHECK(cub::DeviceScan::ExclusiveSum(tmp, sb, gslots, gbase, ngroups + 1, st));
     cudaFreeAsync(tmp, st);
     unsigned long long nslots = 0;
-    SCHECK(cudaMemcpyAsync(&nslots, base + nslices, sizeof(nslots), cudaMemcpyDeviceToHost, st));
+    SCHECK(cudaMemcpyAsync(&nslots, gbase + ngroups, sizeof(nslots), cudaMemcpyDeviceToHost, st));
     SCHECK(cudaStreamSynchronize(st));
     int rc = GABP_OK;
-    if (nslots >= 0xffffffffull) {
+    if (nslots + kSlotPad >= 0xffffffffull) {
         rc = GABP_EINVAL;  // caller keeps the tile layout only
         snprintf(err, errlen, "slice layout needs %llu slots (> 32-bit)", nslots);
     } else {
@@ -1091,20 +1067,17 @@ int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
         SCHECK(cudaMallocAsync(&g.sdeg, sizeof(uint32_t) * npos, st));
         SCHECK(cudaMallocAsync(&g.snd, sizeof(double2) * npos, st));
         SCHECK(cudaMallocAsync(&g.srhs, sizeof(double) * npos, st));
-        // + kSlotPad: the register-batch kernel loads whole batches past a slice's width
+        // + kSlotPad: the register-batch kernel loads whole batches past a group's width
         SCHECK(cudaMallocAsync(&g.scol, sizeof(uint32_t) * (nslots + kSlotPad), st));
         SCHECK(cudaMallocAsync(&g.scoef, sizeof(double) * (nslots + kSlotPad), st));
         SCHECK(cudaMemsetAsync(g.scol + nslots, 0, sizeof(uint32_t) * kSlotPad, st));
         SCHECK(cudaMemsetAsync(g.scoef + nslots, 0, sizeof(double) * kSlotPad, st));
-        // kernel variant: register batches for long rows, the cp.async ring for short ones
-        const double mean_w = (double)nslots / (double)(nslices * 32);
+        // kernel: the group TMA ring; GABP_SLICE_VARIANT=0/1 selects the register-batch /
+        // cp.async kernels (kept as cross-checks, tests/test_gpu_parity.py)
         g.slice_variant = 2;
         if (const char *ev = getenv("GABP_SLICE_VARIANT")) g.slice_variant = atoi(ev);
         if (g.slice_variant < 0 || g.slice_variant > 2) g.slice_variant = 2;
-        // TMA ring: claim units of >= 8 chunks (one atomic per unit)
-        const double chunks = fmax(1.0, ceil(mean_w / kTC));
-        g.slice_unit = (int)fmin(32.0, fmax(1.0, round(8.0 / chunks)));
-        slice_info_kernel<<<grid_of(nslices), 256, 0, st>>>(nslices, wslots, base,
+        slice_info_kernel<<<grid_of(nslices), 256, 0, st>>>(nslices, gslots, gbase,
                                                             g.slice_info);
         const int64_t big = m > g.n - m ? m : g.n - m;
         slice_pos_kernel<<<grid_of(big), 256, 0, st>>>(g.n, g.row_lo, g.row_hi, m_pad, m,
@@ -1120,9 +1093,8 @@ int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
     cudaFreeAsync(rows, st);
     cudaFreeAsync(sorted_deg, st);
     cudaFreeAsync(sorted_rows, st);
-    cudaFreeAsync(off, st);
-    cudaFreeAsync(wslots, st);
-    cudaFreeAsync(base, st);
+    cudaFreeAsync(gslots, st);
+    cudaFreeAsync(gbase, st);
     SCHECK(cudaStreamSynchronize(st));
     return rc;
 }
@@ -1171,14 +1143,13 @@ cudaError_t prepare_slice_kernels() {
                                                            kLThreads, 0)) != cudaSuccess)
         return e;
     g_grid_ldg = sms * (occ > 0 ? occ : 1);
-    if ((e = cudaFuncSetAttribute(slice_kernel_tma<kTW>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kTmaSmem)) != cudaSuccess)
+    if ((e = cudaFuncSetAttribute(slice_kernel_grp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kGrpSmem)) != cudaSuccess)
         return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slice_kernel_tma<kTW>,
-                                                           kTThreads, kTmaSmem)) != cudaSuccess)
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slice_kernel_grp, kGThreads,
+                                                           kGrpSmem)) != cudaSuccess)
         return e;
-    g_grid_tma = sms * (occ > 0 ? occ : 1);
+    g_grid_grp = sms * (occ > 0 ? occ : 1);
     return cudaSuccess;
 }
 
@@ -1196,10 +1167,10 @@ static void launch_slice_fast(const SweepArgs &a, cudaStream_t st) {
 
 cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st) {
     if (a.slice_variant == 2) {
-        int64_t grid = g_grid_tma > 0 ? g_grid_tma : 148;
-        const int64_t need = (a.nslices + kTW - 1) / kTW;
+        int64_t grid = g_grid_grp > 0 ? g_grid_grp : 148;
+        const int64_t need = a.nslices / kGroup;
         if (grid > need) grid = need > 0 ? need : 1;
-        slice_kernel_tma<kTW><<<(unsigned)grid, kTThreads, kTmaSmem, st>>>(a);
+        slice_kernel_grp<<<(unsigned)grid, kGThreads, kGrpSmem, st>>>(a);
     } else {
         launch_slice_fast(a, st);
     }

@@ -436,7 +436,8 @@ def _ragged_system(seed=5):
 def test_slice_layout_built():
     s = G.gen_poisson2d(33, 0).system
     g = G.build_graph(s)
-    assert g.info.num_slices == (s.n + 31) // 32
+    # slices of 32 rows, the last group of slices completed with padding slices
+    assert (s.n + 31) // 32 <= g.info.num_slices < (s.n + 31) // 32 + 16
     assert g.info.num_slots >= g.num_edges
 
 
