@@ -375,7 +375,7 @@ def run_ours(args):
     g_close = g.close
     g_info_span = float(g.info.twin_span)
     slice_path = sched == "broadcast" and int(g.info.num_slices) > 0
-    kname = (("slice_kernel_ldg", "slice_kernel_pipe", "slice_kernel_tma")[int(g.info.slice_variant)]
+    kname = (("slice_kernel_ldg", "slice_kernel_pipe", "slice_kernel_grp")[int(g.info.slice_variant)]
              + " + exact twin (exits unless flagged)") if slice_path else f"sweep_kernel<{sched}>"
 
     # e2e: the drop-in call with pinned host buffers, H2D + build + solve + D2H timed

@@ -336,6 +336,45 @@ def test_config4_poisson3d_small_slab_vs_oracle():
     np.testing.assert_array_equal(r.means, orc.means)
 
 
+def _subbox_system(s, p, lo, L):
+    """The 3-D grid system restricted to the box [lo, lo + L)^3 (z, y, x), nodes renumbered
+    lexicographically -- so every row keeps its neighbours in ascending order."""
+    z, y, x = np.meshgrid(*(np.arange(c, c + L) for c in lo), indexing="ij")
+    glob = (z * p * p + y * p + x).ravel()
+    loc = -np.ones(p ** 3, dtype=np.int64)
+    loc[glob] = np.arange(glob.size)
+    li, lj = loc[s.pair_i], loc[s.pair_j]
+    keep = (li >= 0) & (lj >= 0)
+    sub = G.SymSystem.from_pairs(s.diag[glob], li[keep], lj[keep], s.pair_v[keep], s.rhs[glob])
+    return sub, glob
+
+
+def test_config4_full_size_locality_vs_oracle():
+    """Config 4 at full size (512^3, 804M directed edges) on one GPU.  After T sweeps from
+    zero messages a marginal depends only on the rows within T+1 hops, so on a sub-box
+    the oracle (run on the restricted system) must reproduce the full-size marginals bitwise
+    wherever the sub-box's cut faces are more than T+1 hops away.  Two boxes: one at the
+    domain corner (three true Dirichlet faces), one in the interior."""
+    p, T, L = 512, 6, 40
+    s = G.gen_poisson3d(p, 0).system
+    r = G.solve(s, G.SolveOptions(schedule="broadcast", epsilon=1e-300, max_iter=T,
+                                  record_means_history=False))
+    assert r.iterations == T
+    m = T + 2  # margin from a cut face
+    for lo in ((0, 0, 0), (200, 300, 100)):
+        sub, glob = _subbox_system(s, p, lo, L)
+        og = oracle.build_graph(sub.diag, sub.rhs, sub.pair_i, sub.pair_j, sub.pair_v)
+        orc = oracle.solve(og, epsilon=1e-300, max_iter=T, schedule="broadcast")
+        assert orc.iterations == T
+        k = np.arange(L)
+        ok_axis = [(k >= (0 if c == 0 else m)) & (k < L - m) for c in lo]
+        inner = (ok_axis[0][:, None, None] & ok_axis[1][None, :, None] &
+                 ok_axis[2][None, None, :]).ravel()
+        assert inner.sum() > 1000
+        np.testing.assert_array_equal(r.means[glob[inner]], orc.means[inner])
+        np.testing.assert_array_equal(r.precisions[glob[inner]], orc.precisions[inner])
+
+
 @pytest.mark.parametrize("case", CASES)
 def test_gather_modes_bitwise_identical(case):
     """Broadcast solve with the twin-message gather and with the aggregate recompute

@@ -1,0 +1,48 @@
+"""Full-size probe of one BASELINE config on one GPU: problem generation, device build,
+back-to-back sweep timing (device events), algorithmic roofline, device memory in use.
+Usage: python tools/config_probe.py --config 4 [--sweeps 20]"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_0810_1119_b200 as G  # noqa: E402
+from paper_0810_1119_b200 import _lib, problems  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=4)
+ap.add_argument("--sweeps", type=int, default=20)
+a = ap.parse_args()
+t0 = time.perf_counter()
+name, fn = problems.CONFIGS[a.config]
+s = fn(0).system
+t1 = time.perf_counter()
+g = G.build_graph(s, 0)
+t2 = time.perf_counter()
+lib = _lib.load()
+ms = ctypes.c_double()
+_lib.check(lib.gabp_bench_sweeps(g.handle, 2, 0, 3, ctypes.byref(ms)))
+_lib.check(lib.gabp_bench_sweeps(g.handle, 2, 0, a.sweeps, ctypes.byref(ms)))
+free_b, total_b = ctypes.c_size_t(), ctypes.c_size_t()
+cudart = None
+try:
+    import torch
+    free, total = torch.cuda.mem_get_info(0)
+except Exception:  # noqa: BLE001
+    free, total = 0, 0
+E, n = g.num_edges, g.n
+algo = 48 * E + 52 * n
+peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json"))).get("hbm_gbs", 6537.3)
+print(json.dumps({
+    "config": a.config, "workload": name, "n": n, "directed_edges": E,
+    "slices": int(g.info.num_slices), "slots": int(g.info.num_slots),
+    "gen_s": round(t1 - t0, 1), "build_s": round(t2 - t1, 2),
+    "device_build_ms": round(float(g.info.build_ms), 1),
+    "ms_per_sweep": round(ms.value, 3), "edge_updates_per_s": E / (ms.value / 1e3),
+    "algorithmic_GBps": algo / (ms.value / 1e3) / 1e9,
+    "frac_of_measured_hbm": algo / (ms.value / 1e3) / 1e9 / peak,
+    "device_mem_used_GB": round((total - free) / 1e9, 1)}))
