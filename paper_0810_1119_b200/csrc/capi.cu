@@ -120,6 +120,9 @@ struct gabp_graph {
     double *dA = nullptr;
     double2 *dmsg[3] = {nullptr, nullptr, nullptr};
     double2 *dnode = nullptr;
+    int64_t Kp = 0;                  // padded dimension (multiple of 32)
+    uint2 *dpairs = nullptr;         // tile pairs of the pair-tile kernel
+    int64_t dnpairs = 0;
 };
 
 struct gabp_state {
@@ -377,6 +380,7 @@ void release_workspace(gabp_graph *G) {
     cudaFree(G->dA);
     for (int b = 0; b < 3; ++b) cudaFree(G->dmsg[b]);
     cudaFree(G->dnode);
+    cudaFree(G->dpairs);
     if (G->dist) {
         cudaFree(G->dist->d_sidx);
         cudaFree(G->dist->d_ridx);
@@ -612,16 +616,22 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
     if (G->is_dense && sched == GABP_SCHED_BROADCAST && opt->gather_mode == GABP_GATHER_AUTO) {
         // dense variant: column walk + edge tiles (dense.cu), same controller protocol
         G->slice_order = false;
-        const int64_t K = G->K;
+        const int64_t K = G->K, Kp = G->Kp;
         for (int b = 0; b < 3; ++b)
-            if (!G->dmsg[b]) CK(cudaMalloc(&G->dmsg[b], sizeof(double2) * K * K));
-        if (!G->dnode) CK(cudaMalloc(&G->dnode, sizeof(double2) * K));
-        CK(cudaMemsetAsync(G->dmsg[0], 0, sizeof(double2) * K * K, st));
+            if (!G->dmsg[b]) CK(cudaMalloc(&G->dmsg[b], sizeof(double2) * Kp * Kp));
+        if (!G->dnode) {
+            CK(cudaMalloc(&G->dnode, sizeof(double2) * Kp));
+            CK(cudaMemset(G->dnode, 0, sizeof(double2) * Kp));  // padding rows stay zero
+        }
+        CK(cudaMemsetAsync(G->dmsg[0], 0, sizeof(double2) * Kp * Kp, st));
         gabp::DenseArgs d{};
         d.K = K;
+        d.ld = Kp;
         d.A = G->dA;
         for (int b = 0; b < 3; ++b) d.msg[b] = G->dmsg[b];
         d.node = G->dnode;
+        d.pairs = G->dpairs;
+        d.npairs = G->dnpairs;
         SweepArgs a = make_args(G);
         const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : 8;
         CK(cudaEventRecord(G->ev[2], st));
@@ -858,8 +868,20 @@ int gabp_graph_create_dense(int64_t n, const double *h_a, const double *h_rhs, i
     gabp_graph *G = *out;
     G->is_dense = 1;
     G->K = n;
-    CK(cudaMalloc(&G->dA, sizeof(double) * n * n));
-    CK(cudaMemcpy(G->dA, h_a, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+    G->Kp = (n + 31) / 32 * 32;  // padded rows/columns: whole 32 x 32 tiles, zero A
+    const int64_t Kp = G->Kp;
+    CK(cudaMalloc(&G->dA, sizeof(double) * Kp * Kp));
+    CK(cudaMemset(G->dA, 0, sizeof(double) * Kp * Kp));
+    CK(cudaMemcpy2D(G->dA, sizeof(double) * Kp, h_a, sizeof(double) * n, sizeof(double) * n, n,
+                    cudaMemcpyHostToDevice));
+    const int64_t nt = Kp / 32;
+    std::vector<uint2> tp;
+    tp.reserve(nt * (nt + 1) / 2);
+    for (int64_t I = 0; I < nt; ++I)
+        for (int64_t J = I; J < nt; ++J) tp.push_back(make_uint2((unsigned)I, (unsigned)J));
+    G->dnpairs = (int64_t)tp.size();
+    CK(cudaMalloc(&G->dpairs, sizeof(uint2) * tp.size()));
+    CK(cudaMemcpy(G->dpairs, tp.data(), sizeof(uint2) * tp.size(), cudaMemcpyHostToDevice));
     return GABP_OK;
 }
 

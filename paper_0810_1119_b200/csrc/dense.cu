@@ -1,27 +1,35 @@
 // dense.cu -- broadcast sweep for a dense A (linear detection, BASELINE config 3).
 //
-// Storage: A is K x K row-major; messages are a padded K x K matrix M[k][j] = m_{k->j}
-// (sender-major, i.e. the out-slot layout of the sparse path; the diagonal and the exact
-// zeros of A -- non-edges in the reference, linalg.py:81-82 -- hold zero messages).
+// Storage: A is Kp x Kp row-major (Kp = K rounded up to 32, padding zero); messages are a
+// Kp x Kp matrix M[k][j] = m_{k->j} (sender-major: the out-slot layout of the sparse path).
+// The diagonal, the padding and the exact zeros of A -- non-edges in the reference
+// (linalg.py:81-82) -- hold zero messages and are skipped by the sums.
 // One launch s = two kernels:
 //
-//   column walk  one CTA per 32 columns: all four warps stream 32-row blocks of A and M
-//                (coalesced 256/512-byte row segments) into a 4-stage shared-memory ring
-//                with LDGSTS while lane l of warp 0 walks column i0+l -- the incoming
-//                messages of node i in ascending sender order, exactly the order of the
-//                reference's np.add.at (solver.py:242-243) -- and A's column for the
-//                residual row of x^{(s-2)}.  Non-edges are skipped, so the sums are bitwise
-//                those of the sparse path.  Writes P_i, P_i*mu~_i, x^{(s-1)}, residual
-//                partials.  (A thread-per-column walk without staging ran 3.8 ms at K=4096:
-//                4096 threads cannot keep HBM busy; the staged walk runs ~0.2 ms.)
-//   edge tiles   32 x 32 tiles: m_ij = f(P_i, N_i, m_ji, A_ij) (broadcast_sweep,
-//                solver.py:249-257) with m_ji read from the transposed tile through shared
-//                memory; max change / blowup / singular statistics; the last CTA runs the
-//                solve decision for sweep s-2 (same Ctrl protocol as the sparse kernel).
+//   column walk  one CTA per 32 columns: lane l of the summing warp walks column i0 + l in
+//                ascending row order -- the incoming messages of node i in ascending sender
+//                order, exactly the order of the reference's np.add.at (solver.py:242-243)
+//                -- and A's column for the residual row of x^{(s-2)}.  One producer lane
+//                streams the 32 x 32 blocks of A and M^{(s-1)} as 2-D tensor copies
+//                (cp.async.bulk.tensor, tensor maps over the padded matrices) and the
+//                x^{(s-2)} block as a 1-D bulk copy into a kColStages-deep mbarrier ring.
+//                Writes P_i, P_i mu~_i, x^{(s-1)}, residual partials.
+//   pair tiles   a CTA takes the tile pair (I, J), I <= J: M^{(s-1)}[I][J], M^{(s-1)}[J][I]
+//                and A[I][J] (A is symmetric) are staged once, and both directions are
+//                updated from them -- m_ij = f(P_i, N_i, m_ji, A_ij) and
+//                m_ji = f(P_j, N_j, m_ij, A_ij) (broadcast_sweep, solver.py:249-257) -- so
+//                each old message is read once, serving as one edge's previous value (the
+//                change statistic) and as its twin's input; the transposed result goes out
+//                through shared memory.  Max change / blowup / singular statistics; the last
+//                CTA runs the solve decision for sweep s-2 (the sparse kernel's protocol).
+// Per edge and sweep: 24 B in the walk, 16 + 4 + 16 B in the pair tiles (was 80 B with
+// one-direction tiles and a column walk without bulk copies).
+#include <cuda.h>  // CUtensorMap (the encoder is fetched at run time: no libcuda link)
+#include <cudaTypedefs.h>
 #include <float.h>
 #include <math.h>
 
-#include "gabp_internal.cuh"
+#include "sweep_common.cuh"
 
 namespace gabp {
 namespace {
@@ -38,112 +46,151 @@ __device__ __forceinline__ double warp_max_d(double v) {
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
-
-constexpr int kColRows = 32;     // rows of A / M per pipeline stage
-constexpr int kColStages = 4;
-constexpr int kColCta = 128;     // 32 columns per CTA; warp 0 sums, all warps load
-
 __device__ __forceinline__ uint32_t s_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cpa16(void *dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s_u32(dst)), "l"(src));
-}
-__device__ __forceinline__ void cpa8(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s_u32(dst)), "l"(src));
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cpa_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
+// ---- column walk -----------------------------------------------------------------------------
+constexpr int kColRows = 32;     // rows of A / M per ring stage
+constexpr int kColStages = 6;
+constexpr int kColCta = 64;      // warp 0 sums, warp 1 produces
+
+struct ColStage {
+    double A[kColRows][32];
+    double2 M[kColRows][32];
+    double X[kColRows];
+};
 struct ColSmem {
-    double A[kColStages][kColRows][32];
-    double2 M[kColStages][kColRows][32];
-    double X[kColStages][kColRows];
+    ColStage st[kColStages];
+    uint64_t full[kColStages];
+    uint64_t empty[kColStages];
     int64_t sweep;
     int skip;
 };
 
-// Stage rows [k0, k0 + kColRows) of columns [i0, i0 + 32) of A and M (and x^{(s-2)}[k]).
-__device__ __forceinline__ void col_stage(ColSmem &S, int st, int64_t k0, int64_t i0, int64_t K,
-                                          const double *A, const double2 *M,
-                                          const double *xprev, int tid) {
-    for (int q = tid; q < kColRows * 32; q += kColCta) {
-        const int r = q >> 5, c = q & 31;
-        const int64_t k = k0 + r, i = i0 + c;
-        if (k < K && i < K) {
-            cpa8(&S.A[st][r][c], A + k * K + i);
-            cpa16(&S.M[st][r][c], M + k * K + i);
-        }
-    }
-    if (xprev && tid < kColRows && k0 + tid < K) cpa8(&S.X[st][tid], xprev + k0 + tid);
+__device__ __forceinline__ void mb_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(s_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "DW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra DW_%=;\n}\n" ::"r"(s_u32(bar)),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
+__device__ __forceinline__ void bulk(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(bar))
+        : "memory");
 }
 
-// Column walk of launch s (solve mode): lane l of warp 0 walks column i0 + l in ascending
-// row order from a 4-stage shared-memory ring the whole CTA fills with LDGSTS.
-__global__ void __launch_bounds__(kColCta) dense_column_kernel(const SweepArgs a,
-                                                               const DenseArgs d) {
-    extern __shared__ __align__(16) unsigned char col_raw[];
+struct __align__(64) DenseMaps {
+    CUtensorMap A;     // Kp x Kp doubles, box 32 x 32
+    CUtensorMap M[3];  // Kp x 2Kp doubles (one double2 = two columns), box 32 x 64
+};
+
+__device__ __forceinline__ void tensor2d(void *dst, const CUtensorMap *map, int x, int y,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(s_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(s_u32(bar))
+        : "memory");
+}
+
+// Column walk of launch s (solve mode).
+__global__ void __launch_bounds__(kColCta, 1) dense_column_kernel(
+    const SweepArgs a, const DenseArgs d, const __grid_constant__ DenseMaps maps) {
+    extern __shared__ __align__(128) unsigned char col_raw[];
     ColSmem &S = *reinterpret_cast<ColSmem *>(col_raw);
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     if (tid == 0) {
         volatile Ctrl *vc = a.ctrl;
         const int64_t s = vc->next_sweep;
         S.skip = vc->done || s > vc->max_iter + 2;
         S.sweep = s;
     }
+    if (tid < kColStages) {
+        mb_init(&S.full[tid], 1u);
+        mb_init(&S.empty[tid], 1u);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
     if (S.skip) return;
     const int64_t s = S.sweep;
     const bool resid = s >= 3;
     const int64_t K = d.K;
-    const double2 *M = d.msg[(s - 1) % 3];
+    const CUtensorMap *mmap = &maps.M[(s - 1) % 3];
     const double *xprev = resid ? a.x[(s - 2) % 3] : nullptr;
     const int64_t i0 = (int64_t)blockIdx.x * 32;
     const int64_t nstage = (K + kColRows - 1) / kColRows;
-    for (int p = 0; p < kColStages - 1; ++p) {
-        if (p < nstage) col_stage(S, p, p * kColRows, i0, K, d.A, M, xprev, tid);
-        cpa_commit();
+
+    if (tid >= 32) {  // ---- producer lane: one 2-D copy each of A and M, the x block ----
+        if (lane == 0) {
+            for (int64_t t = 0; t < nstage; ++t) {
+                const int st = (int)(t % kColStages);
+                if (t >= kColStages)
+                    mb_wait(&S.empty[st], (unsigned)((t / kColStages) - 1) & 1u);
+                const int64_t k0 = t * kColRows;
+                const int rows = (int)((K - k0) < kColRows ? (K - k0) : kColRows);
+                // x block: whole 16-byte units (x arrays carry kNodePad >= 2 doubles of padding)
+                const unsigned xb = resid ? (unsigned)(((rows + 1) & ~1) * 8) : 0u;
+                mb_expect_tx(&S.full[st], (unsigned)(sizeof(double) * 32 * 32 +
+                                                     sizeof(double2) * 32 * 32) + xb);
+                tensor2d(&S.st[st].A[0][0], &maps.A, (int)i0, (int)k0, &S.full[st]);
+                tensor2d(&S.st[st].M[0][0], mmap, (int)(2 * i0), (int)k0, &S.full[st]);
+                if (xb) bulk(&S.st[st].X[0], xprev + k0, xb, &S.full[st]);
+            }
+        }
+        return;
     }
-    const int lane = tid & 31;
+    // ---- summing warp: lane = column ----
     const int64_t i = i0 + lane;
-    const bool sum_lane = tid < 32 && i < K;
+    const bool col = i < K;
     double sp = 0.0, sn = 0.0, y = 0.0;
-    if (sum_lane) {
+    if (col) {
         const NodeRec nd = a.nd[i];
         sp = nd.diag;
         sn = nd.pnum;
         y = resid ? nd.diag * xprev[i] : 0.0;
     }
     for (int64_t t = 0; t < nstage; ++t) {
-        cpa_wait<kColStages - 2>();
-        __syncthreads();  // stage t landed for every thread; stage t-1 fully consumed
-        const int64_t tn = t + kColStages - 1;
-        if (tn < nstage)
-            col_stage(S, (int)(tn % kColStages), tn * kColRows, i0, K, d.A, M, xprev, tid);
-        cpa_commit();
-        if (sum_lane) {
-            const int st = (int)(t % kColStages);
-            const int64_t k0 = t * kColRows;
-            const int rows = (int)((K - k0) < kColRows ? (K - k0) : kColRows);
-            for (int r = 0; r < rows; ++r) {  // ascending k: the reference's order
-                const int64_t k = k0 + r;
-                const double akj = S.A[st][r][lane];
-                if (k == i || akj == 0.0) continue;  // no edge
-                const double2 m = S.M[st][r][lane];
-                sp = sp + m.x;
-                sn = sn + m.x * m.y;
-                if (resid) y = y + akj * S.X[st][r];
+        const int st = (int)(t % kColStages);
+        mb_wait(&S.full[st], (unsigned)(t / kColStages) & 1u);
+        const ColStage &C = S.st[st];
+        const int64_t k0 = t * kColRows;
+        if (col) {
+            // all kColRows rows: the padding rows of the last block have A = 0 (no edge)
+#pragma unroll 16
+            for (int r = 0; r < kColRows; ++r) {  // ascending k: the reference's order
+                const double akj = C.A[r][lane];
+                const bool edge = k0 + r != i && akj != 0.0;  // non-edges add nothing
+                const double2 m = C.M[r][lane];
+                const double sp1 = sp + m.x, sn1 = sn + m.x * m.y;
+                sp = edge ? sp1 : sp;
+                sn = edge ? sn1 : sn;
+                if (resid) {
+                    const double y1 = y + akj * C.X[r];
+                    y = edge ? y1 : y;
+                }
             }
         }
+        __syncwarp();
+        if (lane == 0) mb_arrive(&S.empty[st]);
     }
-    cpa_wait<0>();
-    if (tid >= 32) return;
     double rsq = 0.0;
     unsigned bad = 0u, agg_sing = 0xffffffffu;
-    if (sum_lane) {
+    if (col) {
         double *xcur = a.x[(s - 1) % 3];
         double *pcur = a.p[(s - 1) % 3];
         double *xh = (a.xhist && s >= 2 && s - 1 <= a.xhist_rows) ? a.xhist + (s - 2) * a.n
@@ -171,8 +218,18 @@ __global__ void __launch_bounds__(kColCta) dense_column_kernel(const SweepArgs a
     }
 }
 
-struct TileSmem {
-    double2 t[kTile][kTile + 1];  // M^{(s-1)}[J][I] block, padded against bank conflicts
+// ---- pair tiles -------------------------------------------------------------------------
+constexpr int kPairCta = 256;  // 32 x 8 threads
+
+struct __align__(16) PairBuf {
+    double2 mij[kTile][kTile + 1];  // M^{(s-1)}[I][J]
+    double2 mji[kTile][kTile + 1];  // M^{(s-1)}[J][I]
+    double aij[kTile][kTile];       // A[I][J]
+    double2 ni[kTile], nj[kTile];   // {P, N} of the rows of I and J
+};
+struct PairSmem {
+    PairBuf b[2];
+    double2 out[kTile][kTile + 1];  // new M[J][I], staged for the coalesced store
     double red_d[8];
     unsigned red_u[8];
     int64_t sweep;
@@ -180,9 +237,54 @@ struct TileSmem {
     int last;
 };
 
-__global__ void __launch_bounds__(256) dense_edge_kernel(const SweepArgs a, const DenseArgs d,
-                                                         int64_t col_blocks) {
-    __shared__ TileSmem S;
+__device__ __forceinline__ void cpa16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// stage the pair (I, J) (tile indices) into buffer B
+__device__ __forceinline__ void pair_stage(PairBuf &B, int64_t I, int64_t J, const DenseArgs &d,
+                                           const double2 *M, int tid) {
+    const int64_t ld = d.ld, i0 = I * kTile, j0 = J * kTile;
+    for (int q = tid; q < kTile * kTile; q += kPairCta) {  // one double2 per copy
+        const int r = q >> 5, c = q & 31;
+        cpa16(&B.mij[r][c], M + (i0 + r) * ld + j0 + c);
+        cpa16(&B.mji[r][c], M + (j0 + r) * ld + i0 + c);
+    }
+    for (int q = tid; q < kTile * kTile / 2; q += kPairCta) {  // two doubles per copy
+        const int r = q >> 4, c = (q & 15) * 2;
+        cpa16(&B.aij[r][c], d.A + (i0 + r) * ld + j0 + c);
+    }
+    if (tid < kTile) {
+        cpa16(&B.ni[tid], d.node + i0 + tid);
+        cpa16(&B.nj[tid], d.node + j0 + tid);
+    }
+}
+
+struct PairStats {
+    double chg = 0.0;
+    unsigned oor = 0u;
+    unsigned long long sing = ~0ull;
+};
+
+// statistics of one new message against its previous value
+__device__ __forceinline__ void pair_stat(double2 nw, double2 old, double pe, uint64_t e,
+                                          double lim, PairStats &ps) {
+    if (pe == 0.0 && e < ps.sing) ps.sing = e;
+    const double d1 = fabs(nw.x - old.x), d2 = fabs(nw.y - old.y);
+    ps.chg = fmax(ps.chg, fmax(d1, d2));
+    if (!(fabs(nw.x) <= lim) || !(fabs(nw.y) <= lim)) ps.oor = 1u;
+}
+
+__global__ void __launch_bounds__(kPairCta) dense_pair_kernel(const SweepArgs a,
+                                                              const DenseArgs d,
+                                                              int64_t col_blocks) {
+    extern __shared__ __align__(16) unsigned char pair_raw[];
+    PairSmem &S = *reinterpret_cast<PairSmem *>(pair_raw);
     const int tid = threadIdx.x;
     Ctrl *ctrl = a.ctrl;
     if (tid == 0) {
@@ -194,52 +296,78 @@ __global__ void __launch_bounds__(256) dense_edge_kernel(const SweepArgs a, cons
     __syncthreads();
     if (S.skip) return;
     const int64_t s = S.sweep;
-    const int64_t K = d.K;
+    const int64_t K = d.K, ld = d.ld;
     const double2 *M = d.msg[(s - 1) % 3];
     double2 *Mo = d.msg[s % 3];
     const double lim = fmin(ctrl->blowup, DBL_MAX);
-    const int64_t nt = (K + kTile - 1) / kTile;
-    double chg = 0.0;
-    unsigned oor = 0u;
-    unsigned long long sing = ~0ull;
-    const int tx = tid & 31, ty = tid >> 5;  // 32 x 8 threads
-    for (int64_t t = blockIdx.x; t < nt * nt; t += gridDim.x) {
-        const int64_t I = (t / nt) * kTile, J = (t % nt) * kTile;
-        // stage M[J + r][I + c] (the reverse messages of this tile)
-        for (int r = ty; r < kTile; r += 8) {
-            const int64_t jr = J + r, ic = I + tx;
-            S.t[r][tx] = (jr < K && ic < K) ? __ldcg(M + jr * K + ic) : make_double2(0.0, 0.0);
-        }
-        __syncthreads();
-        for (int r = ty; r < kTile; r += 8) {
-            const int64_t i = I + r, j = J + tx;
-            if (i >= K || j >= K || i == j) continue;
-            const double c = __ldg(d.A + i * K + j);
-            if (c == 0.0) continue;
-            const double2 rev = S.t[tx][r];  // m_{j->i}
-            const double2 nd = __ldg(d.node + i);
-            const double pe = nd.x - rev.x;
-            const double num = nd.y - rev.x * rev.y;
-            const double np_ = (-c * c) / pe;
-            const double nm = num / c;
-            const int64_t e = i * K + j;
-            const double2 old = __ldcs(M + e);
-            __stcs(Mo + e, make_double2(np_, nm));
-            if (pe == 0.0 && (unsigned long long)e < sing) sing = (unsigned long long)e;
-            const double d1 = fabs(np_ - old.x), d2 = fabs(nm - old.y);
-            chg = d1 > chg ? d1 : chg;
-            chg = d2 > chg ? d2 : chg;
-            if (!(fabs(np_) <= lim) || !(fabs(nm) <= lim)) oor = 1u;
-        }
-        __syncthreads();
+    const int64_t npairs = d.npairs;
+    PairStats ps;
+    const int tx = tid & 31, ty = tid >> 5;
+    int64_t p = blockIdx.x;
+    if (p < npairs) {
+        const uint2 ij = d.pairs[p];
+        pair_stage(S.b[0], ij.x, ij.y, d, M, tid);
     }
+    cpa_commit();
+    for (int k = 0; p < npairs; p += gridDim.x, ++k) {
+        const int64_t pn = p + gridDim.x;
+        if (pn < npairs) {
+            const uint2 ij = d.pairs[pn];
+            pair_stage(S.b[(k + 1) & 1], ij.x, ij.y, d, M, tid);
+        }
+        cpa_commit();
+        cpa_wait<1>();
+        __syncthreads();  // pair p landed for every thread
+        const PairBuf &B = S.b[k & 1];
+        const uint2 ij = d.pairs[p];
+        const int64_t I = ij.x, J = ij.y, i0 = I * kTile, j0 = J * kTile;
+        const bool diag = I == J;
+        for (int r = ty; r < kTile; r += 8) {
+            const int64_t i = i0 + r, j = j0 + tx;
+            const double c = B.aij[r][tx];
+            double2 nij = make_double2(0.0, 0.0), nji = make_double2(0.0, 0.0);
+            if (c != 0.0 && i != j && i < K && j < K) {
+                // m = f(node, twin message, A) = (-c^2 / pe, (N - P_t mu_t) / c) for both
+                // directions (solver.py:249-257): the four divisions overlap on the
+                // compiler's fast path; the rare out-of-range operand redoes all four
+                const double2 oij = B.mij[r][tx], oji = B.mji[tx][r];
+                const double2 ndi = B.ni[r], ndj = B.nj[tx];
+                const double pe1 = ndi.x - oji.x, num1 = ndi.y - oji.x * oji.y;
+                const double pe2 = ndj.x - oij.x, num2 = ndj.y - oij.x * oij.y;
+                const double cc = -c * c;
+                bool k1, k2, k3, k4;
+                nij.x = ddiv_fast(cc, pe1, k1);
+                nij.y = ddiv_fast(num1, c, k2);
+                nji.x = ddiv_fast(cc, pe2, k3);
+                nji.y = ddiv_fast(num2, c, k4);
+                if (!(k1 && k2 && k3 && k4)) {
+                    nij.x = div_slow(cc, pe1);
+                    nij.y = div_slow(num1, c);
+                    nji.x = div_slow(cc, pe2);
+                    nji.y = div_slow(num2, c);
+                }
+                pair_stat(nij, oij, pe1, (uint64_t)(i * K + j), lim, ps);
+                if (diag)
+                    nji = make_double2(0.0, 0.0);  // (the (j, i) element of the tile does it)
+                else
+                    pair_stat(nji, oji, pe2, (uint64_t)(j * K + i), lim, ps);
+            }
+            __stcs(Mo + i * ld + j, nij);
+            S.out[tx][r] = nji;
+        }
+        __syncthreads();  // out complete; buffer k&1 free for the prefetch two pairs ahead
+        if (!diag)
+            for (int r = ty; r < kTile; r += 8) __stcs(Mo + (j0 + r) * ld + i0 + tx, S.out[r][tx]);
+    }
+    cpa_wait<0>();
     // CTA reductions + last-CTA decision (the sparse kernel's protocol)
     const int warp = tid >> 5, lane = tid & 31;
-    chg = warp_max_d(chg);
-    oor = __reduce_or_sync(~0u, oor);
-    const unsigned sl = (unsigned)(sing & 0xffffffffu), sh = (unsigned)(sing >> 32);
+    double chg = warp_max_d(ps.chg);
+    const unsigned oor = __reduce_or_sync(~0u, ps.oor);
+    const unsigned sl = (unsigned)(ps.sing & 0xffffffffu), sh = (unsigned)(ps.sing >> 32);
     const unsigned msh = __reduce_min_sync(~0u, sh);
     const unsigned msl = __reduce_min_sync(~0u, sh == msh ? sl : 0xffffffffu);
+    __syncthreads();  // (the last pair's transposed store read S.out)
     if (lane == 0) {
         S.red_d[warp] = chg;
         S.red_u[warp] = oor;
@@ -270,7 +398,7 @@ __global__ void __launch_bounds__(256) dense_edge_kernel(const SweepArgs a, cons
     double part = 0.0;
     if (s >= 3) {
         volatile const double *rp = a.rsq_part;
-        for (int64_t b = tid; b < col_blocks; b += 256) part += rp[b];
+        for (int64_t b = tid; b < col_blocks; b += kPairCta) part += rp[b];
     }
     part = warp_sum_d(part);
     if (lane == 0) S.red_d[warp] = part;
@@ -291,28 +419,76 @@ __global__ void __launch_bounds__(256) dense_edge_kernel(const SweepArgs a, cons
     }
 }
 
-int g_edge_grid = 0;
+int g_pair_grid = 0;
+
+// Tensor maps of the current dense buffers (re-encoded when the buffers change).
+DenseMaps g_maps;
+const void *g_maps_key[4] = {nullptr, nullptr, nullptr, nullptr};
+
+cudaError_t encode_maps(const DenseArgs &d) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint32_t elem[2] = {1, 1};
+    {
+        const cuuint64_t dim[2] = {(cuuint64_t)d.ld, (cuuint64_t)d.ld};
+        const cuuint64_t stride[1] = {(cuuint64_t)d.ld * sizeof(double)};
+        const cuuint32_t box[2] = {32, 32};
+        if (encode(&g_maps.A, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(d.A), dim,
+                   stride, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    for (int b = 0; b < 3; ++b) {
+        const cuuint64_t dim[2] = {(cuuint64_t)(2 * d.ld), (cuuint64_t)d.ld};
+        const cuuint64_t stride[1] = {(cuuint64_t)d.ld * sizeof(double2)};
+        const cuuint32_t box[2] = {64, 32};
+        if (encode(&g_maps.M[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, d.msg[b], dim, stride, box,
+                   elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    g_maps_key[0] = d.A;
+    for (int b = 0; b < 3; ++b) g_maps_key[b + 1] = d.msg[b];
+    return cudaSuccess;
+}
 
 }  // namespace
 
 cudaError_t launch_dense_sweep(const SweepArgs &a, const DenseArgs &d, cudaStream_t st) {
-    if (g_edge_grid == 0) {
-        cudaFuncSetAttribute(dense_column_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(ColSmem));
+    if (g_maps_key[0] != d.A || g_maps_key[1] != d.msg[0] || g_maps_key[2] != d.msg[1] ||
+        g_maps_key[3] != d.msg[2]) {
+        cudaError_t e = encode_maps(d);
+        if (e != cudaSuccess) return e;
+    }
+    if (g_pair_grid == 0) {
+        cudaError_t e = cudaFuncSetAttribute(
+            dense_column_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ColSmem));
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(dense_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(PairSmem));
+        if (e != cudaSuccess) return e;
         int dev = 0, sms = 0, occ = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dense_edge_kernel, 256, 0);
-        g_edge_grid = sms * (occ > 0 ? occ : 1);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dense_pair_kernel, kPairCta,
+                                                      sizeof(PairSmem));
+        g_pair_grid = sms * (occ > 0 ? occ : 1);
     }
-    const int64_t cb = (d.K + 31) / 32;
-    dense_column_kernel<<<(unsigned)cb, kColCta, sizeof(ColSmem), st>>>(a, d);
+    const int64_t cb = d.ld / 32;
+    dense_column_kernel<<<(unsigned)cb, kColCta, sizeof(ColSmem), st>>>(a, d, g_maps);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const int64_t nt = (d.K + kTile - 1) / kTile;
-    int64_t grid = g_edge_grid;
-    if (grid > nt * nt) grid = nt * nt;
-    dense_edge_kernel<<<(unsigned)grid, 256, 0, st>>>(a, d, cb);
+    int64_t grid = g_pair_grid;
+    if (grid > d.npairs) grid = d.npairs;
+    dense_pair_kernel<<<(unsigned)grid, kPairCta, sizeof(PairSmem), st>>>(a, d, cb);
     return cudaGetLastError();
 }
 

@@ -208,9 +208,12 @@ __device__ __forceinline__ void decide_sweep(volatile Ctrl *c, SweepArgs const &
 // dense variant (dense.cu): A row-major K x K, messages a padded K x K matrix ring
 struct DenseArgs {
     int64_t K;
+    int64_t ld;      // leading dimension: K rounded up to 32 (A, msg and node are padded)
     const double *A;
     double2 *msg[3];
     double2 *node;   // {P_i, P_i mu~_i} of the state read by the launch
+    const uint2 *pairs;  // upper-triangle tile pairs (I <= J) of the pair-tile kernel
+    int64_t npairs;
 };
 cudaError_t launch_dense_sweep(const SweepArgs &a, const DenseArgs &d, cudaStream_t st);
 
