@@ -167,6 +167,23 @@ int gabp_sweep(const gabp_graph_t *g, gabp_state_t *s, int32_t schedule, double 
 int gabp_infer_marginals(const gabp_graph_t *g, const gabp_state_t *s, double *h_means,
                          double *h_precs);
 
+/* ---- acceleration (acceleration.py) --------------------------------------------- */
+
+/* Steffensen restart (acceleration.py:177-183 gated_extrapolate, :74-96 aitken_extrapolate,
+ * applied by set_target to the mean messages, :123-126): the mean messages of x2 are
+ * replaced in place by the componentwise Aitken extrapolant of the mean messages of x0,
+ * x1, x2 -- gated (gated != 0: kept only where |second difference| >= stability x
+ * max(|first differences|), x2 elsewhere) or plain.  Precision messages are untouched.
+ * Bitwise equal to the numpy expressions. */
+int gabp_state_extrapolate(const gabp_state_t *x0, const gabp_state_t *x1, gabp_state_t *x2,
+                           double guard, double stability, int32_t gated);
+/* _GabpStepper.blown() (acceleration.py:128-133): *blown = 1 when a message is not finite
+ * or max |message| > blowup. */
+int gabp_state_blown(const gabp_state_t *s, double blowup, int32_t *blown);
+/* np.max(np.abs(a.mean - b.mean), initial=0.0) (acceleration.py:259): NaN if any
+ * difference is NaN. */
+int gabp_state_mean_max_diff(const gabp_state_t *a, const gabp_state_t *b, double *out);
+
 /* ---- solve (solver.py:307-346) ---------------------------------------------------- */
 
 /* solve(system, options) on a built graph.  Runs the sweep loop on the device with a

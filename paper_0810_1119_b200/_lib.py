@@ -118,6 +118,10 @@ def load():
         "gabp_sweep": (ctypes.c_int, [_vp, _vp, _i32, _dp, ctypes.POINTER(_i64),
                                       ctypes.POINTER(_i32)]),
         "gabp_infer_marginals": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+        "gabp_state_extrapolate": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double,
+                                                  ctypes.c_double, _i32]),
+        "gabp_state_blown": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.POINTER(_i32)]),
+        "gabp_state_mean_max_diff": (ctypes.c_int, [_vp, _vp, _dp]),
         "gabp_solve": (ctypes.c_int, [_vp, ctypes.POINTER(Options), _vp, _vp, _vp, _vp,
                                       ctypes.POINTER(Report)]),
         "gabp_solve_device": (ctypes.c_int, [_vp, ctypes.POINTER(Options), _vp, _vp,

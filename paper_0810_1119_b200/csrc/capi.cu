@@ -964,10 +964,10 @@ int gabp_state_create(const gabp_graph_t *G, gabp_state_t **out) {
     S->g = G;
     const_cast<gabp_graph *>(G)->refs.fetch_add(1);
     const int64_t E = G->g.E > 0 ? G->g.E : 1;
-    for (int b = 0; b < 2; ++b) {
-        cudaError_t e = cudaMalloc(&S->buf[b], sizeof(double2) * E);
+    for (int b = 0; b < 2; ++b) {  // (stream-ordered pool blocks: a state per sweep is cheap)
+        cudaError_t e = cudaMallocAsync(&S->buf[b], sizeof(double2) * E, G->stream);
         if (e != cudaSuccess) {
-            cudaFree(S->buf[0]);
+            if (S->buf[0]) cudaFreeAsync(S->buf[0], G->stream);
             graph_release(const_cast<gabp_graph *>(G));
             delete S;
             return fail(GABP_ENOMEM, "state allocation: %s", cudaGetErrorString(e));
@@ -995,9 +995,9 @@ int gabp_state_clone(const gabp_state_t *S, gabp_state_t **out) {
 void gabp_state_destroy(gabp_state_t *S) {
     if (!S) return;
     cudaSetDevice(S->g->device);
+    cudaFreeAsync(S->buf[0], S->g->stream);
+    cudaFreeAsync(S->buf[1], S->g->stream);
     cudaStreamSynchronize(S->g->stream);
-    cudaFree(S->buf[0]);
-    cudaFree(S->buf[1]);
     graph_release(const_cast<gabp_graph *>(S->g));
     delete S;
 }
@@ -1093,6 +1093,57 @@ int gabp_sweep(const gabp_graph_t *Gc, gabp_state_t *S, int32_t schedule, double
     S->cur ^= 1;
     S->iteration += 1;
     S->messages_sent += (schedule == GABP_SCHED_BROADCAST) ? G->g.n : G->g.E;
+    return GABP_OK;
+}
+
+// ---- acceleration (acceleration.py) --------------------------------------------------------
+
+int gabp_state_extrapolate(const gabp_state_t *x0, const gabp_state_t *x1, gabp_state_t *x2,
+                           double guard, double stability, int32_t gated) {
+    if (!x0 || !x1 || !x2) return fail(GABP_EINVAL, "NULL state");
+    if (x0->g != x2->g || x1->g != x2->g) return fail(GABP_EINVAL, "states of different graphs");
+    if (!(guard > 0.0)) return fail(GABP_EINVAL, "denom_guard must be positive");
+    const gabp_graph *G = x2->g;
+    CK(cudaSetDevice(G->device));
+    CK(gabp::launch_extrapolate(G->g.E, x0->buf[x0->cur], x1->buf[x1->cur], x2->buf[x2->cur],
+                                guard, stability, gated ? 1 : 0, G->stream));
+    CK(cudaStreamSynchronize(G->stream));
+    return GABP_OK;
+}
+
+static int absmax_bits(const gabp_graph *G, const double2 *a, const double2 *b, int which,
+                       unsigned long long *bits) {
+    unsigned long long *d = nullptr;
+    CK(cudaMallocAsync(&d, sizeof(unsigned long long), G->stream));
+    CK(gabp::launch_absmax(G->g.E, a, b, which, d, G->stream));
+    CK(cudaMemcpyAsync(bits, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, G->stream));
+    CK(cudaFreeAsync(d, G->stream));
+    CK(cudaStreamSynchronize(G->stream));
+    return GABP_OK;
+}
+
+int gabp_state_blown(const gabp_state_t *S, double blowup, int32_t *blown) {
+    if (!S || !blown) return fail(GABP_EINVAL, "NULL argument");
+    CK(cudaSetDevice(S->g->device));
+    unsigned long long bits = 0;
+    const double2 *m = S->buf[S->cur];
+    int rc = absmax_bits(S->g, m, m, 0, &bits);
+    if (rc) return rc;
+    const unsigned long long inf_bits = 0x7ff0000000000000ull;
+    // not every message finite, or the biggest |message| above blowup (acceleration.py:150-155)
+    *blown = bits >= inf_bits || __builtin_bit_cast(double, bits) > blowup;
+    return GABP_OK;
+}
+
+int gabp_state_mean_max_diff(const gabp_state_t *a, const gabp_state_t *b, double *out) {
+    if (!a || !b || !out) return fail(GABP_EINVAL, "NULL argument");
+    if (a->g != b->g) return fail(GABP_EINVAL, "states of different graphs");
+    CK(cudaSetDevice(a->g->device));
+    unsigned long long bits = 0;
+    int rc = absmax_bits(a->g, a->buf[a->cur], b->buf[b->cur], 1, &bits);
+    if (rc) return rc;
+    // np.max(np.abs(y - y_prev), initial=0.0): NaN if any difference is NaN
+    *out = bits > 0x7ff0000000000000ull ? NAN : __builtin_bit_cast(double, bits);
     return GABP_OK;
 }
 

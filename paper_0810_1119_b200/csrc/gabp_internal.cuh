@@ -217,6 +217,14 @@ struct DenseArgs {
 };
 cudaError_t launch_dense_sweep(const SweepArgs &a, const DenseArgs &d, cudaStream_t st);
 
+// acceleration (accel.cu): gated Aitken restart of the mean messages, in place in m2
+// (gated = 0: plain aitken_extrapolate); max |.| reductions as ordered bit patterns
+// (which = 0: both components of a, 1: |a.mu - b.mu|), result in *d_out
+cudaError_t launch_extrapolate(int64_t E, const double2 *m0, const double2 *m1, double2 *m2,
+                               double guard, double stability, int gated, cudaStream_t st);
+cudaError_t launch_absmax(int64_t E, const double2 *a, const double2 *b, int which,
+                          unsigned long long *d_out, cudaStream_t st);
+
 // multi-rank helpers (dist.cu)
 cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st);
 cudaError_t launch_halo_pack(const SweepArgs &a, const uint32_t *idx, int64_t cnt, double *buf,
