@@ -63,11 +63,12 @@ __device__ __forceinline__ double qdiv(double a, double b, Stats &st) {
 
 // msg(agg, m): the outgoing message of an edge from its row aggregate and the incoming
 // pair, as (P, mu) (solver.py:249-257)
+// rc = ddiv_rcp(c): both messages of an edge divide by A_ij and share the reciprocal
 template <bool EXACT>
-__device__ __forceinline__ void edge_msg(double c, double pe, double num, double &P, double &mu,
-                                         Stats &st) {
+__device__ __forceinline__ void edge_msg(double c, double rc, double pe, double num, double &P,
+                                         double &mu, Stats &st) {
     P = qdiv<EXACT>(-c * c, pe, st);
-    mu = qdiv<EXACT>(num, c, st);
+    mu = EXACT ? num / c : ddiv_fast_acc_r(num, c, rc, st.dr);
 }
 
 // CSR edge id of the message j -> i held in slot q of position p (exact launch only)
@@ -232,17 +233,18 @@ __device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, S
                     i3[u] = make_double2(0.0, 0.0);
                 }
             }
-            double m2p[kUL], m2m[kUL], ip[kUL], im[kUL], pe[kUL];
+            double m2p[kUL], m2m[kUL], ip[kUL], im[kUL], pe[kUL], rc[kUL];
 #pragma unroll
             for (int u = 0; u < kUL; ++u) {
                 const bool v = q0 + u < d;
                 if (!v) c[u] = 1.0;
+                rc[u] = EXACT ? 0.0 : ddiv_rcp(c[u]);
                 m2p[u] = 0.0;  // m^{(0)} = 0 at launch 2
                 m2m[u] = 0.0;
                 if (PH == 3) {  // own outgoing message of sweep s-2
                     const double pe2 = v ? a3.x - i3[u].x : 1.0;
                     const double nu2 = v ? a3.y - i3[u].x * i3[u].y : 1.0;
-                    edge_msg<EXACT>(c[u], pe2, nu2, m2p[u], m2m[u], st);
+                    edge_msg<EXACT>(c[u], rc[u], pe2, nu2, m2p[u], m2m[u], st);
                 }
             }
 #pragma unroll
@@ -250,7 +252,7 @@ __device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, S
                 const bool v = q0 + u < d;
                 pe[u] = v ? gP[u] - m2p[u] : 1.0;
                 const double num = v ? gN[u] - m2p[u] * m2m[u] : 1.0;
-                edge_msg<EXACT>(c[u], pe[u], num, ip[u], im[u], st);
+                edge_msg<EXACT>(c[u], rc[u], pe[u], num, ip[u], im[u], st);
             }
 #pragma unroll
             for (int u = 0; u < kUL; ++u) {
@@ -462,18 +464,19 @@ __device__ __forceinline__ void slice_sweep_pipe(const SweepArgs &a, int64_t s, 
                 rhs_i = S.rhs[lane];
             }
         }
-        double c[kUP], m2p[kUP], m2m[kUP], ip[kUP], im[kUP], pe[kUP];
+        double c[kUP], m2p[kUP], m2m[kUP], ip[kUP], im[kUP], pe[kUP], rc[kUP];
 #pragma unroll
         for (int u = 0; u < kUP; ++u) {
             const bool v = C.b * kUP + u < d;
             c[u] = v ? S.c[u][lane] : 1.0;
+            rc[u] = ddiv_rcp(c[u]);
             m2p[u] = 0.0;  // m^{(0)} = 0 at launch 2
             m2m[u] = 0.0;
             if (PH == 3) {  // own outgoing message of sweep s-2
                 const double2 i3 = S.i3[u][lane];
                 const double pe2 = v ? a3.x - i3.x : 1.0;
                 const double nu2 = v ? a3.y - i3.x * i3.y : 1.0;
-                edge_msg<EXACT>(c[u], pe2, nu2, m2p[u], m2m[u], st);
+                edge_msg<EXACT>(c[u], rc[u], pe2, nu2, m2p[u], m2m[u], st);
             }
         }
 #pragma unroll
@@ -482,7 +485,7 @@ __device__ __forceinline__ void slice_sweep_pipe(const SweepArgs &a, int64_t s, 
             const double2 ag = S.ag[u][lane];
             pe[u] = v ? ag.x - m2p[u] : 1.0;
             const double num = v ? ag.y - m2p[u] * m2m[u] : 1.0;
-            edge_msg<EXACT>(c[u], pe[u], num, ip[u], im[u], st);
+            edge_msg<EXACT>(c[u], rc[u], pe[u], num, ip[u], im[u], st);
         }
         const int64_t p = C.sl * 32 + lane;
 #pragma unroll
@@ -724,12 +727,13 @@ __device__ __forceinline__ void grp_consume(const SweepArgs &a, int64_t s, Stats
         }
         const int s0 = (int)(k % kGS);
         const GStage &S = G.st[s0];
-        double cc[kGC], m2p[kGC], m2m[kGC], ip[kGC], im[kGC], pe[kGC];
+        double cc[kGC], m2p[kGC], m2m[kGC], ip[kGC], im[kGC], pe[kGC], rc[kGC];
         double2 i2v[kGC];
 #pragma unroll
         for (int u = 0; u < kGC; ++u) {
             const bool v = m.b * kGC + u < d;
             cc[u] = v ? S.c[u][t] : 1.0;
+            rc[u] = ddiv_rcp(cc[u]);
             m2p[u] = 0.0;  // m^{(0)} = 0 at launch 2
             m2m[u] = 0.0;
             i2v[u] = make_double2(0.0, 0.0);
@@ -738,7 +742,7 @@ __device__ __forceinline__ void grp_consume(const SweepArgs &a, int64_t s, Stats
                 i2v[u] = S.i2[u][t];
                 const double pe2 = v ? a3.x - i3.x : 1.0;
                 const double nu2 = v ? a3.y - i3.x * i3.y : 1.0;
-                edge_msg<false>(cc[u], pe2, nu2, m2p[u], m2m[u], st);
+                edge_msg<false>(cc[u], rc[u], pe2, nu2, m2p[u], m2m[u], st);
             }
         }
         __syncwarp();
@@ -748,7 +752,7 @@ __device__ __forceinline__ void grp_consume(const SweepArgs &a, int64_t s, Stats
             const bool v = m.b * kGC + u < d;
             pe[u] = v ? gP[u] - m2p[u] : 1.0;
             const double num = v ? gN[u] - m2p[u] * m2m[u] : 1.0;
-            edge_msg<false>(cc[u], pe[u], num, ip[u], im[u], st);
+            edge_msg<false>(cc[u], rc[u], pe[u], num, ip[u], im[u], st);
         }
         const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
 #pragma unroll
