@@ -29,6 +29,7 @@ GATHER_IDS = {"auto": 0, "message": 1, "recompute": 2, "slice": 3}
 # every symbol include/gabp_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED = (
     "gabp_last_error", "gabp_version", "gabp_device_count",
+    "gabp_state_extrapolate", "gabp_state_blown", "gabp_state_mean_max_diff",
     "gabp_graph_create", "gabp_graph_create_device", "gabp_graph_create_dense",
     "gabp_graph_destroy", "gabp_graph_info", "gabp_graph_export", "gabp_graph_set_rhs",
     "gabp_graph_stream",

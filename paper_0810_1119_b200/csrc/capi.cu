@@ -63,6 +63,7 @@ struct NcclApi {
 
 // Multi-rank state of a graph that holds one rank's row block.
 struct DistState {
+    bool comm_nccl = true;         // false for in-process partitions (device copies)
     int rank = 0, world = 1;
     int64_t n_global = 0;
     double bnorm = 0.0;
@@ -73,6 +74,9 @@ struct DistState {
     uint32_t *d_sidx = nullptr, *d_ridx = nullptr;
     double *d_sbuf = nullptr, *d_rbuf = nullptr;       // 4 doubles per node, per-peer blocks
     double *d_stats = nullptr;                          // [0..4] max, [5] sum
+    // split sweep (boundary groups, then interior groups under the exchange)
+    cudaStream_t xstream = nullptr;  // exchange stream
+    cudaEvent_t ev_bnd = nullptr, ev_sweep = nullptr, ev_done = nullptr;
 };
 
 // pinned host mirror of a graph's controller and poll flags (capi.cu pinned_get)
@@ -366,6 +370,10 @@ SweepArgs make_args(gabp_graph *G) {
     a.srhs = g.srhs;
     a.scol = g.scol;
     a.scoef = g.scoef;
+    a.sl_lo = 0;
+    a.sl_hi = g.nslices;
+    a.part_base = 0;
+    a.exact_primary = 0;
     return a;
 }
 
@@ -387,6 +395,10 @@ void release_workspace(gabp_graph *G) {
         cudaFree(G->dist->d_sbuf);
         cudaFree(G->dist->d_rbuf);
         cudaFree(G->dist->d_stats);
+        if (G->dist->xstream) cudaStreamDestroy(G->dist->xstream);
+        if (G->dist->ev_bnd) cudaEventDestroy(G->dist->ev_bnd);
+        if (G->dist->ev_sweep) cudaEventDestroy(G->dist->ev_sweep);
+        if (G->dist->ev_done) cudaEventDestroy(G->dist->ev_done);
         if (G->dist->comm && g_nccl.commDestroy) g_nccl.commDestroy(G->dist->comm);
         delete G->dist;
         G->dist = nullptr;
@@ -542,9 +554,94 @@ int finish_loop(gabp_graph *G, double *device_ms) {
     return GABP_OK;
 }
 
+constexpr int kReserveSms = 2;  // SMs the interior part leaves to the exchange kernels
+
+int dist_ensure_comm(DistState *D) {
+    if (D->xstream) return GABP_OK;
+    CK(cudaStreamCreateWithFlags(&D->xstream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&D->ev_bnd, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&D->ev_sweep, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&D->ev_done, cudaEventDisableTiming));
+    return GABP_OK;
+}
+
+// Split sweep of a multi-rank slice-path launch: the leading bnd_groups groups hold every
+// row a peer needs.  Worth it when they are a minority (structured partitions); for a
+// random graph nearly every row is a boundary row and the sweep stays whole.
+int64_t split_slices(const gabp_graph *G) {
+    const DeviceGraph &g = G->g;
+    if (g.nslices == 0 || g.slice_variant == 1 || g.bnd_groups <= 0) return 0;
+    const int64_t ng = g.nslices / 15;  // (kGroup; the split is at whole groups)
+    if (2 * g.bnd_groups > ng) return 0;
+    return g.bnd_groups * 15;
+}
+
+// Launches of one split sweep: boundary part (exact) on st, then the interior part (fast +
+// twin) on st; the halo of the boundary part moves on the comm stream meanwhile (pack,
+// grouped send/recv, unpack), and the statistics are reduced and the decision taken after
+// both.  The next launch waits for all of it.
+int dist_launch_split(gabp_graph *G, const SweepArgs &a, int64_t nbs, cudaStream_t st,
+                      cudaStream_t cs) {
+    DistState *D = G->dist;
+    SweepArgs b = a;
+    b.sl_lo = 0;
+    b.sl_hi = nbs;
+    int64_t gb = 0;
+    CK(gabp::launch_slice_boundary(b, &gb, st));
+    CK(cudaEventRecord(D->ev_bnd, st));
+    SweepArgs in = a;
+    in.sl_lo = nbs;
+    in.part_base = gb;
+    CK(gabp::launch_slice_part(in, kReserveSms, st));
+    CK(cudaEventRecord(D->ev_sweep, st));
+    // exchange of the boundary rows' new states, under the interior part
+    CK(cudaStreamWaitEvent(cs, D->ev_bnd, 0));
+    for (size_t q = 0; q < D->peers.size(); ++q)
+        CK(gabp::launch_halo_pack(a, D->d_sidx + D->soff[q], D->scount[q],
+                                  D->d_sbuf + 4 * D->soff[q], cs, 1));
+    if (D->comm_nccl) {
+        NK(g_nccl.groupStart());
+        for (size_t q = 0; q < D->peers.size(); ++q) {
+            if (D->scount[q])
+                NK(g_nccl.send(D->d_sbuf + 4 * D->soff[q], 4 * D->scount[q], ncclFloat64,
+                               D->peers[q], D->comm, cs));
+            if (D->rcount[q])
+                NK(g_nccl.recv(D->d_rbuf + 4 * D->roff[q], 4 * D->rcount[q], ncclFloat64,
+                               D->peers[q], D->comm, cs));
+        }
+        NK(g_nccl.groupEnd());
+    }
+    return GABP_OK;
+}
+
+int dist_finish_split(gabp_graph *G, const SweepArgs &a, cudaStream_t st, cudaStream_t cs) {
+    DistState *D = G->dist;
+    for (size_t q = 0; q < D->peers.size(); ++q)
+        CK(gabp::launch_halo_unpack(a, D->d_ridx + D->roff[q], D->rcount[q],
+                                    D->d_rbuf + 4 * D->roff[q], cs, 1));
+    CK(cudaStreamWaitEvent(cs, D->ev_sweep, 0));
+    if (D->world > 1 && D->comm_nccl) {
+        NK(g_nccl.allReduce(D->d_stats, D->d_stats, 5, ncclFloat64, ncclMax, D->comm, cs));
+        NK(g_nccl.allReduce(D->d_stats + 5, D->d_stats + 5, 1, ncclFloat64, ncclSum, D->comm,
+                            cs));
+    }
+    CK(gabp::launch_finish(a, cs));
+    CK(cudaEventRecord(D->ev_done, cs));
+    CK(cudaStreamWaitEvent(st, D->ev_done, 0));
+    return GABP_OK;
+}
+
 // One multi-rank launch on this rank, NCCL transport: sweep, all-reduce of the launch's
 // statistics, decision, halo exchange of the node aggregates and marginals.
 int dist_launch_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
+    DistState *D0 = G->dist;
+    if (const int64_t nbs = split_slices(G)) {
+        int rc = dist_ensure_comm(D0);
+        if (rc) return rc;
+        rc = dist_launch_split(G, a, nbs, st, D0->xstream);
+        if (rc) return rc;
+        return dist_finish_split(G, a, st, D0->xstream);
+    }
     DistState *D = G->dist;
     CK(gabp::launch_sweep(a, GABP_SCHED_BROADCAST, gabp::kModeSolve, dist_gather(G), st));
     if (D->world > 1) {
@@ -556,7 +653,7 @@ int dist_launch_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
     if (D->peers.empty()) return GABP_OK;
     for (size_t q = 0; q < D->peers.size(); ++q)
         CK(gabp::launch_halo_pack(a, D->d_sidx + D->soff[q], D->scount[q],
-                                  D->d_sbuf + 4 * D->soff[q], st));
+                                  D->d_sbuf + 4 * D->soff[q], st, 0));
     NK(g_nccl.groupStart());
     for (size_t q = 0; q < D->peers.size(); ++q) {
         if (D->scount[q])
@@ -569,7 +666,7 @@ int dist_launch_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
     NK(g_nccl.groupEnd());
     for (size_t q = 0; q < D->peers.size(); ++q)
         CK(gabp::launch_halo_unpack(a, D->d_ridx + D->roff[q], D->rcount[q],
-                                    D->d_rbuf + 4 * D->roff[q], st));
+                                    D->d_rbuf + 4 * D->roff[q], st, 0));
     return GABP_OK;
 }
 
@@ -1321,9 +1418,20 @@ int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_optio
     CK(cudaEventRecord(G0->ev[2], G0->stream));
     const int64_t total = opt->max_iter + 2;
     for (int64_t s = 0; s < total; ++s) {
-        for (int p = 0; p < nparts; ++p)
-            CK(gabp::launch_sweep(args[p], GABP_SCHED_BROADCAST, gabp::kModeSolve,
-                                  dist_gather(parts[p]), parts[p]->stream));
+        for (int p = 0; p < nparts; ++p) {
+            if (const int64_t nbs = split_slices(parts[p])) {  // the NCCL path's split sweep
+                SweepArgs b = args[p], in = args[p];
+                b.sl_hi = nbs;
+                int64_t gb = 0;
+                CK(gabp::launch_slice_boundary(b, &gb, parts[p]->stream));
+                in.sl_lo = nbs;
+                in.part_base = gb;
+                CK(gabp::launch_slice_part(in, kReserveSms, parts[p]->stream));
+            } else {
+                CK(gabp::launch_sweep(args[p], GABP_SCHED_BROADCAST, gabp::kModeSolve,
+                                      dist_gather(parts[p]), parts[p]->stream));
+            }
+        }
         double red[6] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0};
         for (int p = 0; p < nparts; ++p) {
             double st6[6];
@@ -1340,7 +1448,7 @@ int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_optio
             DistState *D = parts[p]->dist;
             for (size_t q = 0; q < D->peers.size(); ++q)
                 CK(gabp::launch_halo_pack(args[p], D->d_sidx + D->soff[q], D->scount[q],
-                                          D->d_sbuf + 4 * D->soff[q], parts[p]->stream));
+                                          D->d_sbuf + 4 * D->soff[q], parts[p]->stream, 0));
             CK(cudaStreamSynchronize(parts[p]->stream));
         }
         for (int p = 0; p < nparts; ++p) {  // move each peer's block for p into p's recv
@@ -1358,7 +1466,7 @@ int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_optio
             }
             for (size_t q = 0; q < D->peers.size(); ++q)
                 CK(gabp::launch_halo_unpack(args[p], D->d_ridx + D->roff[q], D->rcount[q],
-                                            D->d_rbuf + 4 * D->roff[q], parts[p]->stream));
+                                            D->d_rbuf + 4 * D->roff[q], parts[p]->stream, 0));
         }
         for (int p = 0; p < nparts; ++p) CK(cudaStreamSynchronize(parts[p]->stream));
         int32_t done = 0;

@@ -41,8 +41,8 @@ __global__ void finish_kernel(const SweepArgs a) {
 // of S_{s-1} (rec[(s-1)%3], or agg[(s-1)%3] and x[(s-1)%3]): exactly what launch s+1
 // gathers for remote neighbours (indices are local ids, or positions on the slice path).
 __global__ void halo_pack_kernel(const SweepArgs a, const uint32_t *idx, int64_t cnt,
-                                 double *buf) {
-    const int64_t s = ((volatile Ctrl *)a.ctrl)->next_sweep - 1;
+                                 double *buf, int pre_finish) {
+    const int64_t s = ((volatile Ctrl *)a.ctrl)->next_sweep - (pre_finish ? 0 : 1);
     double4 *b4 = reinterpret_cast<double4 *>(buf);
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
          k += (int64_t)gridDim.x * blockDim.x) {
@@ -58,8 +58,8 @@ __global__ void halo_pack_kernel(const SweepArgs a, const uint32_t *idx, int64_t
 }
 
 __global__ void halo_unpack_kernel(const SweepArgs a, const uint32_t *idx, int64_t cnt,
-                                   const double *buf) {
-    const int64_t s = ((volatile Ctrl *)a.ctrl)->next_sweep - 1;
+                                   const double *buf, int pre_finish) {
+    const int64_t s = ((volatile Ctrl *)a.ctrl)->next_sweep - (pre_finish ? 0 : 1);
     const double4 *b4 = reinterpret_cast<const double4 *>(buf);
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
          k += (int64_t)gridDim.x * blockDim.x) {
@@ -92,16 +92,16 @@ cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st) {
 }
 
 cudaError_t launch_halo_pack(const SweepArgs &a, const uint32_t *idx, int64_t cnt, double *buf,
-                             cudaStream_t st) {
+                             cudaStream_t st, int pre_finish) {
     if (cnt <= 0) return cudaSuccess;
-    halo_pack_kernel<<<blocks_for(cnt), 256, 0, st>>>(a, idx, cnt, buf);
+    halo_pack_kernel<<<blocks_for(cnt), 256, 0, st>>>(a, idx, cnt, buf, pre_finish);
     return cudaGetLastError();
 }
 
 cudaError_t launch_halo_unpack(const SweepArgs &a, const uint32_t *idx, int64_t cnt,
-                               const double *buf, cudaStream_t st) {
+                               const double *buf, cudaStream_t st, int pre_finish) {
     if (cnt <= 0) return cudaSuccess;
-    halo_unpack_kernel<<<blocks_for(cnt), 256, 0, st>>>(a, idx, cnt, buf);
+    halo_unpack_kernel<<<blocks_for(cnt), 256, 0, st>>>(a, idx, cnt, buf, pre_finish);
     return cudaGetLastError();
 }
 

@@ -138,6 +138,12 @@ struct SweepArgs {
     int msg_lag;        // message statistics of a launch refer to sweep s - msg_lag
     NodeState *rec[3];  // slice path: node state of S_t in rec[t % 3] (position order)
     int slice_variant;  // slice kernel: 0 register batches, 1 cp.async ring, 2 group TMA ring
+    // slice range of this launch (whole groups; multi-rank split: boundary / interior) and
+    // the offset of its CTAs' residual partials (a sweep split over launches sums the
+    // partials of all of them, in CTA order)
+    int64_t sl_lo, sl_hi;
+    int64_t part_base;
+    int exact_primary;  // the exact kernel runs as the sweep itself, not as a twin
     int slice_path;     // this launch family is the slice path (halo records)
     // slice layout (slice.cu): lane-per-row broadcast solve, nodes in position order
     int64_t nslices;
@@ -227,10 +233,11 @@ cudaError_t launch_absmax(int64_t E, const double2 *a, const double2 *b, int whi
 
 // multi-rank helpers (dist.cu)
 cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st);
+// pre_finish = 1: called between the sweep launch and its finish_kernel (split sweep)
 cudaError_t launch_halo_pack(const SweepArgs &a, const uint32_t *idx, int64_t cnt, double *buf,
-                             cudaStream_t st);
+                             cudaStream_t st, int pre_finish);
 cudaError_t launch_halo_unpack(const SweepArgs &a, const uint32_t *idx, int64_t cnt,
-                               const double *buf, cudaStream_t st);
+                               const double *buf, cudaStream_t st, int pre_finish);
 
 // graph build (build.cu)
 struct DeviceGraph {
@@ -250,6 +257,7 @@ struct DeviceGraph {
     int64_t row_lo = 0, row_hi = 0;  // swept rows
     // slice layout (build_slices, slice.cu); nslices == 0 when not built
     int64_t nslices = 0, nslots = 0, npos = 0;
+    int64_t bnd_groups = 0;     // multi-rank: leading groups holding the boundary rows
     int slice_variant = 2;      // 0: register batches, 1: cp.async ring, 2: group TMA ring
     uint2 *slice_info = nullptr;
     uint32_t *pos = nullptr;    // local row -> position
@@ -273,6 +281,8 @@ void free_graph(DeviceGraph &g, cudaStream_t st);
 int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
 cudaError_t prepare_slice_kernels();
 cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st);
+cudaError_t launch_slice_part(const SweepArgs &a, int reserve_sms, cudaStream_t st);
+cudaError_t launch_slice_boundary(const SweepArgs &a, int64_t *grid, cudaStream_t st);
 cudaError_t refresh_slice_nodes(const DeviceGraph &g, cudaStream_t st);
 cudaError_t slice_to_rows(const DeviceGraph &g, int64_t lo, int64_t cnt, const double *in,
                           int stride, double *out, cudaStream_t st);

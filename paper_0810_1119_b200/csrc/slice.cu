@@ -145,7 +145,7 @@ __device__ __forceinline__ void slice_first(const SweepArgs &a, int64_t s, Stats
     NodeState *rec1 = a.rec[0];  // S_0 (s = 1)
     double *xh = xhist_row(a, s);
     const int64_t nwarps = (int64_t)gridDim.x * NW;
-    for (int64_t sl = (int64_t)blockIdx.x * NW + (threadIdx.x >> 5); sl < a.nslices;
+    for (int64_t sl = a.sl_lo + (int64_t)blockIdx.x * NW + (threadIdx.x >> 5); sl < a.sl_hi;
          sl += nwarps) {
         const int64_t p = sl * 32 + lane;
         const double2 nd = __ldg(a.snd + p);
@@ -193,7 +193,7 @@ __device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, S
     const Ring<R> r(a);
     double *xh = xhist_row(a, s);
     const int64_t nwarps = (int64_t)gridDim.x * kLWarps;
-    for (int64_t sl = (int64_t)blockIdx.x * kLWarps + (threadIdx.x >> 5); sl < a.nslices;
+    for (int64_t sl = a.sl_lo + (int64_t)blockIdx.x * kLWarps + (threadIdx.x >> 5); sl < a.sl_hi;
          sl += nwarps) {
         const uint2 si = __ldg(a.slice_info + sl);
         const int64_t p = sl * 32 + lane;
@@ -580,8 +580,8 @@ __device__ __forceinline__ void t_bulk_ef(void *dst, const void *src, unsigned b
         : "memory");
 }
 
-__device__ __forceinline__ uint2 group_info(const SweepArgs &a, int64_t g, int64_t ngroups) {
-    return g < ngroups ? __ldg(a.slice_info + g * kGroup) : make_uint2(0u, 0u);
+__device__ __forceinline__ uint2 group_info(const SweepArgs &a, int64_t g, int64_t g_hi) {
+    return g < g_hi ? __ldg(a.slice_info + g * kGroup) : make_uint2(0u, 0u);
 }
 __device__ __forceinline__ uint32_t chunks_of(uint32_t w) {
     return w > 0 ? (w + kGC - 1) / kGC : 1u;
@@ -592,7 +592,7 @@ template <int PH, int R>
 __device__ __forceinline__ void grp_produce(const SweepArgs &a, GRing &G, uint32_t *ctr,
                                             int lane) {
     const Ring<R> r(a);
-    const int64_t ngroups = a.nslices / kGroup;
+    const int64_t g_lo = a.sl_lo / kGroup, ngroups = a.sl_hi / kGroup;  // claims from g_lo
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     uint32_t u0 = 0, u1 = 0, pend = 0;
@@ -601,7 +601,7 @@ __device__ __forceinline__ void grp_produce(const SweepArgs &a, GRing &G, uint32
         u1 = atomicAdd(ctr, 1u);
         pend = atomicAdd(ctr, 1u);
     }
-    int64_t gcur = __shfl_sync(~0u, u0, 0), gnxt = __shfl_sync(~0u, u1, 0);
+    int64_t gcur = g_lo + __shfl_sync(~0u, u0, 0), gnxt = g_lo + __shfl_sync(~0u, u1, 0);
     uint2 icur = group_info(a, gcur, ngroups), inxt = group_info(a, gnxt, ngroups);
     uint32_t b = 0, nb = chunks_of(icur.y);
     for (uint32_t k = 0;; ++k) {
@@ -639,7 +639,7 @@ __device__ __forceinline__ void grp_produce(const SweepArgs &a, GRing &G, uint32
         if (++b >= nb) {  // next group: claimed two groups ago, descriptor loaded one ago
             gcur = gnxt;
             icur = inxt;
-            gnxt = __shfl_sync(~0u, pend, 0);
+            gnxt = g_lo + __shfl_sync(~0u, pend, 0);
             inxt = group_info(a, gnxt, ngroups);
             if (lane == 0) pend = atomicAdd(ctr, 1u);
             b = 0;
@@ -794,7 +794,7 @@ __device__ __forceinline__ bool slice_prologue(SM &S, const SweepArgs &a, bool e
     if (threadIdx.x == 0) {
         volatile Ctrl *vc = a.ctrl;
         const int64_t s = vc->next_sweep;
-        S.skip = vc->done || s > vc->max_iter + 2 || (exact && vc->redo != 2);
+        S.skip = vc->done || s > vc->max_iter + 2 || (exact && !a.exact_primary && vc->redo != 2);
         S.sweep = s;
     }
     __syncthreads();
@@ -903,13 +903,31 @@ static_assert(kSlotPad >= kStride * (kUL + 1), "slot padding must cover a regist
 // stable radix sort orders every window by degree, descending (degrees <= 4096).
 constexpr int kDegBits = 13;
 static_assert(kSliceMaxDegree < (1 << kDegBits), "degree must fit the key");
+// A rank's rows with a halo neighbour (a neighbour outside [row_lo, row_hi)) are
+// *boundary* rows: with split != 0 they sort before every interior row (top key bit), so
+// the first groups hold exactly the rows whose new states the peers need (DESIGN.md
+// "Multi-GPU"); *nbnd counts them.
 __global__ void slice_key_kernel(int64_t row_lo, int64_t m, const uint32_t *row_ptr,
-                                 uint32_t *key, uint32_t *rows) {
+                                 const EdgeRec *er, int split, uint32_t *key, uint32_t *rows,
+                                 unsigned long long *nbnd) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= m) return;
     const int64_t i = row_lo + r;
     const uint32_t d = row_ptr[i + 1] - row_ptr[i];
-    key[r] = ((uint32_t)(r / kSortWin) << kDegBits) | ((1u << kDegBits) - 1u - d);
+    uint32_t interior = 0u;
+    if (split) {
+        interior = 1u;
+        for (uint32_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+            const int64_t j = er[e].col;
+            if (j < row_lo || j >= row_lo + m) {
+                interior = 0u;
+                break;
+            }
+        }
+        if (!interior) atomicAdd(nbnd, 1ull);
+    }
+    key[r] = (interior << 31) | ((uint32_t)(r / kSortWin) << kDegBits) |
+             ((1u << kDegBits) - 1u - d);
     rows[r] = (uint32_t)i;
 }
 
@@ -1033,11 +1051,20 @@ int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
     SCHECK(cudaMallocAsync(&sorted_rows, sizeof(uint32_t) * m, st));
     SCHECK(cudaMallocAsync(&gslots, sizeof(unsigned long long) * (ngroups + 1), st));
     SCHECK(cudaMallocAsync(&gbase, sizeof(unsigned long long) * (ngroups + 1), st));
-    slice_key_kernel<<<grid_of(m), 256, 0, st>>>(g.row_lo, m, g.row_ptr, deg, rows);
+    // multi-rank row block: boundary rows first (their groups run before the exchange)
+    const int split = (g.row_lo > 0 || g.row_hi < g.n) ? 1 : 0;
+    unsigned long long *d_nbnd = gslots;  // (scratch until the group widths)
+    SCHECK(cudaMemsetAsync(d_nbnd, 0, sizeof(unsigned long long), st));
+    slice_key_kernel<<<grid_of(m), 256, 0, st>>>(g.row_lo, m, g.row_ptr, g.er, split, deg, rows,
+                                                 d_nbnd);
     SCHECK(cudaGetLastError());
+    unsigned long long nbnd = 0;
+    SCHECK(cudaMemcpyAsync(&nbnd, d_nbnd, sizeof(nbnd), cudaMemcpyDeviceToHost, st));
     // stable: rows of equal degree keep their order (structured grids stay contiguous)
     int end_bit = kDegBits;
-    while (end_bit < 32 && ((nseg - 1) >> (end_bit - kDegBits)) > 0) ++end_bit;
+    while (end_bit < 31 && ((nseg - 1) >> (end_bit - kDegBits)) > 0) ++end_bit;
+    if (split) end_bit = 32;
+    static_assert(kSortWin >= (1 << 16), "window ids must fit below the boundary bit");
     size_t tb = 0;
     SCHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, deg, sorted_deg, rows, sorted_rows, m,
                                            0, end_bit, st));
@@ -1065,6 +1092,7 @@ int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
         g.nslices = nslices;
         g.nslots = (int64_t)nslots;
         g.npos = npos;
+        g.bnd_groups = split ? (int64_t)((nbnd + kStride - 1) / kStride) : 0;
         SCHECK(cudaMallocAsync(&g.slice_info, sizeof(uint2) * nslices, st));
         SCHECK(cudaMallocAsync(&g.pos, sizeof(uint32_t) * (g.n > 0 ? g.n : 1), st));
         SCHECK(cudaMallocAsync(&g.srow, sizeof(uint32_t) * npos, st));
@@ -1157,6 +1185,16 @@ cudaError_t prepare_slice_kernels() {
     return cudaSuccess;
 }
 
+// the exact register-batch kernel over [a.sl_lo, a.sl_hi): the twin (runs only when the
+// fast launch flagged itself) or, with a.exact_primary, the sweep itself; returns its grid
+static int64_t launch_slice_exact(const SweepArgs &a, cudaStream_t st) {
+    int64_t gx = g_grid_ldg > 0 ? g_grid_ldg : 148 * 2;
+    const int64_t nx = (a.sl_hi - a.sl_lo + kLWarps - 1) / kLWarps;
+    if (gx > nx) gx = nx > 0 ? nx : 1;
+    slice_kernel_ldg<true><<<(unsigned)gx, kLThreads, 0, st>>>(a);
+    return gx;
+}
+
 static void launch_slice_fast(const SweepArgs &a, cudaStream_t st) {
     const int64_t nw = a.slice_variant ? kPWarps : kLWarps;
     int64_t grid = a.slice_variant ? g_grid_pipe : g_grid_ldg;
@@ -1170,19 +1208,38 @@ static void launch_slice_fast(const SweepArgs &a, cudaStream_t st) {
 }
 
 cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st) {
+    return launch_slice_part(a, 0, st);
+}
+
+// One sweep over [a.sl_lo, a.sl_hi) with the fast kernel (reserve_sms SMs left free for a
+// concurrent exchange), then the exact twin over every slice: a flagged launch is redone
+// whole, so the statistics of an earlier part of the same sweep are re-taken too.
+cudaError_t launch_slice_part(const SweepArgs &a, int reserve_sms, cudaStream_t st) {
     if (a.slice_variant == 2) {
-        int64_t grid = g_grid_grp > 0 ? g_grid_grp : 148;
-        const int64_t need = a.nslices / kGroup;
-        if (grid > need) grid = need > 0 ? need : 1;
+        int64_t grid = (g_grid_grp > 0 ? g_grid_grp : 148) - reserve_sms;
+        const int64_t need = (a.sl_hi - a.sl_lo) / kGroup;
+        if (grid > need) grid = need;
+        if (grid < 1) grid = 1;
         slice_kernel_grp<<<(unsigned)grid, kGThreads, kGrpSmem, st>>>(a);
     } else {
         launch_slice_fast(a, st);
     }
     // exact twin: exits at once unless the fast launch flagged itself (Ctrl.redo)
-    int64_t gx = g_grid_ldg > 0 ? g_grid_ldg : 148 * 2;
-    const int64_t nx = (a.nslices + kLWarps - 1) / kLWarps;
-    if (gx > nx) gx = nx > 0 ? nx : 1;
-    slice_kernel_ldg<true><<<(unsigned)gx, kLThreads, 0, st>>>(a);
+    SweepArgs t = a;
+    t.sl_lo = 0;
+    t.sl_hi = a.nslices;
+    t.part_base = 0;
+    t.exact_primary = 0;
+    launch_slice_exact(t, st);
+    return cudaGetLastError();
+}
+
+// The boundary part of a split multi-rank sweep: exact divisions, so its results (sent to
+// the peers before the interior part runs) never need the twin.
+cudaError_t launch_slice_boundary(const SweepArgs &a, int64_t *grid, cudaStream_t st) {
+    SweepArgs b = a;
+    b.exact_primary = 1;
+    *grid = launch_slice_exact(b, st);
     return cudaGetLastError();
 }
 
