@@ -686,6 +686,92 @@ __device__ __forceinline__ void t_gather(const GStage &S, const GMeta &m, const 
     }
 }
 
+// Running sums of the rows a consumer lane owns (one row per group).
+struct GRow {
+    uint32_t d = 0;
+    double2 a3 = make_double2(0.0, 0.0);
+    double sp = 0.0, sn = 0.0, y = 0.0, rhs_i = 0.0, diag = 0.0;
+};
+
+// Chunk k of a consumer warp: waits for chunk k+1 and issues its header and gathers into
+// (nP, nN, nx), then computes chunk k from its stage and the gathers (gP, gN, gx).  Returns
+// false after the last chunk; otherwise m becomes chunk k+1's descriptor.  The loop calls
+// it with the two gather buffers swapped on alternate chunks (no register copies).
+template <int PH, int R>
+__device__ __forceinline__ bool grp_step(const SweepArgs &a, const Ring<R> &r, double *xh,
+                                         Stats &st, GRing &G, int lane, int warp, int t,
+                                         uint32_t k, GMeta &m, THdr &hn, GRow &row,
+                                         const double (&gP)[kGC], const double (&gN)[kGC],
+                                         const double (&gx)[kGC], double (&nP)[kGC],
+                                         double (&nN)[kGC], double (&nx)[kGC]) {
+    if (m.b == 0) {  // row header (loaded one chunk ago)
+        row.d = hn.d;
+        row.diag = hn.nd.x;
+        row.sp = hn.nd.x;
+        row.sn = hn.nd.y;
+        if (PH == 3) {
+            row.a3 = hn.a3;
+            row.y = hn.nd.x * hn.xo;
+            row.rhs_i = hn.rhs;
+        }
+    }
+    // header and gathers of chunk k+1
+    const int s1 = (int)((k + 1) % kGS);
+    t_wait(&G.full[s1], ((k + 1) / kGS) & 1u);
+    const GMeta mn = G.meta[s1];
+    if (mn.g >= 0) {
+        if (mn.b == 0) t_header<PH, R>(a, r, ((int64_t)mn.g * kGroup + warp) * 32 + lane, hn);
+        t_gather(G.st[s1], mn, r.g2, t, nP, nN, nx);
+    }
+    const int s0 = (int)(k % kGS);
+    const GStage &S = G.st[s0];
+    const uint32_t d = row.d;
+    double cc[kGC], m2p[kGC], m2m[kGC], ip[kGC], im[kGC], pe[kGC], rc[kGC];
+    double2 i2v[kGC];
+#pragma unroll
+    for (int u = 0; u < kGC; ++u) {
+        const bool v = m.b * kGC + u < d;
+        cc[u] = v ? S.c[u][t] : 1.0;
+        rc[u] = ddiv_rcp(cc[u]);
+        m2p[u] = 0.0;  // m^{(0)} = 0 at launch 2
+        m2m[u] = 0.0;
+        i2v[u] = make_double2(0.0, 0.0);
+        if (PH == 3) {  // own outgoing message of sweep s-2
+            const double2 i3 = S.i3[u][t];
+            i2v[u] = S.i2[u][t];
+            const double pe2 = v ? row.a3.x - i3.x : 1.0;
+            const double nu2 = v ? row.a3.y - i3.x * i3.y : 1.0;
+            edge_msg<false>(cc[u], rc[u], pe2, nu2, m2p[u], m2m[u], st);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) t_arrive(&G.empty[s0]);  // the stage's data is in registers now
+#pragma unroll
+    for (int u = 0; u < kGC; ++u) {  // incoming of S_{s-1}
+        const bool v = m.b * kGC + u < d;
+        pe[u] = v ? gP[u] - m2p[u] : 1.0;
+        const double num = v ? gN[u] - m2p[u] * m2m[u] : 1.0;
+        edge_msg<false>(cc[u], rc[u], pe[u], num, ip[u], im[u], st);
+    }
+    const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
+#pragma unroll
+    for (int u = 0; u < kGC; ++u) {
+        const uint32_t q = m.b * kGC + u;
+        if (q < d) {
+            row.sp = row.sp + ip[u];
+            row.sn = row.sn + ip[u] * im[u];  // (prec * mean), solver.py:243
+            if (PH == 3) row.y = row.y + cc[u] * gx[u];
+            __stcs(r.I1 + m.gbase + (uint32_t)kStride * q + t, make_double2(ip[u], im[u]));
+            msg_stats<false>(st, a, ip[u], im[u], i2v[u], pe[u], p, q);
+        }
+    }
+    if (m.b + 1 == m.nb && row.diag != 0.0)  // row done (A_ii == 0: padding lane)
+        node_done<PH, false>(st, a, r.g1, xh, p, row.sp, row.sn, row.y, row.rhs_i);
+    if (mn.g < 0) return false;
+    m = mn;
+    return true;
+}
+
 // Consumer warp `warp`: slice warp of every group, lane per row.
 template <int PH, int R>
 __device__ __forceinline__ void grp_consume(const SweepArgs &a, int64_t s, Stats &st, int lane,
@@ -696,86 +782,18 @@ __device__ __forceinline__ void grp_consume(const SweepArgs &a, int64_t s, Stats
     t_wait(&G.full[0], 0u);
     GMeta m = G.meta[0];
     if (m.g < 0) return;
-    double gP[kGC], gN[kGC], gx[kGC];
+    double gA[3][kGC], gB[3][kGC];  // gathers {P, N, x}: chunk k in one, k+1 in the other
     THdr hn;
     t_header<PH, R>(a, r, ((int64_t)m.g * kGroup + warp) * 32 + lane, hn);
-    t_gather(G.st[0], m, r.g2, t, gP, gN, gx);
-
-    uint32_t d = 0;
-    double2 a3 = make_double2(0.0, 0.0);
-    double sp = 0.0, sn = 0.0, y = 0.0, rhs_i = 0.0, diag = 0.0;
-    for (uint32_t k = 0;; ++k) {
-        if (m.b == 0) {  // row header (loaded one chunk ago)
-            d = hn.d;
-            diag = hn.nd.x;
-            sp = hn.nd.x;
-            sn = hn.nd.y;
-            if (PH == 3) {
-                a3 = hn.a3;
-                y = hn.nd.x * hn.xo;
-                rhs_i = hn.rhs;
-            }
-        }
-        // header and gathers of chunk k+1
-        double nP[kGC] = {}, nN[kGC] = {}, nx[kGC] = {};
-        const int s1 = (int)((k + 1) % kGS);
-        t_wait(&G.full[s1], ((k + 1) / kGS) & 1u);
-        const GMeta mn = G.meta[s1];
-        if (mn.g >= 0) {
-            if (mn.b == 0) t_header<PH, R>(a, r, ((int64_t)mn.g * kGroup + warp) * 32 + lane, hn);
-            t_gather(G.st[s1], mn, r.g2, t, nP, nN, nx);
-        }
-        const int s0 = (int)(k % kGS);
-        const GStage &S = G.st[s0];
-        double cc[kGC], m2p[kGC], m2m[kGC], ip[kGC], im[kGC], pe[kGC], rc[kGC];
-        double2 i2v[kGC];
-#pragma unroll
-        for (int u = 0; u < kGC; ++u) {
-            const bool v = m.b * kGC + u < d;
-            cc[u] = v ? S.c[u][t] : 1.0;
-            rc[u] = ddiv_rcp(cc[u]);
-            m2p[u] = 0.0;  // m^{(0)} = 0 at launch 2
-            m2m[u] = 0.0;
-            i2v[u] = make_double2(0.0, 0.0);
-            if (PH == 3) {  // own outgoing message of sweep s-2
-                const double2 i3 = S.i3[u][t];
-                i2v[u] = S.i2[u][t];
-                const double pe2 = v ? a3.x - i3.x : 1.0;
-                const double nu2 = v ? a3.y - i3.x * i3.y : 1.0;
-                edge_msg<false>(cc[u], rc[u], pe2, nu2, m2p[u], m2m[u], st);
-            }
-        }
-        __syncwarp();
-        if (lane == 0) t_arrive(&G.empty[s0]);  // the stage's data is in registers now
-#pragma unroll
-        for (int u = 0; u < kGC; ++u) {  // incoming of S_{s-1}
-            const bool v = m.b * kGC + u < d;
-            pe[u] = v ? gP[u] - m2p[u] : 1.0;
-            const double num = v ? gN[u] - m2p[u] * m2m[u] : 1.0;
-            edge_msg<false>(cc[u], rc[u], pe[u], num, ip[u], im[u], st);
-        }
-        const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
-#pragma unroll
-        for (int u = 0; u < kGC; ++u) {
-            const uint32_t q = m.b * kGC + u;
-            if (q < d) {
-                sp = sp + ip[u];
-                sn = sn + ip[u] * im[u];  // (prec * mean), solver.py:243
-                if (PH == 3) y = y + cc[u] * gx[u];
-                __stcs(r.I1 + m.gbase + (uint32_t)kStride * q + t, make_double2(ip[u], im[u]));
-                msg_stats<false>(st, a, ip[u], im[u], i2v[u], pe[u], p, q);
-            }
-        }
-        if (m.b + 1 == m.nb && diag != 0.0)  // row done (A_ii == 0: padding lane)
-            node_done<PH, false>(st, a, r.g1, xh, p, sp, sn, y, rhs_i);
-        if (mn.g < 0) break;
-        m = mn;
-#pragma unroll
-        for (int u = 0; u < kGC; ++u) {
-            gP[u] = nP[u];
-            gN[u] = nN[u];
-            gx[u] = nx[u];
-        }
+    t_gather(G.st[0], m, r.g2, t, gA[0], gA[1], gA[2]);
+    GRow row;
+    for (uint32_t k = 0;; k += 2) {
+        if (!grp_step<PH, R>(a, r, xh, st, G, lane, warp, t, k, m, hn, row, gA[0], gA[1], gA[2],
+                             gB[0], gB[1], gB[2]))
+            break;
+        if (!grp_step<PH, R>(a, r, xh, st, G, lane, warp, t, k + 1, m, hn, row, gB[0], gB[1],
+                             gB[2], gA[0], gA[1], gA[2]))
+            break;
     }
 }
 
