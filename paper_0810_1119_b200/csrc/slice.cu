@@ -86,20 +86,16 @@ __device__ __forceinline__ void st_node(NodeState *g, double P, double N, double
                  "d"(0.0) : "memory");
 }
 
-// Statistics of sweep s-1 on its message j -> i = (ip, im) against S_{s-2}'s (i2);
-// a zero P_excl or aggregate is reported by the exact launch (the fast one flags it).
+// Statistics of sweep s-1 on its message j -> i = (ip, im) against S_{s-2}'s (i2).
+// A zero P_excl is reported by the exact launch only: in the fast one the division by it
+// yields a NaN quotient, which fails the deferred range test and flags the launch.
 template <bool EXACT>
 __device__ __forceinline__ void msg_stats(Stats &st, const SweepArgs &a, double ip, double im,
                                           double2 i2, double pe, int64_t p, uint32_t q) {
     const double d1 = fabs(ip - i2.x), d2 = fabs(im - i2.y);
     st.chg = fmax(st.chg, fmax(d1, d2));  // NaN differences ignored, as '>' ignores them
     if (!(fabs(ip) <= st.lim) || !(fabs(im) <= st.lim)) st.out_of_range = 1u;
-    if (pe == 0.0) {
-        if (EXACT)
-            st.sing = min(st.sing, twin_edge(a, p, q));
-        else
-            st.redo = 1u;
-    }
+    if (EXACT && pe == 0.0) st.sing = min(st.sing, twin_edge(a, p, q));
 }
 
 // Row done: marginal of S_{s-1} and the node state record (solver.py:247-255, 286).
@@ -110,12 +106,8 @@ __device__ __forceinline__ void node_done(Stats &st, const SweepArgs &a, NodeSta
     const double xi = qdiv<EXACT>(sn, sp, st);
     if (!(fabs(xi) <= DBL_MAX)) st.means_bad = 1u;
     if (xh) xh[__ldg(a.srow + p)] = xi;
-    if (sp == 0.0) {
-        if (EXACT)
-            st.agg_sing = min(st.agg_sing, __ldg(a.srow + p));
-        else
-            st.redo = 1u;
-    }
+    if (EXACT && sp == 0.0)  // (fast launch: N / 0 fails the deferred range test)
+        st.agg_sing = min(st.agg_sing, __ldg(a.srow + p));
     st_node(rec1 + p, sp, sp * xi, xi);  // (sum_p * mu_tilde)
     if (PH == 3) {
         const double r = y - rhs_i;
