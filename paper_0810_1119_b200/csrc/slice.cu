@@ -1098,6 +1098,12 @@ int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
     if (nslots + kSlotPad >= 0xffffffffull) {
         rc = GABP_EINVAL;  // caller keeps the tile layout only
         snprintf(err, errlen, "slice layout needs %llu slots (> 32-bit)", nslots);
+    } else if (nslots > 2ull * (unsigned long long)g.E + (1ull << 20)) {
+        // a skewed degree distribution pads groups to their widest row: more than twice
+        // the edges in slots would stream mostly padding -- the CSR tiles have none
+        rc = GABP_EINVAL;
+        snprintf(err, errlen, "slice layout would pad %lld edges to %llu slots",
+                 (long long)g.E, nslots);
     } else {
         g.nslices = nslices;
         g.nslots = (int64_t)nslots;

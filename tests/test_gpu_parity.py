@@ -560,3 +560,21 @@ def test_slice_kernel_variants_bitwise(variant, which, monkeypatch):
     np.testing.assert_array_equal(r.precisions, orc.precisions)
     np.testing.assert_array_equal(np.asarray(r.max_change_history),
                                   np.asarray(orc.max_change_history))
+
+
+def test_skewed_degrees_fall_back_to_tiles():
+    """One degree-3000 hub among degree-2 rows: padding every row of the hub's group to
+    the hub's width would stream mostly padding, so the build keeps the CSR tiles; the
+    solve still matches the oracle bitwise."""
+    n = 20000
+    pi = np.concatenate([np.zeros(3000, dtype=np.int64), np.arange(3001, n - 1)])
+    pj = np.concatenate([np.arange(1, 3001), np.arange(3002, n)])
+    pv = np.full(pi.size, 0.1)
+    s = G.SymSystem.from_pairs(np.full(n, 400.0), pi, pj, pv, np.ones(n))
+    g = G.build_graph(s)
+    assert g.info.num_slices == 0
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    orc = oracle.solve(og, epsilon=1e-12, schedule="broadcast")
+    r = G.solve_graph(g, G.SolveOptions(schedule="broadcast", epsilon=1e-12))
+    assert r.iterations == orc.iterations
+    np.testing.assert_array_equal(r.means, orc.means)
