@@ -43,8 +43,9 @@ extern "C" {
 #define GABP_GATHER_MESSAGE 1   /* row tiles, gather the twin message m_ji itself */
 #define GABP_GATHER_RECOMPUTE 2 /* row tiles, broadcast only: gather node j's aggregate and
                                    recompute m_ji */
-#define GABP_GATHER_SLICE 3     /* slice layout (lane per row), broadcast solve only:
-                                   recompute m_ji as GABP_GATHER_RECOMPUTE */
+#define GABP_GATHER_SLICE 3     /* slice layout (lane per row): broadcast solve recomputes
+                                   m_ji as GABP_GATHER_RECOMPUTE; parallel solve sums the
+                                   row's incoming slots and stores to the twin slots */
 
 typedef struct gabp_graph gabp_graph_t;  /* device-resident GaussianGraph */
 typedef struct gabp_state gabp_state_t;  /* device-resident MessageState  */

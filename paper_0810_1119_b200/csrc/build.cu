@@ -211,6 +211,7 @@ void free_graph(DeviceGraph &g, cudaStream_t st) {
     if (g.srhs) cudaFreeAsync(g.srhs, st);
     if (g.scol) cudaFreeAsync(g.scol, st);
     if (g.scoef) cudaFreeAsync(g.scoef, st);
+    if (g.stwin) cudaFreeAsync(g.stwin, st);
     g = DeviceGraph{};
 }
 

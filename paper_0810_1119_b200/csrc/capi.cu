@@ -370,6 +370,7 @@ SweepArgs make_args(gabp_graph *G) {
     a.srhs = g.srhs;
     a.scol = g.scol;
     a.scoef = g.scoef;
+    a.stwin = g.stwin;
     a.sl_lo = 0;
     a.sl_hi = g.nslices;
     a.part_base = 0;
@@ -416,8 +417,6 @@ int check_options(const gabp_options_t *opt) {
         return fail(GABP_EINVAL, "schedule must be parallel (0) or broadcast (2)");
     if (opt->gather_mode < GABP_GATHER_AUTO || opt->gather_mode > GABP_GATHER_SLICE)
         return fail(GABP_EINVAL, "unknown gather mode %d", opt->gather_mode);
-    if (opt->gather_mode == GABP_GATHER_SLICE && opt->schedule != GABP_SCHED_BROADCAST)
-        return fail(GABP_EINVAL, "the slice layout runs the broadcast schedule");
     return GABP_OK;
 }
 
@@ -437,7 +436,15 @@ int dist_gather(const gabp_graph *G) {
 // (L2-resident, contiguous DRAM traffic only) when the twin messages are far away in
 // memory; gather the twin message itself when it is near (structured grids).
 int pick_gather(const gabp_graph *G, const gabp_options_t *opt) {
-    if (opt->schedule != GABP_SCHED_BROADCAST) return gabp::kGatherMessage;
+    if (opt->schedule != GABP_SCHED_BROADCAST) {
+        // parallel schedule: the slice-group kernel (exclusion sums over the row's
+        // contiguous incoming slots, scattered twin stores) on whole graphs with slices
+        const bool whole = G->g.row_lo == 0 && G->g.row_hi == G->g.n;
+        if (opt->gather_mode == GABP_GATHER_SLICE ||
+            (opt->gather_mode == GABP_GATHER_AUTO && G->g.nslices > 0 && whole))
+            return gabp::kGatherSliceParallel;
+        return gabp::kGatherMessage;
+    }
     if (opt->gather_mode == GABP_GATHER_MESSAGE) return gabp::kGatherMessage;
     if (opt->gather_mode == GABP_GATHER_RECOMPUTE) return gabp::kGatherRecompute;
     if (G->g.nslices > 0) return gabp::kGatherSlice;  // AUTO or SLICE
@@ -744,7 +751,12 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
     rc = check_slice(G, opt);
     if (rc) return rc;
     const int gather = pick_gather(G, opt);
-    G->slice_order = gather == gabp::kGatherSlice;
+    if (gather == gabp::kGatherSliceParallel && !G->g.stwin) {
+        rc = gabp::build_stwin(G->g, st, g_err, sizeof(g_err));
+        if (rc) return rc;
+        G->ws_gen++;  // captured sweeps hold the slot pointers
+    }
+    G->slice_order = gather == gabp::kGatherSlice || gather == gabp::kGatherSliceParallel;
     const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
     const double tc0 = host_ms();
     rc = get_chunk_exec(G, sched, gather, C);
@@ -1592,6 +1604,12 @@ int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int32_t gather_mode, in
     if (rc == GABP_OK) rc = check_slice(G, &o);
     if (rc) return rc;
     const int gather = pick_gather(G, &o);
+    if (gather == gabp::kGatherSliceParallel && !G->g.stwin) {
+        rc = gabp::build_stwin(G->g, st, g_err, sizeof(g_err));
+        if (rc) return rc;
+        G->ws_gen++;
+    }
+    a.stwin = G->g.stwin;
     CK(cudaEventRecord(G->ev[2], st));
     for (int64_t k = 0; k < sweeps; ++k)
         CK(gabp::launch_sweep(a, schedule, gabp::kModeSolve, gather, st));

@@ -94,6 +94,7 @@ struct Ctrl {
     int32_t means_nonfinite[kStatSlots];
     unsigned long long agg_singular[kStatSlots];   // broadcast: first node with P_i == 0
     unsigned long long singular_min[kStatSlots];   // first edge with P_excl == 0
+    uint32_t work_twin;         // claims of an exact group twin (zeroed when redo becomes 2)
     uint32_t work[kStatSlots];  // slice TMA kernel: next work unit of launch s (slot s % 4);
                                 // the last CTA of launch s zeroes slot (s + 2) % 4
 };
@@ -154,6 +155,7 @@ struct SweepArgs {
     const double *srhs;        // b_i per position
     const uint32_t *scol;      // position of the destination, per slot
     const double *scoef;       // A_ij per slot
+    const uint32_t *stwin;     // slot of the twin message (parallel schedule), per slot
 };
 
 // kernels (sweep.cu); prepare_sweep_kernels() must run once per device before launches
@@ -161,7 +163,8 @@ cudaError_t prepare_sweep_kernels();
 int read_timeline(long long *out, int n);  // GABP_TIMELINE builds only
 // gather: kGatherMessage (twin message msg_old[rev]) or kGatherRecompute (node aggregate of
 // the previous state + recomputation, broadcast schedule in solve mode only)
-enum Gather { kGatherMessage = 0, kGatherRecompute = 1, kGatherSlice = 2 };
+enum Gather { kGatherMessage = 0, kGatherRecompute = 1, kGatherSlice = 2,
+              kGatherSliceParallel = 3 };
 cudaError_t launch_sweep(const SweepArgs &a, int schedule, int mode, int gather, cudaStream_t st);
 cudaError_t launch_marginals(int64_t n, const uint32_t *row_ptr, const EdgeRec *er,
                              const double *diag, const double *prior_num, const double2 *msg,
@@ -266,6 +269,7 @@ struct DeviceGraph {
     double *srhs = nullptr;
     uint32_t *scol = nullptr;
     double *scoef = nullptr;
+    uint32_t *stwin = nullptr;  // built on the first parallel-schedule solve (build_stwin)
 };
 
 // Builds CSR + twin index + tiles from device-resident inputs.  Returns a GABP_* code
@@ -283,6 +287,9 @@ cudaError_t prepare_slice_kernels();
 cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st);
 cudaError_t launch_slice_part(const SweepArgs &a, int reserve_sms, cudaStream_t st);
 cudaError_t launch_slice_boundary(const SweepArgs &a, int64_t *grid, cudaStream_t st);
+// parallel schedule over the slice groups (slice.cu); build_stwin first
+cudaError_t launch_slice_parallel(const SweepArgs &a, cudaStream_t st);
+int build_stwin(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
 cudaError_t refresh_slice_nodes(const DeviceGraph &g, cudaStream_t st);
 cudaError_t slice_to_rows(const DeviceGraph &g, int64_t lo, int64_t cnt, const double *in,
                           int stride, double *out, cudaStream_t st);

@@ -903,7 +903,294 @@ __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_grp(const SweepArgs
     sweep_epilogue<kGThreads, kModeSolve, 1>(S.tail, a, s, s >= 3, st, tid);
 }
 
-int g_grid_ldg = 0, g_grid_pipe = 0, g_grid_grp = 0;
+// ---- parallel schedule over the slice groups ------------------------------------------------
+// _sweep_parallel (solver.py:146-173): every directed edge i -> j gets its exclusion sums
+//   P_excl = A_ii + sum_{k != j} P_ki,  N_excl = A_ii mu_ii + sum_{k != j} P_ki mu_ki
+// in ascending k (np.add.at over excl_pos), then m_ij = (-A_ij^2 / P_excl, N_excl / A_ij).
+// Storage is the incoming layout of the broadcast slice path: slot (i, q) holds
+// I_iq = m_{k_q -> i}.  Launch s reads row i's incoming messages of S_{s-1} -- contiguous
+// slots, streamed by the group producer -- and writes its outgoing messages of S_s into
+// the twin slots (stwin, scattered 16-byte stores).  The exclusion sums are O(degree^2):
+// the outgoing edges of a row are taken kPB at a time (register accumulators), one pass
+// over the row's incoming columns per block -- pass 0 from DRAM with everything else
+// (I^{(s-2)} for the change statistic, coefficients and columns for the residual), later
+// passes re-read only I^{(s-1)}, which stays in L2 (a group's columns are 16 B x 480 per
+// column).  Pass 0 also forms the full sums: marginal x^{(s-1)} and the residual row of
+// x^{(s-2)}, as the broadcast kernel.  Statistics of sweep s-1 (LAG 1): every message is
+// exactly one row's incoming slot.
+#ifndef GABP_PAR_BLOCK
+#define GABP_PAR_BLOCK 8
+#endif
+constexpr int kPB = GABP_PAR_BLOCK;  // outgoing edges per exclusion pass
+
+__device__ __forceinline__ uint32_t par_passes(uint32_t w) {
+    return w > kPB ? (w + kPB - 1) / kPB : 1u;
+}
+
+// Producer of the parallel kernel: per group, npass passes of ceil(w / kGC) chunks.
+template <bool STATS, bool RESID, bool EXACT>
+__device__ __forceinline__ void par_produce(const SweepArgs &a, GRing &G, uint32_t *ctr,
+                                            const double2 *I1, const double2 *I2, int lane) {
+    const int64_t g_lo = a.sl_lo / kGroup, ngroups = a.sl_hi / kGroup;
+    uint64_t pol_ef, pol_el;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_el));
+    uint32_t u0 = 0, u1 = 0, pend = 0;
+    if (lane == 0) {
+        u0 = atomicAdd(ctr, 1u);
+        u1 = atomicAdd(ctr, 1u);
+        pend = atomicAdd(ctr, 1u);
+    }
+    int64_t gcur = g_lo + __shfl_sync(~0u, u0, 0), gnxt = g_lo + __shfl_sync(~0u, u1, 0);
+    uint2 icur = group_info(a, gcur, ngroups), inxt = group_info(a, gnxt, ngroups);
+    uint32_t b = 0, pass = 0, nb = chunks_of(icur.y), np = par_passes(icur.y);
+    for (uint32_t k = 0;; ++k) {
+        const int stg = (int)(k % kGS);
+        if (k >= (uint32_t)kGS) t_wait(&G.empty[stg], ((k / kGS) - 1u) & 1u);
+        if (gcur >= ngroups) {
+            if (lane == 0) {
+                G.meta[stg].g = -1;
+                t_arrive(&G.full[stg]);
+            }
+            return;
+        }
+        if (lane == 0) {
+            const uint32_t w = icur.y, q0 = b * kGC;
+            const uint32_t nc = w > q0 ? min((uint32_t)kGC, w - q0) : 0u;
+            const uint32_t slot = icur.x + (uint32_t)kStride * q0;
+            GMeta &m = G.meta[stg];
+            m.g = (int32_t)gcur;
+            m.b = b;
+            m.nb = nb;
+            m.w = w;
+            m.gbase = icur.x;
+            m.pad[0] = pass;
+            m.pad[1] = np;
+            GStage &S = G.st[stg];
+            const unsigned per = pass == 0 ? 16u + (STATS ? 16u : 0u) + (RESID ? 12u : 0u) : 16u;
+            t_expect_tx(&G.full[stg], nc * (uint32_t)kStride * per);
+            if (nc) {
+                // I^{(s-1)} (the i3 buffer) is re-read by the later passes: keep it in L2
+                t_bulk_ef(&S.i3[0][0], I1 + slot, nc * kStride * 16u, &G.full[stg],
+                          np > 1 ? pol_el : pol_ef);
+                if (pass == 0) {
+                    if (STATS)
+                        t_bulk_ef(&S.i2[0][0], I2 + slot, nc * kStride * 16u, &G.full[stg], pol_ef);
+                    if (RESID) {
+                        t_bulk_ef(&S.c[0][0], a.scoef + slot, nc * kStride * 8u, &G.full[stg],
+                                  pol_ef);
+                        t_bulk_ef(&S.col[0][0], a.scol + slot, nc * kStride * 4u, &G.full[stg],
+                                  pol_ef);
+                    }
+                }
+            }
+        }
+        if (++b >= nb) {
+            b = 0;
+            if (++pass >= np) {
+                pass = 0;
+                gcur = gnxt;
+                icur = inxt;
+                gnxt = g_lo + __shfl_sync(~0u, pend, 0);
+                inxt = group_info(a, gnxt, ngroups);
+                if (lane == 0) pend = atomicAdd(ctr, 1u);
+                nb = chunks_of(icur.y);
+                np = par_passes(icur.y);
+            }
+        }
+    }
+}
+
+struct ParRow {
+    uint32_t d = 0;
+    double pP = 0.0, pN = 0.0;             // prior precision and numerator
+    double sp = 0.0, sn = 0.0, y = 0.0, rhs_i = 0.0;
+    double aP[kPB], aN[kPB];               // exclusion sums of the current block
+    double cb[kPB];                        // A_ij of the block's edges
+    uint32_t tw[kPB];                      // their twin slots
+};
+
+// Consumer of the parallel kernel (warp `warp`, lane per row).
+template <bool STATS, bool RESID, bool EXACT>
+__device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats &st, int lane,
+                                            int warp, GRing &G, const NodeState *g2,
+                                            NodeState *g1, double2 *I0) {
+    double *xh = xhist_row(a, s);
+    const int t = warp * 32 + lane;
+    t_wait(&G.full[0], 0u);
+    GMeta m = G.meta[0];
+    if (m.g < 0) return;
+    ParRow row;
+    THdr hn;
+    const int64_t p_first = ((int64_t)m.g * kGroup + warp) * 32 + lane;
+    hn.nd = __ldg(a.snd + p_first);
+    hn.d = __ldg(a.sdeg + p_first);
+    if (RESID) {
+        hn.xo = __ldcg(&g2[p_first].x);
+        hn.rhs = __ldg(a.srhs + p_first);
+    }
+    double gx[kGC] = {}, nx[kGC] = {};
+    if (RESID) {  // residual gathers of chunk 0 (x_j^{(s-2)})
+#pragma unroll
+        for (int u = 0; u < kGC; ++u)
+            if (u < (int)m.w) gx[u] = __ldcg(&g2[G.st[0].col[u][t]].x);
+    }
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t pass = m.pad[0];
+        const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
+        const uint32_t slot0 = m.gbase + (uint32_t)t;
+        if (m.b == 0) {
+            if (pass == 0) {  // row header (loaded one chunk ago)
+                row.d = hn.d;
+                row.pP = hn.nd.x;
+                row.pN = hn.nd.y;
+                row.sp = hn.nd.x;
+                row.sn = hn.nd.y;
+                if (RESID) {
+                    row.y = hn.nd.x * hn.xo;
+                    row.rhs_i = hn.rhs;
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < kPB; ++jj) {  // block `pass`: sums start at the prior
+                row.aP[jj] = row.pP;
+                row.aN[jj] = row.pN;
+                const uint32_t j = pass * kPB + jj;
+                row.cb[jj] = 1.0;
+                row.tw[jj] = 0u;
+                if (j < row.d) {
+                    row.cb[jj] = __ldg(a.scoef + slot0 + (uint32_t)kStride * j);
+                    row.tw[jj] = __ldg(a.stwin + slot0 + (uint32_t)kStride * j);
+                }
+            }
+        }
+        // next chunk: header and residual gathers
+        const int s1 = (int)((k + 1) % kGS);
+        t_wait(&G.full[s1], ((k + 1) / kGS) & 1u);
+        const GMeta mn = G.meta[s1];
+        if (mn.g >= 0) {
+            if (mn.b == 0 && mn.pad[0] == 0) {
+                const int64_t pn = ((int64_t)mn.g * kGroup + warp) * 32 + lane;
+                hn.nd = __ldg(a.snd + pn);
+                hn.d = __ldg(a.sdeg + pn);
+                if (RESID) {
+                    hn.xo = __ldcg(&g2[pn].x);
+                    hn.rhs = __ldg(a.srhs + pn);
+                }
+            }
+            if (RESID && mn.pad[0] == 0) {
+#pragma unroll
+                for (int u = 0; u < kGC; ++u)
+                    if (mn.b * kGC + u < mn.w) nx[u] = __ldcg(&g2[G.st[s1].col[u][t]].x);
+            }
+        }
+        const int s0 = (int)(k % kGS);
+        const GStage &S = G.st[s0];
+        const uint32_t d = row.d;
+#pragma unroll
+        for (int u = 0; u < kGC; ++u) {
+            const uint32_t q = m.b * kGC + u;
+            if (q < d) {
+                const double2 v = S.i3[u][t];  // I^{(s-1)}_iq = m_{k_q -> i}
+                const double vP = v.x, vN = v.x * v.y;  // (prec * mean), solver.py:148
+                if (pass == 0) {
+                    row.sp = row.sp + vP;
+                    row.sn = row.sn + vN;
+                    if (RESID) row.y = row.y + S.c[u][t] * gx[u];
+                    if (STATS) {
+                        const double2 o = S.i2[u][t];
+                        const double d1 = fabs(v.x - o.x), d2 = fabs(v.y - o.y);
+                        st.chg = fmax(st.chg, fmax(d1, d2));
+                        if (!(fabs(v.x) <= st.lim) || !(fabs(v.y) <= st.lim))
+                            st.out_of_range = 1u;
+                    }
+                }
+#pragma unroll
+                for (int jj = 0; jj < kPB; ++jj) {
+                    if (q != pass * kPB + jj) {
+                        row.aP[jj] = row.aP[jj] + vP;
+                        row.aN[jj] = row.aN[jj] + vN;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) t_arrive(&G.empty[s0]);
+        if (m.b + 1 == m.nb) {  // end of pass: the block's messages, scattered to the twins
+#pragma unroll
+            for (int jj = 0; jj < kPB; ++jj) {
+                const uint32_t j = pass * kPB + jj;
+                if (j < d) {
+                    const double c = row.cb[jj];
+                    const double rc = EXACT ? 0.0 : ddiv_rcp(c);
+                    double P, mu;
+                    edge_msg<EXACT>(c, rc, row.aP[jj], row.aN[jj], P, mu, st);
+                    __stcg(I0 + row.tw[jj], make_double2(P, mu));
+                    // P_excl(i -> j) = 0 (solver.py:150-154): sweep s itself, so the slot of
+                    // the launch's own sweep (agg_sing), not the lagged message slot
+                    if (EXACT && row.aP[jj] == 0.0)
+                        st.agg_sing = min(st.agg_sing, a.row_ptr[__ldg(a.srow + p)] + j);
+                }
+            }
+            if (pass == 0 && row.pP != 0.0) {  // marginal of S_{s-1}, residual of x^{(s-2)}
+                const double xi = qdiv<EXACT>(row.sn, row.sp, st);
+                if (!(fabs(xi) <= DBL_MAX)) st.means_bad = 1u;
+                if (xh) xh[__ldg(a.srow + p)] = xi;
+                st_node(g1 + p, row.sp, row.sp * xi, xi);
+                if (RESID) {
+                    const double r = row.y - row.rhs_i;
+                    st.rsq += r * r;
+                }
+            }
+        }
+        if (mn.g < 0) break;
+        m = mn;
+#pragma unroll
+        for (int u = 0; u < kGC; ++u) gx[u] = nx[u];
+    }
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kGThreads, 1) slice_kernel_par(const SweepArgs a) {
+    __shared__ GrpSmem S;
+    extern __shared__ __align__(128) unsigned char par_raw[];
+    GRing &G = *reinterpret_cast<GRing *>(par_raw);
+    if (!slice_prologue(S, a, EXACT)) return;
+    const int64_t s = S.sweep;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < kGS) {
+        t_mbar_init(&G.full[tid], 1u);
+        t_mbar_init(&G.empty[tid], (unsigned)kGroup);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+    uint32_t *ctr = EXACT ? &a.ctrl->work_twin : &a.ctrl->work[s % kStatSlots];
+    const double2 *I1 = a.msg[(s + 2) % 3];  // I^{(s-1)}
+    const double2 *I2 = a.msg[(s + 1) % 3];  // I^{(s-2)}
+    double2 *I0 = a.msg[s % 3];              // I^{(s)}, written
+    const NodeState *g2 = a.rec[(s + 1) % 3];
+    NodeState *g1 = a.rec[(s + 2) % 3];
+    Stats st;
+    st.lim = fmin(a.ctrl->blowup, DBL_MAX);
+    if (warp == kGroup) {
+        if (s >= 3)
+            par_produce<true, true, EXACT>(a, G, ctr, I1, I2, lane);
+        else if (s == 2)
+            par_produce<true, false, EXACT>(a, G, ctr, I1, I2, lane);
+        else
+            par_produce<false, false, EXACT>(a, G, ctr, I1, I2, lane);
+    } else {
+        if (s >= 3)
+            par_consume<true, true, EXACT>(a, s, st, lane, warp, G, g2, g1, I0);
+        else if (s == 2)
+            par_consume<true, false, EXACT>(a, s, st, lane, warp, G, g2, g1, I0);
+        else
+            par_consume<false, false, EXACT>(a, s, st, lane, warp, G, g2, g1, I0);
+    }
+    sweep_epilogue<kGThreads, kModeSolve, 1>(S.tail, a, s, s >= 3, st, tid);
+}
+
+int g_grid_ldg = 0, g_grid_pipe = 0, g_grid_grp = 0, g_grid_par = 0;
 
 // ---- build -------------------------------------------------------------------------------
 constexpr int kSortWin = kStride * 2048;  // rows per degree-sort window (whole groups)
@@ -1147,6 +1434,30 @@ int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
     return rc;
 }
 
+// slot of every swept CSR edge, then the twin slot of every slot (parallel schedule)
+__global__ void eslot_kernel(int64_t npos_sw, const uint2 *info, const uint32_t *srow,
+                             const uint32_t *sdeg, const uint32_t *row_ptr, uint32_t *eslot) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= npos_sw) return;
+    const uint32_t d = sdeg[p];
+    if (!d) return;
+    const uint2 si = info[p >> 5];
+    const uint32_t e0 = row_ptr[srow[p]], l = (uint32_t)(p & 31);
+    for (uint32_t q = 0; q < d; ++q) eslot[e0 + q] = si.x + (uint32_t)kStride * q + l;
+}
+__global__ void stwin_kernel(int64_t npos_sw, const uint2 *info, const uint32_t *srow,
+                             const uint32_t *sdeg, const uint32_t *row_ptr, const EdgeRec *er,
+                             const uint32_t *eslot, uint32_t *stwin) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= npos_sw) return;
+    const uint32_t d = sdeg[p];
+    if (!d) return;
+    const uint2 si = info[p >> 5];
+    const uint32_t e0 = row_ptr[srow[p]], l = (uint32_t)(p & 31);
+    for (uint32_t q = 0; q < d; ++q)
+        stwin[si.x + (uint32_t)kStride * q + l] = eslot[er[e0 + q].rev];
+}
+
 // per-position copies of the node priors and rhs (after every prior computation)
 cudaError_t refresh_slice_nodes(const DeviceGraph &g, cudaStream_t st) {
     if (g.nslices == 0) return cudaSuccess;
@@ -1168,6 +1479,27 @@ cudaError_t slice_map_index(const DeviceGraph &g, uint32_t *idx, int64_t cnt, cu
     if (cnt <= 0) return cudaSuccess;
     map_pos_kernel<<<grid_of(cnt), 256, 0, st>>>(cnt, g.pos, idx);
     return cudaGetLastError();
+}
+
+int build_stwin(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
+    if (g.stwin || g.nslices == 0) return GABP_OK;
+    if (g.row_lo != 0 || g.row_hi != g.n) {
+        snprintf(err, errlen, "the parallel slice kernel runs on whole graphs only");
+        return GABP_EINVAL;
+    }
+    uint32_t *eslot = nullptr;
+    SCHECK(cudaMallocAsync(&eslot, sizeof(uint32_t) * (g.E > 0 ? g.E : 1), st));
+    SCHECK(cudaMallocAsync(&g.stwin, sizeof(uint32_t) * (g.nslots + kSlotPad), st));
+    SCHECK(cudaMemsetAsync(g.stwin, 0, sizeof(uint32_t) * (g.nslots + kSlotPad), st));
+    const int64_t npos_sw = g.nslices * 32;
+    eslot_kernel<<<grid_of(npos_sw), 256, 0, st>>>(npos_sw, g.slice_info, g.srow, g.sdeg,
+                                                   g.row_ptr, eslot);
+    stwin_kernel<<<grid_of(npos_sw), 256, 0, st>>>(npos_sw, g.slice_info, g.srow, g.sdeg,
+                                                   g.row_ptr, g.er, eslot, g.stwin);
+    SCHECK(cudaGetLastError());
+    cudaFreeAsync(eslot, st);
+    SCHECK(cudaStreamSynchronize(st));
+    return GABP_OK;
 }
 
 cudaError_t prepare_slice_kernels() {
@@ -1198,6 +1530,14 @@ cudaError_t prepare_slice_kernels() {
                                                            kGrpSmem)) != cudaSuccess)
         return e;
     g_grid_grp = sms * (occ > 0 ? occ : 1);
+    for (auto k : {slice_kernel_par<false>, slice_kernel_par<true>})
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kGrpSmem)) != cudaSuccess)
+            return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slice_kernel_par<false>,
+                                                           kGThreads, kGrpSmem)) != cudaSuccess)
+        return e;
+    g_grid_par = sms * (occ > 0 ? occ : 1);
     return cudaSuccess;
 }
 
@@ -1247,6 +1587,18 @@ cudaError_t launch_slice_part(const SweepArgs &a, int reserve_sms, cudaStream_t 
     t.part_base = 0;
     t.exact_primary = 0;
     launch_slice_exact(t, st);
+    return cudaGetLastError();
+}
+
+// Parallel schedule: the fast kernel, then its exact twin (exits unless flagged).
+cudaError_t launch_slice_parallel(const SweepArgs &a, cudaStream_t st) {
+    int64_t grid = g_grid_par > 0 ? g_grid_par : 148;
+    const int64_t need = (a.sl_hi - a.sl_lo) / kGroup;
+    if (grid > need) grid = need > 0 ? need : 1;
+    slice_kernel_par<false><<<(unsigned)grid, kGThreads, kGrpSmem, st>>>(a);
+    SweepArgs t = a;
+    t.exact_primary = 0;
+    slice_kernel_par<true><<<(unsigned)grid, kGThreads, kGrpSmem, st>>>(t);
     return cudaGetLastError();
 }
 

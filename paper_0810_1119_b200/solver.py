@@ -63,8 +63,8 @@ class SolveOptions:
             raise ValueError(f"schedule must be one of {SCHEDULES}")
         if self.gather_mode not in _lib.GATHER_IDS:
             raise ValueError(f"gather_mode must be one of {tuple(_lib.GATHER_IDS)}")
-        if self.gather_mode == "slice" and self.schedule != "broadcast":
-            raise ValueError("the slice layout runs the broadcast schedule")
+        if self.gather_mode == "slice" and self.schedule == "serial":
+            raise ValueError("the slice layout runs the synchronous schedules")
 
 
 def _gpu_schedule(schedule: str) -> int:

@@ -498,7 +498,7 @@ def test_slice_ragged_vs_tiles_and_oracle():
 def test_slice_needs_broadcast_and_layout():
     s = G.gen_poisson2d(8, 0).system
     with pytest.raises(ValueError):
-        G.SolveOptions(schedule="parallel", gather_mode="slice")
+        G.SolveOptions(schedule="serial", gather_mode="slice")
     # a hub longer than the slice limit: tiles only, auto still solves
     n = 5001
     pi = np.zeros(n - 1, dtype=np.int64)
@@ -578,3 +578,34 @@ def test_skewed_degrees_fall_back_to_tiles():
     r = G.solve_graph(g, G.SolveOptions(schedule="broadcast", epsilon=1e-12))
     assert r.iterations == orc.iterations
     np.testing.assert_array_equal(r.means, orc.means)
+
+
+@pytest.mark.parametrize("which", ["ragged", "random64k", "poisson2d_200", "golden"])
+def test_parallel_schedule_slice_kernel_bitwise(which):
+    """The parallel schedule on the slice groups (exclusion sums over the contiguous
+    incoming slots, scattered twin stores) against the oracle and the tile kernel."""
+    if which == "ragged":
+        systems = [_ragged_system()]
+    elif which == "random64k":
+        systems = [G.gen_random_sparse(1 << 16, 16, 3).system]
+    elif which == "poisson2d_200":
+        systems = [G.gen_poisson2d(200, 4).system]
+    else:
+        systems = [gc.system(gc.load(c)) for c in CASES]
+    for s in systems:
+        og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+        orc = oracle.solve(og, epsilon=1e-300, max_iter=80, schedule="parallel",
+                           rel_residual_tol=1e-8)
+        g = G.build_graph(s)
+        for mode in ("slice", "message"):
+            if mode == "slice" and int(g.info.num_slices) == 0:
+                continue
+            r = G.solve_graph(g, G.SolveOptions(schedule="parallel", epsilon=1e-300,
+                                                max_iter=80, rel_residual_tol=1e-8,
+                                                gather_mode=mode))
+            assert r.iterations == orc.iterations and r.converged == orc.converged, mode
+            assert r.diverged == orc.diverged
+            np.testing.assert_array_equal(r.means, orc.means)
+            np.testing.assert_array_equal(r.precisions, orc.precisions)
+            np.testing.assert_array_equal(np.asarray(r.max_change_history),
+                                          np.asarray(orc.max_change_history))
