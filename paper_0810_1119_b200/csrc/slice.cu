@@ -1055,6 +1055,11 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
             for (int jj = 0; jj < kPB; ++jj) {  // block `pass`: sums start at the prior
                 row.aP[jj] = row.pP;
                 row.aN[jj] = row.pN;
+            }
+        }
+        if (m.b + 1 == m.nb) {  // last chunk of the pass: the block's coefficients and twins
+#pragma unroll
+            for (int jj = 0; jj < kPB; ++jj) {
                 const uint32_t j = pass * kPB + jj;
                 row.cb[jj] = 1.0;
                 row.tw[jj] = 0u;
