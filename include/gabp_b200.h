@@ -91,6 +91,10 @@ typedef struct {
     int64_t messages_sent;    /* MessageState.messages_sent of the final state */
     double device_ms;         /* CUDA-event time of the sweep loop */
     double final_rel_residual;/* ||Ax-b||/||b|| of the returned means */
+    int64_t residual_probes;  /* residual-only launches / twin probes that decided a sweep
+                                 one launch early */
+    int64_t kernel_launches;  /* kernels the solve loop enqueued (incl. launches that exit at
+                                 once after the decision); 0 for multi-rank solves */
 } gabp_report_t;
 
 const char *gabp_last_error(void);

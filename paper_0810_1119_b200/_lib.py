@@ -65,7 +65,8 @@ class Report(ctypes.Structure):
     _fields_ = [("converged", ctypes.c_int32), ("diverged", ctypes.c_int32),
                 ("iterations", ctypes.c_int64), ("n_hist", ctypes.c_int64),
                 ("sweeps_launched", ctypes.c_int64), ("messages_sent", ctypes.c_int64),
-                ("device_ms", ctypes.c_double), ("final_rel_residual", ctypes.c_double)]
+                ("device_ms", ctypes.c_double), ("final_rel_residual", ctypes.c_double),
+                ("residual_probes", ctypes.c_int64), ("kernel_launches", ctypes.c_int64)]
 
 
 class GabpError(RuntimeError):

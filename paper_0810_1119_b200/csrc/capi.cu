@@ -109,6 +109,7 @@ struct gabp_graph {
     double *change_hist = nullptr, *res_hist = nullptr, *rsq_hist = nullptr;
     int64_t hist_cap = 0;
     uint64_t ws_gen = 0;
+    int64_t kernels_launched = 0;  // kernels the last solve loop enqueued (report)
     // cached CUDA graph of a chunk of sweep launches
     cudaGraphExec_t chunk_exec = nullptr;
     int chunk_len = 0, chunk_sched = -1, chunk_gather = -1;
@@ -558,6 +559,10 @@ int finish_loop(gabp_graph *G, double *device_ms) {
     }
     if (!G->h_ctrl->done)
         return fail(GABP_ECUDA, "solve loop ended without a decision (internal error)");
+    if (host_timing())
+        fprintf(stderr, "[gabp] solve: %lld sweeps, %lld launched, %d residual probes\n",
+                (long long)G->h_ctrl->iterations, (long long)(G->h_ctrl->next_sweep - 1),
+                (int)G->h_ctrl->probes);
     return GABP_OK;
 }
 
@@ -691,8 +696,11 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
     const double t_setup = host_ms();
     int rc = solve_setup(G, opt);
     if (rc) return rc;
+    G->kernels_launched = 0;
     cudaStream_t st = G->stream;
-    const int64_t total = opt->max_iter + 2;
+    // max_iter + 2 sweep launches, plus at most one residual-only launch per sweep (slice
+    // path, probe_next) -- the loop normally stops on the polled done flag long before
+    const int64_t total = 2 * opt->max_iter + 4;
     int64_t launched = 0;
     Poller P{G};
     if (G->dist) {
@@ -728,6 +736,7 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
             CK(cudaMemset(G->dnode, 0, sizeof(double2) * Kp));  // padding rows stay zero
         }
         CK(cudaMemsetAsync(G->dmsg[0], 0, sizeof(double2) * Kp * Kp, st));
+        G->kernels_launched = 0;
         gabp::DenseArgs d{};
         d.K = K;
         d.ld = Kp;
@@ -743,6 +752,7 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
             const int64_t k = total - launched < C ? total - launched : C;
             for (int64_t q = 0; q < k; ++q) CK(gabp::launch_dense_sweep(a, d, st));
             launched += k;
+            G->kernels_launched += 2 * k;  // column walk + pair tiles
             if (P.after_chunk(st, &rc)) break;
             if (rc) return rc;
         }
@@ -765,9 +775,13 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         fprintf(stderr, "[gabp] run_solve: setup %.2f ms, chunk graph (%d sweeps) %.2f ms\n",
                 tc0 - t_setup, C, host_ms() - tc0);
     SweepArgs a = make_args(G);
+    // kernels per sweep launch: slice paths fast kernel + exact twin, tile path one
+    const int kps = (gather == gabp::kGatherSlice || gather == gabp::kGatherSliceParallel) ? 2 : 1;
+    G->kernels_launched = 0;
     CK(cudaEventRecord(G->ev[2], st));
     while (launched < total) {
         const int64_t k = total - launched < C ? total - launched : C;
+        G->kernels_launched += kps * k;
         if (k == C) {
             CK(cudaGraphLaunch(G->chunk_exec, st));
         } else {
@@ -793,6 +807,8 @@ void fill_report(gabp_graph *G, const gabp_options_t *opt, double ms, double rsq
     rep->messages_sent =
         c.iterations * (opt->schedule == GABP_SCHED_BROADCAST ? G->g.n : G->g.E);
     rep->device_ms = ms;
+    rep->residual_probes = c.probes;
+    rep->kernel_launches = G->kernels_launched;
     rep->final_rel_residual =
         (c.n_hist >= 1 && G->g.rhs_norm > 0.0) ? sqrt(rsq_last) / G->g.rhs_norm : NAN;
 }

@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <float.h>
 #include <stdint.h>
 
 #include "../../include/gabp_b200.h"
@@ -97,6 +98,9 @@ struct Ctrl {
     uint32_t work_twin;         // claims of an exact group twin (zeroed when redo becomes 2)
     uint32_t work[kStatSlots];  // slice TMA kernel: next work unit of launch s (slot s % 4);
                                 // the last CTA of launch s zeroes slot (s + 2) % 4
+    int64_t probe_t;            // slice path: sweep T whose residual the exact twin after
+                                // launch T+1 computes, deciding T a launch early (0: none)
+    int32_t probes;             // residual probes run (diagnostics)
 };
 
 // A fresh controller: every "first index" slot at the kNoIndex sentinel.
@@ -156,6 +160,7 @@ struct SweepArgs {
     const uint32_t *scol;      // position of the destination, per slot
     const double *scoef;       // A_ij per slot
     const uint32_t *stwin;     // slot of the twin message (parallel schedule), per slot
+    int probe;                 // the exact twin of this launch can run the residual probe
 };
 
 // kernels (sweep.cu); prepare_sweep_kernels() must run once per device before launches
@@ -173,12 +178,40 @@ cudaError_t launch_residual_sq(int64_t n, const uint32_t *row_ptr, const EdgeRec
                                const double *diag, const double *rhs, const double *x,
                                double *part, int64_t nparts, double *out, cudaStream_t st);
 
+// Controller fields a decision reads, loaded together from L2 (ld.global.cg, independent
+// loads the compiler issues back to back): the decision sits on the critical path between
+// two launches, where a chain of volatile loads costs ~0.3 us each.
+struct CtrlSnap {
+    int32_t done, msg_nonfinite, means_nonfinite;
+    int64_t max_iter, n;
+    unsigned long long change_bits, singular_min, agg_singular;
+    double epsilon, rel_tol, bnorm;
+};
+__device__ __forceinline__ CtrlSnap ctrl_snap(volatile Ctrl *vc, int slot) {
+    const Ctrl *c = const_cast<const Ctrl *>(vc);
+    CtrlSnap r;
+    r.done = __ldcg(&c->done);
+    r.msg_nonfinite = __ldcg(&c->msg_nonfinite[slot]);
+    r.means_nonfinite = __ldcg(&c->means_nonfinite[slot]);
+    r.max_iter = (int64_t)__ldcg(reinterpret_cast<const long long *>(&c->max_iter));
+    r.n = (int64_t)__ldcg(reinterpret_cast<const long long *>(&c->n));
+    r.change_bits = __ldcg(&c->change_bits[slot]);
+    r.singular_min = __ldcg(&c->singular_min[slot]);
+    r.agg_singular = __ldcg(&c->agg_singular[slot]);
+    r.epsilon = __ldcg(&c->epsilon);
+    r.rel_tol = __ldcg(&c->rel_tol);
+    r.bnorm = __ldcg(&c->bnorm);
+    return r;
+}
+
 // Decision for sweep t (solver.py:321-345), executed by one thread of the last CTA (or of
 // finish_kernel in multi-rank mode).
 __device__ __forceinline__ void decide_sweep(volatile Ctrl *c, SweepArgs const &a, int64_t t, double rsq_t) {
-    if (t < 1 || c->done || t > c->max_iter) return;
+    if (t < 1) return;
     const int slot = (int)(t % kStatSlots);
-    if (c->singular_min[slot] != kNoIndex || c->agg_singular[slot] != kNoIndex) {
+    const CtrlSnap k = ctrl_snap(c, slot);
+    if (k.done || t > k.max_iter) return;
+    if (k.singular_min != kNoIndex || k.agg_singular != kNoIndex) {
         // SingularSubgraphError: state not advanced, no history row (solver.py:322-326)
         c->diverged = 1;
         c->iterations = t - 1;
@@ -189,29 +222,60 @@ __device__ __forceinline__ void decide_sweep(volatile Ctrl *c, SweepArgs const &
     }
     // max change over the finite differences (a NaN difference, possible only when a
     // message is non-finite -- the run is then diverged -- is not propagated)
-    const double change =
-        __longlong_as_double((long long)(unsigned long long)c->change_bits[slot]);
-    const bool means_finite = !c->means_nonfinite[slot];
-    const double res = means_finite ? sqrt(rsq_t) / (double)c->n : INFINITY;
+    const double change = __longlong_as_double((long long)k.change_bits);
+    const bool means_finite = !k.means_nonfinite;
+    const double res = means_finite ? sqrt(rsq_t) / (double)k.n : INFINITY;
     a.change_hist[t - 1] = change;
     a.res_hist[t - 1] = res;
     a.rsq_hist[t - 1] = means_finite ? rsq_t : INFINITY;
     c->n_hist = t;
     c->iterations = t;
     c->final_slot = t % 3;
-    if (c->msg_nonfinite[slot] || !means_finite) {  // not finite or biggest > blowup
+    if (k.msg_nonfinite || !means_finite) {  // not finite or biggest > blowup
         c->diverged = 1;
         c->done = 1;
-    } else if (change < c->epsilon) {
+    } else if (change < k.epsilon) {
         c->converged = 1;
         c->done = 1;
-    } else if (c->rel_tol > 0.0 && sqrt(rsq_t) < c->rel_tol * c->bnorm) {
+    } else if (k.rel_tol > 0.0 && sqrt(rsq_t) < k.rel_tol * k.bnorm) {
         c->converged = 1;
         c->done = 1;
-    } else if (t >= c->max_iter) {
+    } else if (t >= k.max_iter) {
         c->diverged = 1;  // sweep cap (solver.py:344-345)
         c->done = 1;
     }
+}
+
+// Residual probe (slice path, slice.cu): at the end of launch T+1 -- after the decision
+// for T-1 -- the statistics of sweep T and of x^{(T)} are complete; only the residual of
+// x^{(T)} is missing, and launch T+2 would compute it alongside a whole sweep T+1 that is
+// thrown away when T ends the solve.  Returns T when that decision is certain (divergence,
+// singular, epsilon test, sweep cap) or when the residual test is predicted to pass
+// (geometric extrapolation of the last two residuals, margin shrinking to 1 as the
+// contraction rate approaches 1, where a missed prediction costs a negligible fraction of
+// the solve); the next launch then computes only the residual of x^{(T)} and decides T.
+// rsq_prev is the squared residual of x^{(T-1)} decided just now.
+__device__ __forceinline__ int64_t probe_next(volatile Ctrl *c, SweepArgs const &a, int64_t T,
+                                              double rsq_prev) {
+    if (T < 1) return 0;
+    const int slot = (int)(T % kStatSlots);
+    const CtrlSnap k = ctrl_snap(c, slot);
+    const double r2 = T >= 3 ? a.rsq_hist[T - 3] : 0.0;  // x^{(T-2)}
+    if (k.done || T > k.max_iter) return 0;
+    if (k.singular_min != kNoIndex || k.agg_singular != kNoIndex || k.msg_nonfinite ||
+        k.means_nonfinite || T >= k.max_iter)
+        return T;
+    if (__longlong_as_double((long long)k.change_bits) < k.epsilon) return T;
+    if (k.rel_tol > 0.0 && T >= 3) {
+        const double r1 = rsq_prev;  // x^{(T-1)}
+        if (r2 > 0.0 && r1 <= DBL_MAX && r2 <= DBL_MAX) {
+            const double rho2 = fmin(r1 / r2, 1.0);  // squared contraction per sweep
+            const double m = 1.0 + 0.5 * (1.0 - sqrt(rho2));
+            const double lim = k.rel_tol * k.bnorm;
+            if (r1 * rho2 < lim * lim * m * m) return T;
+        }
+    }
+    return 0;
 }
 
 // dense variant (dense.cu): A row-major K x K, messages a padded K x K matrix ring

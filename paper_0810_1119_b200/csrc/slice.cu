@@ -50,6 +50,7 @@ struct SliceSmem {
     TailSmem<8> tail;  // up to 256 threads per CTA
     int64_t sweep;
     int skip;
+    int probe;
 };
 
 // IEEE a / b.  The fast kernels use the replicated div.rn fast path only and flag the
@@ -789,6 +790,84 @@ __device__ __forceinline__ void grp_consume(const SweepArgs &a, int64_t s, Stats
     }
 }
 
+// Residual-only group launch (the probe on the TMA ring): the producer streams scoef and
+// scol (12 B per slot, as for launch 2); consumers gather x^{(s-2)} and form the residual
+// rows of x^{(s-2)} exactly as a full launch s would (grp_step, PH 3).
+template <int R>
+__device__ __forceinline__ void grp_consume_res(const SweepArgs &a, Stats &st, int lane,
+                                                int warp, GRing &G) {
+    const Ring<R> r(a);
+    const int t = warp * 32 + lane;
+    t_wait(&G.full[0], 0u);
+    GMeta m = G.meta[0];
+    if (m.g < 0) return;
+    double2 hnd;
+    double hxo = 0.0, hrhs = 0.0;
+    uint32_t hd;
+    {
+        const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
+        hnd = __ldg(a.snd + p);
+        hd = __ldg(a.sdeg + p);
+        hxo = __ldcg(&r.g2[p].x);
+        hrhs = __ldg(a.srhs + p);
+    }
+    double gx[kGC], nx[kGC];
+#pragma unroll
+    for (int u = 0; u < kGC; ++u)
+        gx[u] = m.b * kGC + u < m.w ? __ldcg(&r.g2[G.st[0].col[u][t]].x) : 0.0;
+    uint32_t d = 0;
+    double y = 0.0, rhs_i = 0.0, diag = 0.0;
+    for (uint32_t k = 0;; ++k) {
+        if (m.b == 0) {
+            d = hd;
+            diag = hnd.x;
+            y = hnd.x * hxo;
+            rhs_i = hrhs;
+        }
+        const int s1 = (int)((k + 1) % kGS);
+        t_wait(&G.full[s1], ((k + 1) / kGS) & 1u);
+        const GMeta mn = G.meta[s1];
+        if (mn.g >= 0) {
+            if (mn.b == 0) {
+                const int64_t pn = ((int64_t)mn.g * kGroup + warp) * 32 + lane;
+                hnd = __ldg(a.snd + pn);
+                hd = __ldg(a.sdeg + pn);
+                hxo = __ldcg(&r.g2[pn].x);
+                hrhs = __ldg(a.srhs + pn);
+            }
+#pragma unroll
+            for (int u = 0; u < kGC; ++u)
+                nx[u] = mn.b * kGC + u < mn.w ? __ldcg(&r.g2[G.st[s1].col[u][t]].x) : 0.0;
+        }
+        const int s0 = (int)(k % kGS);
+        double cc[kGC];
+#pragma unroll
+        for (int u = 0; u < kGC; ++u) cc[u] = G.st[s0].c[u][t];
+        __syncwarp();
+        if (lane == 0) t_arrive(&G.empty[s0]);
+#pragma unroll
+        for (int u = 0; u < kGC; ++u)
+            if (m.b * kGC + u < d) y = y + cc[u] * gx[u];
+        if (m.b + 1 == m.nb && diag != 0.0) {
+            const double rr = y - rhs_i;
+            st.rsq += rr * rr;
+        }
+        if (mn.g < 0) break;
+        m = mn;
+#pragma unroll
+        for (int u = 0; u < kGC; ++u) gx[u] = nx[u];
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void slice_res_grp(const SweepArgs &a, Stats &st, int lane, int warp,
+                                              GRing &G, uint32_t *ctr) {
+    if (warp == kGroup)
+        grp_produce<2, R>(a, G, ctr, lane);
+    else
+        grp_consume_res<R>(a, st, lane, warp, G);
+}
+
 template <int PH, int R>
 __device__ __forceinline__ void slice_sweep_grp(const SweepArgs &a, int64_t s, Stats &st,
                                                 int lane, int warp, GRing &G, uint32_t *ctr) {
@@ -804,20 +883,115 @@ __device__ __forceinline__ bool slice_prologue(SM &S, const SweepArgs &a, bool e
     if (threadIdx.x == 0) {
         volatile Ctrl *vc = a.ctrl;
         const int64_t s = vc->next_sweep;
-        S.skip = vc->done || s > vc->max_iter + 2 || (exact && !a.exact_primary && vc->redo != 2);
+        const bool twin = exact && !a.exact_primary;
+        S.skip = vc->done || s > vc->max_iter + 2 || (twin && vc->redo != 2);
+        // the residual probe the last launch asked for (probe_next): run by an idle exact
+        // twin (a.probe == 1) or as a residual-only group launch (a.probe == 2)
+        const bool mine = twin ? (a.probe == 1 && vc->redo != 2) : (!exact && a.probe == 2);
+        S.probe = mine && !vc->done && vc->probe_t != 0 && vc->probe_t == s - 2;
         S.sweep = s;
     }
     __syncthreads();
     return !S.skip;
 }
 
-// EXACT = false: the sweep with fast-path divisions only (every launch).  EXACT = true:
-// the same sweep with IEEE divisions, launched right after it; it runs only when the fast
-// launch flagged an out-of-range division or a singular value (Ctrl.redo == 2).
+// ---- residual probe ----------------------------------------------------------------------
+// Run by the exact twin after launch T+1 when that launch's decision step expects sweep T
+// to end the solve (probe_next, gabp_internal.cuh): the residual of x^{(T)} in one pass over
+// scol / scoef (12 B per slot) with gathers of x^{(T)}, then the decision for T -- so launch
+// T+2, which would otherwise compute it next to a whole discarded sweep T+1, exits at once.
+// Per row the sweep kernels' sum (A_ii x_i, then + A_ij x_j in ascending j); rows summed per
+// warp, CTA partials in CTA order.  Batches of kRU columns: all slot loads, then all
+// gathers, then the sums (memory-level parallelism of a latency-bound pass).
+constexpr int kRU = 16;
+
+// Residual of x^{(t)} summed over the CTAs (partials in CTA order), then the decision for
+// t.  work_slot >= 0: a residual-only group launch, which leaves next_sweep alone (the next
+// launch runs the same sweep when t was not the last) and re-arms its claim counter.
+template <int NT>
+__device__ __forceinline__ void probe_finish(TailSmem<NT / 32> &T, const SweepArgs &a,
+                                             int64_t t, double rsq, int work_slot) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    rsq = warp_sum(rsq);
+    if (lane == 0) T.red_d[0][warp] = rsq;
+    __syncthreads();
+    if (tid == 0) {
+        double b = 0.0;
+        for (int w = 0; w < NT / 32; ++w) b += T.red_d[0][w];
+        a.rsq_part[blockIdx.x] = b;
+        __threadfence();
+        T.last = atomicAdd(&a.ctrl->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!T.last) return;
+    __threadfence();
+    double part = 0.0;
+    volatile const double *rp = a.rsq_part;
+    for (int64_t b = tid; b < (int64_t)gridDim.x; b += NT) part += rp[b];
+    part = warp_sum(part);
+    __syncthreads();
+    if (lane == 0) T.red_d[0][warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+        double rsq_t = 0.0;
+        for (int w = 0; w < NT / 32; ++w) rsq_t += T.red_d[0][w];
+        volatile Ctrl *c = a.ctrl;
+        decide_sweep(c, a, t, rsq_t);
+        if (work_slot >= 0) c->work[work_slot] = 0u;
+        c->ticket = 0u;
+        c->probe_t = 0;
+        c->probes = c->probes + 1;
+        __threadfence();
+    }
+}
+
+template <int NT>
+__device__ __noinline__ void probe_residual(TailSmem<NT / 32> &T, const SweepArgs &a, int64_t t) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const NodeState *xr = a.rec[t % 3];
+    const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+    double rsq = 0.0;
+    for (int64_t sl = (int64_t)blockIdx.x * (NT / 32) + warp; sl < a.nslices; sl += nw) {
+        const int64_t p = sl * 32 + lane;
+        const uint2 si = __ldg(a.slice_info + sl);
+        const double2 nd = __ldg(a.snd + p);
+        const uint32_t d = __ldg(a.sdeg + p);
+        double y = nd.x * __ldcg(&xr[p].x);
+        for (uint32_t q0 = 0; q0 < si.y; q0 += kRU) {  // (si.y: the group width, warp-uniform)
+            const uint32_t slot = si.x + (uint32_t)kStride * q0 + (uint32_t)lane;
+            uint32_t cj[kRU];
+            double cv[kRU], xv[kRU];
+#pragma unroll
+            for (int u = 0; u < kRU; ++u) {
+                cj[u] = 0u;
+                cv[u] = 0.0;
+                if (q0 + u < si.y) {
+                    cj[u] = __ldcs(a.scol + slot + (uint32_t)kStride * u);
+                    cv[u] = __ldcs(a.scoef + slot + (uint32_t)kStride * u);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kRU; ++u) xv[u] = q0 + u < si.y ? __ldcg(&xr[cj[u]].x) : 0.0;
+#pragma unroll
+            for (int u = 0; u < kRU; ++u)
+                if (q0 + u < d) y = y + cv[u] * xv[u];
+        }
+        if (nd.x != 0.0) {  // (A_ii == 0: padding lane)
+            const double r = y - __ldg(a.srhs + p);
+            rsq += r * r;
+        }
+    }
+    probe_finish<NT>(T, a, t, rsq, -1);
+}
 template <bool EXACT>
 __global__ void __launch_bounds__(kLThreads, 2) slice_kernel_ldg(const SweepArgs a) {
     __shared__ SliceSmem S;
-    if (!slice_prologue(S, a, EXACT)) return;
+    if (!slice_prologue(S, a, EXACT)) {
+        if (EXACT && S.probe)
+            probe_residual<kLThreads>(*reinterpret_cast<TailSmem<kLWarps> *>(&S.tail), a,
+                                      S.sweep - 2);
+        return;
+    }
     const int64_t s = S.sweep;
     const int tid = threadIdx.x, lane = tid & 31;
     Stats st;
@@ -869,6 +1043,7 @@ struct GrpSmem {
     TailSmem<kGroup + 1> tail;
     int64_t sweep;
     int skip;
+    int probe;
 };
 
 __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_grp(const SweepArgs a) {
@@ -887,6 +1062,17 @@ __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_grp(const SweepArgs
     uint32_t *ctr = &a.ctrl->work[s % kStatSlots];
     Stats st;
     st.lim = fmin(a.ctrl->blowup, DBL_MAX);
+    if (S.probe) {  // residual-only launch: decide sweep s-2 without computing sweep s-1
+        const int r = (int)(s % 3);
+        if (r == 0)
+            slice_res_grp<0>(a, st, lane, warp, G, ctr);
+        else if (r == 1)
+            slice_res_grp<1>(a, st, lane, warp, G, ctr);
+        else
+            slice_res_grp<2>(a, st, lane, warp, G, ctr);
+        probe_finish<kGThreads>(S.tail, a, s - 2, st.rsq, (int)(s % kStatSlots));
+        return;
+    }
     if (s >= 3) {
         const int r = (int)(s % 3);
         if (r == 0)
@@ -1160,7 +1346,10 @@ __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_par(const SweepArgs
     __shared__ GrpSmem S;
     extern __shared__ __align__(128) unsigned char par_raw[];
     GRing &G = *reinterpret_cast<GRing *>(par_raw);
-    if (!slice_prologue(S, a, EXACT)) return;
+    if (!slice_prologue(S, a, EXACT)) {
+        if (EXACT && S.probe) probe_residual<kGThreads>(S.tail, a, S.sweep - 2);
+        return;
+    }
     const int64_t s = S.sweep;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < kGS) {
@@ -1546,6 +1735,12 @@ cudaError_t prepare_slice_kernels() {
     return cudaSuccess;
 }
 
+// GABP_NO_PROBE=1 disables the residual probe (A/B timing)
+static bool probe_enabled() {
+    static const int off = getenv("GABP_NO_PROBE") ? atoi(getenv("GABP_NO_PROBE")) : 0;
+    return !off;
+}
+
 // the exact register-batch kernel over [a.sl_lo, a.sl_hi): the twin (runs only when the
 // fast launch flagged itself) or, with a.exact_primary, the sweep itself; returns its grid
 static int64_t launch_slice_exact(const SweepArgs &a, cudaStream_t st) {
@@ -1575,7 +1770,10 @@ cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st) {
 // One sweep over [a.sl_lo, a.sl_hi) with the fast kernel (reserve_sms SMs left free for a
 // concurrent exchange), then the exact twin over every slice: a flagged launch is redone
 // whole, so the statistics of an earlier part of the same sweep are re-taken too.
-cudaError_t launch_slice_part(const SweepArgs &a, int reserve_sms, cudaStream_t st) {
+cudaError_t launch_slice_part(const SweepArgs &a0, int reserve_sms, cudaStream_t st) {
+    SweepArgs a = a0;
+    // residual probe: a residual-only group launch (variant 2), else run by the exact twin
+    a.probe = (!a0.dist && probe_enabled()) ? (a0.slice_variant == 2 ? 2 : 1) : 0;
     if (a.slice_variant == 2) {
         int64_t grid = (g_grid_grp > 0 ? g_grid_grp : 148) - reserve_sms;
         const int64_t need = (a.sl_hi - a.sl_lo) / kGroup;
@@ -1596,7 +1794,9 @@ cudaError_t launch_slice_part(const SweepArgs &a, int reserve_sms, cudaStream_t 
 }
 
 // Parallel schedule: the fast kernel, then its exact twin (exits unless flagged).
-cudaError_t launch_slice_parallel(const SweepArgs &a, cudaStream_t st) {
+cudaError_t launch_slice_parallel(const SweepArgs &a0, cudaStream_t st) {
+    SweepArgs a = a0;
+    a.probe = (!a0.dist && probe_enabled()) ? 1 : 0;
     int64_t grid = g_grid_par > 0 ? g_grid_par : 148;
     const int64_t need = (a.sl_hi - a.sl_lo) / kGroup;
     if (grid > need) grid = need > 0 ? need : 1;

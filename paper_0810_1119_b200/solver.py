@@ -160,6 +160,8 @@ class SolveReport:
     device_ms: float = 0.0
     sweeps_launched: int = 0
     final_rel_residual: float = float("nan")
+    residual_probes: int = 0
+    kernel_launches: int = 0
 
 
 def initial_state(graph: GaussianGraph, schedule: str = "parallel") -> MessageState:
@@ -257,6 +259,8 @@ def solve_graph(graph: GaussianGraph, options: SolveOptions | None = None) -> So
         device_ms=float(rep.device_ms),
         sweeps_launched=int(rep.sweeps_launched),
         final_rel_residual=float(rep.final_rel_residual),
+        residual_probes=int(rep.residual_probes),
+        kernel_launches=int(rep.kernel_launches),
     )
 
 
