@@ -576,8 +576,52 @@ __device__ __forceinline__ void t_bulk_ef(void *dst, const void *src, unsigned b
 __device__ __forceinline__ uint2 group_info(const SweepArgs &a, int64_t g, int64_t g_hi) {
     return g < g_hi ? __ldg(a.slice_info + g * kGroup) : make_uint2(0u, 0u);
 }
+template <int CW = kGC>
 __device__ __forceinline__ uint32_t chunks_of(uint32_t w) {
-    return w > 0 ? (w + kGC - 1) / kGC : 1u;
+    return w > 0 ? (w + CW - 1) / CW : 1u;
+}
+
+// Launch kinds of the group kernel (PH): 3 a full launch (scoef, scol, I^{(s-2)}, I^{(s-3)}:
+// 44 B per slot); 4 launch 3, whose I^{(s-3)} = I^{(0)} is +0 (no stream: 28 B); 2 launch 2,
+// whose m^{(0)} = 0 (scoef, scol: 12 B); 5 a residual-only launch (12 B).  The 12-byte kinds
+// lay a stage out as NStage, kNC2 / kNCR columns per chunk instead of kGC: the same bytes
+// per ring trip, so the ring keeps as much DRAM traffic in flight as a full launch does.
+template <int CW>
+struct NStage {
+    double c[CW][kStride];
+    uint32_t col[CW][kStride];
+};
+#ifndef GABP_NC2
+#define GABP_NC2 3
+#endif
+constexpr int kNC2 = GABP_NC2;  // launch 2: gathers {P, N} and the edge divisions in registers
+#ifndef GABP_NCR
+#define GABP_NCR 6
+#endif
+constexpr int kNCR = GABP_NCR;  // residual-only launch
+static_assert(sizeof(NStage<kNCR>) <= sizeof(GStage) && sizeof(NStage<kNC2>) <= sizeof(GStage),
+              "a narrow stage must fit a ring stage");
+template <int PH>
+constexpr int stage_cw() {
+    return PH == 2 ? kNC2 : PH == 5 ? kNCR : kGC;
+}
+template <int PH>
+constexpr unsigned stage_bytes() {
+    return PH == 3 ? 44u : PH == 4 ? 28u : 12u;
+}
+template <int PH>
+__device__ __forceinline__ const double *st_c(const GStage &S, int u) {
+    if constexpr (PH == 2 || PH == 5)
+        return reinterpret_cast<const NStage<stage_cw<PH>()> &>(S).c[u];
+    else
+        return S.c[u];
+}
+template <int PH>
+__device__ __forceinline__ const uint32_t *st_col(const GStage &S, int u) {
+    if constexpr (PH == 2 || PH == 5)
+        return reinterpret_cast<const NStage<stage_cw<PH>()> &>(S).col[u];
+    else
+        return S.col[u];
 }
 
 // Producer warp: claims groups and fills the ring until the claims run out.
@@ -596,7 +640,8 @@ __device__ __forceinline__ void grp_produce(const SweepArgs &a, GRing &G, uint32
     }
     int64_t gcur = g_lo + __shfl_sync(~0u, u0, 0), gnxt = g_lo + __shfl_sync(~0u, u1, 0);
     uint2 icur = group_info(a, gcur, ngroups), inxt = group_info(a, gnxt, ngroups);
-    uint32_t b = 0, nb = chunks_of(icur.y);
+    constexpr int CW = stage_cw<PH>();
+    uint32_t b = 0, nb = chunks_of<CW>(icur.y);
     for (uint32_t k = 0;; ++k) {
         const int stg = (int)(k % kGS);
         if (k >= (uint32_t)kGS) t_wait(&G.empty[stg], ((k / kGS) - 1u) & 1u);
@@ -608,8 +653,8 @@ __device__ __forceinline__ void grp_produce(const SweepArgs &a, GRing &G, uint32
             return;
         }
         if (lane == 0) {
-            const uint32_t w = icur.y, q0 = b * kGC;
-            const uint32_t nc = w > q0 ? min((uint32_t)kGC, w - q0) : 0u;
+            const uint32_t w = icur.y, q0 = b * CW;
+            const uint32_t nc = w > q0 ? min((uint32_t)CW, w - q0) : 0u;
             const uint32_t slot = icur.x + (uint32_t)kStride * q0;
             GMeta &m = G.meta[stg];
             m.g = (int32_t)gcur;
@@ -617,15 +662,21 @@ __device__ __forceinline__ void grp_produce(const SweepArgs &a, GRing &G, uint32
             m.nb = nb;
             m.w = w;
             m.gbase = icur.x;
-            GStage &S = G.st[stg];
             // (0 bytes: a group of isolated rows; the arrive alone completes the phase)
-            t_expect_tx(&G.full[stg], nc * (uint32_t)kStride * (PH == 3 ? 44u : 12u));
+            t_expect_tx(&G.full[stg], nc * (uint32_t)kStride * stage_bytes<PH>());
             if (nc) {
-                t_bulk_ef(&S.c[0][0], a.scoef + slot, nc * kStride * 8u, &G.full[stg], pol);
-                t_bulk_ef(&S.col[0][0], a.scol + slot, nc * kStride * 4u, &G.full[stg], pol);
-                if (PH == 3) {
+                if constexpr (PH == 2 || PH == 5) {
+                    NStage<CW> &N = reinterpret_cast<NStage<CW> &>(G.st[stg]);
+                    t_bulk_ef(&N.c[0][0], a.scoef + slot, nc * kStride * 8u, &G.full[stg], pol);
+                    t_bulk_ef(&N.col[0][0], a.scol + slot, nc * kStride * 4u, &G.full[stg], pol);
+                } else {
+                    GStage &S = G.st[stg];
+                    t_bulk_ef(&S.c[0][0], a.scoef + slot, nc * kStride * 8u, &G.full[stg], pol);
+                    t_bulk_ef(&S.col[0][0], a.scol + slot, nc * kStride * 4u, &G.full[stg], pol);
                     t_bulk_ef(&S.i2[0][0], r.I2 + slot, nc * kStride * 16u, &G.full[stg], pol);
-                    t_bulk_ef(&S.i3[0][0], r.I3 + slot, nc * kStride * 16u, &G.full[stg], pol);
+                    if (PH == 3)
+                        t_bulk_ef(&S.i3[0][0], r.I3 + slot, nc * kStride * 16u, &G.full[stg],
+                                  pol);
                 }
             }
         }
@@ -636,7 +687,7 @@ __device__ __forceinline__ void grp_produce(const SweepArgs &a, GRing &G, uint32
             inxt = group_info(a, gnxt, ngroups);
             if (lane == 0) pend = atomicAdd(ctr, 1u);
             b = 0;
-            nb = chunks_of(icur.y);
+            nb = chunks_of<CW>(icur.y);
         }
     }
 }
@@ -656,7 +707,7 @@ __device__ __forceinline__ void t_header(const SweepArgs &a, const Ring<R> &r, i
                                          THdr &h) {
     h.nd = __ldg(a.snd + p);
     h.d = __ldg(a.sdeg + p);
-    if (PH == 3) {
+    if (PH == 3 || PH == 4) {
         h.a3 = __ldcg(reinterpret_cast<const double2 *>(r.g3 + p));
         h.xo = __ldcg(&r.g2[p].x);
         h.rhs = __ldg(a.srhs + p);
@@ -664,13 +715,14 @@ __device__ __forceinline__ void t_header(const SweepArgs &a, const Ring<R> &r, i
 }
 
 // neighbour gathers of a landed chunk (node states of S_{s-2}), one chunk ahead of use
+template <int PH, int CW = stage_cw<PH>()>
 __device__ __forceinline__ void t_gather(const GStage &S, const GMeta &m, const NodeState *g2,
-                                         int t, double (&gP)[kGC], double (&gN)[kGC],
-                                         double (&gx)[kGC]) {
+                                         int t, double (&gP)[CW], double (&gN)[CW],
+                                         double (&gx)[CW]) {
 #pragma unroll
-    for (int u = 0; u < kGC; ++u) {
-        if (m.b * kGC + u < m.w) {
-            ld_node(g2 + S.col[u][t], gP[u], gN[u], gx[u]);
+    for (int u = 0; u < CW; ++u) {
+        if (m.b * CW + u < m.w) {
+            ld_node(g2 + st_col<PH>(S, u)[t], gP[u], gN[u], gx[u]);
         } else {
             gP[u] = 1.0;
             gN[u] = 1.0;
@@ -690,19 +742,19 @@ struct GRow {
 // (nP, nN, nx), then computes chunk k from its stage and the gathers (gP, gN, gx).  Returns
 // false after the last chunk; otherwise m becomes chunk k+1's descriptor.  The loop calls
 // it with the two gather buffers swapped on alternate chunks (no register copies).
-template <int PH, int R>
+template <int PH, int R, int CW = stage_cw<PH>()>
 __device__ __forceinline__ bool grp_step(const SweepArgs &a, const Ring<R> &r, double *xh,
                                          Stats &st, GRing &G, int lane, int warp, int t,
                                          uint32_t k, GMeta &m, THdr &hn, GRow &row,
-                                         const double (&gP)[kGC], const double (&gN)[kGC],
-                                         const double (&gx)[kGC], double (&nP)[kGC],
-                                         double (&nN)[kGC], double (&nx)[kGC]) {
+                                         const double (&gP)[CW], const double (&gN)[CW],
+                                         const double (&gx)[CW], double (&nP)[CW],
+                                         double (&nN)[CW], double (&nx)[CW]) {
     if (m.b == 0) {  // row header (loaded one chunk ago)
         row.d = hn.d;
         row.diag = hn.nd.x;
         row.sp = hn.nd.x;
         row.sn = hn.nd.y;
-        if (PH == 3) {
+        if (PH == 3 || PH == 4) {
             row.a3 = hn.a3;
             row.y = hn.nd.x * hn.xo;
             row.rhs_i = hn.rhs;
@@ -714,23 +766,24 @@ __device__ __forceinline__ bool grp_step(const SweepArgs &a, const Ring<R> &r, d
     const GMeta mn = G.meta[s1];
     if (mn.g >= 0) {
         if (mn.b == 0) t_header<PH, R>(a, r, ((int64_t)mn.g * kGroup + warp) * 32 + lane, hn);
-        t_gather(G.st[s1], mn, r.g2, t, nP, nN, nx);
+        t_gather<PH>(G.st[s1], mn, r.g2, t, nP, nN, nx);
     }
     const int s0 = (int)(k % kGS);
     const GStage &S = G.st[s0];
     const uint32_t d = row.d;
-    double cc[kGC], m2p[kGC], m2m[kGC], ip[kGC], im[kGC], pe[kGC], rc[kGC];
-    double2 i2v[kGC];
+    double cc[CW], m2p[CW], m2m[CW], ip[CW], im[CW], pe[CW], rc[CW];
+    double2 i2v[CW];
 #pragma unroll
-    for (int u = 0; u < kGC; ++u) {
-        const bool v = m.b * kGC + u < d;
-        cc[u] = v ? S.c[u][t] : 1.0;
+    for (int u = 0; u < CW; ++u) {
+        const bool v = m.b * CW + u < d;
+        cc[u] = v ? st_c<PH>(S, u)[t] : 1.0;
         rc[u] = ddiv_rcp(cc[u]);
         m2p[u] = 0.0;  // m^{(0)} = 0 at launch 2
         m2m[u] = 0.0;
         i2v[u] = make_double2(0.0, 0.0);
-        if (PH == 3) {  // own outgoing message of sweep s-2
-            const double2 i3 = S.i3[u][t];
+        if (PH == 3 || PH == 4) {  // own outgoing message of sweep s-2
+            // (launch 3: I^{(0)} = +0, not streamed; x - (+0) == x bit for bit)
+            const double2 i3 = PH == 3 ? S.i3[u][t] : make_double2(0.0, 0.0);
             i2v[u] = S.i2[u][t];
             const double pe2 = v ? row.a3.x - i3.x : 1.0;
             const double nu2 = v ? row.a3.y - i3.x * i3.y : 1.0;
@@ -740,26 +793,26 @@ __device__ __forceinline__ bool grp_step(const SweepArgs &a, const Ring<R> &r, d
     __syncwarp();
     if (lane == 0) t_arrive(&G.empty[s0]);  // the stage's data is in registers now
 #pragma unroll
-    for (int u = 0; u < kGC; ++u) {  // incoming of S_{s-1}
-        const bool v = m.b * kGC + u < d;
+    for (int u = 0; u < CW; ++u) {  // incoming of S_{s-1}
+        const bool v = m.b * CW + u < d;
         pe[u] = v ? gP[u] - m2p[u] : 1.0;
         const double num = v ? gN[u] - m2p[u] * m2m[u] : 1.0;
         edge_msg<false>(cc[u], rc[u], pe[u], num, ip[u], im[u], st);
     }
     const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
 #pragma unroll
-    for (int u = 0; u < kGC; ++u) {
-        const uint32_t q = m.b * kGC + u;
+    for (int u = 0; u < CW; ++u) {
+        const uint32_t q = m.b * CW + u;
         if (q < d) {
             row.sp = row.sp + ip[u];
             row.sn = row.sn + ip[u] * im[u];  // (prec * mean), solver.py:243
-            if (PH == 3) row.y = row.y + cc[u] * gx[u];
+            if (PH == 3 || PH == 4) row.y = row.y + cc[u] * gx[u];
             __stcs(r.I1 + m.gbase + (uint32_t)kStride * q + t, make_double2(ip[u], im[u]));
             msg_stats<false>(st, a, ip[u], im[u], i2v[u], pe[u], p, q);
         }
     }
     if (m.b + 1 == m.nb && row.diag != 0.0)  // row done (A_ii == 0: padding lane)
-        node_done<PH, false>(st, a, r.g1, xh, p, row.sp, row.sn, row.y, row.rhs_i);
+        node_done<(PH == 4 ? 3 : PH), false>(st, a, r.g1, xh, p, row.sp, row.sn, row.y, row.rhs_i);
     if (mn.g < 0) return false;
     m = mn;
     return true;
@@ -775,10 +828,11 @@ __device__ __forceinline__ void grp_consume(const SweepArgs &a, int64_t s, Stats
     t_wait(&G.full[0], 0u);
     GMeta m = G.meta[0];
     if (m.g < 0) return;
-    double gA[3][kGC], gB[3][kGC];  // gathers {P, N, x}: chunk k in one, k+1 in the other
+    constexpr int CW = stage_cw<PH>();
+    double gA[3][CW], gB[3][CW];  // gathers {P, N, x}: chunk k in one, k+1 in the other
     THdr hn;
     t_header<PH, R>(a, r, ((int64_t)m.g * kGroup + warp) * 32 + lane, hn);
-    t_gather(G.st[0], m, r.g2, t, gA[0], gA[1], gA[2]);
+    t_gather<PH>(G.st[0], m, r.g2, t, gA[0], gA[1], gA[2]);
     GRow row;
     for (uint32_t k = 0;; k += 2) {
         if (!grp_step<PH, R>(a, r, xh, st, G, lane, warp, t, k, m, hn, row, gA[0], gA[1], gA[2],
@@ -791,71 +845,73 @@ __device__ __forceinline__ void grp_consume(const SweepArgs &a, int64_t s, Stats
 }
 
 // Residual-only group launch (the probe on the TMA ring): the producer streams scoef and
-// scol (12 B per slot, as for launch 2); consumers gather x^{(s-2)} and form the residual
-// rows of x^{(s-2)} exactly as a full launch s would (grp_step, PH 3).
+// scol (12 B per slot, kNCR columns per stage); consumers gather x^{(s-2)} and form the
+// residual rows of x^{(s-2)} exactly as a full launch s would (grp_step, PH 3).  The pass is
+// bound by the gathers' L2 latency, so a consumer copies a landed stage's coefficients into
+// registers, issues its gathers and releases the stage at once, keeping kRD chunks of
+// gathers in flight.
+constexpr int kRD = 3;  // chunks of gathers in flight per consumer
 template <int R>
 __device__ __forceinline__ void grp_consume_res(const SweepArgs &a, Stats &st, int lane,
                                                 int warp, GRing &G) {
+    constexpr int CW = kNCR;
     const Ring<R> r(a);
     const int t = warp * 32 + lane;
-    t_wait(&G.full[0], 0u);
-    GMeta m = G.meta[0];
-    if (m.g < 0) return;
-    double2 hnd;
-    double hxo = 0.0, hrhs = 0.0;
-    uint32_t hd;
-    {
-        const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
-        hnd = __ldg(a.snd + p);
-        hd = __ldg(a.sdeg + p);
-        hxo = __ldcg(&r.g2[p].x);
-        hrhs = __ldg(a.srhs + p);
-    }
-    double gx[kGC], nx[kGC];
+    double cv[kRD][CW], xv[kRD][CW];
+    GMeta mq[kRD];
+    // chunk k: wait for its stage, take coefficients and gathers, release the stage
+    auto issue = [&](uint32_t k, int slot) -> bool {
+        const int sg = (int)(k % kGS);
+        t_wait(&G.full[sg], (k / kGS) & 1u);
+        const GMeta m = G.meta[sg];
+        mq[slot] = m;
+        if (m.g < 0) return false;
+        const GStage &S = G.st[sg];
 #pragma unroll
-    for (int u = 0; u < kGC; ++u)
-        gx[u] = m.b * kGC + u < m.w ? __ldcg(&r.g2[G.st[0].col[u][t]].x) : 0.0;
+        for (int u = 0; u < CW; ++u) {
+            const bool v = m.b * CW + u < m.w;
+            const uint32_t j = st_col<5>(S, u)[t];
+            cv[slot][u] = st_c<5>(S, u)[t];
+            xv[slot][u] = v ? __ldcg(&r.g2[j].x) : 0.0;
+        }
+        __syncwarp();
+        if (lane == 0) t_arrive(&G.empty[sg]);
+        return true;
+    };
+    // chunks are issued strictly in order and never past the end marker (the producer
+    // fills no stage after it): `more` is the liveness of the last chunk issued
+    bool live[kRD], more = true;
+#pragma unroll
+    for (int q = 0; q < kRD; ++q) {
+        if (more) more = issue(q, q);
+        live[q] = more;
+    }
+    if (!live[0]) return;
     uint32_t d = 0;
     double y = 0.0, rhs_i = 0.0, diag = 0.0;
-    for (uint32_t k = 0;; ++k) {
-        if (m.b == 0) {
-            d = hd;
-            diag = hnd.x;
-            y = hnd.x * hxo;
-            rhs_i = hrhs;
-        }
-        const int s1 = (int)((k + 1) % kGS);
-        t_wait(&G.full[s1], ((k + 1) / kGS) & 1u);
-        const GMeta mn = G.meta[s1];
-        if (mn.g >= 0) {
-            if (mn.b == 0) {
-                const int64_t pn = ((int64_t)mn.g * kGroup + warp) * 32 + lane;
-                hnd = __ldg(a.snd + pn);
-                hd = __ldg(a.sdeg + pn);
-                hxo = __ldcg(&r.g2[pn].x);
-                hrhs = __ldg(a.srhs + pn);
+    for (uint32_t k = 0;; k += kRD) {
+#pragma unroll
+        for (int q = 0; q < kRD; ++q) {
+            if (!live[q]) return;
+            const GMeta m = mq[q];
+            if (m.b == 0) {  // row header
+                const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
+                const double2 nd = __ldg(a.snd + p);
+                d = __ldg(a.sdeg + p);
+                diag = nd.x;
+                y = nd.x * __ldcg(&r.g2[p].x);
+                rhs_i = __ldg(a.srhs + p);
             }
 #pragma unroll
-            for (int u = 0; u < kGC; ++u)
-                nx[u] = mn.b * kGC + u < mn.w ? __ldcg(&r.g2[G.st[s1].col[u][t]].x) : 0.0;
+            for (int u = 0; u < CW; ++u)
+                if (m.b * CW + u < d) y = y + cv[q][u] * xv[q][u];
+            if (m.b + 1 == m.nb && diag != 0.0) {
+                const double rr = y - rhs_i;
+                st.rsq += rr * rr;
+            }
+            if (more) more = issue(k + kRD + q, q);
+            live[q] = more;
         }
-        const int s0 = (int)(k % kGS);
-        double cc[kGC];
-#pragma unroll
-        for (int u = 0; u < kGC; ++u) cc[u] = G.st[s0].c[u][t];
-        __syncwarp();
-        if (lane == 0) t_arrive(&G.empty[s0]);
-#pragma unroll
-        for (int u = 0; u < kGC; ++u)
-            if (m.b * kGC + u < d) y = y + cc[u] * gx[u];
-        if (m.b + 1 == m.nb && diag != 0.0) {
-            const double rr = y - rhs_i;
-            st.rsq += rr * rr;
-        }
-        if (mn.g < 0) break;
-        m = mn;
-#pragma unroll
-        for (int u = 0; u < kGC; ++u) gx[u] = nx[u];
     }
 }
 
@@ -863,7 +919,7 @@ template <int R>
 __device__ __forceinline__ void slice_res_grp(const SweepArgs &a, Stats &st, int lane, int warp,
                                               GRing &G, uint32_t *ctr) {
     if (warp == kGroup)
-        grp_produce<2, R>(a, G, ctr, lane);
+        grp_produce<5, R>(a, G, ctr, lane);
     else
         grp_consume_res<R>(a, st, lane, warp, G);
 }
@@ -1073,7 +1129,7 @@ __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_grp(const SweepArgs
         probe_finish<kGThreads>(S.tail, a, s - 2, st.rsq, (int)(s % kStatSlots));
         return;
     }
-    if (s >= 3) {
+    if (s >= 4) {
         const int r = (int)(s % 3);
         if (r == 0)
             slice_sweep_grp<3, 0>(a, s, st, lane, warp, G, ctr);
@@ -1081,6 +1137,8 @@ __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_grp(const SweepArgs
             slice_sweep_grp<3, 1>(a, s, st, lane, warp, G, ctr);
         else
             slice_sweep_grp<3, 2>(a, s, st, lane, warp, G, ctr);
+    } else if (s == 3) {
+        slice_sweep_grp<4, 0>(a, s, st, lane, warp, G, ctr);
     } else if (s == 2) {
         slice_sweep_grp<2, 2>(a, s, st, lane, warp, G, ctr);
     } else {
