@@ -1166,9 +1166,17 @@ __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_grp(const SweepArgs
 #define GABP_PAR_BLOCK 8
 #endif
 constexpr int kPB = GABP_PAR_BLOCK;  // outgoing edges per exclusion pass
+static_assert(kPB % kGC == 0, "a block starts on a chunk boundary");
 
 __device__ __forceinline__ uint32_t par_passes(uint32_t w) {
     return w > kPB ? (w + kPB - 1) / kPB : 1u;
+}
+// Pass p >= 1 starts at column p kPB: the exclusion sums of edges p kPB .. p kPB + kPB - 1
+// share the sequential prefix A_ii + sum_{q < p kPB} P_qi (no edge of the block is excluded
+// from it), carried over from pass p-1 -- the same operations in the same order as summing
+// from column 0, and half the column visits of a full re-walk per block.
+__device__ __forceinline__ uint32_t par_first_chunk(uint32_t pass) {
+    return pass * (uint32_t)(kPB / kGC);
 }
 
 // Producer of the parallel kernel: per group, npass passes of ceil(w / kGC) chunks.
@@ -1230,8 +1238,9 @@ __device__ __forceinline__ void par_produce(const SweepArgs &a, GRing &G, uint32
             }
         }
         if (++b >= nb) {
-            b = 0;
+            b = par_first_chunk(pass + 1);
             if (++pass >= np) {
+                b = 0;
                 pass = 0;
                 gcur = gnxt;
                 icur = inxt;
@@ -1249,6 +1258,7 @@ struct ParRow {
     uint32_t d = 0;
     double pP = 0.0, pN = 0.0;             // prior precision and numerator
     double sp = 0.0, sn = 0.0, y = 0.0, rhs_i = 0.0;
+    double preP = 0.0, preN = 0.0;         // prefix sums up to the current block's first edge
     double aP[kPB], aN[kPB];               // exclusion sums of the current block
     double cb[kPB];                        // A_ij of the block's edges
     uint32_t tw[kPB];                      // their twin slots
@@ -1283,22 +1293,24 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
         const uint32_t pass = m.pad[0];
         const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
         const uint32_t slot0 = m.gbase + (uint32_t)t;
-        if (m.b == 0) {
+        if (m.b == par_first_chunk(pass)) {
             if (pass == 0) {  // row header (loaded one chunk ago)
                 row.d = hn.d;
                 row.pP = hn.nd.x;
                 row.pN = hn.nd.y;
                 row.sp = hn.nd.x;
                 row.sn = hn.nd.y;
+                row.preP = hn.nd.x;
+                row.preN = hn.nd.y;
                 if (RESID) {
                     row.y = hn.nd.x * hn.xo;
                     row.rhs_i = hn.rhs;
                 }
             }
 #pragma unroll
-            for (int jj = 0; jj < kPB; ++jj) {  // block `pass`: sums start at the prior
-                row.aP[jj] = row.pP;
-                row.aN[jj] = row.pN;
+            for (int jj = 0; jj < kPB; ++jj) {  // block `pass`: sums start at its prefix
+                row.aP[jj] = row.preP;
+                row.aN[jj] = row.preN;
             }
         }
         if (m.b + 1 == m.nb) {  // last chunk of the pass: the block's coefficients and twins
@@ -1318,7 +1330,7 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
         t_wait(&G.full[s1], ((k + 1) / kGS) & 1u);
         const GMeta mn = G.meta[s1];
         if (mn.g >= 0) {
-            if (mn.b == 0 && mn.pad[0] == 0) {
+            if (mn.b == 0 && mn.pad[0] == 0) {  // (pass 0 of a group starts at chunk 0)
                 const int64_t pn = ((int64_t)mn.g * kGroup + warp) * 32 + lane;
                 hn.nd = __ldg(a.snd + pn);
                 hn.d = __ldg(a.sdeg + pn);
@@ -1336,6 +1348,8 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
         const int s0 = (int)(k % kGS);
         const GStage &S = G.st[s0];
         const uint32_t d = row.d;
+        const uint32_t blk = pass * kPB;  // first edge of the block (warp-uniform)
+        const bool inblk = m.b * kGC < blk + kPB;  // chunk meets the block's own columns
 #pragma unroll
         for (int u = 0; u < kGC; ++u) {
             const uint32_t q = m.b * kGC + u;
@@ -1354,9 +1368,21 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
                             st.out_of_range = 1u;
                     }
                 }
+                if (inblk) {
+                    if (q < blk + kPB) {  // the next block's prefix
+                        row.preP = row.preP + vP;
+                        row.preN = row.preN + vN;
+                    }
 #pragma unroll
-                for (int jj = 0; jj < kPB; ++jj) {
-                    if (q != pass * kPB + jj) {
+                    for (int jj = 0; jj < kPB; ++jj) {
+                        if (q != blk + jj) {
+                            row.aP[jj] = row.aP[jj] + vP;
+                            row.aN[jj] = row.aN[jj] + vN;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < kPB; ++jj) {
                         row.aP[jj] = row.aP[jj] + vP;
                         row.aN[jj] = row.aN[jj] + vN;
                     }
@@ -1735,6 +1761,7 @@ cudaError_t slice_map_index(const DeviceGraph &g, uint32_t *idx, int64_t cnt, cu
 
 int build_stwin(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
     if (g.stwin || g.nslices == 0) return GABP_OK;
+
     if (g.row_lo != 0 || g.row_hi != g.n) {
         snprintf(err, errlen, "the parallel slice kernel runs on whole graphs only");
         return GABP_EINVAL;
