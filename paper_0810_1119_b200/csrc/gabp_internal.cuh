@@ -160,7 +160,10 @@ struct SweepArgs {
     const uint32_t *scol;      // position of the destination, per slot
     const double *scoef;       // A_ij per slot
     const uint32_t *stwin;     // slot of the twin message (parallel schedule), per slot
-    int probe;                 // the exact twin of this launch can run the residual probe
+    int probe;                 // residual probe: 0 off, 1 run by the exact twin, 2 as a
+                               // residual-only group launch (probe_next)
+    int probe_force;           // test hook (GABP_PROBE_FORCE=1): request a probe after every
+                               // launch, so every mispredicted probe path runs
 };
 
 // kernels (sweep.cu); prepare_sweep_kernels() must run once per device before launches
@@ -262,6 +265,7 @@ __device__ __forceinline__ int64_t probe_next(volatile Ctrl *c, SweepArgs const 
     const CtrlSnap k = ctrl_snap(c, slot);
     const double r2 = T >= 3 ? a.rsq_hist[T - 3] : 0.0;  // x^{(T-2)}
     if (k.done || T > k.max_iter) return 0;
+    if (a.probe_force) return T;
     if (k.singular_min != kNoIndex || k.agg_singular != kNoIndex || k.msg_nonfinite ||
         k.means_nonfinite || T >= k.max_iter)
         return T;

@@ -1825,6 +1825,11 @@ static bool probe_enabled() {
     static const int off = getenv("GABP_NO_PROBE") ? atoi(getenv("GABP_NO_PROBE")) : 0;
     return !off;
 }
+// GABP_PROBE_FORCE=1: a probe after every launch (tests the mispredicted-probe path)
+static int probe_forced() {
+    static const int on = getenv("GABP_PROBE_FORCE") ? atoi(getenv("GABP_PROBE_FORCE")) : 0;
+    return on ? 1 : 0;
+}
 
 // the exact register-batch kernel over [a.sl_lo, a.sl_hi): the twin (runs only when the
 // fast launch flagged itself) or, with a.exact_primary, the sweep itself; returns its grid
@@ -1859,6 +1864,7 @@ cudaError_t launch_slice_part(const SweepArgs &a0, int reserve_sms, cudaStream_t
     SweepArgs a = a0;
     // residual probe: a residual-only group launch (variant 2), else run by the exact twin
     a.probe = (!a0.dist && probe_enabled()) ? (a0.slice_variant == 2 ? 2 : 1) : 0;
+    a.probe_force = probe_forced();
     if (a.slice_variant == 2) {
         int64_t grid = (g_grid_grp > 0 ? g_grid_grp : 148) - reserve_sms;
         const int64_t need = (a.sl_hi - a.sl_lo) / kGroup;
@@ -1882,6 +1888,7 @@ cudaError_t launch_slice_part(const SweepArgs &a0, int reserve_sms, cudaStream_t
 cudaError_t launch_slice_parallel(const SweepArgs &a0, cudaStream_t st) {
     SweepArgs a = a0;
     a.probe = (!a0.dist && probe_enabled()) ? 1 : 0;
+    a.probe_force = probe_forced();
     int64_t grid = g_grid_par > 0 ? g_grid_par : 148;
     const int64_t need = (a.sl_hi - a.sl_lo) / kGroup;
     if (grid > need) grid = need > 0 ? need : 1;
