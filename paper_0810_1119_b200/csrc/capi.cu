@@ -125,6 +125,7 @@ struct gabp_graph {
     double *dA = nullptr;
     double2 *dmsg[3] = {nullptr, nullptr, nullptr};
     double2 *dnode = nullptr;
+    uint32_t *demask = nullptr;      // edge bitmask: initial (-0, +0) non-edge messages
     int64_t Kp = 0;                  // padded dimension (multiple of 32)
     uint2 *dpairs = nullptr;         // tile pairs of the pair-tile kernel
     int64_t dnpairs = 0;
@@ -390,6 +391,7 @@ void release_workspace(gabp_graph *G) {
     cudaFree(G->dA);
     for (int b = 0; b < 3; ++b) cudaFree(G->dmsg[b]);
     cudaFree(G->dnode);
+    cudaFree(G->demask);
     cudaFree(G->dpairs);
     if (G->dist) {
         cudaFree(G->dist->d_sidx);
@@ -735,7 +737,9 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
             CK(cudaMalloc(&G->dnode, sizeof(double2) * Kp));
             CK(cudaMemset(G->dnode, 0, sizeof(double2) * Kp));  // padding rows stay zero
         }
-        CK(cudaMemsetAsync(G->dmsg[0], 0, sizeof(double2) * Kp * Kp, st));
+        // S_0: +0 messages on the edges, (-0, +0) on the non-edges (dense.cu: adding them is
+        // the exact identity, so the column walk needs no edge test)
+        CK(gabp::launch_dense_init(G->demask, Kp, G->dmsg[0], st));
         G->kernels_launched = 0;
         gabp::DenseArgs d{};
         d.K = K;
@@ -744,6 +748,8 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         for (int b = 0; b < 3; ++b) d.msg[b] = G->dmsg[b];
         d.node = G->dnode;
         d.pairs = G->dpairs;
+        d.emask = G->demask;
+
         d.npairs = G->dnpairs;
         SweepArgs a = make_args(G);
         const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : 8;
@@ -1005,6 +1011,9 @@ int gabp_graph_create_dense(int64_t n, const double *h_a, const double *h_rhs, i
     for (int64_t I = 0; I < nt; ++I)
         for (int64_t J = I; J < nt; ++J) tp.push_back(make_uint2((unsigned)I, (unsigned)J));
     G->dnpairs = (int64_t)tp.size();
+    CK(cudaMalloc(&G->demask, sizeof(uint32_t) * Kp * (Kp / 32)));
+    CK(gabp::launch_dense_mask(G->dA, Kp, G->demask, 0));
+    CK(cudaDeviceSynchronize());
     CK(cudaMalloc(&G->dpairs, sizeof(uint2) * tp.size()));
     CK(cudaMemcpy(G->dpairs, tp.data(), sizeof(uint2) * tp.size(), cudaMemcpyHostToDevice));
     return GABP_OK;

@@ -3,16 +3,20 @@
 // Storage: A is Kp x Kp row-major (Kp = K rounded up to 32, padding zero); messages are a
 // Kp x Kp matrix M[k][j] = m_{k->j} (sender-major: the out-slot layout of the sparse path).
 // The diagonal, the padding and the exact zeros of A -- non-edges in the reference
-// (linalg.py:81-82) -- hold zero messages and are skipped by the sums.
+// (linalg.py:81-82) -- hold the message (P, mu) = (-0, +0): P and P mu are then -0, and
+// x + (-0) == x for every x in round-to-nearest (-0 included), so the column walk adds
+// every entry without an edge test and gets the reference's sums over edges bit for bit.
+// (Edges start at (+0, +0), the reference's initial messages; launch_dense_init.)
 // One launch s = two kernels:
 //
 //   column walk  one CTA per 32 columns: lane l of the summing warp walks column i0 + l in
 //                ascending row order -- the incoming messages of node i in ascending sender
-//                order, exactly the order of the reference's np.add.at (solver.py:242-243)
+//                order, exactly the order of the reference's np.add.at (solver.py:242-243).
 //                -- and A's column for the residual row of x^{(s-2)}.  One producer lane
 //                streams the 32 x 32 blocks of A and M^{(s-1)} as 2-D tensor copies
 //                (cp.async.bulk.tensor, tensor maps over the padded matrices) and the
-//                x^{(s-2)} block as a 1-D bulk copy into a kColStages-deep mbarrier ring.
+//                x^{(s-2)} block as a 1-D bulk copy into a kColStages-deep mbarrier ring;
+//                the sums are plain dependent adds (non-edges add -0, no edge test).
 //                Writes P_i, P_i mu~_i, x^{(s-1)}, residual partials.
 //   pair tiles   a CTA takes the tile pair (I, J), I <= J: M^{(s-1)}[I][J], M^{(s-1)}[J][I]
 //                and A[I][J] (A is symmetric) are staged once, and both directions are
@@ -22,6 +26,9 @@
 //                change statistic) and as its twin's input; the transposed result goes out
 //                through shared memory.  Max change / blowup / singular statistics; the last
 //                CTA runs the solve decision for sweep s-2 (the sparse kernel's protocol).
+//                (Moving the residual rows here -- the A tile is staged anyway -- cost the
+//                issue-bound pair kernel 44 us per sweep at K = 4096 against 20 us of extra
+//                A stream in the walk, so they stay in the walk.)
 // Per edge and sweep: 24 B in the walk, 16 + 4 + 16 B in the pair tiles (was 80 B with
 // one-direction tiles and a column walk without bulk copies).
 #include <cuda.h>  // CUtensorMap (the encoder is fetched at run time: no libcuda link)
@@ -51,13 +58,13 @@ __device__ __forceinline__ uint32_t s_u32(const void *p) {
 }
 
 // ---- column walk -----------------------------------------------------------------------------
-constexpr int kColRows = 32;     // rows of A / M per ring stage
-constexpr int kColStages = 6;
+constexpr int kColRows = 32;     // rows of M per ring stage
+constexpr int kColStages = 8;
 constexpr int kColCta = 64;      // warp 0 sums, warp 1 produces
 
-struct ColStage {
-    double A[kColRows][32];
+struct __align__(128) ColStage {
     double2 M[kColRows][32];
+    double A[kColRows][32];
     double X[kColRows];
 };
 struct ColSmem {
@@ -133,7 +140,8 @@ __global__ void __launch_bounds__(kColCta, 1) dense_column_kernel(
     const CUtensorMap *mmap = &maps.M[(s - 1) % 3];
     const double *xprev = resid ? a.x[(s - 2) % 3] : nullptr;
     const int64_t i0 = (int64_t)blockIdx.x * 32;
-    const int64_t nstage = (K + kColRows - 1) / kColRows;
+    const int64_t nstage = d.ld / kColRows;  // padding rows hold (-0, +0) messages, A = 0
+    (void)i0;
 
     if (tid >= 32) {  // ---- producer lane: one 2-D copy each of A and M, the x block ----
         if (lane == 0) {
@@ -144,12 +152,15 @@ __global__ void __launch_bounds__(kColCta, 1) dense_column_kernel(
                 const int64_t k0 = t * kColRows;
                 const int rows = (int)((K - k0) < kColRows ? (K - k0) : kColRows);
                 // x block: whole 16-byte units (x arrays carry kNodePad >= 2 doubles of padding)
-                const unsigned xb = resid ? (unsigned)(((rows + 1) & ~1) * 8) : 0u;
-                mb_expect_tx(&S.full[st], (unsigned)(sizeof(double) * 32 * 32 +
-                                                     sizeof(double2) * 32 * 32) + xb);
-                tensor2d(&S.st[st].A[0][0], &maps.A, (int)i0, (int)k0, &S.full[st]);
+                const unsigned xb = resid && rows > 0 ? (unsigned)(((rows + 1) & ~1) * 8) : 0u;
+                mb_expect_tx(&S.full[st],
+                             (unsigned)(sizeof(double2) * 32 * kColRows) +
+                                 (resid ? (unsigned)(sizeof(double) * 32 * kColRows) + xb : 0u));
                 tensor2d(&S.st[st].M[0][0], mmap, (int)(2 * i0), (int)k0, &S.full[st]);
-                if (xb) bulk(&S.st[st].X[0], xprev + k0, xb, &S.full[st]);
+                if (resid) {  // (no residual before launch 3)
+                    tensor2d(&S.st[st].A[0][0], &maps.A, (int)i0, (int)k0, &S.full[st]);
+                    if (xb) bulk(&S.st[st].X[0], xprev + k0, xb, &S.full[st]);
+                }
             }
         }
         return;
@@ -162,27 +173,29 @@ __global__ void __launch_bounds__(kColCta, 1) dense_column_kernel(
         const NodeRec nd = a.nd[i];
         sp = nd.diag;
         sn = nd.pnum;
-        y = resid ? nd.diag * xprev[i] : 0.0;
     }
     for (int64_t t = 0; t < nstage; ++t) {
         const int st = (int)(t % kColStages);
         mb_wait(&S.full[st], (unsigned)(t / kColStages) & 1u);
         const ColStage &C = S.st[st];
         const int64_t k0 = t * kColRows;
-        if (col) {
-            // all kColRows rows: the padding rows of the last block have A = 0 (no edge)
+        if (resid) {
+            const int rows = (int)((K - k0) < kColRows ? (K - k0) : kColRows);
 #pragma unroll 16
             for (int r = 0; r < kColRows; ++r) {  // ascending k: the reference's order
-                const double akj = C.A[r][lane];
-                const bool edge = k0 + r != i && akj != 0.0;  // non-edges add nothing
+                const double2 m = C.M[r][lane];  // (non-edges: -0, -0 * +0 = -0: identities)
+                sp = sp + m.x;
+                sn = sn + m.x * m.y;
+                // residual row: sum_k A_ki x_k (A symmetric), the diagonal included; rows
+                // past K have A = 0 and an unfilled x slot
+                y = y + C.A[r][lane] * (r < rows ? C.X[r] : 0.0);
+            }
+        } else {
+#pragma unroll 16
+            for (int r = 0; r < kColRows; ++r) {
                 const double2 m = C.M[r][lane];
-                const double sp1 = sp + m.x, sn1 = sn + m.x * m.y;
-                sp = edge ? sp1 : sp;
-                sn = edge ? sn1 : sn;
-                if (resid) {
-                    const double y1 = y + akj * C.X[r];
-                    y = edge ? y1 : y;
-                }
+                sp = sp + m.x;
+                sn = sn + m.x * m.y;
             }
         }
         __syncwarp();
@@ -218,20 +231,54 @@ __global__ void __launch_bounds__(kColCta, 1) dense_column_kernel(
     }
 }
 
+// S_0 of the dense ring: (+0, +0) on edges, (-0, +0) elsewhere.
+__global__ void dense_init_kernel(const uint32_t *emask, int64_t ld, double2 *msg) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // q = k * ld + j
+    if (q >= ld * ld) return;
+    const int64_t k = q / ld, j = q % ld;
+    const bool edge = (emask[(j >> 5) * ld + k] >> (j & 31)) & 1u;
+    msg[q] = make_double2(edge ? 0.0 : -0.0, 0.0);
+}
+
+// Edge bitmask of a padded dense A: word (cb, k) bit l = A[k][32 cb + l] != 0 and k != 32 cb + l.
+__global__ void dense_mask_kernel(const double *A, int64_t ld, uint32_t *emask) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // q = cb * ld + k
+    const int64_t nb = ld / 32;
+    if (q >= nb * ld) return;
+    const int64_t cb = q / ld, k = q % ld;
+    uint32_t w = 0u;
+    for (int l = 0; l < 32; ++l) {
+        const int64_t j = cb * 32 + l;
+        if (A[k * ld + j] != 0.0 && j != k) w |= 1u << l;
+    }
+    emask[q] = w;
+}
+
 // ---- pair tiles -------------------------------------------------------------------------
-constexpr int kPairCta = 256;  // 32 x 8 threads
+#ifndef GABP_PAIR_CTA
+#define GABP_PAIR_CTA 256
+#endif
+#ifndef GABP_PAIR_BUFS
+#define GABP_PAIR_BUFS 2
+#endif
+constexpr int kPairCta = GABP_PAIR_CTA;    // 32 x kPairWarps threads
+constexpr int kPairWarps = kPairCta / 32;
+constexpr int kPairBufs = GABP_PAIR_BUFS;  // staged pairs: kPairBufs - 1 in flight ahead
+static_assert(kPairCta % 256 == 0 && kPairCta <= 1024, "tile rows split evenly over warps");
 
 struct __align__(16) PairBuf {
     double2 mij[kTile][kTile + 1];  // M^{(s-1)}[I][J]
     double2 mji[kTile][kTile + 1];  // M^{(s-1)}[J][I]
     double aij[kTile][kTile];       // A[I][J]
     double2 ni[kTile], nj[kTile];   // {P, N} of the rows of I and J
+    uint2 ij;                       // the staged pair (I, J)
 };
 struct PairSmem {
-    PairBuf b[2];
+    PairBuf b[kPairBufs];
     double2 out[kTile][kTile + 1];  // new M[J][I], staged for the coalesced store
-    double red_d[8];
-    unsigned red_u[8];
+    double red_d[kPairWarps];
+    unsigned red_u[kPairWarps];
+    uint2 next_ij[kPairBufs];       // tile pairs of the coming stagings (thread 0 writes)
     int64_t sweep;
     int skip;
     int last;
@@ -250,19 +297,29 @@ __device__ __forceinline__ void cpa_wait() {
 __device__ __forceinline__ void pair_stage(PairBuf &B, int64_t I, int64_t J, const DenseArgs &d,
                                            const double2 *M, int tid) {
     const int64_t ld = d.ld, i0 = I * kTile, j0 = J * kTile;
-    for (int q = tid; q < kTile * kTile; q += kPairCta) {  // one double2 per copy
-        const int r = q >> 5, c = q & 31;
-        cpa16(&B.mij[r][c], M + (i0 + r) * ld + j0 + c);
-        cpa16(&B.mji[r][c], M + (j0 + r) * ld + i0 + c);
+    {  // one double2 per copy: rows tid/32 + kPairWarps m, column tid % 32
+        const int r0 = tid >> 5, c = tid & 31;
+        const double2 *gij = M + (i0 + r0) * ld + j0 + c, *gji = M + (j0 + r0) * ld + i0 + c;
+        const int64_t step = (int64_t)kPairWarps * ld;
+#pragma unroll
+        for (int m = 0; m < kTile / kPairWarps; ++m) {
+            cpa16(&B.mij[r0 + m * kPairWarps][c], gij + m * step);
+            cpa16(&B.mji[r0 + m * kPairWarps][c], gji + m * step);
+        }
     }
-    for (int q = tid; q < kTile * kTile / 2; q += kPairCta) {  // two doubles per copy
-        const int r = q >> 4, c = (q & 15) * 2;
-        cpa16(&B.aij[r][c], d.A + (i0 + r) * ld + j0 + c);
+    {  // two doubles per copy
+        constexpr int RPP = kPairCta / 16;  // rows per pass
+        const int r0 = tid >> 4, c = (tid & 15) * 2;
+        const double *ga = d.A + (i0 + r0) * ld + j0 + c;
+#pragma unroll
+        for (int m = 0; m < kTile / RPP; ++m)
+            cpa16(&B.aij[r0 + m * RPP][c], ga + (int64_t)m * RPP * ld);
     }
     if (tid < kTile) {
         cpa16(&B.ni[tid], d.node + i0 + tid);
         cpa16(&B.nj[tid], d.node + j0 + tid);
     }
+    if (tid == 0) B.ij = make_uint2((unsigned)I, (unsigned)J);
 }
 
 struct PairStats {
@@ -271,13 +328,77 @@ struct PairStats {
     unsigned long long sing = ~0ull;
 };
 
+// Tile pair p of the upper triangle (I <= J) in row-major order: row I holds nt - I pairs,
+// so pairs before row I number I nt - I (I - 1) / 2.  Computed, not loaded: a pair-list load
+// sat on the critical path of every staging (10 % of the stall samples).
+__device__ __forceinline__ uint2 pair_of(int64_t p, int64_t nt) {
+    const double b = 2.0 * (double)nt + 1.0;
+    int64_t I = (int64_t)((b - sqrt(b * b - 8.0 * (double)p)) * 0.5);
+    if (I < 0) I = 0;
+    auto before = [nt](int64_t i) { return i * nt - i * (i - 1) / 2; };
+    while (I > 0 && before(I) > p) --I;
+    while (before(I + 1) <= p) ++I;
+    return make_uint2((unsigned)I, (unsigned)(I + (p - before(I))));
+}
+
 // statistics of one new message against its previous value
-__device__ __forceinline__ void pair_stat(double2 nw, double2 old, double pe, uint64_t e,
-                                          double lim, PairStats &ps) {
-    if (pe == 0.0 && e < ps.sing) ps.sing = e;
+template <bool EXACT>
+__device__ __forceinline__ void pair_stat(double2 nw, double2 old, double pe, int64_t i,
+                                          int64_t j, int64_t K, double lim, PairStats &ps) {
+    if (EXACT && pe == 0.0) {  // (exact pass only: the edge id is formed only here)
+        const uint64_t e = (uint64_t)(i * K + j);
+        if (e < ps.sing) ps.sing = e;
+    }
     const double d1 = fabs(nw.x - old.x), d2 = fabs(nw.y - old.y);
     ps.chg = fmax(ps.chg, fmax(d1, d2));
     if (!(fabs(nw.x) <= lim) || !(fabs(nw.y) <= lim)) ps.oor = 1u;
+}
+
+// The tile pair's 32 x 32 elements of one thread column (rows ty + kPairWarps m): both
+// directions' new messages, stored (m_ij to global, m_ji to the transpose buffer), with
+// their statistics in ps.  EXACT = false: the divisions' range tests are deferred into dr
+// (no branch per element); a pair whose test fails anywhere is redone with EXACT = true,
+// which also reports a zero exclusion precision (the fast path turns it into a NaN
+// quotient, which fails the range test).
+template <bool EXACT>
+__device__ __forceinline__ void pair_elems(const PairBuf &B, PairSmem &S, double2 *Mo,
+                                           int64_t ld, int64_t K, int64_t i0, int64_t j0,
+                                           bool diag, int tx, int ty, double lim,
+                                           PairStats &ps, DivRange &dr) {
+    const int rmax = (int)(K - i0 < kTile ? K - i0 : kTile);  // rows / columns < K
+    const bool jin = j0 + tx < K;
+    const double2 ndj = B.nj[tx];
+    double2 *orow = Mo + (i0 + ty) * ld + j0 + tx;
+#pragma unroll
+    for (int m = 0; m < kTile / kPairWarps; ++m) {
+        const int r = ty + m * kPairWarps;
+        const double c = B.aij[r][tx];
+        double2 nij = make_double2(-0.0, 0.0), nji = make_double2(-0.0, 0.0);
+        if (c != 0.0 && (!diag || r != tx) && r < rmax && jin) {
+            // m = f(node, twin message, A) = (-c^2 / pe, (N - P_t mu_t) / c) for both
+            // directions (solver.py:249-257); the two divisions by A_ij share its reciprocal
+            const double2 oij = B.mij[r][tx], oji = B.mji[tx][r];
+            const double2 ndi = B.ni[r];
+            const double pe1 = ndi.x - oji.x, num1 = ndi.y - oji.x * oji.y;
+            const double pe2 = ndj.x - oij.x, num2 = ndj.y - oij.x * oij.y;
+            const double cc = -c * c;
+            if (EXACT) {
+                nij = make_double2(cc / pe1, num1 / c);
+                nji = make_double2(cc / pe2, num2 / c);
+            } else {
+                const double rc = ddiv_rcp(c);
+                nij = make_double2(ddiv_fast_acc(cc, pe1, dr), ddiv_fast_acc_r(num1, c, rc, dr));
+                nji = make_double2(ddiv_fast_acc(cc, pe2, dr), ddiv_fast_acc_r(num2, c, rc, dr));
+            }
+            pair_stat<EXACT>(nij, oij, pe1, i0 + r, j0 + tx, K, lim, ps);
+            if (diag)
+                nji = make_double2(-0.0, 0.0);  // (the (j, i) element of the tile does it)
+            else
+                pair_stat<EXACT>(nji, oji, pe2, j0 + tx, i0 + r, K, lim, ps);
+        }
+        __stcs(orow + (int64_t)m * kPairWarps * ld, nij);
+        S.out[tx][r] = nji;
+    }
 }
 
 __global__ void __launch_bounds__(kPairCta) dense_pair_kernel(const SweepArgs a,
@@ -287,11 +408,17 @@ __global__ void __launch_bounds__(kPairCta) dense_pair_kernel(const SweepArgs a,
     PairSmem &S = *reinterpret_cast<PairSmem *>(pair_raw);
     const int tid = threadIdx.x;
     Ctrl *ctrl = a.ctrl;
+    const int64_t npairs = d.npairs, nt = d.ld / kTile;
     if (tid == 0) {
         volatile Ctrl *vc = ctrl;
         const int64_t s = vc->next_sweep;
         S.skip = vc->done || s > vc->max_iter + 2;
         S.sweep = s;
+        // tile pairs of the first stagings (thread 0 computes, the barriers publish)
+        for (int q = 0; q < kPairBufs; ++q) {
+            const int64_t pq = (int64_t)blockIdx.x + (int64_t)q * gridDim.x;
+            S.next_ij[q] = pq < npairs ? pair_of(pq, nt) : make_uint2(0u, 0u);
+        }
     }
     __syncthreads();
     if (S.skip) return;
@@ -300,64 +427,52 @@ __global__ void __launch_bounds__(kPairCta) dense_pair_kernel(const SweepArgs a,
     const double2 *M = d.msg[(s - 1) % 3];
     double2 *Mo = d.msg[s % 3];
     const double lim = fmin(ctrl->blowup, DBL_MAX);
-    const int64_t npairs = d.npairs;
     PairStats ps;
     const int tx = tid & 31, ty = tid >> 5;
     int64_t p = blockIdx.x;
-    if (p < npairs) {
-        const uint2 ij = d.pairs[p];
-        pair_stage(S.b[0], ij.x, ij.y, d, M, tid);
-    }
-    cpa_commit();
-    for (int k = 0; p < npairs; p += gridDim.x, ++k) {
-        const int64_t pn = p + gridDim.x;
-        if (pn < npairs) {
-            const uint2 ij = d.pairs[pn];
-            pair_stage(S.b[(k + 1) & 1], ij.x, ij.y, d, M, tid);
-        }
+#pragma unroll
+    for (int q = 0; q < kPairBufs - 1; ++q) {  // kPairBufs - 1 pairs in flight
+        const int64_t pq = p + (int64_t)q * gridDim.x;
+        if (pq < npairs) pair_stage(S.b[q], S.next_ij[q].x, S.next_ij[q].y, d, M, tid);
         cpa_commit();
-        cpa_wait<1>();
-        __syncthreads();  // pair p landed for every thread
-        const PairBuf &B = S.b[k & 1];
-        const uint2 ij = d.pairs[p];
+    }
+    for (int k = 0; p < npairs; p += gridDim.x, ++k) {
+        // buffer (k-1) % kPairBufs was released by the barrier ending iteration k-1; its
+        // pair indices were published by that barrier (slot (k-1) % kPairBufs of next_ij)
+        const int64_t pn = p + (int64_t)(kPairBufs - 1) * gridDim.x;
+        const int nb = (k + kPairBufs - 1) % kPairBufs;
+        if (pn < npairs) pair_stage(S.b[nb], S.next_ij[nb].x, S.next_ij[nb].y, d, M, tid);
+        cpa_commit();
+        cpa_wait<kPairBufs - 1>();
+        __syncthreads();  // pair p landed for every thread; next_ij[nb] read by all
+        if (tid == 0) {   // indices of the pair staged next iteration into buffer nb + 1
+            const int64_t pq = pn + gridDim.x;
+            S.next_ij[(nb + 1) % kPairBufs] = pq < npairs ? pair_of(pq, nt) : make_uint2(0u, 0u);
+        }
+        const PairBuf &B = S.b[k % kPairBufs];
+        const uint2 ij = B.ij;
         const int64_t I = ij.x, J = ij.y, i0 = I * kTile, j0 = J * kTile;
         const bool diag = I == J;
-        for (int r = ty; r < kTile; r += 8) {
-            const int64_t i = i0 + r, j = j0 + tx;
-            const double c = B.aij[r][tx];
-            double2 nij = make_double2(0.0, 0.0), nji = make_double2(0.0, 0.0);
-            if (c != 0.0 && i != j && i < K && j < K) {
-                // m = f(node, twin message, A) = (-c^2 / pe, (N - P_t mu_t) / c) for both
-                // directions (solver.py:249-257): the four divisions overlap on the
-                // compiler's fast path; the rare out-of-range operand redoes all four
-                const double2 oij = B.mij[r][tx], oji = B.mji[tx][r];
-                const double2 ndi = B.ni[r], ndj = B.nj[tx];
-                const double pe1 = ndi.x - oji.x, num1 = ndi.y - oji.x * oji.y;
-                const double pe2 = ndj.x - oij.x, num2 = ndj.y - oij.x * oij.y;
-                const double cc = -c * c;
-                bool k1, k2, k3, k4;
-                nij.x = ddiv_fast(cc, pe1, k1);
-                nij.y = ddiv_fast(num1, c, k2);
-                nji.x = ddiv_fast(cc, pe2, k3);
-                nji.y = ddiv_fast(num2, c, k4);
-                if (!(k1 && k2 && k3 && k4)) {
-                    nij.x = div_slow(cc, pe1);
-                    nij.y = div_slow(num1, c);
-                    nji.x = div_slow(cc, pe2);
-                    nji.y = div_slow(num2, c);
-                }
-                pair_stat(nij, oij, pe1, (uint64_t)(i * K + j), lim, ps);
-                if (diag)
-                    nji = make_double2(0.0, 0.0);  // (the (j, i) element of the tile does it)
-                else
-                    pair_stat(nji, oji, pe2, (uint64_t)(j * K + i), lim, ps);
-            }
-            __stcs(Mo + i * ld + j, nij);
-            S.out[tx][r] = nji;
+        PairStats pt;
+        DivRange dr;
+        pair_elems<false>(B, S, Mo, ld, K, i0, j0, diag, tx, ty, lim, pt, dr);
+        // out complete; buffer k % kPairBufs free for the staging kPairBufs - 1 pairs ahead
+        if (__syncthreads_or(!div_range_ok(dr))) {
+            PairStats pe;
+            DivRange dx;
+            pair_elems<true>(B, S, Mo, ld, K, i0, j0, diag, tx, ty, lim, pe, dx);
+            pt = pe;
+            __syncthreads();
         }
-        __syncthreads();  // out complete; buffer k&1 free for the prefetch two pairs ahead
-        if (!diag)
-            for (int r = ty; r < kTile; r += 8) __stcs(Mo + (j0 + r) * ld + i0 + tx, S.out[r][tx]);
+        ps.chg = fmax(ps.chg, pt.chg);
+        ps.oor |= pt.oor;
+        ps.sing = pt.sing < ps.sing ? pt.sing : ps.sing;
+        if (!diag) {
+            double2 *trow = Mo + (j0 + ty) * ld + i0 + tx;
+#pragma unroll
+            for (int m = 0; m < kTile / kPairWarps; ++m)
+                __stcs(trow + (int64_t)m * kPairWarps * ld, S.out[ty + m * kPairWarps][tx]);
+        }
     }
     cpa_wait<0>();
     // CTA reductions + last-CTA decision (the sparse kernel's protocol)
@@ -380,7 +495,7 @@ __global__ void __launch_bounds__(kPairCta) dense_pair_kernel(const SweepArgs a,
     if (tid == 0) {
         double bc = 0.0;
         unsigned f = 0u;
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < kPairWarps; ++w) {
             bc = fmax(bc, S.red_d[w]);
             f |= S.red_u[w];
         }
@@ -405,7 +520,7 @@ __global__ void __launch_bounds__(kPairCta) dense_pair_kernel(const SweepArgs a,
     __syncthreads();
     if (tid == 0) {
         double rsq_t = 0.0;
-        for (int w = 0; w < 8; ++w) rsq_t += S.red_d[w];
+        for (int w = 0; w < kPairWarps; ++w) rsq_t += S.red_d[w];
         decide_sweep(ctrl, a, s - 2, rsq_t);
         const int nslot = (int)((s + 1) % kStatSlots);
         ctrl->change_bits[nslot] = 0ull;
@@ -461,6 +576,18 @@ cudaError_t encode_maps(const DenseArgs &d) {
 }
 
 }  // namespace
+
+cudaError_t launch_dense_mask(const double *A, int64_t ld, uint32_t *emask, cudaStream_t st) {
+    const int64_t n = (ld / 32) * ld;
+    dense_mask_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A, ld, emask);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_init(const uint32_t *emask, int64_t ld, double2 *msg, cudaStream_t st) {
+    const int64_t n = ld * ld;
+    dense_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(emask, ld, msg);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_dense_sweep(const SweepArgs &a, const DenseArgs &d, cudaStream_t st) {
     if (g_maps_key[0] != d.A || g_maps_key[1] != d.msg[0] || g_maps_key[2] != d.msg[1] ||

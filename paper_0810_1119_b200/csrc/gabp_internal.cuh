@@ -291,8 +291,11 @@ struct DenseArgs {
     double2 *node;   // {P_i, P_i mu~_i} of the state read by the launch
     const uint2 *pairs;  // upper-triangle tile pairs (I <= J) of the pair-tile kernel
     int64_t npairs;
+    const uint32_t *emask;  // [ld/32][ld]: bit l of word (cb, k) = A[k][32 cb + l] is an edge
 };
 cudaError_t launch_dense_sweep(const SweepArgs &a, const DenseArgs &d, cudaStream_t st);
+cudaError_t launch_dense_mask(const double *A, int64_t ld, uint32_t *emask, cudaStream_t st);
+cudaError_t launch_dense_init(const uint32_t *emask, int64_t ld, double2 *msg, cudaStream_t st);
 
 // acceleration (accel.cu): gated Aitken restart of the mean messages, in place in m2
 // (gated = 0: plain aitken_extrapolate); max |.| reductions as ordered bit patterns
