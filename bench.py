@@ -387,7 +387,8 @@ def run_ours(args):
     g_info_span = float(g.info.twin_span)
     slice_path = sched == "broadcast" and int(g.info.num_slices) > 0
     kname = (("slice_kernel_ldg", "slice_kernel_pipe", "slice_kernel_grp")[int(g.info.slice_variant)]
-             + " + exact twin (exits unless flagged)") if slice_path else f"sweep_kernel<{sched}>"
+             + " (exact twin tail-launched only when a launch flags itself)") if slice_path \
+        else f"sweep_kernel<{sched}>"
 
     # e2e: the drop-in call with pinned host buffers, H2D + build + solve + D2H timed
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, min(args.steps, 20))

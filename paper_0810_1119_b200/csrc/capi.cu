@@ -634,10 +634,12 @@ int dist_finish_split(gabp_graph *G, const SweepArgs &a, cudaStream_t st, cudaSt
         CK(gabp::launch_halo_unpack(a, D->d_ridx + D->roff[q], D->rcount[q],
                                     D->d_rbuf + 4 * D->roff[q], cs, 1));
     CK(cudaStreamWaitEvent(cs, D->ev_sweep, 0));
-    if (D->world > 1 && D->comm_nccl) {
+    if (D->world > 1 && D->comm_nccl) {  // (one group: one NCCL launch)
+        NK(g_nccl.groupStart());
         NK(g_nccl.allReduce(D->d_stats, D->d_stats, 5, ncclFloat64, ncclMax, D->comm, cs));
         NK(g_nccl.allReduce(D->d_stats + 5, D->d_stats + 5, 1, ncclFloat64, ncclSum, D->comm,
                             cs));
+        NK(g_nccl.groupEnd());
     }
     CK(gabp::launch_finish(a, cs));
     CK(cudaEventRecord(D->ev_done, cs));
@@ -658,17 +660,26 @@ int dist_launch_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
     }
     DistState *D = G->dist;
     CK(gabp::launch_sweep(a, GABP_SCHED_BROADCAST, gabp::kModeSolve, dist_gather(G), st));
-    if (D->world > 1) {
-        NK(g_nccl.allReduce(D->d_stats, D->d_stats, 5, ncclFloat64, ncclMax, D->comm, st));
-        NK(g_nccl.allReduce(D->d_stats + 5, D->d_stats + 5, 1, ncclFloat64, ncclSum, D->comm,
-                            st));
-    }
-    CK(gabp::launch_finish(a, st));
-    if (D->peers.empty()) return GABP_OK;
+    // the halo is packed straight after the sweep (before the decision: pre_finish), so the
+    // statistics all-reduce and the halo send/recv go out as one NCCL group and the
+    // all-reduce's latency hides under the exchange; the decision and the unpack follow
     for (size_t q = 0; q < D->peers.size(); ++q)
         CK(gabp::launch_halo_pack(a, D->d_sidx + D->soff[q], D->scount[q],
-                                  D->d_sbuf + 4 * D->soff[q], st, 0));
+                                  D->d_sbuf + 4 * D->soff[q], st, 1));
+    if (D->world <= 1 || D->peers.empty()) {
+        if (D->world > 1) {
+            NK(g_nccl.groupStart());
+            NK(g_nccl.allReduce(D->d_stats, D->d_stats, 5, ncclFloat64, ncclMax, D->comm, st));
+            NK(g_nccl.allReduce(D->d_stats + 5, D->d_stats + 5, 1, ncclFloat64, ncclSum,
+                                D->comm, st));
+            NK(g_nccl.groupEnd());
+        }
+        CK(gabp::launch_finish(a, st));
+        return GABP_OK;
+    }
     NK(g_nccl.groupStart());
+    NK(g_nccl.allReduce(D->d_stats, D->d_stats, 5, ncclFloat64, ncclMax, D->comm, st));
+    NK(g_nccl.allReduce(D->d_stats + 5, D->d_stats + 5, 1, ncclFloat64, ncclSum, D->comm, st));
     for (size_t q = 0; q < D->peers.size(); ++q) {
         if (D->scount[q])
             NK(g_nccl.send(D->d_sbuf + 4 * D->soff[q], 4 * D->scount[q], ncclFloat64,
@@ -678,6 +689,7 @@ int dist_launch_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
                            D->peers[q], D->comm, st));
     }
     NK(g_nccl.groupEnd());
+    CK(gabp::launch_finish(a, st));
     for (size_t q = 0; q < D->peers.size(); ++q)
         CK(gabp::launch_halo_unpack(a, D->d_ridx + D->roff[q], D->rcount[q],
                                     D->d_rbuf + 4 * D->roff[q], st, 0));
@@ -781,8 +793,9 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         fprintf(stderr, "[gabp] run_solve: setup %.2f ms, chunk graph (%d sweeps) %.2f ms\n",
                 tc0 - t_setup, C, host_ms() - tc0);
     SweepArgs a = make_args(G);
-    // kernels per sweep launch: slice paths fast kernel + exact twin, tile path one
-    const int kps = (gather == gabp::kGatherSlice || gather == gabp::kGatherSliceParallel) ? 2 : 1;
+    // kernels per sweep launch: the fast kernel (exact twins, host- or tail-launched, count
+    // themselves on the device: Ctrl.twin_launches)
+    const int kps = 1;
     G->kernels_launched = 0;
     CK(cudaEventRecord(G->ev[2], st));
     while (launched < total) {
@@ -814,7 +827,7 @@ void fill_report(gabp_graph *G, const gabp_options_t *opt, double ms, double rsq
         c.iterations * (opt->schedule == GABP_SCHED_BROADCAST ? G->g.n : G->g.E);
     rep->device_ms = ms;
     rep->residual_probes = c.probes;
-    rep->kernel_launches = G->kernels_launched;
+    rep->kernel_launches = G->kernels_launched + c.twin_launches;
     rep->final_rel_residual =
         (c.n_hist >= 1 && G->g.rhs_norm > 0.0) ? sqrt(rsq_last) / G->g.rhs_norm : NAN;
 }

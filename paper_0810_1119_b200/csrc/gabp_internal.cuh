@@ -101,6 +101,8 @@ struct Ctrl {
     int64_t probe_t;            // slice path: sweep T whose residual the exact twin after
                                 // launch T+1 computes, deciding T a launch early (0: none)
     int32_t probes;             // residual probes run (diagnostics)
+    int32_t twin_launches;      // exact-twin kernels launched, host- or tail-launched (each
+                                // counts itself)
 };
 
 // A fresh controller: every "first index" slot at the kNoIndex sentinel.
@@ -164,6 +166,8 @@ struct SweepArgs {
                                // residual-only group launch (probe_next)
     int probe_force;           // test hook (GABP_PROBE_FORCE=1): request a probe after every
                                // launch, so every mispredicted probe path runs
+    int twin_tail;             // group launch: the exact twin is tail-launched from the
+    int twin_grid;             // device only when the launch flags itself (slice.cu)
 };
 
 // kernels (sweep.cu); prepare_sweep_kernels() must run once per device before launches

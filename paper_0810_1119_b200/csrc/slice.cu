@@ -940,6 +940,7 @@ __device__ __forceinline__ bool slice_prologue(SM &S, const SweepArgs &a, bool e
         volatile Ctrl *vc = a.ctrl;
         const int64_t s = vc->next_sweep;
         const bool twin = exact && !a.exact_primary;
+        if (twin && blockIdx.x == 0) atomicAdd(&a.ctrl->twin_launches, 1);
         S.skip = vc->done || s > vc->max_iter + 2 || (twin && vc->redo != 2);
         // the residual probe the last launch asked for (probe_next): run by an idle exact
         // twin (a.probe == 1) or as a residual-only group launch (a.probe == 2)
@@ -1144,7 +1145,20 @@ __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_grp(const SweepArgs
     } else {
         slice_first<kGroup + 1, false>(a, s, st, lane);
     }
-    sweep_epilogue<kGThreads, kModeSolve, 1>(S.tail, a, s, s >= 3, st, tid);
+    const bool flagged = sweep_epilogue<kGThreads, kModeSolve, 1>(S.tail, a, s, s >= 3, st, tid);
+    if (flagged && a.twin_tail) {
+        // a fast-path division left its range: the exact twin redoes this sweep, launched
+        // from here into the tail of this grid (CUDA dynamic parallelism) -- it runs after
+        // this grid and before the next launch of the stream, and only when needed (a
+        // host-launched twin that exits at once cost 16 us of every config-1 sweep)
+        SweepArgs t = a;
+        t.sl_lo = 0;
+        t.sl_hi = a.nslices;
+        t.part_base = 0;
+        t.exact_primary = 0;
+        t.twin_tail = 0;
+        slice_kernel_ldg<true><<<(unsigned)a.twin_grid, kLThreads, 0, cudaStreamTailLaunch>>>(t);
+    }
 }
 
 // ---- parallel schedule over the slice groups ------------------------------------------------
@@ -1820,6 +1834,12 @@ cudaError_t prepare_slice_kernels() {
     return cudaSuccess;
 }
 
+// GABP_TWIN_LAUNCH=1 keeps the host-launched exact twin on the group path (A/B timing)
+static bool twin_tail_enabled() {
+    static const int v = getenv("GABP_TWIN_LAUNCH") ? atoi(getenv("GABP_TWIN_LAUNCH")) : 0;
+    return !v;
+}
+
 // GABP_NO_PROBE=1 disables the residual probe (A/B timing)
 static bool probe_enabled() {
     static const int off = getenv("GABP_NO_PROBE") ? atoi(getenv("GABP_NO_PROBE")) : 0;
@@ -1865,6 +1885,14 @@ cudaError_t launch_slice_part(const SweepArgs &a0, int reserve_sms, cudaStream_t
     // residual probe: a residual-only group launch (variant 2), else run by the exact twin
     a.probe = (!a0.dist && probe_enabled()) ? (a0.slice_variant == 2 ? 2 : 1) : 0;
     a.probe_force = probe_forced();
+    a.twin_tail = (a.slice_variant == 2 && !a0.dist && a0.sl_lo == 0 &&
+                   a0.sl_hi == a0.nslices && twin_tail_enabled()) ? 1 : 0;
+    {
+        int64_t gx = g_grid_ldg > 0 ? g_grid_ldg : 148 * 2;
+        const int64_t nx = (a.nslices + kLWarps - 1) / kLWarps;
+        if (gx > nx) gx = nx > 0 ? nx : 1;
+        a.twin_grid = (int)gx;
+    }
     if (a.slice_variant == 2) {
         int64_t grid = (g_grid_grp > 0 ? g_grid_grp : 148) - reserve_sms;
         const int64_t need = (a.sl_hi - a.sl_lo) / kGroup;
@@ -1874,7 +1902,9 @@ cudaError_t launch_slice_part(const SweepArgs &a0, int reserve_sms, cudaStream_t
     } else {
         launch_slice_fast(a, st);
     }
-    // exact twin: exits at once unless the fast launch flagged itself (Ctrl.redo)
+    // exact twin: exits at once unless the fast launch flagged itself (Ctrl.redo); the
+    // whole-graph group launch tail-launches it from the device instead
+    if (a.twin_tail) return cudaGetLastError();
     SweepArgs t = a;
     t.sl_lo = 0;
     t.sl_hi = a.nslices;
