@@ -237,9 +237,10 @@ int gabp_dist_results(gabp_graph_t *g, const gabp_options_t *opt, double *h_mean
                       double *h_precs, double *h_change_hist, double *h_res_hist,
                       gabp_report_t *rep);
 
-/* Sweep-kernel timing hook for bench.py: runs `sweeps` synchronous sweeps of the
- * solve kernel from the current state and returns the average device time per
- * sweep kernel launch (CUDA events on the graph stream). */
+/* Sweep-kernel timing hook for bench.py: from zero messages, runs 3 untimed launches
+ * (the first launches stream less than a full sweep), then `sweeps` launches of the solve
+ * kernel, and returns their average device time per sweep (CUDA events on the graph
+ * stream; exact twins included when a launch flags itself). */
 int gabp_bench_sweeps(gabp_graph_t *g, int32_t schedule, int32_t gather_mode, int64_t sweeps,
                       double *ms_per_sweep);
 

@@ -8,13 +8,13 @@
 //
 //   1. validate + degree histogram            (one pass over the pairs, atomics)
 //   2. row_ptr = exclusive scan(degree)       (CUB DeviceScan)
-//   3. scatter both directions of every pair  (atomic cursor per row)
-//   4. sort every row by column               (CUB DeviceSegmentedSort, payload 2p+dir)
-//   5. pos[payload] = e, rev[e] = pos[payload ^ 1], duplicate check
+//   3. keys (row << cb | col) of both directions of every pair, one stable radix sort
+//      (CUB DeviceRadixSort, payload 2p+dir): rows ascending, neighbours ascending
+//   4. pos[payload] = e, rev[e] = pos[payload ^ 1], duplicate check (equal keys)
 //   6. tiles: boundary where the edge bucket changes or every kTileRows rows
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
-#include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_radix_sort.cuh>
 #include <stdio.h>
 
 #include "gabp_internal.cuh"
@@ -41,34 +41,34 @@ __global__ void count_kernel(int64_t n, int64_t np, const int64_t *pi, const int
     }
 }
 
-__global__ void scatter_kernel(int64_t np, const int64_t *pi, const int64_t *pj,
-                               uint32_t *cursor, uint32_t *tcol, uint32_t *tpl) {
+// Both directions of every pair as one sort key (row << cb) | col, payload 2p / 2p + 1 (the
+// pair and the direction).  One stable radix sort of the keys gives the CSR edge order --
+// rows ascending, neighbours ascending (graph.py:84-91) -- with no per-row sort.
+__global__ void key_kernel(int64_t np, const int64_t *pi, const int64_t *pj, int cb,
+                           unsigned long long *key, uint32_t *pl) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np;
          p += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t i = (uint32_t)pi[p], j = (uint32_t)pj[p];
-        const uint32_t a = atomicAdd(&cursor[i], 1u);
-        tcol[a] = j;
-        tpl[a] = (uint32_t)(2 * p);
-        const uint32_t b = atomicAdd(&cursor[j], 1u);
-        tcol[b] = i;
-        tpl[b] = (uint32_t)(2 * p + 1);
+        const unsigned long long i = (unsigned long long)pi[p], j = (unsigned long long)pj[p];
+        key[2 * p] = (i << cb) | j;
+        key[2 * p + 1] = (j << cb) | i;
+        pl[2 * p] = (uint32_t)(2 * p);
+        pl[2 * p + 1] = (uint32_t)(2 * p + 1);
     }
 }
 
-__device__ __forceinline__ uint32_t row_of(uint32_t pl, const int64_t *pi, const int64_t *pj) {
-    const int64_t p = pl >> 1;
-    return (uint32_t)((pl & 1u) ? pj[p] : pi[p]);
-}
-
-__global__ void pos_kernel(int64_t E, const uint32_t *scol, const uint32_t *spl,
-                           const int64_t *pi, const int64_t *pj, uint32_t *pos, int *err,
-                           unsigned long long *err_at) {
+// scol and the payload position of every sorted edge; a key equal to its predecessor is a
+// duplicate pair (reported by its pair index)
+__global__ void pos_key_kernel(int64_t E, const unsigned long long *key, const uint32_t *spl,
+                               int cb, uint32_t *scol, uint32_t *pos, int *err,
+                               unsigned long long *err_at) {
+    const unsigned long long mask = (1ull << cb) - 1ull;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
          e += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = key[e];
         const uint32_t pl = spl[e];
+        scol[e] = (uint32_t)(k & mask);
         pos[pl] = (uint32_t)e;
-        if (e > 0 && scol[e] == scol[e - 1] &&
-            row_of(pl, pi, pj) == row_of(spl[e - 1], pi, pj)) {
+        if (e > 0 && k == key[e - 1]) {
             atomicCAS(err, 0, (int)kErrDup);
             atomicMin(err_at, (unsigned long long)(pl >> 1));
         }
@@ -349,48 +349,40 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
         }
     }
     if (E > 0) {
-        // 3. scatter
-        uint32_t *tcol = nullptr, *tpl = nullptr, *scol = nullptr, *spl = nullptr;
-        BCHECK(cudaMallocAsync(&tcol, sizeof(uint32_t) * E, st));
-        BCHECK(cudaMallocAsync(&tpl, sizeof(uint32_t) * E, st));
-        BCHECK(cudaMemcpyAsync(deg, g.row_ptr, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice,
-                               st));  // deg becomes the cursor
-        scatter_kernel<<<grid_for(npairs), 256, 0, st>>>(npairs, d_pi, d_pj, deg, tcol, tpl);
-        BCHECK(cudaGetLastError());
-        // 4. per-row sort by column
-        BCHECK(cudaMallocAsync(&scol, sizeof(uint32_t) * E, st));
+        // 3. CSR order: one stable radix sort of (row, col) keys of both directions
+        int cb = 1;
+        while (cb < 32 && ((unsigned long long)(n - 1) >> cb) != 0ull) ++cb;
+        unsigned long long *kin = nullptr, *kout = nullptr;
+        uint32_t *plin = nullptr, *spl = nullptr;
+        BCHECK(cudaMallocAsync(&kin, sizeof(unsigned long long) * E, st));
+        BCHECK(cudaMallocAsync(&kout, sizeof(unsigned long long) * E, st));
+        BCHECK(cudaMallocAsync(&plin, sizeof(uint32_t) * E, st));
         BCHECK(cudaMallocAsync(&spl, sizeof(uint32_t) * E, st));
+        key_kernel<<<grid_for(npairs), 256, 0, st>>>(npairs, d_pi, d_pj, cb, kin, plin);
+        BCHECK(cudaGetLastError());
         size_t sb = 0;
-        BCHECK(cub::DeviceSegmentedSort::SortPairs(nullptr, sb, tcol, scol, tpl, spl, (int64_t)E,
-                                                   (int64_t)n, g.row_ptr, g.row_ptr + 1, st));
+        BCHECK(cub::DeviceRadixSort::SortPairs(nullptr, sb, kin, kout, plin, spl, (int64_t)E, 0,
+                                               2 * cb, st));
         if (sb > tmp_cap) {
             cudaFreeAsync(tmp, st);
             tmp_cap = sb;
             BCHECK(cudaMallocAsync(&tmp, tmp_cap, st));
         }
-        BCHECK(cub::DeviceSegmentedSort::SortPairs(tmp, sb, tcol, scol, tpl, spl, (int64_t)E,
-                                                   (int64_t)n, g.row_ptr, g.row_ptr + 1, st));
-        cudaFreeAsync(tcol, st);
-        // 5. twin index
-        uint32_t *pos = tpl;  // reuse
-        pos_kernel<<<grid_for(E), 256, 0, st>>>(E, scol, spl, d_pi, d_pj, pos, d_err, d_at);
+        BCHECK(cub::DeviceRadixSort::SortPairs(tmp, sb, kin, kout, plin, spl, (int64_t)E, 0,
+                                               2 * cb, st));
+        // 4. twin index: pos[payload] = edge id; scol from the keys (buffers reused)
+        uint32_t *scol = plin;
+        uint32_t *pos = reinterpret_cast<uint32_t *>(kin);
+        pos_key_kernel<<<grid_for(E), 256, 0, st>>>(E, kout, spl, cb, scol, pos, d_err, d_at);
         BCHECK(cudaGetLastError());
         if (val_ready) BCHECK(cudaStreamWaitEvent(st, val_ready, 0));
         edge_kernel<<<grid_for(E), 256, 0, st>>>(E, scol, spl, pos, d_pv, g.er, d_err, d_at);
         BCHECK(cudaGetLastError());
-        cudaFreeAsync(scol, st);
+        cudaFreeAsync(kin, st);
+        cudaFreeAsync(kout, st);
+        cudaFreeAsync(plin, st);
         cudaFreeAsync(spl, st);
-        cudaFreeAsync(tpl, st);
-        double *d_span = nullptr;
-        BCHECK(cudaMallocAsync(&d_span, sizeof(double), st));
-        BCHECK(cudaMemsetAsync(d_span, 0, sizeof(double), st));
-        twin_span_kernel<<<grid_for(E), 256, 0, st>>>(E, g.er, d_span);
-        BCHECK(cudaGetLastError());
-        double h_span = 0.0;
-        BCHECK(cudaMemcpyAsync(&h_span, d_span, sizeof(double), cudaMemcpyDeviceToHost, st));
-        BCHECK(cudaStreamSynchronize(st));
-        cudaFreeAsync(d_span, st);
-        g.twin_span = h_span / (double)E;
+        g.twin_span = -1.0;  // computed only if the tile layout ends up serving the solve
     }
     // 6. tiles
     {
@@ -451,6 +443,19 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
         const int rc = build_slices(g, st, err, errlen);
         if (rc == GABP_ENOMEM || rc == GABP_ECUDA) return rc;
         err[0] = 0;  // too many slots for 32-bit ids: the row tiles remain
+    }
+    if (g.nslices == 0 && E > 0) {
+        // no slice layout: the tile kernels choose their gather by the twin locality
+        double *d_span = nullptr;
+        BCHECK(cudaMallocAsync(&d_span, sizeof(double), st));
+        BCHECK(cudaMemsetAsync(d_span, 0, sizeof(double), st));
+        twin_span_kernel<<<grid_for(E), 256, 0, st>>>(E, g.er, d_span);
+        BCHECK(cudaGetLastError());
+        double h_span = 0.0;
+        BCHECK(cudaMemcpyAsync(&h_span, d_span, sizeof(double), cudaMemcpyDeviceToHost, st));
+        BCHECK(cudaStreamSynchronize(st));
+        cudaFreeAsync(d_span, st);
+        g.twin_span = h_span / (double)E;
     }
     return compute_priors(g, st, err, errlen);
 }
