@@ -1185,15 +1185,21 @@ static_assert(kPB % kGC == 0, "a block starts on a chunk boundary");
 __device__ __forceinline__ uint32_t par_passes(uint32_t w) {
     return w > kPB ? (w + kPB - 1) / kPB : 1u;
 }
-// Pass p >= 1 starts at column p kPB: the exclusion sums of edges p kPB .. p kPB + kPB - 1
-// share the sequential prefix A_ii + sum_{q < p kPB} P_qi (no edge of the block is excluded
-// from it), carried over from pass p-1 -- the same operations in the same order as summing
-// from column 0, and half the column visits of a full re-walk per block.
-__device__ __forceinline__ uint32_t par_first_chunk(uint32_t pass) {
-    return pass * (uint32_t)(kPB / kGC);
-}
 
-// Producer of the parallel kernel: per group, npass passes of ceil(w / kGC) chunks.
+// Producer of the parallel kernel: per group, np passes; pass 0 streams every column in
+// chunks of kGC (all streams), pass p >= 1 streams I^{(s-1)} alone from column p kPB in
+// chunks of kPC columns (a stage holds kPC x kStride messages: as many bytes per ring trip
+// as a pass-0 chunk).  Descriptor: b = first column of the chunk, nb = 1 on the last chunk
+// of a pass, pad = {pass, passes, columns in the chunk}.
+#ifndef GABP_PAR_PC
+#define GABP_PAR_PC 5
+#endif
+constexpr int kPC = GABP_PAR_PC;
+struct PStage {
+    double2 i[kPC][kStride];
+};
+static_assert(sizeof(PStage) <= sizeof(GStage), "a later-pass chunk must fit a ring stage");
+
 template <bool STATS, bool RESID, bool EXACT>
 __device__ __forceinline__ void par_produce(const SweepArgs &a, GRing &G, uint32_t *ctr,
                                             const double2 *I1, const double2 *I2, int lane) {
@@ -1209,7 +1215,7 @@ __device__ __forceinline__ void par_produce(const SweepArgs &a, GRing &G, uint32
     }
     int64_t gcur = g_lo + __shfl_sync(~0u, u0, 0), gnxt = g_lo + __shfl_sync(~0u, u1, 0);
     uint2 icur = group_info(a, gcur, ngroups), inxt = group_info(a, gnxt, ngroups);
-    uint32_t b = 0, pass = 0, nb = chunks_of(icur.y), np = par_passes(icur.y);
+    uint32_t q0 = 0, pass = 0, np = par_passes(icur.y);
     for (uint32_t k = 0;; ++k) {
         const int stg = (int)(k % kGS);
         if (k >= (uint32_t)kGS) t_wait(&G.empty[stg], ((k / kGS) - 1u) & 1u);
@@ -1220,26 +1226,28 @@ __device__ __forceinline__ void par_produce(const SweepArgs &a, GRing &G, uint32
             }
             return;
         }
+        const uint32_t w = icur.y, cw = pass == 0 ? (uint32_t)kGC : (uint32_t)kPC;
+        const uint32_t nc = w > q0 ? min(cw, w - q0) : 0u;
+        const bool last = q0 + cw >= w;
         if (lane == 0) {
-            const uint32_t w = icur.y, q0 = b * kGC;
-            const uint32_t nc = w > q0 ? min((uint32_t)kGC, w - q0) : 0u;
             const uint32_t slot = icur.x + (uint32_t)kStride * q0;
             GMeta &m = G.meta[stg];
             m.g = (int32_t)gcur;
-            m.b = b;
-            m.nb = nb;
+            m.b = q0;
+            m.nb = last ? 1u : 0u;
             m.w = w;
             m.gbase = icur.x;
             m.pad[0] = pass;
             m.pad[1] = np;
-            GStage &S = G.st[stg];
+            m.pad[2] = nc;
             const unsigned per = pass == 0 ? 16u + (STATS ? 16u : 0u) + (RESID ? 12u : 0u) : 16u;
             t_expect_tx(&G.full[stg], nc * (uint32_t)kStride * per);
             if (nc) {
-                // I^{(s-1)} (the i3 buffer) is re-read by the later passes: keep it in L2
-                t_bulk_ef(&S.i3[0][0], I1 + slot, nc * kStride * 16u, &G.full[stg],
-                          np > 1 ? pol_el : pol_ef);
+                // I^{(s-1)} is re-read by the later passes: keep it in L2 while they run
+                const uint64_t pol = np > 1 && pass + 1 < np ? pol_el : pol_ef;
                 if (pass == 0) {
+                    GStage &S = G.st[stg];
+                    t_bulk_ef(&S.i3[0][0], I1 + slot, nc * kStride * 16u, &G.full[stg], pol);
                     if (STATS)
                         t_bulk_ef(&S.i2[0][0], I2 + slot, nc * kStride * 16u, &G.full[stg], pol_ef);
                     if (RESID) {
@@ -1248,22 +1256,25 @@ __device__ __forceinline__ void par_produce(const SweepArgs &a, GRing &G, uint32
                         t_bulk_ef(&S.col[0][0], a.scol + slot, nc * kStride * 4u, &G.full[stg],
                                   pol_ef);
                     }
+                } else {
+                    PStage &P = reinterpret_cast<PStage &>(G.st[stg]);
+                    t_bulk_ef(&P.i[0][0], I1 + slot, nc * kStride * 16u, &G.full[stg], pol);
                 }
             }
         }
-        if (++b >= nb) {
-            b = par_first_chunk(pass + 1);
+        if (last) {
             if (++pass >= np) {
-                b = 0;
                 pass = 0;
                 gcur = gnxt;
                 icur = inxt;
                 gnxt = g_lo + __shfl_sync(~0u, pend, 0);
                 inxt = group_info(a, gnxt, ngroups);
                 if (lane == 0) pend = atomicAdd(ctr, 1u);
-                nb = chunks_of(icur.y);
                 np = par_passes(icur.y);
             }
+            q0 = pass * kPB;
+        } else {
+            q0 += cw;
         }
     }
 }
@@ -1277,6 +1288,32 @@ struct ParRow {
     double cb[kPB];                        // A_ij of the block's edges
     uint32_t tw[kPB];                      // their twin slots
 };
+
+// One incoming term of column q into the block's exclusion sums (and the next block's
+// prefix while q is one of the block's own columns); q is warp-uniform.  Pass p >= 1
+// starts at column p kPB: the exclusion sums of edges p kPB .. p kPB + kPB - 1 share the
+// sequential prefix A_ii + sum_{q < p kPB} P_qi (no edge of the block is excluded from it),
+// carried over from pass p-1 -- the same operations in the same order as summing from
+// column 0, and half the column visits of a full re-walk per block.
+__device__ __forceinline__ void par_accum(ParRow &row, uint32_t q, uint32_t blk, double vP,
+                                          double vN) {
+    if (q < blk + kPB) {
+        row.preP = row.preP + vP;
+        row.preN = row.preN + vN;
+#pragma unroll
+        for (int jj = 0; jj < kPB; ++jj)
+            if (q != blk + jj) {
+                row.aP[jj] = row.aP[jj] + vP;
+                row.aN[jj] = row.aN[jj] + vN;
+            }
+    } else {
+#pragma unroll
+        for (int jj = 0; jj < kPB; ++jj) {
+            row.aP[jj] = row.aP[jj] + vP;
+            row.aN[jj] = row.aN[jj] + vN;
+        }
+    }
+}
 
 // Consumer of the parallel kernel (warp `warp`, lane per row).
 template <bool STATS, bool RESID, bool EXACT>
@@ -1305,9 +1342,10 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
     }
     for (uint32_t k = 0;; ++k) {
         const uint32_t pass = m.pad[0];
+        const uint32_t blk = pass * kPB;  // first edge of the block (warp-uniform)
         const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
         const uint32_t slot0 = m.gbase + (uint32_t)t;
-        if (m.b == par_first_chunk(pass)) {
+        if (m.b == blk) {  // first chunk of the pass
             if (pass == 0) {  // row header (loaded one chunk ago)
                 row.d = hn.d;
                 row.pP = hn.nd.x;
@@ -1327,10 +1365,12 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
                 row.aN[jj] = row.preN;
             }
         }
-        if (m.b + 1 == m.nb) {  // last chunk of the pass: the block's coefficients and twins
+        // last chunk of the pass: the block's coefficients and twin slots (loading them on
+        // the pass's first chunk instead, held across the pass, measured 2 % slower)
+        if (m.nb) {
 #pragma unroll
             for (int jj = 0; jj < kPB; ++jj) {
-                const uint32_t j = pass * kPB + jj;
+                const uint32_t j = blk + jj;
                 row.cb[jj] = 1.0;
                 row.tw[jj] = 0u;
                 if (j < row.d) {
@@ -1344,7 +1384,7 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
         t_wait(&G.full[s1], ((k + 1) / kGS) & 1u);
         const GMeta mn = G.meta[s1];
         if (mn.g >= 0) {
-            if (mn.b == 0 && mn.pad[0] == 0) {  // (pass 0 of a group starts at chunk 0)
+            if (mn.b == 0 && mn.pad[0] == 0) {  // (pass 0 of a group starts at column 0)
                 const int64_t pn = ((int64_t)mn.g * kGroup + warp) * 32 + lane;
                 hn.nd = __ldg(a.snd + pn);
                 hn.d = __ldg(a.sdeg + pn);
@@ -1356,21 +1396,19 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
             if (RESID && mn.pad[0] == 0) {
 #pragma unroll
                 for (int u = 0; u < kGC; ++u)
-                    if (mn.b * kGC + u < mn.w) nx[u] = __ldcg(&g2[G.st[s1].col[u][t]].x);
+                    if (mn.b + u < mn.w) nx[u] = __ldcg(&g2[G.st[s1].col[u][t]].x);
             }
         }
         const int s0 = (int)(k % kGS);
-        const GStage &S = G.st[s0];
         const uint32_t d = row.d;
-        const uint32_t blk = pass * kPB;  // first edge of the block (warp-uniform)
-        const bool inblk = m.b * kGC < blk + kPB;  // chunk meets the block's own columns
+        if (pass == 0) {
+            const GStage &S = G.st[s0];
 #pragma unroll
-        for (int u = 0; u < kGC; ++u) {
-            const uint32_t q = m.b * kGC + u;
-            if (q < d) {
-                const double2 v = S.i3[u][t];  // I^{(s-1)}_iq = m_{k_q -> i}
-                const double vP = v.x, vN = v.x * v.y;  // (prec * mean), solver.py:148
-                if (pass == 0) {
+            for (int u = 0; u < kGC; ++u) {
+                const uint32_t q = m.b + u;
+                if (q < d) {
+                    const double2 v = S.i3[u][t];  // I^{(s-1)}_iq = m_{k_q -> i}
+                    const double vP = v.x, vN = v.x * v.y;  // (prec * mean), solver.py:148
                     row.sp = row.sp + vP;
                     row.sn = row.sn + vN;
                     if (RESID) row.y = row.y + S.c[u][t] * gx[u];
@@ -1381,34 +1419,26 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
                         if (!(fabs(v.x) <= st.lim) || !(fabs(v.y) <= st.lim))
                             st.out_of_range = 1u;
                     }
+                    par_accum(row, q, blk, vP, vN);
                 }
-                if (inblk) {
-                    if (q < blk + kPB) {  // the next block's prefix
-                        row.preP = row.preP + vP;
-                        row.preN = row.preN + vN;
-                    }
+            }
+        } else {
+            const PStage &P = reinterpret_cast<const PStage &>(G.st[s0]);
 #pragma unroll
-                    for (int jj = 0; jj < kPB; ++jj) {
-                        if (q != blk + jj) {
-                            row.aP[jj] = row.aP[jj] + vP;
-                            row.aN[jj] = row.aN[jj] + vN;
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int jj = 0; jj < kPB; ++jj) {
-                        row.aP[jj] = row.aP[jj] + vP;
-                        row.aN[jj] = row.aN[jj] + vN;
-                    }
+            for (int u = 0; u < kPC; ++u) {
+                const uint32_t q = m.b + u;
+                if (q < d) {
+                    const double2 v = P.i[u][t];
+                    par_accum(row, q, blk, v.x, v.x * v.y);
                 }
             }
         }
         __syncwarp();
         if (lane == 0) t_arrive(&G.empty[s0]);
-        if (m.b + 1 == m.nb) {  // end of pass: the block's messages, scattered to the twins
+        if (m.nb) {  // end of pass: the block's messages, scattered to the twins
 #pragma unroll
             for (int jj = 0; jj < kPB; ++jj) {
-                const uint32_t j = pass * kPB + jj;
+                const uint32_t j = blk + jj;
                 if (j < d) {
                     const double c = row.cb[jj];
                     const double rc = EXACT ? 0.0 : ddiv_rcp(c);
