@@ -189,7 +189,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT,
         "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
         "ms_per_step": res["seconds_per_run"] * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": name, "schedule": args.schedule, "n": system.n,
                    "offdiag_pairs": int(system.pair_v.size), "stop": "||Ax-b||/||b|| < 1e-8"},
         "cpu_baseline": res,
@@ -439,7 +439,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup),
             "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            # the same graph at every N (N > 1: row blocks of it, run_ours_dist)
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, BASELINE config %d)" % args.config,
             "config": {"workload": name, "schedule": sched, "n": n, "directed_edges": E,
                        "stop": "||Ax-b||/||b|| < 1e-8 (epsilon disabled)",
