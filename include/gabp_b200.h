@@ -46,6 +46,10 @@ extern "C" {
 #define GABP_GATHER_SLICE 3     /* slice layout (lane per row): broadcast solve recomputes
                                    m_ji as GABP_GATHER_RECOMPUTE; parallel solve sums the
                                    row's incoming slots and stores to the twin slots */
+#define GABP_GATHER_ROWS 4      /* parallel schedule: warp per row over the CSR order, the
+                                   row's incoming terms in a shared-memory strip, one
+                                   exclusion sum per lane (rows <= 256 edges); the broadcast
+                                   schedule treats it as GABP_GATHER_AUTO */
 
 typedef struct gabp_graph gabp_graph_t;  /* device-resident GaussianGraph */
 typedef struct gabp_state gabp_state_t;  /* device-resident MessageState  */

@@ -24,7 +24,7 @@ GABP_ESINGULAR = -5
 GABP_EDUP = -6
 
 SCHED_IDS = {"parallel": 0, "broadcast": 2}
-GATHER_IDS = {"auto": 0, "message": 1, "recompute": 2, "slice": 3}
+GATHER_IDS = {"auto": 0, "message": 1, "recompute": 2, "slice": 3, "rows": 4}
 
 # every symbol include/gabp_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED = (

@@ -418,7 +418,7 @@ int check_options(const gabp_options_t *opt) {
     if (!(opt->blowup > 1.0)) return fail(GABP_EINVAL, "blowup must exceed 1");
     if (opt->schedule != GABP_SCHED_PARALLEL && opt->schedule != GABP_SCHED_BROADCAST)
         return fail(GABP_EINVAL, "schedule must be parallel (0) or broadcast (2)");
-    if (opt->gather_mode < GABP_GATHER_AUTO || opt->gather_mode > GABP_GATHER_SLICE)
+    if (opt->gather_mode < GABP_GATHER_AUTO || opt->gather_mode > GABP_GATHER_ROWS)
         return fail(GABP_EINVAL, "unknown gather mode %d", opt->gather_mode);
     return GABP_OK;
 }
@@ -427,6 +427,10 @@ int check_slice(const gabp_graph *G, const gabp_options_t *opt) {
     if (opt->gather_mode == GABP_GATHER_SLICE && G->g.nslices == 0)
         return fail(GABP_EINVAL, "graph has no slice layout (max degree %lld)",
                     (long long)G->g.max_degree);
+    if (opt->gather_mode == GABP_GATHER_ROWS && opt->schedule == GABP_SCHED_PARALLEL &&
+        G->g.max_degree > gabp::kRowParMaxDegree)
+        return fail(GABP_EINVAL, "gather mode rows: max degree %lld > %d",
+                    (long long)G->g.max_degree, gabp::kRowParMaxDegree);
     return GABP_OK;
 }
 
@@ -443,6 +447,14 @@ int pick_gather(const gabp_graph *G, const gabp_options_t *opt) {
         // parallel schedule: the slice-group kernel (exclusion sums over the row's
         // contiguous incoming slots, scattered twin stores) on whole graphs with slices
         const bool whole = G->g.row_lo == 0 && G->g.row_hi == G->g.n;
+        if (opt->gather_mode == GABP_GATHER_ROWS) return gabp::kGatherRowParallel;
+        // high-degree rows (config 1: mean 32): warp per row, one exclusion sum per lane
+        // (rowpar.cu, 1.55 ms/sweep against 1.70 for the slice groups, whose later passes
+        // re-stream the row); low degrees stay on the slice groups (degree 4: 1.04 ms
+        // against 15.7 -- a warp per 4-edge row idles 28 lanes)
+        if (opt->gather_mode == GABP_GATHER_AUTO && whole && G->g.n > 0 &&
+            G->g.E >= 24 * G->g.n && G->g.max_degree <= gabp::kRowParMaxDegree)
+            return gabp::kGatherRowParallel;
         if (opt->gather_mode == GABP_GATHER_SLICE ||
             (opt->gather_mode == GABP_GATHER_AUTO && G->g.nslices > 0 && whole))
             return gabp::kGatherSliceParallel;
@@ -837,6 +849,7 @@ gabp_graph *new_graph(int device, int *rc) {
     G->device = device;
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = gabp::prepare_sweep_kernels();
+    if (e == cudaSuccess) e = gabp::prepare_rowpar_kernels();
     if (e == cudaSuccess) e = gabp::prepare_slice_kernels();
     if (e == cudaSuccess) {
         // keep freed blocks in the device pool (graphs, workspaces and build scratch are

@@ -176,8 +176,13 @@ int read_timeline(long long *out, int n);  // GABP_TIMELINE builds only
 // gather: kGatherMessage (twin message msg_old[rev]) or kGatherRecompute (node aggregate of
 // the previous state + recomputation, broadcast schedule in solve mode only)
 enum Gather { kGatherMessage = 0, kGatherRecompute = 1, kGatherSlice = 2,
-              kGatherSliceParallel = 3 };
+              kGatherSliceParallel = 3, kGatherRowParallel = 4 };
 cudaError_t launch_sweep(const SweepArgs &a, int schedule, int mode, int gather, cudaStream_t st);
+// parallel schedule, warp per row over the CSR order (rowpar.cu); rows of at most
+// kRowParMaxDegree edges (the per-warp strip of incoming terms)
+constexpr int kRowParMaxDegree = 256;
+cudaError_t prepare_rowpar_kernels();
+cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st);
 cudaError_t launch_marginals(int64_t n, const uint32_t *row_ptr, const EdgeRec *er,
                              const double *diag, const double *prior_num, const double2 *msg,
                              double *means, double *precs, cudaStream_t st);

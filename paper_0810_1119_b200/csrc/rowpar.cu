@@ -1,0 +1,404 @@
+// rowpar.cu -- the parallel schedule (solver.py:146-173, the reference's default) as a
+// warp-per-row sweep over the CSR edge order.
+//
+// The exclusion sum of edge i -> j is P_i\j = A_ii + sum_{k != j} P_ki, accumulated in
+// ascending k (np.add.at over excl_pos, solver.py:149-150).  Bitwise parity forbids the
+// subtraction trick of the broadcast schedule, so a row of degree d costs d (d - 1) adds.
+// A lane per row (slice.cu: slice_kernel_par) must keep the row's incoming terms in
+// registers and re-streams them once per block of outgoing edges; here the row's
+// incoming terms sit once in a per-warp shared-memory strip and the d exclusion sums run
+// in parallel, lane j walking the strip with one broadcast load per term and skipping
+// k == j by predicate.  Per row:
+//
+//   load     lanes over the row's edge slots (coalesced): EdgeRec {rev, col, A_ij}, own
+//            message m_ij of S_{s-1} (change statistic), twin message m_ji = msg[rev]
+//            (one gathered sector), x_j^{(s-2)} (residual, L2-resident)
+//   strip    T[q] = {P_qi, P_qi * mu_qi} (product rounded first, solver.py:148), padded
+//            to a multiple of 8 with {-0, -0} (x + (-0) == x for every x: the exact
+//            identity, so the walk has no tail)
+//   walk     lane j: p = A_ii, n = A_ii mu_ii; p += T[k].P, n += T[k].N for k != j
+//            (rows of 33..64 edges: two sums per lane over one walk)
+//   edge     P_ij = -A_ij^2 / P_i\j, mu_ij = N_i\j / A_ij (solver.py:155-156), coalesced
+//            store, max |dP|, |dmu|, blow-up test, first singular edge
+//   node     lane d-1 holds the full sum (its exclusion sum + its own term, the same
+//            additions in the same order): marginal x_i^{(s-1)} = N_i / P_i; residual row
+//            of x^{(s-2)} from a warp reduction (the residual is compared to 1e-9, not bits)
+//
+// Launch protocol, statistics and decision: exactly those of the CSR tile kernel
+// (sweep.cu, sweep_epilogue with LAG 0), so the solve loop and controller are unchanged.
+#include <float.h>
+#include <math.h>
+
+#include "sweep_common.cuh"
+
+namespace gabp {
+namespace {
+
+constexpr int kRThreads = 256;
+constexpr int kRWarps = kRThreads / 32;
+constexpr int kRStrip = kRowParMaxDegree + 8;
+
+struct RowSmem {
+    double2 T[kRWarps][kRStrip];
+    TailSmem<kRWarps> tail;
+    int64_t sweep;
+    int skip;
+};
+
+struct RowCtx {
+    const double2 *min_;  // S_{s-1}
+    const double *xprev;  // x^{(s-2)} (residual)
+    double2 *mout;        // S_s
+    double *xcur, *pcur, *xh;
+    bool resid;
+    uint64_t pol;         // L2 evict-first
+};
+
+// Streams (edge records, own old messages, twin gathers, new messages) are touched once per
+// sweep: L2 evict-first, so the L2-resident x^{(s-2)} gathers of the residual stay cached.
+__device__ __forceinline__ uint64_t pol_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int4 ld_ef_i4(const void *ptr, uint64_t pol) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(ptr), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double2 ld_ef_d2(const double2 *ptr, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(ptr), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_ef_d2(double2 *ptr, double2 v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;"
+                 ::"l"(ptr), "d"(v.x), "d"(v.y), "l"(pol)
+                 : "memory");
+}
+
+__device__ __forceinline__ EdgeRec er_of(int4 v) {
+    EdgeRec r;
+    r.rev = (uint32_t)v.x;
+    r.col = (uint32_t)v.y;
+    r.coeff = __hiloint2double(v.w, v.z);
+    return r;
+}
+__device__ __forceinline__ EdgeRec ld_er_cs(const EdgeRec *p) {
+    return er_of(__ldcs(reinterpret_cast<const int4 *>(p)));
+}
+__device__ __forceinline__ EdgeRec ld_er(const EdgeRec *p) {
+    return er_of(__ldg(reinterpret_cast<const int4 *>(p)));
+}
+
+template <int MODE>
+__device__ __forceinline__ void row_node(const SweepArgs &a, const RowCtx &x, uint32_t i,
+                                         double sp, double sn, Stats &st) {
+    bool ok;
+    double xi = ddiv_fast(sn, sp, ok);  // infer_marginals of the state read (solver.py:286)
+    if (!ok) xi = div_slow(sn, sp);
+    if (MODE == kModeSolve) {
+        x.xcur[i] = xi;
+        x.pcur[i] = sp;
+        if (!(fabs(xi) <= DBL_MAX)) st.means_bad = 1u;
+        if (x.xh) x.xh[i] = xi;
+    }
+}
+
+__device__ __forceinline__ void edge_out(const RowCtx &x, uint32_t e, double c, double pe,
+                                         double num, double2 old, Stats &st) {
+    bool okp, okm;
+    double np_ = ddiv_fast(-c * c, pe, okp);
+    double nm = ddiv_fast(num, c, okm);
+    if (!okp) np_ = div_slow(-c * c, pe);
+    if (!okm) nm = div_slow(num, c);
+    st_ef_d2(x.mout + e, make_double2(np_, nm), x.pol);
+    st.edge(e, pe, np_, nm, old);
+}
+
+// One row of the warp's stream, first 64 edge slots in registers (lane l: slots l, l + 32).
+struct RowPre {
+    uint32_t i = 0, e0 = 0, d = 0;
+    double2 nd = make_double2(0.0, 0.0);  // {A_ii, A_ii mu_ii}
+    int4 er[2];                           // EdgeRec {rev, col, A_ij} as loaded
+};
+
+__device__ __forceinline__ void pre_load(const SweepArgs &a, RowPre &r, uint32_t i, uint32_t e0,
+                                         uint32_t e1, int lane, uint64_t pol) {
+    r.i = i;
+    r.e0 = e0;
+    r.d = e1 - e0;
+    r.nd = __ldg(reinterpret_cast<const double2 *>(a.nd + i));
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const uint32_t q = lane + 32 * u;
+        r.er[u] = q < r.d ? ld_ef_i4(a.er + e0 + q, pol) : make_int4(0, 0, 0, 0);
+    }
+}
+
+// The row being gathered: its twin messages, x_j, own old messages in flight.
+struct RowGat {
+    uint32_t i = 0, e0 = 0, d = 0;
+    double2 nd = make_double2(0.0, 0.0);
+    double c[2];     // A_ij
+    double2 o[2];    // own message of S_{s-1}
+    double2 in[2];   // twin message m_ji of S_{s-1}
+    double xg[2];    // x_j^{(s-2)}
+};
+
+__device__ __forceinline__ void gat_issue(const SweepArgs &a, const RowCtx &x, const RowPre &p,
+                                          RowGat &g, int lane) {
+    g.i = p.i;
+    g.e0 = p.e0;
+    g.d = p.d;
+    g.nd = p.nd;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const uint32_t q = lane + 32 * u;
+        const EdgeRec r = er_of(p.er[u]);
+        g.c[u] = r.coeff;
+        g.o[u] = make_double2(0.0, 0.0);
+        g.in[u] = make_double2(0.0, 0.0);
+        g.xg[u] = 0.0;
+        if (q < p.d && p.d <= 64) {
+            g.o[u] = ld_ef_d2(x.min_ + p.e0 + q, x.pol);
+            g.in[u] = ld_ef_d2(x.min_ + r.rev, x.pol);
+            if (x.resid) g.xg[u] = __ldcg(x.xprev + r.col);
+        }
+    }
+}
+
+// Walk of a row of at most 32 R edges whose strip is filled.
+template <int R, int MODE>
+__device__ __forceinline__ void row_walk(const SweepArgs &a, const RowCtx &x, const double2 *T,
+                                         const RowGat &g, int lane, Stats &st) {
+    const uint32_t d = g.d, dpad = (d + 7u) & ~7u;
+    double p[R], n[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+        p[u] = g.nd.x;
+        n[u] = g.nd.y;
+    }
+    // lane j reads T[t + (t >= j)]: terms 0..j-1, then j+1..dpad (T[dpad] is a {-0, -0}
+    // pad), so the skip is an address select off the dependent add chain (a predicated add
+    // compiles to add + 2 selects on the chain)
+    for (uint32_t t = 0; t < dpad; t += 8) {
+        const double2 *b0 = T + t, *b1 = T + t + 1;
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const int jt = lane + 32 * u - (int)t;  // lane's own slot relative to the block
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double2 v = (jt > k ? b0 : b1)[k];
+                p[u] = p[u] + v.x;
+                n[u] = n[u] + v.y;
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+        const uint32_t j = lane + 32 * u;
+        if (j < d) {
+            edge_out(x, g.e0 + j, g.c[u], p[u], n[u], g.o[u], st);
+            if (j == d - 1)  // full sums: the last exclusion sum plus the last term
+                row_node<MODE>(a, x, g.i, p[u] + g.in[u].x, n[u] + g.in[u].x * g.in[u].y, st);
+        }
+    }
+}
+
+// Strip fill, walk and node work of a gathered row of at most 64 edges.
+template <int MODE>
+__device__ __forceinline__ void row_fast(const SweepArgs &a, const RowCtx &x, double2 *T,
+                                         const RowGat &g, int lane, Stats &st) {
+    const uint32_t d = g.d, dpad = (d + 7u) & ~7u;
+    double yp = 0.0;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const uint32_t q = lane + 32 * u;
+        if (q < d) {
+            T[q] = make_double2(g.in[u].x, g.in[u].x * g.in[u].y);  // (prec * mean)
+            if (x.resid) yp = yp + g.c[u] * g.xg[u];
+        } else if (q <= dpad) {
+            T[q] = make_double2(-0.0, -0.0);
+        }
+    }
+    if (dpad == 64 && lane == 0) T[64] = make_double2(-0.0, -0.0);
+    __syncwarp();
+    if (d <= 32)
+        row_walk<1, MODE>(a, x, T, g, lane, st);
+    else
+        row_walk<2, MODE>(a, x, T, g, lane, st);
+    __syncwarp();  // the strip is rewritten by the next row
+    if (d == 0 && lane == 0) row_node<MODE>(a, x, g.i, g.nd.x, g.nd.y, st);
+    if (x.resid) {
+        yp = warp_sum(yp);
+        if (lane == 0) {
+            const double y = g.nd.x * __ldg(x.xprev + g.i) + yp;
+            const double res = y - __ldg(a.rhs + g.i);
+            st.rsq += res * res;
+        }
+    }
+}
+
+// Rows of 65 .. kRowParMaxDegree edges: the strip is filled in rounds of 32 slots and
+// walked in rounds of 32 exclusion sums; the edge's own operands are reloaded.
+template <int MODE>
+__device__ void row_long(const SweepArgs &a, const RowCtx &x, double2 *T, uint32_t i,
+                         uint32_t e0, uint32_t d, NodeRec nd, int lane, Stats &st) {
+    const uint32_t dpad = (d + 7u) & ~7u;
+    double yp = 0.0;
+    for (uint32_t q = lane; q < dpad; q += 32) {
+        if (q < d) {
+            const EdgeRec r = ld_er(a.er + e0 + q);
+            const double2 in = __ldcg(x.min_ + r.rev);
+            T[q] = make_double2(in.x, in.x * in.y);
+            if (x.resid) yp = yp + r.coeff * __ldcg(x.xprev + r.col);
+        } else {
+            T[q] = make_double2(-0.0, -0.0);
+        }
+    }
+    __syncwarp();
+    for (uint32_t jb = 0; jb < d; jb += 32) {
+        const uint32_t j = jb + lane;
+        double p = nd.diag, n = nd.pnum;
+        for (uint32_t t = 0; t < dpad; t += 8) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double2 v = T[t + k];
+                if (t + k != j) {
+                    p = p + v.x;
+                    n = n + v.y;
+                }
+            }
+        }
+        if (j < d) {
+            const double2 own = T[j];
+            edge_out(x, e0 + j, __ldg(&a.er[e0 + j].coeff), p, n, __ldcs(x.min_ + e0 + j), st);
+            if (j == d - 1) row_node<MODE>(a, x, i, p + own.x, n + own.y, st);
+        }
+    }
+    __syncwarp();
+    if (x.resid) {
+        yp = warp_sum(yp);
+        if (lane == 0) {
+            const double y = nd.diag * __ldg(x.xprev + i) + yp;
+            const double res = y - __ldg(a.rhs + i);
+            st.rsq += res * res;
+        }
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kRThreads, 2) rowpar_kernel(const SweepArgs a) {
+    __shared__ RowSmem S;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    Ctrl *ctrl = a.ctrl;
+    if (tid == 0) {
+        if (MODE == kModeSolve) {
+            volatile Ctrl *vc = ctrl;
+            const int64_t s = vc->next_sweep;
+            S.skip = vc->done || s > vc->max_iter + 2;
+            S.sweep = s;
+        } else {
+            S.skip = 0;
+            S.sweep = 1;
+        }
+    }
+    __syncthreads();
+    if (S.skip) return;
+    const int64_t s = S.sweep;
+    RowCtx x;
+    x.resid = (MODE == kModeSolve) && s >= 3;
+    x.min_ = a.msg[(s - 1) % 3];
+    x.xprev = x.resid ? a.x[(s - 2) % 3] : nullptr;
+    x.mout = a.msg[s % 3];
+    x.xcur = (MODE == kModeSolve) ? a.x[(s - 1) % 3] : nullptr;
+    x.pcur = (MODE == kModeSolve) ? a.p[(s - 1) % 3] : nullptr;
+    x.xh = (MODE == kModeSolve && a.xhist && s >= 2 && s - 1 <= a.xhist_rows)
+               ? a.xhist + (s - 2) * a.n : nullptr;
+    x.pol = pol_evict_first();
+    Stats st;
+    st.lim = (MODE == kModeSolve) ? fmin(ctrl->blowup, DBL_MAX) : DBL_MAX;
+    double2 *T = S.T[warp];
+
+    // The swept rows (a rank's owned block, [first tile row, last tile row)) are cut into
+    // one contiguous range per warp.  Software pipeline over the warp's rows: while row i
+    // walks, the gathers of row i+1 and the edge records of row i+2 are in flight.
+    const uint32_t r_lo = __ldg(&a.tile_info[0].x);
+    const uint32_t r_hi = __ldg(&a.tile_info[a.ntiles - 1].y);
+    const int64_t nw = (int64_t)gridDim.x * kRWarps, gw = (int64_t)blockIdx.x * kRWarps + warp;
+    const uint32_t rb = r_lo + (uint32_t)(((int64_t)(r_hi - r_lo) * gw) / nw);
+    const uint32_t re = r_lo + (uint32_t)(((int64_t)(r_hi - r_lo) * (gw + 1)) / nw);
+    if (rb < re) {
+        RowPre pb, pc;
+        RowGat ga, gb;
+        uint32_t ep = __ldg(a.row_ptr + rb);
+        uint32_t e1 = __ldg(a.row_ptr + rb + 1);
+        pre_load(a, pb, rb, ep, e1, lane, x.pol);
+        gat_issue(a, x, pb, ga, lane);
+        uint32_t rp2 = rb + 2 <= re ? __ldg(a.row_ptr + rb + 2) : 0u;
+        if (rb + 1 < re) pre_load(a, pb, rb + 1, e1, rp2, lane, x.pol);
+        uint32_t rp3 = rb + 3 <= re ? __ldg(a.row_ptr + rb + 3) : 0u;
+        for (uint32_t i = rb; i < re; ++i) {
+            if (i + 1 < re) gat_issue(a, x, pb, gb, lane);  // gathers of row i+1
+            if (i + 2 < re) {                               // edge records of row i+2
+                pre_load(a, pc, i + 2, rp2, rp3, lane, x.pol);
+                rp2 = rp3;
+                rp3 = i + 4 <= re ? __ldg(a.row_ptr + i + 4) : 0u;
+            }
+            if (ga.d <= 64) {
+                row_fast<MODE>(a, x, T, ga, lane, st);
+            } else {
+                NodeRec nd;
+                nd.diag = ga.nd.x;
+                nd.pnum = ga.nd.y;
+                row_long<MODE>(a, x, T, ga.i, ga.e0, ga.d, nd, lane, st);
+            }
+            ga = gb;
+            pb = pc;
+        }
+    }
+    __syncthreads();
+    sweep_epilogue<kRThreads, MODE, 0>(S.tail, a, s, x.resid, st, tid);
+}
+
+int g_row_grid[2] = {0, 0};
+
+}  // namespace
+
+cudaError_t prepare_rowpar_kernels() {
+    int dev = 0, sms = 0;
+    cudaError_t e;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+        return e;
+    int occ = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpar_kernel<kModeSolve>,
+                                                           kRThreads, 0)) != cudaSuccess)
+        return e;
+    g_row_grid[kModeSolve] = sms * (occ > 0 ? occ : 1);
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpar_kernel<kModeSingle>,
+                                                           kRThreads, 0)) != cudaSuccess)
+        return e;
+    g_row_grid[kModeSingle] = sms * (occ > 0 ? occ : 1);
+    return cudaSuccess;
+}
+
+cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st) {
+    if (a.ntiles <= 0) return cudaSuccess;
+    const int m = mode == kModeSolve ? kModeSolve : kModeSingle;
+    int64_t grid = g_row_grid[m] > 0 ? g_row_grid[m] : 148 * 4;
+    const int64_t need = (a.ntiles + kRWarps - 1) / kRWarps;
+    if (grid > need) grid = need;
+    if (m == kModeSolve)
+        rowpar_kernel<kModeSolve><<<(unsigned)grid, kRThreads, 0, st>>>(a);
+    else
+        rowpar_kernel<kModeSingle><<<(unsigned)grid, kRThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace gabp

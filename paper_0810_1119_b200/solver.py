@@ -50,7 +50,7 @@ class SolveOptions:
     sweeps_per_poll: int = 0                # sweeps per CUDA-graph chunk; 0 = auto
     device: int | None = None
     record_means_history: bool | None = None  # None: auto (n * max_iter <= 2^24)
-    gather_mode: str = "auto"   # auto | message | recompute | slice (bitwise-identical)
+    gather_mode: str = "auto"   # auto | message | recompute | slice | rows (bitwise-identical)
 
     def __post_init__(self):
         if self.epsilon <= 0.0:
@@ -63,7 +63,7 @@ class SolveOptions:
             raise ValueError(f"schedule must be one of {SCHEDULES}")
         if self.gather_mode not in _lib.GATHER_IDS:
             raise ValueError(f"gather_mode must be one of {tuple(_lib.GATHER_IDS)}")
-        if self.gather_mode == "slice" and self.schedule == "serial":
+        if self.gather_mode in ("slice", "rows") and self.schedule == "serial":
             raise ValueError("the slice layout runs the synchronous schedules")
 
 

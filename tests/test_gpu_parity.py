@@ -580,6 +580,58 @@ def test_skewed_degrees_fall_back_to_tiles():
     np.testing.assert_array_equal(r.means, orc.means)
 
 
+def _degree_ladder_system(seed=11):
+    """Stars of every degree class the warp-per-row kernel distinguishes (0, 1..32 in one
+    register slot per lane, 33..64 in two, 65..256 through the strip rounds), hubs joined
+    by a chain so the graph is connected, diagonally dominant."""
+    rng = np.random.default_rng(seed)
+    degs = [1, 2, 7, 8, 9, 31, 32, 33, 40, 63, 64, 65, 100, 128, 200, 255]
+    pairs, nxt, hubs = {}, 0, []
+    for d in degs:
+        h = nxt
+        hubs.append(h)
+        for k in range(1, d + 1):
+            pairs[(h, h + k)] = rng.uniform(-1, 1)
+        nxt = h + d + 1
+    for a, b in zip(hubs[:-1], hubs[1:]):
+        pairs[(a + 1, b + 1)] = rng.uniform(-1, 1)
+    n = nxt + 5  # trailing isolated nodes
+    pi = np.array([p[0] for p in pairs], dtype=np.int64)
+    pj = np.array([p[1] for p in pairs], dtype=np.int64)
+    pv = np.array(list(pairs.values()))
+    absrow = np.zeros(n)
+    np.add.at(absrow, pi, np.abs(pv))
+    np.add.at(absrow, pj, np.abs(pv))
+    diag = 1.3 * absrow + (absrow == 0)
+    return G.SymSystem.from_pairs(diag, pi, pj, pv, rng.standard_normal(n))
+
+
+@pytest.mark.parametrize("sweep_cap", [1, 2, 3, 5, 60])
+def test_parallel_rows_kernel_degree_ladder(sweep_cap):
+    """Warp-per-row parallel kernel (rowpar.cu) on every degree class, stopped after each
+    of the first sweeps (messages, change history, marginals of every launch kind) and at
+    convergence: bitwise equal to the oracle."""
+    s = _degree_ladder_system()
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    orc = oracle.solve(og, epsilon=1e-12, max_iter=sweep_cap, schedule="parallel")
+    r = G.solve(s, G.SolveOptions(schedule="parallel", epsilon=1e-12, max_iter=sweep_cap,
+                                  gather_mode="rows"))
+    assert r.iterations == orc.iterations and r.converged == orc.converged
+    np.testing.assert_array_equal(r.means, orc.means)
+    np.testing.assert_array_equal(r.precisions, orc.precisions)
+    np.testing.assert_array_equal(np.asarray(r.max_change_history),
+                                  np.asarray(orc.max_change_history))
+
+
+def test_parallel_rows_kernel_rejects_long_rows():
+    n = 400
+    pi = np.zeros(300, dtype=np.int64)
+    pj = np.arange(1, 301)
+    s = G.SymSystem.from_pairs(np.full(n, 100.0), pi, pj, np.full(300, 0.1), np.ones(n))
+    with pytest.raises(Exception):
+        G.solve(s, G.SolveOptions(schedule="parallel", gather_mode="rows"))
+
+
 @pytest.mark.parametrize("which", ["ragged", "random64k", "poisson2d_200", "golden"])
 def test_parallel_schedule_slice_kernel_bitwise(which):
     """The parallel schedule on the slice groups (exclusion sums over the contiguous
@@ -597,8 +649,10 @@ def test_parallel_schedule_slice_kernel_bitwise(which):
         orc = oracle.solve(og, epsilon=1e-300, max_iter=80, schedule="parallel",
                            rel_residual_tol=1e-8)
         g = G.build_graph(s)
-        for mode in ("slice", "message"):
+        for mode in ("slice", "message", "rows"):
             if mode == "slice" and int(g.info.num_slices) == 0:
+                continue
+            if mode == "rows" and int(g.info.max_degree) > 256:
                 continue
             r = G.solve_graph(g, G.SolveOptions(schedule="parallel", epsilon=1e-300,
                                                 max_iter=80, rel_residual_tol=1e-8,
