@@ -183,7 +183,7 @@ def run_reference(args):
     probe = cpu_run(system, 1, 0, args.cpu_sample_sweeps, args.schedule)
     per = probe["seconds_per_run"]
     steps = max(1, min(steps, int(120.0 / max(per, 1e-3))))
-    warmup = min(warmup, 2)
+    warmup = max(0, min(warmup, int(60.0 / max(per, 1e-3))))  # W as asked, within ~1 min
     res = cpu_run(system, steps, warmup, args.cpu_sample_sweeps, args.schedule)
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT,
