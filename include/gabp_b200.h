@@ -173,6 +173,16 @@ int gabp_sweep(const gabp_graph_t *g, gabp_state_t *s, int32_t schedule, double 
 
 /* infer_marginals(graph, state) (solver.py:275-287): means = num / prec_tot
  * (non-finite where prec_tot == 0), precisions = prec_tot. Host outputs, length n. */
+/* One serial sweep (solver.py:176-217 _sweep_serial; replaces the reference's pure-Python
+ * loop): in place on s, nodes in `order` (norder host int64 entries, repeats allowed; NULL =
+ * ascending 0..n-1), each recomputing all its outgoing messages from its current incoming
+ * ones.  Run as dependency levels (tasks on non-adjacent nodes in parallel), bitwise the
+ * sequential loop.  out_of_range = some updated message is non-finite or |v| > blowup;
+ * GABP_ESINGULAR with *singular_edge = the first P_excl == 0 edge in loop order, the state
+ * left unchanged.  Rows of at most 256 edges; whole graphs only. */
+int gabp_sweep_serial(const gabp_graph_t *g, gabp_state_t *s, const int64_t *order,
+                      int64_t norder, double blowup, double *max_change, int32_t *out_of_range,
+                      int64_t *singular_edge, int32_t *num_levels);
 int gabp_infer_marginals(const gabp_graph_t *g, const gabp_state_t *s, double *h_means,
                          double *h_precs);
 

@@ -13,6 +13,8 @@
  *   parallel      solver.py:146-173 _sweep_parallel: exclusion sums accumulated in
  *                                  ascending-k order (np.add.at over excl_edge)
  *   broadcast     solver.py:232-272 broadcast_sweep: node aggregate then subtraction
+ *   serial        solver.py:176-217 _sweep_serial: in place, node by node in the given
+ *                                  order (sequential; single thread)
  *   marginals     solver.py:275-287 infer_marginals
  *   residual      linalg.py:285-288 residual_norm_per_eq (row-wise summation order;
  *                                  the reference sums in dict order -> differs in
@@ -185,6 +187,48 @@ void oracle_sweep_parallel(int64_t n, const int64_t *row_ptr, const int64_t *col
     out->max_change = mc;
     out->singular = sing == INT64_MAX ? -1 : sing;
     out->singular_is_node = 0;
+}
+
+/* _sweep_serial (solver.py:176-217): in place, nodes in `order` (NULL = 0..n-1); node i
+ * recomputes every outgoing message from its current incoming ones (exclusion sums in
+ * ascending neighbour order, solver.py:188-197).  Stops at the first P_excl == 0 edge in
+ * loop order (the reference raises there) and reports it. */
+void oracle_sweep_serial(int64_t n, const int64_t *row_ptr, const int64_t *rev,
+                         const double *coeff, const double *prior_prec, const double *prior_num,
+                         double *prec, double *mean, const int64_t *order, int64_t norder,
+                         orc_sweep_out *out) {
+    double mc = 0.0;
+    out->singular = -1;
+    out->singular_is_node = 0;
+    if (!order) norder = n;
+    for (int64_t t = 0; t < norder; ++t) {
+        const int64_t i = order ? order[t] : t;
+        const int64_t s = row_ptr[i], u = row_ptr[i + 1];
+        for (int64_t e = s; e < u; ++e) {
+            double acc_p = prior_prec[i];
+            double acc_num = prior_num[i];
+            for (int64_t q = s; q < u; ++q) {
+                if (q == e) continue;
+                const int64_t r = rev[q]; /* incoming edge (k -> i), current value */
+                acc_p += prec[r];
+                acc_num += prec[r] * mean[r];
+            }
+            if (acc_p == 0.0) {
+                out->singular = e;
+                out->max_change = mc;
+                return;
+            }
+            const double c = coeff[e];
+            const double np_ = -c * c / acc_p;
+            const double nm = acc_num / c;
+            const double dp = fabs(np_ - prec[e]), dm = fabs(nm - mean[e]);
+            if (dp > mc) mc = dp; /* solver.py:204-207: plain '>' (NaN never wins) */
+            if (dm > mc) mc = dm;
+            prec[e] = np_;
+            mean[e] = nm;
+        }
+    }
+    out->max_change = mc;
 }
 
 /* node aggregates shared by broadcast_sweep (solver.py:240-243) and infer_marginals

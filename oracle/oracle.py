@@ -143,6 +143,63 @@ def sweep(g: OracleGraph, prec, mean, schedule: str = "parallel"):
     return po, mo, float(out.max_change), int(out.singular)
 
 
+def sweep_serial(g: OracleGraph, prec, mean, order=None):
+    """solver.py:176-217 on copies: (prec', mean', max_change, singular edge | -1)."""
+    po = np.array(prec, dtype=np.float64, copy=True)
+    mo = np.array(mean, dtype=np.float64, copy=True)
+    out = _SweepOut()
+    if order is None:
+        optr, norder = None, 0
+    else:
+        o = np.ascontiguousarray(order, dtype=np.int64)
+        optr, norder = _p64(o), o.size
+    lib().oracle_sweep_serial(ctypes.c_int64(g.n), _p64(g.row_ptr), _p64(g.rev), _pf(g.coeff),
+                              _pf(g.diag), _pf(g.prior_num), _pf(po), _pf(mo), optr,
+                              ctypes.c_int64(norder), ctypes.byref(out))
+    return po, mo, float(out.max_change), int(out.singular)
+
+
+def solve_serial(g: OracleGraph, epsilon=1e-6, max_iter=10_000, blowup=1e10, order=None,
+                 rel_residual_tol=None) -> "OracleReport":
+    """solver.py:307-346 with the serial schedule (+ optional relative-residual stop)."""
+    E = g.num_edges
+    prec = np.zeros(E)
+    mean = np.zeros(E)
+    bnorm = float(np.linalg.norm(g.rhs))
+    ch, rh = [], []
+    converged = diverged = False
+    it = 0
+    for _ in range(max_iter):
+        p2, m2, mc, sing = sweep_serial(g, prec, mean, order)
+        if sing >= 0:
+            diverged = True
+            break
+        prec, mean = p2, m2
+        it += 1
+        means, _ = marginals(g, prec, mean)
+        finite_means = bool(np.all(np.isfinite(means)))
+        res = float(np.sqrt(residual_sq(g, means)) / g.n) if finite_means else np.inf
+        ch.append(mc)
+        rh.append(res)
+        with np.errstate(all="ignore"):
+            biggest = max(float(np.max(np.abs(prec), initial=0.0)),
+                          float(np.max(np.abs(mean), initial=0.0)))
+        finite = bool(np.all(np.isfinite(prec)) and np.all(np.isfinite(mean)))
+        if not finite or biggest > blowup or not finite_means:
+            diverged = True
+            break
+        if mc < epsilon:
+            converged = True
+            break
+        if rel_residual_tol and res * g.n < rel_residual_tol * bnorm:
+            converged = True
+            break
+    if not converged and not diverged:
+        diverged = True
+    means, precs = marginals(g, prec, mean)
+    return OracleReport(converged, diverged, it, means, precs, np.array(ch), np.array(rh))
+
+
 def marginals(g: OracleGraph, prec, mean):
     prec = np.ascontiguousarray(prec, dtype=np.float64)
     mean = np.ascontiguousarray(mean, dtype=np.float64)

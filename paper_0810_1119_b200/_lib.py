@@ -35,7 +35,7 @@ EXPORTED = (
     "gabp_graph_stream",
     "gabp_state_create", "gabp_state_clone", "gabp_state_destroy", "gabp_state_reset",
     "gabp_state_read", "gabp_state_write", "gabp_state_counters",
-    "gabp_sweep", "gabp_infer_marginals",
+    "gabp_sweep", "gabp_sweep_serial", "gabp_infer_marginals",
     "gabp_solve", "gabp_solve_device", "gabp_solve_system", "gabp_residual_norm_per_eq",
     "gabp_bench_sweeps", "gabp_graph_create_ex", "gabp_nccl_unique_id", "gabp_dist_attach",
     "gabp_dist_solve_local", "gabp_dist_results",
@@ -132,6 +132,10 @@ def load():
                                              ctypes.POINTER(Options), _vp, _vp, _vp, _vp,
                                              ctypes.POINTER(Report)]),
         "gabp_residual_norm_per_eq": (ctypes.c_int, [_vp, _vp, _dp]),
+        "gabp_sweep_serial": (ctypes.c_int, [_vp, _vp, _vp, _i64, ctypes.c_double, _dp,
+                                             ctypes.POINTER(ctypes.c_int32),
+                                             ctypes.POINTER(ctypes.c_int64),
+                                             ctypes.POINTER(ctypes.c_int32)]),
         "gabp_bench_sweeps": (ctypes.c_int, [_vp, _i32, _i32, _i64, _dp]),
         "gabp_graph_create_ex": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
                                                 _i32, ctypes.POINTER(_vp)]),

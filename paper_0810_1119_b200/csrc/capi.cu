@@ -3,6 +3,7 @@
 // convergence test of the sweep two launches back (gabp_internal.cuh, Ctrl), so the
 // host only enqueues CUDA-graph chunks of sweeps and polls one flag per chunk, one
 // chunk ahead -- no per-sweep host synchronisation.
+#include <float.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -129,6 +130,12 @@ struct gabp_graph {
     int64_t Kp = 0;                  // padded dimension (multiple of 32)
     uint2 *dpairs = nullptr;         // tile pairs of the pair-tile kernel
     int64_t dnpairs = 0;
+    // serial schedule: dependency levels of the last order (gabp_sweep_serial)
+    bool serial_valid = false, serial_ascending = false;
+    std::vector<int64_t> serial_order;
+    std::vector<int64_t> serial_lvl;       // task offsets per level
+    uint2 *d_serial = nullptr;             // tasks {node, order position}, level by level
+    std::vector<uint32_t> h_rp, h_col;     // host CSR (level build)
 };
 
 struct gabp_state {
@@ -1049,6 +1056,7 @@ static void graph_release(gabp_graph *G) {
     if (G->refs.fetch_sub(1) != 1) return;
     cudaSetDevice(G->device);
     cudaStreamSynchronize(G->stream);
+    if (G->d_serial) cudaFree(G->d_serial);
     release_workspace(G);
     gabp::free_graph(G->g, G->stream);
     cudaStreamSynchronize(G->stream);
@@ -1207,6 +1215,125 @@ int gabp_state_counters(const gabp_state_t *S, int64_t *iteration, int64_t *mess
     if (!S) return fail(GABP_EINVAL, "NULL state");
     if (iteration) *iteration = S->iteration;
     if (messages_sent) *messages_sent = S->messages_sent;
+    return GABP_OK;
+}
+
+// ---- serial schedule (solver.py:176-217) ------------------------------------------------
+// Dependency levels of a task sequence (the order): task t on node i goes one level above
+// the last task on i or on any neighbour of i; tasks of one level touch disjoint messages
+// (rowpar.cu: serial_level_kernel), so levels run in parallel and give the in-place
+// sequential result exactly.  Built on the host from a copy of the CSR, cached per order.
+static int serial_levels(gabp_graph *G, const int64_t *order, int64_t norder) {
+    const int64_t n = G->g.n;
+    const bool asc = order == nullptr;
+    if (asc) norder = n;
+    if (G->serial_valid && G->serial_ascending == asc &&
+        (asc || ((int64_t)G->serial_order.size() == norder &&
+                 memcmp(G->serial_order.data(), order, sizeof(int64_t) * norder) == 0)))
+        return GABP_OK;
+    for (int64_t t = 0; !asc && t < norder; ++t)
+        if (order[t] < 0 || order[t] >= n)
+            return fail(GABP_EINVAL, "serial order entry %lld out of range [0, %lld)",
+                        (long long)order[t], (long long)n);
+    if ((int64_t)G->h_rp.size() != n + 1) {
+        G->h_rp.resize(n + 1);
+        CK(cudaMemcpy(G->h_rp.data(), G->g.row_ptr, sizeof(uint32_t) * (n + 1),
+                      cudaMemcpyDeviceToHost));
+        std::vector<gabp::EdgeRec> er(G->g.E);
+        if (G->g.E)
+            CK(cudaMemcpy(er.data(), G->g.er, sizeof(gabp::EdgeRec) * G->g.E,
+                          cudaMemcpyDeviceToHost));
+        G->h_col.resize(G->g.E);
+        for (int64_t e = 0; e < G->g.E; ++e) G->h_col[e] = er[e].col;
+    }
+    std::vector<uint32_t> last(n, 0u), lev(norder);
+    uint32_t nlev = 0;
+    for (int64_t t = 0; t < norder; ++t) {
+        const int64_t i = asc ? t : order[t];
+        uint32_t L = last[i];
+        for (uint32_t e = G->h_rp[i]; e < G->h_rp[i + 1]; ++e) {
+            const uint32_t k = G->h_col[e];
+            L = last[k] > L ? last[k] : L;
+        }
+        lev[t] = L + 1;
+        last[i] = L + 1;
+        nlev = L + 1 > nlev ? L + 1 : nlev;
+    }
+    G->serial_lvl.assign((size_t)nlev + 1, 0);
+    for (int64_t t = 0; t < norder; ++t) G->serial_lvl[lev[t]]++;
+    for (uint32_t l = 1; l <= nlev; ++l) G->serial_lvl[l] += G->serial_lvl[l - 1];
+    std::vector<int64_t> fill(G->serial_lvl.begin(), G->serial_lvl.end() - 1);
+    std::vector<uint2> tasks(norder > 0 ? norder : 1);
+    for (int64_t t = 0; t < norder; ++t) {
+        const int64_t i = asc ? t : order[t];
+        tasks[fill[lev[t] - 1]++] = make_uint2((uint32_t)i, (uint32_t)t);
+    }
+    if (G->d_serial) cudaFree(G->d_serial);
+    G->d_serial = nullptr;
+    CK(cudaMalloc(&G->d_serial, sizeof(uint2) * tasks.size()));
+    CK(cudaMemcpy(G->d_serial, tasks.data(), sizeof(uint2) * tasks.size(),
+                  cudaMemcpyHostToDevice));
+    G->serial_ascending = asc;
+    if (asc)
+        G->serial_order.clear();
+    else
+        G->serial_order.assign(order, order + norder);
+    G->serial_valid = true;
+    return GABP_OK;
+}
+
+int gabp_sweep_serial(const gabp_graph_t *Gc, gabp_state_t *S, const int64_t *order,
+                      int64_t norder, double blowup, double *max_change, int32_t *out_of_range,
+                      int64_t *singular_edge, int32_t *num_levels) {
+    gabp_graph *G = const_cast<gabp_graph *>(Gc);
+    if (!G || !S || S->g != Gc) return fail(GABP_EINVAL, "state does not belong to graph");
+    if (order && norder < 0) return fail(GABP_EINVAL, "negative order length");
+    if (G->g.row_lo != 0 || G->g.row_hi != G->g.n)
+        return fail(GABP_EINVAL, "serial schedule needs the whole graph");
+    if (G->g.max_degree > gabp::kRowParMaxDegree)
+        return fail(GABP_EINVAL, "serial schedule: max degree %lld > %d",
+                    (long long)G->g.max_degree, gabp::kRowParMaxDegree);
+    CK(cudaSetDevice(G->device));
+    int rc = ensure_workspace(G, 1);
+    if (rc) return rc;
+    rc = serial_levels(G, order, norder);
+    if (rc) return rc;
+    if (singular_edge) *singular_edge = -1;
+    if (max_change) *max_change = 0.0;
+    if (out_of_range) *out_of_range = 0;
+    if (num_levels) *num_levels = (int32_t)(G->serial_lvl.size() - 1);
+    Ctrl c = gabp::fresh_ctrl();
+    *G->h_ctrl = c;
+    CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, G->stream));
+    SweepArgs a = make_args(G);
+    // in place on a copy (solver.py:177-178 works on lists made from the state): a sweep
+    // that meets a singular exclusion sum leaves the state as it was, like the reference
+    double2 *msg = S->buf[S->cur ^ 1];
+    if (G->g.E)
+        CK(cudaMemcpyAsync(msg, S->buf[S->cur], sizeof(double2) * G->g.E,
+                           cudaMemcpyDeviceToDevice, G->stream));
+    const double lim = blowup < DBL_MAX ? blowup : DBL_MAX;
+    for (size_t l = 0; l + 1 < G->serial_lvl.size(); ++l)
+        CK(gabp::launch_serial_level(a, msg, G->d_serial + G->serial_lvl[l],
+                                     G->serial_lvl[l + 1] - G->serial_lvl[l], lim, G->stream));
+    CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, G->stream));
+    CK(cudaStreamSynchronize(G->stream));
+    const Ctrl &h = *G->h_ctrl;
+    if (h.singular_min[1] != gabp::kNoIndex) {
+        const int64_t e = (int64_t)(h.singular_min[1] & 0xffffffffull);
+        if (singular_edge) *singular_edge = e;
+        return fail(GABP_ESINGULAR, "P_excl = 0 on edge %lld", (long long)e);
+    }
+    S->cur ^= 1;
+    S->iteration += 1;
+    S->messages_sent += G->g.E;
+    if (out_of_range) *out_of_range = h.msg_nonfinite[1] ? 1 : 0;
+    if (max_change) {
+        double v;
+        unsigned long long bits = h.change_bits[1];
+        memcpy(&v, &bits, sizeof(v));
+        *max_change = v;
+    }
     return GABP_OK;
 }
 

@@ -366,6 +366,80 @@ __global__ void __launch_bounds__(kRThreads, 2) rowpar_kernel(const SweepArgs a)
     sweep_epilogue<kRThreads, MODE, 0>(S.tail, a, s, x.resid, st, tid);
 }
 
+
+// ---- serial schedule (solver.py:176-217) as dependency levels ------------------------------
+// The reference updates node by node in a given order, in place: node i recomputes all its
+// outgoing messages m_ij from its current incoming messages m_ki.  Two tasks interact only
+// when they are on the same node or on adjacent nodes (i reads m_ki that k writes, and k
+// reads m_ik that i writes), so tasks grouped into dependency levels (level(t) = 1 + the
+// highest level of an earlier task on node(t) or a neighbour; capi.cu: serial_levels) and
+// run level after level give the sequential result bit for bit: a task sees exactly the
+// messages the sequential loop would show it.  One launch per level, a warp per task; the
+// task's d exclusion sums run one per lane as in rowpar_kernel (rows <= 256 edges).
+__global__ void __launch_bounds__(kRThreads, 2) serial_level_kernel(const SweepArgs a,
+                                                                   double2 *msg,
+                                                                   const uint2 *tasks,
+                                                                   int64_t cnt, double lim) {
+    __shared__ RowSmem S;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double2 *T = S.T[warp];
+    Stats st;
+    st.lim = lim;
+    const int64_t nw = (int64_t)gridDim.x * kRWarps;
+    for (int64_t w = (int64_t)blockIdx.x * kRWarps + warp; w < cnt; w += nw) {
+        const uint2 tk = __ldg(tasks + w);  // {node, position in the order}
+        const uint32_t i = tk.x;
+        const uint32_t e0 = __ldg(a.row_ptr + i), d = __ldg(a.row_ptr + i + 1) - e0;
+        const double2 nd = __ldg(reinterpret_cast<const double2 *>(a.nd + i));
+        const uint32_t dpad = (d + 7u) & ~7u;
+        for (uint32_t q = lane; q < dpad; q += 32) {
+            if (q < d) {
+                const EdgeRec r = ld_er(a.er + e0 + q);
+                const double2 in = __ldcg(msg + r.rev);  // m_ki as the loop would see it
+                T[q] = make_double2(in.x, in.x * in.y);
+            } else {
+                T[q] = make_double2(-0.0, -0.0);
+            }
+        }
+        __syncwarp();
+        for (uint32_t jb = 0; jb < d; jb += 32) {
+            const uint32_t j = jb + lane;
+            double p = nd.x, n = nd.y;
+            for (uint32_t t = 0; t < dpad; t += 8) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double2 v = T[t + k];
+                    if (t + k != j) {
+                        p = p + v.x;
+                        n = n + v.y;
+                    }
+                }
+            }
+            if (j < d) {
+                const uint32_t e = e0 + j;
+                const double c = __ldg(&a.er[e].coeff);
+                const double2 old = __ldcg(msg + e);
+                bool okp, okm;
+                double np_ = ddiv_fast(-c * c, p, okp);
+                double nm = ddiv_fast(n, c, okm);
+                if (!okp) np_ = div_slow(-c * c, p);
+                if (!okm) nm = div_slow(n, c);
+                if (p == 0.0)  // the first in loop order: (order position, edge)
+                    atomicMin(&a.ctrl->singular_min[1],
+                              ((unsigned long long)tk.y << 32) | (unsigned long long)e);
+                __stcg(msg + e, make_double2(np_, nm));
+                const double d1 = fabs(np_ - old.x), d2 = fabs(nm - old.y);
+                st.chg = d1 > st.chg ? d1 : st.chg;
+                st.chg = d2 > st.chg ? d2 : st.chg;
+                if (!(fabs(np_) <= st.lim) || !(fabs(nm) <= st.lim)) st.out_of_range = 1u;
+            }
+        }
+        __syncwarp();  // the strip is rewritten by the next task
+    }
+    __syncthreads();
+    sweep_epilogue<kRThreads, kModeSingle, 0>(S.tail, a, 1, false, st, tid);
+}
+
 int g_row_grid[2] = {0, 0};
 
 }  // namespace
@@ -386,6 +460,16 @@ cudaError_t prepare_rowpar_kernels() {
         return e;
     g_row_grid[kModeSingle] = sms * (occ > 0 ? occ : 1);
     return cudaSuccess;
+}
+
+cudaError_t launch_serial_level(const SweepArgs &a, double2 *msg, const uint2 *tasks,
+                                int64_t cnt, double lim, cudaStream_t st) {
+    if (cnt <= 0) return cudaSuccess;
+    int64_t grid = g_row_grid[kModeSingle] > 0 ? g_row_grid[kModeSingle] : 148 * 2;
+    const int64_t need = (cnt + kRWarps - 1) / kRWarps;
+    if (grid > need) grid = need;
+    serial_level_kernel<<<(unsigned)grid, kRThreads, 0, st>>>(a, msg, tasks, cnt, lim);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st) {

@@ -8,14 +8,16 @@ meaning and error behaviour for the synchronous schedules:
   MessageState      solver.py:57-74   device-resident messages, host copies on access
   SolveReport       solver.py:77-89   (+ device_ms, sweeps_launched, final_rel_residual)
   initial_state     solver.py:92-97
-  sweep             solver.py:220-229 parallel | broadcast
+  sweep             solver.py:220-229 parallel | broadcast | serial
   broadcast_sweep   solver.py:232-272
   infer_marginals   solver.py:275-287
   solve             solver.py:307-346
 
 Every sweep runs in the CUDA library (include/gabp_b200.h); there is no CPU path.
-The "serial" schedule (solver.py:176-217: an in-place Gauss-Seidel-ordered sweep) is
-inherently sequential and outside this synchronous hot path: it raises.
+The "serial" schedule (solver.py:176-217: an in-place, node-ordered sweep) runs as
+dependency levels of the order (gabp_sweep_serial: tasks on non-adjacent nodes in
+parallel, bitwise the sequential loop); its solve loop is the reference's, driven from the
+host one sweep at a time (solver.py:307-346), the other schedules solve on the device.
 """
 
 from __future__ import annotations
@@ -30,7 +32,7 @@ from .graph import GaussianGraph, build_graph
 from .linalg import SymSystem
 
 SCHEDULES = ("parallel", "serial", "broadcast")
-GPU_SCHEDULES = ("parallel", "broadcast")
+GPU_SCHEDULES = ("parallel", "broadcast")  # device solve loop (gabp_solve)
 _AUTO_MEANS_HISTORY_DOUBLES = 1 << 24
 
 
@@ -190,8 +192,46 @@ def _sweep(graph: GaussianGraph, state: MessageState, schedule: str):
     return out, float(mc.value)
 
 
+def _order_arg(order):
+    if order is None:
+        return None, 0, None
+    arr = np.ascontiguousarray(np.asarray(order, dtype=np.int64).reshape(-1))
+    return arr, int(arr.size), arr.ctypes.data_as(ctypes.c_void_p)
+
+
+def _serial_inplace(graph: GaussianGraph, state: MessageState, order_arg, blowup: float):
+    """One serial sweep in place on `state`: (max change, out of range, levels)."""
+    _, norder, optr = order_arg
+    mc = ctypes.c_double()
+    oor = ctypes.c_int32()
+    se = ctypes.c_int64()
+    nl = ctypes.c_int32()
+    rc = _lib.load().gabp_sweep_serial(graph.handle, state.handle, optr, norder, blowup,
+                                       ctypes.byref(mc), ctypes.byref(oor), ctypes.byref(se),
+                                       ctypes.byref(nl))
+    if rc == _lib.GABP_ESINGULAR:
+        k = int(se.value)
+        raise SingularSubgraphError(f"P_excl({int(graph.src[k])} -> {int(graph.dst[k])}) = 0")
+    _lib.check(rc)
+    return float(mc.value), bool(oor.value), int(nl.value)
+
+
+def _sweep_serial(graph: GaussianGraph, state: MessageState, order):
+    """solver.py:176-217: in-place node-ordered round on a copy of the state."""
+    out = state.copy()
+    out.schedule = "serial"
+    try:
+        mc, _, _ = _serial_inplace(graph, out, _order_arg(order), float("inf"))
+    except BaseException:
+        out.close()
+        raise
+    return out, mc
+
+
 def sweep(graph: GaussianGraph, state: MessageState, options: SolveOptions):
     """One message-passing round; returns (new state, max message change)."""
+    if options.schedule == "serial":
+        return _sweep_serial(graph, state, options.serial_order)
     return _sweep(graph, state, options.schedule)
 
 
@@ -230,9 +270,74 @@ def _want_means_history(options: SolveOptions, n: int) -> bool:
     return bool(options.record_means_history)
 
 
+def _solve_serial(graph: GaussianGraph, options: SolveOptions) -> SolveReport:
+    """solver.py:307-346 with the serial schedule: one device sweep (dependency levels)
+    per iteration, then the reference's tests on the tentative means (device marginals and
+    residual), the message change and the blow-up / finiteness flags of the sweep."""
+    import time
+    n = graph.n
+    lib = _lib.load()
+    order_arg = _order_arg(options.serial_order)
+    state = initial_state(graph, "serial")
+    want_hist = _want_means_history(options, n)
+    bnorm = float(graph.info.rhs_norm)
+    max_hist, res_hist, means_hist = [], [], []
+    converged = diverged = False
+    res = float("nan")
+    launches = 0
+    t0 = time.perf_counter()
+    try:
+        for _ in range(options.max_iter):
+            try:
+                max_change, out_of_range, levels = _serial_inplace(graph, state, order_arg,
+                                                                   float(options.blowup))
+            except SingularSubgraphError:
+                diverged = True
+                break
+            launches += levels
+            means, _ = infer_marginals(graph, state)
+            means_finite = bool(np.all(np.isfinite(means)))
+            if means_finite:
+                r = ctypes.c_double()
+                _lib.check(lib.gabp_residual_norm_per_eq(graph.handle, _lib.ptr(means),
+                                                         ctypes.byref(r)))
+                res = float(r.value)
+            else:
+                res = float("inf")
+            max_hist.append(max_change)
+            res_hist.append(res)
+            if want_hist:
+                means_hist.append(means)
+            if out_of_range or not means_finite:
+                diverged = True
+                break
+            if max_change < options.epsilon:
+                converged = True
+                break
+            if (options.rel_residual_tol and bnorm > 0.0
+                    and res * n / bnorm < options.rel_residual_tol):
+                converged = True
+                break
+        if not converged and not diverged:
+            diverged = True  # cap exhausted
+        means, precs = infer_marginals(graph, state)
+        return SolveReport(
+            converged=converged, diverged=diverged, iterations=state.iteration,
+            means=means, precisions=precs, max_change_history=max_hist,
+            residual_history=res_hist, means_history=means_hist,
+            messages_sent=state.messages_sent, precisions_exact=graph.is_tree(),
+            device_ms=(time.perf_counter() - t0) * 1e3, sweeps_launched=state.iteration,
+            final_rel_residual=(res * n / bnorm) if bnorm > 0.0 and res_hist else float("nan"),
+            kernel_launches=launches)
+    finally:
+        state.close()
+
+
 def solve_graph(graph: GaussianGraph, options: SolveOptions | None = None) -> SolveReport:
     """solve() on an already built graph (reuses its device workspace)."""
     options = options or SolveOptions()
+    if options.schedule == "serial":
+        return _solve_serial(graph, options)
     n = graph.n
     hist = np.empty((options.max_iter, n)) if _want_means_history(options, n) else None
     o = _options_struct(options, n, hist)
@@ -272,7 +377,8 @@ def solve(system: SymSystem, options: SolveOptions | None = None) -> SolveReport
     are recorded.  Divergence (blowup, non-finite values, a singular exclusion sum, the
     sweep cap) is reported, never raised."""
     options = options or SolveOptions()
-    _gpu_schedule(options.schedule)
+    if options.schedule != "serial":
+        _gpu_schedule(options.schedule)
     graph = build_graph(system, options.device)
     try:
         return solve_graph(graph, options)

@@ -22,3 +22,9 @@ def system(rec):
     from paper_0810_1119_b200.linalg import SymSystem
     return SymSystem.from_pairs(rec["diag"], rec["pair_i"], rec["pair_j"], rec["pair_v"],
                                 rec["rhs"])
+
+
+def load_serial(name):
+    """Serial-schedule fixtures (tests/golden/make_golden_serial.py)."""
+    with np.load(os.path.join(GOLDEN, "serial", f"{name}.npz")) as z:
+        return {k: z[k] for k in z.files}

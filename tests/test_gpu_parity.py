@@ -663,3 +663,84 @@ def test_parallel_schedule_slice_kernel_bitwise(which):
             np.testing.assert_array_equal(r.precisions, orc.precisions)
             np.testing.assert_array_equal(np.asarray(r.max_change_history),
                                           np.asarray(orc.max_change_history))
+
+
+# ---------------------------------------------------------------------------------------
+# serial schedule (solver.py:176-217) as dependency levels (rowpar.cu serial_level_kernel)
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("tag", ["asc", "custom"])
+def test_serial_sweep_trace_vs_reference(case, tag):
+    """Device serial sweeps (ascending order, and a custom order with a repeated and a
+    missing node) bitwise equal to the reference's own in-place loop."""
+    rec = gc.load(case)
+    srec = gc.load_serial(case)
+    g = G.build_graph(gc.system(rec))
+    order = None if tag == "asc" else [int(v) for v in srec["order"]]
+    opts = G.SolveOptions(schedule="serial", serial_order=order)
+    st = G.initial_state(g, "serial")
+    want_p, want_m = srec[f"{tag}_trace_prec"], srec[f"{tag}_trace_mean"]
+    want_c = srec[f"{tag}_trace_change"]
+    for t in range(want_p.shape[0]):
+        st, mc = G.sweep(g, st, opts)
+        np.testing.assert_array_equal(st.prec, want_p[t])
+        np.testing.assert_array_equal(st.mean, want_m[t])
+        assert mc == want_c[t]
+    if int(srec[f"{tag}_trace_singular_at"]) > 0:
+        with pytest.raises(G.SingularSubgraphError):
+            G.sweep(g, st, opts)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_serial_solve_vs_reference(case):
+    rec = gc.load(case)
+    srec = gc.load_serial(case)
+    tol = float(rec["rel_residual_tol"]) or None
+    r = G.solve(gc.system(rec), G.SolveOptions(schedule="serial", epsilon=float(rec["epsilon"]),
+                                               max_iter=int(rec["max_iter"]),
+                                               rel_residual_tol=tol))
+    assert r.converged == bool(srec["serial_converged"])
+    assert r.diverged == bool(srec["serial_diverged"])
+    assert r.iterations == int(srec["serial_iterations"])
+    want = srec["serial_means"]
+    fin = np.isfinite(want)
+    np.testing.assert_array_equal(np.isfinite(r.means), fin)
+    np.testing.assert_array_equal(r.means[fin], want[fin])
+    np.testing.assert_array_equal(r.precisions, srec["serial_precisions"])
+    np.testing.assert_array_equal(np.asarray(r.max_change_history), srec["serial_change_hist"])
+    rh = srec["serial_res_hist"]
+    atol = 1e-12 * float(np.max(rh[np.isfinite(rh)], initial=0.0))
+    np.testing.assert_allclose(np.asarray(r.residual_history), rh, rtol=1e-9, atol=atol)
+
+
+@pytest.mark.parametrize("which", ["random64k", "poisson2d_200", "ladder", "ragged"])
+def test_serial_large_vs_oracle(which):
+    """Many dependency levels and wide levels: device serial solve (ascending and a seeded
+    random order) bitwise equal to the sequential C oracle."""
+    if which == "random64k":
+        s = G.gen_random_sparse(1 << 16, 16, 3).system
+    elif which == "poisson2d_200":
+        s = G.gen_poisson2d(200, 4).system
+    elif which == "ladder":
+        s = _degree_ladder_system()
+    else:
+        s = _ragged_system()
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    rng = np.random.default_rng(7)
+    for order in (None, [int(v) for v in rng.permutation(s.n)]):
+        orc = oracle.solve_serial(og, epsilon=1e-300, max_iter=12, order=order,
+                                  rel_residual_tol=1e-10)
+        r = G.solve(s, G.SolveOptions(schedule="serial", epsilon=1e-300, max_iter=12,
+                                      serial_order=order, rel_residual_tol=1e-10))
+        assert r.iterations == orc.iterations and r.converged == orc.converged
+        np.testing.assert_array_equal(r.means, orc.means)
+        np.testing.assert_array_equal(r.precisions, orc.precisions)
+        np.testing.assert_array_equal(np.asarray(r.max_change_history),
+                                      orc.max_change_history)
+
+
+def test_serial_order_errors():
+    s = G.gen_poisson2d(8, 0).system
+    with pytest.raises(Exception):
+        G.solve(s, G.SolveOptions(schedule="serial", serial_order=[0, 1, s.n]))

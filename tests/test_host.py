@@ -48,9 +48,15 @@ def test_solve_options_validation():
         G.SolveOptions(schedule="bogus")
 
 
-def test_serial_schedule_is_rejected_not_emulated():
+def test_serial_schedule_options():
+    """The serial schedule runs on the device (gabp_sweep_serial, dependency levels); it
+    has no slice / row-kernel gather modes and no device solve-loop options struct."""
+    G.SolveOptions(schedule="serial", serial_order=[2, 0, 1])
+    for mode in ("slice", "rows"):
+        with pytest.raises(ValueError):
+            G.SolveOptions(schedule="serial", gather_mode=mode)
     with pytest.raises(ValueError, match="synchronous"):
-        G.solve(G.load_instance("toy3").system, G.SolveOptions(schedule="serial"))
+        G.solver._gpu_schedule("serial")
 
 
 def test_symsystem_forms_agree():

@@ -180,6 +180,21 @@ def test_steffensen_and_aitken_bitwise_vs_reference(path, sched):
                  f"{sched}_steff_s0")
 
 
+ACCEL_SERIAL = sorted(glob.glob(os.path.join(os.path.dirname(NEXT), "serial", "accel_*.npz")))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", ACCEL_SERIAL, ids=os.path.basename)
+def test_steffensen_and_aitken_serial_bitwise_vs_reference(path):
+    """Acceleration around the serial schedule (device dependency levels)."""
+    rec = _npz(path)
+    s = L.SymSystem.from_pairs(rec["diag"], rec["pair_i"], rec["pair_j"], rec["pair_v"],
+                               rec["rhs"])
+    opts = G.SolveOptions(schedule="serial")
+    _same_report(A.steffensen_solve("gabp", s, opts), rec, "serial_steff")
+    _same_report(A.aitken_solve("gabp", s, opts), rec, "serial_aitken")
+
+
 @pytest.mark.gpu
 def test_accelerated_solve_dispatch_gpu():
     s = G.load_instance("cdma3").system
@@ -205,6 +220,29 @@ def test_steffensen_large_graph_device_restart():
 
 
 # ---- augmented least squares: the solve (GPU) ----------------------------------------------
+
+LSQ_DEFAULT = sorted(glob.glob(os.path.join(os.path.dirname(NEXT), "serial", "lsq_*.npz")))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", LSQ_DEFAULT, ids=os.path.basename)
+def test_solve_least_squares_default_options_vs_reference(path):
+    """The reference's default options (serial schedule, epsilon 1e-10): same x bit for
+    bit, or the same divergence with the same spectral diagnostic."""
+    rec = _npz(path)
+    s = L.RectMatrix.from_dense(rec["dense"])
+    if int(rec["diverged"]):
+        with pytest.raises(PI.LeastSquaresDivergence) as ei:
+            PI.solve_least_squares(s, rec["y"], float(rec["psi"]))
+        assert ei.value.rho == pytest.approx(float(rec["rho"]), rel=1e-9)
+        return
+    x = PI.solve_least_squares(s, rec["y"], float(rec["psi"]))
+    np.testing.assert_array_equal(_bits(x), _bits(rec["x"]))
+
+
+def test_lsq_default_fixtures_present():
+    assert len(LSQ_DEFAULT) == 7
+
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("path", LSQ, ids=os.path.basename)
