@@ -135,6 +135,9 @@ struct gabp_graph {
     std::vector<int64_t> serial_order;
     std::vector<int64_t> serial_lvl;       // task offsets per level
     uint2 *d_serial = nullptr;             // tasks {node, order position}, level by level
+    cudaGraphExec_t serial_exec = nullptr; // the level launches, captured once per order
+    uint64_t serial_gen = 0;               // workspace generation of the capture
+    double serial_lim = 0.0;               // blow-up limit of the capture
     std::vector<uint32_t> h_rp, h_col;     // host CSR (level build)
 };
 
@@ -1057,6 +1060,7 @@ static void graph_release(gabp_graph *G) {
     cudaSetDevice(G->device);
     cudaStreamSynchronize(G->stream);
     if (G->d_serial) cudaFree(G->d_serial);
+    if (G->serial_exec) cudaGraphExecDestroy(G->serial_exec);
     release_workspace(G);
     gabp::free_graph(G->g, G->stream);
     cudaStreamSynchronize(G->stream);
@@ -1270,6 +1274,8 @@ static int serial_levels(gabp_graph *G, const int64_t *order, int64_t norder) {
     }
     if (G->d_serial) cudaFree(G->d_serial);
     G->d_serial = nullptr;
+    if (G->serial_exec) cudaGraphExecDestroy(G->serial_exec);
+    G->serial_exec = nullptr;
     CK(cudaMalloc(&G->d_serial, sizeof(uint2) * tasks.size()));
     CK(cudaMemcpy(G->d_serial, tasks.data(), sizeof(uint2) * tasks.size(),
                   cudaMemcpyHostToDevice));
@@ -1302,20 +1308,45 @@ int gabp_sweep_serial(const gabp_graph_t *Gc, gabp_state_t *S, const int64_t *or
     if (max_change) *max_change = 0.0;
     if (out_of_range) *out_of_range = 0;
     if (num_levels) *num_levels = (int32_t)(G->serial_lvl.size() - 1);
-    Ctrl c = gabp::fresh_ctrl();
-    *G->h_ctrl = c;
-    CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, G->stream));
-    SweepArgs a = make_args(G);
     // in place on a copy (solver.py:177-178 works on lists made from the state): a sweep
     // that meets a singular exclusion sum leaves the state as it was, like the reference
     double2 *msg = S->buf[S->cur ^ 1];
+    Ctrl c = gabp::fresh_ctrl();
+    c.serial_msg = msg;
+    *G->h_ctrl = c;
+    CK(cudaMemcpyAsync(G->ctrl, G->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, G->stream));
     if (G->g.E)
         CK(cudaMemcpyAsync(msg, S->buf[S->cur], sizeof(double2) * G->g.E,
                            cudaMemcpyDeviceToDevice, G->stream));
     const double lim = blowup < DBL_MAX ? blowup : DBL_MAX;
-    for (size_t l = 0; l + 1 < G->serial_lvl.size(); ++l)
-        CK(gabp::launch_serial_level(a, msg, G->d_serial + G->serial_lvl[l],
-                                     G->serial_lvl[l + 1] - G->serial_lvl[l], lim, G->stream));
+    // the level launches as one CUDA graph (a grid has thousands of levels: host launches
+    // cost ~7 us each), captured once per order, workspace and blow-up limit
+    if (G->serial_exec && (G->serial_gen != G->ws_gen || G->serial_lim != lim)) {
+        cudaGraphExecDestroy(G->serial_exec);
+        G->serial_exec = nullptr;
+    }
+    if (!G->serial_exec && G->serial_lvl.size() > 1) {
+        SweepArgs a = make_args(G);
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(G->stream, cudaStreamCaptureModeThreadLocal));
+        for (size_t l = 0; l + 1 < G->serial_lvl.size(); ++l) {
+            cudaError_t e = gabp::launch_serial_level(a, G->d_serial + G->serial_lvl[l],
+                                                      G->serial_lvl[l + 1] - G->serial_lvl[l],
+                                                      lim, G->stream);
+            if (e != cudaSuccess) {
+                cudaStreamEndCapture(G->stream, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                return fail(GABP_ECUDA, "serial level capture: %s", cudaGetErrorString(e));
+            }
+        }
+        CK(cudaStreamEndCapture(G->stream, &graph));
+        cudaError_t e = cudaGraphInstantiate(&G->serial_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CK(e);
+        G->serial_gen = G->ws_gen;
+        G->serial_lim = lim;
+    }
+    if (G->serial_exec) CK(cudaGraphLaunch(G->serial_exec, G->stream));
     CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, G->stream));
     CK(cudaStreamSynchronize(G->stream));
     const Ctrl &h = *G->h_ctrl;

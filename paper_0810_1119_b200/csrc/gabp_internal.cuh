@@ -103,6 +103,8 @@ struct Ctrl {
     int32_t probes;             // residual probes run (diagnostics)
     int32_t twin_launches;      // exact-twin kernels launched, host- or tail-launched (each
                                 // counts itself)
+    double2 *serial_msg;        // serial sweep: the message buffer the levels update in place
+                                // (set per sweep, so one captured graph serves every buffer)
 };
 
 // A fresh controller: every "first index" slot at the kNoIndex sentinel.
@@ -183,9 +185,10 @@ cudaError_t launch_sweep(const SweepArgs &a, int schedule, int mode, int gather,
 constexpr int kRowParMaxDegree = 256;
 cudaError_t prepare_rowpar_kernels();
 cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st);
-// serial schedule: one dependency level of tasks {node, order position}, in place on msg
-cudaError_t launch_serial_level(const SweepArgs &a, double2 *msg, const uint2 *tasks,
-                                int64_t cnt, double lim, cudaStream_t st);
+// serial schedule: one dependency level of tasks {node, order position}, in place on the
+// buffer a.ctrl->serial_msg
+cudaError_t launch_serial_level(const SweepArgs &a, const uint2 *tasks, int64_t cnt, double lim,
+                                cudaStream_t st);
 cudaError_t launch_marginals(int64_t n, const uint32_t *row_ptr, const EdgeRec *er,
                              const double *diag, const double *prior_num, const double2 *msg,
                              double *means, double *precs, cudaStream_t st);

@@ -377,10 +377,11 @@ __global__ void __launch_bounds__(kRThreads, 2) rowpar_kernel(const SweepArgs a)
 // messages the sequential loop would show it.  One launch per level, a warp per task; the
 // task's d exclusion sums run one per lane as in rowpar_kernel (rows <= 256 edges).
 __global__ void __launch_bounds__(kRThreads, 2) serial_level_kernel(const SweepArgs a,
-                                                                   double2 *msg,
                                                                    const uint2 *tasks,
                                                                    int64_t cnt, double lim) {
     __shared__ RowSmem S;
+    double2 *msg = reinterpret_cast<double2 *>(
+        __ldcg(reinterpret_cast<const unsigned long long *>(&a.ctrl->serial_msg)));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double2 *T = S.T[warp];
     Stats st;
@@ -462,13 +463,13 @@ cudaError_t prepare_rowpar_kernels() {
     return cudaSuccess;
 }
 
-cudaError_t launch_serial_level(const SweepArgs &a, double2 *msg, const uint2 *tasks,
-                                int64_t cnt, double lim, cudaStream_t st) {
+cudaError_t launch_serial_level(const SweepArgs &a, const uint2 *tasks, int64_t cnt, double lim,
+                                cudaStream_t st) {
     if (cnt <= 0) return cudaSuccess;
     int64_t grid = g_row_grid[kModeSingle] > 0 ? g_row_grid[kModeSingle] : 148 * 2;
     const int64_t need = (cnt + kRWarps - 1) / kRWarps;
     if (grid > need) grid = need;
-    serial_level_kernel<<<(unsigned)grid, kRThreads, 0, st>>>(a, msg, tasks, cnt, lim);
+    serial_level_kernel<<<(unsigned)grid, kRThreads, 0, st>>>(a, tasks, cnt, lim);
     return cudaGetLastError();
 }
 
