@@ -135,6 +135,8 @@ struct gabp_graph {
     std::vector<int64_t> serial_order;
     std::vector<int64_t> serial_lvl;       // task offsets per level
     uint2 *d_serial = nullptr;             // tasks {node, order position}, level by level
+    int64_t *d_serial_lvl = nullptr;       // level offsets on the device
+    int64_t serial_maxw = 0;               // tasks of the widest level
     cudaGraphExec_t serial_exec = nullptr; // the level launches, captured once per order
     uint64_t serial_gen = 0;               // workspace generation of the capture
     double serial_lim = 0.0;               // blow-up limit of the capture
@@ -1060,6 +1062,7 @@ static void graph_release(gabp_graph *G) {
     cudaSetDevice(G->device);
     cudaStreamSynchronize(G->stream);
     if (G->d_serial) cudaFree(G->d_serial);
+    if (G->d_serial_lvl) cudaFree(G->d_serial_lvl);
     if (G->serial_exec) cudaGraphExecDestroy(G->serial_exec);
     release_workspace(G);
     gabp::free_graph(G->g, G->stream);
@@ -1279,6 +1282,16 @@ static int serial_levels(gabp_graph *G, const int64_t *order, int64_t norder) {
     CK(cudaMalloc(&G->d_serial, sizeof(uint2) * tasks.size()));
     CK(cudaMemcpy(G->d_serial, tasks.data(), sizeof(uint2) * tasks.size(),
                   cudaMemcpyHostToDevice));
+    if (G->d_serial_lvl) cudaFree(G->d_serial_lvl);
+    G->d_serial_lvl = nullptr;
+    CK(cudaMalloc(&G->d_serial_lvl, sizeof(int64_t) * G->serial_lvl.size()));
+    CK(cudaMemcpy(G->d_serial_lvl, G->serial_lvl.data(), sizeof(int64_t) * G->serial_lvl.size(),
+                  cudaMemcpyHostToDevice));
+    G->serial_maxw = 0;
+    for (uint32_t l = 0; l < nlev; ++l) {
+        const int64_t w = G->serial_lvl[l + 1] - G->serial_lvl[l];
+        G->serial_maxw = w > G->serial_maxw ? w : G->serial_maxw;
+    }
     G->serial_ascending = asc;
     if (asc)
         G->serial_order.clear();
@@ -1319,34 +1332,42 @@ int gabp_sweep_serial(const gabp_graph_t *Gc, gabp_state_t *S, const int64_t *or
         CK(cudaMemcpyAsync(msg, S->buf[S->cur], sizeof(double2) * G->g.E,
                            cudaMemcpyDeviceToDevice, G->stream));
     const double lim = blowup < DBL_MAX ? blowup : DBL_MAX;
-    // the level launches as one CUDA graph (a grid has thousands of levels: host launches
-    // cost ~7 us each), captured once per order, workspace and blow-up limit
-    if (G->serial_exec && (G->serial_gen != G->ws_gen || G->serial_lim != lim)) {
-        cudaGraphExecDestroy(G->serial_exec);
-        G->serial_exec = nullptr;
-    }
-    if (!G->serial_exec && G->serial_lvl.size() > 1) {
+    const int nlev = (int)G->serial_lvl.size() - 1;
+    if (nlev <= 512 && !getenv("GABP_SERIAL_LEVEL_LAUNCHES")) {
+        // few, wide levels: one cooperative launch, a grid barrier between levels
         SweepArgs a = make_args(G);
-        cudaGraph_t graph;
-        CK(cudaStreamBeginCapture(G->stream, cudaStreamCaptureModeThreadLocal));
-        for (size_t l = 0; l + 1 < G->serial_lvl.size(); ++l) {
-            cudaError_t e = gabp::launch_serial_level(a, G->d_serial + G->serial_lvl[l],
-                                                      G->serial_lvl[l + 1] - G->serial_lvl[l],
-                                                      lim, G->stream);
-            if (e != cudaSuccess) {
-                cudaStreamEndCapture(G->stream, &graph);
-                if (graph) cudaGraphDestroy(graph);
-                return fail(GABP_ECUDA, "serial level capture: %s", cudaGetErrorString(e));
-            }
+        CK(gabp::launch_serial_sweep(a, G->d_serial, G->d_serial_lvl, nlev, G->serial_maxw, lim,
+                                     G->stream));
+    } else {
+        // many levels: the level launches as one CUDA graph (host launches cost ~7 us each),
+        // captured once per order, workspace and blow-up limit
+        if (G->serial_exec && (G->serial_gen != G->ws_gen || G->serial_lim != lim)) {
+            cudaGraphExecDestroy(G->serial_exec);
+            G->serial_exec = nullptr;
         }
-        CK(cudaStreamEndCapture(G->stream, &graph));
-        cudaError_t e = cudaGraphInstantiate(&G->serial_exec, graph, 0);
-        cudaGraphDestroy(graph);
-        CK(e);
-        G->serial_gen = G->ws_gen;
-        G->serial_lim = lim;
+        if (!G->serial_exec && G->serial_lvl.size() > 1) {
+            SweepArgs a = make_args(G);
+            cudaGraph_t graph;
+            CK(cudaStreamBeginCapture(G->stream, cudaStreamCaptureModeThreadLocal));
+            for (size_t l = 0; l + 1 < G->serial_lvl.size(); ++l) {
+                cudaError_t e = gabp::launch_serial_level(a, G->d_serial + G->serial_lvl[l],
+                                                          G->serial_lvl[l + 1] - G->serial_lvl[l],
+                                                          lim, G->stream);
+                if (e != cudaSuccess) {
+                    cudaStreamEndCapture(G->stream, &graph);
+                    if (graph) cudaGraphDestroy(graph);
+                    return fail(GABP_ECUDA, "serial level capture: %s", cudaGetErrorString(e));
+                }
+            }
+            CK(cudaStreamEndCapture(G->stream, &graph));
+            cudaError_t e = cudaGraphInstantiate(&G->serial_exec, graph, 0);
+            cudaGraphDestroy(graph);
+            CK(e);
+            G->serial_gen = G->ws_gen;
+            G->serial_lim = lim;
+        }
+        if (G->serial_exec) CK(cudaGraphLaunch(G->serial_exec, G->stream));
     }
-    if (G->serial_exec) CK(cudaGraphLaunch(G->serial_exec, G->stream));
     CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, G->stream));
     CK(cudaStreamSynchronize(G->stream));
     const Ctrl &h = *G->h_ctrl;

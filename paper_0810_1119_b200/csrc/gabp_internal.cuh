@@ -105,6 +105,7 @@ struct Ctrl {
                                 // counts itself)
     double2 *serial_msg;        // serial sweep: the message buffer the levels update in place
                                 // (set per sweep, so one captured graph serves every buffer)
+    uint32_t bar_count, bar_gen;  // serial sweep: grid barrier between levels
 };
 
 // A fresh controller: every "first index" slot at the kNoIndex sentinel.
@@ -189,6 +190,10 @@ cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st);
 // buffer a.ctrl->serial_msg
 cudaError_t launch_serial_level(const SweepArgs &a, const uint2 *tasks, int64_t cnt, double lim,
                                 cudaStream_t st);
+// the whole serial sweep as one cooperative launch (grid barrier between levels); lvl =
+// device level offsets [nlev + 1], max_cnt = the widest level
+cudaError_t launch_serial_sweep(const SweepArgs &a, const uint2 *tasks, const int64_t *lvl,
+                                int nlev, int64_t max_cnt, double lim, cudaStream_t st);
 cudaError_t launch_marginals(int64_t n, const uint32_t *row_ptr, const EdgeRec *er,
                              const double *diag, const double *prior_num, const double2 *msg,
                              double *means, double *precs, cudaStream_t st);

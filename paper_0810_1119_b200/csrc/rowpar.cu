@@ -376,6 +376,80 @@ __global__ void __launch_bounds__(kRThreads, 2) rowpar_kernel(const SweepArgs a)
 // run level after level give the sequential result bit for bit: a task sees exactly the
 // messages the sequential loop would show it.  One launch per level, a warp per task; the
 // task's d exclusion sums run one per lane as in rowpar_kernel (rows <= 256 edges).
+// One serial task {node, order position}: node i's outgoing messages from its current
+// incoming ones, in place on msg (solver.py:181-209).
+__device__ __forceinline__ void serial_task(const SweepArgs &a, double2 *msg, uint2 tk,
+                                            double2 *T, int lane, Stats &st) {
+    const uint32_t i = tk.x;
+    const uint32_t e0 = __ldg(a.row_ptr + i), d = __ldg(a.row_ptr + i + 1) - e0;
+    const double2 nd = __ldg(reinterpret_cast<const double2 *>(a.nd + i));
+    const uint32_t dpad = (d + 7u) & ~7u;
+    for (uint32_t q = lane; q < dpad; q += 32) {
+        if (q < d) {
+            const EdgeRec r = ld_er(a.er + e0 + q);
+            const double2 in = __ldcg(msg + r.rev);  // m_ki as the loop would see it
+            T[q] = make_double2(in.x, in.x * in.y);
+        } else {
+            T[q] = make_double2(-0.0, -0.0);
+        }
+    }
+    __syncwarp();
+    for (uint32_t jb = 0; jb < d; jb += 32) {
+        const uint32_t j = jb + lane;
+        double p = nd.x, n = nd.y;
+        for (uint32_t t = 0; t < dpad; t += 8) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double2 v = T[t + k];
+                if (t + k != j) {
+                    p = p + v.x;
+                    n = n + v.y;
+                }
+            }
+        }
+        if (j < d) {
+            const uint32_t e = e0 + j;
+            const double c = __ldg(&a.er[e].coeff);
+            const double2 old = __ldcg(msg + e);
+            bool okp, okm;
+            double np_ = ddiv_fast(-c * c, p, okp);
+            double nm = ddiv_fast(n, c, okm);
+            if (!okp) np_ = div_slow(-c * c, p);
+            if (!okm) nm = div_slow(n, c);
+            if (p == 0.0)  // the first in loop order: (order position, edge)
+                atomicMin(&a.ctrl->singular_min[1],
+                          ((unsigned long long)tk.y << 32) | (unsigned long long)e);
+            __stcg(msg + e, make_double2(np_, nm));
+            const double d1 = fabs(np_ - old.x), d2 = fabs(nm - old.y);
+            st.chg = d1 > st.chg ? d1 : st.chg;
+            st.chg = d2 > st.chg ? d2 : st.chg;
+            if (!(fabs(np_) <= st.lim) || !(fabs(nm) <= st.lim)) st.out_of_range = 1u;
+        }
+    }
+    __syncwarp();  // the strip is rewritten by the next task
+}
+
+// Software grid barrier of a cooperative launch (every CTA resident): arrive, and the last
+// CTA to arrive opens the next generation.  Writes before it are visible after it (fences
+// on both sides; messages are read through L2).
+__device__ __forceinline__ void grid_barrier(Ctrl *c, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = &c->bar_gen;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(&c->bar_count, 1u) == nblocks - 1u) {
+            c->bar_count = 0u;
+            __threadfence();
+            atomicAdd(&c->bar_gen, 1u);
+        } else {
+            while (*gen == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(kRThreads, 2) serial_level_kernel(const SweepArgs a,
                                                                    const uint2 *tasks,
                                                                    int64_t cnt, double lim) {
@@ -383,59 +457,36 @@ __global__ void __launch_bounds__(kRThreads, 2) serial_level_kernel(const SweepA
     double2 *msg = reinterpret_cast<double2 *>(
         __ldcg(reinterpret_cast<const unsigned long long *>(&a.ctrl->serial_msg)));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double2 *T = S.T[warp];
     Stats st;
     st.lim = lim;
     const int64_t nw = (int64_t)gridDim.x * kRWarps;
-    for (int64_t w = (int64_t)blockIdx.x * kRWarps + warp; w < cnt; w += nw) {
-        const uint2 tk = __ldg(tasks + w);  // {node, position in the order}
-        const uint32_t i = tk.x;
-        const uint32_t e0 = __ldg(a.row_ptr + i), d = __ldg(a.row_ptr + i + 1) - e0;
-        const double2 nd = __ldg(reinterpret_cast<const double2 *>(a.nd + i));
-        const uint32_t dpad = (d + 7u) & ~7u;
-        for (uint32_t q = lane; q < dpad; q += 32) {
-            if (q < d) {
-                const EdgeRec r = ld_er(a.er + e0 + q);
-                const double2 in = __ldcg(msg + r.rev);  // m_ki as the loop would see it
-                T[q] = make_double2(in.x, in.x * in.y);
-            } else {
-                T[q] = make_double2(-0.0, -0.0);
-            }
-        }
-        __syncwarp();
-        for (uint32_t jb = 0; jb < d; jb += 32) {
-            const uint32_t j = jb + lane;
-            double p = nd.x, n = nd.y;
-            for (uint32_t t = 0; t < dpad; t += 8) {
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const double2 v = T[t + k];
-                    if (t + k != j) {
-                        p = p + v.x;
-                        n = n + v.y;
-                    }
-                }
-            }
-            if (j < d) {
-                const uint32_t e = e0 + j;
-                const double c = __ldg(&a.er[e].coeff);
-                const double2 old = __ldcg(msg + e);
-                bool okp, okm;
-                double np_ = ddiv_fast(-c * c, p, okp);
-                double nm = ddiv_fast(n, c, okm);
-                if (!okp) np_ = div_slow(-c * c, p);
-                if (!okm) nm = div_slow(n, c);
-                if (p == 0.0)  // the first in loop order: (order position, edge)
-                    atomicMin(&a.ctrl->singular_min[1],
-                              ((unsigned long long)tk.y << 32) | (unsigned long long)e);
-                __stcg(msg + e, make_double2(np_, nm));
-                const double d1 = fabs(np_ - old.x), d2 = fabs(nm - old.y);
-                st.chg = d1 > st.chg ? d1 : st.chg;
-                st.chg = d2 > st.chg ? d2 : st.chg;
-                if (!(fabs(np_) <= st.lim) || !(fabs(nm) <= st.lim)) st.out_of_range = 1u;
-            }
-        }
-        __syncwarp();  // the strip is rewritten by the next task
+    for (int64_t w = (int64_t)blockIdx.x * kRWarps + warp; w < cnt; w += nw)
+        serial_task(a, msg, __ldg(tasks + w), S.T[warp], lane, st);
+    __syncthreads();
+    sweep_epilogue<kRThreads, kModeSingle, 0>(S.tail, a, 1, false, st, tid);
+}
+
+// The whole sweep in one cooperative launch: level after level, a grid barrier between
+// levels.  Used for orders with few, wide levels (config 1: 88 levels, 2.89 -> 2.46 ms per
+// sweep against the graph of level launches); with thousands of narrow levels (a 4096^2
+// grid: 8191) a barrier costs more than a dependent launch in a graph (44.7 vs 39.8 ms).
+__global__ void __launch_bounds__(kRThreads, 2) serial_sweep_kernel(const SweepArgs a,
+                                                                   const uint2 *tasks,
+                                                                   const int64_t *lvl,
+                                                                   int nlev, double lim) {
+    __shared__ RowSmem S;
+    double2 *msg = reinterpret_cast<double2 *>(
+        __ldcg(reinterpret_cast<const unsigned long long *>(&a.ctrl->serial_msg)));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    Stats st;
+    st.lim = lim;
+    const int64_t nw = (int64_t)gridDim.x * kRWarps;
+    const int64_t gw = (int64_t)blockIdx.x * kRWarps + warp;
+    for (int l = 0; l < nlev; ++l) {
+        const int64_t lo = __ldg(lvl + l), cnt = __ldg(lvl + l + 1) - lo;
+        for (int64_t w = gw; w < cnt; w += nw)
+            serial_task(a, msg, __ldg(tasks + lo + w), S.T[warp], lane, st);
+        if (l + 1 < nlev) grid_barrier(a.ctrl, gridDim.x);
     }
     __syncthreads();
     sweep_epilogue<kRThreads, kModeSingle, 0>(S.tail, a, 1, false, st, tid);
@@ -471,6 +522,29 @@ cudaError_t launch_serial_level(const SweepArgs &a, const uint2 *tasks, int64_t 
     if (grid > need) grid = need;
     serial_level_kernel<<<(unsigned)grid, kRThreads, 0, st>>>(a, tasks, cnt, lim);
     return cudaGetLastError();
+}
+
+cudaError_t launch_serial_sweep(const SweepArgs &a, const uint2 *tasks, const int64_t *lvl,
+                                int nlev, int64_t max_cnt, double lim, cudaStream_t st) {
+    if (nlev <= 0) return cudaSuccess;
+    static int coop_grid = 0;
+    if (coop_grid == 0) {
+        int dev = 0, sms = 0, occ = 0;
+        cudaError_t e;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+            return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, serial_sweep_kernel,
+                                                               kRThreads, 0)) != cudaSuccess)
+            return e;
+        coop_grid = sms * (occ > 0 ? occ : 1);
+    }
+    int64_t grid = coop_grid;
+    const int64_t need = (max_cnt + kRWarps - 1) / kRWarps;
+    if (grid > need) grid = need > 0 ? need : 1;
+    void *args[] = {(void *)&a, (void *)&tasks, (void *)&lvl, (void *)&nlev, (void *)&lim};
+    return cudaLaunchCooperativeKernel((const void *)serial_sweep_kernel, dim3((unsigned)grid),
+                                       dim3(kRThreads), args, 0, st);
 }
 
 cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st) {

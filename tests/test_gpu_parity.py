@@ -744,3 +744,17 @@ def test_serial_order_errors():
     s = G.gen_poisson2d(8, 0).system
     with pytest.raises(Exception):
         G.solve(s, G.SolveOptions(schedule="serial", serial_order=[0, 1, s.n]))
+
+
+@pytest.mark.parametrize("which", ["ladder", "poisson2d_200"])
+def test_serial_level_launch_path_vs_oracle(which, monkeypatch):
+    """The per-level launch path (CUDA graph of level launches, GABP_SERIAL_LEVEL_LAUNCHES)
+    gives the same bits as the cooperative one-launch sweep and the oracle."""
+    s = _degree_ladder_system() if which == "ladder" else G.gen_poisson2d(200, 4).system
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    orc = oracle.solve_serial(og, epsilon=1e-300, max_iter=6)
+    monkeypatch.setenv("GABP_SERIAL_LEVEL_LAUNCHES", "1")
+    r = G.solve(s, G.SolveOptions(schedule="serial", epsilon=1e-300, max_iter=6))
+    assert r.iterations == orc.iterations
+    np.testing.assert_array_equal(r.means, orc.means)
+    np.testing.assert_array_equal(np.asarray(r.max_change_history), orc.max_change_history)
