@@ -34,6 +34,7 @@ from .linalg import SymSystem
 SCHEDULES = ("parallel", "serial", "broadcast")
 GPU_SCHEDULES = ("parallel", "broadcast")  # device solve loop (gabp_solve)
 _AUTO_MEANS_HISTORY_DOUBLES = 1 << 24
+_SERIAL_COOP_MAX_LEVELS = 512  # capi.cu gabp_sweep_serial: cooperative sweep up to here
 
 
 class SingularSubgraphError(ArithmeticError):
@@ -294,7 +295,9 @@ def _solve_serial(graph: GaussianGraph, options: SolveOptions) -> SolveReport:
             except SingularSubgraphError:
                 diverged = True
                 break
-            launches += levels
+            # one cooperative launch for short orders, one launch per level otherwise
+            # (capi.cu: gabp_sweep_serial)
+            launches += 1 if levels <= _SERIAL_COOP_MAX_LEVELS else levels
             means, _ = infer_marginals(graph, state)
             means_finite = bool(np.all(np.isfinite(means)))
             if means_finite:
