@@ -1246,12 +1246,18 @@ static int serial_levels(gabp_graph *G, const int64_t *order, int64_t norder) {
         G->h_rp.resize(n + 1);
         CK(cudaMemcpy(G->h_rp.data(), G->g.row_ptr, sizeof(uint32_t) * (n + 1),
                       cudaMemcpyDeviceToHost));
-        std::vector<gabp::EdgeRec> er(G->g.E);
-        if (G->g.E)
-            CK(cudaMemcpy(er.data(), G->g.er, sizeof(gabp::EdgeRec) * G->g.E,
-                          cudaMemcpyDeviceToHost));
         G->h_col.resize(G->g.E);
-        for (int64_t e = 0; e < G->g.E; ++e) G->h_col[e] = er[e].col;
+        if (G->g.E) {  // the column field only (4 B per edge through PCIe, not the record)
+            uint32_t *dcol = nullptr;
+            CK(cudaMalloc(&dcol, sizeof(uint32_t) * G->g.E));
+            cudaError_t e = gabp::launch_edge_col(G->g.E, G->g.er, dcol, G->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(G->stream);
+            if (e == cudaSuccess)
+                e = cudaMemcpy(G->h_col.data(), dcol, sizeof(uint32_t) * G->g.E,
+                               cudaMemcpyDeviceToHost);
+            cudaFree(dcol);
+            CK(e);
+        }
     }
     std::vector<uint32_t> last(n, 0u), lev(norder);
     uint32_t nlev = 0;

@@ -190,6 +190,7 @@ cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st);
 // buffer a.ctrl->serial_msg
 cudaError_t launch_serial_level(const SweepArgs &a, const uint2 *tasks, int64_t cnt, double lim,
                                 cudaStream_t st);
+cudaError_t launch_edge_col(int64_t E, const EdgeRec *er, uint32_t *col, cudaStream_t st);
 // the whole serial sweep as one cooperative launch (grid barrier between levels); lvl =
 // device level offsets [nlev + 1], max_cnt = the widest level
 cudaError_t launch_serial_sweep(const SweepArgs &a, const uint2 *tasks, const int64_t *lvl,

@@ -492,6 +492,14 @@ __global__ void __launch_bounds__(kRThreads, 2) serial_sweep_kernel(const SweepA
     sweep_epilogue<kRThreads, kModeSingle, 0>(S.tail, a, 1, false, st, tid);
 }
 
+// Destination column of every edge record (the host builds the serial levels from the CSR
+// without copying the 16-byte records).
+__global__ void edge_col_kernel(int64_t E, const EdgeRec *er, uint32_t *col) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x)
+        col[e] = __ldg(&er[e].col);
+}
+
 int g_row_grid[2] = {0, 0};
 
 }  // namespace
@@ -521,6 +529,12 @@ cudaError_t launch_serial_level(const SweepArgs &a, const uint2 *tasks, int64_t 
     const int64_t need = (cnt + kRWarps - 1) / kRWarps;
     if (grid > need) grid = need;
     serial_level_kernel<<<(unsigned)grid, kRThreads, 0, st>>>(a, tasks, cnt, lim);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_edge_col(int64_t E, const EdgeRec *er, uint32_t *col, cudaStream_t st) {
+    if (E <= 0) return cudaSuccess;
+    edge_col_kernel<<<148 * 8, 256, 0, st>>>(E, er, col);
     return cudaGetLastError();
 }
 
