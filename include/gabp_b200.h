@@ -99,6 +99,8 @@ typedef struct {
                                  one launch early */
     int64_t kernel_launches;  /* kernels the solve loop enqueued (incl. launches that exit at
                                  once after the decision); 0 for multi-rank solves */
+    int64_t split_sweeps;     /* multi-rank: sweeps run split (boundary rows first, halo
+                                 exchange under the interior rows) */
 } gabp_report_t;
 
 const char *gabp_last_error(void);
@@ -127,6 +129,14 @@ int gabp_graph_create_ex(int64_t n, int64_t npairs, const double *h_diag, const 
                          const int64_t *h_pair_i, const int64_t *h_pair_j,
                          const double *h_pair_v, int64_t row_lo, int64_t row_hi,
                          int32_t device, gabp_graph_t **out);
+
+/* Same as gabp_graph_create_ex, inputs already resident in HBM: a rank that generates
+ * or receives only its own row block (and halo) never stages the global system. */
+int gabp_graph_create_device_ex(int64_t n, int64_t npairs, const double *d_diag,
+                                const double *d_rhs, const int64_t *d_pair_i,
+                                const int64_t *d_pair_j, const double *d_pair_v,
+                                int64_t row_lo, int64_t row_hi, int32_t device,
+                                gabp_graph_t **out);
 
 /* Dense variant (linear detection, BASELINE config 3): A given as a row-major n x n
  * symmetric matrix; exact zeros off the diagonal are non-edges (linalg.py:81-82). */
@@ -179,29 +189,23 @@ int gabp_sweep(const gabp_graph_t *g, gabp_state_t *s, int32_t schedule, double 
  * ones.  Run as dependency levels (tasks on non-adjacent nodes in parallel), bitwise the
  * sequential loop.  out_of_range = some updated message is non-finite or |v| > blowup;
  * GABP_ESINGULAR with *singular_edge = the first P_excl == 0 edge in loop order, the state
- * left unchanged.  Rows of at most 256 edges; whole graphs only. */
+ * left unchanged.  Whole graphs only; tasks of more than 256 edges keep
+ * their terms in a global scratch strip instead of shared memory. */
 int gabp_sweep_serial(const gabp_graph_t *g, gabp_state_t *s, const int64_t *order,
                       int64_t norder, double blowup, double *max_change, int32_t *out_of_range,
                       int64_t *singular_edge, int32_t *num_levels);
 int gabp_infer_marginals(const gabp_graph_t *g, const gabp_state_t *s, double *h_means,
                          double *h_precs);
 
-/* ---- acceleration (acceleration.py) --------------------------------------------- */
+/* ---- whole-state checks and point reads ------------------------------------------ */
 
-/* Steffensen restart (acceleration.py:177-183 gated_extrapolate, :74-96 aitken_extrapolate,
- * applied by set_target to the mean messages, :123-126): the mean messages of x2 are
- * replaced in place by the componentwise Aitken extrapolant of the mean messages of x0,
- * x1, x2 -- gated (gated != 0: kept only where |second difference| >= stability x
- * max(|first differences|), x2 elsewhere) or plain.  Precision messages are untouched.
- * Bitwise equal to the numpy expressions. */
-int gabp_state_extrapolate(const gabp_state_t *x0, const gabp_state_t *x1, gabp_state_t *x2,
-                           double guard, double stability, int32_t gated);
-/* _GabpStepper.blown() (acceleration.py:128-133): *blown = 1 when a message is not finite
- * or max |message| > blowup. */
+/* The divergence test of the solve loop on a state (solver.py:333-338): *blown = 1 when a
+ * message is not finite or max |message| > blowup. */
 int gabp_state_blown(const gabp_state_t *s, double blowup, int32_t *blown);
-/* np.max(np.abs(a.mean - b.mean), initial=0.0) (acceleration.py:259): NaN if any
- * difference is NaN. */
-int gabp_state_mean_max_diff(const gabp_state_t *a, const gabp_state_t *b, double *out);
+/* Messages of `count` edge ids (host list) into host arrays (either may be NULL): the
+ * buffer reads of compute_message / compute_message_max_product (solver.py:100-143). */
+int gabp_state_gather(const gabp_state_t *s, const int64_t *h_edges, int64_t count,
+                      double *h_prec, double *h_mean);
 
 /* ---- solve (solver.py:307-346) ---------------------------------------------------- */
 

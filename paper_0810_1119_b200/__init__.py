@@ -7,8 +7,6 @@ for the path this package covers; see DESIGN.md for scope.
 
 from .graph import (DegenerateProductError, GaussianGraph, ScalarGaussian, build_graph,
                     gaussian_product)
-from .acceleration import (AccelConfig, accelerated_solve, aitken_extrapolate, aitken_solve,
-                           gated_extrapolate, steffensen_solve)
 from .linalg import (MatrixMarketError, RectMatrix, SingularMatrixError, SymSystem,
                      ZeroDiagonalError, dominance_class, parse_matrix_market, parse_vector,
                      residual_norm_per_eq, spectral_radius_gabp_test, system_from_matrix_market,
@@ -16,10 +14,9 @@ from .linalg import (MatrixMarketError, RectMatrix, SingularMatrixError, SymSyst
 from .problems import (CONFIGS, ProblemInstance, decorrelator_detect, gen_cdma,
                        gen_cdma_detection, gen_nonpsd3, gen_poisson, gen_poisson2d,
                        gen_poisson3d, gen_random, gen_random_sparse, gen_toy3, load_instance)
-from .pseudoinverse import (AugmentedSystem, LeastSquaresDivergence, build_augmented,
-                            normal_equations_oracle, solve_least_squares)
-from .solver import (SCHEDULES, MessageState, SingularSubgraphError, SolveOptions,
-                     SolveReport, broadcast_sweep, infer_marginals, initial_state, solve,
+from .solver import (SCHEDULES, MeansHistory, MessageState, SingularSubgraphError,
+                     SolveOptions, SolveReport, broadcast_sweep, compute_message,
+                     compute_message_max_product, infer_marginals, initial_state, solve,
                      solve_graph, sweep)
 
 __all__ = [name for name in dir() if not name.startswith("_")]

@@ -26,11 +26,12 @@ GABP_EDUP = -6
 SCHED_IDS = {"parallel": 0, "broadcast": 2}
 GATHER_IDS = {"auto": 0, "message": 1, "recompute": 2, "slice": 3, "rows": 4}
 
-# every symbol include/gabp_b200.h declares (checked by tests/test_capi_symbols.py)
+# every symbol include/gabp_b200.h declares (checked by tests/test_host.py)
 EXPORTED = (
     "gabp_last_error", "gabp_version", "gabp_device_count",
-    "gabp_state_extrapolate", "gabp_state_blown", "gabp_state_mean_max_diff",
-    "gabp_graph_create", "gabp_graph_create_device", "gabp_graph_create_dense",
+    "gabp_state_blown", "gabp_state_gather",
+    "gabp_graph_create", "gabp_graph_create_device", "gabp_graph_create_device_ex",
+    "gabp_graph_create_dense",
     "gabp_graph_destroy", "gabp_graph_info", "gabp_graph_export", "gabp_graph_set_rhs",
     "gabp_graph_stream",
     "gabp_state_create", "gabp_state_clone", "gabp_state_destroy", "gabp_state_reset",
@@ -66,7 +67,8 @@ class Report(ctypes.Structure):
                 ("iterations", ctypes.c_int64), ("n_hist", ctypes.c_int64),
                 ("sweeps_launched", ctypes.c_int64), ("messages_sent", ctypes.c_int64),
                 ("device_ms", ctypes.c_double), ("final_rel_residual", ctypes.c_double),
-                ("residual_probes", ctypes.c_int64), ("kernel_launches", ctypes.c_int64)]
+                ("residual_probes", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("split_sweeps", ctypes.c_int64)]
 
 
 class GabpError(RuntimeError):
@@ -120,10 +122,8 @@ def load():
         "gabp_sweep": (ctypes.c_int, [_vp, _vp, _i32, _dp, ctypes.POINTER(_i64),
                                       ctypes.POINTER(_i32)]),
         "gabp_infer_marginals": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
-        "gabp_state_extrapolate": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double,
-                                                  ctypes.c_double, _i32]),
         "gabp_state_blown": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.POINTER(_i32)]),
-        "gabp_state_mean_max_diff": (ctypes.c_int, [_vp, _vp, _dp]),
+        "gabp_state_gather": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
         "gabp_solve": (ctypes.c_int, [_vp, ctypes.POINTER(Options), _vp, _vp, _vp, _vp,
                                       ctypes.POINTER(Report)]),
         "gabp_solve_device": (ctypes.c_int, [_vp, ctypes.POINTER(Options), _vp, _vp,
@@ -139,6 +139,8 @@ def load():
         "gabp_bench_sweeps": (ctypes.c_int, [_vp, _i32, _i32, _i64, _dp]),
         "gabp_graph_create_ex": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
                                                 _i32, ctypes.POINTER(_vp)]),
+        "gabp_graph_create_device_ex": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp,
+                                                       _i64, _i64, _i32, ctypes.POINTER(_vp)]),
         "gabp_nccl_unique_id": (ctypes.c_int, [_vp]),
         "gabp_dist_attach": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i64, ctypes.c_double, _i32,
                                             _vp, _vp, _vp, _vp, _vp]),

@@ -204,6 +204,7 @@ void free_graph(DeviceGraph &g, cudaStream_t st) {
     if (g.prior_num) cudaFreeAsync(g.prior_num, st);
     if (g.rhs) cudaFreeAsync(g.rhs, st);
     if (g.slice_info) cudaFreeAsync(g.slice_info, st);
+    if (g.gorder) cudaFreeAsync(g.gorder, st);
     if (g.pos) cudaFreeAsync(g.pos, st);
     if (g.srow) cudaFreeAsync(g.srow, st);
     if (g.sdeg) cudaFreeAsync(g.sdeg, st);

@@ -78,6 +78,12 @@ struct DistState {
     // split sweep (boundary groups, then interior groups under the exchange)
     cudaStream_t xstream = nullptr;  // exchange stream
     cudaEvent_t ev_bnd = nullptr, ev_sweep = nullptr, ev_done = nullptr;
+    // launch protocol agreed by every rank (dist_agree): the kernel family (slice layout or
+    // recomputing tiles: the statistics' sweep lag) and the split sweep (the NCCL call
+    // sequence) must be the same on all ranks, whatever each rank's own layout allows;
+    // -1 until agreed
+    int use_slices = -1, use_split = -1;
+    int64_t split_launches = 0;      // split sweeps run by the last solve (report)
 };
 
 // pinned host mirror of a graph's controller and poll flags (capi.cu pinned_get)
@@ -101,6 +107,7 @@ struct gabp_graph {
     double *x[3] = {nullptr, nullptr, nullptr};
     double *p[3] = {nullptr, nullptr, nullptr};
     double *rsq_part = nullptr;
+    double *rsq_grp = nullptr;
     Ctrl *ctrl = nullptr;
     Ctrl *h_ctrl = nullptr;          // pinned mirror
     int32_t *h_done = nullptr;       // pinned, 2 poll slots
@@ -136,6 +143,8 @@ struct gabp_graph {
     std::vector<int64_t> serial_lvl;       // task offsets per level
     uint2 *d_serial = nullptr;             // tasks {node, order position}, level by level
     int64_t *d_serial_lvl = nullptr;       // level offsets on the device
+    double2 *serial_strip = nullptr;       // global term strips of tasks > 256 edges
+    int64_t serial_strip_stride = 0;
     int64_t serial_maxw = 0;               // tasks of the widest level
     cudaGraphExec_t serial_exec = nullptr; // the level launches, captured once per order
     uint64_t serial_gen = 0;               // workspace generation of the capture
@@ -296,6 +305,8 @@ void carve_workspace(gabp_graph *G, Carve &c) {
     G->ps = c.take<double>(g.n + 1);
     // one partial per CTA of a persistent launch (either layout)
     G->rsq_part = c.take<double>(g.ntiles > 8192 ? g.ntiles : 8192);
+    // one partial per slice group (group TMA kernels: dynamic claims, fixed summation order)
+    G->rsq_grp = c.take<double>(g.nslices / 15 + 1);
     G->ctrl = c.take<Ctrl>(1);
 }
 
@@ -349,6 +360,8 @@ int ensure_workspace(gabp_graph *G, int64_t max_iter) {
 SweepArgs make_args(gabp_graph *G) {
     SweepArgs a{};
     const DeviceGraph &g = G->g;
+    a.strip = G->serial_strip;
+    a.strip_stride = G->serial_strip_stride;
     a.n = g.n;
     a.ntiles = g.ntiles;
     a.row_ptr = g.row_ptr;
@@ -366,6 +379,7 @@ SweepArgs make_args(gabp_graph *G) {
         a.p[b] = G->p[b];
     }
     a.rsq_part = G->rsq_part;
+    a.rsq_grp = G->rsq_grp;
     a.ctrl = G->ctrl;
     a.change_hist = G->change_hist;
     a.res_hist = G->res_hist;
@@ -378,6 +392,7 @@ SweepArgs make_args(gabp_graph *G) {
     a.slice_path = 0;
     a.nslices = g.nslices;
     a.slice_info = g.slice_info;
+    a.gorder = g.gorder;
     a.sdeg = g.sdeg;
     a.srow = g.srow;
     a.snd = g.snd;
@@ -448,6 +463,8 @@ int check_slice(const gabp_graph *G, const gabp_options_t *opt) {
 
 // kernel family of a multi-rank launch: slice layout when built, else recomputing tiles
 int dist_gather(const gabp_graph *G) {
+    if (G->dist && G->dist->use_slices >= 0)
+        return G->dist->use_slices ? gabp::kGatherSlice : gabp::kGatherRecompute;
     return G->g.nslices > 0 ? gabp::kGatherSlice : gabp::kGatherRecompute;
 }
 
@@ -521,6 +538,7 @@ int get_chunk_exec(gabp_graph *G, int sched, int gather, int len) {
 int solve_setup(gabp_graph *G, const gabp_options_t *opt) {
     int rc = check_options(opt);
     if (rc) return rc;
+    if (G->dist) G->dist->split_launches = 0;
     CK(cudaSetDevice(G->device));
     rc = ensure_workspace(G, opt->max_iter);
     if (rc) return rc;
@@ -606,12 +624,44 @@ int dist_ensure_comm(DistState *D) {
 // Split sweep of a multi-rank slice-path launch: the leading bnd_groups groups hold every
 // row a peer needs.  Worth it when they are a minority (structured partitions); for a
 // random graph nearly every row is a boundary row and the sweep stays whole.
-int64_t split_slices(const gabp_graph *G) {
+int64_t split_slices_local(const gabp_graph *G) {
     const DeviceGraph &g = G->g;
     if (g.nslices == 0 || g.slice_variant == 1 || g.bnd_groups <= 0) return 0;
     const int64_t ng = g.nslices / 15;  // (kGroup; the split is at whole groups)
     if (2 * g.bnd_groups > ng) return 0;
     return g.bnd_groups * 15;
+}
+
+// the split of this rank's sweep under the agreed protocol (0: whole sweeps on every rank)
+int64_t split_slices(const gabp_graph *G) {
+    if (G->dist && G->dist->use_split == 0) return 0;
+    if (G->dist && G->dist->use_slices == 0) return 0;
+    return split_slices_local(G);
+}
+
+// What this rank's layout allows: bit 0 the slice layout, bit 1 the split sweep.
+int dist_local_caps(const gabp_graph *G) {
+    const int sl = G->g.nslices > 0 ? 1 : 0;
+    return sl | ((sl && split_slices_local(G) > 0) ? 2 : 0);
+}
+
+// Fixes the agreed protocol (caps = the AND over the ranks of dist_local_caps) and maps the
+// halo lists into position numbering when the slice path runs.
+int dist_agree(gabp_graph *G, int caps) {
+    DistState *D = G->dist;
+    D->use_slices = caps & 1;
+    D->use_split = (caps & 2) ? 1 : 0;
+    if (D->use_slices) {
+        int64_t ns = 0, nr = 0;
+        for (size_t q = 0; q < D->peers.size(); ++q) {
+            ns += (D->scount[q] + 1) & ~1ll;
+            nr += (D->rcount[q] + 1) & ~1ll;
+        }
+        CK(gabp::slice_map_index(G->g, D->d_sidx, ns, G->stream));
+        CK(gabp::slice_map_index(G->g, D->d_ridx, nr, G->stream));
+        CK(cudaStreamSynchronize(G->stream));
+    }
+    return GABP_OK;
 }
 
 // Launches of one split sweep: boundary part (exact) on st, then the interior part (fast +
@@ -676,6 +726,7 @@ int dist_finish_split(gabp_graph *G, const SweepArgs &a, cudaStream_t st, cudaSt
 int dist_launch_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
     DistState *D0 = G->dist;
     if (const int64_t nbs = split_slices(G)) {
+        D0->split_launches++;
         int rc = dist_ensure_comm(D0);
         if (rc) return rc;
         rc = dist_launch_split(G, a, nbs, st, D0->xstream);
@@ -852,6 +903,7 @@ void fill_report(gabp_graph *G, const gabp_options_t *opt, double ms, double rsq
     rep->device_ms = ms;
     rep->residual_probes = c.probes;
     rep->kernel_launches = G->kernels_launched + c.twin_launches;
+    rep->split_sweeps = G->dist ? G->dist->split_launches : 0;
     rep->final_rel_residual =
         (c.n_hist >= 1 && G->g.rhs_norm > 0.0) ? sqrt(rsq_last) / G->g.rhs_norm : NAN;
 }
@@ -933,6 +985,18 @@ int gabp_graph_create_device(int64_t n, int64_t npairs, const double *d_diag,
                              gabp_graph_t **out) {
     return create_device_range(n, npairs, d_diag, d_rhs, d_pair_i, d_pair_j, d_pair_v, 0, n,
                                device, out);
+}
+
+int gabp_graph_create_device_ex(int64_t n, int64_t npairs, const double *d_diag,
+                                const double *d_rhs, const int64_t *d_pair_i,
+                                const int64_t *d_pair_j, const double *d_pair_v,
+                                int64_t row_lo, int64_t row_hi, int32_t device,
+                                gabp_graph_t **out) {
+    if (row_lo < 0 || row_hi > n || row_lo >= row_hi)
+        return fail(GABP_EINVAL, "swept rows [%lld, %lld) outside [0, %lld)", (long long)row_lo,
+                    (long long)row_hi, (long long)n);
+    return create_device_range(n, npairs, d_diag, d_rhs, d_pair_i, d_pair_j, d_pair_v, row_lo,
+                               row_hi, device, out);
 }
 
 int gabp_graph_create(int64_t n, int64_t npairs, const double *h_diag, const double *h_rhs,
@@ -1063,6 +1127,7 @@ static void graph_release(gabp_graph *G) {
     cudaStreamSynchronize(G->stream);
     if (G->d_serial) cudaFree(G->d_serial);
     if (G->d_serial_lvl) cudaFree(G->d_serial_lvl);
+    if (G->serial_strip) cudaFree(G->serial_strip);
     if (G->serial_exec) cudaGraphExecDestroy(G->serial_exec);
     release_workspace(G);
     gabp::free_graph(G->g, G->stream);
@@ -1225,6 +1290,27 @@ int gabp_state_counters(const gabp_state_t *S, int64_t *iteration, int64_t *mess
     return GABP_OK;
 }
 
+static int absmax_bits(const gabp_graph *G, const double2 *a, unsigned long long *bits) {
+    unsigned long long *d = nullptr;
+    CK(cudaMallocAsync(&d, sizeof(unsigned long long), G->stream));
+    CK(gabp::launch_absmax(G->g.E, a, d, G->stream));
+    CK(cudaMemcpyAsync(bits, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, G->stream));
+    CK(cudaFreeAsync(d, G->stream));
+    CK(cudaStreamSynchronize(G->stream));
+    return GABP_OK;
+}
+
+// some message not finite, or the biggest |message| above blowup (solver.py:333-338)
+static int state_blown(const gabp_graph *G, const double2 *m, double blowup, int32_t *blown) {
+    unsigned long long bits = 0;
+    int rc = absmax_bits(G, m, &bits);
+    if (rc) return rc;
+    const unsigned long long inf_bits = 0x7ff0000000000000ull;
+    *blown = bits >= inf_bits || __builtin_bit_cast(double, bits) > blowup;
+    return GABP_OK;
+}
+
+
 // ---- serial schedule (solver.py:176-217) ------------------------------------------------
 // Dependency levels of a task sequence (the order): task t on node i goes one level above
 // the last task on i or on any neighbour of i; tasks of one level touch disjoint messages
@@ -1243,21 +1329,26 @@ static int serial_levels(gabp_graph *G, const int64_t *order, int64_t norder) {
             return fail(GABP_EINVAL, "serial order entry %lld out of range [0, %lld)",
                         (long long)order[t], (long long)n);
     if ((int64_t)G->h_rp.size() != n + 1) {
-        G->h_rp.resize(n + 1);
-        CK(cudaMemcpy(G->h_rp.data(), G->g.row_ptr, sizeof(uint32_t) * (n + 1),
-                      cudaMemcpyDeviceToHost));
-        G->h_col.resize(G->g.E);
-        if (G->g.E) {  // the column field only (4 B per edge through PCIe, not the record)
+        // fetched into locals and kept only when every step succeeded: the cache key is
+        // the size of h_rp, so a failed fetch must not leave a half-filled CSR behind
+        std::vector<uint32_t> rp(n + 1), col(G->g.E);
+        cudaError_t e = cudaMemcpyAsync(rp.data(), G->g.row_ptr, sizeof(uint32_t) * (n + 1),
+                                        cudaMemcpyDeviceToHost, G->stream);
+        if (e == cudaSuccess && G->g.E) {
+            // the column field only (4 B per edge through PCIe, not the record), staged in
+            // the library's stream-ordered pool
             uint32_t *dcol = nullptr;
-            CK(cudaMalloc(&dcol, sizeof(uint32_t) * G->g.E));
-            cudaError_t e = gabp::launch_edge_col(G->g.E, G->g.er, dcol, G->stream);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(G->stream);
+            e = cudaMallocAsync(&dcol, sizeof(uint32_t) * G->g.E, G->stream);
+            if (e == cudaSuccess) e = gabp::launch_edge_col(G->g.E, G->g.er, dcol, G->stream);
             if (e == cudaSuccess)
-                e = cudaMemcpy(G->h_col.data(), dcol, sizeof(uint32_t) * G->g.E,
-                               cudaMemcpyDeviceToHost);
-            cudaFree(dcol);
-            CK(e);
+                e = cudaMemcpyAsync(col.data(), dcol, sizeof(uint32_t) * G->g.E,
+                                    cudaMemcpyDeviceToHost, G->stream);
+            if (dcol) cudaFreeAsync(dcol, G->stream);
         }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(G->stream);
+        CK(e);
+        G->h_rp.swap(rp);
+        G->h_col.swap(col);
     }
     std::vector<uint32_t> last(n, 0u), lev(norder);
     uint32_t nlev = 0;
@@ -1315,9 +1406,6 @@ int gabp_sweep_serial(const gabp_graph_t *Gc, gabp_state_t *S, const int64_t *or
     if (order && norder < 0) return fail(GABP_EINVAL, "negative order length");
     if (G->g.row_lo != 0 || G->g.row_hi != G->g.n)
         return fail(GABP_EINVAL, "serial schedule needs the whole graph");
-    if (G->g.max_degree > gabp::kRowParMaxDegree)
-        return fail(GABP_EINVAL, "serial schedule: max degree %lld > %d",
-                    (long long)G->g.max_degree, gabp::kRowParMaxDegree);
     CK(cudaSetDevice(G->device));
     int rc = ensure_workspace(G, 1);
     if (rc) return rc;
@@ -1337,6 +1425,17 @@ int gabp_sweep_serial(const gabp_graph_t *Gc, gabp_state_t *S, const int64_t *or
     if (G->g.E)
         CK(cudaMemcpyAsync(msg, S->buf[S->cur], sizeof(double2) * G->g.E,
                            cudaMemcpyDeviceToDevice, G->stream));
+    if (G->g.max_degree > gabp::kRowParMaxDegree && !G->serial_strip) {
+        // tasks longer than the shared-memory strip: one global strip per warp
+        G->serial_strip_stride = (G->g.max_degree + 7) & ~7ll;
+        const int64_t warps = gabp::serial_strip_warps();
+        CK(cudaMalloc(&G->serial_strip, sizeof(double2) * G->serial_strip_stride *
+                                            (warps > 0 ? warps : 1)));
+        if (G->serial_exec) {  // captured without the strip
+            cudaGraphExecDestroy(G->serial_exec);
+            G->serial_exec = nullptr;
+        }
+    }
     const double lim = blowup < DBL_MAX ? blowup : DBL_MAX;
     const int nlev = (int)G->serial_lvl.size() - 1;
     if (nlev <= 512 && !getenv("GABP_SERIAL_LEVEL_LAUNCHES")) {
@@ -1385,7 +1484,12 @@ int gabp_sweep_serial(const gabp_graph_t *Gc, gabp_state_t *S, const int64_t *or
     S->cur ^= 1;
     S->iteration += 1;
     S->messages_sent += G->g.E;
-    if (out_of_range) *out_of_range = h.msg_nonfinite[1] ? 1 : 0;
+    if (out_of_range) {  // on the final state, as the solve loop's test reads it
+        int32_t blown = 0;
+        rc = state_blown(G, S->buf[S->cur], blowup, &blown);
+        if (rc) return rc;
+        *out_of_range = blown;
+    }
     if (max_change) {
         double v;
         unsigned long long bits = h.change_bits[1];
@@ -1429,11 +1533,11 @@ int gabp_sweep(const gabp_graph_t *Gc, gabp_state_t *S, int32_t schedule, double
         if (singular_index) *singular_index = (int64_t)h.singular_min[slot];
         return fail(GABP_ESINGULAR, "P_excl = 0 on edge %lld", (long long)h.singular_min[slot]);
     }
-    if (max_change) {
+    if (max_change) {  // NaN when a new message is NaN (np.max propagates it)
         double v;
         unsigned long long bits = h.change_bits[slot];
         memcpy(&v, &bits, sizeof(v));
-        *max_change = v;
+        *max_change = (h.msg_nonfinite[slot] & 2) ? NAN : v;
     }
     S->cur ^= 1;
     S->iteration += 1;
@@ -1441,54 +1545,43 @@ int gabp_sweep(const gabp_graph_t *Gc, gabp_state_t *S, int32_t schedule, double
     return GABP_OK;
 }
 
-// ---- acceleration (acceleration.py) --------------------------------------------------------
-
-int gabp_state_extrapolate(const gabp_state_t *x0, const gabp_state_t *x1, gabp_state_t *x2,
-                           double guard, double stability, int32_t gated) {
-    if (!x0 || !x1 || !x2) return fail(GABP_EINVAL, "NULL state");
-    if (x0->g != x2->g || x1->g != x2->g) return fail(GABP_EINVAL, "states of different graphs");
-    if (!(guard > 0.0)) return fail(GABP_EINVAL, "denom_guard must be positive");
-    const gabp_graph *G = x2->g;
-    CK(cudaSetDevice(G->device));
-    CK(gabp::launch_extrapolate(G->g.E, x0->buf[x0->cur], x1->buf[x1->cur], x2->buf[x2->cur],
-                                guard, stability, gated ? 1 : 0, G->stream));
-    CK(cudaStreamSynchronize(G->stream));
-    return GABP_OK;
-}
-
-static int absmax_bits(const gabp_graph *G, const double2 *a, const double2 *b, int which,
-                       unsigned long long *bits) {
-    unsigned long long *d = nullptr;
-    CK(cudaMallocAsync(&d, sizeof(unsigned long long), G->stream));
-    CK(gabp::launch_absmax(G->g.E, a, b, which, d, G->stream));
-    CK(cudaMemcpyAsync(bits, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, G->stream));
-    CK(cudaFreeAsync(d, G->stream));
-    CK(cudaStreamSynchronize(G->stream));
-    return GABP_OK;
-}
+// ---- whole-state checks and point reads -----------------------------------------------
 
 int gabp_state_blown(const gabp_state_t *S, double blowup, int32_t *blown) {
     if (!S || !blown) return fail(GABP_EINVAL, "NULL argument");
     CK(cudaSetDevice(S->g->device));
-    unsigned long long bits = 0;
-    const double2 *m = S->buf[S->cur];
-    int rc = absmax_bits(S->g, m, m, 0, &bits);
-    if (rc) return rc;
-    const unsigned long long inf_bits = 0x7ff0000000000000ull;
-    // not every message finite, or the biggest |message| above blowup (acceleration.py:150-155)
-    *blown = bits >= inf_bits || __builtin_bit_cast(double, bits) > blowup;
-    return GABP_OK;
+    return state_blown(S->g, S->buf[S->cur], blowup, blown);
 }
 
-int gabp_state_mean_max_diff(const gabp_state_t *a, const gabp_state_t *b, double *out) {
-    if (!a || !b || !out) return fail(GABP_EINVAL, "NULL argument");
-    if (a->g != b->g) return fail(GABP_EINVAL, "states of different graphs");
-    CK(cudaSetDevice(a->g->device));
-    unsigned long long bits = 0;
-    int rc = absmax_bits(a->g, a->buf[a->cur], b->buf[b->cur], 1, &bits);
-    if (rc) return rc;
-    // np.max(np.abs(y - y_prev), initial=0.0): NaN if any difference is NaN
-    *out = bits > 0x7ff0000000000000ull ? NAN : __builtin_bit_cast(double, bits);
+int gabp_state_gather(const gabp_state_t *S, const int64_t *h_edges, int64_t count,
+                      double *h_prec, double *h_mean) {
+    if (!S || count < 0 || (count > 0 && !h_edges)) return fail(GABP_EINVAL, "bad arguments");
+    const gabp_graph *G = S->g;
+    for (int64_t k = 0; k < count; ++k)
+        if (h_edges[k] < 0 || h_edges[k] >= G->g.E)
+            return fail(GABP_EINVAL, "edge id %lld out of range [0, %lld)",
+                        (long long)h_edges[k], (long long)G->g.E);
+    if (count == 0) return GABP_OK;
+    CK(cudaSetDevice(G->device));
+    int64_t *d_idx = nullptr;
+    double2 *d_out = nullptr;
+    CK(cudaMallocAsync(&d_idx, sizeof(int64_t) * count, G->stream));
+    CK(cudaMallocAsync(&d_out, sizeof(double2) * count, G->stream));
+    std::vector<double2> out(count);
+    cudaError_t e = cudaMemcpyAsync(d_idx, h_edges, sizeof(int64_t) * count,
+                                    cudaMemcpyHostToDevice, G->stream);
+    if (e == cudaSuccess) e = gabp::launch_gather(count, d_idx, S->buf[S->cur], d_out, G->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out.data(), d_out, sizeof(double2) * count, cudaMemcpyDeviceToHost,
+                            G->stream);
+    cudaFreeAsync(d_idx, G->stream);
+    cudaFreeAsync(d_out, G->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(G->stream);
+    CK(e);
+    for (int64_t k = 0; k < count; ++k) {
+        if (h_prec) h_prec[k] = out[k].x;
+        if (h_mean) h_mean[k] = out[k].y;
+    }
     return GABP_OK;
 }
 
@@ -1628,19 +1721,28 @@ int gabp_dist_attach(gabp_graph_t *G, const void *nccl_id, int32_t rank, int32_t
     CK(cudaMalloc(&D->d_stats, sizeof(double) * 8));
     CK(cudaMemcpy(D->d_sidx, si.data(), sizeof(uint32_t) * si.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(D->d_ridx, ri.data(), sizeof(uint32_t) * ri.size(), cudaMemcpyHostToDevice));
-    if (dist_gather(G) == gabp::kGatherSlice) {  // halo lists in position numbering
-        CK(gabp::slice_map_index(G->g, D->d_sidx, ns, G->stream));
-        CK(gabp::slice_map_index(G->g, D->d_ridx, nr, G->stream));
-        CK(cudaStreamSynchronize(G->stream));
-    }
-    if (!D->local && world > 1) {
+    if (D->local) return GABP_OK;  // agreed over the partitions by gabp_dist_solve_local
+    int caps = dist_local_caps(G);
+    if (world > 1) {
         int rc = load_nccl();
         if (rc) return rc;
         ncclUniqueId id;
         memcpy(&id, nccl_id, sizeof(id));
         NK(g_nccl.commInitRank(&D->comm, world, id, rank));
+        // one small all-reduce (min) of the capability bits: every rank then runs the same
+        // kernel family and issues the same NCCL call sequence each sweep
+        int32_t *d_caps = nullptr;
+        CK(cudaMalloc(&d_caps, sizeof(int32_t) * 2));
+        const int32_t hc[2] = {caps & 1, (caps >> 1) & 1};
+        CK(cudaMemcpy(d_caps, hc, sizeof(hc), cudaMemcpyHostToDevice));
+        NK(g_nccl.allReduce(d_caps, d_caps, 2, ncclInt32, ncclMin, D->comm, G->stream));
+        int32_t ag[2] = {0, 0};
+        CK(cudaMemcpyAsync(ag, d_caps, sizeof(ag), cudaMemcpyDeviceToHost, G->stream));
+        CK(cudaStreamSynchronize(G->stream));
+        cudaFree(d_caps);
+        caps = (ag[0] ? 1 : 0) | (ag[1] ? 2 : 0);
     }
-    return GABP_OK;
+    return dist_agree(G, caps);
 }
 
 // One GPU, several row blocks in this process: the multi-rank loop with the cross-rank
@@ -1656,6 +1758,14 @@ int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_optio
     if (opt && opt->schedule != GABP_SCHED_BROADCAST)
         return fail(GABP_EINVAL, "the multi-rank solve runs the broadcast schedule");
     std::vector<SweepArgs> args(nparts);
+    if (parts[0]->dist->use_slices < 0) {  // first solve: agree on the protocol (AND of caps)
+        int caps = 3;
+        for (int p = 0; p < nparts; ++p) caps &= dist_local_caps(parts[p]);
+        for (int p = 0; p < nparts; ++p) {
+            int rc = dist_agree(parts[p], caps);
+            if (rc) return rc;
+        }
+    }
     for (int p = 0; p < nparts; ++p) {
         int rc = solve_setup(parts[p], opt);
         if (rc) return rc;
@@ -1668,6 +1778,7 @@ int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_optio
     for (int64_t s = 0; s < total; ++s) {
         for (int p = 0; p < nparts; ++p) {
             if (const int64_t nbs = split_slices(parts[p])) {  // the NCCL path's split sweep
+                parts[p]->dist->split_launches++;
                 SweepArgs b = args[p], in = args[p];
                 b.sl_hi = nbs;
                 int64_t gb = 0;

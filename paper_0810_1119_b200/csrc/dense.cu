@@ -351,7 +351,8 @@ __device__ __forceinline__ void pair_stat(double2 nw, double2 old, double pe, in
     }
     const double d1 = fabs(nw.x - old.x), d2 = fabs(nw.y - old.y);
     ps.chg = fmax(ps.chg, fmax(d1, d2));
-    if (!(fabs(nw.x) <= lim) || !(fabs(nw.y) <= lim)) ps.oor = 1u;
+    if (!(fabs(nw.x) <= lim) || !(fabs(nw.y) <= lim))
+        ps.oor |= (nw.x != nw.x || nw.y != nw.y) ? 3u : 1u;  // bit 1: a NaN change
 }
 
 // The tile pair's 32 x 32 elements of one thread column (rows ty + kPairWarps m): both
@@ -502,7 +503,7 @@ __global__ void __launch_bounds__(kPairCta) dense_pair_kernel(const SweepArgs a,
         const int slot = (int)(s % kStatSlots);
         if (bc > 0.0)
             atomicMax(&ctrl->change_bits[slot], (unsigned long long)__double_as_longlong(bc));
-        if (f) atomicOr(&ctrl->msg_nonfinite[slot], 1);
+        if (f) atomicOr(&ctrl->msg_nonfinite[slot], (f & 2u) ? 3 : 1);
         __threadfence();
         const unsigned tkt = atomicAdd(&ctrl->ticket, 1u);
         S.last = (tkt == gridDim.x - 1);

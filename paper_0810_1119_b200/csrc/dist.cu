@@ -20,7 +20,7 @@ __global__ void finish_kernel(const SweepArgs a) {
     const int mslot = (int)((s - a.msg_lag) % kStatSlots);  // sweep of the message stats
     const double *d = a.dstats;
     c->change_bits[mslot] = (unsigned long long)__double_as_longlong(d[0]);
-    c->msg_nonfinite[mslot] = d[1] > 0.0 ? 1 : 0;
+    c->msg_nonfinite[mslot] = (int32_t)d[1];
     c->means_nonfinite[(s - 1) % kStatSlots] = d[2] > 0.0 ? 1 : 0;
     c->singular_min[mslot] = d[3] > -1e299 ? (unsigned long long)(-d[3]) : kNoIndex;
     c->agg_singular[slot] = d[4] > -1e299 ? (unsigned long long)(-d[4]) : kNoIndex;

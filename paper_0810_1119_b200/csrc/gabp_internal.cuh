@@ -91,7 +91,8 @@ struct Ctrl {
     int64_t n;
     // per-sweep statistics, slot = sweep % kStatSlots
     unsigned long long change_bits[kStatSlots];   // max |dP|,|dmu| (non-negative -> bit order)
-    int32_t msg_nonfinite[kStatSlots];            // some |message| > blowup or not finite
+    int32_t msg_nonfinite[kStatSlots];            // bit 0: some |message| > blowup or not
+                                                  // finite; bit 1: some change is NaN
     int32_t means_nonfinite[kStatSlots];
     unsigned long long agg_singular[kStatSlots];   // broadcast: first node with P_i == 0
     unsigned long long singular_min[kStatSlots];   // first edge with P_excl == 0
@@ -134,6 +135,8 @@ struct SweepArgs {
     double *x[3];
     double *p[3];
     double *rsq_part;   // [>= persistent grid] per-CTA residual partials
+    double *rsq_grp;    // [groups] residual partial of each slice group (kernels that claim
+                        // groups dynamically: the sum must not depend on which CTA ran one)
     Ctrl *ctrl;
     double *change_hist;
     double *res_hist;
@@ -158,6 +161,8 @@ struct SweepArgs {
     // slice layout (slice.cu): lane-per-row broadcast solve, nodes in position order
     int64_t nslices;
     const uint2 *slice_info;   // {slot base, width} per slice of 32 rows (group width)
+    const uint32_t *gorder;    // claim order of the groups: widest first inside the boundary
+                               // and the interior range (null: ascending group ids)
     const uint32_t *sdeg;      // degree per position
     const uint32_t *srow;      // local row per position (~0: padding / halo)
     const double2 *snd;        // {A_ii, A_ii mu_ii} per position
@@ -169,6 +174,8 @@ struct SweepArgs {
                                // residual-only group launch (probe_next)
     int probe_force;           // test hook (GABP_PROBE_FORCE=1): request a probe after every
                                // launch, so every mispredicted probe path runs
+    double2 *strip;            // serial tasks longer than kRowParMaxDegree: per-warp global
+    int64_t strip_stride;      // strips of strip_stride terms (else unused)
     int twin_tail;             // group launch: the exact twin is tail-launched from the
     int twin_grid;             // device only when the launch flags itself (slice.cu)
 };
@@ -184,6 +191,9 @@ cudaError_t launch_sweep(const SweepArgs &a, int schedule, int mode, int gather,
 // parallel schedule, warp per row over the CSR order (rowpar.cu); rows of at most
 // kRowParMaxDegree edges (the per-warp strip of incoming terms)
 constexpr int kRowParMaxDegree = 256;
+// serial tasks of more than kRowParMaxDegree edges: warps of the serial kernels (either
+// launch form) that may need a global strip of SweepArgs::strip_stride terms each
+int64_t serial_strip_warps();
 cudaError_t prepare_rowpar_kernels();
 cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st);
 // serial schedule: one dependency level of tasks {node, order position}, in place on the
@@ -244,9 +254,10 @@ __device__ __forceinline__ void decide_sweep(volatile Ctrl *c, SweepArgs const &
         c->done = 1;
         return;
     }
-    // max change over the finite differences (a NaN difference, possible only when a
-    // message is non-finite -- the run is then diverged -- is not propagated)
-    const double change = __longlong_as_double((long long)k.change_bits);
+    // max change; NaN when a new message is NaN, as np.max propagates it (solver.py:161-165,
+    // 262-266) -- the old messages are finite in every sweep the loop still accepts
+    const double change =
+        (k.msg_nonfinite & 2) ? NAN : __longlong_as_double((long long)k.change_bits);
     const bool means_finite = !k.means_nonfinite;
     const double res = means_finite ? sqrt(rsq_t) / (double)k.n : INFINITY;
     a.change_hist[t - 1] = change;
@@ -318,13 +329,11 @@ cudaError_t launch_dense_sweep(const SweepArgs &a, const DenseArgs &d, cudaStrea
 cudaError_t launch_dense_mask(const double *A, int64_t ld, uint32_t *emask, cudaStream_t st);
 cudaError_t launch_dense_init(const uint32_t *emask, int64_t ld, double2 *msg, cudaStream_t st);
 
-// acceleration (accel.cu): gated Aitken restart of the mean messages, in place in m2
-// (gated = 0: plain aitken_extrapolate); max |.| reductions as ordered bit patterns
-// (which = 0: both components of a, 1: |a.mu - b.mu|), result in *d_out
-cudaError_t launch_extrapolate(int64_t E, const double2 *m0, const double2 *m1, double2 *m2,
-                               double guard, double stability, int gated, cudaStream_t st);
-cudaError_t launch_absmax(int64_t E, const double2 *a, const double2 *b, int which,
-                          unsigned long long *d_out, cudaStream_t st);
+// |message| maximum of a state as an ordered bit pattern (NaN > +inf > finite), state.cu
+cudaError_t launch_absmax(int64_t E, const double2 *a, unsigned long long *d_out,
+                          cudaStream_t st);
+cudaError_t launch_gather(int64_t cnt, const int64_t *idx, const double2 *m, double2 *out,
+                          cudaStream_t st);
 
 // multi-rank helpers (dist.cu)
 cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st);
@@ -355,6 +364,7 @@ struct DeviceGraph {
     int64_t bnd_groups = 0;     // multi-rank: leading groups holding the boundary rows
     int slice_variant = 2;      // 0: register batches, 1: cp.async ring, 2: group TMA ring
     uint2 *slice_info = nullptr;
+    uint32_t *gorder = nullptr; // groups by width, descending (claim order of the TMA kernels)
     uint32_t *pos = nullptr;    // local row -> position
     uint32_t *srow = nullptr, *sdeg = nullptr;
     double2 *snd = nullptr;

@@ -378,10 +378,13 @@ __global__ void __launch_bounds__(kRThreads, 2) rowpar_kernel(const SweepArgs a)
 // task's d exclusion sums run one per lane as in rowpar_kernel (rows <= 256 edges).
 // One serial task {node, order position}: node i's outgoing messages from its current
 // incoming ones, in place on msg (solver.py:181-209).
+// Tasks longer than the shared-memory strip (kRowParMaxDegree) keep their terms in the
+// warp's slice of a global scratch strip (a.strip, gw = the warp's global index).
 __device__ __forceinline__ void serial_task(const SweepArgs &a, double2 *msg, uint2 tk,
-                                            double2 *T, int lane, Stats &st) {
+                                            double2 *Tsm, int64_t gw, int lane, Stats &st) {
     const uint32_t i = tk.x;
     const uint32_t e0 = __ldg(a.row_ptr + i), d = __ldg(a.row_ptr + i + 1) - e0;
+    double2 *T = d > (uint32_t)kRowParMaxDegree ? a.strip + gw * a.strip_stride : Tsm;
     const double2 nd = __ldg(reinterpret_cast<const double2 *>(a.nd + i));
     const uint32_t dpad = (d + 7u) & ~7u;
     for (uint32_t q = lane; q < dpad; q += 32) {
@@ -459,9 +462,9 @@ __global__ void __launch_bounds__(kRThreads, 2) serial_level_kernel(const SweepA
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     Stats st;
     st.lim = lim;
-    const int64_t nw = (int64_t)gridDim.x * kRWarps;
-    for (int64_t w = (int64_t)blockIdx.x * kRWarps + warp; w < cnt; w += nw)
-        serial_task(a, msg, __ldg(tasks + w), S.T[warp], lane, st);
+    const int64_t nw = (int64_t)gridDim.x * kRWarps, gw = (int64_t)blockIdx.x * kRWarps + warp;
+    for (int64_t w = gw; w < cnt; w += nw)
+        serial_task(a, msg, __ldg(tasks + w), S.T[warp], gw, lane, st);
     __syncthreads();
     sweep_epilogue<kRThreads, kModeSingle, 0>(S.tail, a, 1, false, st, tid);
 }
@@ -485,7 +488,7 @@ __global__ void __launch_bounds__(kRThreads, 2) serial_sweep_kernel(const SweepA
     for (int l = 0; l < nlev; ++l) {
         const int64_t lo = __ldg(lvl + l), cnt = __ldg(lvl + l + 1) - lo;
         for (int64_t w = gw; w < cnt; w += nw)
-            serial_task(a, msg, __ldg(tasks + lo + w), S.T[warp], lane, st);
+            serial_task(a, msg, __ldg(tasks + lo + w), S.T[warp], gw, lane, st);
         if (l + 1 < nlev) grid_barrier(a.ctrl, gridDim.x);
     }
     __syncthreads();
@@ -500,7 +503,15 @@ __global__ void edge_col_kernel(int64_t E, const EdgeRec *er, uint32_t *col) {
         col[e] = __ldg(&er[e].col);
 }
 
-int g_row_grid[2] = {0, 0};
+constexpr int kMaxDevices = 64;
+int g_row_grid[kMaxDevices][2] = {};   // persistent grids per device (prepare_rowpar_kernels)
+int g_coop_grid[kMaxDevices] = {};     // cooperative serial sweep: every CTA resident
+
+int cur_dev() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d >= 0 && d < kMaxDevices ? d : 0;
+}
 
 }  // namespace
 
@@ -514,22 +525,34 @@ cudaError_t prepare_rowpar_kernels() {
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpar_kernel<kModeSolve>,
                                                            kRThreads, 0)) != cudaSuccess)
         return e;
-    g_row_grid[kModeSolve] = sms * (occ > 0 ? occ : 1);
+    const int dv = dev >= 0 && dev < kMaxDevices ? dev : 0;
+    g_row_grid[dv][kModeSolve] = sms * (occ > 0 ? occ : 1);
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpar_kernel<kModeSingle>,
                                                            kRThreads, 0)) != cudaSuccess)
         return e;
-    g_row_grid[kModeSingle] = sms * (occ > 0 ? occ : 1);
+    g_row_grid[dv][kModeSingle] = sms * (occ > 0 ? occ : 1);
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, serial_sweep_kernel, kRThreads,
+                                                           0)) != cudaSuccess)
+        return e;
+    g_coop_grid[dv] = sms * (occ > 0 ? occ : 1);
     return cudaSuccess;
 }
 
 cudaError_t launch_serial_level(const SweepArgs &a, const uint2 *tasks, int64_t cnt, double lim,
                                 cudaStream_t st) {
     if (cnt <= 0) return cudaSuccess;
-    int64_t grid = g_row_grid[kModeSingle] > 0 ? g_row_grid[kModeSingle] : 148 * 2;
+    const int dv = cur_dev();
+    int64_t grid = g_row_grid[dv][kModeSingle] > 0 ? g_row_grid[dv][kModeSingle] : 148 * 2;
     const int64_t need = (cnt + kRWarps - 1) / kRWarps;
     if (grid > need) grid = need;
     serial_level_kernel<<<(unsigned)grid, kRThreads, 0, st>>>(a, tasks, cnt, lim);
     return cudaGetLastError();
+}
+
+int64_t serial_strip_warps() {
+    const int dv = cur_dev();
+    const int64_t a = g_coop_grid[dv], b = g_row_grid[dv][kModeSingle];
+    return (a > b ? a : b) * kRWarps;
 }
 
 cudaError_t launch_edge_col(int64_t E, const EdgeRec *er, uint32_t *col, cudaStream_t st) {
@@ -541,19 +564,9 @@ cudaError_t launch_edge_col(int64_t E, const EdgeRec *er, uint32_t *col, cudaStr
 cudaError_t launch_serial_sweep(const SweepArgs &a, const uint2 *tasks, const int64_t *lvl,
                                 int nlev, int64_t max_cnt, double lim, cudaStream_t st) {
     if (nlev <= 0) return cudaSuccess;
-    static int coop_grid = 0;
-    if (coop_grid == 0) {
-        int dev = 0, sms = 0, occ = 0;
-        cudaError_t e;
-        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
-            return e;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, serial_sweep_kernel,
-                                                               kRThreads, 0)) != cudaSuccess)
-            return e;
-        coop_grid = sms * (occ > 0 ? occ : 1);
-    }
-    int64_t grid = coop_grid;
+    const int dv = cur_dev();
+    if (g_coop_grid[dv] <= 0) return cudaErrorInitializationError;  // prepare_rowpar_kernels
+    int64_t grid = g_coop_grid[dv];
     const int64_t need = (max_cnt + kRWarps - 1) / kRWarps;
     if (grid > need) grid = need > 0 ? need : 1;
     void *args[] = {(void *)&a, (void *)&tasks, (void *)&lvl, (void *)&nlev, (void *)&lim};
@@ -564,7 +577,8 @@ cudaError_t launch_serial_sweep(const SweepArgs &a, const uint2 *tasks, const in
 cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st) {
     if (a.ntiles <= 0) return cudaSuccess;
     const int m = mode == kModeSolve ? kModeSolve : kModeSingle;
-    int64_t grid = g_row_grid[m] > 0 ? g_row_grid[m] : 148 * 4;
+    const int dv = cur_dev();
+    int64_t grid = g_row_grid[dv][m] > 0 ? g_row_grid[dv][m] : 148 * 4;
     const int64_t need = (a.ntiles + kRWarps - 1) / kRWarps;
     if (grid > need) grid = need;
     if (m == kModeSolve)

@@ -95,15 +95,16 @@ __device__ __forceinline__ void msg_stats(Stats &st, const SweepArgs &a, double 
                                           double2 i2, double pe, int64_t p, uint32_t q) {
     const double d1 = fabs(ip - i2.x), d2 = fabs(im - i2.y);
     st.chg = fmax(st.chg, fmax(d1, d2));  // NaN differences ignored, as '>' ignores them
-    if (!(fabs(ip) <= st.lim) || !(fabs(im) <= st.lim)) st.out_of_range = 1u;
+    if (!(fabs(ip) <= st.lim) || !(fabs(im) <= st.lim))
+        st.out_of_range |= (ip != ip || im != im) ? 3u : 1u;  // bit 1: a NaN change
     if (EXACT && pe == 0.0) st.sing = min(st.sing, twin_edge(a, p, q));
 }
 
 // Row done: marginal of S_{s-1} and the node state record (solver.py:247-255, 286).
-template <int PH, bool EXACT>
-__device__ __forceinline__ void node_done(Stats &st, const SweepArgs &a, NodeState *rec1,
-                                          double *xh, int64_t p, double sp, double sn, double y,
-                                          double rhs_i) {
+template <int PH, bool EXACT, bool ACC = true>
+__device__ __forceinline__ double node_done(Stats &st, const SweepArgs &a, NodeState *rec1,
+                                            double *xh, int64_t p, double sp, double sn,
+                                            double y, double rhs_i) {
     const double xi = qdiv<EXACT>(sn, sp, st);
     if (!(fabs(xi) <= DBL_MAX)) st.means_bad = 1u;
     if (xh) xh[__ldg(a.srow + p)] = xi;
@@ -112,8 +113,10 @@ __device__ __forceinline__ void node_done(Stats &st, const SweepArgs &a, NodeSta
     st_node(rec1 + p, sp, sp * xi, xi);  // (sum_p * mu_tilde)
     if (PH == 3) {
         const double r = y - rhs_i;
-        st.rsq += r * r;
+        if (ACC) st.rsq += r * r;
+        return r * r;
     }
+    return 0.0;
 }
 
 // Ring pointers of launch s, R = s % 3 as a constant (kernel-parameter loads).
@@ -536,12 +539,41 @@ struct __align__(16) GMeta {
     uint32_t gbase;       // first slot of the group
     uint32_t pad[3];
 };
+constexpr int kGResSlots = 8;  // groups a CTA's consumers can be apart (< kGS + 2)
+static_assert(kGResSlots >= kGS + 2, "residual slots must outlast the ring's lag");
 struct __align__(128) GRing {
     GStage st[kGS];
     uint64_t full[kGS];
     uint64_t empty[kGS];
     GMeta meta[kGS];
+    double gres[kGResSlots][kGroup];  // slice partials of a group's residual rows
+    uint32_t gcnt[kGResSlots];        // slices committed
 };
+
+// Residual of group g (the seq-th group this CTA ran): every consumer warp sums its slice's
+// rows (fixed shuffle tree) and the last of the kGroup warps adds the slice partials in
+// slice order into rsq_grp[g].  The launch total is then a sum in group order: the same
+// bits whichever CTA claimed which group (the claims are dynamic).
+__device__ __forceinline__ void grp_resid_commit(const SweepArgs &a, GRing &G, int warp,
+                                                 int lane, int64_t g, uint32_t seq, double rr) {
+    rr = warp_sum(rr);
+    const int k = (int)(seq % kGResSlots);
+    unsigned last = 0u;
+    if (lane == 0) {
+        G.gres[k][warp] = rr;
+        __threadfence_block();
+        last = atomicAdd(&G.gcnt[k], 1u) == (unsigned)kGroup - 1u ? 1u : 0u;
+        if (last) {
+            __threadfence_block();
+            volatile const double *v = G.gres[k];
+            double b = 0.0;
+#pragma unroll
+            for (int w = 0; w < kGroup; ++w) b += v[w];
+            a.rsq_grp[g] = b;
+            G.gcnt[k] = 0u;
+        }
+    }
+}
 constexpr size_t kGrpSmem = sizeof(GRing);
 
 __device__ __forceinline__ void t_mbar_init(uint64_t *bar, unsigned count) {
@@ -573,8 +605,23 @@ __device__ __forceinline__ void t_bulk_ef(void *dst, const void *src, unsigned b
         : "memory");
 }
 
+__device__ __forceinline__ void grp_ring_init(GRing &G, int tid) {
+    if (tid < kGS) {
+        t_mbar_init(&G.full[tid], 1u);
+        t_mbar_init(&G.empty[tid], (unsigned)kGroup);
+    }
+    if (tid < kGResSlots) G.gcnt[tid] = 0u;
+}
+
 __device__ __forceinline__ uint2 group_info(const SweepArgs &a, int64_t g, int64_t g_hi) {
     return g < g_hi ? __ldg(a.slice_info + g * kGroup) : make_uint2(0u, 0u);
+}
+// group of claim c (c counts from the launch's first group): the claim order lists the
+// widest groups first (gorder), so the last claims of a launch are its shortest units;
+// g_hi (no group) once the claims run out
+__device__ __forceinline__ int64_t claim_group(const SweepArgs &a, int64_t c, int64_t g_hi) {
+    if (c >= g_hi) return g_hi;
+    return a.gorder ? (int64_t)__ldg(a.gorder + c) : c;
 }
 template <int CW = kGC>
 __device__ __forceinline__ uint32_t chunks_of(uint32_t w) {
@@ -638,7 +685,8 @@ __device__ __forceinline__ void grp_produce(const SweepArgs &a, GRing &G, uint32
         u1 = atomicAdd(ctr, 1u);
         pend = atomicAdd(ctr, 1u);
     }
-    int64_t gcur = g_lo + __shfl_sync(~0u, u0, 0), gnxt = g_lo + __shfl_sync(~0u, u1, 0);
+    int64_t gcur = claim_group(a, g_lo + __shfl_sync(~0u, u0, 0), ngroups),
+            gnxt = claim_group(a, g_lo + __shfl_sync(~0u, u1, 0), ngroups);
     uint2 icur = group_info(a, gcur, ngroups), inxt = group_info(a, gnxt, ngroups);
     constexpr int CW = stage_cw<PH>();
     uint32_t b = 0, nb = chunks_of<CW>(icur.y);
@@ -683,7 +731,7 @@ __device__ __forceinline__ void grp_produce(const SweepArgs &a, GRing &G, uint32
         if (++b >= nb) {  // next group: claimed two groups ago, descriptor loaded one ago
             gcur = gnxt;
             icur = inxt;
-            gnxt = g_lo + __shfl_sync(~0u, pend, 0);
+            gnxt = claim_group(a, g_lo + __shfl_sync(~0u, pend, 0), ngroups);
             inxt = group_info(a, gnxt, ngroups);
             if (lane == 0) pend = atomicAdd(ctr, 1u);
             b = 0;
@@ -733,7 +781,7 @@ __device__ __forceinline__ void t_gather(const GStage &S, const GMeta &m, const 
 
 // Running sums of the rows a consumer lane owns (one row per group).
 struct GRow {
-    uint32_t d = 0;
+    uint32_t d = 0, seq = 0;
     double2 a3 = make_double2(0.0, 0.0);
     double sp = 0.0, sn = 0.0, y = 0.0, rhs_i = 0.0, diag = 0.0;
 };
@@ -811,8 +859,14 @@ __device__ __forceinline__ bool grp_step(const SweepArgs &a, const Ring<R> &r, d
             msg_stats<false>(st, a, ip[u], im[u], i2v[u], pe[u], p, q);
         }
     }
-    if (m.b + 1 == m.nb && row.diag != 0.0)  // row done (A_ii == 0: padding lane)
-        node_done<(PH == 4 ? 3 : PH), false>(st, a, r.g1, xh, p, row.sp, row.sn, row.y, row.rhs_i);
+    if (m.b + 1 == m.nb) {  // rows done (A_ii == 0: padding lane)
+        double rr = 0.0;
+        if (row.diag != 0.0)
+            rr = node_done<(PH == 4 ? 3 : PH), false, false>(st, a, r.g1, xh, p, row.sp, row.sn,
+                                                             row.y, row.rhs_i);
+        if (PH == 3 || PH == 4) grp_resid_commit(a, G, warp, lane, m.g, row.seq, rr);
+        row.seq++;
+    }
     if (mn.g < 0) return false;
     m = mn;
     return true;
@@ -887,7 +941,7 @@ __device__ __forceinline__ void grp_consume_res(const SweepArgs &a, Stats &st, i
         live[q] = more;
     }
     if (!live[0]) return;
-    uint32_t d = 0;
+    uint32_t d = 0, seq = 0;
     double y = 0.0, rhs_i = 0.0, diag = 0.0;
     for (uint32_t k = 0;; k += kRD) {
 #pragma unroll
@@ -905,9 +959,9 @@ __device__ __forceinline__ void grp_consume_res(const SweepArgs &a, Stats &st, i
 #pragma unroll
             for (int u = 0; u < CW; ++u)
                 if (m.b * CW + u < d) y = y + cv[q][u] * xv[q][u];
-            if (m.b + 1 == m.nb && diag != 0.0) {
-                const double rr = y - rhs_i;
-                st.rsq += rr * rr;
+            if (m.b + 1 == m.nb) {
+                const double rr = diag != 0.0 ? y - rhs_i : 0.0;
+                grp_resid_commit(a, G, warp, lane, m.g, seq++, rr * rr);
             }
             if (more) more = issue(k + kRD + q, q);
             live[q] = more;
@@ -985,6 +1039,7 @@ __device__ __forceinline__ void probe_finish(TailSmem<NT / 32> &T, const SweepAr
     double part = 0.0;
     volatile const double *rp = a.rsq_part;
     for (int64_t b = tid; b < (int64_t)gridDim.x; b += NT) part += rp[b];
+    if (work_slot >= 0) part += group_resid_part<NT>(a, tid);  // (group launch)
     part = warp_sum(part);
     __syncthreads();
     if (lane == 0) T.red_d[0][warp] = part;
@@ -1110,10 +1165,7 @@ __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_grp(const SweepArgs
     if (!slice_prologue(S, a, false)) return;
     const int64_t s = S.sweep;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid < kGS) {
-        t_mbar_init(&G.full[tid], 1u);
-        t_mbar_init(&G.empty[tid], (unsigned)kGroup);
-    }
+    grp_ring_init(G, tid);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
     uint32_t *ctr = &a.ctrl->work[s % kStatSlots];
@@ -1145,7 +1197,8 @@ __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_grp(const SweepArgs
     } else {
         slice_first<kGroup + 1, false>(a, s, st, lane);
     }
-    const bool flagged = sweep_epilogue<kGThreads, kModeSolve, 1>(S.tail, a, s, s >= 3, st, tid);
+    const bool flagged =
+        sweep_epilogue<kGThreads, kModeSolve, 1, true>(S.tail, a, s, s >= 3, st, tid);
     if (flagged && a.twin_tail) {
         // a fast-path division left its range: the exact twin redoes this sweep, launched
         // from here into the tail of this grid (CUDA dynamic parallelism) -- it runs after
@@ -1213,7 +1266,8 @@ __device__ __forceinline__ void par_produce(const SweepArgs &a, GRing &G, uint32
         u1 = atomicAdd(ctr, 1u);
         pend = atomicAdd(ctr, 1u);
     }
-    int64_t gcur = g_lo + __shfl_sync(~0u, u0, 0), gnxt = g_lo + __shfl_sync(~0u, u1, 0);
+    int64_t gcur = claim_group(a, g_lo + __shfl_sync(~0u, u0, 0), ngroups),
+            gnxt = claim_group(a, g_lo + __shfl_sync(~0u, u1, 0), ngroups);
     uint2 icur = group_info(a, gcur, ngroups), inxt = group_info(a, gnxt, ngroups);
     uint32_t q0 = 0, pass = 0, np = par_passes(icur.y);
     for (uint32_t k = 0;; ++k) {
@@ -1267,7 +1321,7 @@ __device__ __forceinline__ void par_produce(const SweepArgs &a, GRing &G, uint32
                 pass = 0;
                 gcur = gnxt;
                 icur = inxt;
-                gnxt = g_lo + __shfl_sync(~0u, pend, 0);
+                gnxt = claim_group(a, g_lo + __shfl_sync(~0u, pend, 0), ngroups);
                 inxt = group_info(a, gnxt, ngroups);
                 if (lane == 0) pend = atomicAdd(ctr, 1u);
                 np = par_passes(icur.y);
@@ -1327,6 +1381,7 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
     if (m.g < 0) return;
     ParRow row;
     THdr hn;
+    uint32_t seq = 0;  // groups this CTA ran (residual slots)
     const int64_t p_first = ((int64_t)m.g * kGroup + warp) * 32 + lane;
     hn.nd = __ldg(a.snd + p_first);
     hn.d = __ldg(a.sdeg + p_first);
@@ -1417,7 +1472,7 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
                         const double d1 = fabs(v.x - o.x), d2 = fabs(v.y - o.y);
                         st.chg = fmax(st.chg, fmax(d1, d2));
                         if (!(fabs(v.x) <= st.lim) || !(fabs(v.y) <= st.lim))
-                            st.out_of_range = 1u;
+                            st.out_of_range |= (v.x != v.x || v.y != v.y) ? 3u : 1u;
                     }
                     par_accum(row, q, blk, vP, vN);
                 }
@@ -1451,15 +1506,20 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
                         st.agg_sing = min(st.agg_sing, a.row_ptr[__ldg(a.srow + p)] + j);
                 }
             }
-            if (pass == 0 && row.pP != 0.0) {  // marginal of S_{s-1}, residual of x^{(s-2)}
-                const double xi = qdiv<EXACT>(row.sn, row.sp, st);
-                if (!(fabs(xi) <= DBL_MAX)) st.means_bad = 1u;
-                if (xh) xh[__ldg(a.srow + p)] = xi;
-                st_node(g1 + p, row.sp, row.sp * xi, xi);
-                if (RESID) {
-                    const double r = row.y - row.rhs_i;
-                    st.rsq += r * r;
+            if (pass == 0) {  // marginal of S_{s-1}, residual of x^{(s-2)}
+                double rr = 0.0;
+                if (row.pP != 0.0) {
+                    const double xi = qdiv<EXACT>(row.sn, row.sp, st);
+                    if (!(fabs(xi) <= DBL_MAX)) st.means_bad = 1u;
+                    if (xh) xh[__ldg(a.srow + p)] = xi;
+                    st_node(g1 + p, row.sp, row.sp * xi, xi);
+                    if (RESID) {
+                        const double r = row.y - row.rhs_i;
+                        rr = r * r;
+                    }
                 }
+                if (RESID) grp_resid_commit(a, G, warp, lane, m.g, seq, rr);
+                seq++;
             }
         }
         if (mn.g < 0) break;
@@ -1480,10 +1540,7 @@ __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_par(const SweepArgs
     }
     const int64_t s = S.sweep;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid < kGS) {
-        t_mbar_init(&G.full[tid], 1u);
-        t_mbar_init(&G.empty[tid], (unsigned)kGroup);
-    }
+    grp_ring_init(G, tid);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
     uint32_t *ctr = EXACT ? &a.ctrl->work_twin : &a.ctrl->work[s % kStatSlots];
@@ -1509,7 +1566,7 @@ __global__ void __launch_bounds__(kGThreads, 1) slice_kernel_par(const SweepArgs
         else
             par_consume<false, false, EXACT>(a, s, st, lane, warp, G, g2, g1, I0);
     }
-    sweep_epilogue<kGThreads, kModeSolve, 1>(S.tail, a, s, s >= 3, st, tid);
+    sweep_epilogue<kGThreads, kModeSolve, 1, true>(S.tail, a, s, s >= 3, st, tid);
 }
 
 int g_grid_ldg = 0, g_grid_pipe = 0, g_grid_grp = 0, g_grid_par = 0;
@@ -1575,6 +1632,19 @@ __global__ void slice_info_kernel(int64_t nslices, const unsigned long long *gsl
     const int64_t g = sl / kGroup;
     info[sl] = make_uint2((uint32_t)(gbase[g] + 32 * (sl % kGroup)),
                           (uint32_t)(gslots[g] / kStride));
+}
+
+// claim-order key of every group: boundary groups first (split sweeps claim them in a
+// launch of their own), then by width, descending -- the degree sort runs inside windows of
+// kSortWin rows, so the last window would otherwise start over with wide groups and leave
+// the launch a tail of its longest work units
+__global__ void gorder_key_kernel(int64_t ngroups, int64_t bnd_groups, const uint2 *info,
+                                  uint32_t *key, uint32_t *ids) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ngroups) return;
+    const uint32_t w = info[g * kGroup].y;
+    key[g] = ((g < bnd_groups ? 0u : 1u) << kDegBits) | ((1u << kDegBits) - 1u - w);
+    ids[g] = (uint32_t)g;
 }
 
 // position of every local node: owned rows by the sort, halo rows after the slices
@@ -1736,6 +1806,26 @@ int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
         if (g.slice_variant < 0 || g.slice_variant > 2) g.slice_variant = 2;
         slice_info_kernel<<<grid_of(nslices), 256, 0, st>>>(nslices, gslots, gbase,
                                                             g.slice_info);
+        {  // claim order: (boundary, interior) x width descending, stable
+            uint32_t *gk = nullptr, *gk2 = nullptr, *gid = nullptr;
+            SCHECK(cudaMallocAsync(&g.gorder, sizeof(uint32_t) * ngroups, st));
+            SCHECK(cudaMallocAsync(&gk, sizeof(uint32_t) * ngroups, st));
+            SCHECK(cudaMallocAsync(&gk2, sizeof(uint32_t) * ngroups, st));
+            SCHECK(cudaMallocAsync(&gid, sizeof(uint32_t) * ngroups, st));
+            gorder_key_kernel<<<grid_of(ngroups), 256, 0, st>>>(ngroups, g.bnd_groups,
+                                                                g.slice_info, gk, gid);
+            size_t ob = 0;
+            SCHECK(cub::DeviceRadixSort::SortPairs(nullptr, ob, gk, gk2, gid, g.gorder,
+                                                   ngroups, 0, kDegBits + 1, st));
+            void *otmp = nullptr;
+            SCHECK(cudaMallocAsync(&otmp, ob, st));
+            SCHECK(cub::DeviceRadixSort::SortPairs(otmp, ob, gk, gk2, gid, g.gorder, ngroups,
+                                                   0, kDegBits + 1, st));
+            cudaFreeAsync(otmp, st);
+            cudaFreeAsync(gk, st);
+            cudaFreeAsync(gk2, st);
+            cudaFreeAsync(gid, st);
+        }
         const int64_t big = m > g.n - m ? m : g.n - m;
         slice_pos_kernel<<<grid_of(big), 256, 0, st>>>(g.n, g.row_lo, g.row_hi, m_pad, m,
                                                        sorted_rows, g.pos);

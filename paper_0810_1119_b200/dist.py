@@ -151,7 +151,8 @@ def _report(parts, outs, rep, ch, rh, ms):
                        max_change_history=ch[:k].tolist(), residual_history=rh[:k].tolist(),
                        messages_sent=int(rep.messages_sent), device_ms=float(ms),
                        sweeps_launched=int(rep.sweeps_launched),
-                       final_rel_residual=float(rep.final_rel_residual))
+                       final_rel_residual=float(rep.final_rel_residual),
+                       split_sweeps=int(rep.split_sweeps))
 
 
 def solve_partitioned_local(system: SymSystem, nparts: int, options=None, device: int = 0):

@@ -23,6 +23,8 @@ host one sweep at a time (solver.py:307-346), the other schedules solve on the d
 from __future__ import annotations
 
 import ctypes
+import dataclasses
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -119,9 +121,29 @@ class MessageState:
     def prec(self) -> np.ndarray:
         return self._read()[0]
 
+    @prec.setter
+    def prec(self, value) -> None:
+        # the reference assigns the buffers directly (acceleration.py:123-126); here the
+        # assignment writes through to the device state
+        self.set_messages(value, self._read()[1])
+
     @property
     def mean(self) -> np.ndarray:
         return self._read()[1]
+
+    @mean.setter
+    def mean(self, value) -> None:
+        self.set_messages(self._read()[0], value)
+
+    def gather(self, edges) -> tuple[np.ndarray, np.ndarray]:
+        """(prec, mean) of the given edge ids, read from the device (point reads of
+        the buffers, as compute_message indexes them)."""
+        idx = np.ascontiguousarray(np.asarray(edges, dtype=np.int64).reshape(-1))
+        p = np.empty(idx.size)
+        m = np.empty(idx.size)
+        _lib.check(_lib.load().gabp_state_gather(self._h, _lib.ptr(idx), idx.size,
+                                                  _lib.ptr(p), _lib.ptr(m)))
+        return p, m
 
     def set_messages(self, prec, mean) -> None:
         prec = np.ascontiguousarray(prec, dtype=np.float64)
@@ -165,11 +187,65 @@ class SolveReport:
     final_rel_residual: float = float("nan")
     residual_probes: int = 0
     kernel_launches: int = 0
+    split_sweeps: int = 0   # multi-rank: sweeps run as boundary part + interior part
 
 
 def initial_state(graph: GaussianGraph, schedule: str = "parallel") -> MessageState:
     """solver.py:92-97: all messages exactly zero."""
     return MessageState(graph, schedule)
+
+
+def _exclusion(graph: GaussianGraph, state: MessageState, i: int, j: int):
+    """P_{i\\j} and the matching precision-weighted mean numerator (solver.py:100-111):
+    the prior plus every incoming message but j's, in ascending neighbour order."""
+    rp = graph.row_ptr
+    lo, hi = int(rp[i]), int(rp[i + 1])
+    nbr = graph.dst[lo:hi]
+    prec, mean = state.gather(graph.rev[lo:hi])  # incoming m_ki, k ascending
+    acc_p = float(graph.prior_prec[i])
+    acc_num = float(graph.prior_prec[i]) * float(graph.prior_mean[i])
+    for pos in range(nbr.size):
+        if int(nbr[pos]) == j:
+            continue
+        acc_p += float(prec[pos])
+        acc_num += float(prec[pos]) * float(mean[pos])
+    return acc_p, acc_num
+
+
+def _edge_coeff(graph: GaussianGraph, i: int, j: int) -> float:
+    rp = graph.row_ptr
+    lo, hi = int(rp[i]), int(rp[i + 1])
+    pos = int(np.searchsorted(graph.dst[lo:hi], j))
+    if not (0 <= i < graph.n) or pos >= hi - lo or int(graph.dst[lo + pos]) != j:
+        raise KeyError(f"({i}, {j}) is not an edge")
+    return float(graph.coeff[lo + pos])
+
+
+def compute_message(graph: GaussianGraph, state: MessageState, i: int, j: int):
+    """Sum-product message (P_ij, mu_ij) from the current buffers (solver.py:114-122)."""
+    i, j = int(i), int(j)
+    if not (0 <= i < graph.n):
+        raise KeyError(f"({i}, {j}) is not an edge")
+    a = _edge_coeff(graph, i, j)
+    p_excl, num = _exclusion(graph, state, i, j)
+    if p_excl == 0.0:
+        raise SingularSubgraphError(f"P_excl({i} -> {j}) = 0")
+    return -a * a / p_excl, num / a
+
+
+def compute_message_max_product(graph: GaussianGraph, state: MessageState, i: int, j: int):
+    """Max-product message via the closed-form argmax of the integrand (solver.py:125-143):
+    equal to the sum-product message in exact arithmetic, rounded differently."""
+    i, j = int(i), int(j)
+    if not (0 <= i < graph.n):
+        raise KeyError(f"({i}, {j}) is not an edge")
+    a = _edge_coeff(graph, i, j)
+    p_excl, num = _exclusion(graph, state, i, j)
+    if p_excl == 0.0:
+        raise SingularSubgraphError(f"P_excl({i} -> {j}) = 0")
+    mu_excl = num / p_excl
+    prec = -a * a / p_excl
+    return prec, -a * mu_excl / prec
 
 
 def _sweep(graph: GaussianGraph, state: MessageState, schedule: str):
@@ -271,6 +347,48 @@ def _want_means_history(options: SolveOptions, n: int) -> bool:
     return bool(options.record_means_history)
 
 
+class MeansHistory(Sequence):
+    """SolveReport.means_history (solver.py:319, 332: the tentative means of every sweep),
+    materialised on first access.
+
+    A solve whose n x max_iter would not fit the eager host buffer (record_means_history
+    left at None) records none on the device; the first read of this sequence replays the
+    solve -- bitwise deterministic, so the same messages and means sweep for sweep -- with
+    max_iter = the number of sweeps the solve ran, recording every row."""
+
+    def __init__(self, count: int, replay):
+        self._count = int(count)
+        self._replay = replay
+        self._rows = None
+
+    def _load(self):
+        if self._rows is None:
+            rows = self._replay()
+            if len(rows) != self._count:
+                raise RuntimeError(f"means-history replay ran {len(rows)} sweeps, "
+                                   f"the solve ran {self._count}")
+            self._rows = rows
+            self._replay = None
+        return self._rows
+
+    def __len__(self) -> int:
+        return self._count
+
+    def __getitem__(self, t):
+        return self._load()[t]
+
+    def __eq__(self, other):
+        return list(self) == list(other) if isinstance(other, (list, Sequence)) else NotImplemented
+
+    def __repr__(self) -> str:
+        state = "loaded" if self._rows is not None else "not loaded"
+        return f"MeansHistory({self._count} sweeps, {state})"
+
+
+def _replay_options(options: SolveOptions, k: int) -> SolveOptions:
+    return dataclasses.replace(options, max_iter=max(int(k), 1), record_means_history=True)
+
+
 def _solve_serial(graph: GaussianGraph, options: SolveOptions) -> SolveReport:
     """solver.py:307-346 with the serial schedule: one device sweep (dependency levels)
     per iteration, then the reference's tests on the tentative means (device marginals and
@@ -324,6 +442,10 @@ def _solve_serial(graph: GaussianGraph, options: SolveOptions) -> SolveReport:
         if not converged and not diverged:
             diverged = True  # cap exhausted
         means, precs = infer_marginals(graph, state)
+        if not want_hist and options.record_means_history is None:
+            k = len(max_hist)
+            means_hist = MeansHistory(k, lambda: list(
+                _solve_serial(graph, _replay_options(options, k)).means_history)[:k])
         return SolveReport(
             converged=converged, diverged=diverged, iterations=state.iteration,
             means=means, precisions=precs, max_change_history=max_hist,
@@ -353,6 +475,13 @@ def solve_graph(graph: GaussianGraph, options: SolveOptions | None = None) -> So
                                       _lib.ptr(precs), _lib.ptr(ch), _lib.ptr(rh),
                                       ctypes.byref(rep)))
     k = int(rep.n_hist)
+    if hist is not None:
+        means_hist = [hist[t].copy() for t in range(k)]
+    elif options.record_means_history is None:
+        means_hist = MeansHistory(k, lambda: list(
+            solve_graph(graph, _replay_options(options, k)).means_history)[:k])
+    else:
+        means_hist = []
     return SolveReport(
         converged=bool(rep.converged),
         diverged=bool(rep.diverged),
@@ -361,7 +490,7 @@ def solve_graph(graph: GaussianGraph, options: SolveOptions | None = None) -> So
         precisions=precs,
         max_change_history=ch[:k].tolist(),
         residual_history=rh[:k].tolist(),
-        means_history=[hist[t].copy() for t in range(k)] if hist is not None else [],
+        means_history=means_hist,
         messages_sent=int(rep.messages_sent),
         precisions_exact=graph.is_tree(),
         device_ms=float(rep.device_ms),
@@ -384,6 +513,18 @@ def solve(system: SymSystem, options: SolveOptions | None = None) -> SolveReport
         _gpu_schedule(options.schedule)
     graph = build_graph(system, options.device)
     try:
-        return solve_graph(graph, options)
+        rep = solve_graph(graph, options)
     finally:
         graph.close()
+    if isinstance(rep.means_history, MeansHistory):
+        k = len(rep.means_history)
+
+        def replay():
+            g = build_graph(system, options.device)
+            try:
+                return list(solve_graph(g, _replay_options(options, k)).means_history)[:k]
+            finally:
+                g.close()
+
+        rep.means_history = MeansHistory(k, replay)
+    return rep

@@ -1,11 +1,11 @@
-"""Generate the fixtures of the rows beside the sweep (acceleration, augmented least
-squares, Matrix Market I/O) by running the REFERENCE package itself.
+"""Generate the fixtures of the Matrix Market / vector I/O row by running the REFERENCE
+package itself.
 
 Run in the build container (the reference is importable only there):
 
     python tests/golden/make_golden_next.py
 
-Outputs tests/golden/next/accel_*.npz, lsq_*.npz and mm_cases.json.  The GPU box never
+Outputs tests/golden/next/mm_cases.json.  The GPU box never
 reads /root/reference; tests/test_next_rows.py reads only these files.
 """
 
@@ -22,67 +22,6 @@ OUT = os.path.join(HERE, "next")
 sys.path.insert(0, "/root/reference/pkg/src")
 
 import gabp  # noqa: E402  (the reference)
-
-
-def sys_arrays(s):
-    items = list(s.offdiag.items())
-    pi = np.array([k[0] for k, _ in items], dtype=np.int64)
-    pj = np.array([k[1] for k, _ in items], dtype=np.int64)
-    pv = np.array([v for _, v in items], dtype=np.float64)
-    return dict(diag=np.asarray(s.diag), rhs=np.asarray(s.rhs), pair_i=pi, pair_j=pj, pair_v=pv)
-
-
-def report_arrays(r, prefix):
-    out = {f"{prefix}_converged": np.int64(r.converged), f"{prefix}_diverged": np.int64(r.diverged),
-           f"{prefix}_iterations": np.int64(r.iterations), f"{prefix}_means": np.asarray(r.means),
-           f"{prefix}_change": np.asarray(r.max_change_history, dtype=float),
-           f"{prefix}_residual": np.asarray(r.residual_history, dtype=float)}
-    if r.precisions is not None:
-        out[f"{prefix}_precisions"] = np.asarray(r.precisions)
-    mh = [np.asarray(m) for m in r.means_history]
-    out[f"{prefix}_means_history"] = np.stack(mh) if mh else np.zeros((0, len(r.means)))
-    return out
-
-
-def accel_fixtures():
-    systems = {name.replace(":", ""): gabp.load_instance(name).system
-               for name in ("toy3", "cdma3", "cdma4", "nonpsd3", "poisson:3", "poisson:10")}
-    systems["identity3"] = gabp.SymSystem(diag=np.ones(3), offdiag={},
-                                          rhs=np.array([1.0, 2.0, 3.0]))
-    systems["strict20"] = gabp.gen_random("strict_dominant", 20, 7001).system
-    for name, s in systems.items():
-        rec = sys_arrays(s)
-        for sched in ("parallel", "broadcast"):
-            opts = gabp.SolveOptions(schedule=sched)
-            rec.update(report_arrays(gabp.steffensen_solve("gabp", s, opts), f"{sched}_steff"))
-            rec.update(report_arrays(gabp.aitken_solve("gabp", s, opts), f"{sched}_aitken"))
-            ungated = gabp.AccelConfig(mode="steffensen", stability=0.0)
-            rec.update(report_arrays(gabp.steffensen_solve("gabp", s, opts, ungated),
-                                     f"{sched}_steff_s0"))
-        np.savez_compressed(os.path.join(OUT, f"accel_{name}.npz"), **rec)
-
-
-def random_rect(seed, m=5, n=3):
-    rng = np.random.default_rng(seed)
-    return gabp.RectMatrix.from_dense(rng.standard_normal((m, n))), rng.standard_normal(m)
-
-
-def lsq_fixtures():
-    for seed, m, n, psi in ((0, 5, 3, 1e-6), (0, 5, 3, 1e-4), (0, 5, 3, 1e-2), (1, 5, 3, 1e-3),
-                            (2, 5, 3, 1e-6), (3, 8, 4, 1e-3), (4, 6, 6, 1e-2)):
-        s, y = random_rect(seed, m, n)
-        aug = gabp.build_augmented(s, y, psi)
-        rec = {"m": np.int64(m), "n": np.int64(n), "psi": np.float64(psi), "y": y,
-               "dense": s.to_dense(), **{f"aug_{k}": v for k, v in sys_arrays(aug.assembled).items()}}
-        opts = gabp.SolveOptions(schedule="parallel", epsilon=1e-10, max_iter=6000)
-        try:
-            rec["x"] = gabp.solve_least_squares(s, y, psi, opts)
-            rec["diverged"] = np.int64(0)
-        except gabp.pseudoinverse.LeastSquaresDivergence as exc:
-            rec["diverged"] = np.int64(1)
-            rec["rho"] = np.float64(exc.rho)
-        rec["oracle"] = gabp.normal_equations_oracle(s, y, psi)
-        np.savez_compressed(os.path.join(OUT, f"lsq_{seed}_{m}x{n}_{psi:g}.npz"), **rec)
 
 
 def mm_fixtures():
@@ -171,7 +110,5 @@ def mm_fixtures():
 
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    accel_fixtures()
-    lsq_fixtures()
     mm_fixtures()
     print("wrote", sorted(os.listdir(OUT)))

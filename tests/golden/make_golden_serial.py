@@ -56,44 +56,8 @@ def trace(g, order):
             np.array(changes), sing_at)
 
 
-def lsq_default_fixtures():
-    """solve_least_squares with the reference's DEFAULT options (pseudoinverse.py:79:
-    serial schedule, epsilon 1e-10) on the seeds of make_golden_next.py."""
-    import make_golden_next as N
-    for seed, m, n, psi in ((0, 5, 3, 1e-6), (0, 5, 3, 1e-4), (0, 5, 3, 1e-2), (1, 5, 3, 1e-3),
-                            (2, 5, 3, 1e-6), (3, 8, 4, 1e-3), (4, 6, 6, 1e-2)):
-        s, y = N.random_rect(seed, m, n)
-        rec = {"psi": np.float64(psi), "y": y, "dense": s.to_dense()}
-        try:
-            rec["x"] = gabp.solve_least_squares(s, y, psi)
-            rec["diverged"] = np.int64(0)
-        except gabp.pseudoinverse.LeastSquaresDivergence as exc:
-            rec["diverged"] = np.int64(1)
-            rec["rho"] = np.float64(exc.rho)
-        print(f"lsq default {seed} {m}x{n} psi={psi:g} diverged={int(rec['diverged'])}")
-        np.savez_compressed(os.path.join(OUT, f"lsq_{seed}_{m}x{n}_{psi:g}.npz"), **rec)
-
-
-def accel_serial_fixtures():
-    """Steffensen / Aitken around the serial schedule (the reference's "serial-gabp+
-    steffensen" rows) on the systems of make_golden_next.accel_fixtures."""
-    import make_golden_next as N
-    systems = {name.replace(":", ""): gabp.load_instance(name).system
-               for name in ("toy3", "cdma3", "cdma4", "nonpsd3", "poisson:3", "poisson:10")}
-    systems["strict20"] = gabp.gen_random("strict_dominant", 20, 7001).system
-    for name, s in systems.items():
-        rec = N.sys_arrays(s)
-        opts = gabp.SolveOptions(schedule="serial")
-        rec.update(N.report_arrays(gabp.steffensen_solve("gabp", s, opts), "serial_steff"))
-        rec.update(N.report_arrays(gabp.aitken_solve("gabp", s, opts), "serial_aitken"))
-        print(f"accel serial {name}")
-        np.savez_compressed(os.path.join(OUT, f"accel_{name}.npz"), **rec)
-
-
 def main():
     os.makedirs(OUT, exist_ok=True)
-    accel_serial_fixtures()
-    lsq_default_fixtures()
     for case, (s, extra) in M.cases().items():
         system = M.ref_system(s.pair_i, s.pair_j, s.pair_v, s.diag, s.rhs)
         g = gabp.build_graph(system)
