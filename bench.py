@@ -64,7 +64,43 @@ def parse():
     ap.add_argument("--cpu-sample-sweeps", type=int, default=0,
                     help="0 = one full solve as the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config blocks (configs 0, 2, 3 on one GPU)")
+    ap.add_argument("--no-scaling", action="store_true",
+                    help="skip the scaling block (Poisson 3-D slabs, fixed sweeps per step)")
+    ap.add_argument("--scaling-p", type=int, default=512,
+                    help="points per side of the scaling block's 3-D grid (BASELINE config 4)")
+    ap.add_argument("--scaling-sweeps", type=int, default=50)
+    ap.add_argument("--scaling-steps", type=int, default=3)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch plumbing only: reach the arm's entry on every rank (gloo, "
+                         "no GPU), print one line from rank 0, exit")
     return ap.parse_args()
+
+
+def config_of(name: str, schedule: str, n: int, directed_edges: int) -> dict:
+    """The workload of the line -- identical in both arms (the measured solve figures go
+    in the "solve" block, not here)."""
+    return {"workload": name, "schedule": schedule, "n": int(n),
+            "directed_edges": int(directed_edges),
+            "stop": "||Ax-b||/||b|| < 1e-8 (epsilon disabled)",
+            "inputs": "synthetic, seeded (paper_0810_1119_b200/problems.py); > L2"}
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def peak_hbm():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+        return float(peaks["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def dist_env():
@@ -189,15 +225,175 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT,
         "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
         "ms_per_step": res["seconds_per_run"] * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": name, "schedule": args.schedule, "n": system.n,
-                   "offdiag_pairs": int(system.pair_v.size), "stop": "||Ax-b||/||b|| < 1e-8"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, BASELINE config %d)" % args.config,
+        "config": config_of(name, args.schedule, system.n, 2 * int(system.pair_v.size)),
         "cpu_baseline": res,
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
     return 0
+
+
+
+# ---------------------------------------------------------------------------------------
+# secondary blocks: the other BASELINE configs on one GPU, and the scaling workload
+# ---------------------------------------------------------------------------------------
+
+def _algo_bytes(E: int, n: int) -> int:
+    return BYTES_PER_EDGE * E + BYTES_PER_NODE * n
+
+
+def _traffic(key: str):
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh)
+    except OSError:
+        return None, None
+    if key not in tr:
+        return None, None
+    return tr[key]["dram_bytes_per_launch"], tr[key].get("source")
+
+
+def _sweep_ms(lib, handle, sched_id: int, sweeps: int) -> float:
+    from paper_0810_1119_b200 import _lib
+    ms = ctypes.c_double()
+    _lib.check(lib.gabp_bench_sweeps(handle, sched_id, 0, 5, ctypes.byref(ms)))
+    _lib.check(lib.gabp_bench_sweeps(handle, sched_id, 0, sweeps, ctypes.byref(ms)))
+    return float(ms.value)
+
+
+def _block(name, n, E, ms_sweep, peak, extra=None, traffic_key=None):
+    algo = _algo_bytes(E, n)
+    ach = algo / (ms_sweep / 1e3) / 1e9
+    tr, src = _traffic(traffic_key) if traffic_key else (None, None)
+    b = {"workload": name, "n": int(n), "directed_edges": int(E),
+         "ms_per_sweep": ms_sweep, "edge_updates_per_s": E / (ms_sweep / 1e3),
+         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                      "frac": ach / peak, "algorithmic_bytes_per_launch": algo,
+                      "traffic": tr, "traffic_source": src}}
+    if extra:
+        b.update(extra)
+    return b
+
+
+def configs_block(dev: int, peak: float) -> dict:
+    """Configs 0 (Poisson 32^2, the reference's own case: time to 1e-8), 2 (Poisson 4096^2)
+    and 3 (dense CDMA K = 4096) on one GPU, steady-state sweeps timed with CUDA events."""
+    import paper_0810_1119_b200 as G
+    from paper_0810_1119_b200 import _lib, grid as GR, problems as P
+    lib = _lib.load()
+    out = {}
+    # config 0: the whole solve is the unit (1731 sweeps of a 1024-node graph)
+    s0 = P.CONFIGS[0][1](0).system
+    g0 = G.build_graph(s0, dev)
+    o0 = G.SolveOptions(schedule="broadcast", epsilon=1e-300, rel_residual_tol=REL_TOL,
+                        device=dev, record_means_history=False)
+    G.solve_graph(g0, o0)
+    runs = [G.solve_graph(g0, o0) for _ in range(3)]
+    best = min(r.device_ms for r in runs)
+    it = runs[0].iterations
+    out["poisson2d-32"] = {
+        "workload": "poisson2d-32", "n": g0.n, "directed_edges": g0.num_edges,
+        "sweeps_to_1e-8": it, "time_to_1e-8_ms": best, "us_per_sweep": 1e3 * best / it,
+        "edge_updates_per_s": it * g0.num_edges / (best / 1e3),
+        "bound": "latency (4 k edges: the graph lives in L2)"}
+    g0.close()
+    # config 2: 4096^2 grid, generated on the device
+    g2 = GR.GridGraph(GR.GridSpec(2, 4096, 0), dev)
+    ms2 = _sweep_ms(lib, g2.handle, 2, 20)
+    out["poisson2d-4096"] = _block("poisson2d-4096", g2.n, g2.num_edges, ms2, peak,
+                                   traffic_key="config2_broadcast")
+    g2.close()
+    # config 3: dense CDMA, dense kernels (time a capped solve: they run in the loop only)
+    s3 = P.CONFIGS[3][1](0).system
+    g3 = G.build_graph(s3, dev)
+    o3 = G.SolveOptions(schedule="broadcast", epsilon=1e-300, max_iter=20, device=dev,
+                        record_means_history=False)
+    G.solve_graph(g3, o3)
+    r3 = min((G.solve_graph(g3, o3) for _ in range(3)), key=lambda r: r.device_ms)
+    ms3 = r3.device_ms / max(r3.sweeps_launched, 1)
+    out["cdma-8192x4096"] = _block("cdma-8192x4096", g3.n, g3.num_edges, ms3, peak,
+                                   {"timing": "capped 20-sweep solves, device time / launches"},
+                                   traffic_key="config3_broadcast")
+    g3.close()
+    return out
+
+
+def scaling_block(args, rank: int, world: int, local: int, peak: float):
+    """BASELINE config 4 (Poisson 512^3, 804 M directed edges) at every N: the same grid in
+    N slabs (N = 1: whole), a fixed number of sweeps per step, strong scaling.  Each rank
+    generates only its slab on its GPU (grid.py)."""
+    import torch
+    import paper_0810_1119_b200 as G
+    from paper_0810_1119_b200 import _lib, dist as D, grid as GR
+    spec = GR.GridSpec(3, args.scaling_p, 0)
+    S = args.scaling_sweeps
+    opts = G.SolveOptions(schedule="broadcast", epsilon=1e-300, max_iter=S, device=local,
+                          record_means_history=False)
+    E = 2 * spec.npairs
+    halo = 0
+    split = 0
+    if world == 1:
+        g = GR.GridGraph(spec, local)
+        lib = _lib.load()
+        o = G.solver._options_struct(opts, spec.n, None)
+        rep = _lib.Report()
+
+        def step():
+            _lib.check(lib.gabp_solve_device(g.handle, ctypes.byref(o), None, None,
+                                             ctypes.byref(rep)))
+            return rep.device_ms, rep.sweeps_launched
+        close = g.close
+    else:
+        import torch.distributed as dist
+        dg = D.DistributedGraph.from_grid(spec, device=local)
+        halo = dg.halo_bytes_per_sweep()
+
+        def step():
+            _, _, rep, _, _ = dg.solve_local_report(opts)
+            nonlocal split
+            split = int(rep.split_sweeps)
+            return rep.device_ms, rep.sweeps_launched
+        close = dg.close
+    step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(local)
+    ms = 0.0
+    sweeps = 0
+    for _ in range(args.scaling_steps):
+        m, launched = step()
+        ms += m
+        sweeps += S
+    close()
+    if world > 1:
+        t = torch.tensor([ms, float(halo)], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+        halo = int(t[1])
+        tt = torch.tensor([float(halo)], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        halo_total = float(tt[0])
+    else:
+        halo_total = 0.0
+    ms_sweep = ms / sweeps
+    algo = _algo_bytes(E, spec.n)
+    ach = algo / (ms_sweep / 1e3) / 1e9
+    return {
+        "workload": spec.name, "n": spec.n, "directed_edges": E, "n_gpus": world,
+        "partition": f"{world} slabs of whole planes (row blocks), NCCL node-level halo"
+                     if world > 1 else "whole grid, one GPU",
+        "sweeps_per_step": S, "steps": args.scaling_steps, "scaling": "strong",
+        "value": sweeps * E / (ms / 1e3), "unit": UNIT, "ms_per_sweep": ms_sweep,
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak * world, "unit": "GB/s",
+                     "frac": ach / (peak * world),
+                     "note": "algorithmic bytes of the global sweep / solve-loop time per "
+                             "sweep (halo exchange and decision included) / (N x peak)"},
+        "halo_bytes_per_sweep": {"max_rank": halo, "total": halo_total},
+        "split_sweeps_rank0": split,
+    }
 
 
 # ---------------------------------------------------------------------------------------
@@ -212,9 +408,9 @@ def pinned_copy(a: np.ndarray):
 
 
 def run_ours_dist(args):
-    """N > 1: the same workload solved by N ranks (row blocks, NCCL halo exchange inside
+    """N > 1: the headline workload solved by N ranks (row blocks, NCCL halo exchange inside
     the library) -- strong scaling; value = reference-counted sweeps x global directed
-    edges / max over ranks of the device time."""
+    edges / max over ranks of the device time.  Then the scaling block (Poisson 3-D slabs)."""
     import torch
     import torch.distributed as dist
 
@@ -222,10 +418,21 @@ def run_ours_dist(args):
     from paper_0810_1119_b200 import dist as D
 
     rank, world, local = dist_env()
+    if args.dry_run:  # the launch path without GPUs (tests/test_bench_launch.py)
+        dist.init_process_group("gloo")
+        t = torch.tensor([float(rank)])
+        dist.all_reduce(t)
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "entry": "run_ours_dist", "n_gpus": world,
+                              "rank_sum": float(t[0])}))
+        dist.destroy_process_group()
+        return 0
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peak, peak_src = peak_hbm()
     name, system, _ = workload(args.config)
     E = 2 * int(system.pair_v.size)
+    n = system.n
     dg = D.DistributedGraph(system, device=local)
     dg_slice = dg.slice_path
     opts = G.SolveOptions(schedule="broadcast", epsilon=1e-300, rel_residual_tol=REL_TOL,
@@ -234,12 +441,13 @@ def run_ours_dist(args):
         dg.solve_local_report(opts)
     dist.barrier()
     torch.cuda.synchronize(local)
-    ms_tot, its, launched = 0.0, [], 0
+    ms_tot, its, launched, swl = 0.0, [], 0, 0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             _, _, rep, _, _ = dg.solve_local_report(opts)
             ms_tot += rep.device_ms
             its.append(int(rep.iterations))
+            swl += int(rep.sweeps_launched)
             # sweep (+ exact twin on the slice path), finish, pack/unpack per launch
             launched += int(rep.sweeps_launched) * (7 if dg_slice else 6)
     dist.barrier()
@@ -248,7 +456,7 @@ def run_ours_dist(args):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t[0])
     value = float(sum(its)) * E / (ms_max / 1e3)
-    halo = D.halo_bytes_per_sweep(dg.part)
+    halo = dg.halo_bytes_per_sweep()
     dg.close()
     # e2e: the public distributed call from host arrays (partition, build, solve, gather)
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(2, min(args.steps, 5))
@@ -264,25 +472,32 @@ def run_ours_dist(args):
     tt = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e_s = float(tt[0])
+    scaling = None if args.no_scaling else scaling_block(args, rank, world, local, peak)
     if rank == 0:
+        ms_sweep = ms_max / max(swl, 1)  # solve-loop time per launch (halo + decision in)
+        algo = _algo_bytes(E, n)
+        ach = algo / (ms_sweep / 1e3) / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup),
             "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, BASELINE config %d)" % args.config,
-            "config": {"workload": name, "schedule": "broadcast", "n": system.n,
-                       "directed_edges": E, "stop": "||Ax-b||/||b|| < 1e-8 (epsilon disabled)",
-                       "sweeps_to_1e-8": its[-1], "time_to_1e-8_ms": ms_max / args.steps,
-                       "parallelism": f"row blocks x{world}, NCCL node-level halo "
-                                      f"({halo} B/sweep on rank 0) + 2 all-reduces/sweep",
-                       "l2": "inputs > L2"},
-            "roofline": None,
+            "config": config_of(name, "broadcast", n, E),
+            "parallelism": f"row blocks x{world}, NCCL node-level halo ({halo} B/sweep on "
+                           f"rank 0) + statistics all-reduce per sweep",
+            "solve": {"sweeps_to_1e-8": its[-1], "time_to_1e-8_ms": ms_max / args.steps},
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak * world,
+                         "unit": "GB/s", "frac": ach / (peak * world), "traffic": None,
+                         "peak_source": peak_src,
+                         "note": "algorithmic bytes of the global sweep / solve-loop time "
+                                 "per launch (exchange, decision included) / (N x peak)"},
             "e2e": {"value": float(e2e_its) * E / e2e_s, "unit": UNIT,
-                    "h2d_bytes_per_step": 8 * 2 * system.n // world + 24 * int(system.pair_v.size) // world,
-                    "d2h_bytes_per_step": 16 * system.n // world, "steps": e2e_steps,
+                    "h2d_bytes_per_step": 8 * 2 * n // world + 24 * int(system.pair_v.size) // world,
+                    "d2h_bytes_per_step": 16 * n // world, "steps": e2e_steps,
                     "ms_per_step": e2e_s / e2e_steps * 1e3},
             "gpu_launches": int(launched), "clocks": clk.summary(), "cpu_baseline": None,
+            "scaling_config": scaling,
         }
         print(json.dumps(line))
     dist.destroy_process_group()
@@ -299,6 +514,9 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world > 1:
         return run_ours_dist(args)
+    if args.dry_run:
+        print(json.dumps({"dry_run": True, "entry": "run_ours", "n_gpus": 1}))
+        return 0
     dev = local
     name, system, gen_s = workload(args.config)
     lib = _lib.load()
@@ -364,25 +582,8 @@ def run_ours(args):
     algo_bytes = BYTES_PER_EDGE * E + BYTES_PER_NODE * n
     achieved = algo_bytes / (ms_sweep.value / 1e3) / 1e9
     achieved_after = algo_bytes / (ms_sweep_after.value / 1e3) / 1e9
-    peaks = {}
-    try:
-        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
-            peaks = json.load(fh)
-    except OSError:
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    traffic = None
-    traffic_src = None
-    try:
-        with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
-            tr = json.load(fh)
-        key = f"config{args.config}_{sched}"
-        if key in tr:
-            traffic = tr[key]["dram_bytes_per_launch"]
-            traffic_src = tr[key].get("source")
-    except OSError:
-        pass
+    peak, peak_src = peak_hbm()
+    traffic, traffic_src = _traffic(f"config{args.config}_{sched}")
     g_close = g.close
     g_info_span = float(g.info.twin_span)
     slice_path = sched == "broadcast" and int(g.info.num_slices) > 0
@@ -429,6 +630,8 @@ def run_ours(args):
     h2d = 8 * 2 * n + 24 * int(system.pair_v.size)
     d2h = 8 * n + 2 * 8 * int(np.mean(its))
 
+    blocks = None if args.no_configs else configs_block(dev, peak)
+    scaling = None if args.no_scaling else scaling_block(args, rank, world, dev, peak)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_run(system, 1, 1, args.cpu_sample_sweeps, sched)
@@ -442,13 +645,12 @@ def run_ours(args):
             # the same graph at every N (N > 1: row blocks of it, run_ours_dist)
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, BASELINE config %d)" % args.config,
-            "config": {"workload": name, "schedule": sched, "n": n, "directed_edges": E,
-                       "stop": "||Ax-b||/||b|| < 1e-8 (epsilon disabled)",
-                       "sweeps_to_1e-8": int(its[-1]),
-                       "time_to_1e-8_ms": total_ms_max / args.steps,
-                       "l2": "inputs > L2: messages 2 x %.2f GB, graph %.2f GB" %
-                             (16 * E / 1e9, 16 * E / 1e9),
-                       "parallelism": "replicas" if world > 1 else "single GPU"},
+            "config": config_of(name, sched, n, E),
+            "parallelism": "single GPU",
+            "solve": {"sweeps_to_1e-8": int(its[-1]),
+                      "time_to_1e-8_ms": total_ms_max / args.steps,
+                      "l2": "inputs > L2: messages 3 x %.2f GB, graph %.2f GB" %
+                            (16 * E / 1e9, 12 * E / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": traffic_src,
@@ -467,6 +669,8 @@ def run_ours(args):
             "gpu_launches": int(launched),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "configs": blocks,
+            "scaling_config": scaling,
         }
         print(json.dumps(line))
     if world > 1:
@@ -478,6 +682,13 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver's own N > 1 form)
+        import subprocess
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     return run_ours(args)
 
 

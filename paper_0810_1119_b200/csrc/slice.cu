@@ -82,6 +82,39 @@ __device__ __forceinline__ void ld_node(const NodeState *g, double &P, double &N
     asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
                  : "=d"(P), "=d"(N), "=d"(x), "=d"(pad) : "l"(g));
 }
+// L2 policies of the node-state traffic (GABP_GATHER_POLICY): the gathered states S_{s-2}
+// are a random-access working set of 32 B x nodes that the message streams (evict-first)
+// must not push out of L2; the written states S_{s-1} are next launch's gather set.
+#ifndef GABP_GATHER_POLICY
+#define GABP_GATHER_POLICY 0
+#endif
+__device__ __forceinline__ uint64_t pol_evict_last_node() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_first_node() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void ld_node_pol(const NodeState *g, double &P, double &N, double &x,
+                                            uint64_t pol) {
+    double pad;
+    asm volatile("ld.global.cg.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=d"(P), "=d"(N), "=d"(x), "=d"(pad) : "l"(g), "l"(pol));
+}
+__device__ __forceinline__ void st_node_pol(NodeState *g, double P, double N, double x,
+                                            uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(g),
+                 "d"(P), "d"(N), "d"(x), "d"(0.0), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double2 ld_f64x2_pol(const double2 *p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
 __device__ __forceinline__ void st_node(NodeState *g, double P, double N, double x) {
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(g), "d"(P), "d"(N), "d"(x),
                  "d"(0.0) : "memory");
@@ -110,7 +143,11 @@ __device__ __forceinline__ double node_done(Stats &st, const SweepArgs &a, NodeS
     if (xh) xh[__ldg(a.srow + p)] = xi;
     if (EXACT && sp == 0.0)  // (fast launch: N / 0 fails the deferred range test)
         st.agg_sing = min(st.agg_sing, __ldg(a.srow + p));
+#if GABP_GATHER_POLICY >= 1
+    st_node_pol(rec1 + p, sp, sp * xi, xi, pol_evict_last_node());  // (sum_p * mu_tilde)
+#else
     st_node(rec1 + p, sp, sp * xi, xi);  // (sum_p * mu_tilde)
+#endif
     if (PH == 3) {
         const double r = y - rhs_i;
         if (ACC) st.rsq += r * r;
@@ -756,7 +793,12 @@ __device__ __forceinline__ void t_header(const SweepArgs &a, const Ring<R> &r, i
     h.nd = __ldg(a.snd + p);
     h.d = __ldg(a.sdeg + p);
     if (PH == 3 || PH == 4) {
+#if GABP_GATHER_POLICY >= 1
+        // S_{s-3}: last use of the state (demoted); S_{s-2}: still gathered this launch
+        h.a3 = ld_f64x2_pol(reinterpret_cast<const double2 *>(r.g3 + p), pol_evict_first_node());
+#else
         h.a3 = __ldcg(reinterpret_cast<const double2 *>(r.g3 + p));
+#endif
         h.xo = __ldcg(&r.g2[p].x);
         h.rhs = __ldg(a.srhs + p);
     }
@@ -770,7 +812,11 @@ __device__ __forceinline__ void t_gather(const GStage &S, const GMeta &m, const 
 #pragma unroll
     for (int u = 0; u < CW; ++u) {
         if (m.b * CW + u < m.w) {
+#if GABP_GATHER_POLICY >= 1
+            ld_node_pol(g2 + st_col<PH>(S, u)[t], gP[u], gN[u], gx[u], pol_evict_last_node());
+#else
             ld_node(g2 + st_col<PH>(S, u)[t], gP[u], gN[u], gx[u]);
+#endif
         } else {
             gP[u] = 1.0;
             gN[u] = 1.0;

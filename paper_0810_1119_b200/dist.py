@@ -189,32 +189,102 @@ def solve_partitioned_local(system: SymSystem, nparts: int, options=None, device
             lib.gabp_graph_destroy(h)
 
 
+def solve_grid_partitioned_local(spec, nparts: int, options=None, device: int = 0):
+    """solve_partitioned_local for a Poisson grid generated on the device (grid.py): the
+    nparts slabs are built from device arrays, never from a host system."""
+    from . import grid as GR
+    from .solver import SolveOptions, _options_struct
+    options = options or SolveOptions(schedule="broadcast")
+    rhs = GR.rhs_device(spec, device)
+    bnorm = float(rhs.norm())
+    parts, handles = [], []
+    lib = _lib.load()
+    try:
+        for r in range(nparts):
+            part = GR.grid_part(spec, nparts, r, device, rhs)
+            handles.append(GR.part_graph(part, device))
+            part.diag = part.rhs = part.pair_i = part.pair_j = part.pair_v = None
+            parts.append(part)
+        del rhs
+        for h, p in zip(handles, parts):
+            _attach(h, p, None, bnorm)
+        o = _options_struct(options, spec.n, None)
+        arr = (ctypes.c_void_p * nparts)(*[h.value for h in handles])
+        ms = ctypes.c_double()
+        _lib.check(lib.gabp_dist_solve_local(nparts, arr, ctypes.byref(o), ctypes.byref(ms)))
+        outs = []
+        ch = np.empty(options.max_iter)
+        rh = np.empty(options.max_iter)
+        rep = _lib.Report()
+        for h, p in zip(handles, parts):
+            m = np.empty(p.hi - p.lo)
+            pr = np.empty(p.hi - p.lo)
+            _lib.check(lib.gabp_dist_results(h, ctypes.byref(o), _lib.ptr(m), _lib.ptr(pr),
+                                             _lib.ptr(ch), _lib.ptr(rh), ctypes.byref(rep)))
+            outs.append((m, pr))
+        return _report(parts, outs, rep, ch, rh, ms.value)
+    finally:
+        for h in handles:
+            lib.gabp_graph_destroy(h)
+
+
+def _nccl_id(rank: int, world: int, group):
+    import torch.distributed as dist
+    if world <= 1:
+        return None
+    raw = (ctypes.c_char * 128)()
+    if rank == 0:
+        _lib.check(_lib.load().gabp_nccl_unique_id(raw))
+    obj = [bytes(raw) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return (ctypes.c_char * 128).from_buffer_copy(obj[0])
+
+
 class DistributedGraph:
     """One rank's row block of a system, built once on this rank's GPU and attached to the
     multi-rank loop (NCCL halo exchange inside the CUDA library); solve() may be called
-    repeatedly.  Every rank constructs it with the same system."""
+    repeatedly.  Every rank constructs it with the same system (or, from_grid, the same
+    grid spec: then each rank generates only its own slab on its device)."""
 
-    def __init__(self, system: SymSystem, group=None, device: int | None = None):
+    def __init__(self, system: SymSystem | None, group=None, device: int | None = None,
+                 _grid=None):
         import torch.distributed as dist
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = _lib.default_device() if device is None else int(device)
-        self.n = system.n
-        bounds = partition_rows(system.n, self.world)
-        self.part = local_part(system, bounds, self.rank)
-        bnorm = float(np.sqrt(np.sum(system.rhs * system.rhs)))
-        lib = _lib.load()
-        nid = None
-        if self.world > 1:
-            raw = (ctypes.c_char * 128)()
-            if self.rank == 0:
-                _lib.check(lib.gabp_nccl_unique_id(raw))
-            obj = [bytes(raw) if self.rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0, group=group)
-            nid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
-        self._h = _part_graph(self.part, self.device)
+        nid = _nccl_id(self.rank, self.world, group)
+        if _grid is not None:
+            from . import grid as GR
+            self.n = _grid.n
+            rhs = GR.rhs_device(_grid, self.device)
+            bnorm = float(rhs.norm())
+            self.part = GR.grid_part(_grid, self.world, self.rank, self.device, rhs)
+            del rhs
+            self._h = GR.part_graph(self.part, self.device)
+            p = self.part
+            p.diag = p.rhs = p.pair_i = p.pair_j = p.pair_v = None
+        else:
+            self.n = system.n
+            bounds = partition_rows(system.n, self.world)
+            self.part = local_part(system, bounds, self.rank)
+            bnorm = float(np.sqrt(np.sum(system.rhs * system.rhs)))
+            self._h = _part_graph(self.part, self.device)
         _attach(self._h, self.part, nid, bnorm)
+
+    @classmethod
+    def from_grid(cls, spec, group=None, device: int | None = None) -> "DistributedGraph":
+        return cls(None, group, device, _grid=spec)
+
+    def halo_bytes_per_sweep(self) -> int:
+        if hasattr(self.part, "halo_bytes_per_sweep"):
+            return self.part.halo_bytes_per_sweep()
+        return halo_bytes_per_sweep(self.part)
+
+    def graph_info(self):
+        info = _lib.GraphInfo()
+        _lib.check(_lib.load().gabp_graph_info(self._h, ctypes.byref(info)))
+        return info
 
     @property
     def handle(self):
