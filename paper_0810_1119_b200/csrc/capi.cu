@@ -851,6 +851,18 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         }
         return finish_loop(G, device_ms);
     }
+    if (sched == GABP_SCHED_BROADCAST && opt->gather_mode == GABP_GATHER_AUTO &&
+        G->g.row_lo == 0 && G->g.row_hi == G->g.n && gabp::small_fits(G->g.n, G->g.E) &&
+        !getenv("GABP_NO_SMALL")) {
+        // small graph: the whole solve loop in one persistent CTA (small.cu) -- sweeps of a
+        // few thousand edges are bound by launch and decision latency, not by HBM
+        SweepArgs a = make_args(G);
+        G->slice_order = false;
+        G->kernels_launched = 1;
+        CK(cudaEventRecord(G->ev[2], st));
+        CK(gabp::launch_small_solve(a, G->g.E, st));
+        return finish_loop(G, device_ms);
+    }
     rc = check_slice(G, opt);
     if (rc) return rc;
     const int gather = pick_gather(G, opt);

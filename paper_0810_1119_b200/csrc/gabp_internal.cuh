@@ -335,6 +335,11 @@ cudaError_t launch_absmax(int64_t E, const double2 *a, unsigned long long *d_out
 cudaError_t launch_gather(int64_t cnt, const int64_t *idx, const double2 *m, double2 *out,
                           cudaStream_t st);
 
+// the whole broadcast solve of a small graph in one persistent CTA (small.cu): messages
+// and node states in shared memory, 32 B x (n + E)
+bool small_fits(int64_t n, int64_t E);
+cudaError_t launch_small_solve(const SweepArgs &a, int64_t E, cudaStream_t st);
+
 // multi-rank helpers (dist.cu)
 cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st);
 // pre_finish = 1: called between the sweep launch and its finish_kernel (split sweep)

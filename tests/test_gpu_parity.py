@@ -84,14 +84,17 @@ def test_marginals_bitwise_vs_oracle(case, sched):
 
 
 @pytest.mark.parametrize("case", CASES)
-@pytest.mark.parametrize("sched", SCHEDS)
+@pytest.mark.parametrize("sched,mode", [("parallel", "auto"), ("broadcast", "auto"),
+                                        ("broadcast", "slice")])
 @pytest.mark.parametrize("poll", [0, 1, 3])
-def test_solve_matches_reference(case, sched, poll):
+def test_solve_matches_reference(case, sched, mode, poll):
+    """auto: small graphs solve in one persistent CTA (csrc/small.cu); slice: the same
+    fixtures through the sweep-per-launch loop of the slice kernels."""
     rec = gc.load(case)
     tol = float(rec["rel_residual_tol"]) or None
     opts = G.SolveOptions(schedule=sched, epsilon=float(rec["epsilon"]),
                           max_iter=int(rec["max_iter"]), rel_residual_tol=tol,
-                          sweeps_per_poll=poll)
+                          sweeps_per_poll=poll, gather_mode=mode)
     r = G.solve(gc.system(rec), opts)
     assert r.converged == bool(rec[f"{sched}_converged"])
     assert r.diverged == bool(rec[f"{sched}_diverged"])
