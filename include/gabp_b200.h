@@ -67,7 +67,7 @@ typedef struct {
     int64_t num_slices;   /* 32-row slices of the slice layout (0: not built) */
     int64_t num_slots;    /* edge slots of the slice layout, padding included */
     int32_t slice_variant;/* slice kernel: 0 register batches, 1 cp.async ring, 2 TMA ring (default) */
-    int32_t reserved;
+    int32_t dia_diagonals;/* diagonals of the stencil layout (0: not a stencil graph) */
 } gabp_graph_info_t;
 
 /* SolveOptions (solver.py:38-54) + extensions after the first four fields. */

@@ -50,7 +50,7 @@ class GraphInfo(ctypes.Structure):
                 ("rhs_norm", ctypes.c_double), ("build_ms", ctypes.c_double),
                 ("twin_span", ctypes.c_double), ("num_slices", ctypes.c_int64),
                 ("num_slots", ctypes.c_int64), ("slice_variant", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("dia_diagonals", ctypes.c_int32)]
 
 
 class Options(ctypes.Structure):

@@ -205,6 +205,11 @@ void free_graph(DeviceGraph &g, cudaStream_t st) {
     if (g.rhs) cudaFreeAsync(g.rhs, st);
     if (g.slice_info) cudaFreeAsync(g.slice_info, st);
     if (g.gorder) cudaFreeAsync(g.gorder, st);
+    if (g.dia_coef) cudaFreeAsync(g.dia_coef, st);
+    if (g.dia_mask) cudaFreeAsync(g.dia_mask, st);
+    g.dia_coef = nullptr;
+    g.dia_mask = nullptr;
+    g.dia_D = 0;
     if (g.pos) cudaFreeAsync(g.pos, st);
     if (g.srow) cudaFreeAsync(g.srow, st);
     if (g.sdeg) cudaFreeAsync(g.sdeg, st);
@@ -457,6 +462,10 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
         BCHECK(cudaStreamSynchronize(st));
         cudaFreeAsync(d_span, st);
         g.twin_span = h_span / (double)E;
+    }
+    {
+        const int rc = build_dia(g, st, err, errlen);
+        if (rc != GABP_OK) return rc;
     }
     return compute_priors(g, st, err, errlen);
 }

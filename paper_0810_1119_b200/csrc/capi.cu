@@ -212,7 +212,8 @@ inline void afree(void *p, cudaStream_t st) {
 // message slots of the solve ring: CSR edges, or slice slots (padding included)
 int64_t msg_slots(const DeviceGraph &g) {
     const int64_t ns = g.nslices > 0 ? g.nslots + gabp::kSlotPad : 0;
-    const int64_t m = g.E > ns ? g.E : ns;
+    int64_t m = g.E > ns ? g.E : ns;
+    if ((int64_t)g.dia_D * g.n > m) m = (int64_t)g.dia_D * g.n;  // diagonal layout (dia.cu)
     return m > 0 ? m : 1;
 }
 
@@ -293,11 +294,20 @@ void carve_workspace(gabp_graph *G, Carve &c) {
     const int64_t E = msg_slots(g);
     // node arrays: row order (tiles) or position order (slices, padding lanes + halo)
     const int64_t nn = (g.n > g.npos ? g.n : g.npos) + gabp::kNodePad;
-    for (int b = 0; b < 3; ++b) G->msg[b] = c.take<double2>(E);
+    // the diagonal kernel stages ranges shifted by up to the widest offset: pad both sides
+    const int64_t pad = g.dia_D > 0 ? gabp::dia_pad(g.dia_O) : 0;
+    for (int b = 0; b < 3; ++b) {
+        G->msg[b] = c.take<double2>(E + 2 * pad);
+        if (G->msg[b]) G->msg[b] += pad;
+    }
     for (int b = 0; b < 3; ++b) G->agg[b] = c.take<double2>(nn);
     for (int b = 0; b < 3; ++b) {
-        G->x[b] = c.take<double>(nn);
-        G->p[b] = c.take<double>(nn);
+        G->x[b] = c.take<double>(nn + 2 * pad);
+        G->p[b] = c.take<double>(nn + 2 * pad);
+        if (G->x[b]) {
+            G->x[b] += pad;
+            G->p[b] += pad;
+        }
     }
     for (int b = 0; b < 3; ++b)
         G->rec[b] = g.nslices > 0 ? c.take<gabp::NodeState>(g.npos + gabp::kNodePad) : nullptr;
@@ -362,6 +372,20 @@ SweepArgs make_args(gabp_graph *G) {
     const DeviceGraph &g = G->g;
     a.strip = G->serial_strip;
     a.strip_stride = G->serial_strip_stride;
+    a.dia_D = g.dia_D;
+    a.dia_nl = g.n;
+    a.dia_r0 = g.row_lo;
+    a.dia_r1 = g.row_hi;
+    a.dia_coef = g.dia_coef;
+    a.dia_mask = g.dia_mask;
+    a.dia_cu = g.dia_cu;
+    a.dia_nlc = g.dia_nlc;
+    a.dia_O = g.dia_O;
+    a.dia_W = g.dia_W;
+    for (int k = 0; k < gabp::kDiaMaxD; ++k) {
+        a.dia_off[k] = g.dia_off.v[k];
+        a.dia_opp[k] = g.dia_opp[k];
+    }
     a.n = g.n;
     a.ntiles = g.ntiles;
     a.row_ptr = g.row_ptr;
@@ -863,6 +887,27 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         CK(gabp::launch_small_solve(a, G->g.E, st));
         return finish_loop(G, device_ms);
     }
+    if (sched == GABP_SCHED_BROADCAST && opt->gather_mode == GABP_GATHER_AUTO &&
+        G->g.dia_D > 0) {
+        // stencil graph: the diagonal layout (dia.cu), one launch per sweep, decision of
+        // sweep s-1 at the end of launch s
+        SweepArgs a = make_args(G);
+        G->slice_order = false;
+        CK(gabp::launch_dia_init(a, st));
+        const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
+        const int64_t dtotal = opt->max_iter + 2;
+        G->kernels_launched = 1;
+        CK(cudaEventRecord(G->ev[2], st));
+        while (launched < dtotal) {
+            const int64_t k = dtotal - launched < C ? dtotal - launched : C;
+            for (int64_t q = 0; q < k; ++q) CK(gabp::launch_dia_sweep(a, st));
+            G->kernels_launched += k;
+            launched += k;
+            if (P.after_chunk(st, &rc)) break;
+            if (rc) return rc;
+        }
+        return finish_loop(G, device_ms);
+    }
     rc = check_slice(G, opt);
     if (rc) return rc;
     const int gather = pick_gather(G, opt);
@@ -927,6 +972,7 @@ gabp_graph *new_graph(int device, int *rc) {
     if (e == cudaSuccess) e = gabp::prepare_sweep_kernels();
     if (e == cudaSuccess) e = gabp::prepare_rowpar_kernels();
     if (e == cudaSuccess) e = gabp::prepare_slice_kernels();
+    if (e == cudaSuccess) e = gabp::prepare_dia_kernels();
     if (e == cudaSuccess) {
         // keep freed blocks in the device pool (graphs, workspaces and build scratch are
         // stream-ordered allocations): no re-mapping on the next build or solve
@@ -1167,7 +1213,7 @@ int gabp_graph_info(const gabp_graph_t *G, gabp_graph_info_t *info) {
     info->num_slices = G->g.nslices;
     info->num_slots = G->g.nslots;
     info->slice_variant = G->g.slice_variant;
-    info->reserved = 0;
+    info->dia_diagonals = G->g.dia_D;
     return GABP_OK;
 }
 
@@ -1960,7 +2006,24 @@ int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int32_t gather_mode, in
     o.max_iter = 1;
     o.blowup = 2.0;
     rc = check_options(&o);
-    if (rc == GABP_OK) rc = check_slice(G, &o);
+    if (rc) return rc;
+    if (schedule == GABP_SCHED_BROADCAST && gather_mode == GABP_GATHER_AUTO && G->g.dia_D > 0) {
+        CK(gabp::launch_dia_init(a, st));
+        for (int k = 0; k < 3; ++k) CK(gabp::launch_dia_sweep(a, st));
+        CK(cudaEventRecord(G->ev[2], st));
+        for (int64_t k = 0; k < sweeps; ++k) CK(gabp::launch_dia_sweep(a, st));
+        CK(cudaEventRecord(G->ev[3], st));
+        CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        float dms = 0.f;
+        CK(cudaEventElapsedTime(&dms, G->ev[2], G->ev[3]));
+        if (G->h_ctrl->done)
+            return fail(GABP_EINVAL, "bench sweeps stopped early (diverged at sweep %lld)",
+                        (long long)G->h_ctrl->iterations);
+        *ms_per_sweep = dms / (double)sweeps;
+        return GABP_OK;
+    }
+    rc = check_slice(G, &o);
     if (rc) return rc;
     const int gather = pick_gather(G, &o);
     if (gather == gabp::kGatherSliceParallel && !G->g.stwin) {

@@ -49,6 +49,12 @@ constexpr unsigned long long kNoIndex = ~0ull;  // "no singular edge/node" senti
 
 enum Mode { kModeSolve = 0, kModeSingle = 1 };
 
+// diagonal (stencil) layout, dia.cu: at most kDiaMaxD diagonals j - i = o_k, ascending
+constexpr int kDiaMaxD = 8;
+struct DiaOffsets {
+    int64_t v[kDiaMaxD];
+};
+
 struct __align__(16) EdgeRec {
     uint32_t rev;   // id of the twin edge j -> i
     uint32_t col;   // destination node j
@@ -174,6 +180,16 @@ struct SweepArgs {
                                // residual-only group launch (probe_next)
     int probe_force;           // test hook (GABP_PROBE_FORCE=1): request a probe after every
                                // launch, so every mispredicted probe path runs
+    // diagonal layout (dia.cu; dia_D == 0: not built)
+    int dia_D;
+    int64_t dia_nl, dia_r0, dia_r1;  // node array length, swept rows
+    int64_t dia_nlc;                 // coefficient row stride (nl rounded up to even)
+    int64_t dia_O, dia_W;            // widest offset; blocked tile order chunk (0: identity)
+    const double *dia_coef;          // [D][nlc] (non-uniform coefficients)
+    const uint8_t *dia_mask;         // [nl] occupied diagonals of a row (uniform coefficient)
+    double dia_cu;                   // the one off-diagonal value when dia_mask is set
+    int64_t dia_off[kDiaMaxD];       // o_k, ascending
+    int dia_opp[kDiaMaxD];           // diagonal of -o_k
     double2 *strip;            // serial tasks longer than kRowParMaxDegree: per-warp global
     int64_t strip_stride;      // strips of strip_stride terms (else unused)
     int twin_tail;             // group launch: the exact twin is tail-launched from the
@@ -335,6 +351,16 @@ cudaError_t launch_absmax(int64_t E, const double2 *a, unsigned long long *d_out
 cudaError_t launch_gather(int64_t cnt, const int64_t *idx, const double2 *m, double2 *out,
                           cudaStream_t st);
 
+// the broadcast solve on the diagonal layout (dia.cu): build_dia after the CSR (a no-op
+// unless every edge lies on one of <= kDiaMaxD symmetric diagonals); launch_dia_init forms
+// the aggregates of S_0 in ring slot 0, then one launch_dia_sweep per sweep
+cudaError_t prepare_dia_kernels();
+cudaError_t launch_dia_init(const SweepArgs &a, cudaStream_t st);
+cudaError_t launch_dia_sweep(const SweepArgs &a, cudaStream_t st);
+// elements of padding the diagonal kernel needs on both sides of the message and node-state
+// arrays (every staged range in bounds)
+int64_t dia_pad(int64_t max_off);
+
 // the whole broadcast solve of a small graph in one persistent CTA (small.cu): messages
 // and node states in shared memory, 32 B x (n + E)
 bool small_fits(int64_t n, int64_t E);
@@ -377,6 +403,14 @@ struct DeviceGraph {
     uint32_t *scol = nullptr;
     double *scoef = nullptr;
     uint32_t *stwin = nullptr;  // built on the first parallel-schedule solve (build_stwin)
+    // diagonal layout (build_dia, dia.cu); dia_D == 0 when the graph is not a stencil
+    int dia_D = 0;
+    int64_t dia_nlc = 0, dia_O = 0, dia_W = 0;
+    double *dia_coef = nullptr;
+    uint8_t *dia_mask = nullptr;  // uniform coefficient dia_cu: occupancy bits per row
+    double dia_cu = 0.0;
+    DiaOffsets dia_off{};
+    int dia_opp[kDiaMaxD] = {};
 };
 
 // Builds CSR + twin index + tiles from device-resident inputs.  Returns a GABP_* code
@@ -390,6 +424,7 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
 void free_graph(DeviceGraph &g, cudaStream_t st);
 // slice layout of the swept rows (slice.cu); GABP_OK or an error (the tile layout stays)
 int build_slices(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
+int build_dia(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
 cudaError_t prepare_slice_kernels();
 cudaError_t launch_slice_sweep(const SweepArgs &a, cudaStream_t st);
 cudaError_t launch_slice_part(const SweepArgs &a, int reserve_sms, cudaStream_t st);
