@@ -416,7 +416,7 @@ SweepArgs make_args(gabp_graph *G) {
     a.slice_path = 0;
     a.nslices = g.nslices;
     a.slice_info = g.slice_info;
-    a.gorder = g.gorder;
+    a.gorder = getenv("GABP_NO_GORDER") ? nullptr : g.gorder;  // (A/B: claim order)
     a.sdeg = g.sdeg;
     a.srow = g.srow;
     a.snd = g.snd;
@@ -666,7 +666,8 @@ int64_t split_slices(const gabp_graph *G) {
 // What this rank's layout allows: bit 0 the slice layout, bit 1 the split sweep.
 int dist_local_caps(const gabp_graph *G) {
     const int sl = G->g.nslices > 0 ? 1 : 0;
-    return sl | ((sl && split_slices_local(G) > 0) ? 2 : 0);
+    const bool nosplit = getenv("GABP_NO_SPLIT") != nullptr;  // (A/B: whole sweeps)
+    return sl | ((sl && !nosplit && split_slices_local(G) > 0) ? 2 : 0);
 }
 
 // Fixes the agreed protocol (caps = the AND over the ranks of dist_local_caps) and maps the

@@ -583,8 +583,10 @@ struct __align__(128) GRing {
     uint64_t full[kGS];
     uint64_t empty[kGS];
     GMeta meta[kGS];
+#ifndef GABP_R1_GRP
     double gres[kGResSlots][kGroup];  // slice partials of a group's residual rows
     uint32_t gcnt[kGResSlots];        // slices committed
+#endif
 };
 
 // Residual of group g (the seq-th group this CTA ran): every consumer warp sums its slice's
@@ -593,6 +595,9 @@ struct __align__(128) GRing {
 // bits whichever CTA claimed which group (the claims are dynamic).
 __device__ __forceinline__ void grp_resid_commit(const SweepArgs &a, GRing &G, int warp,
                                                  int lane, int64_t g, uint32_t seq, double rr) {
+#if defined(GABP_NO_RESID_COMMIT) || defined(GABP_R1_GRP)
+    return;
+#else
     rr = warp_sum(rr);
     const int k = (int)(seq % kGResSlots);
     unsigned last = 0u;
@@ -610,6 +615,7 @@ __device__ __forceinline__ void grp_resid_commit(const SweepArgs &a, GRing &G, i
             G.gcnt[k] = 0u;
         }
     }
+#endif
 }
 constexpr size_t kGrpSmem = sizeof(GRing);
 
@@ -647,7 +653,9 @@ __device__ __forceinline__ void grp_ring_init(GRing &G, int tid) {
         t_mbar_init(&G.full[tid], 1u);
         t_mbar_init(&G.empty[tid], (unsigned)kGroup);
     }
+#ifndef GABP_R1_GRP
     if (tid < kGResSlots) G.gcnt[tid] = 0u;
+#endif
 }
 
 __device__ __forceinline__ uint2 group_info(const SweepArgs &a, int64_t g, int64_t g_hi) {
@@ -825,6 +833,29 @@ __device__ __forceinline__ void t_gather(const GStage &S, const GMeta &m, const 
     }
 }
 
+// Stage data a consumer reads from shared memory and uses only after releasing the stage
+// must have ARRIVED in registers before the release: the mbarrier arrive does not wait for
+// the lane's outstanding shared loads, and the producer's next bulk copy may overwrite the
+// stage while one is still in flight (seen as a rare wrong change statistic -- the old
+// message I^{(s-2)} is the one operand used after the release).  An empty asm that takes
+// the values as inputs makes the lane wait on their scoreboard first.
+// (the token is an integer fold of the values' bits, fed to the arrive as an operand: the
+// folding instructions read the loaded registers, so they wait for the loads, and the arrive
+// cannot issue before them)
+__device__ __forceinline__ uint32_t hold(uint32_t tok, double v) {
+    return tok ^ (uint32_t)__double2hiint(v) ^ (uint32_t)__double2loint(v);
+}
+__device__ __forceinline__ uint32_t hold(uint32_t tok, double2 v) {
+    return hold(hold(tok, v.x), v.y);
+}
+__device__ __forceinline__ void t_arrive_after(uint64_t *bar, uint32_t tok) {
+    asm volatile(
+        "{\n .reg .b32 t;\n mov.b32 t, %1;\n"
+        " mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(su32(bar)),
+        "r"(tok)
+        : "memory");
+}
+
 // Running sums of the rows a consumer lane owns (one row per group).
 struct GRow {
     uint32_t d = 0, seq = 0;
@@ -884,8 +915,11 @@ __device__ __forceinline__ bool grp_step(const SweepArgs &a, const Ring<R> &r, d
             edge_msg<false>(cc[u], rc[u], pe2, nu2, m2p[u], m2m[u], st);
         }
     }
-    __syncwarp();
-    if (lane == 0) t_arrive(&G.empty[s0]);  // the stage's data is in registers now
+    uint32_t tok = 0u;
+#pragma unroll
+    for (int u = 0; u < CW; ++u) tok = hold(tok, i2v[u]);  // (used after the release)
+    tok = __reduce_or_sync(~0u, tok);  // every lane's loads landed
+    if (lane == 0) t_arrive_after(&G.empty[s0], tok);  // the stage's data is in registers now
 #pragma unroll
     for (int u = 0; u < CW; ++u) {  // incoming of S_{s-1}
         const bool v = m.b * CW + u < d;
@@ -905,7 +939,13 @@ __device__ __forceinline__ bool grp_step(const SweepArgs &a, const Ring<R> &r, d
             msg_stats<false>(st, a, ip[u], im[u], i2v[u], pe[u], p, q);
         }
     }
+#if defined(GABP_R1_GRP) || defined(GABP_R1_ROWDONE)
+    if (m.b + 1 == m.nb && row.diag != 0.0)  // row done (A_ii == 0: padding lane)
+        node_done<(PH == 4 ? 3 : PH), false>(st, a, r.g1, xh, p, row.sp, row.sn, row.y, row.rhs_i);
+    if (false) {
+#else
     if (m.b + 1 == m.nb) {  // rows done (A_ii == 0: padding lane)
+#endif
         double rr = 0.0;
         if (row.diag != 0.0)
             rr = node_done<(PH == 4 ? 3 : PH), false, false>(st, a, r.g1, xh, p, row.sp, row.sn,
@@ -974,8 +1014,11 @@ __device__ __forceinline__ void grp_consume_res(const SweepArgs &a, Stats &st, i
             cv[slot][u] = st_c<5>(S, u)[t];
             xv[slot][u] = v ? __ldcg(&r.g2[j].x) : 0.0;
         }
-        __syncwarp();
-        if (lane == 0) t_arrive(&G.empty[sg]);
+        uint32_t tok = 0u;
+#pragma unroll
+        for (int u = 0; u < CW; ++u) tok = hold(tok, cv[slot][u]);  // (used after the release)
+        tok = __reduce_or_sync(~0u, tok);
+        if (lane == 0) t_arrive_after(&G.empty[sg], tok);
         return true;
     };
     // chunks are issued strictly in order and never past the end marker (the producer
