@@ -104,6 +104,10 @@ typedef struct {
 } gabp_report_t;
 
 const char *gabp_last_error(void);
+/* Gives the device memory the library keeps for reuse (released solve workspaces and
+ * staging buffers of earlier graphs) back to the device; an allocation that fails does this
+ * once by itself before it reports GABP_ENOMEM. */
+int gabp_release_cached(int32_t device);
 int gabp_version(void);
 int gabp_device_count(int32_t *count);
 

@@ -28,7 +28,7 @@ GATHER_IDS = {"auto": 0, "message": 1, "recompute": 2, "slice": 3, "rows": 4}
 
 # every symbol include/gabp_b200.h declares (checked by tests/test_host.py)
 EXPORTED = (
-    "gabp_last_error", "gabp_version", "gabp_device_count",
+    "gabp_last_error", "gabp_version", "gabp_device_count", "gabp_release_cached",
     "gabp_state_blown", "gabp_state_gather",
     "gabp_graph_create", "gabp_graph_create_device", "gabp_graph_create_device_ex",
     "gabp_graph_create_dense",
@@ -137,6 +137,7 @@ def load():
                                              ctypes.POINTER(ctypes.c_int64),
                                              ctypes.POINTER(ctypes.c_int32)]),
         "gabp_bench_sweeps": (ctypes.c_int, [_vp, _i32, _i32, _i64, _dp]),
+        "gabp_release_cached": (ctypes.c_int, [_i32]),
         "gabp_graph_create_ex": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
                                                 _i32, ctypes.POINTER(_vp)]),
         "gabp_graph_create_device_ex": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp,
@@ -183,3 +184,9 @@ def device_count() -> int:
 def default_device() -> int:
     env = os.environ.get("LOCAL_RANK")
     return int(env) if env is not None else 0
+
+
+def release_cached(device: int | None = None) -> None:
+    """Give the device memory the library caches for reuse back to the device
+    (gabp_release_cached)."""
+    check(load().gabp_release_cached(default_device() if device is None else int(device)))

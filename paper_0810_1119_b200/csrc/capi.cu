@@ -275,6 +275,29 @@ bool spare_keep(int kind, int device, void *p, size_t bytes) {
     return false;
 }
 
+// Frees the spare blocks of a device and trims its pool: the memory of earlier graphs comes
+// back to the device (on an allocation failure, and on request: gabp_release_cached).
+void release_spares(int device) {
+    std::vector<void *> ps;
+    {
+        std::lock_guard<std::mutex> lk(g_spare_mu);
+        for (auto &k : g_spare)
+            for (auto &b : k)
+                if (b.p && b.device == device) {
+                    ps.push_back(b.p);
+                    b.p = nullptr;
+                }
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    for (void *p : ps) cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    cudaSetDevice(cur);
+}
+
 // One stream-ordered block from the retained device pool holds the whole solve workspace
 // (a repeated solve, or a new graph of similar size, reuses the cached block).
 struct Carve {
@@ -329,7 +352,12 @@ int ensure_workspace(gabp_graph *G, int64_t max_iter) {
         Carve size{nullptr};
         carve_workspace(G, size);
         G->ws_base = static_cast<char *>(spare_take(0, G->device, size.off));
-        if (!G->ws_base) CK(cudaMallocAsync(&G->ws_base, size.off, st));
+        if (!G->ws_base && cudaMallocAsync(&G->ws_base, size.off, st) != cudaSuccess) {
+            cudaGetLastError();  // out of memory: give the cached spares back, retry once
+            G->ws_base = nullptr;
+            release_spares(G->device);
+            CK(cudaMallocAsync(&G->ws_base, size.off, st));
+        }
         G->ws_bytes = size.off;
         tw1 = host_ms();
         Carve c{G->ws_base};
@@ -1026,6 +1054,16 @@ static int create_device_range(int64_t n, int64_t npairs, const double *d_diag,
     rc = gabp::build_graph_device(G->g, n, npairs, d_diag, d_rhs, d_pair_i, d_pair_j, d_pair_v,
                                   row_lo, row_hi, G->stream, g_err, sizeof(g_err), idx_ready,
                                   val_ready);
+    if (rc == GABP_ENOMEM) {  // the cached spares of earlier graphs back to the device, once
+        cudaStreamSynchronize(G->stream);
+        gabp::free_graph(G->g, G->stream);
+        cudaStreamSynchronize(G->stream);
+        cudaGetLastError();
+        release_spares(device);
+        rc = gabp::build_graph_device(G->g, n, npairs, d_diag, d_rhs, d_pair_i, d_pair_j,
+                                      d_pair_v, row_lo, row_hi, G->stream, g_err,
+                                      sizeof(g_err), idx_ready, val_ready);
+    }
     if (rc != GABP_OK) {
         cudaStreamSynchronize(G->stream);
         gabp::free_graph(G->g, G->stream);
@@ -1035,6 +1073,14 @@ static int create_device_range(int64_t n, int64_t npairs, const double *d_diag,
         return rc;
     }
     *out = G;
+    return GABP_OK;
+}
+
+int gabp_release_cached(int32_t device) {
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) return fail(GABP_EINVAL, "no device %d", device);
+    release_spares(device);
     return GABP_OK;
 }
 
