@@ -101,6 +101,9 @@ typedef struct {
                                  once after the decision); 0 for multi-rank solves */
     int64_t split_sweeps;     /* multi-rank: sweeps run split (boundary rows first, halo
                                  exchange under the interior rows) */
+    int64_t dist_layout;      /* multi-rank kernel family agreed by the ranks: 0 none (one
+                                 rank), 1 slice layout (node-state halo), 2 row tiles,
+                                 3 diagonal layout (message + node-state halo) */
 } gabp_report_t;
 
 const char *gabp_last_error(void);

@@ -84,6 +84,12 @@ struct DistState {
     // -1 until agreed
     int use_slices = -1, use_split = -1;
     int64_t split_launches = 0;      // split sweeps run by the last solve (report)
+    // diagonal layout across ranks (every rank a stencil graph with the same diagonals):
+    // per peer the diagonals whose incoming messages cross the cut, each way
+    int use_dia = 0;
+    std::vector<gabp::DiaHalo> dsend, drecv;
+    int dia_w = 0;                   // doubles per exchanged node: {P, x} + 2 per diagonal
+    double *d_dsbuf = nullptr, *d_drbuf = nullptr;
 };
 
 // pinned host mirror of a graph's controller and poll flags (capi.cu pinned_get)
@@ -477,6 +483,8 @@ void release_workspace(gabp_graph *G) {
         cudaFree(G->dist->d_ridx);
         cudaFree(G->dist->d_sbuf);
         cudaFree(G->dist->d_rbuf);
+        if (G->dist->d_dsbuf) cudaFree(G->dist->d_dsbuf);
+        if (G->dist->d_drbuf) cudaFree(G->dist->d_drbuf);
         cudaFree(G->dist->d_stats);
         if (G->dist->xstream) cudaStreamDestroy(G->dist->xstream);
         if (G->dist->ev_bnd) cudaEventDestroy(G->dist->ev_bnd);
@@ -691,6 +699,17 @@ int64_t split_slices(const gabp_graph *G) {
     return split_slices_local(G);
 }
 
+// Signature of a rank's diagonal layout (0: none): ranks run it together only when every
+// rank has the same diagonals.
+int64_t dia_signature(const gabp_graph *G) {
+    const DeviceGraph &g = G->g;
+    if (g.dia_D <= 0 || getenv("GABP_NO_DIST_DIA")) return 0;
+    uint64_t h = 1469598103934665603ull ^ (uint64_t)g.dia_D;
+    for (int k = 0; k < g.dia_D; ++k) h = (h ^ (uint64_t)g.dia_off.v[k]) * 1099511628211ull;
+    h ^= g.dia_mask ? 0x5bd1e995ull : 0ull;  // (the same kernel specialization too)
+    return (int64_t)(h & 0x3fffffffffffffffull) | 1;
+}
+
 // What this rank's layout allows: bit 0 the slice layout, bit 1 the split sweep.
 int dist_local_caps(const gabp_graph *G) {
     const int sl = G->g.nslices > 0 ? 1 : 0;
@@ -698,12 +717,39 @@ int dist_local_caps(const gabp_graph *G) {
     return sl | ((sl && !nosplit && split_slices_local(G) > 0) ? 2 : 0);
 }
 
-// Fixes the agreed protocol (caps = the AND over the ranks of dist_local_caps) and maps the
-// halo lists into position numbering when the slice path runs.
-int dist_agree(gabp_graph *G, int caps) {
+// Fixes the agreed protocol (caps = the AND over the ranks of dist_local_caps; dia = every
+// rank has the same diagonal layout) and maps the halo lists into position numbering when
+// the slice path runs.  The diagonal layout runs on local row numbering: to the peer above a
+// rank sends its boundary rows' incoming messages on the positive diagonals (the peer's rows
+// read them as twins), to the peer below those on the negative ones.
+int dist_agree(gabp_graph *G, int caps, bool dia) {
     DistState *D = G->dist;
     D->use_slices = caps & 1;
     D->use_split = (caps & 2) ? 1 : 0;
+    D->use_dia = dia ? 1 : 0;
+    if (dia) {
+        const DeviceGraph &g = G->g;
+        D->dsend.assign(D->peers.size(), gabp::DiaHalo{});
+        D->drecv.assign(D->peers.size(), gabp::DiaHalo{});
+        for (size_t q = 0; q < D->peers.size(); ++q) {
+            const bool up = D->peers[q] > D->rank;
+            for (int k = 0; k < g.dia_D; ++k) {
+                const bool pos = g.dia_off.v[k] > 0;
+                gabp::DiaHalo &s = D->dsend[q], &r = D->drecv[q];
+                if (pos == up) s.diag[s.nd++] = k;
+                else r.diag[r.nd++] = k;
+            }
+        }
+        D->dia_w = 2 + g.dia_D;  // {P, x} + 2 x (D / 2) message doubles
+        int64_t ns = 0, nr = 0;
+        for (size_t q = 0; q < D->peers.size(); ++q) {
+            ns += (D->scount[q] + 1) & ~1ll;
+            nr += (D->rcount[q] + 1) & ~1ll;
+        }
+        CK(cudaMalloc(&D->d_dsbuf, sizeof(double) * D->dia_w * (ns > 0 ? ns : 1)));
+        CK(cudaMalloc(&D->d_drbuf, sizeof(double) * D->dia_w * (nr > 0 ? nr : 1)));
+        return GABP_OK;  // (halo lists stay in row numbering)
+    }
     if (D->use_slices) {
         int64_t ns = 0, nr = 0;
         for (size_t q = 0; q < D->peers.size(); ++q) {
@@ -824,12 +870,80 @@ int dist_launch_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
     return GABP_OK;
 }
 
+// ---- diagonal layout across ranks --------------------------------------------------------
+int dia_pack_all(gabp_graph *G, const SweepArgs &a, int64_t s_fix, int post, cudaStream_t st) {
+    DistState *D = G->dist;
+    for (size_t q = 0; q < D->peers.size(); ++q)
+        CK(gabp::launch_dia_pack(a, D->d_sidx + D->soff[q], D->scount[q],
+                                 D->d_dsbuf + D->dia_w * D->soff[q], D->dsend[q], s_fix, post,
+                                 st));
+    return GABP_OK;
+}
+int dia_unpack_all(gabp_graph *G, const SweepArgs &a, int64_t s_fix, int post,
+                   cudaStream_t st) {
+    DistState *D = G->dist;
+    for (size_t q = 0; q < D->peers.size(); ++q)
+        CK(gabp::launch_dia_unpack(a, D->d_ridx + D->roff[q], D->rcount[q],
+                                   D->d_drbuf + D->dia_w * D->roff[q], D->drecv[q], s_fix,
+                                   post, st));
+    return GABP_OK;
+}
+// the halo's point-to-point part, inside an open NCCL group
+int dia_p2p(gabp_graph *G, cudaStream_t st) {
+    DistState *D = G->dist;
+    for (size_t q = 0; q < D->peers.size(); ++q) {
+        if (D->scount[q])
+            NK(g_nccl.send(D->d_dsbuf + D->dia_w * D->soff[q], D->dia_w * D->scount[q],
+                           ncclFloat64, D->peers[q], D->comm, st));
+        if (D->rcount[q])
+            NK(g_nccl.recv(D->d_drbuf + D->dia_w * D->roff[q], D->dia_w * D->rcount[q],
+                           ncclFloat64, D->peers[q], D->comm, st));
+    }
+    return GABP_OK;
+}
+// S_0's aggregates of the owned rows, then the halo rows' from the peers (their local
+// priors are placeholders)
+int dia_start_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
+    DistState *D = G->dist;
+    CK(gabp::launch_dia_init(a, st));
+    int rc = dia_pack_all(G, a, 0, 0, st);
+    if (rc) return rc;
+    if (D->world > 1 && !D->peers.empty()) {
+        NK(g_nccl.groupStart());
+        rc = dia_p2p(G, st);
+        if (rc) return rc;
+        NK(g_nccl.groupEnd());
+    }
+    return dia_unpack_all(G, a, 0, 0, st);
+}
+// One launch: the sweep (its last CTA publishes the rank's statistics of sweep s-1), the
+// halo of S_s packed at once, then one NCCL group with the statistics all-reduce and the
+// point-to-point halo, the decision, the unpack.
+int dia_launch_nccl(gabp_graph *G, const SweepArgs &a, cudaStream_t st) {
+    DistState *D = G->dist;
+    CK(gabp::launch_dia_sweep(a, st));
+    int rc = dia_pack_all(G, a, -1, 0, st);
+    if (rc) return rc;
+    if (D->world > 1) {
+        NK(g_nccl.groupStart());
+        NK(g_nccl.allReduce(D->d_stats, D->d_stats, 5, ncclFloat64, ncclMax, D->comm, st));
+        NK(g_nccl.allReduce(D->d_stats + 5, D->d_stats + 5, 1, ncclFloat64, ncclSum, D->comm,
+                            st));
+        rc = dia_p2p(G, st);
+        if (rc) return rc;
+        NK(g_nccl.groupEnd());
+    }
+    CK(gabp::launch_dia_finish(a, st));
+    return dia_unpack_all(G, a, -1, 1, st);
+}
+
 SweepArgs make_dist_args(gabp_graph *G) {
     SweepArgs a = make_args(G);
     a.dist = 1;
     a.dstats = G->dist->d_stats;
     a.msg_lag = dist_gather(G) == gabp::kGatherSlice ? 1 : 0;
     a.slice_path = a.msg_lag;
+    if (G->dist->use_dia) a.msg_lag = a.slice_path = 0;
     return a;
 }
 
@@ -851,13 +965,17 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         if (opt->schedule != GABP_SCHED_BROADCAST)
             return fail(GABP_EINVAL, "the multi-rank solve runs the broadcast schedule");
         SweepArgs a = make_dist_args(G);
-        G->slice_order = dist_gather(G) == gabp::kGatherSlice;
+        G->slice_order = !G->dist->use_dia && dist_gather(G) == gabp::kGatherSlice;
         const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
         CK(cudaEventRecord(G->ev[2], st));
+        if (G->dist->use_dia) {
+            rc = dia_start_nccl(G, a, st);
+            if (rc) return rc;
+        }
         while (launched < total) {
             const int64_t k = total - launched < C ? total - launched : C;
             for (int64_t q = 0; q < k; ++q) {
-                rc = dist_launch_nccl(G, a, st);
+                rc = G->dist->use_dia ? dia_launch_nccl(G, a, st) : dist_launch_nccl(G, a, st);
                 if (rc) return rc;
             }
             launched += k;
@@ -990,6 +1108,7 @@ void fill_report(gabp_graph *G, const gabp_options_t *opt, double ms, double rsq
     rep->residual_probes = c.probes;
     rep->kernel_launches = G->kernels_launched + c.twin_launches;
     rep->split_sweeps = G->dist ? G->dist->split_launches : 0;
+    rep->dist_layout = !G->dist ? 0 : G->dist->use_dia ? 3 : G->dist->use_slices ? 1 : 2;
     rep->final_rel_residual =
         (c.n_hist >= 1 && G->g.rhs_norm > 0.0) ? sqrt(rsq_last) / G->g.rhs_norm : NAN;
 }
@@ -1828,6 +1947,8 @@ int gabp_dist_attach(gabp_graph_t *G, const void *nccl_id, int32_t rank, int32_t
     CK(cudaMemcpy(D->d_ridx, ri.data(), sizeof(uint32_t) * ri.size(), cudaMemcpyHostToDevice));
     if (D->local) return GABP_OK;  // agreed over the partitions by gabp_dist_solve_local
     int caps = dist_local_caps(G);
+    const int64_t sig = dia_signature(G);
+    bool dia = sig != 0;
     if (world > 1) {
         int rc = load_nccl();
         if (rc) return rc;
@@ -1846,8 +1967,95 @@ int gabp_dist_attach(gabp_graph_t *G, const void *nccl_id, int32_t rank, int32_t
         CK(cudaStreamSynchronize(G->stream));
         cudaFree(d_caps);
         caps = (ag[0] ? 1 : 0) | (ag[1] ? 2 : 0);
+        // the diagonal layout only if every rank has the same one: min and max of the
+        // signatures agree (max as the min of the negated)
+        int64_t *d_sig = nullptr;
+        CK(cudaMalloc(&d_sig, sizeof(int64_t) * 2));
+        const int64_t hs[2] = {sig, -sig};
+        CK(cudaMemcpy(d_sig, hs, sizeof(hs), cudaMemcpyHostToDevice));
+        NK(g_nccl.allReduce(d_sig, d_sig, 2, ncclInt64, ncclMin, D->comm, G->stream));
+        int64_t as[2] = {0, 0};
+        CK(cudaMemcpyAsync(as, d_sig, sizeof(as), cudaMemcpyDeviceToHost, G->stream));
+        CK(cudaStreamSynchronize(G->stream));
+        cudaFree(d_sig);
+        dia = as[0] != 0 && as[0] == -as[1];
     }
-    return dist_agree(G, caps);
+    return dist_agree(G, caps, dia);
+}
+
+// In-process partitions on the diagonal layout: the NCCL loop of dia_launch_nccl with the
+// statistics reduced on the host and the halo moved by device copies.
+int dia_move_local(int nparts, gabp_graph_t **parts) {
+    for (int p = 0; p < nparts; ++p) CK(cudaStreamSynchronize(parts[p]->stream));
+    for (int p = 0; p < nparts; ++p) {
+        DistState *D = parts[p]->dist;
+        for (size_t q = 0; q < D->peers.size(); ++q) {
+            const int src = D->peers[q];
+            DistState *S = parts[src]->dist;
+            size_t qs = 0;
+            while (qs < S->peers.size() && S->peers[qs] != p) ++qs;
+            if (qs == S->peers.size() || S->scount[qs] != D->rcount[q] ||
+                S->dsend[qs].nd != D->drecv[q].nd)
+                return fail(GABP_EINVAL, "halo lists of ranks %d and %d disagree", p, src);
+            CK(cudaMemcpyAsync(D->d_drbuf + D->dia_w * D->roff[q],
+                               S->d_dsbuf + S->dia_w * S->soff[qs],
+                               sizeof(double) * D->dia_w * D->rcount[q],
+                               cudaMemcpyDeviceToDevice, parts[p]->stream));
+        }
+    }
+    return GABP_OK;
+}
+
+int dia_solve_local(int nparts, gabp_graph_t **parts, std::vector<SweepArgs> &args,
+                    int64_t total, double *device_ms) {
+    for (int p = 0; p < nparts; ++p) {
+        CK(gabp::launch_dia_init(args[p], parts[p]->stream));
+        int rc = dia_pack_all(parts[p], args[p], 0, 0, parts[p]->stream);
+        if (rc) return rc;
+    }
+    int rc = dia_move_local(nparts, parts);
+    if (rc) return rc;
+    for (int p = 0; p < nparts; ++p) {
+        rc = dia_unpack_all(parts[p], args[p], 0, 0, parts[p]->stream);
+        if (rc) return rc;
+    }
+    gabp_graph *G0 = parts[0];
+    for (int64_t s = 0; s < total; ++s) {
+        for (int p = 0; p < nparts; ++p) CK(gabp::launch_dia_sweep(args[p], parts[p]->stream));
+        double red[6] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0};
+        for (int p = 0; p < nparts; ++p) {
+            double st6[6];
+            CK(cudaMemcpyAsync(st6, parts[p]->dist->d_stats, sizeof(st6),
+                               cudaMemcpyDeviceToHost, parts[p]->stream));
+            CK(cudaStreamSynchronize(parts[p]->stream));
+            for (int k = 0; k < 5; ++k) red[k] = fmax(red[k], st6[k]);
+            red[5] += st6[5];
+        }
+        for (int p = 0; p < nparts; ++p) {
+            CK(cudaMemcpyAsync(parts[p]->dist->d_stats, red, sizeof(red), cudaMemcpyHostToDevice,
+                               parts[p]->stream));
+            CK(gabp::launch_dia_finish(args[p], parts[p]->stream));
+            rc = dia_pack_all(parts[p], args[p], -1, 1, parts[p]->stream);
+            if (rc) return rc;
+        }
+        rc = dia_move_local(nparts, parts);
+        if (rc) return rc;
+        for (int p = 0; p < nparts; ++p) {
+            rc = dia_unpack_all(parts[p], args[p], -1, 1, parts[p]->stream);
+            if (rc) return rc;
+        }
+        for (int p = 0; p < nparts; ++p) CK(cudaStreamSynchronize(parts[p]->stream));
+        int32_t done = 0;
+        CK(cudaMemcpy(&done, &G0->ctrl->done, sizeof(done), cudaMemcpyDeviceToHost));
+        if (done) break;
+    }
+    double ms = 0.0;
+    for (int p = 0; p < nparts; ++p) {
+        int rc2 = finish_loop(parts[p], p == 0 ? &ms : nullptr);
+        if (rc2 && p == 0) return rc2;
+    }
+    if (device_ms) *device_ms = ms;
+    return GABP_OK;
 }
 
 // One GPU, several row blocks in this process: the multi-rank loop with the cross-rank
@@ -1865,9 +2073,14 @@ int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_optio
     std::vector<SweepArgs> args(nparts);
     if (parts[0]->dist->use_slices < 0) {  // first solve: agree on the protocol (AND of caps)
         int caps = 3;
-        for (int p = 0; p < nparts; ++p) caps &= dist_local_caps(parts[p]);
+        const int64_t sig0 = dia_signature(parts[0]);
+        bool dia = sig0 != 0;
         for (int p = 0; p < nparts; ++p) {
-            int rc = dist_agree(parts[p], caps);
+            caps &= dist_local_caps(parts[p]);
+            dia = dia && dia_signature(parts[p]) == sig0;
+        }
+        for (int p = 0; p < nparts; ++p) {
+            int rc = dist_agree(parts[p], caps, dia);
             if (rc) return rc;
         }
     }
@@ -1875,11 +2088,13 @@ int gabp_dist_solve_local(int32_t nparts, gabp_graph_t **parts, const gabp_optio
         int rc = solve_setup(parts[p], opt);
         if (rc) return rc;
         args[p] = make_dist_args(parts[p]);
-        parts[p]->slice_order = dist_gather(parts[p]) == gabp::kGatherSlice;
+        parts[p]->slice_order = !parts[p]->dist->use_dia &&
+                                dist_gather(parts[p]) == gabp::kGatherSlice;
     }
     gabp_graph *G0 = parts[0];
     CK(cudaEventRecord(G0->ev[2], G0->stream));
     const int64_t total = opt->max_iter + 2;
+    if (parts[0]->dist->use_dia) return dia_solve_local(nparts, parts, args, total, device_ms);
     for (int64_t s = 0; s < total; ++s) {
         for (int p = 0; p < nparts; ++p) {
             if (const int64_t nbs = split_slices(parts[p])) {  // the NCCL path's split sweep

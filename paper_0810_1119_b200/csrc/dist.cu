@@ -77,6 +77,77 @@ __global__ void halo_unpack_kernel(const SweepArgs a, const uint32_t *idx, int64
     }
 }
 
+// ---- diagonal layout (dia.cu) -------------------------------------------------------------
+// Launch s of the diagonal kernel decides sweep s-1: its statistics slots are sweep s's, the
+// aggregates' singular test is sweep s+1's, the residual is x^{(s-1)}'s; the published (and
+// now reduced) statistics are sweep s-1's (dia.cu dia_epilogue).
+__global__ void dia_finish_kernel(const SweepArgs a) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    volatile Ctrl *c = a.ctrl;
+    if (c->done) return;
+    const int64_t s = c->next_sweep;
+    const int ms = (int)((s - 1) % kStatSlots);
+    const double *d = a.dstats;
+    c->change_bits[ms] = (unsigned long long)__double_as_longlong(d[0]);
+    c->msg_nonfinite[ms] = (int32_t)d[1];
+    c->means_nonfinite[ms] = d[2] > 0.0 ? 1 : 0;
+    c->singular_min[ms] = d[3] > -1e299 ? (unsigned long long)(-d[3]) : kNoIndex;
+    c->agg_singular[ms] = d[4] > -1e299 ? (unsigned long long)(-d[4]) : kNoIndex;
+    decide_sweep(c, a, s - 1, d[5]);
+    const int n1 = (int)((s + 1) % kStatSlots), n2 = (int)((s + 2) % kStatSlots);
+    c->change_bits[n1] = 0ull;
+    c->msg_nonfinite[n1] = 0;
+    c->means_nonfinite[n1] = 0;
+    c->singular_min[n1] = kNoIndex;
+    c->agg_singular[n2] = kNoIndex;
+    c->next_sweep = s + 1;
+    __threadfence();
+}
+
+// Halo of the diagonal layout: per exchanged node {P_i, x_i} of S_s and the row's incoming
+// messages on the listed diagonals -- the ones a neighbour across the cut reads as twins
+// (the peer's row j needs m_{j -> i} = row i's incoming slot from j for its update of
+// m_{i -> j}).  s < 0: the sweep of the launch just run (next_sweep, minus one after its
+// finish kernel).
+__global__ void dia_pack_kernel(const SweepArgs a, const uint32_t *idx, int64_t cnt,
+                                double *buf, DiaHalo h, int64_t s_fix, int post_finish) {
+    const int64_t s = s_fix >= 0 ? s_fix
+                                 : ((volatile Ctrl *)a.ctrl)->next_sweep - (post_finish ? 1 : 0);
+    const double *p = a.p[s % 3], *x = a.x[s % 3];
+    const double2 *m = a.msg[s & 1];
+    const int w = 2 + 2 * h.nd;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx[k];
+        double *b = buf + k * w;
+        b[0] = p[i];
+        b[1] = x[i];
+        for (int q = 0; q < h.nd; ++q) {
+            const double2 v = m[(int64_t)h.diag[q] * a.dia_nl + i];
+            b[2 + 2 * q] = v.x;
+            b[3 + 2 * q] = v.y;
+        }
+    }
+}
+__global__ void dia_unpack_kernel(const SweepArgs a, const uint32_t *idx, int64_t cnt,
+                                  const double *buf, DiaHalo h, int64_t s_fix,
+                                  int post_finish) {
+    const int64_t s = s_fix >= 0 ? s_fix
+                                 : ((volatile Ctrl *)a.ctrl)->next_sweep - (post_finish ? 1 : 0);
+    double *p = a.p[s % 3], *x = a.x[s % 3];
+    double2 *m = a.msg[s & 1];
+    const int w = 2 + 2 * h.nd;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx[k];
+        const double *b = buf + k * w;
+        p[i] = b[0];
+        x[i] = b[1];
+        for (int q = 0; q < h.nd; ++q)
+            m[(int64_t)h.diag[q] * a.dia_nl + i] = make_double2(b[2 + 2 * q], b[3 + 2 * q]);
+    }
+}
+
 inline unsigned blocks_for(int64_t cnt) {
     int64_t b = (cnt + 255) / 256;
     if (b < 1) b = 1;
@@ -88,6 +159,26 @@ inline unsigned blocks_for(int64_t cnt) {
 
 cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st) {
     finish_kernel<<<1, 32, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dia_finish(const SweepArgs &a, cudaStream_t st) {
+    dia_finish_kernel<<<1, 32, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dia_pack(const SweepArgs &a, const uint32_t *idx, int64_t cnt, double *buf,
+                            const DiaHalo &h, int64_t s_fix, int post_finish, cudaStream_t st) {
+    if (cnt <= 0) return cudaSuccess;
+    dia_pack_kernel<<<blocks_for(cnt), 256, 0, st>>>(a, idx, cnt, buf, h, s_fix, post_finish);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dia_unpack(const SweepArgs &a, const uint32_t *idx, int64_t cnt,
+                              const double *buf, const DiaHalo &h, int64_t s_fix,
+                              int post_finish, cudaStream_t st) {
+    if (cnt <= 0) return cudaSuccess;
+    dia_unpack_kernel<<<blocks_for(cnt), 256, 0, st>>>(a, idx, cnt, buf, h, s_fix, post_finish);
     return cudaGetLastError();
 }
 

@@ -368,6 +368,18 @@ cudaError_t launch_small_solve(const SweepArgs &a, int64_t E, cudaStream_t st);
 
 // multi-rank helpers (dist.cu)
 cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st);
+// diagonal layout across ranks: the decision for sweep s-1 after launch s, and the halo of
+// {P, x} plus the incoming messages on the diagonals that cross to a peer
+struct DiaHalo {
+    int nd;                 // diagonals exchanged with this peer
+    int diag[kDiaMaxD];
+};
+cudaError_t launch_dia_finish(const SweepArgs &a, cudaStream_t st);
+cudaError_t launch_dia_pack(const SweepArgs &a, const uint32_t *idx, int64_t cnt, double *buf,
+                            const DiaHalo &h, int64_t s_fix, int post_finish, cudaStream_t st);
+cudaError_t launch_dia_unpack(const SweepArgs &a, const uint32_t *idx, int64_t cnt,
+                              const double *buf, const DiaHalo &h, int64_t s_fix,
+                              int post_finish, cudaStream_t st);
 // pre_finish = 1: called between the sweep launch and its finish_kernel (split sweep)
 cudaError_t launch_halo_pack(const SweepArgs &a, const uint32_t *idx, int64_t cnt, double *buf,
                              cudaStream_t st, int pre_finish);

@@ -152,7 +152,8 @@ def _report(parts, outs, rep, ch, rh, ms):
                        messages_sent=int(rep.messages_sent), device_ms=float(ms),
                        sweeps_launched=int(rep.sweeps_launched),
                        final_rel_residual=float(rep.final_rel_residual),
-                       split_sweeps=int(rep.split_sweeps))
+                       split_sweeps=int(rep.split_sweeps),
+                       dist_layout=int(rep.dist_layout))
 
 
 def solve_partitioned_local(system: SymSystem, nparts: int, options=None, device: int = 0):

@@ -188,6 +188,7 @@ class SolveReport:
     residual_probes: int = 0
     kernel_launches: int = 0
     split_sweeps: int = 0   # multi-rank: sweeps run as boundary part + interior part
+    dist_layout: int = 0    # multi-rank kernel family: 1 slice, 2 tiles, 3 diagonal
 
 
 def initial_state(graph: GaussianGraph, schedule: str = "parallel") -> MessageState:

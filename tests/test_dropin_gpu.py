@@ -231,7 +231,7 @@ def test_probe_and_poll_modes_reproducible():
 @pytest.mark.parametrize("kind,nparts,split", [("poisson3d_32", 8, False),
                                                ("poisson2d_256", 4, True),
                                                ("poisson3d_32", 2, True)])
-def test_partitions_agree_on_the_split(kind, nparts, split):
+def test_partitions_agree_on_the_split(kind, nparts, split, monkeypatch):
     """Poisson 32^3 in 8 row blocks: the end blocks could split their sweep (one boundary
     plane), the middle ones cannot (two planes, 5 of 9 groups) -- every rank must then run
     whole sweeps, or the NCCL call sequences differ.  The solve stays bitwise
@@ -241,9 +241,39 @@ def test_partitions_agree_on_the_split(kind, nparts, split):
     opts = G.SolveOptions(schedule="broadcast", epsilon=1e-300, rel_residual_tol=1e-6,
                           max_iter=3000)
     one = G.solve(s, opts)
+    # the grids would agree on the diagonal layout; this is the slice protocol's test
+    monkeypatch.setenv("GABP_NO_DIST_DIA", "1")
     part = D.solve_partitioned_local(s, nparts, opts)
+    assert part.dist_layout == 1
     assert (part.split_sweeps > 0) == split, part.split_sweeps
     assert part.iterations == one.iterations
     np.testing.assert_array_equal(part.means, one.means)
+    np.testing.assert_array_equal(np.asarray(part.max_change_history),
+                                  np.asarray(one.max_change_history))
+
+
+@pytest.mark.parametrize("kind,nparts", [("poisson3d_32", 8), ("poisson2d_256", 3),
+                                         ("stencil_random", 4)])
+def test_partitions_on_the_diagonal_layout(kind, nparts):
+    """Row blocks of stencil graphs agree on the diagonal layout (dist_layout 3): halo =
+    {P, x} and the incoming messages on the diagonals that cross the cut; bitwise the
+    single-partition solve, including unequal blocks (256 rows in 3) and a stencil with
+    random coefficients."""
+    from tests.test_dia_gpu import _random_stencil
+    if kind == "poisson3d_32":
+        s = G.gen_poisson3d(32, 1).system
+    elif kind == "poisson2d_256":
+        s = G.gen_poisson2d(256, 1).system
+    else:  # random coefficients (no edge dropped: the host partitioner's halo is then the
+        # whole neighbour row, so local ids keep the diagonal offsets)
+        s = _random_stencil(64, 2, 3, drop=0.0)
+    opts = G.SolveOptions(schedule="broadcast", epsilon=1e-300, rel_residual_tol=1e-7,
+                          max_iter=4000)
+    one = G.solve(s, opts)
+    part = D.solve_partitioned_local(s, nparts, opts)
+    assert part.dist_layout == 3
+    assert part.iterations == one.iterations and part.converged == one.converged
+    np.testing.assert_array_equal(part.means, one.means)
+    np.testing.assert_array_equal(part.precisions, one.precisions)
     np.testing.assert_array_equal(np.asarray(part.max_change_history),
                                   np.asarray(one.max_change_history))

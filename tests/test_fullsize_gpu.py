@@ -84,14 +84,23 @@ def test_config2_4096_200_sweeps_vs_oracle(grid4096, sched):
         assert g.info.dia_diagonals == 4  # (auto ran the diagonal layout)
 
 
+@pytest.mark.parametrize("layout", ["diagonal", "slice"])
 @pytest.mark.parametrize("nparts", [2, 4, 8])
-def test_config2_4096_strips_bitwise_one_partition(grid4096, nparts):
+def test_config2_4096_strips_bitwise_one_partition(grid4096, nparts, layout, monkeypatch):
+    """diagonal: the ranks' stencil layout (message + node-state halo per cut edge);
+    slice: the slice layout with the split sweep (boundary rows first, the exchange under
+    the interior rows)."""
     spec, g, _ = grid4096
+    if layout == "slice":
+        monkeypatch.setenv("GABP_NO_DIST_DIA", "1")
     opts = G.SolveOptions(schedule="broadcast", epsilon=1e-300, max_iter=120,
                           record_means_history=False)
     one = G.solve_graph(g, opts)
     part = D.solve_grid_partitioned_local(spec, nparts, opts)
-    assert part.split_sweeps > 0  # boundary rows first, exchange under the interior
+    if layout == "slice":
+        assert part.dist_layout == 1 and part.split_sweeps > 0
+    else:
+        assert part.dist_layout == 3
     _same(part, one)
 
 
@@ -135,9 +144,15 @@ def cube400():
     return spec, opts, one
 
 
+@pytest.mark.parametrize("layout", ["diagonal", "slice"])
 @pytest.mark.parametrize("nparts", [2, 4, 8])
-def test_config4_400_cube_slabs_bitwise_one_partition(cube400, nparts):
+def test_config4_400_cube_slabs_bitwise_one_partition(cube400, nparts, layout, monkeypatch):
     spec, opts, one = cube400
+    if layout == "slice":
+        monkeypatch.setenv("GABP_NO_DIST_DIA", "1")
     part = D.solve_grid_partitioned_local(spec, nparts, opts)
-    assert part.split_sweeps > 0
+    if layout == "slice":
+        assert part.dist_layout == 1 and part.split_sweeps > 0
+    else:
+        assert part.dist_layout == 3
     _same(part, one)
