@@ -1831,13 +1831,15 @@ int gabp_infer_marginals(const gabp_graph_t *G, const gabp_state_t *S, double *h
 // ---- solve --------------------------------------------------------------------------------
 
 // Marginals of the last solve in row order: the slice path keeps them in position order,
-// in the node state records {P_i, P_i mu~_i, x_i, -}.
+// in the node state records {P_i, x_i}.
 static int rows_order(gabp_graph *G, int64_t slot, int64_t r0, int64_t nr, const double **xm,
                       const double **pm) {
     if (!G->slice_order) return GABP_OK;
     const double *rec = reinterpret_cast<const double *>(G->rec[slot]);
-    CK(gabp::slice_to_rows(G->g, r0, nr, rec + 2, 4, G->xs, G->stream));
-    CK(gabp::slice_to_rows(G->g, r0, nr, rec, 4, G->ps, G->stream));
+    constexpr int kRecStride = (int)(sizeof(gabp::NodeState) / sizeof(double));
+    CK(gabp::slice_to_rows(G->g, r0, nr, rec + offsetof(gabp::NodeState, x) / sizeof(double),
+                           kRecStride, G->xs, G->stream));
+    CK(gabp::slice_to_rows(G->g, r0, nr, rec, kRecStride, G->ps, G->stream));
     *xm = G->xs;
     *pm = G->ps;
     return GABP_OK;

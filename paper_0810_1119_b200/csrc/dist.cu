@@ -49,7 +49,7 @@ __global__ void halo_pack_kernel(const SweepArgs a, const uint32_t *idx, int64_t
         const uint32_t i = idx[k];
         if (a.slice_path) {
             const NodeState r = a.rec[(s - 1) % 3][i];
-            b4[k] = make_double4(r.P, r.N, r.x, 0.0);
+            b4[k] = make_double4(r.P, r.P * r.x, r.x, 0.0);
         } else {
             const double2 g = a.agg[(s - 1) % 3][i];
             b4[k] = make_double4(g.x, g.y, a.x[(s - 1) % 3][i], 0.0);
@@ -68,7 +68,6 @@ __global__ void halo_unpack_kernel(const SweepArgs a, const uint32_t *idx, int64
         if (a.slice_path) {
             NodeState &r = a.rec[(s - 1) % 3][i];
             r.P = v.x;
-            r.N = v.y;
             r.x = v.z;
         } else {
             a.agg[(s - 1) % 3][i] = make_double2(v.x, v.y);

@@ -61,14 +61,24 @@ struct __align__(16) EdgeRec {
     double coeff;   // A_ij
 };
 
-// Per-sweep state of a node on the slice path: aggregate {P_i, P_i mu~_i} of S_t and the
-// marginal x_i^{(t)} -- one 32-byte sector, gathered with one 256-bit load.
+// Per-sweep state of a node on the slice path: the aggregate precision P_i of S_t and the
+// marginal x_i^{(t)} = mu~_i.  The aggregate numerator the messages use is the reference's
+// rounded product (sum_p * mu_tilde) (solver.py:254): one multiplication of the two stored
+// values, formed where it is used.  One node per 32-byte sector (one 256-bit gather).
+// GABP_NODE16 packs two nodes per sector: measured on config 1 it halves the gather working
+// set (L2 gather misses 10.4 M -> 2.5 M sectors, DRAM 2.23 -> 2.05 GB per launch) and is
+// still 4 % slower (0.381 vs 0.365 ms/sweep; profiles/r02_evidence.md), so it stays a probe.
+#ifdef GABP_NODE16
+struct __align__(16) NodeState {
+    double P, x;
+};
+#else
 struct __align__(32) NodeState {
     double P;   // P_i = A_ii + sum_k P_ki
-    double N;   // P_i * mu~_i
-    double x;   // x_i = N_i / P_i (the marginal mean)
-    double pad;
+    double x;   // x_i = N_i / P_i (the marginal mean, mu~_i of the next sweep)
+    double pad[2];
 };
+#endif
 
 struct __align__(16) NodeRec {
     double diag;    // A_ii

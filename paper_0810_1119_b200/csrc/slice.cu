@@ -77,16 +77,27 @@ __device__ __forceinline__ uint32_t twin_edge(const SweepArgs &a, int64_t p, uin
     return a.er[a.row_ptr[a.srow[p]] + q].rev;
 }
 
-__device__ __forceinline__ void ld_node(const NodeState *g, double &P, double &N, double &x) {
-    double pad;
+// (the numerator (sum_p * mu_tilde), solver.py:254, is formed where it is used -- P * x at
+// the load would make the lane wait for the gather it has just issued)
+__device__ __forceinline__ void ld_node(const NodeState *g, double &P, double &x) {
+#ifdef GABP_NODE16
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(P), "=d"(x) : "l"(g));
+#else
+    double p0, p1;  // (the whole sector: one 256-bit load)
     asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
-                 : "=d"(P), "=d"(N), "=d"(x), "=d"(pad) : "l"(g));
+                 : "=d"(P), "=d"(x), "=d"(p0), "=d"(p1) : "l"(g));
+#endif
 }
 // L2 policies of the node-state traffic (GABP_GATHER_POLICY): the gathered states S_{s-2}
 // are a random-access working set of 32 B x nodes that the message streams (evict-first)
 // must not push out of L2; the written states S_{s-1} are next launch's gather set.
+// Measured on config 1 (tools/gpu/lib_ab.sh, profiles/r02_evidence.md): 0 = no hints 0.365
+// ms/sweep; 1 = gathered and written states evict-last, the own S_{s-3} read evict-first
+// 0.362; 2 = also the once-per-launch row header (prior, degree, b_i) without L1 allocation
+// and evict-first 0.360 (the L1 holds the in-flight gathers: a 5-stage ring, which leaves
+// 28 KB of L1, runs 0.448).
 #ifndef GABP_GATHER_POLICY
-#define GABP_GATHER_POLICY 0
+#define GABP_GATHER_POLICY 2
 #endif
 __device__ __forceinline__ uint64_t pol_evict_last_node() {
     uint64_t p;
@@ -98,16 +109,25 @@ __device__ __forceinline__ uint64_t pol_evict_first_node() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ void ld_node_pol(const NodeState *g, double &P, double &N, double &x,
+__device__ __forceinline__ void ld_node_pol(const NodeState *g, double &P, double &x,
                                             uint64_t pol) {
-    double pad;
+#ifdef GABP_NODE16
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(P), "=d"(x) : "l"(g), "l"(pol));
+#else
+    double p0, p1;
     asm volatile("ld.global.cg.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=d"(P), "=d"(N), "=d"(x), "=d"(pad) : "l"(g), "l"(pol));
+                 : "=d"(P), "=d"(x), "=d"(p0), "=d"(p1) : "l"(g), "l"(pol));
+#endif
 }
-__device__ __forceinline__ void st_node_pol(NodeState *g, double P, double N, double x,
-                                            uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(g),
-                 "d"(P), "d"(N), "d"(x), "d"(0.0), "l"(pol) : "memory");
+__device__ __forceinline__ void st_node_pol(NodeState *g, double P, double x, uint64_t pol) {
+#ifdef GABP_NODE16
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(g), "d"(P), "d"(x),
+                 "l"(pol) : "memory");
+#else
+    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %3}, %4;" ::"l"(g), "d"(P),
+                 "d"(x), "d"(0.0), "l"(pol) : "memory");
+#endif
 }
 __device__ __forceinline__ double2 ld_f64x2_pol(const double2 *p, uint64_t pol) {
     double2 v;
@@ -115,9 +135,13 @@ __device__ __forceinline__ double2 ld_f64x2_pol(const double2 *p, uint64_t pol) 
                  : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
     return v;
 }
-__device__ __forceinline__ void st_node(NodeState *g, double P, double N, double x) {
-    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(g), "d"(P), "d"(N), "d"(x),
-                 "d"(0.0) : "memory");
+__device__ __forceinline__ void st_node(NodeState *g, double P, double x) {
+#ifdef GABP_NODE16
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(g), "d"(P), "d"(x) : "memory");
+#else  // (whole sectors: a partial-sector store costs a fill)
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %3};" ::"l"(g), "d"(P), "d"(x), "d"(0.0)
+                 : "memory");
+#endif
 }
 
 // Statistics of sweep s-1 on its message j -> i = (ip, im) against S_{s-2}'s (i2).
@@ -144,9 +168,9 @@ __device__ __forceinline__ double node_done(Stats &st, const SweepArgs &a, NodeS
     if (EXACT && sp == 0.0)  // (fast launch: N / 0 fails the deferred range test)
         st.agg_sing = min(st.agg_sing, __ldg(a.srow + p));
 #if GABP_GATHER_POLICY >= 1
-    st_node_pol(rec1 + p, sp, sp * xi, xi, pol_evict_last_node());  // (sum_p * mu_tilde)
+    st_node_pol(rec1 + p, sp, xi, pol_evict_last_node());
 #else
-    st_node(rec1 + p, sp, sp * xi, xi);  // (sum_p * mu_tilde)
+    st_node(rec1 + p, sp, xi);
 #endif
     if (PH == 3) {
         const double r = y - rhs_i;
@@ -235,7 +259,8 @@ __device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, S
         double2 a3 = make_double2(0.0, 0.0);
         double y = 0.0, rhs_i = 0.0;
         if (PH == 3) {
-            a3 = __ldcg(reinterpret_cast<const double2 *>(r.g3 + p));
+            a3 = __ldcg(reinterpret_cast<const double2 *>(r.g3 + p));  // {P_i, x_i}
+            a3.y = a3.x * a3.y;  // (sum_p * mu_tilde), solver.py:254
             y = nd.x * __ldcg(&r.g2[p].x);
             rhs_i = __ldg(a.srhs + p);
         }
@@ -250,9 +275,9 @@ __device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, S
             double2 i2[kUL], i3[kUL];
 #pragma unroll
             for (int u = 0; u < kUL; ++u) col[u] = coln[u];
-            double gP[kUL], gN[kUL], gx[kUL];
+            double gP[kUL], gx[kUL];
 #pragma unroll
-            for (int u = 0; u < kUL; ++u) ld_node(r.g2 + col[u], gP[u], gN[u], gx[u]);
+            for (int u = 0; u < kUL; ++u) ld_node(r.g2 + col[u], gP[u], gx[u]);
 #pragma unroll
             for (int u = 0; u < kUL; ++u) {
                 const uint32_t slot = base + (uint32_t)kStride * (q0 + u);
@@ -284,7 +309,7 @@ __device__ __forceinline__ void slice_sweep_ldg(const SweepArgs &a, int64_t s, S
             for (int u = 0; u < kUL; ++u) {  // incoming of S_{s-1}
                 const bool v = q0 + u < d;
                 pe[u] = v ? gP[u] - m2p[u] : 1.0;
-                const double num = v ? gN[u] - m2p[u] * m2m[u] : 1.0;
+                const double num = v ? gP[u] * gx[u] - m2p[u] * m2m[u] : 1.0;  // (sum_p * mu_tilde)
                 edge_msg<EXACT>(c[u], rc[u], pe[u], num, ip[u], im[u], st);
             }
 #pragma unroll
@@ -492,7 +517,8 @@ __device__ __forceinline__ void slice_sweep_pipe(const SweepArgs &a, int64_t s, 
             sp = nd.x;
             sn = nd.y;
             if (PH == 3) {
-                a3 = S.a3[lane];
+                a3 = S.a3[lane];  // {P_i, x_i}
+                a3.y = a3.x * a3.y;
                 y = nd.x * S.xo[lane];
                 rhs_i = S.rhs[lane];
             }
@@ -515,9 +541,9 @@ __device__ __forceinline__ void slice_sweep_pipe(const SweepArgs &a, int64_t s, 
 #pragma unroll
         for (int u = 0; u < kUP; ++u) {  // incoming of S_{s-1}
             const bool v = C.b * kUP + u < d;
-            const double2 ag = S.ag[u][lane];
+            const double2 ag = S.ag[u][lane];  // {P_j, x_j}
             pe[u] = v ? ag.x - m2p[u] : 1.0;
-            const double num = v ? ag.y - m2p[u] * m2m[u] : 1.0;
+            const double num = v ? ag.x * ag.y - m2p[u] * m2m[u] : 1.0;
             edge_msg<EXACT>(c[u], rc[u], pe[u], num, ip[u], im[u], st);
         }
         const int64_t p = C.sl * 32 + lane;
@@ -576,7 +602,7 @@ struct __align__(16) GMeta {
     uint32_t gbase;       // first slot of the group
     uint32_t pad[3];
 };
-constexpr int kGResSlots = 8;  // groups a CTA's consumers can be apart (< kGS + 2)
+constexpr int kGResSlots = kGS + 4;  // groups a CTA's consumers can be apart (< kGS + 2)
 static_assert(kGResSlots >= kGS + 2, "residual slots must outlast the ring's lag");
 struct __align__(128) GRing {
     GStage st[kGS];
@@ -790,7 +816,7 @@ __device__ __forceinline__ void grp_produce(const SweepArgs &a, GRing &G, uint32
 // one chunk ahead of use like the gathers.
 struct THdr {
     double2 nd;   // {A_ii, prior numerator}
-    double2 a3;   // {P_i, N_i} of S_{s-3}
+    double2 a3;   // {P_i, x_i} of S_{s-3}
     double xo;    // x_i^{(s-2)}
     double rhs;
     uint32_t d;
@@ -798,8 +824,15 @@ struct THdr {
 template <int PH, int R>
 __device__ __forceinline__ void t_header(const SweepArgs &a, const Ring<R> &r, int64_t p,
                                          THdr &h) {
+#if GABP_GATHER_POLICY >= 2  // read once per launch: no L1 allocation, demoted in L2
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(h.nd.x), "=d"(h.nd.y) : "l"(a.snd + p), "l"(pol_evict_first_node()));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(h.d) : "l"(a.sdeg + p), "l"(pol_evict_first_node()));
+#else
     h.nd = __ldg(a.snd + p);
     h.d = __ldg(a.sdeg + p);
+#endif
     if (PH == 3 || PH == 4) {
 #if GABP_GATHER_POLICY >= 1
         // S_{s-3}: last use of the state (demoted); S_{s-2}: still gathered this launch
@@ -808,26 +841,29 @@ __device__ __forceinline__ void t_header(const SweepArgs &a, const Ring<R> &r, i
         h.a3 = __ldcg(reinterpret_cast<const double2 *>(r.g3 + p));
 #endif
         h.xo = __ldcg(&r.g2[p].x);
+#if GABP_GATHER_POLICY >= 2
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                     : "=d"(h.rhs) : "l"(a.srhs + p), "l"(pol_evict_first_node()));
+#else
         h.rhs = __ldg(a.srhs + p);
+#endif
     }
 }
 
 // neighbour gathers of a landed chunk (node states of S_{s-2}), one chunk ahead of use
 template <int PH, int CW = stage_cw<PH>()>
 __device__ __forceinline__ void t_gather(const GStage &S, const GMeta &m, const NodeState *g2,
-                                         int t, double (&gP)[CW], double (&gN)[CW],
-                                         double (&gx)[CW]) {
+                                         int t, double (&gP)[CW], double (&gx)[CW]) {
 #pragma unroll
     for (int u = 0; u < CW; ++u) {
         if (m.b * CW + u < m.w) {
 #if GABP_GATHER_POLICY >= 1
-            ld_node_pol(g2 + st_col<PH>(S, u)[t], gP[u], gN[u], gx[u], pol_evict_last_node());
+            ld_node_pol(g2 + st_col<PH>(S, u)[t], gP[u], gx[u], pol_evict_last_node());
 #else
-            ld_node(g2 + st_col<PH>(S, u)[t], gP[u], gN[u], gx[u]);
+            ld_node(g2 + st_col<PH>(S, u)[t], gP[u], gx[u]);
 #endif
         } else {
             gP[u] = 1.0;
-            gN[u] = 1.0;
             gx[u] = 0.0;
         }
     }
@@ -864,23 +900,22 @@ struct GRow {
 };
 
 // Chunk k of a consumer warp: waits for chunk k+1 and issues its header and gathers into
-// (nP, nN, nx), then computes chunk k from its stage and the gathers (gP, gN, gx).  Returns
+// (nP, nx), then computes chunk k from its stage and the gathers (gP, gx).  Returns
 // false after the last chunk; otherwise m becomes chunk k+1's descriptor.  The loop calls
 // it with the two gather buffers swapped on alternate chunks (no register copies).
 template <int PH, int R, int CW = stage_cw<PH>()>
 __device__ __forceinline__ bool grp_step(const SweepArgs &a, const Ring<R> &r, double *xh,
                                          Stats &st, GRing &G, int lane, int warp, int t,
                                          uint32_t k, GMeta &m, THdr &hn, GRow &row,
-                                         const double (&gP)[CW], const double (&gN)[CW],
-                                         const double (&gx)[CW], double (&nP)[CW],
-                                         double (&nN)[CW], double (&nx)[CW]) {
+                                         const double (&gP)[CW], const double (&gx)[CW],
+                                         double (&nP)[CW], double (&nx)[CW]) {
     if (m.b == 0) {  // row header (loaded one chunk ago)
         row.d = hn.d;
         row.diag = hn.nd.x;
         row.sp = hn.nd.x;
         row.sn = hn.nd.y;
         if (PH == 3 || PH == 4) {
-            row.a3 = hn.a3;
+            row.a3 = make_double2(hn.a3.x, hn.a3.x * hn.a3.y);  // {P_i, (sum_p * mu_tilde)}
             row.y = hn.nd.x * hn.xo;
             row.rhs_i = hn.rhs;
         }
@@ -891,7 +926,7 @@ __device__ __forceinline__ bool grp_step(const SweepArgs &a, const Ring<R> &r, d
     const GMeta mn = G.meta[s1];
     if (mn.g >= 0) {
         if (mn.b == 0) t_header<PH, R>(a, r, ((int64_t)mn.g * kGroup + warp) * 32 + lane, hn);
-        t_gather<PH>(G.st[s1], mn, r.g2, t, nP, nN, nx);
+        t_gather<PH>(G.st[s1], mn, r.g2, t, nP, nx);
     }
     const int s0 = (int)(k % kGS);
     const GStage &S = G.st[s0];
@@ -915,16 +950,18 @@ __device__ __forceinline__ bool grp_step(const SweepArgs &a, const Ring<R> &r, d
             edge_msg<false>(cc[u], rc[u], pe2, nu2, m2p[u], m2m[u], st);
         }
     }
+#ifndef GABP_LATE_RELEASE
     uint32_t tok = 0u;
 #pragma unroll
     for (int u = 0; u < CW; ++u) tok = hold(tok, i2v[u]);  // (used after the release)
     tok = __reduce_or_sync(~0u, tok);  // every lane's loads landed
     if (lane == 0) t_arrive_after(&G.empty[s0], tok);  // the stage's data is in registers now
+#endif
 #pragma unroll
     for (int u = 0; u < CW; ++u) {  // incoming of S_{s-1}
         const bool v = m.b * CW + u < d;
         pe[u] = v ? gP[u] - m2p[u] : 1.0;
-        const double num = v ? gN[u] - m2p[u] * m2m[u] : 1.0;
+        const double num = v ? gP[u] * gx[u] - m2p[u] * m2m[u] : 1.0;  // (sum_p * mu_tilde)
         edge_msg<false>(cc[u], rc[u], pe[u], num, ip[u], im[u], st);
     }
     const int64_t p = ((int64_t)m.g * kGroup + warp) * 32 + lane;
@@ -939,6 +976,15 @@ __device__ __forceinline__ bool grp_step(const SweepArgs &a, const Ring<R> &r, d
             msg_stats<false>(st, a, ip[u], im[u], i2v[u], pe[u], p, q);
         }
     }
+#ifdef GABP_LATE_RELEASE
+    {  // release after the last use of the stage (no operand outlives it in registers)
+        uint32_t tok = 0u;
+#pragma unroll
+        for (int u = 0; u < CW; ++u) tok = hold(tok, i2v[u]);
+        tok = __reduce_or_sync(~0u, tok);
+        if (lane == 0) t_arrive_after(&G.empty[s0], tok);
+    }
+#endif
 #if defined(GABP_R1_GRP) || defined(GABP_R1_ROWDONE)
     if (m.b + 1 == m.nb && row.diag != 0.0)  // row done (A_ii == 0: padding lane)
         node_done<(PH == 4 ? 3 : PH), false>(st, a, r.g1, xh, p, row.sp, row.sn, row.y, row.rhs_i);
@@ -969,17 +1015,17 @@ __device__ __forceinline__ void grp_consume(const SweepArgs &a, int64_t s, Stats
     GMeta m = G.meta[0];
     if (m.g < 0) return;
     constexpr int CW = stage_cw<PH>();
-    double gA[3][CW], gB[3][CW];  // gathers {P, N, x}: chunk k in one, k+1 in the other
+    double gA[2][CW], gB[2][CW];  // gathers {P, x}: chunk k in one, k+1 in the other
     THdr hn;
     t_header<PH, R>(a, r, ((int64_t)m.g * kGroup + warp) * 32 + lane, hn);
-    t_gather<PH>(G.st[0], m, r.g2, t, gA[0], gA[1], gA[2]);
+    t_gather<PH>(G.st[0], m, r.g2, t, gA[0], gA[1]);
     GRow row;
     for (uint32_t k = 0;; k += 2) {
-        if (!grp_step<PH, R>(a, r, xh, st, G, lane, warp, t, k, m, hn, row, gA[0], gA[1], gA[2],
-                             gB[0], gB[1], gB[2]))
+        if (!grp_step<PH, R>(a, r, xh, st, G, lane, warp, t, k, m, hn, row, gA[0], gA[1], gB[0],
+                             gB[1]))
             break;
         if (!grp_step<PH, R>(a, r, xh, st, G, lane, warp, t, k + 1, m, hn, row, gB[0], gB[1],
-                             gB[2], gA[0], gA[1], gA[2]))
+                             gA[0], gA[1]))
             break;
     }
 }
@@ -1601,7 +1647,7 @@ __device__ __forceinline__ void par_consume(const SweepArgs &a, int64_t s, Stats
                     const double xi = qdiv<EXACT>(row.sn, row.sp, st);
                     if (!(fabs(xi) <= DBL_MAX)) st.means_bad = 1u;
                     if (xh) xh[__ldg(a.srow + p)] = xi;
-                    st_node(g1 + p, row.sp, row.sp * xi, xi);
+                    st_node(g1 + p, row.sp, xi);
                     if (RESID) {
                         const double r = row.y - row.rhs_i;
                         rr = r * r;
