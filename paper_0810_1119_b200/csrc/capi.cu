@@ -156,6 +156,8 @@ struct gabp_graph {
     uint64_t serial_gen = 0;               // workspace generation of the capture
     double serial_lim = 0.0;               // blow-up limit of the capture
     std::vector<uint32_t> h_rp, h_col;     // host CSR (level build)
+    int small_state = 0;                   // small.cu plan: 0 not tried, 1 fits, -1 does not
+    gabp::SmallPart small_part = {};
 };
 
 struct gabp_state {
@@ -651,6 +653,23 @@ struct Poller {
     }
 };
 
+// Plans the one-launch cluster solve of a small graph once per graph (small.cu): the row
+// offsets come to the host (<= 64 KB) and the cluster's row blocks are cut there.
+bool small_graph(gabp_graph *G) {
+    if (G->small_state == 0) {
+        G->small_state = -1;
+        if (gabp::small_candidate(G->g.n, G->g.E)) {
+            std::vector<uint32_t> rp((size_t)G->g.n + 1);
+            if (cudaMemcpyAsync(rp.data(), G->g.row_ptr, sizeof(uint32_t) * rp.size(),
+                                cudaMemcpyDeviceToHost, G->stream) == cudaSuccess &&
+                cudaStreamSynchronize(G->stream) == cudaSuccess &&
+                gabp::small_plan(G->g.n, rp.data(), &G->small_part))
+                G->small_state = 1;
+        }
+    }
+    return G->small_state > 0;
+}
+
 int finish_loop(gabp_graph *G, double *device_ms) {
     cudaStream_t st = G->stream;
     CK(cudaEventRecord(G->ev[3], st));
@@ -1023,15 +1042,16 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         return finish_loop(G, device_ms);
     }
     if (sched == GABP_SCHED_BROADCAST && opt->gather_mode == GABP_GATHER_AUTO &&
-        G->g.row_lo == 0 && G->g.row_hi == G->g.n && gabp::small_fits(G->g.n, G->g.E) &&
+        G->g.row_lo == 0 && G->g.row_hi == G->g.n && small_graph(G) &&
         !getenv("GABP_NO_SMALL")) {
-        // small graph: the whole solve loop in one persistent CTA (small.cu) -- sweeps of a
-        // few thousand edges are bound by launch and decision latency, not by HBM
+        // small graph: the whole solve loop in one launch of one thread-block cluster
+        // (small.cu) -- sweeps of a few thousand edges are bound by launch and decision
+        // latency, not by HBM
         SweepArgs a = make_args(G);
         G->slice_order = false;
         G->kernels_launched = 1;
         CK(cudaEventRecord(G->ev[2], st));
-        CK(gabp::launch_small_solve(a, G->g.E, st));
+        CK(gabp::launch_small_solve(a, G->small_part, st));
         return finish_loop(G, device_ms);
     }
     if (sched == GABP_SCHED_BROADCAST && opt->gather_mode == GABP_GATHER_AUTO &&

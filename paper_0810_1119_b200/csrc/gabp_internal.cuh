@@ -371,10 +371,17 @@ cudaError_t launch_dia_sweep(const SweepArgs &a, cudaStream_t st);
 // arrays (every staged range in bounds)
 int64_t dia_pad(int64_t max_off);
 
-// the whole broadcast solve of a small graph in one persistent CTA (small.cu): messages
-// and node states in shared memory, 32 B x (n + E)
-bool small_fits(int64_t n, int64_t E);
-cudaError_t launch_small_solve(const SweepArgs &a, int64_t E, cudaStream_t st);
+// the whole broadcast solve of a small graph in one launch of one thread-block cluster
+// (small.cu): messages and node states in the distributed shared memory of <= 8 CTAs
+constexpr int kSmallMaxCluster = 8;
+struct SmallPart {
+    int C;                              // CTAs in the cluster
+    int cfg;                            // thread configuration (small.cu: kSmallCfg)
+    uint32_t nb[kSmallMaxCluster + 1];  // CTA c owns rows [nb[c], nb[c+1])
+};
+bool small_candidate(int64_t n, int64_t E);  // sizes a cluster could hold at all
+bool small_plan(int64_t n, const uint32_t *row_ptr, SmallPart *out);
+cudaError_t launch_small_solve(const SweepArgs &a, const SmallPart &p, cudaStream_t st);
 
 // multi-rank helpers (dist.cu)
 cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st);
