@@ -298,7 +298,7 @@ def configs_block(dev: int, peak: float) -> dict:
         "workload": "poisson2d-32", "n": g0.n, "directed_edges": g0.num_edges,
         "sweeps_to_1e-8": it, "time_to_1e-8_ms": best, "us_per_sweep": 1e3 * best / it,
         "edge_updates_per_s": it * g0.num_edges / (best / 1e3),
-        "bound": "latency (4 k edges: the graph lives in L2)"}
+        "bound": "latency (one launch of an 8-CTA cluster, every operand in distributed shared memory)"}
     g0.close()
     # config 2: 4096^2 grid, generated on the device
     g2 = GR.GridGraph(GR.GridSpec(2, 4096, 0), dev)

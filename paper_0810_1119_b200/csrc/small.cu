@@ -34,6 +34,7 @@
 // its own slow path when the range test fails).
 #include <float.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "sweep_common.cuh"
 
@@ -443,6 +444,10 @@ bool small_plan(int64_t n, const uint32_t *row_ptr, SmallPart *out) {
     // (powers of two: 1, 2, 4, 8)
     int Cp = 1;
     while (Cp < C && Cp < kSmallMaxCluster) Cp *= 2;
+    if (const char *f = getenv("GABP_SMALL_C")) {  // probe: force the first cluster size tried
+        const int v = atoi(f);
+        if (v == 1 || v == 2 || v == 4 || v == 8) Cp = v;
+    }
     for (int C2 = Cp; C2 <= kSmallMaxCluster; C2 *= 2) {
         SmallPart p = {};
         p.C = C2;

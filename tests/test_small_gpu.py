@@ -1,4 +1,5 @@
-"""Small graphs: the whole broadcast solve in one persistent CTA (csrc/small.cu) --
+"""Small graphs: the whole broadcast solve in one launch of one thread-block cluster
+(csrc/small.cu: row blocks over <= 8 CTAs, distributed shared memory) --
 BASELINE config 0, the reference's own case (Poisson 32x32 to ||Ax-b||/||b|| < 1e-8,
 1731 sweeps), bitwise against the C oracle and against the sweep-per-launch slice loop.
 The golden fixtures run through it in tests/test_gpu_parity.py (gather mode auto)."""
@@ -65,7 +66,7 @@ def test_config0_rel_residual_reached_and_fast():
     assert r.device_ms / r.iterations < 10e-3, r.device_ms
 
 
-@pytest.mark.parametrize("n,k", [(700, 3), (1500, 1), (64, 20)])
+@pytest.mark.parametrize("n,k", [(700, 3), (1500, 1), (64, 20), (3000, 2), (6000, 1)])
 def test_random_small_graphs_match_oracle(n, k):
     s = G.gen_random_sparse(n, k, 11).system
     og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
@@ -76,3 +77,38 @@ def test_random_small_graphs_match_oracle(n, k):
     assert r.iterations == o.iterations
     np.testing.assert_array_equal(_bits(r.means), _bits(o.means))
     np.testing.assert_array_equal(np.asarray(r.max_change_history), o.max_change_history)
+
+
+def test_cluster_divergence_matches_oracle():
+    """A dense CDMA system of 96 users (9120 directed edges over 8 CTAs): GaBP blows up on
+    it; the divergent trajectory, its stop sweep and flags are the oracle's."""
+    s = G.gen_cdma_detection(192, 96, 0.5, 3)[0].system
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    kw = dict(epsilon=1e-12, max_iter=400)
+    o = oracle.solve(og, schedule="broadcast", **kw)
+    r = G.solve(s, G.SolveOptions(schedule="broadcast", **kw))
+    assert r.kernel_launches == 1
+    assert (r.iterations, r.converged, r.diverged) == (o.iterations, o.converged, o.diverged)
+    np.testing.assert_array_equal(_bits(r.means), _bits(o.means))
+    np.testing.assert_array_equal(_bits(np.asarray(r.max_change_history)),
+                                  _bits(o.max_change_history))
+
+
+def test_hub_row_larger_than_a_cta_takes_the_launch_per_sweep_path():
+    """A star with a hub of 2500 edges: no CTA of the cluster can hold the hub's row, so the
+    solve runs one launch per sweep -- same results as the oracle."""
+    n = 2501
+    pi = np.zeros(n - 1, dtype=np.int64)
+    pj = np.arange(1, n, dtype=np.int64)
+    rng = np.random.default_rng(5)
+    pv = rng.uniform(-1.0, 1.0, n - 1)
+    diag = np.full(n, 2.0)
+    diag[0] = 1.1 * np.abs(pv).sum()
+    s = G.SymSystem.from_pairs(diag, pi, pj, pv, rng.standard_normal(n))
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    kw = dict(epsilon=1e-10, max_iter=200)
+    o = oracle.solve(og, schedule="broadcast", **kw)
+    r = G.solve(s, G.SolveOptions(schedule="broadcast", **kw))
+    assert r.kernel_launches > 1
+    assert r.iterations == o.iterations
+    np.testing.assert_array_equal(_bits(r.means), _bits(o.means))
