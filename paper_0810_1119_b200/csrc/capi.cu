@@ -1041,7 +1041,8 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         }
         return finish_loop(G, device_ms);
     }
-    if (sched == GABP_SCHED_BROADCAST && opt->gather_mode == GABP_GATHER_AUTO &&
+    if ((sched == GABP_SCHED_BROADCAST || sched == GABP_SCHED_PARALLEL) &&
+        opt->gather_mode == GABP_GATHER_AUTO && !G->dist &&
         G->g.row_lo == 0 && G->g.row_hi == G->g.n && small_graph(G) &&
         !getenv("GABP_NO_SMALL")) {
         // small graph: the whole solve loop in one launch of one thread-block cluster
@@ -1051,7 +1052,7 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         G->slice_order = false;
         G->kernels_launched = 1;
         CK(cudaEventRecord(G->ev[2], st));
-        CK(gabp::launch_small_solve(a, G->small_part, st));
+        CK(gabp::launch_small_solve(a, G->small_part, sched == GABP_SCHED_PARALLEL, st));
         return finish_loop(G, device_ms);
     }
     if (sched == GABP_SCHED_BROADCAST && opt->gather_mode == GABP_GATHER_AUTO &&

@@ -381,7 +381,8 @@ struct SmallPart {
 };
 bool small_candidate(int64_t n, int64_t E);  // sizes a cluster could hold at all
 bool small_plan(int64_t n, const uint32_t *row_ptr, SmallPart *out);
-cudaError_t launch_small_solve(const SweepArgs &a, const SmallPart &p, cudaStream_t st);
+cudaError_t launch_small_solve(const SweepArgs &a, const SmallPart &p, bool parallel,
+                               cudaStream_t st);
 
 // multi-rank helpers (dist.cu)
 cudaError_t launch_finish(const SweepArgs &a, cudaStream_t st);

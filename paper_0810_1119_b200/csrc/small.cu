@@ -100,7 +100,11 @@ __device__ __forceinline__ uint32_t owner_of(const uint32_t *b, int C, uint32_t 
 }
 
 // NT compute threads + one decision warp; EPT edge slots and NPT rows per compute thread
-template <int NT, int EPT, int NPT>
+// PAR: the parallel schedule (solver.py:146-173) -- B(u) forms every outgoing message from
+// the exclusion sum over its row's incoming slots (ascending, own slot skipped) instead of
+// aggregate minus twin; the node phase, statistics and decisions are the same (no aggregate
+// singular test: _sweep_parallel raises on P_excl only).
+template <int NT, int EPT, int NPT, bool PAR>
 __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs a,
                                                                 const SmallPart part) {
     constexpr int kW = NT / 32;
@@ -114,6 +118,8 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
     double *sA = reinterpret_cast<double *>(sm_raw + (2 * EL + 3 * NL) * sizeof(double2));
     uint32_t *sX = reinterpret_cast<uint32_t *>(sm_raw + (2 * EL + 3 * NL) * sizeof(double2) +
                                                 EL * sizeof(double));
+    double2 *sND = reinterpret_cast<double2 *>(sm_raw + (2 * EL + 3 * NL) * sizeof(double2) +
+                                               EL * (sizeof(double) + sizeof(uint32_t)));  // [NL]
     __shared__ SmRed red[2];
     __shared__ SmCtl ctl;
     __shared__ uint32_t s_nb[kClMax + 1], s_eb[kClMax + 1];
@@ -140,6 +146,7 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
 
     // S_0 = 0, graph records into shared memory and registers
     uint32_t esrc[EPT], etw[EPT];
+    uint32_t ers[EPT], ere[EPT];  // (PAR) the source row's slots
     double emcc[EPT], erc[EPT];
     double2 mold[EPT];
     uint32_t ne0[NPT], ne1[NPT];
@@ -150,6 +157,7 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
             const uint32_t e = tid + k * NT;
             esrc[k] = 0u;
             etw[k] = 0u;
+            ers[k] = ere[k] = 0u;
             emcc[k] = -1.0;
             erc[k] = 1.0;
             mold[k] = make_double2(0.0, 0.0);
@@ -166,6 +174,10 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
                 }
                 const EdgeRec r = a.er[ge];
                 esrc[k] = lo - n0;
+                if (PAR) {
+                    ers[k] = __ldg(a.row_ptr + lo) - e0;
+                    ere[k] = __ldg(a.row_ptr + lo + 1) - e0;
+                }
                 const uint32_t ot = owner_of(s_eb, C, r.rev);
                 etw[k] = cl_map(&sI[0][r.rev - s_eb[ot]], ot);
                 emcc[k] = -r.coeff * r.coeff;  // (-coeff * coeff, solver.py:256)
@@ -187,6 +199,7 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
                 ndg[q] = __ldg(&a.nd[i].diag);
                 npn[q] = __ldg(&a.nd[i].pnum);
                 nrh[q] = __ldg(a.rhs + i);
+                if (PAR) sND[il] = make_double2(ndg[q], npn[q]);
             }
         }
     }
@@ -242,7 +255,7 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
                     DivRange dr;
                     double x = ddiv_fast_acc(N, P, dr);
                     if (!div_range_ok(dr)) x = div_slow(N, P);  // (rare: out of the fast range)
-                    if (P == 0.0) asing = min(asing, n0 + il);
+                    if (!PAR && P == 0.0) asing = min(asing, n0 + il);
                     if (!(fabs(x) <= DBL_MAX)) mbad = 1u;
                     sR[rn][il] = make_double2(P, x);
                     if (xh) xh[n0 + il] = x;
@@ -260,15 +273,35 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
             unsigned fl = 0u, sing = 0xffffffffu;
             DivRange dr;  // fast-path range test of all this thread's divisions, applied once
             double2 mnew[EPT];
+            // P_excl and the numerator of edge slot e = (row i, neighbour j): broadcast --
+            // aggregate minus the twin message m_ji (solver.py:247-254); parallel -- prior
+            // plus the row's incoming terms in ascending order, own slot skipped (:147-150)
+            auto edge_in = [&](int k, uint32_t e, double &pe, double &num) {
+                if (PAR) {
+                    const double2 nd = sND[esrc[k]];
+                    pe = nd.x;
+                    num = nd.y;
+                    for (uint32_t q = ers[k]; q < ere[k]; ++q) {
+                        const double2 v = Io[q];
+                        if (q != e) {
+                            pe = pe + v.x;
+                            num = num + v.x * v.y;  // (prec * mean), solver.py:148
+                        }
+                    }
+                } else {
+                    const double2 ri = Rt[esrc[k]];
+                    const double2 v = Io[e];  // m_ji of S_{u-1}: row i's incoming slot from j
+                    pe = ri.x - v.x;
+                    num = ri.x * ri.y - v.x * v.y;
+                }
+            };
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
                 const uint32_t e = tid + k * NT;
                 mnew[k] = mold[k];
                 if (e < eloc) {
-                    const double2 ri = Rt[esrc[k]];
-                    const double2 v = Io[e];  // m_ji of S_{u-1}: row i's incoming slot from j
-                    const double pe = ri.x - v.x;
-                    const double num = ri.x * ri.y - v.x * v.y;
+                    double pe, num;
+                    edge_in(k, e, pe, num);
                     const double np_ = ddiv_fast_acc(emcc[k], pe, dr);
                     const double nm = ddiv_fast_acc_r(num, sA[e], erc[k], dr);
                     if (pe == 0.0) sing = min(sing, e0 + e);
@@ -281,10 +314,8 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
                 for (int k = 0; k < EPT; ++k) {
                     const uint32_t e = tid + k * NT;
                     if (e < eloc) {
-                        const double2 ri = Rt[esrc[k]];
-                        const double2 v = Io[e];
-                        const double pe = ri.x - v.x;
-                        const double num = ri.x * ri.y - v.x * v.y;
+                        double pe, num;
+                        edge_in(k, e, pe, num);
                         mnew[k] = make_double2(div_slow(emcc[k], pe), div_slow(num, sA[e]));
                     }
                 }
@@ -409,13 +440,13 @@ struct SmallCfg {
 };
 constexpr SmallCfg kSmallCfg[2] = {{256, 2, 1}, {480, 4, 2}};
 
-template <int NT, int EPT, int NPT>
+template <int NT, int EPT, int NPT, bool PAR>
 cudaError_t launch_small_t(const SweepArgs &a, const SmallPart &p, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)p.C);
     cfg.blockDim = dim3(NT + 32);
-    constexpr size_t kSmem = (size_t)NT * (EPT * (2 * 16 + 8 + 4) + NPT * 3 * 16);
-    auto k = small_solve_kernel<NT, EPT, NPT>;
+    constexpr size_t kSmem = (size_t)NT * (EPT * (2 * 16 + 8 + 4) + NPT * 4 * 16);
+    auto k = small_solve_kernel<NT, EPT, NPT, PAR>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kSmem);
     if (e != cudaSuccess) return e;
@@ -487,9 +518,13 @@ bool small_candidate(int64_t n, int64_t E) {
            E <= (int64_t)kSmallMaxCluster * s.nt * s.ept;
 }
 
-cudaError_t launch_small_solve(const SweepArgs &a, const SmallPart &p, cudaStream_t st) {
-    if (p.cfg == 0) return launch_small_t<256, 2, 1>(a, p, st);
-    return launch_small_t<480, 4, 2>(a, p, st);
+cudaError_t launch_small_solve(const SweepArgs &a, const SmallPart &p, bool parallel,
+                               cudaStream_t st) {
+    if (parallel)
+        return p.cfg == 0 ? launch_small_t<256, 2, 1, true>(a, p, st)
+                          : launch_small_t<480, 4, 2, true>(a, p, st);
+    return p.cfg == 0 ? launch_small_t<256, 2, 1, false>(a, p, st)
+                      : launch_small_t<480, 4, 2, false>(a, p, st);
 }
 
 }  // namespace gabp

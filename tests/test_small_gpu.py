@@ -112,3 +112,48 @@ def test_hub_row_larger_than_a_cta_takes_the_launch_per_sweep_path():
     assert r.kernel_launches > 1
     assert r.iterations == o.iterations
     np.testing.assert_array_equal(_bits(r.means), _bits(o.means))
+
+
+@pytest.mark.parametrize("kw", [dict(epsilon=1e-300, rel_residual_tol=1e-8),
+                                dict(epsilon=1e-9), dict(epsilon=1e-300, max_iter=7)])
+def test_config0_parallel_schedule_in_the_cluster(kw):
+    """The reference's default schedule (solver.py:146-173) through the cluster kernel:
+    exclusion sums over the row's local slots, bitwise the oracle."""
+    s = G.gen_poisson2d(32, 0).system
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    o = oracle.solve(og, schedule="parallel", **kw)
+    r = G.solve(s, G.SolveOptions(schedule="parallel", record_means_history=True, **kw))
+    assert r.kernel_launches == 1
+    assert (r.iterations, r.converged, r.diverged) == (o.iterations, o.converged, o.diverged)
+    np.testing.assert_array_equal(_bits(r.means), _bits(o.means))
+    np.testing.assert_array_equal(_bits(r.precisions), _bits(o.precisions))
+    np.testing.assert_array_equal(np.asarray(r.max_change_history), o.max_change_history)
+    np.testing.assert_allclose(r.residual_history, o.residual_history, rtol=1e-9, atol=0)
+    assert len(r.means_history) == r.iterations
+    np.testing.assert_array_equal(_bits(r.means_history[-1]), _bits(r.means))
+
+
+@pytest.mark.parametrize("n,k", [(700, 3), (64, 20), (3000, 2)])
+def test_random_small_graphs_parallel_match_oracle(n, k):
+    s = G.gen_random_sparse(n, k, 12).system
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    kw = dict(epsilon=1e-300, rel_residual_tol=1e-11, max_iter=500)
+    o = oracle.solve(og, schedule="parallel", **kw)
+    r = G.solve(s, G.SolveOptions(schedule="parallel", **kw))
+    assert r.kernel_launches == 1
+    assert r.iterations == o.iterations
+    np.testing.assert_array_equal(_bits(r.means), _bits(o.means))
+    np.testing.assert_array_equal(np.asarray(r.max_change_history), o.max_change_history)
+
+
+def test_cluster_parallel_divergence_matches_oracle():
+    s = G.gen_cdma_detection(192, 96, 0.5, 3)[0].system
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    kw = dict(epsilon=1e-12, max_iter=400)
+    o = oracle.solve(og, schedule="parallel", **kw)
+    r = G.solve(s, G.SolveOptions(schedule="parallel", **kw))
+    assert r.kernel_launches == 1
+    assert (r.iterations, r.converged, r.diverged) == (o.iterations, o.converged, o.diverged)
+    np.testing.assert_array_equal(_bits(r.means), _bits(o.means))
+    np.testing.assert_array_equal(_bits(np.asarray(r.max_change_history)),
+                                  _bits(o.max_change_history))
