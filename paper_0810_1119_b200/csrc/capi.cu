@@ -1076,6 +1076,27 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         }
         return finish_loop(G, device_ms);
     }
+    if (sched == GABP_SCHED_PARALLEL && opt->gather_mode == GABP_GATHER_AUTO &&
+        G->g.dia_D > 0 && G->g.row_lo == 0 && G->g.row_hi == G->g.n &&
+        !getenv("GABP_NO_DIA_PAR")) {
+        // stencil graph, the reference's default schedule: exclusion sums over the row's own
+        // slots, outgoing messages into the neighbours' shifted slots (dia.cu)
+        SweepArgs a = make_args(G);
+        G->slice_order = false;
+        const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
+        const int64_t ptotal = opt->max_iter + 2;
+        G->kernels_launched = 0;
+        CK(cudaEventRecord(G->ev[2], st));
+        while (launched < ptotal) {
+            const int64_t k = ptotal - launched < C ? ptotal - launched : C;
+            for (int64_t q = 0; q < k; ++q) CK(gabp::launch_dia_par_sweep(a, st));
+            G->kernels_launched += k;
+            launched += k;
+            if (P.after_chunk(st, &rc)) break;
+            if (rc) return rc;
+        }
+        return finish_loop(G, device_ms);
+    }
     rc = check_slice(G, opt);
     if (rc) return rc;
     const int gather = pick_gather(G, opt);

@@ -301,6 +301,142 @@ __global__ void __launch_bounds__(kDRows, GABP_DIA_MINB) dia_sweep_kernel(const 
     }
 }
 
+// ---- parallel schedule on the diagonal layout ----------------------------------------------
+// solver.py:146-173: every outgoing message from the exclusion sum over the row's incoming
+// slots (prior first, ascending neighbours, own slot skipped).  A row's incoming slots are
+// its own D slots (coalesced); its outgoing message to j = i + o_k goes into j's slot
+// (opp k, j) -- a shifted, coalesced WRITE of the same array, and the old outgoing message
+// (the change statistic) is the shifted read the broadcast kernel makes for its twin.  So the
+// reference's default schedule streams a stencil graph like the broadcast one: per slot 16 B
+// read + 16 B written, the second touch of every old message from L2.  Launch protocol of
+// the CSR kernels (sweep_epilogue, LAG 0): launch s reads S_{s-1}, writes S_s, forms the
+// marginals x^{(s-1)} of the state it read and the residual row of x^{(s-2)}, decides sweep
+// s-2.  Divisions: the fast path with its range test per division, IEEE '/' when it fails.
+template <int D, bool UNIFORM>
+__global__ void __launch_bounds__(kDRows, GABP_DIA_MINB) dia_par_kernel(const SweepArgs a) {
+    __shared__ TailSmem<kDRows / 32> T;
+    __shared__ int64_t s_sweep;
+    __shared__ int s_skip;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        volatile Ctrl *vc = a.ctrl;
+        const int64_t s = vc->next_sweep;
+        s_sweep = s;
+        s_skip = vc->done || s > vc->max_iter + 2;
+    }
+    __syncthreads();
+    if (s_skip) return;
+    const int64_t s = s_sweep;
+    const int64_t nl = a.dia_nl, nlc = a.dia_nlc;
+    const double2 *mo = a.msg[(s - 1) % 3];
+    double2 *mn = a.msg[s % 3];
+    const bool resid = s >= 3;
+    const double *xp = a.x[(s + 1) % 3];  // x^{(s-2)} (residual), read when resid
+    double *xc = a.x[(s - 1) % 3], *pc = a.p[(s - 1) % 3];
+    double *xh = (a.xhist && s >= 2 && s - 1 <= a.xhist_rows) ? a.xhist + (s - 2) * a.n : nullptr;
+    Stats st;
+    st.lim = fmin(a.ctrl->blowup, DBL_MAX);
+    int64_t off[D], tws[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        off[k] = a.dia_off[k];
+        tws[k] = (int64_t)a.dia_opp[k] * nl + off[k];  // slot (opp k, i + o_k): tws[k] + i
+    }
+    const double cu = a.dia_cu, mccu = -cu * cu;  // (-coeff * coeff, solver.py:156)
+    const double rcu = UNIFORM ? ddiv_rcp(cu) : 1.0;
+    const int64_t r0 = a.dia_r0, r1 = a.dia_r1, r0e = r0 & ~1ll;
+    const int64_t nt = dia_ntiles(a);
+    for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
+        const int64_t i = dia_tile_row(a, r0e, t) + tid;
+        if (i < r0 || i >= r1) continue;
+        // ---- loads
+        double c[D], xj[D];
+        double2 in[D], old[D];
+        unsigned mask = 0u;
+        if (UNIFORM) mask = a.dia_mask[i];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            if (!UNIFORM) c[k] = __ldcs(a.dia_coef + k * nlc + i);
+            // (touch order as in the broadcast kernel: only the second touch streams)
+            if (off[k] > 0) {
+                old[k] = __ldcg(mo + tws[k] + i);  // m_ij of S_{s-1}: j's slot from i
+                in[k] = __ldcg(mo + k * nl + i);   // m_ji of S_{s-1}
+            } else {
+                old[k] = __ldcs(mo + tws[k] + i);
+                in[k] = __ldcs(mo + k * nl + i);
+            }
+            xj[k] = resid ? __ldcg(xp + i + off[k]) : 0.0;
+        }
+        const NodeRec nd = a.nd[i];
+        const double xi = resid ? __ldcg(xp + i) : 0.0, bi = __ldcs(a.rhs + i);
+        // ---- incoming terms (an empty slot adds -0.0: the identity of IEEE addition)
+        bool v[D];
+        double tp[D], tn[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            v[k] = UNIFORM ? ((mask >> k) & 1u) != 0u : c[k] != 0.0;
+            tp[k] = v[k] ? in[k].x : -0.0;
+            tn[k] = v[k] ? in[k].x * in[k].y : -0.0;  // (prec * mean), solver.py:148
+        }
+        // marginals of S_{s-1} (infer_marginals, solver.py:275-287) and the residual row
+        double P = nd.diag, N = nd.pnum, y = nd.diag * xi;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            P = P + tp[k];
+            N = N + tn[k];
+            const double ck = UNIFORM ? cu : c[k];
+            y = y + (v[k] ? ck * xj[k] : -0.0);
+        }
+        bool okx;
+        double x = ddiv_fast(N, P, okx);
+        if (!okx) x = div_slow(N, P);
+        if (!(fabs(x) <= DBL_MAX)) st.means_bad = 1u;
+        __stcg(pc + i, P);
+        __stcg(xc + i, x);
+        if (xh) xh[i] = x;
+        if (resid) {
+            const double r = y - bi;
+            st.rsq += r * r;
+        }
+        // ---- the D outgoing messages
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            double pe = nd.diag, num = nd.pnum;
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                if (q != k) {
+                    pe = pe + tp[q];
+                    num = num + tn[q];
+                }
+            }
+            if (v[k]) {
+                const double ck = UNIFORM ? cu : c[k];
+                const double mcc = UNIFORM ? mccu : -ck * ck;
+                bool okp, okm;
+                double np_ = ddiv_fast(mcc, pe, okp);
+                double nm = UNIFORM ? ddiv_fast_r(num, ck, rcu, okm) : ddiv_fast(num, ck, okm);
+                if (!okp) np_ = div_slow(mcc, pe);
+                if (!okm) nm = div_slow(num, ck);
+                __stcs(mn + tws[k] + i, make_double2(np_, nm));
+                const double d1 = fabs(np_ - old[k].x), d2 = fabs(nm - old[k].y);
+                st.chg = fmax(st.chg, fmax(d1, d2));
+                if (!(fabs(np_) <= st.lim) || !(fabs(nm) <= st.lim))
+                    st.out_of_range |= (np_ != np_ || nm != nm) ? 3u : 1u;
+                if (pe == 0.0) {  // the CSR id of edge i -> j (solver.py:150-154)
+                    const unsigned before = UNIFORM ? __popc(mask & ((1u << k) - 1u)) : [&] {
+                        unsigned b = 0u;
+                        for (int q = 0; q < k; ++q) b += v[q] ? 1u : 0u;
+                        return b;
+                    }();
+                    st.sing = min(st.sing, a.row_ptr[i] + before);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    sweep_epilogue<kDRows, kModeSolve, 0>(T, a, s, resid, st, tid);
+}
+
 // Aggregates and marginals of S_0 (all messages +0) into ring slot 0: the same sums as a
 // sweep forms them, so the +0 terms leave exactly the bits a sum over zero messages has.
 template <int D>
@@ -507,6 +643,28 @@ void dia_launch_t(const SweepArgs &a, cudaStream_t st) {
         dia_sweep_kernel<D, true, false><<<(unsigned)grid, kDRows, 0, st>>>(a);
     else
         dia_sweep_kernel<D, false, false><<<(unsigned)grid, kDRows, 0, st>>>(a);
+}
+
+template <int D>
+void dia_par_launch_t(const SweepArgs &a, cudaStream_t st) {
+    const int64_t nt = dia_ntiles(a);
+    int64_t grid = g_dia_grid > 0 ? g_dia_grid : 148 * 2;
+    if (grid > nt) grid = nt > 0 ? nt : 1;
+    if (a.dia_mask)
+        dia_par_kernel<D, true><<<(unsigned)grid, kDRows, 0, st>>>(a);
+    else
+        dia_par_kernel<D, false><<<(unsigned)grid, kDRows, 0, st>>>(a);
+}
+
+cudaError_t launch_dia_par_sweep(const SweepArgs &a, cudaStream_t st) {
+    switch (a.dia_D) {
+        case 2: dia_par_launch_t<2>(a, st); break;
+        case 4: dia_par_launch_t<4>(a, st); break;
+        case 6: dia_par_launch_t<6>(a, st); break;
+        case 8: dia_par_launch_t<8>(a, st); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_dia_sweep(const SweepArgs &a, cudaStream_t st) {

@@ -367,6 +367,9 @@ cudaError_t launch_gather(int64_t cnt, const int64_t *idx, const double2 *m, dou
 cudaError_t prepare_dia_kernels();
 cudaError_t launch_dia_init(const SweepArgs &a, cudaStream_t st);
 cudaError_t launch_dia_sweep(const SweepArgs &a, cudaStream_t st);
+// the parallel schedule on the diagonal layout (launch protocol of the CSR kernels: no init,
+// max_iter + 2 launches, decision of sweep s-2 in launch s)
+cudaError_t launch_dia_par_sweep(const SweepArgs &a, cudaStream_t st);
 // elements of padding the diagonal kernel needs on both sides of the message and node-state
 // arrays (every staged range in bounds)
 int64_t dia_pad(int64_t max_off);

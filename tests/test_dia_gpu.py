@@ -21,6 +21,13 @@ def _need_gpu():
     oracle.build()
 
 
+@pytest.fixture(autouse=True)
+def _no_cluster_path(monkeypatch):
+    # the smaller systems here would fit the one-launch cluster solve (small.cu): keep them
+    # on the diagonal-layout kernels this file tests
+    monkeypatch.setenv("GABP_NO_SMALL", "1")
+
+
 def _bits(a):
     return np.asarray(a, dtype=np.float64).view(np.uint64)
 
@@ -116,3 +123,53 @@ def test_dia_bench_sweeps():
         assert 0.0 < ms.value < 5.0
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("name", list(SYSTEMS))
+@pytest.mark.parametrize("kw", [dict(epsilon=1e-300, rel_residual_tol=1e-8, max_iter=20000),
+                                dict(epsilon=1e-7, max_iter=20000),
+                                dict(epsilon=1e-300, max_iter=9)])
+def test_dia_parallel_schedule_matches_oracle(name, kw):
+    """The reference's default schedule (solver.py:146-173) on the diagonal layout
+    (dia_par_kernel): exclusion sums over the row's own slots, outgoing messages written into
+    the neighbours' shifted slots."""
+    s = SYSTEMS[name]()
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    o = oracle.solve(og, schedule="parallel", **kw)
+    r = G.solve(s, G.SolveOptions(schedule="parallel", **kw))
+    assert (r.iterations, r.converged, r.diverged) == (o.iterations, o.converged, o.diverged)
+    np.testing.assert_array_equal(_bits(r.means), _bits(o.means))
+    np.testing.assert_array_equal(_bits(r.precisions), _bits(o.precisions))
+    np.testing.assert_array_equal(np.asarray(r.max_change_history), o.max_change_history)
+    np.testing.assert_allclose(r.residual_history, o.residual_history, rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("name", ["poisson3d-16", "stencil2d-48-random"])
+def test_dia_parallel_means_history_equals_slice_loop(name, monkeypatch):
+    s = SYSTEMS[name]()
+    kw = dict(schedule="parallel", epsilon=1e-300, max_iter=40, record_means_history=True)
+    r = G.solve(s, G.SolveOptions(**kw))
+    monkeypatch.setenv("GABP_NO_DIA_PAR", "1")
+    sl = G.solve(s, G.SolveOptions(**kw))
+    assert r.iterations == sl.iterations == 40
+    for a, b in zip(r.means_history, sl.means_history):
+        np.testing.assert_array_equal(_bits(a), _bits(b))
+    np.testing.assert_array_equal(_bits(np.asarray(r.max_change_history)),
+                                  _bits(np.asarray(sl.max_change_history)))
+
+
+def test_dia_parallel_divergent_stencil():
+    p = 40
+    pi, pj = P._grid2d_pairs(p)
+    rng = np.random.default_rng(9)
+    s = G.SymSystem.from_pairs(np.full(p * p, 2.2), pi, pj, np.full(pi.size, -1.0),
+                               rng.standard_normal(p * p))
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    kw = dict(epsilon=1e-300, max_iter=3000)
+    o = oracle.solve(og, schedule="parallel", **kw)
+    r = G.solve(s, G.SolveOptions(schedule="parallel", **kw))
+    assert (r.iterations, r.converged, r.diverged) == (o.iterations, o.converged, o.diverged)
+    np.testing.assert_array_equal(np.asarray(r.max_change_history), o.max_change_history)
+    fin = np.isfinite(o.means)
+    np.testing.assert_array_equal(np.isfinite(r.means), fin)
+    np.testing.assert_array_equal(_bits(r.means[fin]), _bits(o.means[fin]))
