@@ -299,12 +299,24 @@ def configs_block(dev: int, peak: float) -> dict:
         "sweeps_to_1e-8": it, "time_to_1e-8_ms": best, "us_per_sweep": 1e3 * best / it,
         "edge_updates_per_s": it * g0.num_edges / (best / 1e3),
         "bound": "latency (one launch of an 8-CTA cluster, every operand in distributed shared memory)"}
+    # the reference's default schedule (parallel) on the same graph, same kernel family
+    op0 = G.SolveOptions(schedule="parallel", epsilon=1e-300, rel_residual_tol=REL_TOL,
+                         device=dev, record_means_history=False)
+    G.solve_graph(g0, op0)
+    rp0 = min((G.solve_graph(g0, op0) for _ in range(3)), key=lambda r: r.device_ms)
+    out["poisson2d-32"]["parallel_schedule"] = {
+        "sweeps_to_1e-8": rp0.iterations, "time_to_1e-8_ms": rp0.device_ms,
+        "us_per_sweep": 1e3 * rp0.device_ms / rp0.iterations}
     g0.close()
     # config 2: 4096^2 grid, generated on the device
     g2 = GR.GridGraph(GR.GridSpec(2, 4096, 0), dev)
     ms2 = _sweep_ms(lib, g2.handle, 2, 20)
     out["poisson2d-4096"] = _block("poisson2d-4096", g2.n, g2.num_edges, ms2, peak,
                                    traffic_key="config2_broadcast")
+    msp2 = _sweep_ms(lib, g2.handle, 0, 20)  # parallel schedule: dia_par_kernel
+    out["poisson2d-4096"]["parallel_schedule"] = {
+        "ms_per_sweep": msp2, "edge_updates_per_s": g2.num_edges / (msp2 / 1e3),
+        "frac": _algo_bytes(g2.num_edges, g2.n) / (msp2 / 1e3) / 1e9 / peak}
     g2.close()
     # config 3: dense CDMA, dense kernels (time a capped solve: they run in the loop only)
     s3 = P.CONFIGS[3][1](0).system
@@ -579,6 +591,11 @@ def run_ours(args):
     value = useful_all / (total_ms_max / 1e3)
 
     ms_sweep_after = sweep_ms()
+    # the other synchronous schedule on the headline graph (steady sweeps, reported beside)
+    other = "parallel" if sched == "broadcast" else "broadcast"
+    ms_other = ctypes.c_double()
+    _lib.check(lib.gabp_bench_sweeps(g.handle, _lib.SCHED_IDS[other], 0, 20,
+                                     ctypes.byref(ms_other)))
     algo_bytes = BYTES_PER_EDGE * E + BYTES_PER_NODE * n
     achieved = algo_bytes / (ms_sweep.value / 1e3) / 1e9
     achieved_after = algo_bytes / (ms_sweep_after.value / 1e3) / 1e9
@@ -662,6 +679,12 @@ def run_ours(args):
                          "timing": "%d back-to-back sweeps before the solve loop" % sweeps,
                          "frac_after_loop": achieved_after / peak,
                          "ms_per_sweep_after_loop": ms_sweep_after.value},
+            other + "_schedule": {
+                "ms_per_sweep": ms_other.value, "edge_updates_per_s": E / (ms_other.value / 1e3),
+                "frac": algo_bytes / (ms_other.value / 1e3) / 1e9 / peak,
+                "note": "steady sweeps of the other synchronous schedule on the same graph "
+                        "(parallel = the reference's default, solver.py:146-173: one random "
+                        "twin gather per edge, 128 B of DRAM each)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                     "ms_per_step": e2e_s / e2e_steps * 1e3},

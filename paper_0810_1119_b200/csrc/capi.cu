@@ -2329,6 +2329,22 @@ int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int32_t gather_mode, in
         *ms_per_sweep = dms / (double)sweeps;
         return GABP_OK;
     }
+    if (schedule == GABP_SCHED_PARALLEL && gather_mode == GABP_GATHER_AUTO && G->g.dia_D > 0 &&
+        !getenv("GABP_NO_DIA_PAR")) {
+        for (int k = 0; k < 3; ++k) CK(gabp::launch_dia_par_sweep(a, st));
+        CK(cudaEventRecord(G->ev[2], st));
+        for (int64_t k = 0; k < sweeps; ++k) CK(gabp::launch_dia_par_sweep(a, st));
+        CK(cudaEventRecord(G->ev[3], st));
+        CK(cudaMemcpyAsync(G->h_ctrl, G->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        float dms = 0.f;
+        CK(cudaEventElapsedTime(&dms, G->ev[2], G->ev[3]));
+        if (G->h_ctrl->done)
+            return fail(GABP_EINVAL, "bench sweeps stopped early (diverged at sweep %lld)",
+                        (long long)G->h_ctrl->iterations);
+        *ms_per_sweep = dms / (double)sweeps;
+        return GABP_OK;
+    }
     rc = check_slice(G, &o);
     if (rc) return rc;
     const int gather = pick_gather(G, &o);
