@@ -269,6 +269,15 @@ int gabp_dist_results(gabp_graph_t *g, const gabp_options_t *opt, double *h_mean
 int gabp_bench_sweeps(gabp_graph_t *g, int32_t schedule, int32_t gather_mode, int64_t sweeps,
                       double *ms_per_sweep);
 
+/* Host-only planning hook of the one-launch cluster solve of small graphs (small.cu; no
+ * device call): cuts the rows [0, n) of a CSR with host offsets row_ptr[n+1] into the row
+ * blocks of the cluster's CTAs.  Returns the number of CTAs (1, 2, 4 or 8; 0 when the graph
+ * does not fit a cluster and takes the launch-per-sweep kernels), block c = rows
+ * [bounds[c], bounds[c+1]) in bounds[9], and the per-CTA capacities of the chosen thread
+ * configuration in cap_edges / cap_rows. */
+int gabp_small_plan(int64_t n, const uint32_t *row_ptr, int64_t *bounds, int64_t *cap_edges,
+                    int64_t *cap_rows);
+
 #ifdef __cplusplus
 }
 #endif

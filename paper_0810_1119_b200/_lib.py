@@ -39,7 +39,7 @@ EXPORTED = (
     "gabp_sweep", "gabp_sweep_serial", "gabp_infer_marginals",
     "gabp_solve", "gabp_solve_device", "gabp_solve_system", "gabp_residual_norm_per_eq",
     "gabp_bench_sweeps", "gabp_graph_create_ex", "gabp_nccl_unique_id", "gabp_dist_attach",
-    "gabp_dist_solve_local", "gabp_dist_results",
+    "gabp_dist_solve_local", "gabp_dist_results", "gabp_small_plan",
 )
 
 
@@ -148,6 +148,8 @@ def load():
         "gabp_dist_solve_local": (ctypes.c_int, [_i32, _vp, ctypes.POINTER(Options), _dp]),
         "gabp_dist_results": (ctypes.c_int, [_vp, ctypes.POINTER(Options), _vp, _vp, _vp, _vp,
                                              ctypes.POINTER(Report)]),
+        "gabp_small_plan": (ctypes.c_int, [_i64, _vp, _vp, ctypes.POINTER(_i64),
+                                           ctypes.POINTER(_i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -2281,6 +2281,20 @@ int gabp_residual_norm_per_eq(const gabp_graph_t *G, const double *h_x, double *
     return GABP_OK;
 }
 
+int gabp_small_plan(int64_t n, const uint32_t *row_ptr, int64_t *bounds, int64_t *cap_edges,
+                    int64_t *cap_rows) {
+    if (n < 1 || !row_ptr || !bounds) return 0;
+    gabp::SmallPart p = {};
+    if (!gabp::small_candidate(n, (int64_t)row_ptr[n]) || !gabp::small_plan(n, row_ptr, &p))
+        return 0;
+    for (int c = 0; c <= p.C; ++c) bounds[c] = (int64_t)p.nb[c];
+    int64_t ce = 0, cr = 0;
+    gabp::small_capacity(p.cfg, &ce, &cr);
+    if (cap_edges) *cap_edges = ce;
+    if (cap_rows) *cap_rows = cr;
+    return p.C;
+}
+
 int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int32_t gather_mode, int64_t sweeps,
                       double *ms_per_sweep) {
     if (!G || sweeps < 1 || !ms_per_sweep) return fail(GABP_EINVAL, "bad argument");

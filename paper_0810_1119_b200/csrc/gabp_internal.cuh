@@ -384,6 +384,7 @@ struct SmallPart {
 };
 bool small_candidate(int64_t n, int64_t E);  // sizes a cluster could hold at all
 bool small_plan(int64_t n, const uint32_t *row_ptr, SmallPart *out);
+void small_capacity(int cfg, int64_t *edges, int64_t *rows);
 cudaError_t launch_small_solve(const SweepArgs &a, const SmallPart &p, bool parallel,
                                cudaStream_t st);
 

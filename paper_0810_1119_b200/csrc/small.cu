@@ -512,6 +512,12 @@ bool small_plan(int64_t n, const uint32_t *row_ptr, SmallPart *out) {
     return false;
 }
 
+void small_capacity(int cfg, int64_t *edges, int64_t *rows) {
+    const SmallCfg &s = kSmallCfg[cfg == 0 ? 0 : 1];
+    *edges = (int64_t)s.nt * s.ept;
+    *rows = (int64_t)s.nt * s.npt;
+}
+
 bool small_candidate(int64_t n, int64_t E) {
     const SmallCfg &s = kSmallCfg[1];
     return n >= 1 && n <= (int64_t)kSmallMaxCluster * s.nt * s.npt &&

@@ -100,3 +100,57 @@ def test_generators_deterministic_and_dominant():
     a, _ = inst.system.to_dense()
     np.testing.assert_array_equal(a, a.T)
     np.testing.assert_allclose(np.diag(a), 1.5)
+
+
+# ---- host planning of the one-launch cluster solve (csrc/small.cu: small_plan) -----------
+
+def _small_plan(row_ptr):
+    import ctypes
+    lib = _lib.load()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.uint32)
+    bounds = np.zeros(9, dtype=np.int64)
+    ce, cr = ctypes.c_int64(), ctypes.c_int64()
+    C = lib.gabp_small_plan(rp.size - 1, rp.ctypes.data, bounds.ctypes.data,
+                            ctypes.byref(ce), ctypes.byref(cr))
+    return C, bounds[:C + 1], ce.value, cr.value
+
+
+def _grid_row_ptr(p):
+    deg = np.full((p, p), 4)
+    deg[0, :] -= 1
+    deg[-1, :] -= 1
+    deg[:, 0] -= 1
+    deg[:, -1] -= 1
+    return np.concatenate([[0], np.cumsum(deg.ravel())])
+
+
+def test_small_plan_config0_eight_balanced_blocks():
+    rp = _grid_row_ptr(32)  # config 0: 1024 rows, 3968 edge slots
+    C, b, ce, cr = _small_plan(rp)
+    assert C == 8 and b[0] == 0 and b[-1] == 1024
+    assert np.all(np.diff(b) > 0)
+    edges = rp[b[1:]] - rp[b[:-1]]
+    rows = np.diff(b)
+    assert edges.max() <= ce and rows.max() <= cr
+    assert edges.max() - edges.min() <= 16 and rows.max() - rows.min() <= 8
+
+
+def test_small_plan_covers_every_row_once_and_respects_capacity():
+    rng = np.random.default_rng(7)
+    for n, lam in ((3, 1.0), (50, 3.0), (700, 6.0), (3000, 4.0), (6000, 2.0), (64, 40.0)):
+        deg = rng.poisson(lam, n)
+        rp = np.concatenate([[0], np.cumsum(deg)])
+        C, b, ce, cr = _small_plan(rp)
+        assert C in (1, 2, 4, 8), (n, lam)
+        assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0)
+        assert (rp[b[1:]] - rp[b[:-1]]).max() <= ce
+        assert np.diff(b).max() <= cr
+
+
+def test_small_plan_rejects_what_no_cluster_holds():
+    # a hub row wider than any CTA's edge capacity; a graph with too many rows
+    rp = np.concatenate([[0], np.cumsum([2500] + [1] * 2500)])
+    assert _small_plan(rp)[0] == 0
+    assert _small_plan(np.arange(0, 4 * 20001, 4))[0] == 0
+    # one CTA's worth of work stays on one CTA
+    assert _small_plan(np.arange(0, 3 * 41, 3))[0] == 1
