@@ -28,6 +28,7 @@
 // (sweep.cu, sweep_epilogue with LAG 0), so the solve loop and controller are unchanged.
 #include <float.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "sweep_common.cuh"
 
@@ -367,6 +368,282 @@ __global__ void __launch_bounds__(kRThreads, 2) rowpar_kernel(const SweepArgs a)
 }
 
 
+// ---- four rows per warp --------------------------------------------------------------------
+// rowpar_kernel spends 6 instructions per exclusion-sum term (compare, two moves that select
+// the strip base, the load, two adds) because a lane's own slot sits at a lane-specific place
+// of every 8-term block, and runs rows of 33..64 edges as two sums per lane with most lanes
+// of the second idle.  Here a warp takes FOUR consecutive rows; lane (g, o) = (lane / 8,
+// lane % 8) works on row g.  The outgoing edges of a row are taken 8 at a time -- own block b,
+// edge j = 8 b + o -- so "is this term block my own block" is the same question for every
+// lane of the warp: term blocks b' != b add their 8 terms with immediate offsets (load + two
+// adds per term), and only the own block (7 terms) pays for the skip.  Lanes are busy for any
+// row length (a row of 40 edges: 5 own blocks of 8 lanes), and the edge divisions run with all
+// 32 lanes.  The rows' twin messages land through cp.async in a per-warp shared-memory buffer
+// (the next quad's gathers under this quad's walk) and are converted in place into the strip
+// {P, P mu}; strips are padded with {-0, -0} to a whole number of blocks and sit at a row
+// stride of 66 entries, so the four rows' broadcast loads hit different banks.
+constexpr int kQThreads = 128;
+constexpr int kQWarps = kQThreads / 32;
+constexpr int kQStride = 66;
+struct __align__(16) QuadBuf {
+    double2 tw[2][4][kQStride];  // twin messages m_ji of S_{s-1}; then the strip {P, P mu}
+                                 // (two quads: the next one lands under this one's walk)
+    double c[2][4][64];          // A_ij
+    double2 xg[4][64];           // the aligned pair of doubles holding x_j^{(s-2)}: consumed
+                                 // by the strip pass, so the next quad's land under the walk
+    uint8_t par[4][64];          // which half of the pair
+};
+static_assert(sizeof(double2) * 4 * kQStride >= sizeof(double2) * (kRowParMaxDegree + 8),
+              "a long row's strip fits a quad's strips");
+constexpr size_t kQuadBytes = sizeof(QuadBuf) * kQWarps;
+
+__device__ __forceinline__ void cpa_tw(double2 *dst, const double2 *src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "l"(pol)
+                 : "memory");
+}
+// x_j as the aligned 16 bytes around it: cp.async.cg bypasses the L1 (an 8-byte
+// cp.async.ca allocates L1 lines: the random x gathers then cost 0.47 ms of a 1.6 ms sweep)
+__device__ __forceinline__ void cpa_x2(double2 *dst, const double *x, uint32_t col) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(x + (col & ~1u))
+                 : "memory");
+}
+
+// this lane's row of a quad
+struct QRow {
+    uint32_t i = 0xffffffffu, e0 = 0, d = 0;  // d: edges walked here (0 for long rows)
+    uint32_t dl = 0;                          // the row's degree when it is a long row
+    double2 nd = make_double2(0.0, 0.0);      // {A_ii, A_ii mu_ii}
+    double xi = 0.0, bi = 0.0;                // x_i^{(s-2)}, b_i
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a) {
+    __shared__ TailSmem<kQWarps> tail;
+    __shared__ int64_t s_sweep;
+    __shared__ int s_skip;
+    extern __shared__ __align__(16) unsigned char quad_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    Ctrl *ctrl = a.ctrl;
+    if (tid == 0) {
+        if (MODE == kModeSolve) {
+            volatile Ctrl *vc = ctrl;
+            const int64_t s = vc->next_sweep;
+            s_skip = vc->done || s > vc->max_iter + 2;
+            s_sweep = s;
+        } else {
+            s_skip = 0;
+            s_sweep = 1;
+        }
+    }
+    __syncthreads();
+    if (s_skip) return;
+    const int64_t s = s_sweep;
+    RowCtx x;
+    x.resid = (MODE == kModeSolve) && s >= 3;
+    x.min_ = a.msg[(s - 1) % 3];
+    x.xprev = x.resid ? a.x[(s - 2) % 3] : nullptr;
+    x.mout = a.msg[s % 3];
+    x.xcur = (MODE == kModeSolve) ? a.x[(s - 1) % 3] : nullptr;
+    x.pcur = (MODE == kModeSolve) ? a.p[(s - 1) % 3] : nullptr;
+    x.xh = (MODE == kModeSolve && a.xhist && s >= 2 && s - 1 <= a.xhist_rows)
+               ? a.xhist + (s - 2) * a.n : nullptr;
+    x.pol = pol_evict_first();
+    Stats st;
+    st.lim = (MODE == kModeSolve) ? fmin(ctrl->blowup, DBL_MAX) : DBL_MAX;
+    QuadBuf &W = reinterpret_cast<QuadBuf *>(quad_raw)[warp];
+    const int g = lane >> 3, o = lane & 7;
+
+    const uint32_t r_lo = __ldg(&a.tile_info[0].x);
+    const uint32_t r_hi = __ldg(&a.tile_info[a.ntiles - 1].y);
+    const int64_t nw = (int64_t)gridDim.x * kQWarps, gw = (int64_t)blockIdx.x * kQWarps + warp;
+    const uint32_t rb = r_lo + (uint32_t)(((int64_t)(r_hi - r_lo) * gw) / nw);
+    const uint32_t re = r_lo + (uint32_t)(((int64_t)(r_hi - r_lo) * (gw + 1)) / nw);
+    const uint32_t nq = (re - rb + 3u) / 4u;
+
+    // row offsets of quad q for this lane's row (empty past the range)
+    auto row_of = [&](uint32_t q, QRow &r) {
+        r = QRow();
+        const uint32_t i = rb + 4u * q + (uint32_t)g;
+        if (q < nq && i < re) {
+            r.i = i;
+            r.e0 = __ldg(a.row_ptr + i);
+            const uint32_t d = __ldg(a.row_ptr + i + 1) - r.e0;
+            r.d = d <= 64u ? d : 0u;
+            r.dl = d <= 64u ? 0u : d;
+        }
+    };
+    // edge records of the row's slots o, o + 8, ... (registers, consumed by the issue stage)
+    auto load_er = [&](const QRow &r, int4 (&er)[8]) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const uint32_t q = (uint32_t)o + 8u * t;
+            er[t] = q < r.d ? ld_ef_i4(a.er + r.e0 + q, x.pol) : make_int4(0, 0, 0, 0);
+        }
+    };
+    // issue stage, part 1: twin gathers of the row into strip buffer `nb`, coefficients, node
+    // operands into registers
+    auto issue_tw = [&](QRow &r, const int4 (&er)[8], int nb) {
+        if (r.i != 0xffffffffu) {
+            r.nd = __ldg(reinterpret_cast<const double2 *>(a.nd + r.i));
+            if (x.resid) {
+                r.xi = __ldg(x.xprev + r.i);
+                r.bi = __ldg(a.rhs + r.i);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const uint32_t q = (uint32_t)o + 8u * t;
+            if (q < r.d) {
+                const EdgeRec e = er_of(er[t]);
+                W.c[nb][g][q] = e.coeff;
+#ifdef GABP_ROW_PROBE_COALESCED  // probe build (wrong results): no random twin gather
+                cpa_tw(&W.tw[nb][g][q], x.min_ + r.e0 + q, x.pol);
+#else
+                cpa_tw(&W.tw[nb][g][q], x.min_ + e.rev, x.pol);
+#endif
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    // part 2 (after the strip pass has consumed the previous quad's x): the x_j gathers
+    auto issue_x = [&](const QRow &r, const int4 (&er)[8]) {
+#ifndef GABP_ROW_PROBE_NOX
+        if (x.resid) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const uint32_t q = (uint32_t)o + 8u * t;
+                if (q < r.d) {
+                    const uint32_t col = (uint32_t)er[t].y;
+                    W.par[g][q] = (uint8_t)(col & 1u);
+                    cpa_x2(&W.xg[g][q], x.xprev, col);
+                }
+            }
+        }
+#endif
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+
+    if (nq > 0) {
+        QRow rc, ri, rl;  // rows of the quad being walked, issued, loaded
+        int4 er[8];
+        row_of(0, ri);
+        load_er(ri, er);
+        issue_tw(ri, er, 0);
+        issue_x(ri, er);
+        row_of(1, rl);
+        load_er(rl, er);
+        for (uint32_t q = 0; q < nq; ++q) {
+            const int cb = (int)(q & 1u);
+            rc = ri;
+            ri = rl;
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // quad q has landed
+            __syncwarp();
+            issue_tw(ri, er, cb ^ 1);  // quad q + 1 (empty past the range)
+            double2 *Tg = W.tw[cb][g];
+            const double *Cg = W.c[cb][g];
+            // strip in place, the row's residual partial
+            const uint32_t nbmax = __reduce_max_sync(~0u, (rc.d + 7u) >> 3);
+            double yp = 0.0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const uint32_t k = (uint32_t)o + 8u * t;
+                if (k < rc.d) {
+                    const double2 v = Tg[k];
+                    Tg[k] = make_double2(v.x, v.x * v.y);  // (prec * mean), solver.py:148
+                    if (x.resid) {
+                        const double2 xp = W.xg[g][k];
+                        yp = yp + Cg[k] * (W.par[g][k] ? xp.y : xp.x);
+                    }
+                } else if (k < 8u * nbmax) {
+                    Tg[k] = make_double2(-0.0, -0.0);
+                }
+            }
+            __syncwarp();
+            issue_x(ri, er);  // (the x buffer is free again)
+            row_of(q + 2, rl);
+            load_er(rl, er);
+            if (x.resid) {  // sum over the row's 8 lanes
+                yp += __shfl_xor_sync(~0u, yp, 1);
+                yp += __shfl_xor_sync(~0u, yp, 2);
+                yp += __shfl_xor_sync(~0u, yp, 4);
+            }
+#ifdef GABP_ROW_PROBE_NOWALK  // probe build (wrong results): the memory side alone
+            for (uint32_t b = 0; b < nbmax; ++b) {
+                const uint32_t j = 8u * b + (uint32_t)o;
+                if (j < rc.d) {
+                    const double2 old = ld_ef_d2(x.min_ + rc.e0 + j, x.pol);
+                    const double2 v = Tg[j];
+                    st_ef_d2(x.mout + rc.e0 + j, make_double2(v.x + old.x, v.y + old.y), x.pol);
+                }
+            }
+            if (false)
+#endif
+            for (uint32_t b = 0; b < nbmax; ++b) {  // own block: edges 8 b .. 8 b + 7
+                const uint32_t j = 8u * b + (uint32_t)o;
+                const bool act = j < rc.d;
+                const double2 old = act ? ld_ef_d2(x.min_ + rc.e0 + j, x.pol)
+                                        : make_double2(0.0, 0.0);
+                double p = rc.nd.x, n = rc.nd.y;
+                for (uint32_t bp = 0; bp < nbmax; ++bp) {
+                    const double2 *base = Tg + 8u * bp;
+                    if (bp != b) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const double2 v = base[k];
+                            p = p + v.x;
+                            n = n + v.y;
+                        }
+                    } else {  // terms 0..o-1, then o+1..7 (the skip is an address select)
+#pragma unroll
+                        for (int k = 0; k < 7; ++k) {
+                            const double2 v = (o > k ? base : base + 1)[k];
+                            p = p + v.x;
+                            n = n + v.y;
+                        }
+                    }
+                }
+                if (act) {
+                    edge_out(x, rc.e0 + j, Cg[j], p, n, old, st);
+                    if (j == rc.d - 1u) {  // full sums: the last exclusion sum + the last term
+                        const double2 own = Tg[j];
+                        row_node<MODE>(a, x, rc.i, p + own.x, n + own.y, st);
+                    }
+                }
+            }
+            const bool plain = rc.i != 0xffffffffu && rc.dl == 0u;
+            if (plain && rc.d == 0u && o == 0) row_node<MODE>(a, x, rc.i, rc.nd.x, rc.nd.y, st);
+            if (x.resid && plain && o == 0) {
+                const double y = rc.nd.x * rc.xi + yp;
+                const double res = y - rc.bi;
+                st.rsq += res * res;
+            }
+            __syncwarp();
+            // rows of more than 64 edges: the whole warp, one row at a time, on the buffer
+            const unsigned lmask = __ballot_sync(~0u, rc.dl != 0u && o == 0);
+            for (int gg = 0; gg < 4; ++gg) {
+                if (lmask & (1u << (8 * gg))) {
+                    const int src = 8 * gg;
+                    NodeRec nd;
+                    nd.diag = __shfl_sync(~0u, rc.nd.x, src);
+                    nd.pnum = __shfl_sync(~0u, rc.nd.y, src);
+                    row_long<MODE>(a, x, &W.tw[cb][0][0], __shfl_sync(~0u, rc.i, src),
+                                   __shfl_sync(~0u, rc.e0, src), __shfl_sync(~0u, rc.dl, src),
+                                   nd, lane, st);
+                    __syncwarp();
+                }
+            }
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    sweep_epilogue<kQThreads, MODE, 0>(tail, a, s, x.resid, st, tid);
+}
+
+
 // ---- serial schedule (solver.py:176-217) as dependency levels ------------------------------
 // The reference updates node by node in a given order, in place: node i recomputes all its
 // outgoing messages m_ij from its current incoming messages m_ki.  Two tasks interact only
@@ -506,6 +783,7 @@ __global__ void edge_col_kernel(int64_t E, const EdgeRec *er, uint32_t *col) {
 constexpr int kMaxDevices = 64;
 int g_row_grid[kMaxDevices][2] = {};   // persistent grids per device (prepare_rowpar_kernels)
 int g_coop_grid[kMaxDevices] = {};     // cooperative serial sweep: every CTA resident
+int g_quad_grid[kMaxDevices][2] = {};  // rowquad_kernel
 
 int cur_dev() {
     int d = 0;
@@ -535,6 +813,21 @@ cudaError_t prepare_rowpar_kernels() {
                                                            0)) != cudaSuccess)
         return e;
     g_coop_grid[dv] = sms * (occ > 0 ? occ : 1);
+    if ((e = cudaFuncSetAttribute(rowquad_kernel<kModeSolve>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kQuadBytes)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(rowquad_kernel<kModeSingle>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kQuadBytes)) != cudaSuccess)
+        return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowquad_kernel<kModeSolve>,
+                                                           kQThreads, kQuadBytes)) != cudaSuccess)
+        return e;
+    g_quad_grid[dv][kModeSolve] = sms * (occ > 0 ? occ : 1);
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowquad_kernel<kModeSingle>,
+                                                           kQThreads, kQuadBytes)) != cudaSuccess)
+        return e;
+    g_quad_grid[dv][kModeSingle] = sms * (occ > 0 ? occ : 1);
     return cudaSuccess;
 }
 
@@ -578,6 +871,17 @@ cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st) {
     if (a.ntiles <= 0) return cudaSuccess;
     const int m = mode == kModeSolve ? kModeSolve : kModeSingle;
     const int dv = cur_dev();
+    static const bool quad = !getenv("GABP_ROW_NO_QUAD");
+    if (quad) {
+        int64_t grid = g_quad_grid[dv][m] > 0 ? g_quad_grid[dv][m] : 148 * 3;
+        const int64_t need = (a.ntiles + kQWarps - 1) / kQWarps;
+        if (grid > need) grid = need;
+        if (m == kModeSolve)
+            rowquad_kernel<kModeSolve><<<(unsigned)grid, kQThreads, kQuadBytes, st>>>(a);
+        else
+            rowquad_kernel<kModeSingle><<<(unsigned)grid, kQThreads, kQuadBytes, st>>>(a);
+        return cudaGetLastError();
+    }
     int64_t grid = g_row_grid[dv][m] > 0 ? g_row_grid[dv][m] : 148 * 4;
     const int64_t need = (a.ntiles + kRWarps - 1) / kRWarps;
     if (grid > need) grid = need;
