@@ -528,18 +528,21 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
     };
 
     if (nq > 0) {
-        QRow rc, ri, rl;  // rows of the quad being walked, issued, loaded
+        QRow rc, ri, rl, rn;  // rows of the quad being walked, issued, loaded; offsets ahead
         int4 er[8];
         row_of(0, ri);
         load_er(ri, er);
         issue_tw(ri, er, 0);
         issue_x(ri, er);
         row_of(1, rl);
+        row_of(2, rn);
         load_er(rl, er);
         for (uint32_t q = 0; q < nq; ++q) {
             const int cb = (int)(q & 1u);
             rc = ri;
             ri = rl;
+            rl = rn;  // (its offsets were loaded a quad ago: no dependent load before load_er)
+            row_of(q + 3, rn);
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // quad q has landed
             __syncwarp();
             issue_tw(ri, er, cb ^ 1);  // quad q + 1 (empty past the range)
@@ -564,55 +567,98 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
             }
             __syncwarp();
             issue_x(ri, er);  // (the x buffer is free again)
-            row_of(q + 2, rl);
             load_er(rl, er);
             if (x.resid) {  // sum over the row's 8 lanes
                 yp += __shfl_xor_sync(~0u, yp, 1);
                 yp += __shfl_xor_sync(~0u, yp, 2);
                 yp += __shfl_xor_sync(~0u, yp, 4);
             }
-#ifdef GABP_ROW_PROBE_NOWALK  // probe build (wrong results): the memory side alone
-            for (uint32_t b = 0; b < nbmax; ++b) {
-                const uint32_t j = 8u * b + (uint32_t)o;
+            // Own blocks two at a time: the lane's edges j0 = 8 b + o and j1 = j0 + 8 share
+            // every term load outside their own blocks and give the lane four independent add
+            // chains.  The edges' own messages of S_{s-1} (change statistic) are loaded a
+            // step ahead.
+            auto ld_old = [&](uint32_t j) {
+                return j < rc.d ? ld_ef_d2(x.min_ + rc.e0 + j, x.pol) : make_double2(0.0, 0.0);
+            };
+            auto finish = [&](uint32_t j, double p, double n, double2 old) {
                 if (j < rc.d) {
-                    const double2 old = ld_ef_d2(x.min_ + rc.e0 + j, x.pol);
-                    const double2 v = Tg[j];
-                    st_ef_d2(x.mout + rc.e0 + j, make_double2(v.x + old.x, v.y + old.y), x.pol);
-                }
-            }
-            if (false)
-#endif
-            for (uint32_t b = 0; b < nbmax; ++b) {  // own block: edges 8 b .. 8 b + 7
-                const uint32_t j = 8u * b + (uint32_t)o;
-                const bool act = j < rc.d;
-                const double2 old = act ? ld_ef_d2(x.min_ + rc.e0 + j, x.pol)
-                                        : make_double2(0.0, 0.0);
-                double p = rc.nd.x, n = rc.nd.y;
-                for (uint32_t bp = 0; bp < nbmax; ++bp) {
-                    const double2 *base = Tg + 8u * bp;
-                    if (bp != b) {
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const double2 v = base[k];
-                            p = p + v.x;
-                            n = n + v.y;
-                        }
-                    } else {  // terms 0..o-1, then o+1..7 (the skip is an address select)
-#pragma unroll
-                        for (int k = 0; k < 7; ++k) {
-                            const double2 v = (o > k ? base : base + 1)[k];
-                            p = p + v.x;
-                            n = n + v.y;
-                        }
-                    }
-                }
-                if (act) {
                     edge_out(x, rc.e0 + j, Cg[j], p, n, old, st);
                     if (j == rc.d - 1u) {  // full sums: the last exclusion sum + the last term
                         const double2 own = Tg[j];
                         row_node<MODE>(a, x, rc.i, p + own.x, n + own.y, st);
                     }
                 }
+            };
+            double2 oa = ld_old((uint32_t)o), ob = ld_old((uint32_t)o + 8u);
+            uint32_t b = 0;
+            for (; b + 1 < nbmax; b += 2) {
+                const uint32_t j0 = 8u * b + (uint32_t)o, j1 = j0 + 8u;
+                const double2 old0 = oa, old1 = ob;
+                oa = ld_old(j0 + 16u);
+                ob = ld_old(j1 + 16u);
+                double p0 = rc.nd.x, n0 = rc.nd.y, p1 = p0, n1 = n0;
+                for (uint32_t bp = 0; bp < nbmax; ++bp) {
+                    const double2 *base = Tg + 8u * bp;
+                    if (bp == b) {  // sum 0 skips its slot (an address select), sum 1 adds all
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const double2 v = base[k];
+                            p1 = p1 + v.x;
+                            n1 = n1 + v.y;
+                            if (k < 7) {
+                                const double2 w = (o > k ? base : base + 1)[k];
+                                p0 = p0 + w.x;
+                                n0 = n0 + w.y;
+                            }
+                        }
+                    } else if (bp == b + 1) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const double2 v = base[k];
+                            p0 = p0 + v.x;
+                            n0 = n0 + v.y;
+                            if (k < 7) {
+                                const double2 w = (o > k ? base : base + 1)[k];
+                                p1 = p1 + w.x;
+                                n1 = n1 + w.y;
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const double2 v = base[k];
+                            p0 = p0 + v.x;
+                            n0 = n0 + v.y;
+                            p1 = p1 + v.x;
+                            n1 = n1 + v.y;
+                        }
+                    }
+                }
+                finish(j0, p0, n0, old0);
+                finish(j1, p1, n1, old1);
+            }
+            if (b < nbmax) {  // an odd last own block
+                const uint32_t j0 = 8u * b + (uint32_t)o;
+                double p0 = rc.nd.x, n0 = rc.nd.y;
+                for (uint32_t bp = 0; bp < nbmax; ++bp) {
+                    const double2 *base = Tg + 8u * bp;
+                    if (bp != b) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const double2 v = base[k];
+                            p0 = p0 + v.x;
+                            n0 = n0 + v.y;
+                        }
+                    } else {  // terms 0..o-1, then o+1..7
+#pragma unroll
+                        for (int k = 0; k < 7; ++k) {
+                            const double2 v = (o > k ? base : base + 1)[k];
+                            p0 = p0 + v.x;
+                            n0 = n0 + v.y;
+                        }
+                    }
+                }
+                finish(j0, p0, n0, oa);
             }
             const bool plain = rc.i != 0xffffffffu && rc.dl == 0u;
             if (plain && rc.d == 0u && o == 0) row_node<MODE>(a, x, rc.i, rc.nd.x, rc.nd.y, st);
