@@ -539,12 +539,13 @@ int pick_gather(const gabp_graph *G, const gabp_options_t *opt) {
         // contiguous incoming slots, scattered twin stores) on whole graphs with slices
         const bool whole = G->g.row_lo == 0 && G->g.row_hi == G->g.n;
         if (opt->gather_mode == GABP_GATHER_ROWS) return gabp::kGatherRowParallel;
-        // high-degree rows (config 1: mean 32): warp per row, one exclusion sum per lane
-        // (rowpar.cu, 1.55 ms/sweep against 1.70 for the slice groups, whose later passes
-        // re-stream the row); low degrees stay on the slice groups (degree 4: 1.04 ms
-        // against 15.7 -- a warp per 4-edge row idles 28 lanes)
+        // mean degree >= 10: four rows per warp over the CSR order (rowpar.cu:
+        // rowquad_kernel; config 1, mean 32: 1.12 ms/sweep against 1.70 for the slice
+        // groups, whose later passes re-stream the row); lower degrees stay on the slice
+        // groups (random graphs of 512 k rows, tools/par_degree_probe.py: mean degree 8
+        // 0.190 ms against 0.251, 12: 0.302 against 0.281, 24: 0.590 against 0.429)
         if (opt->gather_mode == GABP_GATHER_AUTO && whole && G->g.n > 0 &&
-            G->g.E >= 24 * G->g.n && G->g.max_degree <= gabp::kRowParMaxDegree)
+            G->g.E >= 10 * G->g.n && G->g.max_degree <= gabp::kRowParMaxDegree)
             return gabp::kGatherRowParallel;
         if (opt->gather_mode == GABP_GATHER_SLICE ||
             (opt->gather_mode == GABP_GATHER_AUTO && G->g.nslices > 0 && whole))
