@@ -192,7 +192,8 @@ def test_state_blown_reads_the_whole_state():
 
 # ---- run-to-run reproducibility -------------------------------------------------------
 
-@pytest.mark.parametrize("sched,mode", [("broadcast", "auto"), ("parallel", "slice")])
+@pytest.mark.parametrize("sched,mode", [("broadcast", "auto"), ("parallel", "slice"),
+                                        ("parallel", "auto")])
 def test_solve_bitwise_reproducible_random_1m(sched, mode):
     """Two solves of config 1 (random 1M, k=16): the same residual history bit for bit and
     the same stop sweep -- the group kernels claim work dynamically, their residual
@@ -212,6 +213,50 @@ def test_solve_bitwise_reproducible_random_1m(sched, mode):
         np.testing.assert_array_equal(_bits(b.residual_history), _bits(a.residual_history))
         np.testing.assert_array_equal(_bits(b.max_change_history), _bits(a.max_change_history))
         np.testing.assert_array_equal(_bits(b.means), _bits(a.means))
+
+
+def test_parallel_quad_kernel_equals_one_row_per_warp_and_oracle_1m(monkeypatch):
+    """Config 1 at full size, parallel schedule: the four-rows-per-warp kernel (AUTO), the
+    slice-group kernel and the oracle agree bit for bit over 6 sweeps (messages through the
+    marginals and the change history; every row of 8..64 edges and both walk paths)."""
+    from oracle import oracle
+    oracle.build()
+    s = G.gen_random_sparse(1 << 20, 16, 0).system
+    kw = dict(schedule="parallel", epsilon=1e-300, max_iter=6, record_means_history=False)
+    a = G.solve(s, G.SolveOptions(**kw))
+    b = G.solve(s, G.SolveOptions(gather_mode="slice", **kw))
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    o = oracle.solve(og, schedule="parallel", epsilon=1e-300, max_iter=6)
+    assert a.iterations == b.iterations == o.iterations == 6
+    np.testing.assert_array_equal(_bits(a.means), _bits(o.means))
+    np.testing.assert_array_equal(_bits(b.means), _bits(o.means))
+    np.testing.assert_array_equal(_bits(a.precisions), _bits(o.precisions))
+    np.testing.assert_array_equal(_bits(np.asarray(a.max_change_history)),
+                                  _bits(o.max_change_history))
+    np.testing.assert_allclose(a.residual_history, o.residual_history, rtol=1e-9, atol=0)
+
+
+def test_cluster_solve_reproducible_20_runs():
+    """The one-launch cluster solve (remote shared-memory stores, cluster barriers): 20 runs
+    of config 0 on both schedules give the same bits."""
+    s = G.gen_poisson2d(32, 0).system
+    g = G.build_graph(s)
+    try:
+        for sched in ("broadcast", "parallel"):
+            opts = G.SolveOptions(schedule=sched, epsilon=1e-300, rel_residual_tol=1e-8,
+                                  record_means_history=False)
+            runs = [G.solve_graph(g, opts) for _ in range(20)]
+            a = runs[0]
+            assert a.kernel_launches == 1 and a.converged
+            for b in runs[1:]:
+                assert b.iterations == a.iterations
+                np.testing.assert_array_equal(_bits(b.means), _bits(a.means))
+                np.testing.assert_array_equal(_bits(b.residual_history),
+                                              _bits(a.residual_history))
+                np.testing.assert_array_equal(_bits(b.max_change_history),
+                                              _bits(a.max_change_history))
+    finally:
+        g.close()
 
 
 def test_probe_and_poll_modes_reproducible():
