@@ -1031,6 +1031,23 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         d.npairs = G->dnpairs;
         SweepArgs a = make_args(G);
         const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : 8;
+        if (!getenv("GABP_DENSE_TWO_KERNELS")) {
+            // one fused kernel per sweep (dense.cu: dense_fused_kernel), decision of sweep
+            // s-1 in launch s like the diagonal layout
+            CK(gabp::launch_dense_fused_init(a, d, st));
+            const int64_t dtotal = opt->max_iter + 2;
+            G->kernels_launched = 1;
+            CK(cudaEventRecord(G->ev[2], st));
+            while (launched < dtotal) {
+                const int64_t k = dtotal - launched < C ? dtotal - launched : C;
+                for (int64_t q = 0; q < k; ++q) CK(gabp::launch_dense_fused_sweep(a, d, st));
+                launched += k;
+                G->kernels_launched += k;
+                if (P.after_chunk(st, &rc)) break;
+                if (rc) return rc;
+            }
+            return finish_loop(G, device_ms);
+        }
         CK(cudaEventRecord(G->ev[2], st));
         while (launched < total) {
             const int64_t k = total - launched < C ? total - launched : C;

@@ -535,6 +535,207 @@ __global__ void __launch_bounds__(kPairCta) dense_pair_kernel(const SweepArgs a,
     }
 }
 
+// ---- fused dense sweep: one kernel per sweep -----------------------------------------------
+// The column walk and the pair tiles read every old message twice and A twice (970 MB of DRAM
+// per sweep at K = 4096 against 798 MB algorithmic) in two launches.  Here one CTA owns a
+// block J of 32 receivers and walks the sender blocks I = 0, 1, ... in ascending order; for
+// the tile (I, J) it forms the NEW incoming messages of its receivers,
+//   m_{k -> j} = (-A_kj^2 / (P_k - P_jk), (P_k x_k - P_jk mu_jk) / A_kj)     (solver.py:247-257)
+// from the sender's aggregate {P_k, x_k} of S_{s-1} and the twin message m_{j -> k} -- the
+// tile (J, I) read transposed -- writes them, takes the change statistic against the old tile
+// (I, J), and hands them to a summing warp that adds them to the receivers' sums in ascending
+// sender order (np.add.at order) together with the residual row terms A_kj x_k.  So a launch
+// computes S_s, its aggregates and marginals x^{(s)}, the residual of x^{(s-1)} and decides
+// sweep s-1 (the diagonal layout's protocol, dia_epilogue): per edge 16 B written, A once,
+// and the old message twice -- as tile (I, J) by block J and as tile (J, I) by block I, which
+// walk towards each other's tile at the same pace, so part of the second touches hit L2.
+//   warps 0..7   message warps: rows 4 w .. 4 w + 3 of the tile, lane = receiver; tiles
+//                staged by cp.async (L1 bypass), three tiles in flight
+//   warp 8       summing warp, one tile behind: lane = receiver, 32 dependent adds per tile
+constexpr int kFusedMsgWarps = 16;
+constexpr int kFusedThreads = 32 * (kFusedMsgWarps + 1);
+constexpr int kFusedStages = 4;
+struct __align__(16) FusedStage {
+    double2 own[kTile][kTile];      // M^{(s-1)}[I][J]: the old messages k -> j
+    double2 twin[kTile][kTile + 1]; // M^{(s-1)}[J][I]: the twin messages j -> k (read [j][k])
+    double A[kTile][kTile];         // A[I][J]
+    double P[kTile], X[kTile];      // aggregates of the senders: P_k, x_k of S_{s-1}
+};
+struct __align__(16) FusedOut {
+    double2 pn[kTile][kTile];       // new message as {P, P mu} (the sums' terms)
+    double ax[kTile][kTile];        // A_kj x_k (residual row terms)
+};
+struct FusedSmem {
+    FusedStage st[kFusedStages];
+    FusedOut out[2];
+    TailSmem<kFusedThreads / 32> tail;
+    double srsq[kFusedThreads / 32];
+    unsigned sasing[kFusedThreads / 32];
+    int64_t sweep;
+    int skip;
+};
+
+__device__ __forceinline__ void cpa8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s_u32(dst)), "l"(src));
+}
+
+__device__ __forceinline__ void fused_stage(FusedStage &F, int64_t I, int64_t J,
+                                            const DenseArgs &d, const double2 *M,
+                                            const double *P, const double *X, int tid) {
+    const int64_t ld = d.ld, i0 = I * kTile, j0 = J * kTile;
+    {  // one double2 per copy: rows tid / 32 + 8 m, column tid % 32
+        const int r0 = tid >> 5, c = tid & 31;
+        const double2 *gown = M + (i0 + r0) * ld + j0 + c, *gtw = M + (j0 + r0) * ld + i0 + c;
+        const int64_t step = (int64_t)kFusedMsgWarps * ld;
+#pragma unroll
+        for (int m = 0; m < kTile / kFusedMsgWarps; ++m) {
+            cpa16(&F.own[r0 + m * kFusedMsgWarps][c], gown + m * step);
+            cpa16(&F.twin[r0 + m * kFusedMsgWarps][c], gtw + m * step);
+        }
+    }
+    {  // two doubles per copy
+        constexpr int RPP = 32 * kFusedMsgWarps / 16;  // rows per pass
+        const int r0 = tid >> 4, c = (tid & 15) * 2;
+        const double *ga = d.A + (i0 + r0) * ld + j0 + c;
+#pragma unroll
+        for (int m = 0; m < kTile / RPP; ++m)
+            cpa16(&F.A[r0 + m * RPP][c], ga + (int64_t)m * RPP * ld);
+    }
+    if (tid < kTile) {  // (rows past K: padding, their A is zero)
+        if (i0 + tid < d.K) {
+            cpa8(&F.P[tid], P + i0 + tid);
+            cpa8(&F.X[tid], X + i0 + tid);
+        } else {
+            F.P[tid] = 0.0;
+            F.X[tid] = 0.0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kFusedThreads, 1) dense_fused_kernel(const SweepArgs a,
+                                                                      const DenseArgs d) {
+    extern __shared__ __align__(16) unsigned char fused_raw[];
+    FusedSmem &S = *reinterpret_cast<FusedSmem *>(fused_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    Ctrl *ctrl = a.ctrl;
+    if (tid == 0) {
+        volatile Ctrl *vc = ctrl;
+        const int64_t s = vc->next_sweep;
+        S.skip = vc->done || s > vc->max_iter + 1;
+        S.sweep = s;
+    }
+    __syncthreads();
+    if (S.skip) return;
+    const int64_t s = S.sweep;
+    const int64_t K = d.K, ld = d.ld, nt = ld / kTile;
+    const double2 *M = d.msg[(s - 1) % 3];
+    double2 *Mo = d.msg[s % 3];
+    const double *Po = a.p[(s - 1) % 3], *Xo = a.x[(s - 1) % 3];
+    const bool resid = s >= 2;
+    const int64_t J = blockIdx.x, j0 = J * kTile;
+    const int64_t j = j0 + lane;
+    const bool msgw = warp < kFusedMsgWarps;
+    Stats st;
+    st.lim = fmin(ctrl->blowup, DBL_MAX);
+    unsigned asing = 0xffffffffu;
+    // summing warp: the receiver's running sums (prior first, solver.py:239-243)
+    double sp = 0.0, sn = 0.0, y = 0.0;
+    if (!msgw && j < K) {
+        const NodeRec nd = a.nd[j];
+        sp = nd.diag;
+        sn = nd.pnum;
+    }
+    if (msgw) {
+#pragma unroll
+        for (int q = 0; q < kFusedStages - 1; ++q) {
+            if (q < nt) fused_stage(S.st[q], q, J, d, M, Po, Xo, tid);
+            cpa_commit();
+        }
+    }
+    for (int64_t t = 0; t <= nt; ++t) {
+        if (msgw) cpa_wait<kFusedStages - 2>();  // tile t has landed (this thread's copies)
+        __syncthreads();  // ... everybody's; out[(t-1) & 1] complete; out[t & 1] and the
+                          // stage of tile t - 1 are free
+        if (msgw) {
+            if (t + kFusedStages - 1 < nt)
+                fused_stage(S.st[(t + kFusedStages - 1) % kFusedStages], t + kFusedStages - 1, J,
+                            d, M, Po, Xo, tid);
+            cpa_commit();
+            if (t < nt) {
+                const FusedStage &F = S.st[t % kFusedStages];
+                FusedOut &O = S.out[t & 1];
+                const int64_t i0 = t * kTile;
+#pragma unroll
+                for (int r = 0; r < kTile / kFusedMsgWarps; ++r) {
+                    const int k = warp * (kTile / kFusedMsgWarps) + r;
+                    const int64_t kk = i0 + k;
+                    const double c = F.A[k][lane];
+                    const double pk = F.P[k], xk = F.X[k];
+                    const bool edge = c != 0.0 && kk != j && kk < K && j < K;
+                    double2 nw = make_double2(-0.0, 0.0);  // non-edges keep (-0, +0)
+                    if (edge) {
+                        const double2 tw = F.twin[lane][k], old = F.own[k][lane];
+                        const double pe = pk - tw.x;
+                        const double num = pk * xk - tw.x * tw.y;  // (sum_p * mu_tilde) - ...
+                        const double cc = -c * c;                  // (-coeff * coeff)
+                        bool okp, okm;
+                        double np_ = ddiv_fast(cc, pe, okp);
+                        double nm = ddiv_fast(num, c, okm);
+                        if (!okp) np_ = div_slow(cc, pe);
+                        if (!okm) nm = div_slow(num, c);
+                        nw = make_double2(np_, nm);
+                        const double d1 = fabs(np_ - old.x), d2 = fabs(nm - old.y);
+                        st.chg = fmax(st.chg, fmax(d1, d2));
+                        if (!(fabs(np_) <= st.lim) || !(fabs(nm) <= st.lim))
+                            st.out_of_range |= (np_ != np_ || nm != nm) ? 3u : 1u;
+                        if (pe == 0.0) st.sing = min(st.sing, (unsigned)(kk * K + j));
+                    }
+                    __stcs(Mo + kk * ld + j, nw);
+                    O.pn[k][lane] = make_double2(nw.x, nw.x * nw.y);  // (prec * mean)
+                    O.ax[k][lane] = c * (kk < K ? xk : 0.0);  // (the diagonal term included)
+                }
+            }
+        } else if (t >= 1) {  // summing warp: tile t - 1, ascending senders
+            const FusedOut &O = S.out[(t - 1) & 1];
+#pragma unroll 8
+            for (int k = 0; k < kTile; ++k) {
+                const double2 v = O.pn[k][lane];
+                sp = sp + v.x;
+                sn = sn + v.y;
+                y = y + O.ax[k][lane];
+            }
+        }
+    }
+    if (!msgw && j < K) {  // aggregates and marginal of S_s, residual row of x^{(s-1)}
+        bool ok;
+        double x = ddiv_fast(sn, sp, ok);
+        if (!ok) x = div_slow(sn, sp);
+        if (sp == 0.0) asing = (unsigned)j;  // (singular for sweep s + 1)
+        if (!(fabs(x) <= DBL_MAX)) st.means_bad = 1u;
+        a.p[s % 3][j] = sp;
+        a.x[s % 3][j] = x;
+        if (a.xhist && s >= 1 && s <= a.xhist_rows) a.xhist[(s - 1) * a.n + j] = x;
+        if (resid) {
+            const double r = y - a.rhs[j];
+            st.rsq = r * r;
+        }
+    }
+    if (msgw) cpa_wait<0>();
+    __syncthreads();
+    dia_epilogue<kFusedThreads, true>(S.tail, S.srsq, S.sasing, a, s, st, asing, 0u, tid);
+}
+
+// aggregates and marginals of S_0 (all messages zero): P_i = A_ii, x_i = A_ii mu_ii / A_ii
+__global__ void dense_fused_init_kernel(const SweepArgs a, int64_t K) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K) return;
+    const NodeRec nd = a.nd[i];
+    // (the sums over S_0's +0 messages leave the prior: x + (+0) == x unless x is -0)
+    const double P = nd.diag + 0.0, N = nd.pnum + 0.0;
+    a.p[0][i] = P;
+    a.x[0][i] = N / P;
+}
+
 int g_pair_grid = 0;
 
 // Tensor maps of the current dense buffers (re-encoded when the buffers change).
@@ -587,6 +788,24 @@ cudaError_t launch_dense_mask(const double *A, int64_t ld, uint32_t *emask, cuda
 cudaError_t launch_dense_init(const uint32_t *emask, int64_t ld, double2 *msg, cudaStream_t st) {
     const int64_t n = ld * ld;
     dense_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(emask, ld, msg);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_fused_init(const SweepArgs &a, const DenseArgs &d, cudaStream_t st) {
+    dense_fused_init_kernel<<<(unsigned)((d.K + 255) / 256), 256, 0, st>>>(a, d.K);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_fused_sweep(const SweepArgs &a, const DenseArgs &d, cudaStream_t st) {
+    static bool ready = false;
+    if (!ready) {
+        cudaError_t e = cudaFuncSetAttribute(dense_fused_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(FusedSmem));
+        if (e != cudaSuccess) return e;
+        ready = true;
+    }
+    dense_fused_kernel<<<(unsigned)(d.ld / kTile), kFusedThreads, sizeof(FusedSmem), st>>>(a, d);
     return cudaGetLastError();
 }
 

@@ -352,6 +352,9 @@ struct DenseArgs {
     const uint32_t *emask;  // [ld/32][ld]: bit l of word (cb, k) = A[k][32 cb + l] is an edge
 };
 cudaError_t launch_dense_sweep(const SweepArgs &a, const DenseArgs &d, cudaStream_t st);
+// one kernel per sweep (dense_fused_kernel): launch protocol of the diagonal layout
+cudaError_t launch_dense_fused_init(const SweepArgs &a, const DenseArgs &d, cudaStream_t st);
+cudaError_t launch_dense_fused_sweep(const SweepArgs &a, const DenseArgs &d, cudaStream_t st);
 cudaError_t launch_dense_mask(const double *A, int64_t ld, uint32_t *emask, cudaStream_t st);
 cudaError_t launch_dense_init(const uint32_t *emask, int64_t ld, double2 *msg, cudaStream_t st);
 
