@@ -579,37 +579,50 @@ __device__ __forceinline__ void cpa8(void *dst, const void *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s_u32(dst)), "l"(src));
 }
 
-__device__ __forceinline__ void fused_stage(FusedStage &F, int64_t I, int64_t J,
-                                            const DenseArgs &d, const double2 *M,
-                                            const double *P, const double *X, int tid) {
-    const int64_t ld = d.ld, i0 = I * kTile, j0 = J * kTile;
-    {  // one double2 per copy: rows tid / 32 + 8 m, column tid % 32
+// Per-thread source pointers of the tile copies, advanced tile by tile (the sender block
+// moves down the rows of the own and A tiles and along the columns of the twin tile).
+struct FusedSrc {
+    const double2 *own, *twin;
+    const double *A, *P, *X;
+    int64_t k0;  // first sender row of the next tile to stage
+};
+__device__ __forceinline__ void fused_stage(FusedStage &F, FusedSrc &g, int64_t ld, int64_t K,
+                                            int tid) {
+    {  // one double2 per copy: rows tid / 32 + kFusedMsgWarps m, column tid % 32
         const int r0 = tid >> 5, c = tid & 31;
-        const double2 *gown = M + (i0 + r0) * ld + j0 + c, *gtw = M + (j0 + r0) * ld + i0 + c;
         const int64_t step = (int64_t)kFusedMsgWarps * ld;
 #pragma unroll
         for (int m = 0; m < kTile / kFusedMsgWarps; ++m) {
-            cpa16(&F.own[r0 + m * kFusedMsgWarps][c], gown + m * step);
-            cpa16(&F.twin[r0 + m * kFusedMsgWarps][c], gtw + m * step);
+            cpa16(&F.own[r0 + m * kFusedMsgWarps][c], g.own + m * step);
+            cpa16(&F.twin[r0 + m * kFusedMsgWarps][c], g.twin + m * step);
         }
     }
     {  // two doubles per copy
         constexpr int RPP = 32 * kFusedMsgWarps / 16;  // rows per pass
         const int r0 = tid >> 4, c = (tid & 15) * 2;
-        const double *ga = d.A + (i0 + r0) * ld + j0 + c;
+        if (RPP >= kTile) {
+            if (r0 < kTile) cpa16(&F.A[r0][c], g.A);
+        } else {
 #pragma unroll
-        for (int m = 0; m < kTile / RPP; ++m)
-            cpa16(&F.A[r0 + m * RPP][c], ga + (int64_t)m * RPP * ld);
+            for (int m = 0; m < (kTile / RPP > 0 ? kTile / RPP : 1); ++m)
+                cpa16(&F.A[r0 + m * RPP][c], g.A + (int64_t)m * RPP * ld);
+        }
     }
     if (tid < kTile) {  // (rows past K: padding, their A is zero)
-        if (i0 + tid < d.K) {
-            cpa8(&F.P[tid], P + i0 + tid);
-            cpa8(&F.X[tid], X + i0 + tid);
+        if (g.k0 + tid < K) {
+            cpa8(&F.P[tid], g.P);
+            cpa8(&F.X[tid], g.X);
         } else {
             F.P[tid] = 0.0;
             F.X[tid] = 0.0;
         }
     }
+    g.own += (int64_t)kTile * ld;
+    g.twin += kTile;
+    g.A += (int64_t)kTile * ld;
+    g.P += kTile;
+    g.X += kTile;
+    g.k0 += kTile;
 }
 
 __global__ void __launch_bounds__(kFusedThreads, 1) dense_fused_kernel(const SweepArgs a,
@@ -645,10 +658,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1) dense_fused_kernel(const Swe
         sp = nd.diag;
         sn = nd.pnum;
     }
+    FusedSrc src;
+    src.own = M + (int64_t)(tid >> 5) * ld + j0 + (tid & 31);
+    src.twin = M + (j0 + (tid >> 5)) * ld + (tid & 31);
+    src.A = d.A + (int64_t)(tid >> 4) * ld + j0 + (tid & 15) * 2;
+    src.P = Po + (tid & 31);
+    src.X = Xo + (tid & 31);
+    src.k0 = 0;
+    const bool jin = j < K;
     if (msgw) {
 #pragma unroll
         for (int q = 0; q < kFusedStages - 1; ++q) {
-            if (q < nt) fused_stage(S.st[q], q, J, d, M, Po, Xo, tid);
+            if (q < nt) fused_stage(S.st[q], src, ld, K, tid);
             cpa_commit();
         }
     }
@@ -658,20 +679,21 @@ __global__ void __launch_bounds__(kFusedThreads, 1) dense_fused_kernel(const Swe
                           // stage of tile t - 1 are free
         if (msgw) {
             if (t + kFusedStages - 1 < nt)
-                fused_stage(S.st[(t + kFusedStages - 1) % kFusedStages], t + kFusedStages - 1, J,
-                            d, M, Po, Xo, tid);
+                fused_stage(S.st[(t + kFusedStages - 1) % kFusedStages], src, ld, K, tid);
             cpa_commit();
             if (t < nt) {
                 const FusedStage &F = S.st[t % kFusedStages];
                 FusedOut &O = S.out[t & 1];
                 const int64_t i0 = t * kTile;
+                const bool diag = t == J;  // (the tile holds the non-edges k == j)
+                const int rmax = (int)(K - i0 < kTile ? K - i0 : kTile);  // sender rows < K
+                double2 *orow = Mo + (i0 + warp * (kTile / kFusedMsgWarps)) * ld + j;
 #pragma unroll
                 for (int r = 0; r < kTile / kFusedMsgWarps; ++r) {
                     const int k = warp * (kTile / kFusedMsgWarps) + r;
-                    const int64_t kk = i0 + k;
                     const double c = F.A[k][lane];
                     const double pk = F.P[k], xk = F.X[k];
-                    const bool edge = c != 0.0 && kk != j && kk < K && j < K;
+                    const bool edge = c != 0.0 && jin && k < rmax && !(diag && k == lane);
                     double2 nw = make_double2(-0.0, 0.0);  // non-edges keep (-0, +0)
                     if (edge) {
                         const double2 tw = F.twin[lane][k], old = F.own[k][lane];
@@ -681,18 +703,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) dense_fused_kernel(const Swe
                         bool okp, okm;
                         double np_ = ddiv_fast(cc, pe, okp);
                         double nm = ddiv_fast(num, c, okm);
-                        if (!okp) np_ = div_slow(cc, pe);
-                        if (!okm) nm = div_slow(num, c);
+                        if (!(okp && okm)) {  // (rare: a quotient outside the fast path's range)
+                            np_ = div_slow(cc, pe);
+                            nm = div_slow(num, c);
+                        }
                         nw = make_double2(np_, nm);
                         const double d1 = fabs(np_ - old.x), d2 = fabs(nm - old.y);
                         st.chg = fmax(st.chg, fmax(d1, d2));
                         if (!(fabs(np_) <= st.lim) || !(fabs(nm) <= st.lim))
                             st.out_of_range |= (np_ != np_ || nm != nm) ? 3u : 1u;
-                        if (pe == 0.0) st.sing = min(st.sing, (unsigned)(kk * K + j));
+                        if (pe == 0.0) st.sing = min(st.sing, (unsigned)((i0 + k) * K + j));
                     }
-                    __stcs(Mo + kk * ld + j, nw);
+                    __stcs(orow + (int64_t)r * ld, nw);
                     O.pn[k][lane] = make_double2(nw.x, nw.x * nw.y);  // (prec * mean)
-                    O.ax[k][lane] = c * (kk < K ? xk : 0.0);  // (the diagonal term included)
+                    O.ax[k][lane] = c * xk;  // (the diagonal term included; padding: 0 * 0)
                 }
             }
         } else if (t >= 1) {  // summing warp: tile t - 1, ascending senders
