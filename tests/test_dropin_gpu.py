@@ -322,3 +322,34 @@ def test_partitions_on_the_diagonal_layout(kind, nparts):
     np.testing.assert_array_equal(part.precisions, one.precisions)
     np.testing.assert_array_equal(np.asarray(part.max_change_history),
                                   np.asarray(one.max_change_history))
+
+
+# ---- packed index upload (gabp_graph_create: 32-bit indices over the link) ---------------
+
+def test_packed_index_upload_builds_the_same_graph(monkeypatch):
+    """Systems of >= 2^20 pairs send their int64 pair indices packed to 32 bits (host
+    threads, chunked under the copies) and widen them on the device: the graph is the one
+    the plain upload builds, element for element."""
+    s = G.gen_random_sparse(1 << 17, 16, 5).system
+    assert s.pair_v.size >= 1 << 20
+    g1 = G.build_graph(s)
+    monkeypatch.setenv("GABP_NO_PACK", "1")
+    g2 = G.build_graph(s)
+    try:
+        for name in ("src", "dst", "rev", "coeff"):
+            np.testing.assert_array_equal(getattr(g1, name), getattr(g2, name), err_msg=name)
+    finally:
+        g1.close()
+        g2.close()
+
+
+@pytest.mark.parametrize("bad", [-1, 1 << 40])
+def test_packed_index_upload_rejects_bad_indices_like_the_plain_one(bad):
+    """An index that does not fit 32 bits leaves the packed path; the device validation
+    reports it exactly as for a small system."""
+    s = G.gen_random_sparse(1 << 17, 16, 5).system
+    pi = s.pair_i.copy()
+    pi[12345] = bad
+    t = G.SymSystem.from_pairs(s.diag, pi, s.pair_j, s.pair_v, s.rhs, validate=False)
+    with pytest.raises(ValueError, match="bad off-diagonal"):
+        G.build_graph(t)
