@@ -917,7 +917,7 @@ cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st) {
     if (a.ntiles <= 0) return cudaSuccess;
     const int m = mode == kModeSolve ? kModeSolve : kModeSingle;
     const int dv = cur_dev();
-    static const bool quad = !getenv("GABP_ROW_NO_QUAD");
+    const bool quad = !getenv("GABP_ROW_NO_QUAD");
     if (quad) {
         int64_t grid = g_quad_grid[dv][m] > 0 ? g_quad_grid[dv][m] : 148 * 3;
         const int64_t need = (a.ntiles + kQWarps - 1) / kQWarps;

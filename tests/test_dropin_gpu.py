@@ -353,3 +353,55 @@ def test_packed_index_upload_rejects_bad_indices_like_the_plain_one(bad):
     t = G.SymSystem.from_pairs(s.diag, pi, s.pair_j, s.pair_v, s.rhs, validate=False)
     with pytest.raises(ValueError, match="bad off-diagonal"):
         G.build_graph(t)
+
+
+# ---- cross-check variants stay bitwise equal to the default kernels ----------------------
+
+def test_parallel_one_row_per_warp_equals_four_rows_per_warp(monkeypatch):
+    """GABP_ROW_NO_QUAD selects the round-1 warp-per-row kernel (rowpar_kernel): same bits
+    as rowquad_kernel on a graph with rows of 0..120 edges (the long-row path included)."""
+    rng = np.random.default_rng(3)
+    n = 20000
+    deg = np.minimum(rng.poisson(14, n) + (rng.random(n) < 0.01) * 90, 120)
+    pi = np.repeat(np.arange(n), deg)
+    pj = rng.integers(0, n, pi.size)
+    keep = pi != pj
+    lo, hi = np.minimum(pi[keep], pj[keep]), np.maximum(pi[keep], pj[keep])
+    key = np.unique(lo.astype(np.int64) * n + hi)
+    pi, pj = key // n, key % n
+    pv = rng.uniform(-1.0, 1.0, pi.size)
+    pv[pv == 0.0] = 0.5
+    absrow = np.bincount(pi, np.abs(pv), n) + np.bincount(pj, np.abs(pv), n)
+    s = G.SymSystem.from_pairs(1.2 * absrow + (absrow == 0), pi, pj, pv, rng.standard_normal(n))
+    kw = dict(schedule="parallel", gather_mode="rows", epsilon=1e-300, max_iter=12,
+              record_means_history=True)
+    a = G.solve(s, G.SolveOptions(**kw))
+    monkeypatch.setenv("GABP_ROW_NO_QUAD", "1")
+    b = G.solve(s, G.SolveOptions(**kw))
+    assert a.iterations == b.iterations == 12
+    for x, y in zip(a.means_history, b.means_history):
+        np.testing.assert_array_equal(_bits(x), _bits(y))
+    np.testing.assert_array_equal(_bits(np.asarray(a.max_change_history)),
+                                  _bits(np.asarray(b.max_change_history)))
+    np.testing.assert_array_equal(_bits(a.precisions), _bits(b.precisions))
+
+
+def test_dense_two_kernel_sweep_equals_fused_sweep(monkeypatch):
+    """GABP_DENSE_TWO_KERNELS selects the column walk + pair tiles: same trajectory as the
+    fused one-kernel sweep (K = 300: padded tiles, diagonal tiles, exact zeros of A)."""
+    s = G.gen_cdma_detection(512, 300, 0.5, 4)[0].system
+    kw = dict(schedule="broadcast", epsilon=1e-300, max_iter=25, record_means_history=True)
+    g = G.build_graph(s, dense=True)
+    try:
+        a = G.solve_graph(g, G.SolveOptions(**kw))
+        monkeypatch.setenv("GABP_DENSE_TWO_KERNELS", "1")
+        b = G.solve_graph(g, G.SolveOptions(**kw))
+    finally:
+        g.close()
+    assert (a.iterations, a.diverged) == (b.iterations, b.diverged)
+    assert len(a.means_history) == len(b.means_history)
+    for x, y in zip(a.means_history, b.means_history):
+        np.testing.assert_array_equal(_bits(x), _bits(y))
+    np.testing.assert_array_equal(_bits(np.asarray(a.max_change_history)),
+                                  _bits(np.asarray(b.max_change_history)))
+    np.testing.assert_allclose(a.residual_history, b.residual_history, rtol=1e-9, atol=0)
