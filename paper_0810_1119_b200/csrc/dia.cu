@@ -208,8 +208,11 @@ __global__ void __launch_bounds__(kDRows, GABP_DIA_MINB) dia_sweep_kernel(const 
 // the CSR kernels (sweep_epilogue, LAG 0): launch s reads S_{s-1}, writes S_s, forms the
 // marginals x^{(s-1)} of the state it read and the residual row of x^{(s-2)}, decides sweep
 // s-2.  Divisions: the fast path with its range test per division, IEEE '/' when it fails.
+// CTAs per SM: three for up to 4 diagonals (80 registers; Poisson 4096^2 0.718 -> 0.633 ms),
+// two for the wider stencils (three spill: 320^3 1.74 -> 2.32 ms)
+constexpr int dia_par_minb(int D) { return D <= 4 ? 3 : 2; }
 template <int D, bool UNIFORM>
-__global__ void __launch_bounds__(kDRows, GABP_DIA_MINB) dia_par_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(kDRows, dia_par_minb(D)) dia_par_kernel(const SweepArgs a) {
     __shared__ TailSmem<kDRows / 32> T;
     __shared__ int64_t s_sweep;
     __shared__ int s_skip;
@@ -553,7 +556,7 @@ void dia_launch_t(const SweepArgs &a, cudaStream_t st) {
 template <int D>
 void dia_par_launch_t(const SweepArgs &a, cudaStream_t st) {
     const int64_t nt = dia_ntiles(a);
-    int64_t grid = g_dia_grid > 0 ? g_dia_grid : 148 * 2;
+    int64_t grid = (g_dia_grid > 0 ? g_dia_grid : 148 * 2) / GABP_DIA_MINB * dia_par_minb(D);
     if (grid > nt) grid = nt > 0 ? nt : 1;
     if (a.dia_mask)
         dia_par_kernel<D, true><<<(unsigned)grid, kDRows, 0, st>>>(a);
