@@ -85,6 +85,11 @@ __device__ __forceinline__ double cl_ld(uint32_t addr) {
     asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned cl_ld_u32(uint32_t addr) {
+    unsigned v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
 // all threads of all CTAs; remote stores before it are visible after it
 __device__ __forceinline__ void cl_barrier() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
@@ -203,14 +208,6 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
             }
         }
     }
-    // partial-statistics slot [rank][warp] of CTA `lane` (lanes < C publish), table 0
-    const uint32_t pub = lane < C ? (uint32_t)lane : 0u;
-    const int wq = warp < kW ? warp : 0;
-    const uint32_t p_chg = cl_map(&red[0].chg[rank][wq], pub);
-    const uint32_t p_rsq = cl_map(&red[0].rsq[rank][wq], pub);
-    const uint32_t p_fl = cl_map(&red[0].fl[rank][wq], pub);
-    const uint32_t p_sing = cl_map(&red[0].sing[rank][wq], pub);
-    const uint32_t p_asing = cl_map(&red[0].asing[rank][wq], pub);
     cl_barrier();  // every CTA's buffers are initialised before a remote store can land
 
     // Iteration u, compute warps:  A(u): marginals of S_{u-1} into R[u % 3] and the residual
@@ -339,26 +336,29 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
             fl = warp_or(fl | (mbad << 2));
             sing = warp_min(sing);
             asing = warp_min(asing);
-            if (lane < C) {
-                const uint32_t tb = (uint32_t)bn * (uint32_t)sizeof(SmRed);
-                cl_st(p_chg + tb, chg);
-                cl_st(p_rsq + tb, rsq);
-                cl_st(p_fl + tb, fl);
-                cl_st(p_sing + tb, sing);
-                cl_st(p_asing + tb, asing);
+            if (lane == 0) {  // into this CTA's own table: the decision warps pull them
+                SmRed &Rw = red[bn];
+                Rw.chg[rank][warp] = chg;
+                Rw.rsq[rank][warp] = rsq;
+                Rw.fl[rank][warp] = fl;
+                Rw.sing[rank][warp] = sing;
+                Rw.asing[rank][warp] = asing;
             }
         } else if (u >= 2) {
             // ---- decision warp: table of iteration u-1 ----------------------------------
             const SmRed &R1 = red[(u - 1) & 1];
             double c_t = 0.0, rsq_p = 0.0;
             unsigned f = 0u, sg = 0xffffffffu, asg = 0xffffffffu;
+            // every CTA's warp partials, read from their owners (ld.shared::cluster; this
+            // warp is off the sweep's critical path, so the compute warps publish nothing
+            // remotely: 280 remote stores per CTA and sweep less before the cluster barrier)
             for (int idx = lane; idx < C * kW; idx += 32) {  // (cta, warp) order per lane
                 const int c = idx / kW, w = idx - c * kW;
-                c_t = fmax(c_t, R1.chg[c][w]);
-                rsq_p += R1.rsq[c][w];
-                f |= R1.fl[c][w];
-                sg = min(sg, R1.sing[c][w]);
-                asg = min(asg, R1.asing[c][w]);
+                c_t = fmax(c_t, cl_ld(cl_map(&R1.chg[c][w], (uint32_t)c)));
+                rsq_p += cl_ld(cl_map(&R1.rsq[c][w], (uint32_t)c));
+                f |= cl_ld_u32(cl_map(&R1.fl[c][w], (uint32_t)c));
+                sg = min(sg, cl_ld_u32(cl_map(&R1.sing[c][w], (uint32_t)c)));
+                asg = min(asg, cl_ld_u32(cl_map(&R1.asing[c][w], (uint32_t)c)));
             }
             c_t = warp_max(c_t);
             rsq_p = warp_sum(rsq_p);
