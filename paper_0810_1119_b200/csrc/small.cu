@@ -210,6 +210,20 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
     }
     cl_barrier();  // every CTA's buffers are initialised before a remote store can land
 
+    // When the CTA's rows fill at most half of its compute threads, the residual row of node
+    // il runs on thread il + NT / 2, beside the thread that sums the node's messages: the
+    // node phase is the stretch every other warp waits for at the CTA barrier.
+    const bool split = NPT == 1 && nloc <= (uint32_t)(NT / 2);
+    uint32_t rr_il = 0xffffffffu, rr_e0 = 0u, rr_e1 = 0u;
+    double rr_dg = 0.0, rr_rh = 0.0;
+    if (split && !decider && tid >= NT / 2 && (uint32_t)(tid - NT / 2) < nloc) {
+        rr_il = (uint32_t)(tid - NT / 2);
+        const uint32_t i = n0 + rr_il;
+        rr_e0 = __ldg(a.row_ptr + i) - e0;
+        rr_e1 = __ldg(a.row_ptr + i + 1) - e0;
+        rr_dg = __ldg(&a.nd[i].diag);
+        rr_rh = __ldg(a.rhs + i);
+    }
     // Iteration u, compute warps:  A(u): marginals of S_{u-1} into R[u % 3] and the residual
     // rows of x^{(u-2)} (R[(u-1) % 3], complete everywhere since the last cluster barrier);
     // CTA barrier; B(u): messages of S_u into the owners' slots, statistics published into
@@ -247,7 +261,7 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
                         const double2 v = Io[e];
                         P = P + v.x;
                         N = N + v.x * v.y;  // (prec * mean), solver.py:240
-                        if (u >= 3) y = y + sA[e] * cl_ld(sX[e] + x_off);
+                        if (!split && u >= 3) y = y + sA[e] * cl_ld(sX[e] + x_off);
                     }
                     DivRange dr;
                     double x = ddiv_fast_acc(N, P, dr);
@@ -256,11 +270,18 @@ __global__ void __launch_bounds__(NT + 32, 1) small_solve_kernel(const SweepArgs
                     if (!(fabs(x) <= DBL_MAX)) mbad = 1u;
                     sR[rn][il] = make_double2(P, x);
                     if (xh) xh[n0 + il] = x;
-                    if (u >= 3) {
+                    if (!split && u >= 3) {
                         const double r = y - nrh[q];
                         rsq += r * r;
                     }
                 }
+            }
+            if (split && u >= 3 && rr_il != 0xffffffffu) {  // residual row of x^{(u-2)}
+                double y = rr_dg * sR[rp][rr_il].y;
+#pragma unroll 4
+                for (uint32_t e = rr_e0; e < rr_e1; ++e) y = y + sA[e] * cl_ld(sX[e] + x_off);
+                const double r = y - rr_rh;
+                rsq += r * r;
             }
             asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");  // the compute warps' R[rn]
             // ---- B(u): messages of S_u, statistics --------------------------------------
