@@ -16,6 +16,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <omp.h>
 #include <vector>
 
 #include "gabp_internal.cuh"
@@ -1341,7 +1342,10 @@ int gabp_graph_create_ex(int64_t n, int64_t npairs, const double *h_diag, const 
     CK(cudaEventCreateWithFlags(&ev_idx, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_val, cudaEventDisableTiming));
     const size_t nb = sizeof(double) * n, pb = sizeof(int64_t) * (npairs > 0 ? npairs : 1);
-    bool pack = npairs >= (1 << 20) && n <= 0xffffffffll && !getenv("GABP_NO_PACK");
+    // (packing runs at host memory bandwidth only with several threads: a process limited
+    // to one or two -- torchrun exports OMP_NUM_THREADS=1 -- sends the int64 indices as is)
+    bool pack = npairs >= (1 << 20) && n <= 0xffffffffll && omp_get_max_threads() >= 4 &&
+                !getenv("GABP_NO_PACK");
     const size_t sbytes = 2 * nb + 3 * pb + (pack ? pb : 0);  // (+ two packed index arrays)
     char *buf = static_cast<char *>(spare_take(1, device, sbytes));
     cudaError_t e = buf ? cudaSuccess : cudaMallocAsync(&buf, sbytes, st);
