@@ -16,6 +16,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "gabp_internal.cuh"
 
@@ -182,6 +183,30 @@ struct Scratch {
     ~Scratch() { if (p) cudaFreeAsync(p, 0); }
 };
 
+
+// ---- binned message order (build_bins) -----------------------------------------------------
+__global__ void bin_key_kernel(int64_t E, const EdgeRec *er, uint32_t rows_per_bin,
+                               uint32_t *key, uint32_t *val) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        key[e] = er[e].col / rows_per_bin;
+        val[e] = (uint32_t)e;
+    }
+}
+__global__ void bin_pos_kernel(int64_t E, const uint32_t *sorted, uint32_t *pos) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E;
+         p += (int64_t)gridDim.x * blockDim.x)
+        pos[sorted[p]] = (uint32_t)p;
+}
+__global__ void bin_rec_kernel(int64_t E, const EdgeRec *er, const uint32_t *pos, EdgeRec *erb) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        EdgeRec r = er[e];
+        r.rev = pos[r.rev];
+        erb[e] = r;
+    }
+}
+
 #define BCHECK(call)                                                                   \
     do {                                                                               \
         cudaError_t _e = (call);                                                       \
@@ -218,6 +243,8 @@ void free_graph(DeviceGraph &g, cudaStream_t st) {
     if (g.scol) cudaFreeAsync(g.scol, st);
     if (g.scoef) cudaFreeAsync(g.scoef, st);
     if (g.stwin) cudaFreeAsync(g.stwin, st);
+    if (g.erb) cudaFreeAsync(g.erb, st);
+    if (g.gout) cudaFreeAsync(g.gout, st);
     g = DeviceGraph{};
 }
 
@@ -468,6 +495,71 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
         if (rc != GABP_OK) return rc;
     }
     return compute_priors(g, st, err, errlen);
+}
+
+// Binned message order of the four-rows-per-warp parallel kernel (rowpar.cu: rowquad_kernel).
+// In CSR order a row's twin messages are spread over the whole message array: every 16-byte
+// gather costs a 128-byte line of DRAM.  Here the message of edge i -> j lives at
+// pos(i -> j) = rank of the edge in the order (bin of j, i, j), bin = j / rows_per_bin: the
+// rows of one bin gather all their incoming messages from one window of E / bins messages
+// (a few MB: every line comes from DRAM once and serves its 8 gathers from L2), and rows
+// swept in ascending order write each bin's messages as an ascending run (lines fill in L2
+// within a few rows).  gout[e] = pos(e), erb[e].rev = pos(rev(e)).
+int build_bins(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
+    if (g.bins != 0) return GABP_OK;
+    g.bins = -1;
+    const int64_t E = g.E;
+    const char *wenv = getenv("GABP_BIN_WINDOW_MB");
+    const double window = (wenv ? atof(wenv) : 48.0) * 1048576.0;
+    // messages that fit L2 anyway, partial graphs, ids past 31 bits: CSR order
+    if (E <= 0 || E >= (1ll << 31) || g.row_lo != 0 || g.row_hi != g.n ||
+        16.0 * (double)E < 6.0 * window || window <= 0.0)
+        return GABP_OK;
+    int64_t nb = (int64_t)(16.0 * (double)E / window + 0.999);
+    if (nb > 4096) nb = 4096;
+    if (nb < 2) return GABP_OK;
+    const uint32_t rpb = (uint32_t)((g.n + nb - 1) / nb);
+    int bits = 1;
+    while ((1ll << bits) < nb) ++bits;
+    uint32_t *key = nullptr, *val = nullptr;
+    void *tmp = nullptr;
+    auto body = [&]() -> cudaError_t {
+        cudaError_t e;
+        size_t tb = 0;
+        if ((e = cudaMallocAsync(&key, sizeof(uint32_t) * 2 * E, st)) != cudaSuccess) return e;
+        if ((e = cudaMallocAsync(&val, sizeof(uint32_t) * 2 * E, st)) != cudaSuccess) return e;
+        bin_key_kernel<<<grid_for(E), 256, 0, st>>>(E, g.er, rpb, key, val);
+        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key + E, val, val + E, E, 0,
+                                                 bits, st)) != cudaSuccess)
+            return e;
+        if ((e = cudaMallocAsync(&tmp, tb, st)) != cudaSuccess) return e;
+        if ((e = cub::DeviceRadixSort::SortPairs(tmp, tb, key, key + E, val, val + E, E, 0, bits,
+                                                 st)) != cudaSuccess)
+            return e;
+        if ((e = cudaMallocAsync(&g.gout, sizeof(uint32_t) * E, st)) != cudaSuccess) return e;
+        if ((e = cudaMallocAsync(&g.erb, sizeof(EdgeRec) * E, st)) != cudaSuccess) return e;
+        bin_pos_kernel<<<grid_for(E), 256, 0, st>>>(E, val + E, g.gout);
+        bin_rec_kernel<<<grid_for(E), 256, 0, st>>>(E, g.er, g.gout, g.erb);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        return cudaStreamSynchronize(st);
+    };
+    const cudaError_t e = body();
+    if (tmp) cudaFreeAsync(tmp, st);
+    if (key) cudaFreeAsync(key, st);
+    if (val) cudaFreeAsync(val, st);
+    if (e != cudaSuccess) {
+        // (out of memory: the solve runs in CSR order; anything else is reported)
+        if (g.gout) cudaFreeAsync(g.gout, st);
+        if (g.erb) cudaFreeAsync(g.erb, st);
+        g.gout = nullptr;
+        g.erb = nullptr;
+        cudaGetLastError();
+        if (e == cudaErrorMemoryAllocation) return GABP_OK;
+        snprintf(err, errlen, "build_bins: %s", cudaGetErrorString(e));
+        return GABP_ECUDA;
+    }
+    g.bins = (int)nb;
+    return GABP_OK;
 }
 
 }  // namespace gabp

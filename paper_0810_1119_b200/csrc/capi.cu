@@ -461,6 +461,10 @@ SweepArgs make_args(gabp_graph *G) {
     a.scol = g.scol;
     a.scoef = g.scoef;
     a.stwin = g.stwin;
+    if (g.bins > 0 && !getenv("GABP_ROW_NO_BIN")) {  // (A/B: CSR message order)
+        a.erb = g.erb;
+        a.gout = g.gout;
+    }
     a.sl_lo = 0;
     a.sl_hi = g.nslices;
     a.part_base = 0;
@@ -1123,6 +1127,12 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         rc = gabp::build_stwin(G->g, st, g_err, sizeof(g_err));
         if (rc) return rc;
         G->ws_gen++;  // captured sweeps hold the slot pointers
+    }
+    if (gather == gabp::kGatherRowParallel && G->g.bins == 0 && !G->dist) {
+        // four rows per warp: messages in binned order when they exceed L2 (build_bins)
+        rc = gabp::build_bins(G->g, st, g_err, sizeof(g_err));
+        if (rc) return rc;
+        G->ws_gen++;  // captured sweeps hold the index pointers
     }
     G->slice_order = gather == gabp::kGatherSlice || gather == gabp::kGatherSliceParallel;
     const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
@@ -2461,6 +2471,12 @@ int gabp_bench_sweeps(gabp_graph_t *G, int32_t schedule, int32_t gather_mode, in
         G->ws_gen++;
     }
     a.stwin = G->g.stwin;
+    if (gather == gabp::kGatherRowParallel && G->g.bins == 0 && !G->dist) {
+        rc = gabp::build_bins(G->g, st, g_err, sizeof(g_err));
+        if (rc) return rc;
+        G->ws_gen++;
+        a = make_args(G);
+    }
     // launches 1-3 stream less than a full sweep (zero initial messages, slice.cu launch
     // kinds): run them untimed, so the figure is the steady-state sweep
     for (int k = 0; k < 3; ++k) CK(gabp::launch_sweep(a, schedule, gabp::kModeSolve, gather, st));

@@ -186,6 +186,10 @@ struct SweepArgs {
     const uint32_t *scol;      // position of the destination, per slot
     const double *scoef;       // A_ij per slot
     const uint32_t *stwin;     // slot of the twin message (parallel schedule), per slot
+    // binned message order of the four-rows-per-warp parallel kernel (rowpar.cu:
+    // build_bins; null: messages in CSR order)
+    const EdgeRec *erb;        // edge records whose rev field is the twin message's position
+    const uint32_t *gout;      // position of the edge's own message
     int probe;                 // residual probe: 0 off, 1 run by the exact twin, 2 as a
                                // residual-only group launch (probe_next)
     int probe_force;           // test hook (GABP_PROBE_FORCE=1): request a probe after every
@@ -440,6 +444,10 @@ struct DeviceGraph {
     uint32_t *scol = nullptr;
     double *scoef = nullptr;
     uint32_t *stwin = nullptr;  // built on the first parallel-schedule solve (build_stwin)
+    // binned message order (rowpar.cu: build_bins), built on the first solve that uses it
+    EdgeRec *erb = nullptr;
+    uint32_t *gout = nullptr;
+    int bins = 0;               // 0: not tried, -1: not worth it (messages fit L2), else count
     // diagonal layout (build_dia, dia.cu); dia_D == 0 when the graph is not a stencil
     int dia_D = 0;
     int64_t dia_nlc = 0, dia_O = 0, dia_W = 0;
@@ -469,6 +477,8 @@ cudaError_t launch_slice_boundary(const SweepArgs &a, int64_t *grid, cudaStream_
 // parallel schedule over the slice groups (slice.cu); build_stwin first
 cudaError_t launch_slice_parallel(const SweepArgs &a, cudaStream_t st);
 int build_stwin(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
+// binned message order for rowquad_kernel (rowpar.cu); g.bins < 0 afterwards: not used
+int build_bins(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen);
 cudaError_t refresh_slice_nodes(const DeviceGraph &g, cudaStream_t st);
 cudaError_t slice_to_rows(const DeviceGraph &g, int64_t lo, int64_t cnt, const double *in,
                           int stride, double *out, cudaStream_t st);

@@ -53,6 +53,10 @@ struct RowCtx {
     double *xcur, *pcur, *xh;
     bool resid;
     uint64_t pol;         // L2 evict-first
+    // binned message order (build_bins): edge records whose rev field is the position of the
+    // twin message, and the position of the edge's own message; null: CSR order
+    const EdgeRec *erb = nullptr;
+    const uint32_t *gout = nullptr;
 };
 
 // Streams (edge records, own old messages, twin gathers, new messages) are touched once per
@@ -79,6 +83,21 @@ __device__ __forceinline__ double2 ld_ef_d2(const double2 *ptr, uint64_t pol) {
 __device__ __forceinline__ void st_ef_d2(double2 *ptr, double2 v, uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;"
                  ::"l"(ptr), "d"(v.x), "d"(v.y), "l"(pol)
+                 : "memory");
+}
+
+// Binned message order: a gathered line serves 8 gathers, a written line fills from 8 rows --
+// the message traffic keeps the default L2 priority (only the once-read records stream).
+__device__ __forceinline__ double2 ld_na_d2(const double2 *ptr) {
+    double2 v;
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(ptr));
+    return v;
+}
+__device__ __forceinline__ void st_na_d2(double2 *ptr, double2 v) {
+    asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(ptr), "d"(v.x),
+                 "d"(v.y)
                  : "memory");
 }
 
@@ -110,14 +129,18 @@ __device__ __forceinline__ void row_node(const SweepArgs &a, const RowCtx &x, ui
     }
 }
 
-__device__ __forceinline__ void edge_out(const RowCtx &x, uint32_t e, double c, double pe,
-                                         double num, double2 old, Stats &st) {
+template <bool BIN = false>
+__device__ __forceinline__ void edge_out(const RowCtx &x, uint32_t e, uint32_t pos, double c,
+                                         double pe, double num, double2 old, Stats &st) {
     bool okp, okm;
     double np_ = ddiv_fast(-c * c, pe, okp);
     double nm = ddiv_fast(num, c, okm);
     if (!okp) np_ = div_slow(-c * c, pe);
     if (!okm) nm = div_slow(num, c);
-    st_ef_d2(x.mout + e, make_double2(np_, nm), x.pol);
+    if (BIN)
+        st_na_d2(x.mout + pos, make_double2(np_, nm));
+    else
+        st_ef_d2(x.mout + pos, make_double2(np_, nm), x.pol);
     st.edge(e, pe, np_, nm, old);
 }
 
@@ -204,7 +227,7 @@ __device__ __forceinline__ void row_walk(const SweepArgs &a, const RowCtx &x, co
     for (int u = 0; u < R; ++u) {
         const uint32_t j = lane + 32 * u;
         if (j < d) {
-            edge_out(x, g.e0 + j, g.c[u], p[u], n[u], g.o[u], st);
+            edge_out(x, g.e0 + j, g.e0 + j, g.c[u], p[u], n[u], g.o[u], st);
             if (j == d - 1)  // full sums: the last exclusion sum plus the last term
                 row_node<MODE>(a, x, g.i, p[u] + g.in[u].x, n[u] + g.in[u].x * g.in[u].y, st);
         }
@@ -252,9 +275,10 @@ __device__ void row_long(const SweepArgs &a, const RowCtx &x, double2 *T, uint32
                          uint32_t e0, uint32_t d, NodeRec nd, int lane, Stats &st) {
     const uint32_t dpad = (d + 7u) & ~7u;
     double yp = 0.0;
+    const EdgeRec *er = x.erb ? x.erb : a.er;
     for (uint32_t q = lane; q < dpad; q += 32) {
         if (q < d) {
-            const EdgeRec r = ld_er(a.er + e0 + q);
+            const EdgeRec r = ld_er(er + e0 + q);
             const double2 in = __ldcg(x.min_ + r.rev);
             T[q] = make_double2(in.x, in.x * in.y);
             if (x.resid) yp = yp + r.coeff * __ldcg(x.xprev + r.col);
@@ -278,7 +302,12 @@ __device__ void row_long(const SweepArgs &a, const RowCtx &x, double2 *T, uint32
         }
         if (j < d) {
             const double2 own = T[j];
-            edge_out(x, e0 + j, __ldg(&a.er[e0 + j].coeff), p, n, __ldcs(x.min_ + e0 + j), st);
+            const uint32_t pos = x.gout ? __ldg(x.gout + e0 + j) : e0 + j;
+            const double c = __ldg(&a.er[e0 + j].coeff);
+            if (x.gout)
+                edge_out<true>(x, e0 + j, pos, c, p, n, ld_na_d2(x.min_ + pos), st);
+            else
+                edge_out<false>(x, e0 + j, pos, c, p, n, __ldcs(x.min_ + pos), st);
             if (j == d - 1) row_node<MODE>(a, x, i, p + own.x, n + own.y, st);
         }
     }
@@ -391,12 +420,25 @@ struct __align__(16) QuadBuf {
     double c[2][4][64];          // A_ij
     double2 xg[4][64];           // the aligned pair of doubles holding x_j^{(s-2)}: consumed
                                  // by the strip pass, so the next quad's land under the walk
-    uint8_t par[4][64];          // which half of the pair
+                                 // (which half: a bit mask in the issuing lane's register)
+    uint32_t go[2][4][64];       // binned message order: position of the edge's own message
 };
 static_assert(sizeof(double2) * 4 * kQStride >= sizeof(double2) * (kRowParMaxDegree + 8),
               "a long row's strip fits a quad's strips");
 constexpr size_t kQuadBytes = sizeof(QuadBuf) * kQWarps;
 
+__device__ __forceinline__ void cpa_tw_n(double2 *dst, const double2 *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa_u32(uint32_t *dst, const uint32_t *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
 __device__ __forceinline__ void cpa_tw(double2 *dst, const double2 *src, uint64_t pol) {
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(dst)),
@@ -420,7 +462,7 @@ struct QRow {
     double xi = 0.0, bi = 0.0;                // x_i^{(s-2)}, b_i
 };
 
-template <int MODE>
+template <int MODE, bool BIN>
 __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a) {
     __shared__ TailSmem<kQWarps> tail;
     __shared__ int64_t s_sweep;
@@ -452,6 +494,11 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
     x.xh = (MODE == kModeSolve && a.xhist && s >= 2 && s - 1 <= a.xhist_rows)
                ? a.xhist + (s - 2) * a.n : nullptr;
     x.pol = pol_evict_first();
+    if (BIN) {
+        x.erb = a.erb;
+        x.gout = a.gout;
+    }
+    const EdgeRec *const erp = BIN ? a.erb : a.er;
     Stats st;
     st.lim = (MODE == kModeSolve) ? fmin(ctrl->blowup, DBL_MAX) : DBL_MAX;
     QuadBuf &W = reinterpret_cast<QuadBuf *>(quad_raw)[warp];
@@ -460,14 +507,22 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
     const uint32_t r_lo = __ldg(&a.tile_info[0].x);
     const uint32_t r_hi = __ldg(&a.tile_info[a.ntiles - 1].y);
     const int64_t nw = (int64_t)gridDim.x * kQWarps, gw = (int64_t)blockIdx.x * kQWarps + warp;
-    const uint32_t rb = r_lo + (uint32_t)(((int64_t)(r_hi - r_lo) * gw) / nw);
-    const uint32_t re = r_lo + (uint32_t)(((int64_t)(r_hi - r_lo) * (gw + 1)) / nw);
-    const uint32_t nq = (re - rb + 3u) / 4u;
+    // CSR order: a contiguous block of rows per warp.  Binned order: the quads dealt round
+    // robin, so the launch sweeps the rows as one ascending front -- all warps gather from
+    // the same bin's window and every bin's writes advance as one run.
+    const uint32_t tq = (r_hi - r_lo + 3u) / 4u;
+    const uint32_t rb =
+        BIN ? r_lo + 4u * (uint32_t)gw : r_lo + (uint32_t)(((int64_t)(r_hi - r_lo) * gw) / nw);
+    const uint32_t re =
+        BIN ? r_hi : r_lo + (uint32_t)(((int64_t)(r_hi - r_lo) * (gw + 1)) / nw);
+    const uint32_t qs = BIN ? 4u * (uint32_t)nw : 4u;  // row stride between a warp's quads
+    const uint32_t nq = BIN ? ((int64_t)tq > gw ? (uint32_t)((tq - gw + nw - 1) / nw) : 0u)
+                            : (re - rb + 3u) / 4u;
 
     // row offsets of quad q for this lane's row (empty past the range)
     auto row_of = [&](uint32_t q, QRow &r) {
         r = QRow();
-        const uint32_t i = rb + 4u * q + (uint32_t)g;
+        const uint32_t i = rb + qs * q + (uint32_t)g;
         if (q < nq && i < re) {
             r.i = i;
             r.e0 = __ldg(a.row_ptr + i);
@@ -481,7 +536,7 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
             const uint32_t q = (uint32_t)o + 8u * t;
-            er[t] = q < r.d ? ld_ef_i4(a.er + r.e0 + q, x.pol) : make_int4(0, 0, 0, 0);
+            er[t] = q < r.d ? ld_ef_i4(erp + r.e0 + q, x.pol) : make_int4(0, 0, 0, 0);
         }
     };
     // issue stage, part 1: twin gathers of the row into strip buffer `nb`, coefficients, node
@@ -503,22 +558,29 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
 #ifdef GABP_ROW_PROBE_COALESCED  // probe build (wrong results): no random twin gather
                 cpa_tw(&W.tw[nb][g][q], x.min_ + r.e0 + q, x.pol);
 #else
-                cpa_tw(&W.tw[nb][g][q], x.min_ + e.rev, x.pol);
+                if (BIN) {
+                    cpa_tw_n(&W.tw[nb][g][q], x.min_ + e.rev);
+                    cpa_u32(&W.go[nb][g][q], a.gout + r.e0 + q);
+                } else {
+                    cpa_tw(&W.tw[nb][g][q], x.min_ + e.rev, x.pol);
+                }
 #endif
             }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     // part 2 (after the strip pass has consumed the previous quad's x): the x_j gathers
+    uint32_t pm = 0u;  // which half of the landed pair is x_j, a bit per slot of this lane
     auto issue_x = [&](const QRow &r, const int4 (&er)[8]) {
 #ifndef GABP_ROW_PROBE_NOX
         if (x.resid) {
+            pm = 0u;
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 const uint32_t q = (uint32_t)o + 8u * t;
                 if (q < r.d) {
                     const uint32_t col = (uint32_t)er[t].y;
-                    W.par[g][q] = (uint8_t)(col & 1u);
+                    pm |= (col & 1u) << t;
                     cpa_x2(&W.xg[g][q], x.xprev, col);
                 }
             }
@@ -559,7 +621,7 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
                     Tg[k] = make_double2(v.x, v.x * v.y);  // (prec * mean), solver.py:148
                     if (x.resid) {
                         const double2 xp = W.xg[g][k];
-                        yp = yp + Cg[k] * (W.par[g][k] ? xp.y : xp.x);
+                        yp = yp + Cg[k] * ((pm >> t) & 1u ? xp.y : xp.x);
                     }
                 } else if (k < 8u * nbmax) {
                     Tg[k] = make_double2(-0.0, -0.0);
@@ -577,12 +639,14 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
             // every term load outside their own blocks and give the lane four independent add
             // chains.  The edges' own messages of S_{s-1} (change statistic) are loaded a
             // step ahead.
+            const uint32_t *Gg = W.go[cb][g];
             auto ld_old = [&](uint32_t j) {
-                return j < rc.d ? ld_ef_d2(x.min_ + rc.e0 + j, x.pol) : make_double2(0.0, 0.0);
+                if (j >= rc.d) return make_double2(0.0, 0.0);
+                return BIN ? ld_na_d2(x.min_ + Gg[j]) : ld_ef_d2(x.min_ + rc.e0 + j, x.pol);
             };
             auto finish = [&](uint32_t j, double p, double n, double2 old) {
                 if (j < rc.d) {
-                    edge_out(x, rc.e0 + j, Cg[j], p, n, old, st);
+                    edge_out<BIN>(x, rc.e0 + j, BIN ? Gg[j] : rc.e0 + j, Cg[j], p, n, old, st);
                     if (j == rc.d - 1u) {  // full sums: the last exclusion sum + the last term
                         const double2 own = Tg[j];
                         row_node<MODE>(a, x, rc.i, p + own.x, n + own.y, st);
@@ -590,73 +654,74 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
                 }
             };
             double2 oa = ld_old((uint32_t)o), ob = ld_old((uint32_t)o + 8u);
+            // The sequential sum before term block b -- prior + t_0 + ... + t_{8b-1} -- is
+            // common to every exclusion sum of the blocks from b on: it is carried (rp, rn)
+            // and each own block's sums start from it and walk only the blocks b.., the same
+            // additions in the same order.  Sum 1 of a pair *is* the carried prefix while it
+            // runs through block b; the prefix past block b + 1 is one more addition on the
+            // lane that skipped the block's last slot (o = 7), broadcast to the row's lanes.
+            double rp = rc.nd.x, rn = rc.nd.y;
             uint32_t b = 0;
             for (; b + 1 < nbmax; b += 2) {
                 const uint32_t j0 = 8u * b + (uint32_t)o, j1 = j0 + 8u;
                 const double2 old0 = oa, old1 = ob;
                 oa = ld_old(j0 + 16u);
                 ob = ld_old(j1 + 16u);
-                double p0 = rc.nd.x, n0 = rc.nd.y, p1 = p0, n1 = n0;
-                for (uint32_t bp = 0; bp < nbmax; ++bp) {
+                double p0 = rp, n0 = rn, p1 = rp, n1 = rn;
+                {  // block b: sum 0 skips its slot (an address select), sum 1 adds all
+                    const double2 *base = Tg + 8u * b;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const double2 v = base[k];
+                        p1 = p1 + v.x;
+                        n1 = n1 + v.y;
+                        if (k < 7) {
+                            const double2 w = (o > k ? base : base + 1)[k];
+                            p0 = p0 + w.x;
+                            n0 = n0 + w.y;
+                        }
+                    }
+                }
+                {  // block b + 1: the other way round
+                    const double2 *base = Tg + 8u * (b + 1u);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const double2 v = base[k];
+                        p0 = p0 + v.x;
+                        n0 = n0 + v.y;
+                        if (k < 7) {
+                            const double2 w = (o > k ? base : base + 1)[k];
+                            p1 = p1 + w.x;
+                            n1 = n1 + w.y;
+                        } else if (b + 2u < nbmax) {  // lane o = 7: (p1, n1) + t_7 = the prefix
+                            rp = __shfl_sync(~0u, p1 + v.x, 7, 8);
+                            rn = __shfl_sync(~0u, n1 + v.y, 7, 8);
+                        }
+                    }
+                }
+                for (uint32_t bp = b + 2u; bp < nbmax; ++bp) {
                     const double2 *base = Tg + 8u * bp;
-                    if (bp == b) {  // sum 0 skips its slot (an address select), sum 1 adds all
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const double2 v = base[k];
-                            p1 = p1 + v.x;
-                            n1 = n1 + v.y;
-                            if (k < 7) {
-                                const double2 w = (o > k ? base : base + 1)[k];
-                                p0 = p0 + w.x;
-                                n0 = n0 + w.y;
-                            }
-                        }
-                    } else if (bp == b + 1) {
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const double2 v = base[k];
-                            p0 = p0 + v.x;
-                            n0 = n0 + v.y;
-                            if (k < 7) {
-                                const double2 w = (o > k ? base : base + 1)[k];
-                                p1 = p1 + w.x;
-                                n1 = n1 + w.y;
-                            }
-                        }
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const double2 v = base[k];
-                            p0 = p0 + v.x;
-                            n0 = n0 + v.y;
-                            p1 = p1 + v.x;
-                            n1 = n1 + v.y;
-                        }
+                    for (int k = 0; k < 8; ++k) {
+                        const double2 v = base[k];
+                        p0 = p0 + v.x;
+                        n0 = n0 + v.y;
+                        p1 = p1 + v.x;
+                        n1 = n1 + v.y;
                     }
                 }
                 finish(j0, p0, n0, old0);
                 finish(j1, p1, n1, old1);
             }
-            if (b < nbmax) {  // an odd last own block
+            if (b < nbmax) {  // an odd last own block: terms 0..o-1, then o+1..7
                 const uint32_t j0 = 8u * b + (uint32_t)o;
-                double p0 = rc.nd.x, n0 = rc.nd.y;
-                for (uint32_t bp = 0; bp < nbmax; ++bp) {
-                    const double2 *base = Tg + 8u * bp;
-                    if (bp != b) {
+                double p0 = rp, n0 = rn;
+                const double2 *base = Tg + 8u * b;
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const double2 v = base[k];
-                            p0 = p0 + v.x;
-                            n0 = n0 + v.y;
-                        }
-                    } else {  // terms 0..o-1, then o+1..7
-#pragma unroll
-                        for (int k = 0; k < 7; ++k) {
-                            const double2 v = (o > k ? base : base + 1)[k];
-                            p0 = p0 + v.x;
-                            n0 = n0 + v.y;
-                        }
-                    }
+                for (int k = 0; k < 7; ++k) {
+                    const double2 v = (o > k ? base : base + 1)[k];
+                    p0 = p0 + v.x;
+                    n0 = n0 + v.y;
                 }
                 finish(j0, p0, n0, oa);
             }
@@ -830,6 +895,7 @@ constexpr int kMaxDevices = 64;
 int g_row_grid[kMaxDevices][2] = {};   // persistent grids per device (prepare_rowpar_kernels)
 int g_coop_grid[kMaxDevices] = {};     // cooperative serial sweep: every CTA resident
 int g_quad_grid[kMaxDevices][2] = {};  // rowquad_kernel
+int g_quad_grid_bin[kMaxDevices] = {}; // rowquad_kernel, binned message order
 
 int cur_dev() {
     int d = 0;
@@ -859,19 +925,26 @@ cudaError_t prepare_rowpar_kernels() {
                                                            0)) != cudaSuccess)
         return e;
     g_coop_grid[dv] = sms * (occ > 0 ? occ : 1);
-    if ((e = cudaFuncSetAttribute(rowquad_kernel<kModeSolve>,
+    if ((e = cudaFuncSetAttribute(rowquad_kernel<kModeSolve, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kQuadBytes)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(rowquad_kernel<kModeSingle>,
+        (e = cudaFuncSetAttribute(rowquad_kernel<kModeSolve, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kQuadBytes)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(rowquad_kernel<kModeSingle, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kQuadBytes)) != cudaSuccess)
         return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowquad_kernel<kModeSolve>,
-                                                           kQThreads, kQuadBytes)) != cudaSuccess)
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+             &occ, rowquad_kernel<kModeSolve, false>, kQThreads, kQuadBytes)) != cudaSuccess)
         return e;
     g_quad_grid[dv][kModeSolve] = sms * (occ > 0 ? occ : 1);
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowquad_kernel<kModeSingle>,
-                                                           kQThreads, kQuadBytes)) != cudaSuccess)
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+             &occ, rowquad_kernel<kModeSolve, true>, kQThreads, kQuadBytes)) != cudaSuccess)
+        return e;
+    g_quad_grid_bin[dv] = sms * (occ > 0 ? occ : 1);
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+             &occ, rowquad_kernel<kModeSingle, false>, kQThreads, kQuadBytes)) != cudaSuccess)
         return e;
     g_quad_grid[dv][kModeSingle] = sms * (occ > 0 ? occ : 1);
     return cudaSuccess;
@@ -919,13 +992,17 @@ cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st) {
     const int dv = cur_dev();
     const bool quad = !getenv("GABP_ROW_NO_QUAD");
     if (quad) {
-        int64_t grid = g_quad_grid[dv][m] > 0 ? g_quad_grid[dv][m] : 148 * 3;
+        const bool bin = m == kModeSolve && a.gout && a.erb;
+        int64_t grid = bin ? g_quad_grid_bin[dv] : g_quad_grid[dv][m];
+        if (grid <= 0) grid = 148 * 3;
         const int64_t need = (a.ntiles + kQWarps - 1) / kQWarps;
         if (grid > need) grid = need;
-        if (m == kModeSolve)
-            rowquad_kernel<kModeSolve><<<(unsigned)grid, kQThreads, kQuadBytes, st>>>(a);
+        if (bin)
+            rowquad_kernel<kModeSolve, true><<<(unsigned)grid, kQThreads, kQuadBytes, st>>>(a);
+        else if (m == kModeSolve)
+            rowquad_kernel<kModeSolve, false><<<(unsigned)grid, kQThreads, kQuadBytes, st>>>(a);
         else
-            rowquad_kernel<kModeSingle><<<(unsigned)grid, kQThreads, kQuadBytes, st>>>(a);
+            rowquad_kernel<kModeSingle, false><<<(unsigned)grid, kQThreads, kQuadBytes, st>>>(a);
         return cudaGetLastError();
     }
     int64_t grid = g_row_grid[dv][m] > 0 ? g_row_grid[dv][m] : 148 * 4;
