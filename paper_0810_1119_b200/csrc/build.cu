@@ -513,7 +513,7 @@ int build_bins(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
     const double window = (wenv ? atof(wenv) : 48.0) * 1048576.0;
     // messages that fit L2 anyway, partial graphs, ids past 31 bits: CSR order
     if (E <= 0 || E >= (1ll << 31) || g.row_lo != 0 || g.row_hi != g.n ||
-        16.0 * (double)E < 6.0 * window || window <= 0.0)
+        16.0 * (double)E < (getenv("GABP_BIN_MIN") ? atof(getenv("GABP_BIN_MIN")) : 6.0) * window || window <= 0.0)
         return GABP_OK;
     int64_t nb = (int64_t)(16.0 * (double)E / window + 0.999);
     if (nb > 4096) nb = 4096;

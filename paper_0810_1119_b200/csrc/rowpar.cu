@@ -458,6 +458,14 @@ __device__ __forceinline__ void cpa_x2(double2 *dst, const double *x, uint32_t c
 struct QRow {
     uint32_t i = 0xffffffffu, e0 = 0, d = 0;  // d: edges walked here (0 for long rows)
     uint32_t dl = 0;                          // the row's degree when it is a long row
+    uint32_t e1 = 0;                          // end offset as loaded (d, dl: QRow::fin)
+    // the offsets are loaded a stage before anything depends on them: d and dl are formed
+    // when the row moves on, not behind the loads
+    __device__ __forceinline__ void fin() {
+        const uint32_t dd = e1 - e0;
+        d = dd <= 64u ? dd : 0u;
+        dl = dd <= 64u ? 0u : dd;
+    }
     double2 nd = make_double2(0.0, 0.0);      // {A_ii, A_ii mu_ii}
     double xi = 0.0, bi = 0.0;                // x_i^{(s-2)}, b_i
 };
@@ -526,9 +534,7 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
         if (q < nq && i < re) {
             r.i = i;
             r.e0 = __ldg(a.row_ptr + i);
-            const uint32_t d = __ldg(a.row_ptr + i + 1) - r.e0;
-            r.d = d <= 64u ? d : 0u;
-            r.dl = d <= 64u ? 0u : d;
+            r.e1 = __ldg(a.row_ptr + i + 1);
         }
     };
     // edge records of the row's slots o, o + 8, ... (registers, consumed by the issue stage)
@@ -541,7 +547,9 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
     };
     // issue stage, part 1: twin gathers of the row into strip buffer `nb`, coefficients, node
     // operands into registers
-    auto issue_tw = [&](QRow &r, const int4 (&er)[8], int nb) {
+    // (issued after the stage's cp.async traffic: a load in flight on the scoreboard of the
+    // edge records would hold their consumers back)
+    auto node_loads = [&](QRow &r) {
         if (r.i != 0xffffffffu) {
             r.nd = __ldg(reinterpret_cast<const double2 *>(a.nd + r.i));
             if (x.resid) {
@@ -549,6 +557,8 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
                 r.bi = __ldg(a.rhs + r.i);
             }
         }
+    };
+    auto issue_tw = [&](const QRow &r, const int4 (&er)[8], int nb) {
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
             const uint32_t q = (uint32_t)o + 8u * t;
@@ -593,10 +603,13 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
         QRow rc, ri, rl, rn;  // rows of the quad being walked, issued, loaded; offsets ahead
         int4 er[8];
         row_of(0, ri);
+        ri.fin();
         load_er(ri, er);
         issue_tw(ri, er, 0);
         issue_x(ri, er);
+        node_loads(ri);
         row_of(1, rl);
+        rl.fin();
         row_of(2, rn);
         load_er(rl, er);
         for (uint32_t q = 0; q < nq; ++q) {
@@ -604,7 +617,7 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
             rc = ri;
             ri = rl;
             rl = rn;  // (its offsets were loaded a quad ago: no dependent load before load_er)
-            row_of(q + 3, rn);
+            rl.fin();
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // quad q has landed
             __syncwarp();
             issue_tw(ri, er, cb ^ 1);  // quad q + 1 (empty past the range)
@@ -629,7 +642,9 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
             }
             __syncwarp();
             issue_x(ri, er);  // (the x buffer is free again)
+            node_loads(ri);
             load_er(rl, er);
+            row_of(q + 3, rn);
             if (x.resid) {  // sum over the row's 8 lanes
                 yp += __shfl_xor_sync(~0u, yp, 1);
                 yp += __shfl_xor_sync(~0u, yp, 2);
@@ -655,19 +670,16 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
             };
             double2 oa = ld_old((uint32_t)o), ob = ld_old((uint32_t)o + 8u);
             // The sequential sum before term block b -- prior + t_0 + ... + t_{8b-1} -- is
-            // common to every exclusion sum of the blocks from b on: it is carried (rp, rn)
+            // common to every exclusion sum of the blocks from b on: it is carried (rp, rn_)
             // and each own block's sums start from it and walk only the blocks b.., the same
             // additions in the same order.  Sum 1 of a pair *is* the carried prefix while it
             // runs through block b; the prefix past block b + 1 is one more addition on the
             // lane that skipped the block's last slot (o = 7), broadcast to the row's lanes.
-            double rp = rc.nd.x, rn = rc.nd.y;
-            uint32_t b = 0;
-            for (; b + 1 < nbmax; b += 2) {
+            double rp = rc.nd.x, rn_ = rc.nd.y;
+            // one step: own blocks b and b + 1 (their old messages in o0, o1)
+            auto walk_pair = [&](uint32_t b, const double2 &o0, const double2 &o1) {
                 const uint32_t j0 = 8u * b + (uint32_t)o, j1 = j0 + 8u;
-                const double2 old0 = oa, old1 = ob;
-                oa = ld_old(j0 + 16u);
-                ob = ld_old(j1 + 16u);
-                double p0 = rp, n0 = rn, p1 = rp, n1 = rn;
+                double p0 = rp, n0 = rn_, p1 = rp, n1 = rn_;
                 {  // block b: sum 0 skips its slot (an address select), sum 1 adds all
                     const double2 *base = Tg + 8u * b;
 #pragma unroll
@@ -695,7 +707,7 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
                             n1 = n1 + w.y;
                         } else if (b + 2u < nbmax) {  // lane o = 7: (p1, n1) + t_7 = the prefix
                             rp = __shfl_sync(~0u, p1 + v.x, 7, 8);
-                            rn = __shfl_sync(~0u, n1 + v.y, 7, 8);
+                            rn_ = __shfl_sync(~0u, n1 + v.y, 7, 8);
                         }
                     }
                 }
@@ -710,12 +722,12 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
                         n1 = n1 + v.y;
                     }
                 }
-                finish(j0, p0, n0, old0);
-                finish(j1, p1, n1, old1);
-            }
-            if (b < nbmax) {  // an odd last own block: terms 0..o-1, then o+1..7
-                const uint32_t j0 = 8u * b + (uint32_t)o;
-                double p0 = rp, n0 = rn;
+                finish(j0, p0, n0, o0);
+                finish(j1, p1, n1, o1);
+            };
+            auto walk_last = [&](uint32_t b, const double2 &o0) {  // an odd last own block:
+                const uint32_t j0 = 8u * b + (uint32_t)o;           // terms 0..o-1, o+1..7
+                double p0 = rp, n0 = rn_;
                 const double2 *base = Tg + 8u * b;
 #pragma unroll
                 for (int k = 0; k < 7; ++k) {
@@ -723,7 +735,30 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
                     p0 = p0 + v.x;
                     n0 = n0 + v.y;
                 }
-                finish(j0, p0, n0, oa);
+                finish(j0, p0, n0, o0);
+            };
+            // The old messages of a step are loaded a step ahead into the register pair the
+            // step before last used (two alternating pairs: no copy of a register whose load
+            // is still in flight).
+            double2 oc = make_double2(0.0, 0.0), od = oc;
+            uint32_t b = 0;
+            for (;;) {
+                if (b + 1 >= nbmax) {
+                    if (b < nbmax) walk_last(b, oa);
+                    break;
+                }
+                oc = ld_old(8u * b + 16u + (uint32_t)o);
+                od = ld_old(8u * b + 24u + (uint32_t)o);
+                walk_pair(b, oa, ob);
+                b += 2;
+                if (b + 1 >= nbmax) {
+                    if (b < nbmax) walk_last(b, oc);
+                    break;
+                }
+                oa = ld_old(8u * b + 16u + (uint32_t)o);
+                ob = ld_old(8u * b + 24u + (uint32_t)o);
+                walk_pair(b, oc, od);
+                b += 2;
             }
             const bool plain = rc.i != 0xffffffffu && rc.dl == 0u;
             if (plain && rc.d == 0u && o == 0) row_node<MODE>(a, x, rc.i, rc.nd.x, rc.nd.y, st);
@@ -735,7 +770,7 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
             __syncwarp();
             // rows of more than 64 edges: the whole warp, one row at a time, on the buffer
             const unsigned lmask = __ballot_sync(~0u, rc.dl != 0u && o == 0);
-            for (int gg = 0; gg < 4; ++gg) {
+            for (int gg = 0; lmask != 0u && gg < 4; ++gg) {
                 if (lmask & (1u << (8 * gg))) {
                     const int src = 8 * gg;
                     NodeRec nd;
