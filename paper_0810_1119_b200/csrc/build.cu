@@ -198,12 +198,13 @@ __global__ void bin_pos_kernel(int64_t E, const uint32_t *sorted, uint32_t *pos)
          p += (int64_t)gridDim.x * blockDim.x)
         pos[sorted[p]] = (uint32_t)p;
 }
-__global__ void bin_rec_kernel(int64_t E, const EdgeRec *er, const uint32_t *pos, EdgeRec *erb) {
+__global__ void bin_rec_kernel(int64_t E, const EdgeRec *er, const uint32_t *pos, uint2 *gidx,
+                               double *gcoef) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
          e += (int64_t)gridDim.x * blockDim.x) {
-        EdgeRec r = er[e];
-        r.rev = pos[r.rev];
-        erb[e] = r;
+        const EdgeRec r = er[e];
+        gidx[e] = make_uint2(pos[r.rev], r.col);
+        gcoef[e] = r.coeff;
     }
 }
 
@@ -243,7 +244,8 @@ void free_graph(DeviceGraph &g, cudaStream_t st) {
     if (g.scol) cudaFreeAsync(g.scol, st);
     if (g.scoef) cudaFreeAsync(g.scoef, st);
     if (g.stwin) cudaFreeAsync(g.stwin, st);
-    if (g.erb) cudaFreeAsync(g.erb, st);
+    if (g.gidx) cudaFreeAsync(g.gidx, st);
+    if (g.gcoef) cudaFreeAsync(g.gcoef, st);
     if (g.gout) cudaFreeAsync(g.gout, st);
     g = DeviceGraph{};
 }
@@ -504,7 +506,7 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
 // rows of one bin gather all their incoming messages from one window of E / bins messages
 // (a few MB: every line comes from DRAM once and serves its 8 gathers from L2), and rows
 // swept in ascending order write each bin's messages as an ascending run (lines fill in L2
-// within a few rows).  gout[e] = pos(e), erb[e].rev = pos(rev(e)).
+// within a few rows).  gout[e] = pos(e), gidx[e] = {pos(rev(e)), j}, gcoef[e] = A_ij.
 int build_bins(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
     if (g.bins != 0) return GABP_OK;
     g.bins = -1;
@@ -537,9 +539,10 @@ int build_bins(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
                                                  st)) != cudaSuccess)
             return e;
         if ((e = cudaMallocAsync(&g.gout, sizeof(uint32_t) * E, st)) != cudaSuccess) return e;
-        if ((e = cudaMallocAsync(&g.erb, sizeof(EdgeRec) * E, st)) != cudaSuccess) return e;
+        if ((e = cudaMallocAsync(&g.gidx, sizeof(uint2) * E, st)) != cudaSuccess) return e;
+        if ((e = cudaMallocAsync(&g.gcoef, sizeof(double) * E, st)) != cudaSuccess) return e;
         bin_pos_kernel<<<grid_for(E), 256, 0, st>>>(E, val + E, g.gout);
-        bin_rec_kernel<<<grid_for(E), 256, 0, st>>>(E, g.er, g.gout, g.erb);
+        bin_rec_kernel<<<grid_for(E), 256, 0, st>>>(E, g.er, g.gout, g.gidx, g.gcoef);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         return cudaStreamSynchronize(st);
     };
@@ -550,9 +553,11 @@ int build_bins(DeviceGraph &g, cudaStream_t st, char *err, size_t errlen) {
     if (e != cudaSuccess) {
         // (out of memory: the solve runs in CSR order; anything else is reported)
         if (g.gout) cudaFreeAsync(g.gout, st);
-        if (g.erb) cudaFreeAsync(g.erb, st);
+        if (g.gidx) cudaFreeAsync(g.gidx, st);
+        if (g.gcoef) cudaFreeAsync(g.gcoef, st);
         g.gout = nullptr;
-        g.erb = nullptr;
+        g.gidx = nullptr;
+        g.gcoef = nullptr;
         cudaGetLastError();
         if (e == cudaErrorMemoryAllocation) return GABP_OK;
         snprintf(err, errlen, "build_bins: %s", cudaGetErrorString(e));

@@ -462,7 +462,8 @@ SweepArgs make_args(gabp_graph *G) {
     a.scoef = g.scoef;
     a.stwin = g.stwin;
     if (g.bins > 0 && !getenv("GABP_ROW_NO_BIN")) {  // (A/B: CSR message order)
-        a.erb = g.erb;
+        a.gidx = g.gidx;
+        a.gcoef = g.gcoef;
         a.gout = g.gout;
     }
     a.sl_lo = 0;

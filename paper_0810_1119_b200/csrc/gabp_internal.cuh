@@ -188,7 +188,9 @@ struct SweepArgs {
     const uint32_t *stwin;     // slot of the twin message (parallel schedule), per slot
     // binned message order of the four-rows-per-warp parallel kernel (rowpar.cu:
     // build_bins; null: messages in CSR order)
-    const EdgeRec *erb;        // edge records whose rev field is the twin message's position
+    const uint2 *gidx;         // per edge {position of the twin message, column}
+    const double *gcoef;       // per edge A_ij (a stream of its own: the kernel keeps only
+                               // the two indices in registers)
     const uint32_t *gout;      // position of the edge's own message
     int probe;                 // residual probe: 0 off, 1 run by the exact twin, 2 as a
                                // residual-only group launch (probe_next)
@@ -445,7 +447,8 @@ struct DeviceGraph {
     double *scoef = nullptr;
     uint32_t *stwin = nullptr;  // built on the first parallel-schedule solve (build_stwin)
     // binned message order (rowpar.cu: build_bins), built on the first solve that uses it
-    EdgeRec *erb = nullptr;
+    uint2 *gidx = nullptr;
+    double *gcoef = nullptr;
     uint32_t *gout = nullptr;
     int bins = 0;               // 0: not tried, -1: not worth it (messages fit L2), else count
     // diagonal layout (build_dia, dia.cu); dia_D == 0 when the graph is not a stencil

@@ -53,9 +53,9 @@ struct RowCtx {
     double *xcur, *pcur, *xh;
     bool resid;
     uint64_t pol;         // L2 evict-first
-    // binned message order (build_bins): edge records whose rev field is the position of the
-    // twin message, and the position of the edge's own message; null: CSR order
-    const EdgeRec *erb = nullptr;
+    // binned message order (build_bins): per edge {position of the twin message, column} and
+    // the position of the edge's own message; null: CSR order
+    const uint2 *gidx = nullptr;
     const uint32_t *gout = nullptr;
 };
 
@@ -275,10 +275,10 @@ __device__ void row_long(const SweepArgs &a, const RowCtx &x, double2 *T, uint32
                          uint32_t e0, uint32_t d, NodeRec nd, int lane, Stats &st) {
     const uint32_t dpad = (d + 7u) & ~7u;
     double yp = 0.0;
-    const EdgeRec *er = x.erb ? x.erb : a.er;
     for (uint32_t q = lane; q < dpad; q += 32) {
         if (q < d) {
-            const EdgeRec r = ld_er(er + e0 + q);
+            EdgeRec r = ld_er(a.er + e0 + q);
+            if (x.gidx) r.rev = __ldg(&x.gidx[e0 + q].x);
             const double2 in = __ldcg(x.min_ + r.rev);
             T[q] = make_double2(in.x, in.x * in.y);
             if (x.resid) yp = yp + r.coeff * __ldcg(x.xprev + r.col);
@@ -439,6 +439,19 @@ __device__ __forceinline__ void cpa_u32(uint32_t *dst, const uint32_t *src) {
                  "l"(src)
                  : "memory");
 }
+__device__ __forceinline__ void cpa_f64(double *dst, const double *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ uint2 ld_ef_u2(const uint2 *ptr, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y)
+                 : "l"(ptr), "l"(pol));
+    return v;
+}
 __device__ __forceinline__ void cpa_tw(double2 *dst, const double2 *src, uint64_t pol) {
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(dst)),
@@ -503,10 +516,9 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
                ? a.xhist + (s - 2) * a.n : nullptr;
     x.pol = pol_evict_first();
     if (BIN) {
-        x.erb = a.erb;
+        x.gidx = a.gidx;
         x.gout = a.gout;
     }
-    const EdgeRec *const erp = BIN ? a.erb : a.er;
     Stats st;
     st.lim = (MODE == kModeSolve) ? fmin(ctrl->blowup, DBL_MAX) : DBL_MAX;
     QuadBuf &W = reinterpret_cast<QuadBuf *>(quad_raw)[warp];
@@ -542,7 +554,12 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
             const uint32_t q = (uint32_t)o + 8u * t;
-            er[t] = q < r.d ? ld_ef_i4(erp + r.e0 + q, x.pol) : make_int4(0, 0, 0, 0);
+            if (BIN) {  // the two indices only: A_ij goes straight to shared memory later
+                const uint2 v = q < r.d ? ld_ef_u2(a.gidx + r.e0 + q, x.pol) : make_uint2(0u, 0u);
+                er[t] = make_int4((int)v.x, (int)v.y, 0, 0);
+            } else {
+                er[t] = q < r.d ? ld_ef_i4(a.er + r.e0 + q, x.pol) : make_int4(0, 0, 0, 0);
+            }
         }
     };
     // issue stage, part 1: twin gathers of the row into strip buffer `nb`, coefficients, node
@@ -564,7 +581,10 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
             const uint32_t q = (uint32_t)o + 8u * t;
             if (q < r.d) {
                 const EdgeRec e = er_of(er[t]);
-                W.c[nb][g][q] = e.coeff;
+                if (BIN)
+                    cpa_f64(&W.c[nb][g][q], a.gcoef + r.e0 + q);
+                else
+                    W.c[nb][g][q] = e.coeff;
 #ifdef GABP_ROW_PROBE_COALESCED  // probe build (wrong results): no random twin gather
                 cpa_tw(&W.tw[nb][g][q], x.min_ + r.e0 + q, x.pol);
 #else
@@ -1027,7 +1047,7 @@ cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st) {
     const int dv = cur_dev();
     const bool quad = !getenv("GABP_ROW_NO_QUAD");
     if (quad) {
-        const bool bin = m == kModeSolve && a.gout && a.erb;
+        const bool bin = m == kModeSolve && a.gout && a.gidx && a.gcoef;
         int64_t grid = bin ? g_quad_grid_bin[dv] : g_quad_grid[dv][m];
         if (grid <= 0) grid = 148 * 3;
         const int64_t need = (a.ntiles + kQWarps - 1) / kQWarps;
