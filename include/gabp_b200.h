@@ -104,6 +104,9 @@ typedef struct {
     int64_t dist_layout;      /* multi-rank kernel family agreed by the ranks: 0 none (one
                                  rank), 1 slice layout (node-state halo), 2 row tiles,
                                  3 diagonal layout (message + node-state halo) */
+    int64_t message_bins;     /* parallel schedule, four-rows-per-warp kernel: bins of the binned
+                                 message order the solve ran in (0: CSR order; DESIGN.md
+                                 "rowquad_kernel") */
 } gabp_report_t;
 
 const char *gabp_last_error(void);

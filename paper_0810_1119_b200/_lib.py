@@ -68,7 +68,8 @@ class Report(ctypes.Structure):
                 ("sweeps_launched", ctypes.c_int64), ("messages_sent", ctypes.c_int64),
                 ("device_ms", ctypes.c_double), ("final_rel_residual", ctypes.c_double),
                 ("residual_probes", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
-                ("split_sweeps", ctypes.c_int64), ("dist_layout", ctypes.c_int64)]
+                ("split_sweeps", ctypes.c_int64), ("dist_layout", ctypes.c_int64),
+                ("message_bins", ctypes.c_int64)]
 
 
 class GabpError(RuntimeError):

@@ -132,6 +132,7 @@ struct gabp_graph {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     double *xhist = nullptr;  // device means history (only while a solve asks for it)
     bool slice_order = false;  // the last solve's x / p ring is in slice position order
+    int bins_used = 0;         // the last solve ran the row kernel in binned message order
     double *xs = nullptr, *ps = nullptr;  // row-order copies of the returned marginals
     int64_t xhist_rows = 0;
     DistState *dist = nullptr;
@@ -979,6 +980,7 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
     int rc = solve_setup(G, opt);
     if (rc) return rc;
     G->kernels_launched = 0;
+    G->bins_used = 0;
     cudaStream_t st = G->stream;
     // max_iter + 2 sweep launches, plus at most one residual-only launch per sweep (slice
     // path, probe_next) -- the loop normally stops on the polled done flag long before
@@ -1136,6 +1138,12 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
         G->ws_gen++;  // captured sweeps hold the index pointers
     }
     G->slice_order = gather == gabp::kGatherSlice || gather == gabp::kGatherSliceParallel;
+    {
+        const SweepArgs ab = make_args(G);
+        G->bins_used = gather == gabp::kGatherRowParallel && ab.gout && !getenv("GABP_ROW_NO_QUAD")
+                           ? G->g.bins
+                           : 0;
+    }
     const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
     const double tc0 = host_ms();
     rc = get_chunk_exec(G, sched, gather, C);
@@ -1181,6 +1189,7 @@ void fill_report(gabp_graph *G, const gabp_options_t *opt, double ms, double rsq
     rep->kernel_launches = G->kernels_launched + c.twin_launches;
     rep->split_sweeps = G->dist ? G->dist->split_launches : 0;
     rep->dist_layout = !G->dist ? 0 : G->dist->use_dia ? 3 : G->dist->use_slices ? 1 : 2;
+    rep->message_bins = G->bins_used;
     rep->final_rel_residual =
         (c.n_hist >= 1 && G->g.rhs_norm > 0.0) ? sqrt(rsq_last) / G->g.rhs_norm : NAN;
 }

@@ -189,6 +189,7 @@ class SolveReport:
     kernel_launches: int = 0
     split_sweeps: int = 0   # multi-rank: sweeps run as boundary part + interior part
     dist_layout: int = 0    # multi-rank kernel family: 1 slice, 2 tiles, 3 diagonal
+    message_bins: int = 0   # parallel row kernel: bins of the binned message order (0: CSR)
 
 
 def initial_state(graph: GaussianGraph, schedule: str = "parallel") -> MessageState:
@@ -499,6 +500,7 @@ def solve_graph(graph: GaussianGraph, options: SolveOptions | None = None) -> So
         final_rel_residual=float(rep.final_rel_residual),
         residual_probes=int(rep.residual_probes),
         kernel_launches=int(rep.kernel_launches),
+        message_bins=int(rep.message_bins),
     )
 
 
