@@ -39,7 +39,10 @@ def main():
     ap.add_argument("--sweeps", type=int, default=50)
     ap.add_argument("--schedule", type=int, default=2)
     a = ap.parse_args()
-    peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6540.0)
+    try:
+        peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)
+    except OSError:  # (driver-written per pod; absent: the profiling recipe's fallback)
+        peak = 6650.0
     res = {}
     for _ in range(a.rounds):
         for lib in a.libs:

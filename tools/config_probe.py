@@ -42,8 +42,11 @@ except Exception:  # noqa: BLE001
     free, total = 0, 0
 E, n = g.num_edges, g.n
 algo = 48 * E + 52 * n
-peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                   "MEASURED_PEAKS.json"))).get("hbm_gbs", 6537.3)
+try:
+    peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                       "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)
+except OSError:  # (driver-written per pod; absent: the profiling recipe's fallback)
+    peak = 6650.0
 print(json.dumps({
     "config": a.config, "workload": name, "n": n, "directed_edges": E,
     "slices": int(g.info.num_slices), "slots": int(g.info.num_slots),

@@ -27,8 +27,11 @@ for _ in range(a.reps):
     _lib.check(lib.gabp_bench_sweeps(g.handle, 2, mode, a.sweeps, ctypes.byref(ms)))
     out.append(ms.value)
 E, n = g.num_edges, g.n
-peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                   "MEASURED_PEAKS.json"))).get("hbm_gbs", 6540.0)
+try:
+    peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)
+except OSError:  # (driver-written per pod; absent: the profiling recipe's fallback)
+    peak = 6650.0
 best = min(out)
 print(json.dumps({"grid": spec.name, "mode": a.mode, "dia": int(g.info.dia_diagonals),
                   "ms": [round(v, 4) for v in out],
