@@ -46,10 +46,14 @@ extern "C" {
 #define GABP_GATHER_SLICE 3     /* slice layout (lane per row): broadcast solve recomputes
                                    m_ji as GABP_GATHER_RECOMPUTE; parallel solve sums the
                                    row's incoming slots and stores to the twin slots */
-#define GABP_GATHER_ROWS 4      /* parallel schedule: warp per row over the CSR order, the
-                                   row's incoming terms in a shared-memory strip, one
-                                   exclusion sum per lane (rows <= 256 edges); the broadcast
-                                   schedule treats it as GABP_GATHER_AUTO */
+#define GABP_GATHER_ROWS 4      /* parallel schedule: four rows per warp over the CSR order,
+                                   the rows' incoming terms in a shared-memory strip, the
+                                   exclusion sums from a carried prefix (rows <= 256 edges).
+                                   A solve whose messages exceed L2 keeps them in a binned
+                                   order (built once per graph, report.message_bins; window
+                                   size GABP_BIN_WINDOW_MB, default 48; GABP_ROW_NO_BIN=1
+                                   keeps the CSR order).  The broadcast schedule treats this
+                                   mode as GABP_GATHER_AUTO */
 
 typedef struct gabp_graph gabp_graph_t;  /* device-resident GaussianGraph */
 typedef struct gabp_state gabp_state_t;  /* device-resident MessageState  */
