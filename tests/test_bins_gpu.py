@@ -80,6 +80,25 @@ def test_binned_order_matches_oracle_and_csr_order(tiny_window, monkeypatch, n, 
                                   np.asarray(r.max_change_history))
 
 
+@pytest.mark.parametrize("sweep_cap", [1, 2, 3, 5, 60])
+def test_binned_order_degree_ladder(tiny_window, sweep_cap):
+    """Every degree class the four-rows-per-warp kernel distinguishes (0, 1..64 in the quads,
+    one or two own blocks, an odd last block; 65..255 through the long-row path) in binned
+    order, stopped after each of the first launches and at convergence."""
+    from tests.test_gpu_parity import _degree_ladder_system
+
+    s = _degree_ladder_system()
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    o = oracle.solve(og, epsilon=1e-12, max_iter=sweep_cap, schedule="parallel")
+    r = _solve_rows(s, epsilon=1e-12, max_iter=sweep_cap)
+    assert r.message_bins >= 2
+    assert r.iterations == o.iterations and r.converged == o.converged
+    np.testing.assert_array_equal(_bits(r.means), _bits(o.means))
+    np.testing.assert_array_equal(_bits(r.precisions), _bits(o.precisions))
+    np.testing.assert_array_equal(np.asarray(r.max_change_history),
+                                  np.asarray(o.max_change_history))
+
+
 def test_binned_graph_is_reused_and_reproducible(tiny_window):
     """One graph, several solves (different caps, then a new right-hand side): the index arrays
     are built once, every solve is bitwise the oracle, repeated solves agree bit for bit."""
