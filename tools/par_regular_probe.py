@@ -25,7 +25,17 @@ pv = rng.uniform(-1.0, 1.0, pi.size)
 pv[pv == 0.0] = 0.25
 absrow = np.bincount(pi, np.abs(pv), n) + np.bincount(pj, np.abs(pv), n)
 s = G.SymSystem.from_pairs(1.1 * absrow, pi, pj, pv, rng.standard_normal(n), validate=False)
-for name, sysm in (("regular-32", s), ("config 1", G.gen_random_sparse(n, k, 0).system)):
+c1 = G.gen_random_sparse(n, k, 0).system
+# config 1 relabelled by degree (rows of equal block count next to each other): the same
+# work, no padding inside a quad -- the most a row permutation in the load stage could win
+deg1 = np.bincount(np.concatenate([c1.pair_i, c1.pair_j]), minlength=n)
+rank = np.empty(n, dtype=np.int64)
+rank[np.argsort(-deg1, kind="stable")] = np.arange(n)
+ri, rj = rank[c1.pair_i], rank[c1.pair_j]
+inv = np.argsort(rank)
+c1s = G.SymSystem.from_pairs(c1.diag[inv], np.minimum(ri, rj), np.maximum(ri, rj), c1.pair_v,
+                             c1.rhs[inv], validate=False)
+for name, sysm in (("regular-32", s), ("config 1", c1), ("config 1 by degree", c1s)):
     g = G.build_graph(sysm, 0)
     deg = np.bincount(np.concatenate([sysm.pair_i, sysm.pair_j]), minlength=n)
     ms = ctypes.c_double()
