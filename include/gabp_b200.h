@@ -48,7 +48,8 @@ extern "C" {
                                    row's incoming slots and stores to the twin slots */
 #define GABP_GATHER_ROWS 4      /* parallel schedule: four rows per warp over the CSR order,
                                    the rows' incoming terms in a shared-memory strip, the
-                                   exclusion sums from a carried prefix (rows <= 256 edges).
+                                   exclusion sums from a carried prefix (rows <= 256 edges;
+                                   AUTO takes it on whole graphs of mean degree >= 7).
                                    A solve whose messages exceed L2 keeps them in a binned
                                    order (built once per graph, report.message_bins; window
                                    size GABP_BIN_WINDOW_MB, default 48; GABP_ROW_NO_BIN=1

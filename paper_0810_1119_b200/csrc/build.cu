@@ -184,6 +184,28 @@ struct Scratch {
 };
 
 
+// rows of more than 32 / 48 / 16 edges (the slot count of rowquad_kernel, rowpar.cu)
+__global__ void deg_class_kernel(int64_t n, const uint32_t *deg, unsigned long long *cnt) {
+    unsigned long long c16 = 0, c32 = 0, c48 = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t d = deg[i];
+        c16 += d > 16u;
+        c32 += d > 32u;
+        c48 += d > 48u;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        c16 += __shfl_xor_sync(~0u, c16, o);
+        c32 += __shfl_xor_sync(~0u, c32, o);
+        c48 += __shfl_xor_sync(~0u, c48, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (c16) atomicAdd(cnt + 2, c16);
+        if (c32) atomicAdd(cnt, c32);
+        if (c48) atomicAdd(cnt + 1, c48);
+    }
+}
+
 // ---- binned message order (build_bins) -----------------------------------------------------
 __global__ void bin_key_kernel(int64_t E, const EdgeRec *er, uint32_t rows_per_bin,
                                uint32_t *key, uint32_t *val) {
@@ -353,6 +375,11 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
     {
         uint32_t *d_max = nullptr;
         BCHECK(cudaMallocAsync(&d_max, sizeof(uint32_t), st));
+        unsigned long long *d_cls = nullptr, h_cls[3] = {0ull, 0ull, 0ull};
+        BCHECK(cudaMallocAsync(&d_cls, sizeof(h_cls), st));
+        BCHECK(cudaMemsetAsync(d_cls, 0, sizeof(h_cls), st));
+        deg_class_kernel<<<148 * 4, 256, 0, st>>>(n, deg, d_cls);
+        BCHECK(cudaGetLastError());
         size_t b2 = 0;
         BCHECK(cub::DeviceReduce::Max(nullptr, b2, deg, d_max, n, st));
         if (b2 > tmp_cap) {
@@ -363,13 +390,18 @@ int build_graph_device(DeviceGraph &g, int64_t n, int64_t npairs, const double *
         BCHECK(cub::DeviceReduce::Max(tmp, b2, deg, d_max, n, st));
         uint32_t h_max = 0;
         BCHECK(cudaMemcpyAsync(&h_max, d_max, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        BCHECK(cudaMemcpyAsync(h_cls, d_cls, sizeof(h_cls), cudaMemcpyDeviceToHost, st));
         int h_err0 = 0;
         BCHECK(cudaMemcpyAsync(&h_err0, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
         unsigned long long h_at0 = 0;
         BCHECK(cudaMemcpyAsync(&h_at0, d_at, 8, cudaMemcpyDeviceToHost, st));
         BCHECK(cudaStreamSynchronize(st));
         cudaFreeAsync(d_max, st);
+        cudaFreeAsync(d_cls, st);
         g.max_degree = h_max;
+        g.rows_gt32 = (int64_t)h_cls[0];
+        g.rows_gt48 = (int64_t)h_cls[1];
+        g.rows_gt16 = (int64_t)h_cls[2];
         if (h_err0 != kErrNone) {
             cudaFreeAsync(tmp, st);
             cudaFreeAsync(deg, st);

@@ -462,6 +462,16 @@ SweepArgs make_args(gabp_graph *G) {
     a.scol = g.scol;
     a.scoef = g.scoef;
     a.stwin = g.stwin;
+    {
+        // slots per lane of the four-rows-per-warp kernel: the smallest instantiation that
+        // leaves at most one row in 1024 to the long-row path (GABP_QUAD_SLOTS: A/B)
+        const int64_t few = g.n / 1024;
+        a.quad_slots = g.rows_gt16 <= few   ? 2
+                       : g.rows_gt32 <= few ? 4
+                       : g.rows_gt48 <= few ? 6
+                                            : 8;
+        if (const char *qs = getenv("GABP_QUAD_SLOTS")) a.quad_slots = atoi(qs);
+    }
     if (g.bins > 0 && !getenv("GABP_ROW_NO_BIN")) {  // (A/B: CSR message order)
         a.gidx = g.gidx;
         a.gcoef = g.gcoef;
@@ -546,13 +556,13 @@ int pick_gather(const gabp_graph *G, const gabp_options_t *opt) {
         // contiguous incoming slots, scattered twin stores) on whole graphs with slices
         const bool whole = G->g.row_lo == 0 && G->g.row_hi == G->g.n;
         if (opt->gather_mode == GABP_GATHER_ROWS) return gabp::kGatherRowParallel;
-        // mean degree >= 10: four rows per warp over the CSR order (rowpar.cu:
-        // rowquad_kernel; config 1, mean 32: 1.12 ms/sweep against 1.70 for the slice
-        // groups, whose later passes re-stream the row); lower degrees stay on the slice
-        // groups (random graphs of 512 k rows, tools/par_degree_probe.py: mean degree 8
-        // 0.190 ms against 0.251, 12: 0.302 against 0.281, 24: 0.590 against 0.429)
+        // mean degree >= 7: four rows per warp (rowpar.cu: rowquad_kernel; config 1, mean
+        // 32: 0.80 ms/sweep against 1.70 for the slice groups, whose later passes re-stream
+        // the row); lower degrees stay on the slice groups (random graphs of 512 k rows,
+        // tools/par_degree_probe.py, slice / rows: mean degree 4 0.094 / 0.116 ms, 8
+        // 0.190 / 0.167, 12 0.300 / 0.197, 24 0.580 / 0.357)
         if (opt->gather_mode == GABP_GATHER_AUTO && whole && G->g.n > 0 &&
-            G->g.E >= 10 * G->g.n && G->g.max_degree <= gabp::kRowParMaxDegree)
+            G->g.E >= 7 * G->g.n && G->g.max_degree <= gabp::kRowParMaxDegree)
             return gabp::kGatherRowParallel;
         if (opt->gather_mode == GABP_GATHER_SLICE ||
             (opt->gather_mode == GABP_GATHER_AUTO && G->g.nslices > 0 && whole))

@@ -192,6 +192,8 @@ struct SweepArgs {
     const double *gcoef;       // per edge A_ij (a stream of its own: the kernel keeps only
                                // the two indices in registers)
     const uint32_t *gout;      // position of the edge's own message
+    int quad_slots;            // rowquad_kernel: slots per lane that cover the graph's rows
+                               // (2, 4, 6 or 8; rows past 8 x slots take the long-row path)
     int probe;                 // residual probe: 0 off, 1 run by the exact twin, 2 as a
                                // residual-only group launch (probe_next)
     int probe_force;           // test hook (GABP_PROBE_FORCE=1): request a probe after every
@@ -451,6 +453,8 @@ struct DeviceGraph {
     double *gcoef = nullptr;
     uint32_t *gout = nullptr;
     int bins = 0;               // 0: not tried, -1: not worth it (messages fit L2), else count
+    int64_t rows_gt16 = 0, rows_gt32 = 0, rows_gt48 = 0;  // rows of more than 16 / 32 / 48
+                                                          // edges (rowquad_kernel)
     // diagonal layout (build_dia, dia.cu); dia_D == 0 when the graph is not a stencil
     int dia_D = 0;
     int64_t dia_nlc = 0, dia_O = 0, dia_W = 0;

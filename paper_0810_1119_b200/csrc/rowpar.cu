@@ -411,21 +411,32 @@ __global__ void __launch_bounds__(kRThreads, 2) rowpar_kernel(const SweepArgs a)
 // (the next quad's gathers under this quad's walk) and are converted in place into the strip
 // {P, P mu}; strips are padded with {-0, -0} to a whole number of blocks and sit at a row
 // stride of 66 entries, so the four rows' broadcast loads hit different banks.
+//
+// QT = slots per lane: the quads hold rows of up to 8 QT edges (longer rows: row_long).  The
+// per-slot loops of every stage run QT times under predicates, so a graph is swept by the
+// instantiation that just covers its rows (QT = 2, 4, 6 or 8, chosen from the degree counts of
+// the build: launch_rowpar) -- config 1 (rows of 17..56 edges) 0.877 ms/sweep with 8 slots,
+// 0.798 with 6.
 constexpr int kQThreads = 128;
 constexpr int kQWarps = kQThreads / 32;
 constexpr int kQStride = 66;
+template <int QT>
 struct __align__(16) QuadBuf {
+    static constexpr int kQCap = 8 * QT;
     double2 tw[2][4][kQStride];  // twin messages m_ji of S_{s-1}; then the strip {P, P mu}
                                  // (two quads: the next one lands under this one's walk)
-    double c[2][4][64];          // A_ij
-    double2 xg[4][64];           // the aligned pair of doubles holding x_j^{(s-2)}: consumed
+    double c[2][4][kQCap];       // A_ij
+    double2 xg[4][kQCap];        // the aligned pair of doubles holding x_j^{(s-2)}: consumed
                                  // by the strip pass, so the next quad's land under the walk
                                  // (which half: a bit mask in the issuing lane's register)
-    uint32_t go[2][4][64];       // binned message order: position of the edge's own message
+    uint32_t go[2][4][kQCap];    // binned message order: position of the edge's own message
 };
 static_assert(sizeof(double2) * 4 * kQStride >= sizeof(double2) * (kRowParMaxDegree + 8),
               "a long row's strip fits a quad's strips");
-constexpr size_t kQuadBytes = sizeof(QuadBuf) * kQWarps;
+template <int QT>
+constexpr size_t quad_bytes() {
+    return sizeof(QuadBuf<QT>) * kQWarps;
+}
 
 __device__ __forceinline__ void cpa_tw_n(double2 *dst, const double2 *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
@@ -474,17 +485,18 @@ struct QRow {
     uint32_t e1 = 0;                          // end offset as loaded (d, dl: QRow::fin)
     // the offsets are loaded a stage before anything depends on them: d and dl are formed
     // when the row moves on, not behind the loads
-    __device__ __forceinline__ void fin() {
+    __device__ __forceinline__ void fin(uint32_t cap) {
         const uint32_t dd = e1 - e0;
-        d = dd <= 64u ? dd : 0u;
-        dl = dd <= 64u ? 0u : dd;
+        d = dd <= cap ? dd : 0u;
+        dl = dd <= cap ? 0u : dd;
     }
     double2 nd = make_double2(0.0, 0.0);      // {A_ii, A_ii mu_ii}
     double xi = 0.0, bi = 0.0;                // x_i^{(s-2)}, b_i
 };
 
-template <int MODE, bool BIN>
+template <int MODE, bool BIN, int QT>
 __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a) {
+    constexpr int kQT = QT;
     __shared__ TailSmem<kQWarps> tail;
     __shared__ int64_t s_sweep;
     __shared__ int s_skip;
@@ -521,7 +533,7 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
     }
     Stats st;
     st.lim = (MODE == kModeSolve) ? fmin(ctrl->blowup, DBL_MAX) : DBL_MAX;
-    QuadBuf &W = reinterpret_cast<QuadBuf *>(quad_raw)[warp];
+    QuadBuf<QT> &W = reinterpret_cast<QuadBuf<QT> *>(quad_raw)[warp];
     const int g = lane >> 3, o = lane & 7;
 
     const uint32_t r_lo = __ldg(&a.tile_info[0].x);
@@ -550,9 +562,9 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
         }
     };
     // edge records of the row's slots o, o + 8, ... (registers, consumed by the issue stage)
-    auto load_er = [&](const QRow &r, int4 (&er)[8]) {
+    auto load_er = [&](const QRow &r, int4 (&er)[kQT]) {
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
+        for (int t = 0; t < kQT; ++t) {
             const uint32_t q = (uint32_t)o + 8u * t;
             if (BIN) {  // the two indices only: A_ij goes straight to shared memory later
                 const uint2 v = q < r.d ? ld_ef_u2(a.gidx + r.e0 + q, x.pol) : make_uint2(0u, 0u);
@@ -575,9 +587,9 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
             }
         }
     };
-    auto issue_tw = [&](const QRow &r, const int4 (&er)[8], int nb) {
+    auto issue_tw = [&](const QRow &r, const int4 (&er)[kQT], int nb) {
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
+        for (int t = 0; t < kQT; ++t) {
             const uint32_t q = (uint32_t)o + 8u * t;
             if (q < r.d) {
                 const EdgeRec e = er_of(er[t]);
@@ -601,13 +613,13 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
     };
     // part 2 (after the strip pass has consumed the previous quad's x): the x_j gathers
     uint32_t pm = 0u;  // which half of the landed pair is x_j, a bit per slot of this lane
-    auto issue_x = [&](const QRow &r, const int4 (&er)[8]) {
+    auto issue_x = [&](const QRow &r, const int4 (&er)[kQT]) {
 #ifndef GABP_ROW_PROBE_NOX
         if (x.resid) {
             pm = 0u;
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const uint32_t q = (uint32_t)o + 8u * t;
+            for (int t = 0; t < kQT; ++t) {
+                    const uint32_t q = (uint32_t)o + 8u * t;
                 if (q < r.d) {
                     const uint32_t col = (uint32_t)er[t].y;
                     pm |= (col & 1u) << t;
@@ -621,15 +633,15 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
 
     if (nq > 0) {
         QRow rc, ri, rl, rn;  // rows of the quad being walked, issued, loaded; offsets ahead
-        int4 er[8];
+        int4 er[kQT];
         row_of(0, ri);
-        ri.fin();
+        ri.fin(8u * QT);
         load_er(ri, er);
         issue_tw(ri, er, 0);
         issue_x(ri, er);
         node_loads(ri);
         row_of(1, rl);
-        rl.fin();
+        rl.fin(8u * QT);
         row_of(2, rn);
         load_er(rl, er);
         for (uint32_t q = 0; q < nq; ++q) {
@@ -637,7 +649,7 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
             rc = ri;
             ri = rl;
             rl = rn;  // (its offsets were loaded a quad ago: no dependent load before load_er)
-            rl.fin();
+            rl.fin(8u * QT);
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // quad q has landed
             __syncwarp();
             issue_tw(ri, er, cb ^ 1);  // quad q + 1 (empty past the range)
@@ -647,7 +659,7 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
             const uint32_t nbmax = __reduce_max_sync(~0u, (rc.d + 7u) >> 3);
             double yp = 0.0;
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
+            for (int t = 0; t < kQT; ++t) {
                 const uint32_t k = (uint32_t)o + 8u * t;
                 if (k < rc.d) {
                     const double2 v = Tg[k];
@@ -949,13 +961,47 @@ __global__ void edge_col_kernel(int64_t E, const EdgeRec *er, uint32_t *col) {
 constexpr int kMaxDevices = 64;
 int g_row_grid[kMaxDevices][2] = {};   // persistent grids per device (prepare_rowpar_kernels)
 int g_coop_grid[kMaxDevices] = {};     // cooperative serial sweep: every CTA resident
-int g_quad_grid[kMaxDevices][2] = {};  // rowquad_kernel
-int g_quad_grid_bin[kMaxDevices] = {}; // rowquad_kernel, binned message order
+// rowquad_kernel grids: [device][slots per lane / 2 - 1][solve CSR, solve binned, single]
+int g_quad_grid[kMaxDevices][4][3] = {};
 
 int cur_dev() {
     int d = 0;
     cudaGetDevice(&d);
     return d >= 0 && d < kMaxDevices ? d : 0;
+}
+
+template <int QT>
+cudaError_t prepare_quad(int dv, int sms) {
+    const int bytes = (int)quad_bytes<QT>();
+    const void *fn[3] = {(const void *)rowquad_kernel<kModeSolve, false, QT>,
+                         (const void *)rowquad_kernel<kModeSolve, true, QT>,
+                         (const void *)rowquad_kernel<kModeSingle, false, QT>};
+    for (int k = 0; k < 3; ++k) {
+        cudaError_t e =
+            cudaFuncSetAttribute(fn[k], cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e != cudaSuccess) return e;
+        int occ = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn[k], kQThreads, bytes);
+        if (e != cudaSuccess) return e;
+        g_quad_grid[dv][QT / 2 - 1][k] = sms * (occ > 0 ? occ : 1);
+    }
+    return cudaSuccess;
+}
+
+template <int QT>
+cudaError_t launch_quad(const SweepArgs &a, int which, int dv, cudaStream_t st) {
+    int64_t grid = g_quad_grid[dv][QT / 2 - 1][which];
+    if (grid <= 0) grid = 148 * 3;
+    const int64_t need = (a.ntiles + kQWarps - 1) / kQWarps;
+    if (grid > need) grid = need;
+    const size_t bytes = quad_bytes<QT>();
+    if (which == 1)
+        rowquad_kernel<kModeSolve, true, QT><<<(unsigned)grid, kQThreads, bytes, st>>>(a);
+    else if (which == 0)
+        rowquad_kernel<kModeSolve, false, QT><<<(unsigned)grid, kQThreads, bytes, st>>>(a);
+    else
+        rowquad_kernel<kModeSingle, false, QT><<<(unsigned)grid, kQThreads, bytes, st>>>(a);
+    return cudaGetLastError();
 }
 
 }  // namespace
@@ -980,28 +1026,11 @@ cudaError_t prepare_rowpar_kernels() {
                                                            0)) != cudaSuccess)
         return e;
     g_coop_grid[dv] = sms * (occ > 0 ? occ : 1);
-    if ((e = cudaFuncSetAttribute(rowquad_kernel<kModeSolve, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kQuadBytes)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(rowquad_kernel<kModeSolve, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kQuadBytes)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(rowquad_kernel<kModeSingle, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kQuadBytes)) != cudaSuccess)
+    if ((e = prepare_quad<2>(dv, sms)) != cudaSuccess ||
+        (e = prepare_quad<4>(dv, sms)) != cudaSuccess ||
+        (e = prepare_quad<6>(dv, sms)) != cudaSuccess ||
+        (e = prepare_quad<8>(dv, sms)) != cudaSuccess)
         return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-             &occ, rowquad_kernel<kModeSolve, false>, kQThreads, kQuadBytes)) != cudaSuccess)
-        return e;
-    g_quad_grid[dv][kModeSolve] = sms * (occ > 0 ? occ : 1);
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-             &occ, rowquad_kernel<kModeSolve, true>, kQThreads, kQuadBytes)) != cudaSuccess)
-        return e;
-    g_quad_grid_bin[dv] = sms * (occ > 0 ? occ : 1);
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-             &occ, rowquad_kernel<kModeSingle, false>, kQThreads, kQuadBytes)) != cudaSuccess)
-        return e;
-    g_quad_grid[dv][kModeSingle] = sms * (occ > 0 ? occ : 1);
     return cudaSuccess;
 }
 
@@ -1048,17 +1077,14 @@ cudaError_t launch_rowpar(const SweepArgs &a, int mode, cudaStream_t st) {
     const bool quad = !getenv("GABP_ROW_NO_QUAD");
     if (quad) {
         const bool bin = m == kModeSolve && a.gout && a.gidx && a.gcoef;
-        int64_t grid = bin ? g_quad_grid_bin[dv] : g_quad_grid[dv][m];
-        if (grid <= 0) grid = 148 * 3;
-        const int64_t need = (a.ntiles + kQWarps - 1) / kQWarps;
-        if (grid > need) grid = need;
-        if (bin)
-            rowquad_kernel<kModeSolve, true><<<(unsigned)grid, kQThreads, kQuadBytes, st>>>(a);
-        else if (m == kModeSolve)
-            rowquad_kernel<kModeSolve, false><<<(unsigned)grid, kQThreads, kQuadBytes, st>>>(a);
-        else
-            rowquad_kernel<kModeSingle, false><<<(unsigned)grid, kQThreads, kQuadBytes, st>>>(a);
-        return cudaGetLastError();
+        const int which = bin ? 1 : m == kModeSolve ? 0 : 2;
+        // slots per lane: the instantiation that just covers the graph's rows (a.quad_slots
+        // from the degree counts of the build; rows past it take the long-row path)
+        const int qt = a.quad_slots <= 2 ? 2 : a.quad_slots <= 4 ? 4 : a.quad_slots <= 6 ? 6 : 8;
+        if (qt == 2) return launch_quad<2>(a, which, dv, st);
+        if (qt == 4) return launch_quad<4>(a, which, dv, st);
+        if (qt == 6) return launch_quad<6>(a, which, dv, st);
+        return launch_quad<8>(a, which, dv, st);
     }
     int64_t grid = g_row_grid[dv][m] > 0 ? g_row_grid[dv][m] : 148 * 4;
     const int64_t need = (a.ntiles + kRWarps - 1) / kRWarps;
