@@ -691,12 +691,16 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
                 if (j >= rc.d) return make_double2(0.0, 0.0);
                 return BIN ? ld_na_d2(x.min_ + Gg[j]) : ld_ef_d2(x.min_ + rc.e0 + j, x.pol);
             };
+            // the row's full sums: the last exclusion sum + the last term, kept by the lane of
+            // the row's last edge (the node division runs once per quad, after the walk)
+            double fsp = rc.nd.x, fsn = rc.nd.y;
             auto finish = [&](uint32_t j, double p, double n, double2 old) {
                 if (j < rc.d) {
                     edge_out<BIN>(x, rc.e0 + j, BIN ? Gg[j] : rc.e0 + j, Cg[j], p, n, old, st);
-                    if (j == rc.d - 1u) {  // full sums: the last exclusion sum + the last term
+                    if (j == rc.d - 1u) {
                         const double2 own = Tg[j];
-                        row_node<MODE>(a, x, rc.i, p + own.x, n + own.y, st);
+                        fsp = p + own.x;
+                        fsn = n + own.y;
                     }
                 }
             };
@@ -793,7 +797,9 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
                 b += 2;
             }
             const bool plain = rc.i != 0xffffffffu && rc.dl == 0u;
-            if (plain && rc.d == 0u && o == 0) row_node<MODE>(a, x, rc.i, rc.nd.x, rc.nd.y, st);
+            // (an isolated row: its prior, on lane o = 0)
+            if (plain && (uint32_t)o == (rc.d == 0u ? 0u : (rc.d - 1u) & 7u))
+                row_node<MODE>(a, x, rc.i, fsp, fsn, st);
             if (x.resid && plain && o == 0) {
                 const double y = rc.nd.x * rc.xi + yp;
                 const double res = y - rc.bi;
