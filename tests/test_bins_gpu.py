@@ -99,6 +99,34 @@ def test_binned_order_degree_ladder(tiny_window, sweep_cap):
                                   np.asarray(o.max_change_history))
 
 
+@pytest.mark.parametrize("binned", [False, True])
+@pytest.mark.parametrize("slots", [2, 4, 6, 8])
+def test_every_slot_count_on_the_degree_ladder(monkeypatch, slots, binned):
+    """rowquad_kernel is instantiated for 2, 4, 6 and 8 slots per lane (rows of up to 16 .. 64
+    edges in the quads; a graph normally runs the smallest one that covers its rows).  Forced
+    here (GABP_QUAD_SLOTS), so every longer row of the ladder takes the long-row path: both
+    message orders, bitwise the oracle."""
+    from tests.test_gpu_parity import _degree_ladder_system
+
+    monkeypatch.setenv("GABP_QUAD_SLOTS", str(slots))
+    if binned:
+        monkeypatch.setenv("GABP_BIN_WINDOW_MB", "0.002")
+        monkeypatch.delenv("GABP_ROW_NO_BIN", raising=False)
+    else:
+        monkeypatch.setenv("GABP_ROW_NO_BIN", "1")
+    s = _degree_ladder_system()
+    og = oracle.build_graph(s.diag, s.rhs, s.pair_i, s.pair_j, s.pair_v)
+    for cap in (2, 60):
+        o = oracle.solve(og, epsilon=1e-12, max_iter=cap, schedule="parallel")
+        r = _solve_rows(s, epsilon=1e-12, max_iter=cap)
+        assert (r.message_bins >= 2) == binned
+        assert r.iterations == o.iterations and r.converged == o.converged
+        np.testing.assert_array_equal(_bits(r.means), _bits(o.means))
+        np.testing.assert_array_equal(_bits(r.precisions), _bits(o.precisions))
+        np.testing.assert_array_equal(np.asarray(r.max_change_history),
+                                      np.asarray(o.max_change_history))
+
+
 def test_binned_graph_is_reused_and_reproducible(tiny_window):
     """One graph, several solves (different caps, then a new right-hand side): the index arrays
     are built once, every solve is bitwise the oracle, repeated solves agree bit for bit."""
