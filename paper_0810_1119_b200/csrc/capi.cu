@@ -585,10 +585,13 @@ int auto_chunk(const gabp_graph *G) {
     return c;
 }
 
+bool chunk_exec_ready(const gabp_graph *G, int sched, int gather, int len) {
+    return G->chunk_exec && G->chunk_len == len && G->chunk_sched == sched &&
+           G->chunk_gather == gather && G->chunk_gen == G->ws_gen;
+}
+
 int get_chunk_exec(gabp_graph *G, int sched, int gather, int len) {
-    if (G->chunk_exec && G->chunk_len == len && G->chunk_sched == sched &&
-        G->chunk_gather == gather && G->chunk_gen == G->ws_gen)
-        return GABP_OK;
+    if (chunk_exec_ready(G, sched, gather, len)) return GABP_OK;
     if (G->chunk_exec) {
         cudaGraphExecDestroy(G->chunk_exec);
         G->chunk_exec = nullptr;
@@ -1155,12 +1158,16 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
                            : 0;
     }
     const int C = opt->sweeps_per_poll > 0 ? opt->sweeps_per_poll : auto_chunk(G);
+    // The chunks run as one CUDA graph each (one host call per chunk).  Capturing and
+    // instantiating it costs ~0.2 ms, which a short solve on a fresh graph (the one-shot
+    // gabp_solve_system) never earns back: its first sweeps are launched directly and the
+    // chunk graph is built only if the solve is still running after them.
+    constexpr int64_t kDirectSweeps = 16;
     const double tc0 = host_ms();
-    rc = get_chunk_exec(G, sched, gather, C);
-    if (rc) return rc;
+    bool have_exec = chunk_exec_ready(G, sched, gather, C);
     if (host_timing())
-        fprintf(stderr, "[gabp] run_solve: setup %.2f ms, chunk graph (%d sweeps) %.2f ms\n",
-                tc0 - t_setup, C, host_ms() - tc0);
+        fprintf(stderr, "[gabp] run_solve: setup %.2f ms, chunk graph (%d sweeps) %s\n",
+                tc0 - t_setup, C, have_exec ? "cached" : "deferred");
     SweepArgs a = make_args(G);
     // kernels per sweep launch: the fast kernel (exact twins, host- or tail-launched, count
     // themselves on the device: Ctrl.twin_launches)
@@ -1170,7 +1177,12 @@ int run_solve(gabp_graph *G, const gabp_options_t *opt, double *device_ms) {
     while (launched < total) {
         const int64_t k = total - launched < C ? total - launched : C;
         G->kernels_launched += kps * k;
-        if (k == C) {
+        if (k == C && !have_exec && launched >= kDirectSweeps) {
+            rc = get_chunk_exec(G, sched, gather, C);
+            if (rc) return rc;
+            have_exec = true;
+        }
+        if (k == C && have_exec) {
             CK(cudaGraphLaunch(G->chunk_exec, st));
         } else {
             for (int64_t q = 0; q < k; ++q)
