@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(kQThreads, 3) rowquad_kernel(const SweepArgs a
                 st.rsq += res * res;
             }
             __syncwarp();
-            // rows of more than 64 edges: the whole warp, one row at a time, on the buffer
+            // rows of more than 8 QT edges: the whole warp, one row at a time, on the buffer
             const unsigned lmask = __ballot_sync(~0u, rc.dl != 0u && o == 0);
             for (int gg = 0; lmask != 0u && gg < 4; ++gg) {
                 if (lmask & (1u << (8 * gg))) {
